@@ -1,0 +1,117 @@
+/*
+ * pe.h -- C ABI of the B200 partial-evaluation library (libpe.so).
+ *
+ * Computes T bivariate images of a sparse n-variate polynomial modulo a prime p at the
+ * points beta^j = (alpha_1^j, ..., alpha_{n-2}^j), j = j0 .. j0+T-1:
+ *
+ *   f = sum_{i<t} c_i x^{dx_i} y^{dy_i} z_1^{e_i,1} ... z_{n-2}^{e_i,n-2}
+ *   out[g*T + k] = coefficient of x^{dx_g} y^{dy_g} in f(x, y, beta^{j0+k})  mod p
+ *
+ * PAPER.md:246-266 (§2.1 "b_t(x1,x2) = f(x1,x2,beta^t)"), PAPER.md:408-419 (§2.3 Eq.
+ * e:def_f), computed by the matrix method: m_i = M_i(alpha) once
+ * (PAPER.md:428-442), a_i seeded at the chunk start by exponentiation,
+ * then per point: coefficient reduction over equal (dx,dy) and a_i <- a_i * m_i
+ * (Alg. 1, Alg. 7).
+ *
+ * Only POD types cross this boundary; all pointers are plain host or device pointers as
+ * stated per call.  All functions are thread-safe across distinct handles; a single handle
+ * is not re-entrant.
+ *
+ * Result contract (readings R1-R9):
+ *   - rows g = 0..G-1 are the distinct (dx,dy) of the INPUT terms (zero-coefficient terms
+ *     included), in descending lexicographic order; pe_bucket_exps()
+ *     returns them;
+ *   - every value is the canonical residue in [0, p); zero coefficients are stored (dense);
+ *   - coefficients are reduced mod p; duplicate full monomials are summed; alpha_k is
+ *     reduced mod p and must be non-zero mod p ("non-zero ... from F_p");
+ *   - j0 = 0 is accepted (beta^0 = (1,...,1)); any j0 with j0+T-1 < 2^64.
+ *   - bit-exact: the result is unique, independent of R / warps / chunk / stream.
+ */
+#ifndef PE_H_
+#define PE_H_
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pe_ctx pe_ctx; /* opaque; owns its device buffers */
+
+enum {
+  PE_OK = 0,
+  PE_EINVAL = -1,    /* NULL / inconsistent argument                                   */
+  PE_ENOTPRIME = -2, /* p composite (deterministic Miller-Rabin, 12 prime bases <= 37)  */
+  PE_ERANGE = -3,    /* p < 3, p >= 2^63, alpha_k == 0 mod p, j0+T-1 overflows, T*G huge  */
+  PE_ENOMEM = -4,    /* host or device allocation failed                                */
+  PE_ECUDA = -5,     /* CUDA runtime error (no device, launch failure, ...)             */
+  PE_ENOTSUP = -6    /* requested path / option not supported for this p               */
+};
+
+enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2 };
+
+/* Tuning knobs (0 = automatic).  They never change the result (pin P13). */
+typedef struct pe_config {
+  int32_t path;  /* PE_PATH_AUTO: FP64 Alg. 2 if p < 2^50 else INT64; env PE_PATH=int|fp64  */
+  int32_t R;     /* terms per lane: 1,2,4,8,16 (FP64: <= 8); auto picks by bucket sizes    */
+  int32_t warps; /* warps per CTA, 1..16 (auto 8)                                          */
+  int32_t chunk; /* points per CTA (multiple of 32; auto by grid coverage)                 */
+} pe_config;
+
+/*
+ * pe_create -- build an evaluation handle on the CUDA device current at the call.
+ *   p       prime, 3 <= p < 2^63.
+ *   t       number of terms (0 allowed: G = 0).
+ *   n       number of variables, n >= 2 (columns 0,1 are x,y; 2..n-1 are z_1..z_{n-2}).
+ *   coeffs  HOST uint64[t], any values (reduced mod p).
+ *   exps    HOST uint32[t*n], row-major: exps[i*n + 0] = deg_x, [i*n+1] = deg_y,
+ *           [i*n + 2 + l] = deg of z_{l+1}.
+ *   alpha   HOST uint64[n-2] (may be NULL iff n == 2), reduced mod p, must be != 0 mod p.
+ * Deep-copies everything; the caller may free its arrays on return.
+ * Returns NULL on error and sets pe_last_error() (PE_EINVAL / PE_ENOTPRIME / PE_ERANGE /
+ * PE_ENOMEM / PE_ECUDA).  Validation happens before any CUDA call.
+ */
+pe_ctx* pe_create(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs,
+                  const uint32_t* exps, const uint64_t* alpha);
+/* Same, with tuning knobs (cfg may be NULL = all automatic). */
+pe_ctx* pe_create_ex(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs,
+                     const uint32_t* exps, const uint64_t* alpha, const pe_config* cfg);
+
+/*
+ * pe_eval -- T images into HOST memory out[G*T] (row g, column k <-> j = j0 + k).
+ * Synchronous.  T == 0 or G == 0 is a no-op returning PE_OK.
+ * Errors: PE_EINVAL (h NULL, out NULL with G*T > 0), PE_ERANGE (j0 + T - 1 >= 2^64),
+ *         PE_ENOMEM, PE_ECUDA.
+ */
+int pe_eval(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* out);
+
+/*
+ * pe_eval_device -- T images into DEVICE memory: d_out[g*ld + k], ld >= T (elements).
+ * Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream): returns after
+ * enqueueing.  The handle's scratch is reused by the next call on the same handle, so calls
+ * on one handle must be stream-ordered (same stream, or synchronised).
+ */
+int pe_eval_device(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* d_out, uint64_t ld,
+                   void* stream);
+
+void pe_destroy(pe_ctx* h); /* NULL-safe; synchronises the handle's device work */
+
+uint64_t pe_num_buckets(const pe_ctx* h);                   /* G (0 if h NULL) */
+int pe_bucket_exps(const pe_ctx* h, uint32_t* dxdy);        /* HOST uint32[2G]: row g -> (dx,dy) */
+
+/* Introspection: values chosen at create. Any pointer may be NULL. */
+int pe_info(const pe_ctx* h, int32_t* path, int32_t* R, int32_t* warps, uint64_t* t_padded,
+            uint64_t* n_slots);
+
+/* m_i = prod_l alpha_l^{e_i,l} mod p for every input term i (HOST uint64[t], input order). */
+int pe_monomials(const pe_ctx* h, uint64_t* m);
+
+int pe_last_error(void);            /* thread-local code of the last failing call */
+const char* pe_strerror(int code);
+
+/* Advisory: 1 iff p > 100 t^2 (distinct m_i likely); never enforced. */
+int pe_interp_bound_ok(uint64_t p, uint64_t t);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PE_H_ */

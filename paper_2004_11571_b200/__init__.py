@@ -1,0 +1,191 @@
+"""B200-native partial modular evaluation of sparse polynomials (arXiv 2004.11571 hot path).
+
+Thin ctypes binding over ``libpe.so`` (C ABI: ``include/pe.h``, ``include/pe_test.h``).
+Argument marshalling only: every step of the evaluation runs in the CUDA kernels of
+``csrc/``.  There is no CPU fallback -- if the library or a GPU is missing, calls raise.
+
+    ctx = Context(p, coeffs, exps, alpha)          # pe_create  (host numpy arrays)
+    out = ctx.eval(j0, T)                          # pe_eval -> numpy uint64 [G, T]
+    ctx.eval_device(j0, T, d_out_ptr, ld, stream)  # pe_eval_device (device pointer)
+    ctx.buckets()                                  # rows (dx, dy), descending lex
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libpe.so")
+
+PE_OK, PE_EINVAL, PE_ENOTPRIME, PE_ERANGE, PE_ENOMEM, PE_ECUDA, PE_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
+PATH_AUTO, PATH_INT, PATH_FP64 = 0, 1, 2
+CORE_SHOUP4, CORE_SHOUP2, CORE_MONT, CORE_FP64, CORE_FP64ADD, CORE_POW, CORE_SHOUP4RAW = range(7)
+
+#: every symbol include/pe.h and include/pe_test.h declare
+EXPORTS = ["pe_create", "pe_create_ex", "pe_eval", "pe_eval_device", "pe_destroy", "pe_num_buckets",
+           "pe_bucket_exps", "pe_info", "pe_monomials", "pe_last_error", "pe_strerror",
+           "pe_interp_bound_ok", "pe_test_core", "pe_bench_core"]
+
+
+class PEError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        self.code = code
+        super().__init__(f"{what}: {lib().pe_strerror(code).decode()} ({code})")
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_int32), ("R", ctypes.c_int32), ("warps", ctypes.c_int32),
+                ("chunk", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libpe.so (built in-tree by ``build.py``); raises if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2004_11571_b200.build` "
+                               "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        u64, u32, i32, vp = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32, ctypes.c_void_p
+        L.pe_create.argtypes = [u64, u64, u32, vp, vp, vp]
+        L.pe_create.restype = vp
+        L.pe_create_ex.argtypes = [u64, u64, u32, vp, vp, vp, ctypes.POINTER(Config)]
+        L.pe_create_ex.restype = vp
+        L.pe_eval.argtypes = [vp, u64, u64, vp]
+        L.pe_eval.restype = ctypes.c_int
+        L.pe_eval_device.argtypes = [vp, u64, u64, vp, u64, vp]
+        L.pe_eval_device.restype = ctypes.c_int
+        L.pe_destroy.argtypes = [vp]
+        L.pe_destroy.restype = None
+        L.pe_num_buckets.argtypes = [vp]
+        L.pe_num_buckets.restype = u64
+        L.pe_bucket_exps.argtypes = [vp, vp]
+        L.pe_bucket_exps.restype = ctypes.c_int
+        L.pe_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
+                              ctypes.POINTER(u64), ctypes.POINTER(u64)]
+        L.pe_info.restype = ctypes.c_int
+        L.pe_monomials.argtypes = [vp, vp]
+        L.pe_monomials.restype = ctypes.c_int
+        L.pe_last_error.argtypes = []
+        L.pe_last_error.restype = ctypes.c_int
+        L.pe_strerror.argtypes = [ctypes.c_int]
+        L.pe_strerror.restype = ctypes.c_char_p
+        L.pe_interp_bound_ok.argtypes = [u64, u64]
+        L.pe_interp_bound_ok.restype = ctypes.c_int
+        L.pe_test_core.argtypes = [ctypes.c_int, u64, u64, vp, vp, vp, vp]
+        L.pe_test_core.restype = ctypes.c_int
+        L.pe_bench_core.argtypes = [ctypes.c_int, u64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_double)]
+        L.pe_bench_core.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None and a.size else None
+
+
+def _check(rc: int, what: str):
+    if rc != PE_OK:
+        raise PEError(rc, what)
+
+
+class Context:
+    """An evaluation handle (``pe_create_ex``).  Arrays are host numpy arrays."""
+
+    def __init__(self, p: int, coeffs, exps, alpha, n: int | None = None, path: int = PATH_AUTO,
+                 R: int = 0, warps: int = 0, chunk: int = 0):
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.uint64).ravel()
+        exps = np.ascontiguousarray(exps, dtype=np.uint32)
+        n = exps.shape[1] if n is None else n
+        exps = exps.reshape(-1, n) if exps.size else np.zeros((0, n), np.uint32)
+        alpha = np.ascontiguousarray(alpha, dtype=np.uint64).ravel()
+        self.p, self.n, self.t = int(p), int(n), int(coeffs.size)
+        cfg = Config(path, R, warps, chunk)
+        L = lib()
+        h = L.pe_create_ex(self.p, self.t, self.n, _ptr(coeffs), _ptr(exps), _ptr(alpha), ctypes.byref(cfg))
+        if not h:
+            raise PEError(L.pe_last_error(), "pe_create")
+        self._h = ctypes.c_void_p(h)
+
+    @classmethod
+    def from_workload(cls, w, **kw) -> "Context":
+        return cls(w.p, w.coeffs, w.exps, w.alpha, n=w.n, **kw)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().pe_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def G(self) -> int:
+        return int(lib().pe_num_buckets(self._h))
+
+    def buckets(self) -> np.ndarray:
+        out = np.zeros((self.G, 2), np.uint32)
+        _check(lib().pe_bucket_exps(self._h, _ptr(out)), "pe_bucket_exps")
+        return out
+
+    def info(self) -> dict:
+        path, R, W = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        tp, ns = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().pe_info(self._h, ctypes.byref(path), ctypes.byref(R), ctypes.byref(W), ctypes.byref(tp),
+                             ctypes.byref(ns)), "pe_info")
+        return {"path": "fp64" if path.value == PATH_FP64 else "int", "R": R.value, "warps": W.value,
+                "t_padded": tp.value, "n_slots": ns.value}
+
+    def monomials(self) -> np.ndarray:
+        out = np.zeros(self.t, np.uint64)
+        _check(lib().pe_monomials(self._h, _ptr(out)), "pe_monomials")
+        return out
+
+    def eval(self, j0: int, T: int, out: np.ndarray | None = None) -> np.ndarray:
+        """pe_eval: host result uint64 [G, T]."""
+        if out is None:
+            out = np.empty((self.G, T), np.uint64)
+        assert out.dtype == np.uint64 and out.flags.c_contiguous and out.size == self.G * T
+        _check(lib().pe_eval(self._h, j0, T, _ptr(out)), "pe_eval")
+        return out
+
+    def eval_device(self, j0: int, T: int, d_out: int, ld: int | None = None, stream: int = 0):
+        """pe_eval_device into a device pointer (e.g. ``torch_tensor.data_ptr()``)."""
+        _check(lib().pe_eval_device(self._h, j0, T, ctypes.c_void_p(d_out), T if ld is None else ld,
+                                    ctypes.c_void_p(stream)), "pe_eval_device")
+
+
+def test_core(variant: int, p: int, a, b, extra=None) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.uint64)
+    b = np.ascontiguousarray(b, dtype=np.uint64)
+    out = np.zeros(a.size, np.uint64)
+    x = None if extra is None else np.ascontiguousarray(extra, dtype=np.uint64)
+    _check(lib().pe_test_core(variant, p, a.size, _ptr(a), _ptr(b), _ptr(x), _ptr(out)), "pe_test_core")
+    return out
+
+
+def bench_core(variant: int, p: int, R: int, blocks: int, threads: int, iters: int):
+    ms, steps, cyc = ctypes.c_float(), ctypes.c_double(), ctypes.c_double()
+    _check(lib().pe_bench_core(variant, p, R, blocks, threads, iters, ctypes.byref(ms), ctypes.byref(steps),
+                               ctypes.byref(cyc)), "pe_bench_core")
+    return ms.value, steps.value, cyc.value
+
+
+def interp_bound_ok(p: int, t: int) -> bool:
+    return bool(lib().pe_interp_bound_ok(p, t))

@@ -1,0 +1,311 @@
+// kernels.cuh -- device kernels of the partial-evaluation path (sm_100a).
+//
+//   k_keys        a2: bucket key (dx<<32 | dy) per term
+//   k_max_exp     max evaluated exponent (power-table size d)
+//   k_power_table a3: beta_k^e tables, Montgomery form
+//   k_setup       a3: m_i, Shoup w_i, reduced c_i in the padded tile layout
+//   k_step        a4+a5+a6: seed a_i = c_i m_i^{j_s}, then per point acc += a_i, a_i <- a_i m_i
+//                 with the per-(x,y) segmented reduction
+//   k_fixup       a6: cross-CTA carries of one bucket -> canonical out
+#pragma once
+#include "modcore.cuh"
+
+namespace pe {
+
+constexpr int kMaxWarps = 16;
+constexpr int kSuper = 32;   // points per shared-memory super-group (one lane per point)
+
+enum PathKind { kInt4 = 0, kInt2 = 1, kFp64 = 2 };
+
+// ---------------------------------------------------------------- 96-bit accumulators
+struct U96 { u32 w0, w1, w2; };
+
+__device__ __forceinline__ void add96_64(U96& x, u64 v) {
+  asm("add.cc.u32 %0, %0, %3;\n\t"
+      "addc.cc.u32 %1, %1, %4;\n\t"
+      "addc.u32 %2, %2, 0;"
+      : "+r"(x.w0), "+r"(x.w1), "+r"(x.w2)
+      : "r"(lo32(v)), "r"(hi32(v)));
+}
+// x = u + v (65 bits) without zero-initialising x.
+__device__ __forceinline__ void set96_sum(U96& x, u64 u, u64 v) {
+  asm("add.cc.u32 %0, %3, %5;\n\t"
+      "addc.cc.u32 %1, %4, %6;\n\t"
+      "addc.u32 %2, 0, 0;"
+      : "=r"(x.w0), "=r"(x.w1), "=r"(x.w2)
+      : "r"(lo32(u)), "r"(hi32(u)), "r"(lo32(v)), "r"(hi32(v)));
+}
+__device__ __forceinline__ void add96(U96& x, const U96& y) {
+  asm("add.cc.u32 %0, %0, %3;\n\t"
+      "addc.cc.u32 %1, %1, %4;\n\t"
+      "addc.u32 %2, %2, %5;"
+      : "+r"(x.w0), "+r"(x.w1), "+r"(x.w2)
+      : "r"(y.w0), "r"(y.w1), "r"(y.w2));
+}
+
+template <int NW>
+__device__ __forceinline__ U96 shfl_xor96(const U96& x, int off) {
+  U96 r;
+  r.w0 = __shfl_xor_sync(0xffffffffu, x.w0, off);
+  r.w1 = __shfl_xor_sync(0xffffffffu, x.w1, off);
+  r.w2 = NW == 3 ? __shfl_xor_sync(0xffffffffu, x.w2, off) : 0u;
+  return r;
+}
+__device__ __forceinline__ U96 sel96(bool c, const U96& a, const U96& b) {
+  U96 r;
+  r.w0 = c ? a.w0 : b.w0;
+  r.w1 = c ? a.w1 : b.w1;
+  r.w2 = c ? a.w2 : b.w2;
+  return r;
+}
+template <int NW>
+__device__ __forceinline__ void add96n(U96& x, const U96& y) {
+  if (NW == 3) {
+    add96(x, y);
+  } else {
+    asm("add.cc.u32 %0, %0, %2;\n\t"
+        "addc.u32 %1, %1, %3;"
+        : "+r"(x.w0), "+r"(x.w1)
+        : "r"(y.w0), "r"(y.w1));
+  }
+}
+
+// Transpose-reduce 8 points over the 32 lanes of a warp (the GPU analogue of the paper's
+// SIMD tree reduction with shuffles): lanes exchange halves of their
+// 8 per-point partial sums at xor-distance 16, 8, 4 (each lane keeps the half matching its
+// lane bit), then butterfly at 2, 1.  Afterwards lane l holds the warp total of point
+// (l >> 2) & 7.  9 exchanges per lane for 8 points instead of 40 for 8 plain butterflies.
+// NW = 32-bit words carried (2 when every partial sum fits 64 bits, else 3).
+template <int NW>
+__device__ __forceinline__ U96 xpose_reduce8(U96 (&v)[8], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  U96 t4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    U96 send = sel96(b4, v[i], v[i + 4]);
+    t4[i] = sel96(b4, v[i + 4], v[i]);
+    add96n<NW>(t4[i], shfl_xor96<NW>(send, 16));
+  }
+  U96 t2[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    U96 send = sel96(b3, t4[i], t4[i + 2]);
+    t2[i] = sel96(b3, t4[i + 2], t4[i]);
+    add96n<NW>(t2[i], shfl_xor96<NW>(send, 8));
+  }
+  U96 send = sel96(b2, t2[0], t2[1]);
+  U96 t1 = sel96(b2, t2[1], t2[0]);
+  add96n<NW>(t1, shfl_xor96<NW>(send, 4));
+  add96n<NW>(t1, shfl_xor96<NW>(t1, 2));
+  add96n<NW>(t1, shfl_xor96<NW>(t1, 1));
+  return t1;
+}
+
+// ---------------------------------------------------------------- setup kernels
+static __global__ void k_keys(const u32* __restrict__ exps, u64 t, u32 n, u64* __restrict__ key,
+                       u32* __restrict__ idx) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < t; i += (u64)gridDim.x * blockDim.x) {
+    key[i] = ((u64)exps[i * n + 0] << 32) | exps[i * n + 1];
+    idx[i] = (u32)i;
+  }
+}
+
+static __global__ void k_max_exp(const u32* __restrict__ exps, u64 t, u32 n, u32* __restrict__ dmax) {
+  u32 mx = 0;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < t; i += (u64)gridDim.x * blockDim.x)
+    for (u32 l = 2; l < n; ++l) mx = max(mx, exps[i * n + l]);
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(dmax, mx);
+}
+
+// table[l*(D+1) + e] = mont(alpha_l^e), one thread per entry (independent exponentiations).
+static __global__ void k_power_table(const u64* __restrict__ alpha, u32 nz, u32 D, u64* __restrict__ table,
+                              ModParams mp) {
+  u64 total = (u64)nz * (D + 1);
+  for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < total; q += (u64)gridDim.x * blockDim.x) {
+    u32 l = (u32)(q / (D + 1)), e = (u32)(q % (D + 1));
+    table[q] = mont_pow(to_mont(alpha[l], mp), e, mp);
+  }
+}
+
+// One thread per padded slot q.  Bucket g of the padded layout owns [poff[g], poff[g+1]);
+// its first cnt[g] slots are the sorted terms bstart[g] .. bstart[g]+cnt[g]-1, the rest are
+// padding (c = 0, m = 1: contributes 0 at every point).
+// m_i = prod_l alpha_l^{e_il} with n-3 Montgomery products from the power tables
+// ("n-3 multiplications for each m_i thanks to the tables of powers").
+static __global__ void k_setup(const u32* __restrict__ exps, const u64* __restrict__ coeffs, u32 n,
+                        const u32* __restrict__ sorted_idx, const u64* __restrict__ poff,
+                        const u64* __restrict__ bstart, u32 G, u64 t_pad,
+                        const u64* __restrict__ table, u32 D, const u64* __restrict__ alpha,
+                        u64* __restrict__ c_out, u64* __restrict__ m_out, u64* __restrict__ w_out,
+                        u32* __restrict__ perm_out, ModParams mp) {
+  for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
+    // bucket g: poff[g] <= q < poff[g+1]
+    u32 lo = 0, hi = G;
+    while (hi - lo > 1) {
+      u32 mid = (lo + hi) >> 1;
+      if (poff[mid] <= q) lo = mid; else hi = mid;
+    }
+    const u32 g = lo;
+    const u64 r = q - poff[g];
+    const u64 cnt = bstart[g + 1] - bstart[g];
+    u64 c = 0, m = 1 % mp.p;
+    u32 src = 0xffffffffu;
+    if (r < cnt) {
+      src = sorted_idx[bstart[g] + r];
+      c = coeffs[src] % mp.p;
+      const u32* e = exps + (u64)src * n;
+      if (n > 2) {
+        u64 acc;
+        if (table) {
+          acc = table[e[2]];
+          for (u32 l = 1; l + 2 < n; ++l) acc = mont_mul(acc, table[(u64)l * (D + 1) + e[2 + l]], mp);
+        } else {  // exponents too large for tables: direct powers
+          acc = mont_pow(to_mont(alpha[0], mp), e[2], mp);
+          for (u32 l = 1; l + 2 < n; ++l)
+            acc = mont_mul(acc, mont_pow(to_mont(alpha[l], mp), e[2 + l], mp), mp);
+        }
+        m = from_mont(acc, mp);
+      }
+    }
+    c_out[q] = c;
+    m_out[q] = m;
+    w_out[q] = shoup_w(m, mp.p);
+    perm_out[q] = src;
+  }
+}
+
+static __global__ void k_scatter_m(const u64* __restrict__ m_pad, const u32* __restrict__ perm, u64 t_pad,
+                            u64* __restrict__ m_orig) {
+  for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
+    u32 s = perm[q];
+    if (s != 0xffffffffu) m_orig[s] = m_pad[q];
+  }
+}
+
+// ---------------------------------------------------------------- the hot kernel
+struct StepArgs {
+  const u64* c;          // [t_pad] reduced coefficients (tile layout)
+  const u64* m;          // [t_pad] m_i
+  const u64* w;          // [t_pad] floor(m_i 2^64 / p)
+  const uint2* wt_info;  // [n_wt] x = partial slot, y = run length if run leader else 0
+  u64* partial;          // [n_slots][ldp]
+  u64 ldp;               // leading dimension of partial (points of this pass)
+  u64 js0;               // j of column 0 of this pass
+  u32 n_wt;              // warp tiles
+  u32 npts;              // points of this pass
+  u32 chunk;             // points per CTA (multiple of kSuper)
+  ModParams mp;
+};
+
+// One warp owns a tile of 32*R terms of ONE (x,y) bucket (buckets are padded to whole
+// tiles); lane l holds terms tile + r*32 + l (r < R) in registers for the CTA's whole point
+// chunk: a_i is read from HBM once per chunk, the GPU form of the paper's T_d dependent
+// evaluations, and the R independent chains per lane are its T_i / M
+// ILP without the T_i copies of a (the no-extra-memory variant,
+// PAPER.md:1979-2046).
+//
+// Per 8 points each lane accumulates acc[k] += a_r (Alg. 7 order: reduce, then multiply,
+// PAPER.md:1642-1643), then a warp transpose-reduce leaves one 96-bit total per point; per
+// 32 points the totals of the warps of one bucket inside the CTA are summed in shared
+// memory, reduced mod p and written as one partial per (CTA run, point).
+template <int PATH, int R>
+__global__ void __launch_bounds__(R >= 16 ? 256 : 512)
+k_step(StepArgs args) {
+  __shared__ U96 sacc[2][kMaxWarps][kSuper];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int W = blockDim.x >> 5;
+  const u32 wt = blockIdx.x * W + warp;
+  const bool active = wt < args.n_wt;
+  const u32 k_begin = blockIdx.y * args.chunk;
+  const u32 cnt = min(args.chunk, args.npts - k_begin);
+  const u64 js = args.js0 + k_begin;
+  const ModParams mp = args.mp;
+
+  // ---- load the lane's R terms and seed a_r = c_r * m_r^{js} (each
+  //      independent chain seeded by exponentiation)
+  u64 a[R], m[R], w[R];
+  double ad[R], md[R];
+  uint2 info = make_uint2(0, 0);
+  if (active) {
+    info = args.wt_info[wt];
+    const u64 base = (u64)wt * (32 * R) + lane;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const u64 q = base + (u64)r * 32;
+      const u64 c = __ldg(args.c + q);
+      m[r] = __ldg(args.m + q);
+      w[r] = __ldg(args.w + q);
+      a[r] = seed_pow(c, m[r], js, mp);
+      if (PATH == kFp64) { ad[r] = (double)a[r]; md[r] = (double)m[r]; }
+    }
+  }
+
+  int buf = 0;
+  for (u32 k0 = 0; k0 < cnt; k0 += kSuper, buf ^= 1) {
+    if (active) {
+#pragma unroll 1
+      for (int s = 0; s < kSuper / 8; ++s) {
+        U96 acc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (PATH == kFp64) {
+            double sum = 0.0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              sum = __dadd_rn(sum, ad[r]);                   // exact: R*p < 2^53
+              ad[r] = mul_fp(ad[r], md[r], mp.pd, mp.u);     // Alg. 2
+            }
+            const u64 si = __double2ull_rn(sum);
+            acc[k].w0 = lo32(si); acc[k].w1 = hi32(si); acc[k].w2 = 0;
+          } else {
+            if (R == 1) {
+              acc[k].w0 = lo32(a[0]); acc[k].w1 = hi32(a[0]); acc[k].w2 = 0;
+            } else {
+              set96_sum(acc[k], a[0], a[1]);
+            }
+#pragma unroll
+            for (int r = 2; r < R; ++r) add96_64(acc[k], a[r]);
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              a[r] = PATH == kInt4 ? mul_shoup4(a[r], m[r], w[r], mp.np)
+                                   : mul_shoup2(a[r], m[r], w[r], mp.np);
+          }
+        }
+        const U96 tot = PATH == kFp64 ? xpose_reduce8<2>(acc, lane) : xpose_reduce8<3>(acc, lane);
+        if ((lane & 3) == 0) sacc[buf][warp][s * 8 + (lane >> 2)] = tot;
+      }
+    }
+    __syncthreads();
+    // run leaders: lane = point within the super-group
+    if (active && info.y) {
+      U96 x = sacc[buf][warp][lane];
+      for (u32 v = 1; v < info.y; ++v) add96(x, sacc[buf][warp + v][lane]);
+      const u32 k = k0 + lane;
+      if (k < cnt) {
+        const u64 lo = ((u64)x.w1 << 32) | x.w0;
+        args.partial[(u64)info.x * args.ldp + k_begin + k] = reduce128(x.w2, lo, mp);
+      }
+    }
+    // double-buffered sacc: the next super-group writes the other buffer; the barrier of
+    // the next iteration orders the reads above before buffer reuse two groups later.
+  }
+}
+
+// out[g*ld + k] = sum over the bucket's partial slots, mod p.  One thread per (g, k).
+static __global__ void k_fixup(const u64* __restrict__ partial, u64 ldp, const u32* __restrict__ slot_start,
+                        u32 G, u32 npts, u32 nkb, u64* __restrict__ out, u64 ld, ModParams mp) {
+  const u32 g = blockIdx.x / nkb;
+  const u32 k = (blockIdx.x % nkb) * blockDim.x + threadIdx.x;
+  if (g >= G || k >= npts) return;
+  u64 lo = 0, hi = 0;
+  for (u32 s = slot_start[g]; s < slot_start[g + 1]; ++s) {
+    const u64 v = partial[(u64)s * ldp + k];
+    lo += v;
+    hi += (lo < v);
+  }
+  out[(u64)g * ld + k] = reduce128(hi, lo, mp);
+}
+
+}  // namespace pe

@@ -1,0 +1,187 @@
+// modcore.cuh -- sm_100a modular-arithmetic core (device, header-only).
+//
+// The paper's operators (x) and (+) (§3.1) on a chip with no 64x64-bit
+// multiplier: every 64-bit product is built from 32-bit IMAD / IMAD.WIDE / IMAD.HI.
+//
+//   * Shoup "fixed multiplier" product (Barrett family): m_i is fixed per
+//     term across all points (a <- a o m), so w_i = floor(m_i 2^64 / p)
+//     is precomputed once and every step costs one approximate 64x64-high product plus two
+//     64x64-low products.
+//       - mul_shoup4: p < 2^62, quotient from 3 of the 4 partial products (drops the a0*w0
+//         term and the carries of the two cross terms => q in [q_shoup-2, q_shoup]), result
+//         lazily in [0, 4p) for ANY input a < 2^64.  4p < 2^64 so the remainder computed
+//         mod 2^64 is exact.
+//       - mul_shoup2: p < 2^63, exact Shoup quotient, one conditional subtract, output in
+//         [0, 2p) for input a < 2^64.
+//   * Montgomery REDC for general products (seeding by exponentiation,
+//     monomial setup, final reductions).  p odd, p < 2^63.
+//   * FP64-FMA Alg. 2 and Alg. 3, p < 2^50, with
+//     explicit round-to-nearest intrinsics so nvcc never contracts or reorders (R11).
+#pragma once
+#include <stdint.h>
+
+namespace pe {
+
+typedef uint64_t u64;
+typedef unsigned int u32;
+
+__device__ __forceinline__ u32 lo32(u64 x) { return (u32)x; }
+__device__ __forceinline__ u32 hi32(u64 x) { return (u32)(x >> 32); }
+
+struct ModParams {
+  u64 p;      // prime, 3 <= p < 2^63
+  u64 np;     // 2^64 - p
+  u64 pinv;   // -p^{-1} mod 2^64 (Montgomery)
+  u64 r1;     // 2^64 mod p   (Montgomery one)
+  u64 r2;     // 2^128 mod p
+  double pd;  // (double)p  (exact when p < 2^53)
+  double u;   // RN(1/p)     (Alg. 2 "u stores 1/(double) p")
+};
+
+// ---------------------------------------------------------------- 32-bit building blocks
+__device__ __forceinline__ u64 mul_wide(u32 a, u32 b) { return (u64)a * b; }   // IMAD.WIDE.U32
+__device__ __forceinline__ u32 mul_hi(u32 a, u32 b) { return __umulhi(a, b); } // IMAD.HI.U32
+
+// Full 64x64 -> 128 product (hi, lo).
+__device__ __forceinline__ void mul128(u64 a, u64 b, u64& hi, u64& lo) {
+  lo = a * b;
+  hi = __umul64hi(a, b);
+}
+
+// ---------------------------------------------------------------- Shoup products
+// w = floor(m * 2^64 / p), m < p.
+// Lazy-4: p < 2^62, any a < 2^64 -> r == a*m (mod p), r in [0, 4p).
+//   q ~ floor(a*w / 2^64) from a1*w1 + hi(a1*w0) + hi(a0*w1) (deficit <= 2 vs Shoup's q)
+//   r = a*m - q*p = a*m + q*(2^64 - p)  (mod 2^64)
+// Written in PTX so that exactly 9 IMAD-pipe ops (3 IMAD.WIDE, 2 IMAD.HI, 4 IMAD) and 2 ALU
+// adds are issued (no zero-extension moves).
+__device__ __forceinline__ u64 mul_shoup4(u64 a, u64 m, u64 w, u64 np) {
+  u64 r;
+  asm("{\n\t"
+      ".reg .u32 a0, a1, m0, m1, w0, w1, n0, n1, t1, t2, q0, q1, r0, r1;\n\t"
+      ".reg .u64 q, rr;\n\t"
+      "mov.b64 {a0, a1}, %1;\n\t"
+      "mov.b64 {m0, m1}, %2;\n\t"
+      "mov.b64 {w0, w1}, %3;\n\t"
+      "mov.b64 {n0, n1}, %4;\n\t"
+      "mul.hi.u32 t1, a1, w0;\n\t"
+      "mul.hi.u32 t2, a0, w1;\n\t"
+      "mul.wide.u32 q, a1, w1;\n\t"
+      "mov.b64 {q0, q1}, q;\n\t"
+      "add.cc.u32 q0, q0, t1;\n\t"
+      "addc.u32 q1, q1, 0;\n\t"
+      "add.cc.u32 q0, q0, t2;\n\t"
+      "addc.u32 q1, q1, 0;\n\t"
+      "mul.wide.u32 rr, a0, m0;\n\t"
+      "mad.wide.u32 rr, q0, n0, rr;\n\t"
+      "mov.b64 {r0, r1}, rr;\n\t"
+      "mad.lo.u32 r1, a0, m1, r1;\n\t"
+      "mad.lo.u32 r1, a1, m0, r1;\n\t"
+      "mad.lo.u32 r1, q0, n1, r1;\n\t"
+      "mad.lo.u32 r1, q1, n0, r1;\n\t"
+      "mov.b64 %0, {r0, r1};\n\t"
+      "}"
+      : "=l"(r)
+      : "l"(a), "l"(m), "l"(w), "l"(np));
+  return r;
+}
+
+// Reference (plain C) form of mul_shoup4, used by the probe to cross-check the PTX.
+__device__ __forceinline__ u64 mul_shoup4_c(u64 a, u64 m, u64 w, u64 np) {
+  const u32 a0 = lo32(a), a1 = hi32(a), w0 = lo32(w), w1 = hi32(w);
+  u64 q = mul_wide(a1, w1) + (u64)mul_hi(a1, w0) + (u64)mul_hi(a0, w1);
+  return a * m + q * np;
+}
+
+// Lazy-2: p < 2^63, exact Shoup quotient, any a < 2^64 -> r in [0, 2p).
+__device__ __forceinline__ u64 mul_shoup2(u64 a, u64 m, u64 w, u64 np) {
+  u64 q = __umul64hi(a, w);
+  return a * m + q * np;
+}
+
+// Conditional subtract: x in [0, 2p) -> [0, p).
+__device__ __forceinline__ u64 csub(u64 x, u64 p) { return x >= p ? x - p : x; }
+
+// ---------------------------------------------------------------- Montgomery
+// REDC(hi:lo) = (hi*2^64 + lo) * 2^-64 mod p, valid when hi:lo < p * 2^64; output in [0, p).
+__device__ __forceinline__ u64 redc(u64 hi, u64 lo, const ModParams& mp) {
+  u64 u = lo * mp.pinv;
+  u64 uh = __umul64hi(u, mp.p);
+  // lo + lo(u*p) == 0 mod 2^64, carry-out == (lo != 0)
+  u64 t = hi + uh + (lo != 0 ? 1ull : 0ull);
+  // t < 2p < 2^64 since p < 2^63
+  return csub(t, mp.p);
+}
+// a*b*2^-64 mod p, a*b < p*2^64 (e.g. a < p, b < 2^64 or a,b < p).
+__device__ __forceinline__ u64 mont_mul(u64 a, u64 b, const ModParams& mp) {
+  u64 hi, lo;
+  mul128(a, b, hi, lo);
+  return redc(hi, lo, mp);
+}
+__device__ __forceinline__ u64 to_mont(u64 a, const ModParams& mp) { return mont_mul(a, mp.r2, mp); }
+__device__ __forceinline__ u64 from_mont(u64 a, const ModParams& mp) { return redc(0, a, mp); }
+// Plain a*b mod p for a, b < p.
+__device__ __forceinline__ u64 mulmod(u64 a, u64 b, const ModParams& mp) {
+  return mont_mul(mont_mul(a, b, mp), mp.r2, mp);
+}
+
+// x^e in Montgomery form: xm = mont(x); returns mont(x^e).  Left-to-right square-and-multiply
+// ("exponentiations by squaring").
+__device__ __forceinline__ u64 mont_pow(u64 xm, u64 e, const ModParams& mp) {
+  u64 r = mp.r1;  // mont(1)
+  if (e == 0) return r;
+  int top = 63 - __clzll(e);
+  r = xm;
+  for (int b = top - 1; b >= 0; --b) {
+    r = mont_mul(r, r, mp);
+    if ((e >> b) & 1) r = mont_mul(r, xm, mp);
+  }
+  return r;
+}
+
+// c * m^e mod p for c < 2^64 (any), m < p.  Returns canonical [0, p).
+__device__ __forceinline__ u64 seed_pow(u64 c, u64 m, u64 e, const ModParams& mp) {
+  u64 xm = mont_pow(to_mont(m, mp), e, mp);   // m^e * R
+  // xm * c * R^-1 = c * m^e; needs xm * c < p * 2^64: xm < p, c < 2^64 ok.
+  return mont_mul(xm, c, mp);
+}
+
+// (hi * 2^64 + lo) mod p for any hi, lo.
+__device__ __forceinline__ u64 reduce128(u64 hi, u64 lo, const ModParams& mp) {
+  u64 h = hi < mp.p ? hi : hi % mp.p;
+  return mont_mul(redc(h, lo, mp), mp.r2, mp);
+}
+
+// floor(m * 2^64 / p) for m < p: restoring long division, 64 quotient bits.
+__device__ __forceinline__ u64 shoup_w(u64 m, u64 p) {
+  u64 r = m, q = 0;
+  #pragma unroll 1
+  for (int i = 0; i < 64; ++i) {
+    // r < p < 2^63 so (r << 1) does not overflow
+    r <<= 1;
+    q <<= 1;
+    if (r >= p) { r -= p; q |= 1; }
+  }
+  return q;
+}
+
+// ---------------------------------------------------------------- FP64 Alg. 2 / Alg. 3
+// Alg. 2, p < 2^50, x,y in [0,p) as exact doubles; returns [0,p).
+__device__ __forceinline__ double mul_fp(double x, double y, double p, double u) {
+  double h = __dmul_rn(x, y);            // line 1: h <- x*y
+  double l = __fma_rn(x, y, -h);         // line 2: l <- fma(x, y, -h)   (h + l == x*y exactly)
+  double b = __dmul_rn(h, u);            // line 3: b <- h*u
+  double c = floor(b);                   // line 4: c <- floor(b)  (quotient +-1)
+  double d = __fma_rn(-c, p, h);         // line 5: d <- fma(-c, p, h)
+  double g = __dadd_rn(d, l);            // line 6: g <- d + l      (remainder +-p)
+  if (g >= p) return __dsub_rn(g, p);    // line 7
+  if (g < 0.0) return __dadd_rn(g, p);   // line 8
+  return g;                              // line 9
+}
+// Alg. 3
+__device__ __forceinline__ double add_fp(double x, double y, double p) {
+  double s = __dadd_rn(x, y);
+  return s >= p ? __dsub_rn(s, p) : s;
+}
+
+}  // namespace pe

@@ -1,0 +1,513 @@
+// pe.cu -- C ABI (include/pe.h) and host planner of the B200 partial-evaluation library.
+//
+// pe_create: validate on the host (before any CUDA call), upload, then on the device:
+//   keys -> CUB radix sort (descending lex on (dx,dy)) -> run-length
+//   encode (the G buckets and their sizes) -> [host: tile plan from the G sizes] ->
+//   power tables -> k_setup (m_i, w_i, c_i in the padded tile layout).
+// pe_eval_device: per pass of points, k_step (seed + hot loop + in-CTA reduction) then
+//   k_fixup (cross-CTA sums -> canonical out).
+#include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/pe.h"
+#include "kernels.cuh"
+
+using namespace pe;
+
+// ---------------------------------------------------------------- errors
+static thread_local int g_last_error = PE_OK;
+static int set_err(int e) { g_last_error = e; return e; }
+
+#define CU(call)                                                                  \
+  do {                                                                            \
+    cudaError_t _e = (call);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      if (getenv("PE_DEBUG")) fprintf(stderr, "pe: %s:%d %s: %s\n", __FILE__,     \
+                                      __LINE__, #call, cudaGetErrorString(_e));   \
+      return set_err(_e == cudaErrorMemoryAllocation ? PE_ENOMEM : PE_ECUDA);     \
+    }                                                                             \
+  } while (0)
+
+// ---------------------------------------------------------------- host number theory
+typedef unsigned __int128 u128;
+static u64 h_mulmod(u64 a, u64 b, u64 p) { return (u64)(((u128)a * b) % p); }
+static u64 h_powmod(u64 b, u64 e, u64 p) {
+  u64 r = 1 % p;
+  b %= p;
+  while (e) {
+    if (e & 1) r = h_mulmod(r, b, p);
+    b = h_mulmod(b, b, p);
+    e >>= 1;
+  }
+  return r;
+}
+// Deterministic Miller-Rabin for 64-bit n with the 12 prime bases <= 37.
+static bool h_is_prime(u64 n) {
+  if (n < 2) return false;
+  static const u64 bases[12] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  for (u64 b : bases) {
+    if (n == b) return true;
+    if (n % b == 0) return false;
+  }
+  u64 d = n - 1;
+  int s = 0;
+  while ((d & 1) == 0) { d >>= 1; ++s; }
+  for (u64 b : bases) {
+    u64 x = h_powmod(b, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int i = 1; i < s; ++i) {
+      x = h_mulmod(x, x, n);
+      if (x == n - 1) { comp = false; break; }
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+static ModParams h_mod_params(u64 p) {
+  ModParams mp;
+  mp.p = p;
+  mp.np = (u64)0 - p;
+  // p^{-1} mod 2^64 by Newton iteration, then negate
+  u64 inv = p;  // correct to 3 bits for odd p
+  for (int i = 0; i < 6; ++i) inv *= 2 - p * inv;
+  mp.pinv = (u64)0 - inv;
+  mp.r1 = (u64)(((u128)1 << 64) % p);
+  mp.r2 = h_mulmod(mp.r1, mp.r1, p);
+  mp.pd = (double)p;
+  mp.u = 1.0 / (double)p;  // RN(1/p) (host IEEE division, default rounding)
+  return mp;
+}
+
+// ---------------------------------------------------------------- handle
+struct pe_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;  // handle's own stream (pe_create, pe_eval)
+  u64 p = 0, t = 0;
+  u32 n = 0;
+  ModParams mp{};
+  int path = kInt4;
+  int R = 8, W = 8, chunk_req = 0;
+  u64 G = 0, t_pad = 0;
+  u32 n_wt = 0, n_slots = 0;
+  std::vector<u32> dxdy;  // host copy [2G]
+  // device
+  u64 *d_c = nullptr, *d_m = nullptr, *d_w = nullptr;
+  u32* d_perm = nullptr;
+  uint2* d_wt_info = nullptr;
+  u32* d_slot_start = nullptr;
+  u64* d_partial = nullptr;
+  size_t partial_elems = 0;
+  u64* d_out_scratch = nullptr;
+  size_t out_scratch_elems = 0;
+  size_t partial_cap_bytes = (size_t)1 << 30;
+};
+
+static void free_all(pe_ctx* h) {
+  if (!h) return;
+  cudaFree(h->d_c); cudaFree(h->d_m); cudaFree(h->d_w); cudaFree(h->d_perm);
+  cudaFree(h->d_wt_info); cudaFree(h->d_slot_start); cudaFree(h->d_partial);
+  cudaFree(h->d_out_scratch);
+  if (h->stream) cudaStreamDestroy(h->stream);
+}
+
+template <class T>
+static int dalloc(T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  CU(cudaMalloc((void**)p, n * sizeof(T)));
+  return PE_OK;
+}
+
+static int env_int(const char* k, int dflt) {
+  const char* v = getenv(k);
+  return v && *v ? atoi(v) : dflt;
+}
+
+// ---------------------------------------------------------------- kernel dispatch
+template <int PATH>
+static cudaError_t launch_step_path(int R, dim3 grid, dim3 block, cudaStream_t s, const StepArgs& a) {
+  switch (R) {
+    case 1: k_step<PATH, 1><<<grid, block, 0, s>>>(a); break;
+    case 2: k_step<PATH, 2><<<grid, block, 0, s>>>(a); break;
+    case 4: k_step<PATH, 4><<<grid, block, 0, s>>>(a); break;
+    case 8: k_step<PATH, 8><<<grid, block, 0, s>>>(a); break;
+    case 16:
+      if (PATH == kFp64) return cudaErrorInvalidValue;
+      k_step<PATH == kFp64 ? kInt4 : PATH, 16><<<grid, block, 0, s>>>(a);
+      break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStream_t s, const StepArgs& a) {
+  if (path == kInt4) return launch_step_path<kInt4>(R, grid, block, s, a);
+  if (path == kInt2) return launch_step_path<kInt2>(R, grid, block, s, a);
+  return launch_step_path<kFp64>(R, grid, block, s, a);
+}
+
+static unsigned grid_for(u64 n, unsigned block) {
+  u64 b = (n + block - 1) / block;
+  if (b == 0) b = 1;
+  return (unsigned)std::min<u64>(b, 148ull * 64);
+}
+
+// ---------------------------------------------------------------- create
+static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64* alpha) {
+  const u64 t = h->t;
+  const u32 n = h->n;
+  const u32 nz = n - 2;
+  CU(cudaGetDevice(&h->device));
+  CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  cudaStream_t s = h->stream;
+  if (t == 0) {
+    h->G = 0;
+    return PE_OK;
+  }
+  if (t >= 0xffffffffull) return set_err(PE_ERANGE);
+
+  // ---- upload (a1)
+  u64* d_coeffs; u32* d_exps; u64* d_alpha;
+  if (dalloc(&d_coeffs, t) || dalloc(&d_exps, t * n) || dalloc(&d_alpha, nz + 1)) return g_last_error;
+  struct Tmp {
+    std::vector<void*> v;
+    ~Tmp() { for (void* p : v) cudaFree(p); }
+  } tmp;
+  tmp.v = {d_coeffs, d_exps, d_alpha};
+  std::vector<u64> alpha_red(nz + 1, 1);
+  for (u32 l = 0; l < nz; ++l) alpha_red[l] = alpha[l] % h->p;
+  CU(cudaMemcpyAsync(d_coeffs, coeffs, t * sizeof(u64), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(d_exps, exps, t * n * sizeof(u32), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(d_alpha, alpha_red.data(), (nz + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
+
+  // ---- keys, sort descending (a2)
+  u64 *d_key, *d_key2; u32 *d_idx, *d_idx2;
+  if (dalloc(&d_key, t) || dalloc(&d_key2, t) || dalloc(&d_idx, t) || dalloc(&d_idx2, t)) return g_last_error;
+  tmp.v.insert(tmp.v.end(), {d_key, d_key2, d_idx, d_idx2});
+  k_keys<<<grid_for(t, 256), 256, 0, s>>>(d_exps, t, n, d_key, d_idx);
+  CU(cudaGetLastError());
+  size_t sort_bytes = 0, rle_bytes = 0;
+  CU(cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, d_key, d_key2, d_idx, d_idx2, (int)t, 0, 64, s));
+  u64* d_ukeys; u32* d_counts; u32* d_nruns;
+  if (dalloc(&d_ukeys, t) || dalloc(&d_counts, t) || dalloc(&d_nruns, 1)) return g_last_error;
+  tmp.v.insert(tmp.v.end(), {d_ukeys, d_counts, d_nruns});
+  CU(cub::DeviceRunLengthEncode::Encode(nullptr, rle_bytes, d_key2, d_ukeys, d_counts, d_nruns, (int)t, s));
+  void* d_cub;
+  if (dalloc((char**)&d_cub, std::max(sort_bytes, rle_bytes))) return g_last_error;
+  tmp.v.push_back(d_cub);
+  CU(cub::DeviceRadixSort::SortPairsDescending(d_cub, sort_bytes, d_key, d_key2, d_idx, d_idx2, (int)t, 0, 64, s));
+  CU(cub::DeviceRunLengthEncode::Encode(d_cub, rle_bytes, d_key2, d_ukeys, d_counts, d_nruns, (int)t, s));
+
+  // max evaluated exponent -> power-table size
+  u32* d_dmax;
+  if (dalloc(&d_dmax, 1)) return g_last_error;
+  tmp.v.push_back(d_dmax);
+  CU(cudaMemsetAsync(d_dmax, 0, sizeof(u32), s));
+  if (nz) {
+    k_max_exp<<<grid_for(t, 256), 256, 0, s>>>(d_exps, t, n, d_dmax);
+    CU(cudaGetLastError());
+  }
+  u32 nruns = 0, D = 0;
+  CU(cudaMemcpyAsync(&nruns, d_nruns, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&D, d_dmax, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  const u64 G = nruns;
+  h->G = G;
+  std::vector<u64> ukeys(G);
+  std::vector<u32> counts(G);
+  CU(cudaMemcpyAsync(ukeys.data(), d_ukeys, G * sizeof(u64), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(counts.data(), d_counts, G * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  h->dxdy.resize(2 * G);
+  for (u64 g = 0; g < G; ++g) { h->dxdy[2 * g] = (u32)(ukeys[g] >> 32); h->dxdy[2 * g + 1] = (u32)ukeys[g]; }
+
+  // ---- host tile plan from the G bucket sizes
+  const int maxR = h->path == kFp64 ? 8 : 16;
+  int R = h->R;
+  if (R == 0) {
+    // largest R whose per-bucket padding wastes <= 6% of the terms (and R <= 8 by default)
+    R = 1;
+    for (int cand = 8; cand >= 1; cand >>= 1) {
+      u64 tile = 32ull * cand, padded = 0;
+      for (u64 g = 0; g < G; ++g) padded += (counts[g] + tile - 1) / tile * tile;
+      if (padded - t <= t * 6 / 100 || cand == 1) { R = cand; break; }
+    }
+  }
+  if (R != 1 && R != 2 && R != 4 && R != 8 && R != 16) return set_err(PE_EINVAL);
+  if (R > maxR) return set_err(PE_ENOTSUP);
+  h->R = R;
+  const u64 tile = 32ull * R;
+  std::vector<u64> poff(G + 1), bstart(G + 1);
+  poff[0] = bstart[0] = 0;
+  for (u64 g = 0; g < G; ++g) {
+    bstart[g + 1] = bstart[g] + counts[g];
+    poff[g + 1] = poff[g] + (counts[g] + tile - 1) / tile * tile;
+  }
+  h->t_pad = poff[G];
+  const u64 n_wt = h->t_pad / tile;
+  if (n_wt >= 0x7fffffffull) return set_err(PE_ERANGE);
+  h->n_wt = (u32)n_wt;
+  const int W = h->W;
+  std::vector<uint2> wt_info(n_wt);
+  std::vector<u32> wt_bucket(n_wt), slot_start(G + 1);
+  for (u64 g = 0; g < G; ++g)
+    for (u64 x = poff[g] / tile; x < poff[g + 1] / tile; ++x) wt_bucket[x] = (u32)g;
+  u32 slot = 0;
+  for (u64 x = 0; x < n_wt; ++x) {
+    bool start = (x % W == 0) || wt_bucket[x] != wt_bucket[x - 1];
+    if (start) {
+      if (x == 0 || wt_bucket[x] != wt_bucket[x - 1]) slot_start[wt_bucket[x]] = slot;
+      u32 len = 1;
+      while ((x + len) % W != 0 && x + len < n_wt && wt_bucket[x + len] == wt_bucket[x]) ++len;
+      wt_info[x] = make_uint2(slot, len);
+      ++slot;
+    } else {
+      wt_info[x] = make_uint2(slot - 1, 0);
+    }
+  }
+  slot_start[G] = slot;
+  h->n_slots = slot;
+
+  // ---- power tables (a3)
+  u64* d_table = nullptr;
+  const u64 tab_entries = (u64)nz * ((u64)D + 1);
+  if (nz && tab_entries <= (1ull << 22)) {
+    if (dalloc(&d_table, tab_entries)) return g_last_error;
+    tmp.v.push_back(d_table);
+    k_power_table<<<grid_for(tab_entries, 128), 128, 0, s>>>(d_alpha, nz, D, d_table, h->mp);
+    CU(cudaGetLastError());
+  }
+  // ---- padded layout + monomials
+  u64 *d_poff, *d_bstart;
+  if (dalloc(&d_poff, G + 1) || dalloc(&d_bstart, G + 1)) return g_last_error;
+  tmp.v.insert(tmp.v.end(), {d_poff, d_bstart});
+  CU(cudaMemcpyAsync(d_poff, poff.data(), (G + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(d_bstart, bstart.data(), (G + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
+  if (dalloc(&h->d_c, h->t_pad) || dalloc(&h->d_m, h->t_pad) || dalloc(&h->d_w, h->t_pad) ||
+      dalloc(&h->d_perm, h->t_pad) || dalloc(&h->d_wt_info, n_wt) || dalloc(&h->d_slot_start, G + 1))
+    return g_last_error;
+  k_setup<<<grid_for(h->t_pad, 256), 256, 0, s>>>(d_exps, d_coeffs, n, d_idx2, d_poff, d_bstart, (u32)G,
+                                                   h->t_pad, d_table, D, d_alpha, h->d_c, h->d_m, h->d_w,
+                                                   h->d_perm, h->mp);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(h->d_wt_info, wt_info.data(), n_wt * sizeof(uint2), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(h->d_slot_start, slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
+  CU(cudaStreamSynchronize(s));  // host vectors above must outlive the copies; tmp frees after
+  return PE_OK;
+}
+
+extern "C" pe_ctx* pe_create_ex(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs,
+                                const uint32_t* exps, const uint64_t* alpha, const pe_config* cfg) {
+  g_last_error = PE_OK;
+  // ---- validation before any CUDA call
+  if (n < 2 || n > 66) { set_err(PE_EINVAL); return nullptr; }
+  if (t > 0 && (!coeffs || !exps)) { set_err(PE_EINVAL); return nullptr; }
+  if (n > 2 && !alpha) { set_err(PE_EINVAL); return nullptr; }
+  if (p < 3 || p >= (1ull << 63)) { set_err(PE_ERANGE); return nullptr; }
+  if (!h_is_prime(p)) { set_err(PE_ENOTPRIME); return nullptr; }
+  for (u32 l = 0; l + 2 < n; ++l)
+    if (alpha[l] % p == 0) { set_err(PE_ERANGE); return nullptr; }
+  int path_req = cfg ? cfg->path : PE_PATH_AUTO;
+  if (path_req == PE_PATH_AUTO) {
+    const char* e = getenv("PE_PATH");
+    if (e && !strcmp(e, "int")) path_req = PE_PATH_INT;
+    if (e && !strcmp(e, "fp64")) path_req = PE_PATH_FP64;
+  }
+  int path;
+  if (path_req == PE_PATH_FP64) {
+    if (p >= (1ull << 50)) { set_err(PE_ENOTSUP); return nullptr; }
+    path = kFp64;
+  } else if (path_req == PE_PATH_INT) {
+    path = p < (1ull << 62) ? kInt4 : kInt2;
+  } else if (path_req == PE_PATH_AUTO) {
+    path = p < (1ull << 50) ? kFp64 : (p < (1ull << 62) ? kInt4 : kInt2);
+  } else {
+    set_err(PE_EINVAL);
+    return nullptr;
+  }
+  int R = cfg && cfg->R ? cfg->R : env_int("PE_R", 0);
+  int W = cfg && cfg->warps ? cfg->warps : env_int("PE_WARPS", 8);
+  int chunk = cfg && cfg->chunk ? cfg->chunk : env_int("PE_CHUNK", 0);
+  if (W < 1 || W > kMaxWarps || (R >= 16 && W > 8) || chunk < 0 || chunk % kSuper) {
+    set_err(PE_EINVAL);
+    return nullptr;
+  }
+  pe_ctx* h = new (std::nothrow) pe_ctx();
+  if (!h) { set_err(PE_ENOMEM); return nullptr; }
+  h->p = p; h->t = t; h->n = n;
+  h->mp = h_mod_params(p);
+  h->path = path;
+  h->R = R; h->W = W; h->chunk_req = chunk;
+  h->partial_cap_bytes = (size_t)env_int("PE_PARTIAL_MB", 1024) << 20;
+  int rc = create_impl(h, coeffs, exps, alpha);
+  if (rc != PE_OK) {
+    int e = g_last_error != PE_OK ? g_last_error : rc;
+    free_all(h);
+    delete h;
+    set_err(e);
+    return nullptr;
+  }
+  return h;
+}
+
+extern "C" pe_ctx* pe_create(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs,
+                             const uint32_t* exps, const uint64_t* alpha) {
+  return pe_create_ex(p, t, n, coeffs, exps, alpha, nullptr);
+}
+
+extern "C" void pe_destroy(pe_ctx* h) {
+  if (!h) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  cudaDeviceSynchronize();
+  free_all(h);
+  cudaSetDevice(cur);
+  delete h;
+}
+
+// ---------------------------------------------------------------- eval
+static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s) {
+  if (T == 0 || h->G == 0) return PE_OK;
+  const u64 nslots = h->n_slots;
+  // pass size bounded by the partial-buffer cap
+  u64 Tp = std::max<u64>(kSuper, h->partial_cap_bytes / 8 / std::max<u64>(nslots, 1));
+  Tp = std::min<u64>(Tp, T);
+  Tp = std::min<u64>(Tp, 1u << 30);
+  const size_t need = (size_t)nslots * Tp;
+  if (need > h->partial_elems) {
+    CU(cudaStreamSynchronize(s));
+    cudaFree(h->d_partial);
+    h->d_partial = nullptr;
+    h->partial_elems = 0;
+    CU(cudaMalloc((void**)&h->d_partial, need * sizeof(u64)));
+    h->partial_elems = need;
+  }
+  const int W = h->W;
+  const u32 n_cta = (h->n_wt + W - 1) / W;
+  for (u64 k0 = 0; k0 < T; k0 += Tp) {
+    const u32 np = (u32)std::min<u64>(Tp, T - k0);
+    u32 chunk = (u32)h->chunk_req;
+    if (chunk == 0) {
+      // cover the SMs: aim for >= 148 * 2 * 4 CTAs, but keep chunks long (seeding cost
+      // ~ 2 log2(j) Montgomery products per term per chunk)
+      const u64 target = 148ull * 2 * 4;
+      u64 nch = std::max<u64>(1, (target + n_cta - 1) / n_cta);
+      nch = std::min<u64>(nch, std::max<u64>(1, np / 512));
+      chunk = (u32)((np + nch - 1) / nch);
+      chunk = (chunk + kSuper - 1) / kSuper * kSuper;
+    }
+    StepArgs a;
+    a.c = h->d_c; a.m = h->d_m; a.w = h->d_w; a.wt_info = h->d_wt_info;
+    a.partial = h->d_partial; a.ldp = np; a.js0 = j0 + k0; a.n_wt = h->n_wt; a.npts = np;
+    a.chunk = chunk; a.mp = h->mp;
+    dim3 grid(n_cta, (np + chunk - 1) / chunk), block(32 * W);
+    cudaError_t e = launch_step(h->path, h->R, grid, block, s, a);
+    if (e != cudaSuccess) return set_err(PE_ECUDA);
+    const u32 nkb = (np + 255) / 256;
+    k_fixup<<<(unsigned)(h->G * nkb), 256, 0, s>>>(h->d_partial, np, h->d_slot_start, (u32)h->G, np, nkb,
+                                                   d_out + k0, ld, h->mp);
+    CU(cudaGetLastError());
+  }
+  return PE_OK;
+}
+
+extern "C" int pe_eval_device(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* d_out, uint64_t ld,
+                              void* stream) {
+  g_last_error = PE_OK;
+  if (!h) return set_err(PE_EINVAL);
+  if (T && j0 + (T - 1) < j0) return set_err(PE_ERANGE);
+  if (T && h->G && (!d_out || ld < T)) return set_err(PE_EINVAL);
+  return eval_device_impl(h, j0, T, d_out, ld, (cudaStream_t)stream);
+}
+
+extern "C" int pe_eval(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* out) {
+  g_last_error = PE_OK;
+  if (!h) return set_err(PE_EINVAL);
+  if (T && j0 + (T - 1) < j0) return set_err(PE_ERANGE);
+  if (T == 0 || h->G == 0) return PE_OK;
+  if (!out) return set_err(PE_EINVAL);
+  int cur = 0;
+  CU(cudaGetDevice(&cur));
+  if (cur != h->device) CU(cudaSetDevice(h->device));
+  const size_t need = (size_t)h->G * T;
+  int rc = PE_OK;
+  if (need > h->out_scratch_elems) {
+    cudaFree(h->d_out_scratch);
+    h->d_out_scratch = nullptr;
+    h->out_scratch_elems = 0;
+    if (cudaMalloc((void**)&h->d_out_scratch, need * sizeof(u64)) != cudaSuccess) rc = set_err(PE_ENOMEM);
+    else h->out_scratch_elems = need;
+  }
+  if (rc == PE_OK) rc = eval_device_impl(h, j0, T, h->d_out_scratch, T, h->stream);
+  if (rc == PE_OK) {
+    if (cudaMemcpyAsync(out, h->d_out_scratch, need * sizeof(u64), cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+        cudaStreamSynchronize(h->stream) != cudaSuccess)
+      rc = set_err(PE_ECUDA);
+  }
+  if (cur != h->device) cudaSetDevice(cur);
+  return rc;
+}
+
+// ---------------------------------------------------------------- introspection
+extern "C" uint64_t pe_num_buckets(const pe_ctx* h) { return h ? h->G : 0; }
+
+extern "C" int pe_bucket_exps(const pe_ctx* h, uint32_t* dxdy) {
+  if (!h || (h->G && !dxdy)) return set_err(PE_EINVAL);
+  if (h->G) memcpy(dxdy, h->dxdy.data(), 2 * h->G * sizeof(u32));
+  return PE_OK;
+}
+
+extern "C" int pe_info(const pe_ctx* h, int32_t* path, int32_t* R, int32_t* warps, uint64_t* t_padded,
+                       uint64_t* n_slots) {
+  if (!h) return set_err(PE_EINVAL);
+  if (path) *path = h->path == kFp64 ? PE_PATH_FP64 : PE_PATH_INT;
+  if (R) *R = h->R;
+  if (warps) *warps = h->W;
+  if (t_padded) *t_padded = h->t_pad;
+  if (n_slots) *n_slots = h->n_slots;
+  return PE_OK;
+}
+
+extern "C" int pe_monomials(const pe_ctx* h, uint64_t* m) {
+  if (!h || (h->t && !m)) return set_err(PE_EINVAL);
+  if (h->t == 0) return PE_OK;
+  u64* d;
+  CU(cudaMalloc((void**)&d, h->t * sizeof(u64)));
+  k_scatter_m<<<grid_for(h->t_pad, 256), 256, 0, h->stream>>>(h->d_m, h->d_perm, h->t_pad, d);
+  cudaError_t e = cudaMemcpyAsync(m, d, h->t * sizeof(u64), cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return set_err(PE_ECUDA);
+  return PE_OK;
+}
+
+extern "C" int pe_last_error(void) { return g_last_error; }
+
+extern "C" const char* pe_strerror(int code) {
+  switch (code) {
+    case PE_OK: return "ok";
+    case PE_EINVAL: return "invalid argument";
+    case PE_ENOTPRIME: return "p is not prime";
+    case PE_ERANGE: return "value out of range";
+    case PE_ENOMEM: return "out of memory";
+    case PE_ECUDA: return "CUDA error";
+    case PE_ENOTSUP: return "not supported for this p";
+    default: return "unknown error";
+  }
+}
+
+extern "C" int pe_interp_bound_ok(uint64_t p, uint64_t t) {
+  u128 b = (u128)100 * t * t;
+  return (u128)p > b ? 1 : 0;
+}

@@ -1,0 +1,192 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element,
+on the same seeded inputs.  Bit-exact: results are canonical
+residues, unique (reading R14)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2004_11571_b200 as pe
+import synth
+
+pytestmark = pytest.mark.gpu
+
+P62, P50 = synth.P62, synth.P50
+
+
+def gpu_eval(w, j0=None, T=None, **kw):
+    with pe.Context.from_workload(w, **kw) as ctx:
+        out = ctx.eval(w.j0 if j0 is None else j0, w.T if T is None else T)
+        rows = ctx.buckets()
+    return rows, out
+
+
+def check_full(w, **kw):
+    rows, out = gpu_eval(w, **kw)
+    assert rows.tolist() == oracle.buckets(w.exps, w.n).tolist()
+    ref = oracle.eval_workload(w)
+    assert out.shape == ref.shape
+    bad = np.argwhere(out != ref)
+    assert bad.size == 0, f"{len(bad)} mismatches, first {bad[:5].tolist()}"
+    return out
+
+
+# ---------------------------------------------------------------- BASELINE configs
+def test_config1_full():
+    check_full(synth.gen_config(1))
+
+
+def test_config2_full():
+    check_full(synth.gen_config(2))
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_config3_4_full_incremental_and_sampled_direct(cfg):
+    w = synth.gen_config(cfg)
+    rows, out = gpu_eval(w)
+    assert rows.tolist() == oracle.buckets(w.exps, w.n).tolist()
+    inc = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
+    assert np.array_equal(out, inc)
+    ks = np.array([0, 1, 31, 32, 1023, 1024, 2047, 4095], np.uint64)
+    ref = oracle.eval_workload(w, ks=ks)
+    assert np.array_equal(out[:, ks.astype(np.int64)], ref)
+
+
+def test_config4_fp64_equals_int():
+    w = synth.gen_config(4, t=200_000, T=512)
+    _, a = gpu_eval(w, path=pe.PATH_FP64)
+    _, b = gpu_eval(w, path=pe.PATH_INT)
+    assert np.array_equal(a, b)
+    ref = oracle.eval_workload(w, ks=np.arange(0, 512, 37, dtype=np.uint64))
+    assert np.array_equal(a[:, 0:512:37], ref)
+
+
+def test_config5_sampled_and_edges():
+    """Full size (t = 10^7, T = 16384, the bench launch configuration): 8 columns against the
+    direct oracle, and the first/last 64 columns against the incremental checker."""
+    w = synth.gen_config(5)
+    with pe.Context.from_workload(w) as ctx:
+        out = ctx.eval(w.j0, w.T)
+        rows = ctx.buckets()
+    assert rows.tolist() == oracle.buckets(w.exps, w.n).tolist()
+    ks = np.array([0, 1, 777, 4096, 8191, 12345, 16382, 16383], np.uint64)
+    ref = oracle.eval_workload(w, ks=ks)
+    assert np.array_equal(out[:, ks.astype(np.int64)], ref)
+    head = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, 64)
+    assert np.array_equal(out[:, :64], head)
+    tail = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0 + w.T - 64, 64)
+    assert np.array_equal(out[:, -64:], tail)
+
+
+# ---------------------------------------------------------------- tuning invariance (P13)
+@pytest.mark.parametrize("R,warps,chunk", [(1, 8, 0), (2, 4, 32), (4, 16, 64), (8, 1, 96), (16, 8, 0),
+                                           (8, 8, 0), (16, 2, 32)])
+def test_tuning_invariance(R, warps, chunk):
+    w = synth.gen_config(2, t=20_000, T=161)
+    ref = oracle.eval_workload(w)
+    _, out = gpu_eval(w, R=R, warps=warps, chunk=chunk)
+    assert np.array_equal(out, ref)
+
+
+def test_multi_pass_partial_buffer(monkeypatch):
+    monkeypatch.setenv("PE_PARTIAL_MB", "1")            # forces several point passes
+    w = synth.gen_config(3, t=50_000, T=700)
+    rows, out = gpu_eval(w, R=1)
+    ref = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
+    assert np.array_equal(out, ref)
+
+
+def test_eval_device_ld_and_stream():
+    import torch
+    w = synth.gen_config(1)
+    ref = oracle.eval_workload(w)
+    G, T = ref.shape
+    s = torch.cuda.Stream()
+    buf = torch.full((G, T + 13), -1, dtype=torch.int64, device="cuda")
+    with pe.Context.from_workload(w) as ctx:
+        ctx.eval_device(w.j0, T, buf.data_ptr(), T + 13, s.cuda_stream)
+        s.synchronize()
+    got = buf.cpu().numpy().view(np.uint64)
+    assert np.array_equal(got[:, :T], ref)
+    assert np.all(got[:, T:] == np.uint64(2**64 - 1))     # padding columns untouched
+
+
+# ---------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("p,n,t,maxdeg,j0,T", [
+    (P62, 6, 300, 4, 1, 1),              # T = 1
+    (P62, 6, 300, 4, 1, 33),             # ragged vs the 32-point super-group
+    (P62, 5, 500, 3, 0, 70),             # j0 = 0 (beta^0)
+    (P62, 5, 200, 3, 2**64 - 40, 40),    # largest j range
+    (13, 4, 60, 3, 0, 50),               # tiny prime (unlucky-point size)
+    (3, 5, 40, 2, 5, 20),                # smallest prime
+    ((1 << 63) - 25, 6, 400, 3, 7, 45),  # INT lazy-2 path (p >= 2^62)
+    (P50, 7, 600, 4, 3, 77),             # FP64 path
+    (2**31 - 1, 3, 100, 9, 1, 64),       # n = 3
+    (1009, 2, 50, 6, 1, 10),             # n = 2 (nothing evaluated)
+])
+def test_edge_shapes(p, n, t, maxdeg, j0, T):
+    w = synth.random_small(100 + t + n, p, n, t, maxdeg, T, j0, coeff_hi=2**64 - 1)
+    check_full(w)
+
+
+def test_single_term_and_single_bucket():
+    w = synth.random_small(201, P62, 5, 1, 3, 40, 1)
+    check_full(w)
+    w = synth.random_small(202, P62, 6, 700, 4, 40, 1)
+    w.exps[:, :2] = 3                                         # G = 1
+    check_full(w)
+
+
+def test_duplicates_zero_coeffs_alpha_ge_p():
+    w = synth.random_small(203, P62, 5, 400, 2, 50, 1, dup=True)
+    w.coeffs[::7] = 0
+    w.coeffs[1::11] = np.uint64(P62 + 5)
+    w.alpha = (w.alpha + np.uint64(P62)).astype(np.uint64)    # alpha >= p, reduced by the callee
+    check_full(w)
+
+
+def test_fermat_periodicity_gpu():
+    w = synth.random_small(204, P62, 6, 500, 3, 64, 1)
+    _, a = gpu_eval(w, j0=1)
+    _, b = gpu_eval(w, j0=1 + (P62 - 1))
+    assert np.array_equal(a, b)
+
+
+def test_empty_polynomial_and_T0():
+    with pe.Context(P62, np.zeros(0, np.uint64), np.zeros((0, 4), np.uint32), [2, 3], n=4) as ctx:
+        assert ctx.G == 0
+        assert ctx.eval(1, 5).shape == (0, 5)
+    w = synth.gen_config(1)
+    with pe.Context.from_workload(w) as ctx:
+        assert ctx.eval(1, 0).shape == (ctx.G, 0)
+
+
+def test_monomials_match_python():
+    w = synth.random_small(205, P62, 7, 3000, 5, 1, 1, dup=True)
+    with pe.Context.from_workload(w) as ctx:
+        m = ctx.monomials()
+    for i in range(0, 3000, 17):
+        v = 1
+        for a, e in zip(w.alpha, w.exps[i, 2:]):
+            v = v * pow(int(a), int(e), P62) % P62
+        assert int(m[i]) == v
+
+
+def test_large_exponents_no_power_table():
+    """Exponents beyond the power-table limit take the direct-power branch of k_setup."""
+    w = synth.random_small(206, P62, 4, 200, 3, 20, 1)
+    w.exps[::3, 2] = np.uint32(3_000_000)
+    w.exps[1::5, 3] = np.uint32(4_000_000_000)
+    check_full(w)
+
+
+def test_error_codes_gpu():
+    with pytest.raises(pe.PEError) as ei:
+        pe.Context(15, [1], [[0, 0, 1]], [2])
+    assert ei.value.code == pe.PE_ENOTPRIME
+    w = synth.gen_config(1)
+    with pe.Context.from_workload(w) as ctx:
+        with pytest.raises(pe.PEError) as ei:
+            ctx.eval(2**64 - 10, 20)
+        assert ei.value.code == pe.PE_ERANGE
