@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the partial-evaluation hot path (BASELINE.json metric) on 1..N B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A step = one pass of the whole hot path over the workload: for the T points, seed a_i at the
+shard start, step-and-reduce, cross-CTA fix-up (pe_eval_device), and for N > 1 the NCCL
+gather of the G x T_r blocks to rank 0.  T is sharded across ranks
+(strong scaling: the config fixes T = 16384 "sharded across 1/2/4/8 GPUs").
+
+value  = t*T / device time per step (max over ranks), inputs resident in HBM.
+e2e    = the same metric through the C ABI from pinned HOST inputs to a HOST result:
+         pe_create (H2D of coeffs/exps/alpha + device planning + K1) + pe_eval(_device)
+         + gather + D2H of the G x T result, every step.
+roofline = k_step (dominant kernel) term-points per launch / its CUDA-event launch time vs
+         the ALU peak derived in DESIGN.md §Roofline (148 SMs x 64 IMAD-pipe lanes/clk x clock
+         / 9 IMAD-pipe instructions per term-point).
+cpu_baseline / --impl reference = the CPU oracle (oracle/, direct definition) on a bounded
+         column sample of the same workload, on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "term-point modular evaluations/sec (62-bit p) at 1/2/4/8 B200; % mulmod roofline"
+UNIT = "term-points/s"
+IMAD_PIPE_OPS_PER_TP = 9          # Shoup-lazy step = 3 IMAD.WIDE + 2 IMAD.HI + 4 IMAD
+IMAD_LANES_PER_CLK_SM = 64        # B300_MICROARCH.md "fma-pipe ... rt_SMSP=2" -> 16 lanes/clk/SMSP x 4
+N_SM = 148
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ---------------------------------------------------------------- clocks sampling
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p:
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+                out, _ = self.p.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        load = [s for s in sm if s > 0.5 * mx] if mx else sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU oracle leg
+def oracle_sample(w, ncols: int, seed: int = 0):
+    """Time the direct oracle (as it stands) on ncols sampled columns of the workload."""
+    import oracle
+    oracle.build()
+    rng = np.random.default_rng(seed)
+    ks = np.sort(rng.choice(w.T, size=min(ncols, w.T), replace=False)).astype(np.uint64)
+    t0 = time.perf_counter()
+    oracle.eval_workload(w, ks=ks)
+    dt = time.perf_counter() - t0
+    return w.t * len(ks), dt, ks
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, w, rank, world):
+    if rank != 0:
+        return
+    cores = host_cores()
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    ncols = cores                                   # one sampled column per core per step
+    times = []
+    tp = 0
+    for i in range(args.warmup + args.steps):
+        n_tp, dt, _ = oracle_sample(w, ncols, seed=i)
+        if i >= args.warmup:
+            times.append(dt)
+            tp = n_tp
+    ms = 1e3 * statistics.mean(times)
+    value = tp / (ms * 1e-3)
+    sample = f"{w.name}: all {w.t} terms x {ncols} sampled columns of T={w.T} per step (direct oracle)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": workload_config(w, None),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(w, info):
+    cfg = {"workload": w.name, "t": w.t, "n": w.n, "T": w.T, "j0": w.j0, "p": w.p,
+           "term_points_per_step": w.t * w.T,
+           "l2": "inputs larger than L2 (c, m, w: 3 x 8 B x t_padded; partials G x T)"}
+    if info:
+        cfg.update({"path": info["path"], "R": info["R"], "warps": info["warps"], "t_padded": info["t_padded"],
+                    "n_slots": info["n_slots"], "G": info.get("G")})
+    return cfg
+
+
+# ---------------------------------------------------------------- GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-cols", type=int, default=0, help="oracle sample columns (0 = 4 x cores)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+
+    import synth
+    t0 = time.perf_counter()
+    w = synth.gen_config(args.config)
+    log(f"[rank {rank}] generated {w.name}: t={w.t} n={w.n} T={w.T} in {time.perf_counter() - t0:.1f}s")
+
+    if args.impl == "reference":
+        return run_reference(args, w, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2004_11571_b200 as pe
+    from paper_2004_11571_b200.dist import ShardedEval
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- handle (pe_create) -- outside the device-timed region
+    t0 = time.perf_counter()
+    ctx = pe.Context.from_workload(w)
+    torch.cuda.synchronize()
+    create_s = time.perf_counter() - t0
+    info = ctx.info()
+    info["G"] = ctx.G
+    sh = ShardedEval(ctx.G, w.T, dev)
+
+    def eval_local(j_first, cnt, out):
+        ctx.eval_device(j_first, cnt, out.data_ptr(), out.shape[1], stream.cuda_stream)
+
+    def step():
+        return sh.run(eval_local, w.j0)
+
+    # ---- device-timed region
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.kernel_stats()                      # drop anything recorded so far
+    barrier()
+    torch.cuda.synchronize()
+    ctx.set_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ctx.set_timing(False)
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    ks = ctx.kernel_stats()
+    value = w.t * w.T / (ms * 1e-3)
+    clocks = clk.summary()
+
+    # ---- roofline of k_step (dominant kernel)
+    pk, pk_kind = peaks()
+    step_ms = ks["step_ms"] / max(ks["step_launches"], 1)
+    launches_tp = ks["term_points"] / max(ks["step_launches"], 1)        # padded term-points / launch
+    algo_tp = w.t * sh.cnt if sh.cnt else 0                                 # algorithmic term-points / launch
+    achieved = algo_tp / (step_ms * 1e-3) if step_ms else 0.0
+    sm_mhz = pk.get("sm_max_mhz", 1965.0)
+    peak = N_SM * sm_mhz * 1e6 * IMAD_LANES_PER_CLK_SM / IMAD_PIPE_OPS_PER_TP
+    roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tterm-pt/s",
+            "frac": achieved / peak if peak else None, "traffic": None,
+            "kernel": f"k_step<{info['path']},R={info['R']}>",
+            "peak_basis": (f"{N_SM} SMs x {sm_mhz:.0f} MHz ({pk_kind} sm_max_mhz) x {IMAD_LANES_PER_CLK_SM} "
+                           f"IMAD-pipe lanes/clk / {IMAD_PIPE_OPS_PER_TP} IMAD-pipe ops per term-point"),
+            "frac_at_run_clock": (achieved / (peak * clocks["sm_mhz"] / sm_mhz)
+                                  if clocks.get("sm_mhz") else None),
+            "step_ms": step_ms, "fixup_ms": ks["fixup_ms"] / max(ks["step_launches"], 1),
+            "padded_term_points_per_launch": launches_tp, "term_points_per_launch": algo_tp}
+    gpu_launches = 2 * ks["step_launches"]           # k_step + k_fixup per pass (rank 0)
+
+    # ---- end-to-end: host inputs -> host result through the C ABI, every step
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64) if a.dtype == np.uint64
+                                         else np.ascontiguousarray(a).view(np.int32)).pin_memory()
+        h_c, h_e, h_a = pin(w.coeffs), pin(w.exps), pin(w.alpha)
+        h_out = torch.empty((ctx.G, w.T), dtype=torch.int64).pin_memory() if sh.is_root else None
+        L = pe.lib()
+        import ctypes
+
+        def e2e_step():
+            h = L.pe_create(w.p, w.t, w.n, ctypes.c_void_p(h_c.data_ptr()), ctypes.c_void_p(h_e.data_ptr()),
+                            ctypes.c_void_p(h_a.data_ptr()))
+            if not h:
+                raise pe.PEError(L.pe_last_error(), "pe_create")
+            try:
+                if world == 1:
+                    rc = L.pe_eval(h, w.j0, w.T, ctypes.c_void_p(h_out.data_ptr()))
+                    if rc:
+                        raise pe.PEError(rc, "pe_eval")
+                else:
+                    def ev(j_first, cnt, out):
+                        rc = L.pe_eval_device(h, j_first, cnt, ctypes.c_void_p(out.data_ptr()), out.shape[1],
+                                              ctypes.c_void_p(stream.cuda_stream))
+                        if rc:
+                            raise pe.PEError(rc, "pe_eval_device")
+                    res = sh.run(ev, w.j0)
+                    if sh.is_root:
+                        h_out.copy_(res)
+                    torch.cuda.synchronize()
+            finally:
+                L.pe_destroy(h)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(max(3, min(args.steps, 5))):
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step()
+            torch.cuda.synchronize()
+            ts.append(max_over_ranks(time.perf_counter() - t0))
+        e2e_s = statistics.median(ts)
+        h2d = w.coeffs.nbytes + w.exps.nbytes + w.alpha.nbytes
+        e2e = {"value": w.t * w.T / e2e_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_s,
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": ctx.G * w.T * 8,
+               "includes": "pe_create (H2D + sort + plan + K1) + eval + gather + D2H, host wall clock, max over ranks"}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        cores = host_cores()
+        os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+        ncols = args.cpu_cols or 4 * cores
+        n_tp, dt, _ = oracle_sample(w, ncols)
+        cpu = {"value": n_tp / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{w.name}: all {w.t} terms x {ncols} random columns of T={w.T} "
+                         f"(direct definition, OpenMP over columns), {dt:.1f} s"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": workload_config(w, info), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": gpu_launches, "clocks": clocks,
+                "create_s": create_s, "parallelism": f"point-range shards x{world}, NCCL gather"}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -105,6 +105,16 @@ int pe_info(const pe_ctx* h, int32_t* path, int32_t* R, int32_t* warps, uint64_t
 /* m_i = prod_l alpha_l^{e_i,l} mod p for every input term i (HOST uint64[t], input order). */
 int pe_monomials(const pe_ctx* h, uint64_t* m);
 
+/*
+ * Kernel timing (for bench.py's roofline): when enabled, pe_eval_device records CUDA events
+ * on its stream around every k_step (hot loop) and k_fixup launch.  pe_kernel_stats waits for
+ * the recorded events, returns the accumulated launch count, device milliseconds of each
+ * kernel and the term-points k_step processed (padded terms x points), then resets them.
+ */
+int pe_set_timing(pe_ctx* h, int enable);
+int pe_kernel_stats(pe_ctx* h, uint64_t* step_launches, double* step_ms, double* fixup_ms,
+                    double* term_points);
+
 int pe_last_error(void);            /* thread-local code of the last failing call */
 const char* pe_strerror(int code);
 

@@ -26,7 +26,7 @@ CORE_SHOUP4, CORE_SHOUP2, CORE_MONT, CORE_FP64, CORE_FP64ADD, CORE_POW, CORE_SHO
 #: every symbol include/pe.h and include/pe_test.h declare
 EXPORTS = ["pe_create", "pe_create_ex", "pe_eval", "pe_eval_device", "pe_destroy", "pe_num_buckets",
            "pe_bucket_exps", "pe_info", "pe_monomials", "pe_last_error", "pe_strerror",
-           "pe_interp_bound_ok", "pe_test_core", "pe_bench_core"]
+           "pe_interp_bound_ok", "pe_test_core", "pe_bench_core", "pe_set_timing", "pe_kernel_stats"]
 
 
 class PEError(RuntimeError):
@@ -83,6 +83,11 @@ def lib():
                                     ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double),
                                     ctypes.POINTER(ctypes.c_double)]
         L.pe_bench_core.restype = ctypes.c_int
+        L.pe_set_timing.argtypes = [vp, ctypes.c_int]
+        L.pe_set_timing.restype = ctypes.c_int
+        L.pe_kernel_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double),
+                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+        L.pe_kernel_stats.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -164,6 +169,15 @@ class Context:
         assert out.dtype == np.uint64 and out.flags.c_contiguous and out.size == self.G * T
         _check(lib().pe_eval(self._h, j0, T, _ptr(out)), "pe_eval")
         return out
+
+    def set_timing(self, enable: bool = True):
+        _check(lib().pe_set_timing(self._h, int(enable)), "pe_set_timing")
+
+    def kernel_stats(self) -> dict:
+        n, s, f, tp = ctypes.c_uint64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        _check(lib().pe_kernel_stats(self._h, ctypes.byref(n), ctypes.byref(s), ctypes.byref(f), ctypes.byref(tp)),
+               "pe_kernel_stats")
+        return {"step_launches": n.value, "step_ms": s.value, "fixup_ms": f.value, "term_points": tp.value}
 
     def eval_device(self, j0: int, T: int, d_out: int, ld: int | None = None, stream: int = 0):
         """pe_eval_device into a device pointer (e.g. ``torch_tensor.data_ptr()``)."""

@@ -110,10 +110,20 @@ struct pe_ctx {
   u64* d_out_scratch = nullptr;
   size_t out_scratch_elems = 0;
   size_t partial_cap_bytes = (size_t)1 << 30;
+  // kernel timing (pe_set_timing / pe_kernel_stats)
+  bool timing = false;
+  struct Rec { cudaEvent_t e0, e1, e2; double tp; };
+  std::vector<Rec> recs;
 };
+
+static void drop_recs(pe_ctx* h) {
+  for (auto& r : h->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); cudaEventDestroy(r.e2); }
+  h->recs.clear();
+}
 
 static void free_all(pe_ctx* h) {
   if (!h) return;
+  drop_recs(h);
   cudaFree(h->d_c); cudaFree(h->d_m); cudaFree(h->d_w); cudaFree(h->d_perm);
   cudaFree(h->d_wt_info); cudaFree(h->d_slot_start); cudaFree(h->d_partial);
   cudaFree(h->d_out_scratch);
@@ -412,12 +422,25 @@ static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaSt
     a.partial = h->d_partial; a.ldp = np; a.js0 = j0 + k0; a.n_wt = h->n_wt; a.npts = np;
     a.chunk = chunk; a.mp = h->mp;
     dim3 grid(n_cta, (np + chunk - 1) / chunk), block(32 * W);
+    pe_ctx::Rec rec{};
+    if (h->timing) {
+      CU(cudaEventCreate(&rec.e0));
+      CU(cudaEventCreate(&rec.e1));
+      CU(cudaEventCreate(&rec.e2));
+      rec.tp = (double)h->t_pad * np;
+      CU(cudaEventRecord(rec.e0, s));
+    }
     cudaError_t e = launch_step(h->path, h->R, grid, block, s, a);
     if (e != cudaSuccess) return set_err(PE_ECUDA);
+    if (h->timing) CU(cudaEventRecord(rec.e1, s));
     const u32 nkb = (np + 255) / 256;
     k_fixup<<<(unsigned)(h->G * nkb), 256, 0, s>>>(h->d_partial, np, h->d_slot_start, (u32)h->G, np, nkb,
                                                    d_out + k0, ld, h->mp);
     CU(cudaGetLastError());
+    if (h->timing) {
+      CU(cudaEventRecord(rec.e2, s));
+      h->recs.push_back(rec);
+    }
   }
   return PE_OK;
 }
@@ -489,6 +512,33 @@ extern "C" int pe_monomials(const pe_ctx* h, uint64_t* m) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   cudaFree(d);
   if (e != cudaSuccess) return set_err(PE_ECUDA);
+  return PE_OK;
+}
+
+extern "C" int pe_set_timing(pe_ctx* h, int enable) {
+  if (!h) return set_err(PE_EINVAL);
+  h->timing = enable != 0;
+  return PE_OK;
+}
+
+extern "C" int pe_kernel_stats(pe_ctx* h, uint64_t* step_launches, double* step_ms, double* fixup_ms,
+                               double* term_points) {
+  if (!h) return set_err(PE_EINVAL);
+  double s_ms = 0, f_ms = 0, tp = 0;
+  for (auto& r : h->recs) {
+    float a = 0, b = 0;
+    if (cudaEventSynchronize(r.e2) != cudaSuccess || cudaEventElapsedTime(&a, r.e0, r.e1) != cudaSuccess ||
+        cudaEventElapsedTime(&b, r.e1, r.e2) != cudaSuccess)
+      return set_err(PE_ECUDA);
+    s_ms += a;
+    f_ms += b;
+    tp += r.tp;
+  }
+  if (step_launches) *step_launches = h->recs.size();
+  if (step_ms) *step_ms = s_ms;
+  if (fixup_ms) *fixup_ms = f_ms;
+  if (term_points) *term_points = tp;
+  drop_recs(h);
   return PE_OK;
 }
 

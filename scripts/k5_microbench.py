@@ -1,6 +1,7 @@
 """K5 microbenchmarks: register-resident pipe rates and the mulmod+add step rate (no memory).
 Prints ops / clock / SM (from clock64 cycles) and ops/s (from CUDA events)."""
-import json, sys
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2004_11571_b200 as pe
 
 P62 = (1 << 62) - 57
