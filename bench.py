@@ -14,8 +14,9 @@ e2e    = the same metric through the C ABI from pinned HOST inputs to a HOST res
          pe_create (H2D of coeffs/exps/alpha + device planning + K1) + pe_eval(_device)
          + gather + D2H of the G x T result, every step.
 roofline = k_step (dominant kernel) term-points per launch / its CUDA-event launch time vs
-         the ALU peak derived in DESIGN.md §Roofline (148 SMs x 64 IMAD-pipe lanes/clk x clock
-         / 9 IMAD-pipe instructions per term-point).
+         the integer-pipe mulmod peak derived in DESIGN.md §Roofline (148 SMs x clock x 64
+         IMAD lanes/clk / 14 IMAD slots per 64-bit Shoup product), plus the register-resident
+         K5 ceiling of the same step measured in the same run.
 cpu_baseline / --impl reference = the CPU oracle (oracle/, direct definition) on a bounded
          column sample of the same workload, on this host's cores.
 """
@@ -36,8 +37,8 @@ import numpy as np  # noqa: E402
 
 METRIC = "term-point modular evaluations/sec (62-bit p) at 1/2/4/8 B200; % mulmod roofline"
 UNIT = "term-points/s"
-IMAD_PIPE_OPS_PER_TP = 9          # Shoup-lazy step = 3 IMAD.WIDE + 2 IMAD.HI + 4 IMAD
-IMAD_LANES_PER_CLK_SM = 64        # B300_MICROARCH.md "fma-pipe ... rt_SMSP=2" -> 16 lanes/clk/SMSP x 4
+IMAD_SLOTS_PER_TP = 14            # 4 low products x 1 + 5 full-width (HI/WIDE) x 2
+IMAD_LANES_PER_CLK_SM = 64        # measured IMAD lanes/clk/SM (profiles/r01_pipe_bench.jsonl)
 N_SM = 148
 
 
@@ -252,16 +253,29 @@ def main():
     algo_tp = w.t * sh.cnt if sh.cnt else 0                                 # algorithmic term-points / launch
     achieved = algo_tp / (step_ms * 1e-3) if step_ms else 0.0
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
-    peak = N_SM * sm_mhz * 1e6 * IMAD_LANES_PER_CLK_SM / IMAD_PIPE_OPS_PER_TP
+    peak = N_SM * sm_mhz * 1e6 * IMAD_LANES_PER_CLK_SM / IMAD_SLOTS_PER_TP
+    # register-resident ceiling of the same step (K5, no memory / reduction), measured now
+    k5 = None
+    try:
+        k5_ms, k5_steps, _ = pe.bench_core(pe.CORE_SHOUP4 if info["path"] == "int" else pe.CORE_FP64,
+                                           w.p, 8, N_SM * 4, 256, 256)
+        k5 = k5_steps / (k5_ms * 1e-3)
+    except pe.PEError:
+        pass
     roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tterm-pt/s",
             "frac": achieved / peak if peak else None, "traffic": None,
             "kernel": f"k_step<{info['path']},R={info['R']}>",
-            "peak_basis": (f"{N_SM} SMs x {sm_mhz:.0f} MHz ({pk_kind} sm_max_mhz) x {IMAD_LANES_PER_CLK_SM} "
-                           f"IMAD-pipe lanes/clk / {IMAD_PIPE_OPS_PER_TP} IMAD-pipe ops per term-point"),
+            "peak_basis": (f"IMAD-pipe model (DESIGN.md Roofline): {N_SM} SMs x {sm_mhz:.0f} MHz ({pk_kind} "
+                           f"sm_max_mhz) x {IMAD_LANES_PER_CLK_SM} IMAD lanes/clk/SM / {IMAD_SLOTS_PER_TP} "
+                           "IMAD slots per 64-bit Shoup mulmod (4 low x 1 + 5 full-width x 2; measured "
+                           "IMAD 64, IMAD.HI 32 lanes/clk/SM, profiles/r01_pipe_bench.jsonl)"),
             "frac_at_run_clock": (achieved / (peak * clocks["sm_mhz"] / sm_mhz)
                                   if clocks.get("sm_mhz") else None),
+            "k5_register_resident_ceiling": k5 / 1e12 if k5 else None,
+            "frac_of_k5_ceiling": achieved / k5 if k5 else None,
             "step_ms": step_ms, "fixup_ms": ks["fixup_ms"] / max(ks["step_launches"], 1),
-            "padded_term_points_per_launch": launches_tp, "term_points_per_launch": algo_tp}
+            "padded_term_points_per_launch": launches_tp, "term_points_per_launch": algo_tp,
+            "algorithmic_bytes_per_launch": 16 * w.t + 8 * ctx.G * sh.cnt}
     gpu_launches = 2 * ks["step_launches"]           # k_step + k_fixup per pass (rank 0)
 
     # ---- end-to-end: host inputs -> host result through the C ABI, every step

@@ -19,7 +19,9 @@ enum {
   PE_CORE_FP64 = 3,    /* Alg. 2, p < 2^50, a,b < p                        */
   PE_CORE_FP64ADD = 4, /* Alg. 3, p < 2^50, a,b < p                        */
   PE_CORE_POW = 5,     /* a * b^e mod p via Montgomery square-and-multiply: e = extra[i]      */
-  PE_CORE_SHOUP4RAW = 6 /* raw lazy output of SHOUP4 (must be < 4p and == a*b mod p)          */
+  PE_CORE_SHOUP4RAW = 6, /* raw lazy output of SHOUP4 (must be < 4p and == a*b mod p)         */
+  PE_CORE_HYB = 7,       /* hybrid FP64-quotient product, p < 2^63; probe canonicalises        */
+  PE_CORE_HYBRAW = 8     /* raw output of HYB (must be in (0, 2p) and == a*b mod p)            */
 };
 
 /*

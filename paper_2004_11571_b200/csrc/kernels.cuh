@@ -15,7 +15,11 @@ namespace pe {
 constexpr int kMaxWarps = 16;
 constexpr int kSuper = 32;   // points per shared-memory super-group (one lane per point)
 
-enum PathKind { kInt4 = 0, kInt2 = 1, kFp64 = 2 };
+enum PathKind { kInt4 = 0, kInt2 = 1, kFp64 = 2, kHyb = 3 };
+// Max threads per CTA of k_step<PATH, R> (register budget: 65536 / threads per thread).
+__host__ __device__ constexpr int step_max_threads(int path, int R) {
+  return (R >= 16 || (path == kHyb && R >= 8)) ? 256 : 512;
+}
 
 // ---------------------------------------------------------------- 96-bit accumulators
 struct U96 { u32 w0, w1, w2; };
@@ -138,6 +142,7 @@ static __global__ void k_setup(const u32* __restrict__ exps, const u64* __restri
                         const u64* __restrict__ bstart, u32 G, u64 t_pad,
                         const u64* __restrict__ table, u32 D, const u64* __restrict__ alpha,
                         u64* __restrict__ c_out, u64* __restrict__ m_out, u64* __restrict__ w_out,
+                        u64* __restrict__ ms_out, double* __restrict__ mp_out, double* __restrict__ msp_out,
                         u32* __restrict__ perm_out, ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
     // bucket g: poff[g] <= q < poff[g+1]
@@ -171,6 +176,11 @@ static __global__ void k_setup(const u32* __restrict__ exps, const u64* __restri
     c_out[q] = c;
     m_out[q] = m;
     w_out[q] = shoup_w(m, mp.p);
+    // mul_hyb constants: ms = m 2^32 mod p, mp = m/p, msp = ms/p (relative error <= 3u each)
+    const u64 ms = mulmod(m, (u64)(((unsigned __int128)1 << 32) % mp.p), mp);
+    ms_out[q] = ms;
+    mp_out[q] = __ddiv_rn(__ull2double_rn(m), __ull2double_rn(mp.p));
+    msp_out[q] = __ddiv_rn(__ull2double_rn(ms), __ull2double_rn(mp.p));
     perm_out[q] = src;
   }
 }
@@ -187,7 +197,10 @@ static __global__ void k_scatter_m(const u64* __restrict__ m_pad, const u32* __r
 struct StepArgs {
   const u64* c;          // [t_pad] reduced coefficients (tile layout)
   const u64* m;          // [t_pad] m_i
-  const u64* w;          // [t_pad] floor(m_i 2^64 / p)
+  const u64* w;          // [t_pad] floor(m_i 2^64 / p)           (Shoup paths)
+  const u64* ms;         // [t_pad] m_i 2^32 mod p                 (hybrid path)
+  const double* mpd;     // [t_pad] RN(m_i / p)                    (hybrid path)
+  const double* mspd;    // [t_pad] RN(ms_i / p)                   (hybrid path)
   const uint2* wt_info;  // [n_wt] x = partial slot, y = run length if run leader else 0
   u64* partial;          // [n_slots][ldp]
   u64 ldp;               // leading dimension of partial (points of this pass)
@@ -210,7 +223,7 @@ struct StepArgs {
 // 32 points the totals of the warps of one bucket inside the CTA are summed in shared
 // memory, reduced mod p and written as one partial per (CTA run, point).
 template <int PATH, int R>
-__global__ void __launch_bounds__(R >= 16 ? 256 : 512)
+__global__ void __launch_bounds__(step_max_threads(PATH, R))
 k_step(StepArgs args) {
   __shared__ U96 sacc[2][kMaxWarps][kSuper];
   const int lane = threadIdx.x & 31;
@@ -226,7 +239,7 @@ k_step(StepArgs args) {
   // ---- load the lane's R terms and seed a_r = c_r * m_r^{js} (each
   //      independent chain seeded by exponentiation)
   u64 a[R], m[R], w[R];
-  double ad[R], md[R];
+  double ad[R], md[R];   // FP64 path: a, m;  hybrid path: mp, msp
   uint2 info = make_uint2(0, 0);
   if (active) {
     info = args.wt_info[wt];
@@ -236,9 +249,10 @@ k_step(StepArgs args) {
       const u64 q = base + (u64)r * 32;
       const u64 c = __ldg(args.c + q);
       m[r] = __ldg(args.m + q);
-      w[r] = __ldg(args.w + q);
       a[r] = seed_pow(c, m[r], js, mp);
       if (PATH == kFp64) { ad[r] = (double)a[r]; md[r] = (double)m[r]; }
+      if (PATH == kHyb) { w[r] = __ldg(args.ms + q); md[r] = __ldg(args.mpd + q); ad[r] = __ldg(args.mspd + q); }
+      if (PATH == kInt4 || PATH == kInt2) w[r] = __ldg(args.w + q);
     }
   }
 
@@ -269,8 +283,9 @@ k_step(StepArgs args) {
             for (int r = 2; r < R; ++r) add96_64(acc[k], a[r]);
 #pragma unroll
             for (int r = 0; r < R; ++r)
-              a[r] = PATH == kInt4 ? mul_shoup4(a[r], m[r], w[r], mp.np)
-                                   : mul_shoup2(a[r], m[r], w[r], mp.np);
+              a[r] = PATH == kHyb ? mul_hyb(a[r], m[r], w[r], md[r], ad[r], mp.np, mp.hc)
+                     : PATH == kInt4 ? mul_shoup4(a[r], m[r], w[r], mp.np)
+                                     : mul_shoup2(a[r], m[r], w[r], mp.np);
           }
         }
         const U96 tot = PATH == kFp64 ? xpose_reduce8<2>(acc, lane) : xpose_reduce8<3>(acc, lane);

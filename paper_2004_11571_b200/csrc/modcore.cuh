@@ -36,6 +36,7 @@ struct ModParams {
   u64 r2;     // 2^128 mod p
   double pd;  // (double)p  (exact when p < 2^53)
   double u;   // RN(1/p)     (Alg. 2 "u stores 1/(double) p")
+  u64 hc;     // mul_hyb constant C = K*p mod 2^64
 };
 
 // ---------------------------------------------------------------- 32-bit building blocks
@@ -92,6 +93,57 @@ __device__ __forceinline__ u64 mul_shoup4_c(u64 a, u64 m, u64 w, u64 np) {
   u64 q = mul_wide(a1, w1) + (u64)mul_hi(a1, w0) + (u64)mul_hi(a0, w1);
   return a * m + q * np;
 }
+
+// ---------------------------------------------------------------- hybrid FP64-quotient product
+// "mul_hyb": the IMAD pipe (fmaheavy) is the bottleneck of the Shoup step while the FP64 pipe
+// is idle, so the quotient is estimated in FP64 (the paper's FP-FMA idea, PAPER.md:679-699,
+// applied to the quotient only).  With a = a1*2^32 + a0 and the per-term constants
+//     ms = m * 2^32 mod p,  mp = RN(m/p),  msp = RN(ms/p)    (m fixed per term)
+// X = a1*ms + a0*m == a*m (mod p) has X/p < 2^33, and e = a1*msp + a0*mp is within
+// delta <= 9*2^-21 of X/p (a1, a0 < 2^32 exact in FP64; |msp - ms/p|, |mp - m/p| <= 3u;
+// DMUL/DFMA rounding <= 2^-21 + 2^-20).  With q = round(e) - 1:
+//     X/p - q in [0.5 - delta, 1.5 + delta]   =>   r = X - q*p in (0, 2p)   for any a < 2^64.
+// round(e) is read from the bits of t = e + 1.5*2^52 (exact, |e| < 2^51); with
+// T = bits(t) and K = bits(1.5*2^52) + 1, q = T - K, so
+//     r = a1*ms + a0*m + T*np + C  (mod 2^64),   np = 2^64 - p,  C = K*p mod 2^64.
+// Integer pipe: 3 IMAD.WIDE + 4 IMAD; FP64 pipe: 2 exact u32->f64 (magic DADD), DMUL, DFMA,
+// DADD.  Valid for every odd p < 2^63 (r < 2p < 2^64).
+__device__ __forceinline__ u64 mul_hyb(u64 a, u64 m, u64 ms, double mp, double msp, u64 np, u64 C) {
+  u64 r;
+  asm("{\n\t"
+      ".reg .u32 a0, a1, m0, m1, s0, s1, n0, n1, t0, t1, r0, r1, hb;\n\t"
+      ".reg .f64 d0, d1, e, t;\n\t"
+      ".reg .u64 rr;\n\t"
+      "mov.u32 hb, 0x43300000;\n\t"
+      "mov.b64 {a0, a1}, %1;\n\t"
+      "mov.b64 {m0, m1}, %2;\n\t"
+      "mov.b64 {s0, s1}, %3;\n\t"
+      "mov.b64 {n0, n1}, %6;\n\t"
+      // exact u32 -> f64: bits {x, 0x43300000} = 2^52 + x
+      "mov.b64 d1, {a1, hb};\n\t"
+      "mov.b64 d0, {a0, hb};\n\t"
+      "sub.rn.f64 d1, d1, 0d4330000000000000;\n\t"
+      "sub.rn.f64 d0, d0, 0d4330000000000000;\n\t"
+      "mul.rn.f64 e, d1, %5;\n\t"
+      "fma.rn.f64 e, d0, %4, e;\n\t"
+      "add.rn.f64 t, e, 0d4338000000000000;\n\t"
+      "mov.b64 {t0, t1}, t;\n\t"
+      "mad.wide.u32 rr, a1, s0, %7;\n\t"
+      "mad.wide.u32 rr, a0, m0, rr;\n\t"
+      "mad.wide.u32 rr, t0, n0, rr;\n\t"
+      "mov.b64 {r0, r1}, rr;\n\t"
+      "mad.lo.u32 r1, a1, s1, r1;\n\t"
+      "mad.lo.u32 r1, a0, m1, r1;\n\t"
+      "mad.lo.u32 r1, t0, n1, r1;\n\t"
+      "mad.lo.u32 r1, t1, n0, r1;\n\t"
+      "mov.b64 %0, {r0, r1};\n\t"
+      "}"
+      : "=l"(r)
+      : "l"(a), "l"(m), "l"(ms), "d"(mp), "d"(msp), "l"(np), "l"(C));
+  return r;
+}
+// Host/device constant C for mul_hyb.
+__host__ __device__ __forceinline__ u64 hyb_C(u64 p) { return 0x4338000000000001ull * p; }
 
 // Lazy-2: p < 2^63, exact Shoup quotient, any a < 2^64 -> r in [0, 2p).
 __device__ __forceinline__ u64 mul_shoup2(u64 a, u64 m, u64 w, u64 np) {

@@ -85,6 +85,7 @@ static ModParams h_mod_params(u64 p) {
   mp.r2 = h_mulmod(mp.r1, mp.r1, p);
   mp.pd = (double)p;
   mp.u = 1.0 / (double)p;  // RN(1/p) (host IEEE division, default rounding)
+  mp.hc = hyb_C(p);
   return mp;
 }
 
@@ -101,7 +102,8 @@ struct pe_ctx {
   u32 n_wt = 0, n_slots = 0;
   std::vector<u32> dxdy;  // host copy [2G]
   // device
-  u64 *d_c = nullptr, *d_m = nullptr, *d_w = nullptr;
+  u64 *d_c = nullptr, *d_m = nullptr, *d_w = nullptr, *d_ms = nullptr;
+  double *d_mpd = nullptr, *d_mspd = nullptr;
   u32* d_perm = nullptr;
   uint2* d_wt_info = nullptr;
   u32* d_slot_start = nullptr;
@@ -125,6 +127,7 @@ static void free_all(pe_ctx* h) {
   if (!h) return;
   drop_recs(h);
   cudaFree(h->d_c); cudaFree(h->d_m); cudaFree(h->d_w); cudaFree(h->d_perm);
+  cudaFree(h->d_ms); cudaFree(h->d_mpd); cudaFree(h->d_mspd);
   cudaFree(h->d_wt_info); cudaFree(h->d_slot_start); cudaFree(h->d_partial);
   cudaFree(h->d_out_scratch);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -160,6 +163,7 @@ static cudaError_t launch_step_path(int R, dim3 grid, dim3 block, cudaStream_t s
   return cudaGetLastError();
 }
 static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStream_t s, const StepArgs& a) {
+  if (path == kHyb) return launch_step_path<kHyb>(R, grid, block, s, a);
   if (path == kInt4) return launch_step_path<kInt4>(R, grid, block, s, a);
   if (path == kInt2) return launch_step_path<kInt2>(R, grid, block, s, a);
   return launch_step_path<kFp64>(R, grid, block, s, a);
@@ -254,6 +258,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   }
   if (R != 1 && R != 2 && R != 4 && R != 8 && R != 16) return set_err(PE_EINVAL);
   if (R > maxR) return set_err(PE_ENOTSUP);
+  if (32 * h->W > step_max_threads(h->path, R)) return set_err(PE_EINVAL);
   h->R = R;
   const u64 tile = 32ull * R;
   std::vector<u64> poff(G + 1), bstart(G + 1);
@@ -303,11 +308,12 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   CU(cudaMemcpyAsync(d_poff, poff.data(), (G + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(d_bstart, bstart.data(), (G + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
   if (dalloc(&h->d_c, h->t_pad) || dalloc(&h->d_m, h->t_pad) || dalloc(&h->d_w, h->t_pad) ||
+      dalloc(&h->d_ms, h->t_pad) || dalloc(&h->d_mpd, h->t_pad) || dalloc(&h->d_mspd, h->t_pad) ||
       dalloc(&h->d_perm, h->t_pad) || dalloc(&h->d_wt_info, n_wt) || dalloc(&h->d_slot_start, G + 1))
     return g_last_error;
   k_setup<<<grid_for(h->t_pad, 256), 256, 0, s>>>(d_exps, d_coeffs, n, d_idx2, d_poff, d_bstart, (u32)G,
                                                    h->t_pad, d_table, D, d_alpha, h->d_c, h->d_m, h->d_w,
-                                                   h->d_perm, h->mp);
+                                                   h->d_ms, h->d_mpd, h->d_mspd, h->d_perm, h->mp);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(h->d_wt_info, wt_info.data(), n_wt * sizeof(uint2), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(h->d_slot_start, slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
@@ -336,10 +342,13 @@ extern "C" pe_ctx* pe_create_ex(uint64_t p, uint64_t t, uint32_t n, const uint64
   if (path_req == PE_PATH_FP64) {
     if (p >= (1ull << 50)) { set_err(PE_ENOTSUP); return nullptr; }
     path = kFp64;
-  } else if (path_req == PE_PATH_INT) {
-    path = p < (1ull << 62) ? kInt4 : kInt2;
-  } else if (path_req == PE_PATH_AUTO) {
-    path = p < (1ull << 50) ? kFp64 : (p < (1ull << 62) ? kInt4 : kInt2);
+  } else if (path_req == PE_PATH_INT || path_req == PE_PATH_AUTO) {
+    // INT64 family: the 32-bit-IMAD Shoup core by default (lazy-4 for p < 2^62, lazy-2
+    // above); PE_CORE=hyb selects the hybrid FP64-quotient core.
+    const char* core = getenv("PE_CORE");
+    const bool hyb = core && !strcmp(core, "hyb");
+    path = hyb ? kHyb : (p < (1ull << 62) ? kInt4 : kInt2);
+    if (path_req == PE_PATH_AUTO && p < (1ull << 50) && !core) path = kFp64;
   } else {
     set_err(PE_EINVAL);
     return nullptr;
@@ -347,7 +356,7 @@ extern "C" pe_ctx* pe_create_ex(uint64_t p, uint64_t t, uint32_t n, const uint64
   int R = cfg && cfg->R ? cfg->R : env_int("PE_R", 0);
   int W = cfg && cfg->warps ? cfg->warps : env_int("PE_WARPS", 8);
   int chunk = cfg && cfg->chunk ? cfg->chunk : env_int("PE_CHUNK", 0);
-  if (W < 1 || W > kMaxWarps || (R >= 16 && W > 8) || chunk < 0 || chunk % kSuper) {
+  if (W < 1 || W > kMaxWarps || chunk < 0 || chunk % kSuper) {
     set_err(PE_EINVAL);
     return nullptr;
   }
@@ -419,6 +428,7 @@ static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaSt
     }
     StepArgs a;
     a.c = h->d_c; a.m = h->d_m; a.w = h->d_w; a.wt_info = h->d_wt_info;
+    a.ms = h->d_ms; a.mpd = h->d_mpd; a.mspd = h->d_mspd;
     a.partial = h->d_partial; a.ldp = np; a.js0 = j0 + k0; a.n_wt = h->n_wt; a.npts = np;
     a.chunk = chunk; a.mp = h->mp;
     dim3 grid(n_cta, (np + chunk - 1) / chunk), block(32 * W);

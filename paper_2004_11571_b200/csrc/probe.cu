@@ -23,6 +23,7 @@ static ModParams probe_params(u64 p) {
   mp.r2 = (u64)(((u128)mp.r1 * mp.r1) % p);
   mp.pd = (double)p;
   mp.u = 1.0 / (double)p;
+  mp.hc = hyb_C(p);
   return mp;
 }
 
@@ -55,6 +56,15 @@ __global__ void k_probe(int variant, u64 N, const u64* a, const u64* b, const u6
         break;
       }
       case PE_CORE_POW: r = seed_pow(ai, bi, x[i], mp); break;
+      case PE_CORE_HYB:
+      case PE_CORE_HYBRAW: {
+        const u64 ms = mulmod(bi, (u64)(((unsigned __int128)1 << 32) % mp.p), mp);
+        const double mpd = __ddiv_rn(__ull2double_rn(bi), __ull2double_rn(mp.p));
+        const double mspd = __ddiv_rn(__ull2double_rn(ms), __ull2double_rn(mp.p));
+        r = mul_hyb(ai, bi, ms, mpd, mspd, mp.np, mp.hc);
+        if (variant == PE_CORE_HYB) r %= mp.p;
+        break;
+      }
     }
     out[i] = r;
   }
@@ -65,7 +75,7 @@ extern "C" int pe_test_core(int variant, uint64_t p, uint64_t N, const uint64_t*
   if (p < 3 || p >= (1ull << 63) || (p & 1) == 0) return PE_ERANGE;
   if ((variant == PE_CORE_SHOUP4 || variant == PE_CORE_SHOUP4RAW) && p >= (1ull << 62)) return PE_ENOTSUP;
   if ((variant == PE_CORE_FP64 || variant == PE_CORE_FP64ADD) && p >= (1ull << 50)) return PE_ENOTSUP;
-  if (variant < 0 || variant > 6 || (N && (!a || !b || !out)) || (variant == PE_CORE_POW && N && !extra))
+  if (variant < 0 || variant > 8 || (N && (!a || !b || !out)) || (variant == PE_CORE_POW && N && !extra))
     return PE_EINVAL;
   if (N == 0) return PE_OK;
   u64 *da, *db, *dx = nullptr, *dout;
@@ -111,7 +121,30 @@ __global__ void k_bench(int iters, u64* sink, long long* cyc, ModParams mp) {
 #pragma unroll
     for (int r = 0; r < R; ++r) x ^= __double2ull_rn(a[r]);
     sink[tid] = x;
-  } else if (V == PE_CORE_SHOUP4 || V == PE_CORE_SHOUP2) {
+  } else if (V == PE_CORE_HYB || V == 20) {
+    u64 a[R], m[R], ms[R];
+    double mpd[R], mspd[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      a[r] = (tid * 7919 + r * 104729 + 1) % mp.p;
+      m[r] = (tid * 31337 + r * 7 + 3) % mp.p;
+      ms[r] = mulmod(m[r], (u64)(((unsigned __int128)1 << 32) % mp.p), mp);
+      mpd[r] = __ddiv_rn(__ull2double_rn(m[r]), __ull2double_rn(mp.p));
+      mspd[r] = __ddiv_rn(__ull2double_rn(ms[r]), __ull2double_rn(mp.p));
+    }
+    U96 acc{0, 0, 0};
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (V < 20) add96_64(acc, a[r]);
+        a[r] = mul_hyb(a[r], m[r], ms[r], mpd[r], mspd[r], mp.np, mp.hc);
+      }
+    }
+    u64 x = acc.w0 ^ ((u64)acc.w1 << 32) ^ acc.w2;
+#pragma unroll
+    for (int r = 0; r < R; ++r) x ^= a[r];
+    sink[tid] = x;
+  } else if (V == PE_CORE_SHOUP4 || V == PE_CORE_SHOUP2 || V == 21) {
     u64 a[R], m[R], w[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -123,8 +156,8 @@ __global__ void k_bench(int iters, u64* sink, long long* cyc, ModParams mp) {
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        add96_64(acc, a[r]);
-        a[r] = V == PE_CORE_SHOUP4 ? mul_shoup4(a[r], m[r], w[r], mp.np) : mul_shoup2(a[r], m[r], w[r], mp.np);
+        if (V < 20) add96_64(acc, a[r]);
+        a[r] = (V == PE_CORE_SHOUP4 || V == 21) ? mul_shoup4(a[r], m[r], w[r], mp.np) : mul_shoup2(a[r], m[r], w[r], mp.np);
       }
     }
     u64 x = acc.w0 ^ ((u64)acc.w1 << 32) ^ acc.w2;
@@ -188,6 +221,9 @@ extern "C" int pe_bench_core(int variant, uint64_t p, int R, int blocks, int thr
       case PE_CORE_SHOUP4: launch_bench_v<PE_CORE_SHOUP4>(R, blocks, threads, iters, sink, cyc, mp); break;
       case PE_CORE_SHOUP2: launch_bench_v<PE_CORE_SHOUP2>(R, blocks, threads, iters, sink, cyc, mp); break;
       case PE_CORE_FP64: launch_bench_v<PE_CORE_FP64>(R, blocks, threads, iters, sink, cyc, mp); break;
+      case PE_CORE_HYB: launch_bench_v<PE_CORE_HYB>(R, blocks, threads, iters, sink, cyc, mp); break;
+      case 20: launch_bench_v<20>(R, blocks, threads, iters, sink, cyc, mp); break;
+      case 21: launch_bench_v<21>(R, blocks, threads, iters, sink, cyc, mp); break;
       case 10: launch_bench_v<10>(R, blocks, threads, iters, sink, cyc, mp); break;
       case 11: launch_bench_v<11>(R, blocks, threads, iters, sink, cyc, mp); break;
       case 12: launch_bench_v<12>(R, blocks, threads, iters, sink, cyc, mp); break;

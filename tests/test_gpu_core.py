@@ -26,7 +26,7 @@ def _expect(a, b, p):
     return np.array([(x * y) % p for x, y in zip(a.tolist(), b.tolist())], dtype=np.uint64)
 
 
-@pytest.mark.parametrize("variant", [pe.CORE_SHOUP4, pe.CORE_SHOUP2, pe.CORE_MONT, pe.CORE_FP64])
+@pytest.mark.parametrize("variant", [pe.CORE_SHOUP4, pe.CORE_SHOUP2, pe.CORE_MONT, pe.CORE_FP64, pe.CORE_HYB])
 def test_exhaustive_small_primes(variant):
     for p in SMALL_PRIMES:
         a, b = np.meshgrid(np.arange(p, dtype=np.uint64), np.arange(p, dtype=np.uint64))
@@ -50,7 +50,7 @@ def test_random_operands_all_primes():
         a = rng.integers(0, p, N, dtype=np.uint64)
         b = rng.integers(0, p, N, dtype=np.uint64)
         want = _expect(a, b, p)
-        for v in (pe.CORE_SHOUP4, pe.CORE_SHOUP2, pe.CORE_MONT, pe.CORE_FP64):
+        for v in (pe.CORE_SHOUP4, pe.CORE_SHOUP2, pe.CORE_MONT, pe.CORE_FP64, pe.CORE_HYB):
             if (v == pe.CORE_SHOUP4 and p >= 1 << 62) or (v == pe.CORE_FP64 and p >= 1 << 50):
                 continue
             assert np.array_equal(pe.test_core(v, p, a, b), want), (v, p)
@@ -77,13 +77,30 @@ def test_lazy_inputs_and_raw_range():
         assert np.array_equal(s2, _expect(a, b, p)), p
 
 
+def test_hybrid_lazy_range_all_primes():
+    """mul_hyb (FP64 quotient + integer remainder) returns r in (0, 2p), r == a*b (mod p), for
+    any a < 2^64 and every odd p < 2^63 (DESIGN.md "Hybrid core" error bound)."""
+    rng = np.random.default_rng(17)
+    for p in _rand_primes() + [3, 13, 509, (1 << 63) - 25]:
+        N = 200_000
+        a = rng.integers(0, np.iinfo(np.uint64).max, N, dtype=np.uint64, endpoint=True)
+        b = rng.integers(0, p, N, dtype=np.uint64)
+        edge_a = np.array([0, 1, p - 1, p, 2 * p - 1, 2**64 - 1, 2**63, 2**62, 2**32 - 1, 2**32], dtype=np.uint64)
+        edge_b = np.array([0, 1, p - 1, p - 2, 1, p - 1, p - 1, p - 1, p - 1, (p - 1) // 2], dtype=np.uint64)
+        a = np.concatenate([a, edge_a])
+        b = np.concatenate([b, edge_b])
+        raw = pe.test_core(pe.CORE_HYBRAW, p, a, b)
+        assert np.all(raw > 0) and np.all(raw < np.uint64(2 * p)), p
+        assert np.array_equal(raw % np.uint64(p), _expect(a, b, p)), p
+
+
 def test_edge_operands_62bit():
     for p in ((1 << 62) - 57, (1 << 63) - 25, (1 << 50) - 27):
         vals = [0, 1, 2, p - 1, p - 2, (p - 1) // 2, 1 << 31, (1 << 32) - 1, 1 << 32]
         a, b = np.meshgrid(np.array(vals, np.uint64), np.array(vals, np.uint64))
         a, b = a.ravel(), b.ravel()
         want = _expect(a, b, p)
-        for v in (pe.CORE_SHOUP2, pe.CORE_MONT) + ((pe.CORE_SHOUP4,) if p < 1 << 62 else ()) + \
+        for v in (pe.CORE_SHOUP2, pe.CORE_MONT, pe.CORE_HYB) + ((pe.CORE_SHOUP4,) if p < 1 << 62 else ()) + \
                 ((pe.CORE_FP64,) if p < 1 << 50 else ()):
             assert np.array_equal(pe.test_core(v, p, a, b), want), (v, p)
         assert pe.test_core(pe.CORE_MONT, p, np.array([p - 1], np.uint64), np.array([p - 1], np.uint64))[0] == 1

@@ -190,3 +190,18 @@ def test_error_codes_gpu():
         with pytest.raises(pe.PEError) as ei:
             ctx.eval(2**64 - 10, 20)
         assert ei.value.code == pe.PE_ERANGE
+
+
+def test_hybrid_core_parity(monkeypatch):
+    """PE_CORE=hyb (FP64 quotient + integer remainder, modcore.cuh mul_hyb) is bit-identical."""
+    monkeypatch.setenv("PE_CORE", "hyb")
+    for w in (synth.gen_config(2, t=30_000, T=97), synth.random_small(207, (1 << 63) - 25, 6, 500, 3, 45, 3),
+              synth.gen_config(4, t=20_000, T=70)):
+        for R in (2, 8):
+            check_full(w, R=R)
+
+
+def test_shoup_core_parity_50bit(monkeypatch):
+    """PE_CORE=shoup on a 50-bit prime (config 4 shape) equals the FP64 Alg. 2 default."""
+    monkeypatch.setenv("PE_CORE", "shoup")
+    check_full(synth.gen_config(4, t=20_000, T=70))
