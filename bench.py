@@ -248,9 +248,10 @@ def main():
 
     # ---- roofline of k_step (dominant kernel)
     pk, pk_kind = peaks()
-    step_ms = ks["step_ms"] / max(ks["step_launches"], 1)
-    launches_tp = ks["term_points"] / max(ks["step_launches"], 1)        # padded term-points / launch
-    algo_tp = w.t * sh.cnt if sh.cnt else 0                                 # algorithmic term-points / launch
+    n_launch = max(ks["step_launches"], 1)                                 # passes x steps (rank 0)
+    step_ms = ks["step_ms"] / n_launch                                     # mean k_step launch time
+    launches_tp = ks["term_points"] / n_launch                             # padded term-points / launch
+    algo_tp = w.t * sh.cnt * args.steps / n_launch if sh.cnt else 0        # algorithmic term-points / launch
     achieved = algo_tp / (step_ms * 1e-3) if step_ms else 0.0
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
     peak = N_SM * sm_mhz * 1e6 * IMAD_LANES_PER_CLK_SM / IMAD_SLOTS_PER_TP
@@ -258,7 +259,7 @@ def main():
     k5 = None
     try:
         k5_ms, k5_steps, _ = pe.bench_core(pe.CORE_SHOUP4 if info["path"] == "int" else pe.CORE_FP64,
-                                           w.p, 8, N_SM * 4, 256, 256)
+                                           w.p, 8, N_SM * 2, 256, 4096)
         k5 = k5_steps / (k5_ms * 1e-3)
     except pe.PEError:
         pass

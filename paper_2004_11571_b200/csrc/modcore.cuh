@@ -59,23 +59,23 @@ __device__ __forceinline__ void mul128(u64 a, u64 b, u64& hi, u64& lo) {
 __device__ __forceinline__ u64 mul_shoup4(u64 a, u64 m, u64 w, u64 np) {
   u64 r;
   asm("{\n\t"
-      ".reg .u32 a0, a1, m0, m1, w0, w1, n0, n1, t1, t2, q0, q1, r0, r1;\n\t"
-      ".reg .u64 q, rr;\n\t"
+      ".reg .u32 a0, a1, m0, m1, w0, w1, n0, n1, t1, t2, s, c, q0, q1, r0, r1;\n\t"
+      ".reg .u64 rr;\n\t"
       "mov.b64 {a0, a1}, %1;\n\t"
       "mov.b64 {m0, m1}, %2;\n\t"
       "mov.b64 {w0, w1}, %3;\n\t"
       "mov.b64 {n0, n1}, %4;\n\t"
       "mul.hi.u32 t1, a1, w0;\n\t"
       "mul.hi.u32 t2, a0, w1;\n\t"
-      "mul.wide.u32 q, a1, w1;\n\t"
-      "mov.b64 {q0, q1}, q;\n\t"
-      "add.cc.u32 q0, q0, t1;\n\t"
-      "addc.u32 q1, q1, 0;\n\t"
-      "add.cc.u32 q0, q0, t2;\n\t"
-      "addc.u32 q1, q1, 0;\n\t"
+      "add.cc.u32 s, t1, t2;\n\t"
+      "addc.u32 c, 0, 0;\n\t"
+      // q = a1*w1 + s + c*2^32 with carry chains (no 64-bit addend pairs -> no predicate spills)
+      "mad.lo.cc.u32 q0, a1, w1, s;\n\t"
+      "madc.hi.u32 q1, a1, w1, c;\n\t"
       "mul.wide.u32 rr, a0, m0;\n\t"
-      "mad.wide.u32 rr, q0, n0, rr;\n\t"
       "mov.b64 {r0, r1}, rr;\n\t"
+      "mad.lo.cc.u32 r0, q0, n0, r0;\n\t"
+      "madc.hi.u32 r1, q0, n0, r1;\n\t"
       "mad.lo.u32 r1, a0, m1, r1;\n\t"
       "mad.lo.u32 r1, a1, m0, r1;\n\t"
       "mad.lo.u32 r1, q0, n1, r1;\n\t"
@@ -226,8 +226,10 @@ __device__ __forceinline__ double mul_fp(double x, double y, double p, double u)
   double c = floor(b);                   // line 4: c <- floor(b)  (quotient +-1)
   double d = __fma_rn(-c, p, h);         // line 5: d <- fma(-c, p, h)
   double g = __dadd_rn(d, l);            // line 6: g <- d + l      (remainder +-p)
-  if (g >= p) return __dsub_rn(g, p);    // line 7
-  if (g < 0.0) return __dadd_rn(g, p);   // line 8
+  // lines 7-9 as selects (no divergent branches): g >= p -> g - p; g < 0 -> g + p; else g
+  const double gm = __dsub_rn(g, p), gp = __dadd_rn(g, p);
+  g = (g >= p) ? gm : g;                 // line 7
+  g = (g < 0.0) ? gp : g;                // line 8 (exclusive with line 7 for g in (-p, 2p))
   return g;                              // line 9
 }
 // Alg. 3

@@ -152,12 +152,26 @@ __global__ void k_bench(int iters, u64* sink, long long* cyc, ModParams mp) {
       m[r] = (tid * 31337 + r * 7 + 3) % mp.p;
       w[r] = shoup_w(m[r], mp.p);
     }
+    // same accumulation structure as k_step: 8 points per group, per point one 96-bit sum of
+    // the R chains (set96_sum + add96_64), `iters` counts points
     U96 acc{0, 0, 0};
-    for (int it = 0; it < iters; ++it) {
+    for (int it = 0; it < iters; it += 8) {
+      U96 pa[8];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (V < 20) add96_64(acc, a[r]);
-        a[r] = (V == PE_CORE_SHOUP4 || V == 21) ? mul_shoup4(a[r], m[r], w[r], mp.np) : mul_shoup2(a[r], m[r], w[r], mp.np);
+      for (int k = 0; k < 8; ++k) {
+        if (V < 20) {
+          if (R == 1) { pa[k].w0 = lo32(a[0]); pa[k].w1 = hi32(a[0]); pa[k].w2 = 0; }
+          else set96_sum(pa[k], a[0], a[1]);
+#pragma unroll
+          for (int r = 2; r < R; ++r) add96_64(pa[k], a[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          a[r] = (V == PE_CORE_SHOUP4 || V == 21) ? mul_shoup4(a[r], m[r], w[r], mp.np) : mul_shoup2(a[r], m[r], w[r], mp.np);
+      }
+      if (V < 20) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) { acc.w0 ^= pa[k].w0; acc.w1 += pa[k].w1; acc.w2 ^= pa[k].w2; }
       }
     }
     u64 x = acc.w0 ^ ((u64)acc.w1 << 32) ^ acc.w2;
