@@ -7,10 +7,9 @@
 //     term across all points (a <- a o m), so w_i = floor(m_i 2^64 / p)
 //     is precomputed once and every step costs one approximate 64x64-high product plus two
 //     64x64-low products.
-//       - mul_shoup4: p < 2^62, quotient from 3 of the 4 partial products (drops the a0*w0
-//         term and the carries of the two cross terms => q in [q_shoup-2, q_shoup]), result
-//         lazily in [0, 4p) for ANY input a < 2^64.  4p < 2^64 so the remainder computed
-//         mod 2^64 is exact.
+//       - mul_shoup4: p < 2^62, quotient from 3 of the 4 partial products (drops only the
+//         a0*w0 term => q in [q_shoup-1, q_shoup]), result lazily in [0, 3p) subset [0, 4p)
+//         for ANY input a < 2^64.  4p < 2^64 so the remainder computed mod 2^64 is exact.
 //       - mul_shoup2: p < 2^63, exact Shoup quotient, one conditional subtract, output in
 //         [0, 2p) for input a < 2^64.
 //   * Montgomery REDC for general products (seeding by exponentiation,
@@ -51,23 +50,28 @@ __device__ __forceinline__ void mul128(u64 a, u64 b, u64& hi, u64& lo) {
 
 // ---------------------------------------------------------------- Shoup products
 // w = floor(m * 2^64 / p), m < p.
-// Lazy-4: p < 2^62, any a < 2^64 -> r == a*m (mod p), r in [0, 4p).
-//   q ~ floor(a*w / 2^64) from a1*w1 + hi(a1*w0) + hi(a0*w1) (deficit <= 2 vs Shoup's q)
+// Lazy-4: p < 2^62, any a < 2^64 -> r == a*m (mod p), r in [0, 3p) (contract: [0, 4p)).
+//   q = a1*w1 + floor((a1*w0 + a0*w1) / 2^32) (deficit <= 1 vs Shoup's q = floor(a*w/2^64))
 //   r = a*m - q*p = a*m + q*(2^64 - p)  (mod 2^64)
-// Written in PTX so that exactly 9 IMAD-pipe ops (3 IMAD.WIDE, 2 IMAD.HI, 4 IMAD) and 2 ALU
-// adds are issued (no zero-extension moves).
+// PTX chosen by SASS slot count (scripts/core_variants.cu, scripts/sass_slots.py): 5 full-width
+// products (IMAD.WIDE, 2 IMAD-pipe slots each) + 4 low IMADs = the 14-slot minimum, with the
+// cross-term sum and the carries on the ALU pipe and no zero-register pairs.
 __device__ __forceinline__ u64 mul_shoup4(u64 a, u64 m, u64 w, u64 np) {
   u64 r;
   asm("{\n\t"
-      ".reg .u32 a0, a1, m0, m1, w0, w1, n0, n1, t1, t2, s, c, q0, q1, r0, r1;\n\t"
-      ".reg .u64 rr;\n\t"
+      ".reg .u32 a0, a1, m0, m1, w0, w1, n0, n1, x1l, x1h, x2l, x2h, z, s, c, q0, q1, r0, r1;\n\t"
+      ".reg .u64 rr, x1, x2;\n\t"
       "mov.b64 {a0, a1}, %1;\n\t"
       "mov.b64 {m0, m1}, %2;\n\t"
       "mov.b64 {w0, w1}, %3;\n\t"
       "mov.b64 {n0, n1}, %4;\n\t"
-      "mul.hi.u32 t1, a1, w0;\n\t"
-      "mul.hi.u32 t2, a0, w1;\n\t"
-      "add.cc.u32 s, t1, t2;\n\t"
+      // cross terms as full products; s:c = floor((a1*w0 + a0*w1) / 2^32) on the ALU
+      "mul.wide.u32 x1, a1, w0;\n\t"
+      "mul.wide.u32 x2, a0, w1;\n\t"
+      "mov.b64 {x1l, x1h}, x1;\n\t"
+      "mov.b64 {x2l, x2h}, x2;\n\t"
+      "add.cc.u32 z, x1l, x2l;\n\t"
+      "addc.cc.u32 s, x1h, x2h;\n\t"
       "addc.u32 c, 0, 0;\n\t"
       // q = a1*w1 + s + c*2^32 with carry chains (no 64-bit addend pairs -> no predicate spills)
       "mad.lo.cc.u32 q0, a1, w1, s;\n\t"
@@ -90,7 +94,8 @@ __device__ __forceinline__ u64 mul_shoup4(u64 a, u64 m, u64 w, u64 np) {
 // Reference (plain C) form of mul_shoup4, used by the probe to cross-check the PTX.
 __device__ __forceinline__ u64 mul_shoup4_c(u64 a, u64 m, u64 w, u64 np) {
   const u32 a0 = lo32(a), a1 = hi32(a), w0 = lo32(w), w1 = hi32(w);
-  u64 q = mul_wide(a1, w1) + (u64)mul_hi(a1, w0) + (u64)mul_hi(a0, w1);
+  const unsigned __int128 cross = (unsigned __int128)mul_wide(a1, w0) + mul_wide(a0, w1);
+  u64 q = mul_wide(a1, w1) + (u64)(cross >> 32);   // floor((a*w - a0*w0) / 2^64)
   return a * m + q * np;
 }
 

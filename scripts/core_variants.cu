@@ -79,12 +79,42 @@ __device__ __forceinline__ u64 mul_v4(u64 a, u64 m, u64 w, u64 np) {
   return r;
 }
 
+// V5: cross terms as full products (pairs), high halves summed on the ALU (+ low-half carry)
+__device__ __forceinline__ u64 mul_v5(u64 a, u64 m, u64 w, u64 np) {
+  u64 r;
+  asm("{\n\t.reg .u32 a0, a1, m0, m1, w0, w1, n0, n1, x1l, x1h, x2l, x2h, s, c, z, q0, q1, r0, r1;\n\t.reg .u64 x1, x2, rr;\n\t"
+      "mov.b64 {a0, a1}, %1;\n\tmov.b64 {m0, m1}, %2;\n\tmov.b64 {w0, w1}, %3;\n\tmov.b64 {n0, n1}, %4;\n\t"
+      "mul.wide.u32 x1, a1, w0;\n\tmul.wide.u32 x2, a0, w1;\n\tmov.b64 {x1l, x1h}, x1;\n\tmov.b64 {x2l, x2h}, x2;\n\t"
+      "add.cc.u32 z, x1l, x2l;\n\taddc.cc.u32 s, x1h, x2h;\n\taddc.u32 c, 0, 0;\n\t"
+      "mad.lo.cc.u32 q0, a1, w1, s;\n\tmadc.hi.u32 q1, a1, w1, c;\n\t"
+      "mul.wide.u32 rr, a0, m0;\n\tmov.b64 {r0, r1}, rr;\n\t"
+      "mad.lo.cc.u32 r0, q0, n0, r0;\n\tmadc.hi.u32 r1, q0, n0, r1;\n\t"
+      "mad.lo.u32 r1, a0, m1, r1;\n\tmad.lo.u32 r1, a1, m0, r1;\n\tmad.lo.u32 r1, q0, n1, r1;\n\tmad.lo.u32 r1, q1, n0, r1;\n\t"
+      "mov.b64 %0, {r0, r1};\n\t}" : "=l"(r) : "l"(a), "l"(m), "l"(w), "l"(np));
+  return r;
+}
+// V6: library form (madc q, mul.wide r)
+__device__ __forceinline__ u64 mul_v6(u64 a, u64 m, u64 w, u64 np) {
+  u64 r;
+  asm("{\n\t.reg .u32 a0, a1, m0, m1, w0, w1, n0, n1, t1, t2, s, c, q0, q1, r0, r1;\n\t.reg .u64 rr;\n\t"
+      "mov.b64 {a0, a1}, %1;\n\tmov.b64 {m0, m1}, %2;\n\tmov.b64 {w0, w1}, %3;\n\tmov.b64 {n0, n1}, %4;\n\t"
+      "mul.hi.u32 t1, a1, w0;\n\tmul.hi.u32 t2, a0, w1;\n\tadd.cc.u32 s, t1, t2;\n\taddc.u32 c, 0, 0;\n\t"
+      "mad.lo.cc.u32 q0, a1, w1, s;\n\tmadc.hi.u32 q1, a1, w1, c;\n\t"
+      "mul.wide.u32 rr, a0, m0;\n\tmov.b64 {r0, r1}, rr;\n\t"
+      "mad.lo.cc.u32 r0, q0, n0, r0;\n\tmadc.hi.u32 r1, q0, n0, r1;\n\t"
+      "mad.lo.u32 r1, a0, m1, r1;\n\tmad.lo.u32 r1, a1, m0, r1;\n\tmad.lo.u32 r1, q0, n1, r1;\n\tmad.lo.u32 r1, q1, n0, r1;\n\t"
+      "mov.b64 %0, {r0, r1};\n\t}" : "=l"(r) : "l"(a), "l"(m), "l"(w), "l"(np));
+  return r;
+}
+
 template <int V>
 __device__ __forceinline__ u64 mulv(u64 a, u64 m, u64 w, u64 np) {
   if (V == 0) return mul_v0(a, m, w, np);
   if (V == 1) return mul_v1(a, m, w, np);
   if (V == 2) return mul_v2(a, m, w, np);
   if (V == 3) return mul_v3(a, m, w, np);
+  if (V == 5) return mul_v5(a, m, w, np);
+  if (V == 6) return mul_v6(a, m, w, np);
   return mul_v4(a, m, w, np);
 }
 
@@ -142,6 +172,8 @@ int main() {
     run<2>("v2_plainC", in, out, 2048);
     run<3>("v3_pairaddend", in, out, 2048);
     run<4>("v4_madc_q_wide_r", in, out, 2048);
+    run<5>("v5_wide_cross", in, out, 2048);
+    run<6>("v6_library", in, out, 2048);
   }
   printf("{\"status\": \"%s\"}\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
