@@ -47,11 +47,15 @@ enum {
   PE_ENOTSUP = -6    /* requested path / option not supported for this p               */
 };
 
-enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2 };
+enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_MIX = 3 };
+/* PE_PATH_MIX is reported by pe_info only (env PE_CORE=mix, p < 2^50): half of every lane's
+ * chains run FP64 Alg. 2 (FP64 pipe), half integer Shoup (IMAD pipe).  Correct but not faster
+ * than pure Alg. 2 on B200 (both are issue-bound), so the automatic path for p < 2^50 is FP64. */
 
 /* Tuning knobs (0 = automatic).  They never change the result (pin P13). */
 typedef struct pe_config {
-  int32_t path;  /* PE_PATH_AUTO: FP64 Alg. 2 if p < 2^50 else INT64; env PE_PATH=int|fp64  */
+  int32_t path;  /* PE_PATH_AUTO: FP64 Alg. 2 if p < 2^50 else INT64 Shoup; PE_PATH_FP64 / PE_PATH_INT
+                    force one.  env PE_PATH=int|fp64, PE_CORE=mix|fp64|hyb|shoup     */
   int32_t R;     /* terms per lane: 1,2,4,8,16 (FP64: <= 8); auto picks by bucket sizes    */
   int32_t warps; /* warps per CTA, 1..16 (auto 8)                                          */
   int32_t chunk; /* points per CTA (multiple of 32; auto by grid coverage)                 */

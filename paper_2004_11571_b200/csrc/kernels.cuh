@@ -15,7 +15,9 @@ namespace pe {
 constexpr int kMaxWarps = 16;
 constexpr int kSuper = 32;   // points per shared-memory super-group (one lane per point)
 
-enum PathKind { kInt4 = 0, kInt2 = 1, kFp64 = 2, kHyb = 3 };
+enum PathKind { kInt4 = 0, kInt2 = 1, kFp64 = 2, kHyb = 3, kMix = 4 };
+// kMix (p < 2^50): in every lane, chains r < R/2 run Alg. 2 on the FP64 pipe and chains
+// r >= R/2 run the Shoup-lazy product on the IMAD pipe, so both multiplier pipes work at once.
 // Max threads per CTA of k_step<PATH, R> (register budget: 65536 / threads per thread).
 __host__ __device__ constexpr int step_max_threads(int path, int R) {
   return (R >= 16 || (path == kHyb && R >= 8)) ? 256 : 512;
@@ -250,9 +252,10 @@ k_step(StepArgs args) {
       const u64 c = __ldg(args.c + q);
       m[r] = __ldg(args.m + q);
       a[r] = seed_pow(c, m[r], js, mp);
-      if (PATH == kFp64) { ad[r] = (double)a[r]; md[r] = (double)m[r]; }
+      const bool fp_chain = PATH == kFp64 || (PATH == kMix && r < R / 2);
+      if (fp_chain) { ad[r] = (double)a[r]; md[r] = (double)m[r]; }
       if (PATH == kHyb) { w[r] = __ldg(args.ms + q); md[r] = __ldg(args.mpd + q); ad[r] = __ldg(args.mspd + q); }
-      if (PATH == kInt4 || PATH == kInt2) w[r] = __ldg(args.w + q);
+      if (PATH == kInt4 || PATH == kInt2 || (PATH == kMix && r >= R / 2)) w[r] = __ldg(args.w + q);
     }
   }
 
@@ -273,6 +276,20 @@ k_step(StepArgs args) {
             }
             const u64 si = __double2ull_rn(sum);
             acc[k].w0 = lo32(si); acc[k].w1 = hi32(si); acc[k].w2 = 0;
+          } else if (PATH == kMix) {
+            constexpr int RF = R / 2;
+            double fs = ad[0];
+#pragma unroll
+            for (int r = 1; r < RF; ++r) fs = __dadd_rn(fs, ad[r]);          // exact: RF*p < 2^52
+            // fs < 2^52 is an integer: bits(2^52 + fs) = 0x4330000000000000 | fs
+            const u64 fb = (u64)__double_as_longlong(__dadd_rn(fs, 4503599627370496.0)) & 0x000fffffffffffffull;
+            set96_sum(acc[k], fb, a[RF]);
+#pragma unroll
+            for (int r = RF + 1; r < R; ++r) add96_64(acc[k], a[r]);
+#pragma unroll
+            for (int r = 0; r < RF; ++r) ad[r] = mul_fp(ad[r], md[r], mp.pd, mp.u);
+#pragma unroll
+            for (int r = RF; r < R; ++r) a[r] = mul_shoup4(a[r], m[r], w[r], mp.np);
           } else {
             if (R == 1) {
               acc[k].w0 = lo32(a[0]); acc[k].w1 = hi32(a[0]); acc[k].w2 = 0;

@@ -163,6 +163,15 @@ static cudaError_t launch_step_path(int R, dim3 grid, dim3 block, cudaStream_t s
   return cudaGetLastError();
 }
 static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStream_t s, const StepArgs& a) {
+  if (path == kMix) {
+    switch (R) {
+      case 2: k_step<kMix, 2><<<grid, block, 0, s>>>(a); break;
+      case 4: k_step<kMix, 4><<<grid, block, 0, s>>>(a); break;
+      case 8: k_step<kMix, 8><<<grid, block, 0, s>>>(a); break;
+      default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+  }
   if (path == kHyb) return launch_step_path<kHyb>(R, grid, block, s, a);
   if (path == kInt4) return launch_step_path<kInt4>(R, grid, block, s, a);
   if (path == kInt2) return launch_step_path<kInt2>(R, grid, block, s, a);
@@ -245,7 +254,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   for (u64 g = 0; g < G; ++g) { h->dxdy[2 * g] = (u32)(ukeys[g] >> 32); h->dxdy[2 * g + 1] = (u32)ukeys[g]; }
 
   // ---- host tile plan from the G bucket sizes
-  const int maxR = h->path == kFp64 ? 8 : 16;
+  const int maxR = (h->path == kFp64 || h->path == kMix) ? 8 : 16;
   int R = h->R;
   if (R == 0) {
     // largest R whose per-bucket padding wastes <= 6% of the terms (and R <= 8 by default)
@@ -258,6 +267,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   }
   if (R != 1 && R != 2 && R != 4 && R != 8 && R != 16) return set_err(PE_EINVAL);
   if (R > maxR) return set_err(PE_ENOTSUP);
+  if (h->path == kMix && R == 1) h->path = kFp64;   // a single chain cannot be split
   if (32 * h->W > step_max_threads(h->path, R)) return set_err(PE_EINVAL);
   h->R = R;
   const u64 tile = 32ull * R;
@@ -348,7 +358,15 @@ extern "C" pe_ctx* pe_create_ex(uint64_t p, uint64_t t, uint32_t n, const uint64
     const char* core = getenv("PE_CORE");
     const bool hyb = core && !strcmp(core, "hyb");
     path = hyb ? kHyb : (p < (1ull << 62) ? kInt4 : kInt2);
-    if (path_req == PE_PATH_AUTO && p < (1ull << 50) && !core) path = kFp64;
+    if (path_req == PE_PATH_AUTO && p < (1ull << 50) && (!core || !strcmp(core, "auto"))) path = kFp64;
+    if (core && !strcmp(core, "mix")) {
+      if (p >= (1ull << 50)) { set_err(PE_ENOTSUP); return nullptr; }
+      path = kMix;
+    }
+    if (core && !strcmp(core, "fp64")) {
+      if (p >= (1ull << 50)) { set_err(PE_ENOTSUP); return nullptr; }
+      path = kFp64;
+    }
   } else {
     set_err(PE_EINVAL);
     return nullptr;
@@ -504,7 +522,7 @@ extern "C" int pe_bucket_exps(const pe_ctx* h, uint32_t* dxdy) {
 extern "C" int pe_info(const pe_ctx* h, int32_t* path, int32_t* R, int32_t* warps, uint64_t* t_padded,
                        uint64_t* n_slots) {
   if (!h) return set_err(PE_EINVAL);
-  if (path) *path = h->path == kFp64 ? PE_PATH_FP64 : PE_PATH_INT;
+  if (path) *path = h->path == kFp64 ? PE_PATH_FP64 : (h->path == kMix ? PE_PATH_MIX : PE_PATH_INT);
   if (R) *R = h->R;
   if (warps) *warps = h->W;
   if (t_padded) *t_padded = h->t_pad;

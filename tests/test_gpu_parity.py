@@ -53,7 +53,7 @@ def test_config3_4_full_incremental_and_sampled_direct(cfg):
     assert np.array_equal(out[:, ks.astype(np.int64)], ref)
 
 
-def test_config4_fp64_equals_int():
+def test_config4_fp64_equals_int_equals_mix():
     w = synth.gen_config(4, t=200_000, T=512)
     _, a = gpu_eval(w, path=pe.PATH_FP64)
     _, b = gpu_eval(w, path=pe.PATH_INT)
@@ -205,3 +205,14 @@ def test_shoup_core_parity_50bit(monkeypatch):
     """PE_CORE=shoup on a 50-bit prime (config 4 shape) equals the FP64 Alg. 2 default."""
     monkeypatch.setenv("PE_CORE", "shoup")
     check_full(synth.gen_config(4, t=20_000, T=70))
+
+
+@pytest.mark.parametrize("R", [2, 4, 8])
+def test_mixed_path_parity(R, monkeypatch):
+    """kMix (PE_CORE=mix): half of every lane's chains on the FP64 pipe (Alg. 2), half on IMAD."""
+    monkeypatch.setenv("PE_CORE", "mix")
+    for w in (synth.gen_config(4, t=30_000, T=99), synth.random_small(208, P50, 6, 700, 4, 40, 0),
+              synth.random_small(209, 1_000_003, 5, 300, 3, 33, 2)):
+        with pe.Context.from_workload(w, R=R) as ctx:
+            assert ctx.info()["path"] == "mix"
+        check_full(w, R=R)
