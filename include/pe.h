@@ -81,6 +81,21 @@ pe_ctx* pe_create_ex(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs,
                      const uint32_t* exps, const uint64_t* alpha, const pe_config* cfg);
 
 /*
+ * pe_create_batch -- several polynomials f_0..f_{npoly-1} evaluated at the SAME points beta^j in
+ * one launch (the gcd workload: images of f and h at the same beta^t;
+ * SURVEY.md §8(f) NEXT-1).  Polynomial k owns terms [sum_{q<k} t_per_poly[q], ... + t_per_poly[k])
+ * of coeffs / exps (same layouts as pe_create).  Output rows are ordered by polynomial, then by
+ * descending (dx,dy) within it; pe_poly_rows gives the row range of each polynomial.
+ * npoly >= 1; a polynomial may have zero terms (zero rows).  Errors as pe_create.
+ */
+pe_ctx* pe_create_batch(uint64_t p, uint32_t npoly, const uint64_t* t_per_poly, uint32_t n,
+                        const uint64_t* coeffs, const uint32_t* exps, const uint64_t* alpha,
+                        const pe_config* cfg);
+uint32_t pe_num_polys(const pe_ctx* h);                       /* npoly (1 for pe_create)        */
+int pe_poly_rows(const pe_ctx* h, uint64_t* row_off);         /* HOST uint64[npoly+1]: rows of f_k
+                                                                 are [row_off[k], row_off[k+1]) */
+
+/*
  * pe_eval -- T images into HOST memory out[G*T] (row g, column k <-> j = j0 + k).
  * Synchronous.  T == 0 or G == 0 is a no-op returning PE_OK.
  * Errors: PE_EINVAL (h NULL, out NULL with G*T > 0), PE_ERANGE (j0 + T - 1 >= 2^64),

@@ -26,7 +26,8 @@ CORE_SHOUP4, CORE_SHOUP2, CORE_MONT, CORE_FP64, CORE_FP64ADD, CORE_POW, CORE_SHO
 #: every symbol include/pe.h and include/pe_test.h declare
 EXPORTS = ["pe_create", "pe_create_ex", "pe_eval", "pe_eval_device", "pe_destroy", "pe_num_buckets",
            "pe_bucket_exps", "pe_info", "pe_monomials", "pe_last_error", "pe_strerror",
-           "pe_interp_bound_ok", "pe_test_core", "pe_bench_core", "pe_set_timing", "pe_kernel_stats"]
+           "pe_interp_bound_ok", "pe_test_core", "pe_bench_core", "pe_set_timing", "pe_kernel_stats",
+           "pe_create_batch", "pe_num_polys", "pe_poly_rows"]
 
 
 class PEError(RuntimeError):
@@ -88,6 +89,12 @@ def lib():
         L.pe_kernel_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         L.pe_kernel_stats.restype = ctypes.c_int
+        L.pe_create_batch.argtypes = [u64, u32, vp, u32, vp, vp, vp, ctypes.POINTER(Config)]
+        L.pe_create_batch.restype = vp
+        L.pe_num_polys.argtypes = [vp]
+        L.pe_num_polys.restype = u32
+        L.pe_poly_rows.argtypes = [vp, vp]
+        L.pe_poly_rows.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -118,6 +125,33 @@ class Context:
         if not h:
             raise PEError(L.pe_last_error(), "pe_create")
         self._h = ctypes.c_void_p(h)
+
+    @classmethod
+    def batch(cls, p: int, polys, alpha, n: int, path: int = PATH_AUTO, R: int = 0, warps: int = 0,
+              chunk: int = 0) -> "Context":
+        """pe_create_batch: ``polys`` = [(coeffs, exps), ...] evaluated at the same points."""
+        cs = [np.ascontiguousarray(c, dtype=np.uint64).ravel() for c, _ in polys]
+        es = [np.ascontiguousarray(e, dtype=np.uint32).reshape(-1, n) for _, e in polys]
+        tper = np.array([c.size for c in cs], np.uint64)
+        coeffs = np.concatenate(cs) if cs else np.zeros(0, np.uint64)
+        exps = np.concatenate(es) if es else np.zeros((0, n), np.uint32)
+        alpha = np.ascontiguousarray(alpha, dtype=np.uint64).ravel()
+        self = cls.__new__(cls)
+        self.p, self.n, self.t = int(p), int(n), int(coeffs.size)
+        cfg = Config(path, R, warps, chunk)
+        L = lib()
+        h = L.pe_create_batch(self.p, len(polys), _ptr(tper), self.n, _ptr(coeffs), _ptr(exps), _ptr(alpha),
+                              ctypes.byref(cfg))
+        if not h:
+            raise PEError(L.pe_last_error(), "pe_create_batch")
+        self._h = ctypes.c_void_p(h)
+        return self
+
+    def poly_rows(self) -> np.ndarray:
+        k = int(lib().pe_num_polys(self._h))
+        out = np.zeros(k + 1, np.uint64)
+        _check(lib().pe_poly_rows(self._h, _ptr(out)), "pe_poly_rows")
+        return out
 
     @classmethod
     def from_workload(cls, w, **kw) -> "Context":

@@ -116,6 +116,44 @@ static __global__ void k_keys(const u32* __restrict__ exps, u64 t, u32 n, u64* _
   }
 }
 
+// Batched polynomials: polynomial id of every (key-sorted) term, from
+// the term offsets poly_off[npoly+1]; iota[j] = j for the stable re-sort by polynomial.
+static __global__ void k_poly_of(const u32* __restrict__ idx_sorted, u64 t, const u64* __restrict__ poly_off,
+                                 u32 npoly, u32* __restrict__ pid, u32* __restrict__ iota) {
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < t; j += (u64)gridDim.x * blockDim.x) {
+    const u64 i = idx_sorted[j];
+    u32 lo = 0, hi = npoly;
+    while (hi - lo > 1) {
+      u32 mid = (lo + hi) >> 1;
+      if (poly_off[mid] <= i) lo = mid; else hi = mid;
+    }
+    pid[j] = lo;
+    iota[j] = (u32)j;
+  }
+}
+static __global__ void k_apply_perm(const u32* __restrict__ perm, u64 t, const u64* __restrict__ key_in,
+                                    const u32* __restrict__ idx_in, u64* __restrict__ key_out,
+                                    u32* __restrict__ idx_out) {
+  for (u64 k = blockIdx.x * (u64)blockDim.x + threadIdx.x; k < t; k += (u64)gridDim.x * blockDim.x) {
+    const u32 j = perm[k];
+    key_out[k] = key_in[j];
+    idx_out[k] = idx_in[j];
+  }
+}
+// Run starts of equal (polynomial, dx, dy) in the sorted order (pid may be NULL: one polynomial).
+static __global__ void k_run_flags(const u64* __restrict__ key, const u32* __restrict__ pid, u64 t,
+                                   unsigned char* __restrict__ flags) {
+  for (u64 k = blockIdx.x * (u64)blockDim.x + threadIdx.x; k < t; k += (u64)gridDim.x * blockDim.x)
+    flags[k] = (k == 0 || key[k] != key[k - 1] || (pid && pid[k] != pid[k - 1])) ? 1 : 0;
+}
+static __global__ void k_gather_runs(const u32* __restrict__ starts, u32 G, const u64* __restrict__ key,
+                                     const u32* __restrict__ pid, u64* __restrict__ ukey, u32* __restrict__ upid) {
+  for (u32 g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+    ukey[g] = key[starts[g]];
+    upid[g] = pid ? pid[starts[g]] : 0;
+  }
+}
+
 static __global__ void k_max_exp(const u32* __restrict__ exps, u64 t, u32 n, u32* __restrict__ dmax) {
   u32 mx = 0;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < t; i += (u64)gridDim.x * blockDim.x)

@@ -8,7 +8,8 @@
 //   k_fixup (cross-CTA sums -> canonical out).
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include <algorithm>
 #include <cstdio>
@@ -101,6 +102,8 @@ struct pe_ctx {
   u64 G = 0, t_pad = 0;
   u32 n_wt = 0, n_slots = 0;
   std::vector<u32> dxdy;  // host copy [2G]
+  std::vector<u64> poly_off{0, 0};   // term offsets of the batched polynomials [npoly+1]
+  std::vector<u64> poly_rows{0, 0};  // first output row of each polynomial [npoly+1]
   // device
   u64 *d_c = nullptr, *d_m = nullptr, *d_w = nullptr, *d_ms = nullptr;
   double *d_mpd = nullptr, *d_mspd = nullptr;
@@ -212,23 +215,49 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   CU(cudaMemcpyAsync(d_exps, exps, t * n * sizeof(u32), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(d_alpha, alpha_red.data(), (nz + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
 
-  // ---- keys, sort descending (a2)
+  // ---- keys, sort descending (a2); batched polynomials: stable re-sort by polynomial id
   u64 *d_key, *d_key2; u32 *d_idx, *d_idx2;
   if (dalloc(&d_key, t) || dalloc(&d_key2, t) || dalloc(&d_idx, t) || dalloc(&d_idx2, t)) return g_last_error;
   tmp.v.insert(tmp.v.end(), {d_key, d_key2, d_idx, d_idx2});
   k_keys<<<grid_for(t, 256), 256, 0, s>>>(d_exps, t, n, d_key, d_idx);
   CU(cudaGetLastError());
-  size_t sort_bytes = 0, rle_bytes = 0;
+  const u32 npoly = (u32)h->poly_off.size() - 1;
+  size_t sort_bytes = 0, sort2_bytes = 0, sel_bytes = 0;
+  unsigned char* d_flags;
+  u32 *d_starts, *d_nruns, *d_pid = nullptr, *d_pid2 = nullptr, *d_iota = nullptr, *d_perm = nullptr;
+  if (dalloc(&d_flags, t) || dalloc(&d_starts, t + 1) || dalloc(&d_nruns, 1)) return g_last_error;
+  tmp.v.insert(tmp.v.end(), {d_flags, d_starts, d_nruns});
+  cub::CountingInputIterator<u32> counting(0);
   CU(cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, d_key, d_key2, d_idx, d_idx2, (int)t, 0, 64, s));
-  u64* d_ukeys; u32* d_counts; u32* d_nruns;
-  if (dalloc(&d_ukeys, t) || dalloc(&d_counts, t) || dalloc(&d_nruns, 1)) return g_last_error;
-  tmp.v.insert(tmp.v.end(), {d_ukeys, d_counts, d_nruns});
-  CU(cub::DeviceRunLengthEncode::Encode(nullptr, rle_bytes, d_key2, d_ukeys, d_counts, d_nruns, (int)t, s));
+  CU(cub::DeviceSelect::Flagged(nullptr, sel_bytes, counting, d_flags, d_starts, d_nruns, (int)t, s));
+  if (npoly > 1) {
+    if (dalloc(&d_pid, t) || dalloc(&d_pid2, t) || dalloc(&d_iota, t) || dalloc(&d_perm, t)) return g_last_error;
+    tmp.v.insert(tmp.v.end(), {d_pid, d_pid2, d_iota, d_perm});
+    CU(cub::DeviceRadixSort::SortPairs(nullptr, sort2_bytes, d_pid, d_pid2, d_iota, d_perm, (int)t, 0, 32, s));
+  }
   void* d_cub;
-  if (dalloc((char**)&d_cub, std::max(sort_bytes, rle_bytes))) return g_last_error;
+  if (dalloc((char**)&d_cub, std::max(std::max(sort_bytes, sort2_bytes), sel_bytes))) return g_last_error;
   tmp.v.push_back(d_cub);
   CU(cub::DeviceRadixSort::SortPairsDescending(d_cub, sort_bytes, d_key, d_key2, d_idx, d_idx2, (int)t, 0, 64, s));
-  CU(cub::DeviceRunLengthEncode::Encode(d_cub, rle_bytes, d_key2, d_ukeys, d_counts, d_nruns, (int)t, s));
+  u64* d_keyS = d_key2;   // final order: (polynomial asc, dx desc, dy desc)
+  u32* d_idxS = d_idx2;
+  if (npoly > 1) {
+    u64* d_poff;
+    if (dalloc(&d_poff, npoly + 1)) return g_last_error;
+    tmp.v.push_back(d_poff);
+    CU(cudaMemcpyAsync(d_poff, h->poly_off.data(), (npoly + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
+    k_poly_of<<<grid_for(t, 256), 256, 0, s>>>(d_idx2, t, d_poff, npoly, d_pid, d_iota);
+    CU(cudaGetLastError());
+    // LSD radix sort is stable: equal polynomial ids keep their (dx,dy)-descending order
+    CU(cub::DeviceRadixSort::SortPairs(d_cub, sort2_bytes, d_pid, d_pid2, d_iota, d_perm, (int)t, 0, 32, s));
+    k_apply_perm<<<grid_for(t, 256), 256, 0, s>>>(d_perm, t, d_key2, d_idx2, d_key, d_idx);
+    CU(cudaGetLastError());
+    d_keyS = d_key;
+    d_idxS = d_idx;
+  }
+  k_run_flags<<<grid_for(t, 256), 256, 0, s>>>(d_keyS, npoly > 1 ? d_pid2 : nullptr, t, d_flags);
+  CU(cudaGetLastError());
+  CU(cub::DeviceSelect::Flagged(d_cub, sel_bytes, counting, d_flags, d_starts, d_nruns, (int)t, s));
 
   // max evaluated exponent -> power-table size
   u32* d_dmax;
@@ -245,13 +274,25 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   CU(cudaStreamSynchronize(s));
   const u64 G = nruns;
   h->G = G;
+  u64* d_ukeys; u32* d_upid;
+  if (dalloc(&d_ukeys, G) || dalloc(&d_upid, G)) return g_last_error;
+  tmp.v.insert(tmp.v.end(), {d_ukeys, d_upid});
+  k_gather_runs<<<grid_for(G, 256), 256, 0, s>>>(d_starts, (u32)G, d_keyS, npoly > 1 ? d_pid2 : nullptr,
+                                                 d_ukeys, d_upid);
+  CU(cudaGetLastError());
   std::vector<u64> ukeys(G);
-  std::vector<u32> counts(G);
+  std::vector<u32> starts(G + 1), upid(G), counts(G);
   CU(cudaMemcpyAsync(ukeys.data(), d_ukeys, G * sizeof(u64), cudaMemcpyDeviceToHost, s));
-  CU(cudaMemcpyAsync(counts.data(), d_counts, G * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(starts.data(), d_starts, G * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(upid.data(), d_upid, G * sizeof(u32), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
+  starts[G] = (u32)t;
+  for (u64 g = 0; g < G; ++g) counts[g] = starts[g + 1] - starts[g];
   h->dxdy.resize(2 * G);
   for (u64 g = 0; g < G; ++g) { h->dxdy[2 * g] = (u32)(ukeys[g] >> 32); h->dxdy[2 * g + 1] = (u32)ukeys[g]; }
+  h->poly_rows.assign(npoly + 1, G);
+  for (u64 g = G; g-- > 0;) h->poly_rows[upid[g]] = g;            // first row of each polynomial
+  for (u32 k = npoly; k-- > 0;) h->poly_rows[k] = std::min(h->poly_rows[k], h->poly_rows[k + 1]);
 
   // ---- host tile plan from the G bucket sizes
   const int maxR = (h->path == kFp64 || h->path == kMix) ? 8 : 16;
@@ -321,7 +362,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
       dalloc(&h->d_ms, h->t_pad) || dalloc(&h->d_mpd, h->t_pad) || dalloc(&h->d_mspd, h->t_pad) ||
       dalloc(&h->d_perm, h->t_pad) || dalloc(&h->d_wt_info, n_wt) || dalloc(&h->d_slot_start, G + 1))
     return g_last_error;
-  k_setup<<<grid_for(h->t_pad, 256), 256, 0, s>>>(d_exps, d_coeffs, n, d_idx2, d_poff, d_bstart, (u32)G,
+  k_setup<<<grid_for(h->t_pad, 256), 256, 0, s>>>(d_exps, d_coeffs, n, d_idxS, d_poff, d_bstart, (u32)G,
                                                    h->t_pad, d_table, D, d_alpha, h->d_c, h->d_m, h->d_w,
                                                    h->d_ms, h->d_mpd, h->d_mspd, h->d_perm, h->mp);
   CU(cudaGetLastError());
@@ -331,10 +372,18 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   return PE_OK;
 }
 
-extern "C" pe_ctx* pe_create_ex(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs,
-                                const uint32_t* exps, const uint64_t* alpha, const pe_config* cfg) {
+static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_poly, uint32_t n,
+                             const uint64_t* coeffs, const uint32_t* exps, const uint64_t* alpha,
+                             const pe_config* cfg) {
   g_last_error = PE_OK;
   // ---- validation before any CUDA call
+  if (npoly < 1 || !t_per_poly) { set_err(PE_EINVAL); return nullptr; }
+  std::vector<u64> poly_off(npoly + 1, 0);
+  for (u32 k = 0; k < npoly; ++k) {
+    poly_off[k + 1] = poly_off[k] + t_per_poly[k];
+    if (poly_off[k + 1] < poly_off[k]) { set_err(PE_ERANGE); return nullptr; }
+  }
+  const u64 t = poly_off[npoly];
   if (n < 2 || n > 66) { set_err(PE_EINVAL); return nullptr; }
   if (t > 0 && (!coeffs || !exps)) { set_err(PE_EINVAL); return nullptr; }
   if (n > 2 && !alpha) { set_err(PE_EINVAL); return nullptr; }
@@ -385,6 +434,8 @@ extern "C" pe_ctx* pe_create_ex(uint64_t p, uint64_t t, uint32_t n, const uint64
   h->path = path;
   h->R = R; h->W = W; h->chunk_req = chunk;
   h->partial_cap_bytes = (size_t)env_int("PE_PARTIAL_MB", 1024) << 20;
+  h->poly_off = poly_off;
+  h->poly_rows.assign(npoly + 1, 0);
   int rc = create_impl(h, coeffs, exps, alpha);
   if (rc != PE_OK) {
     int e = g_last_error != PE_OK ? g_last_error : rc;
@@ -396,9 +447,28 @@ extern "C" pe_ctx* pe_create_ex(uint64_t p, uint64_t t, uint32_t n, const uint64
   return h;
 }
 
+extern "C" pe_ctx* pe_create_ex(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs,
+                                const uint32_t* exps, const uint64_t* alpha, const pe_config* cfg) {
+  return create_common(p, 1, &t, n, coeffs, exps, alpha, cfg);
+}
+
 extern "C" pe_ctx* pe_create(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs,
                              const uint32_t* exps, const uint64_t* alpha) {
   return pe_create_ex(p, t, n, coeffs, exps, alpha, nullptr);
+}
+
+extern "C" pe_ctx* pe_create_batch(uint64_t p, uint32_t npoly, const uint64_t* t_per_poly, uint32_t n,
+                                   const uint64_t* coeffs, const uint32_t* exps, const uint64_t* alpha,
+                                   const pe_config* cfg) {
+  return create_common(p, npoly, t_per_poly, n, coeffs, exps, alpha, cfg);
+}
+
+extern "C" uint32_t pe_num_polys(const pe_ctx* h) { return h ? (uint32_t)h->poly_off.size() - 1 : 0; }
+
+extern "C" int pe_poly_rows(const pe_ctx* h, uint64_t* row_off) {
+  if (!h || !row_off) return set_err(PE_EINVAL);
+  memcpy(row_off, h->poly_rows.data(), h->poly_rows.size() * sizeof(u64));
+  return PE_OK;
 }
 
 extern "C" void pe_destroy(pe_ctx* h) {

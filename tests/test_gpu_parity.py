@@ -216,3 +216,44 @@ def test_mixed_path_parity(R, monkeypatch):
         with pe.Context.from_workload(w, R=R) as ctx:
             assert ctx.info()["path"] == "mix"
         check_full(w, R=R)
+
+
+# ---------------------------------------------------------------- NEXT-1: batched polynomials
+def test_batch_polys_same_points():
+    """pe_create_batch: f_0..f_3 at the same beta^j (PAPER.md:367-392 gcd images); rows per
+    polynomial equal separate single-polynomial oracle evaluations."""
+    p, n, T, j0 = P62, 6, 45, 1
+    rng = np.random.default_rng(301)
+    alpha = rng.integers(1, p, n - 2, dtype=np.uint64)
+    polys = []
+    for seed, t in ((302, 400), (303, 0), (304, 1), (305, 250)):
+        w = synth.random_small(seed, p, n, t, 3, T, j0) if t else None
+        polys.append((w.coeffs, w.exps) if w else (np.zeros(0, np.uint64), np.zeros((0, n), np.uint32)))
+    # neighbouring polynomials sharing a key at the boundary: last key of f_2 == first key of f_3
+    polys[2] = (polys[2][0], polys[2][1].copy())
+    polys[2][1][0, :2] = polys[3][1][:, :2].max(axis=0)
+    with pe.Context.batch(p, polys, alpha, n) as ctx:
+        rows_off = ctx.poly_rows().astype(np.int64)
+        out = ctx.eval(j0, T)
+        rows = ctx.buckets()
+    assert rows_off[0] == 0 and rows_off[-1] == out.shape[0] and len(rows_off) == len(polys) + 1
+    for k, (c, e) in enumerate(polys):
+        a, b = rows_off[k], rows_off[k + 1]
+        if c.size == 0:
+            assert a == b
+            continue
+        ref = oracle.eval_direct(p, n, c, e, alpha, j0, T)
+        assert rows[a:b].tolist() == oracle.buckets(e, n).tolist(), k
+        assert np.array_equal(out[a:b], ref), k
+
+
+def test_batch_config3_pair():
+    """f and h of config-3 shape (10^5 terms each) in one launch."""
+    f = synth.gen_config(3, t=100_000, T=200)
+    h = synth.gen_config(3, t=100_000, T=200, seed=99)
+    with pe.Context.batch(f.p, [(f.coeffs, f.exps), (h.coeffs, h.exps)], f.alpha, f.n) as ctx:
+        ro = ctx.poly_rows().astype(np.int64)
+        out = ctx.eval(f.j0, f.T)
+    inc_f = oracle.eval_incremental(f.p, f.n, f.coeffs, f.exps, f.alpha, f.j0, f.T)
+    inc_h = oracle.eval_incremental(f.p, f.n, h.coeffs, h.exps, f.alpha, f.j0, f.T)
+    assert np.array_equal(out[ro[0]:ro[1]], inc_f) and np.array_equal(out[ro[1]:ro[2]], inc_h)
