@@ -47,7 +47,9 @@ enum {
   PE_ENOTSUP = -6    /* requested path / option not supported for this p               */
 };
 
-enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_MIX = 3 };
+enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_MIX = 3, PE_PATH_INT32 = 4 };
+/* PE_PATH_INT32 is reported by pe_info only: every p < 2^31 (any requested path except FP64)
+ * uses 32-bit Shoup products. */
 /* PE_PATH_MIX is reported by pe_info only (env PE_CORE=mix, p < 2^50): half of every lane's
  * chains run FP64 Alg. 2 (FP64 pipe), half integer Shoup (IMAD pipe).  Correct but not faster
  * than pure Alg. 2 on B200 (both are issue-bound), so the automatic path for p < 2^50 is FP64. */

@@ -20,7 +20,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libpe.so")
 
 PE_OK, PE_EINVAL, PE_ENOTPRIME, PE_ERANGE, PE_ENOMEM, PE_ECUDA, PE_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
-PATH_AUTO, PATH_INT, PATH_FP64, PATH_MIX = 0, 1, 2, 3
+PATH_AUTO, PATH_INT, PATH_FP64, PATH_MIX, PATH_INT32 = 0, 1, 2, 3, 4
 CORE_SHOUP4, CORE_SHOUP2, CORE_MONT, CORE_FP64, CORE_FP64ADD, CORE_POW, CORE_SHOUP4RAW, CORE_HYB, CORE_HYBRAW = range(9)
 
 #: every symbol include/pe.h and include/pe_test.h declare
@@ -188,7 +188,7 @@ class Context:
         tp, ns = ctypes.c_uint64(), ctypes.c_uint64()
         _check(lib().pe_info(self._h, ctypes.byref(path), ctypes.byref(R), ctypes.byref(W), ctypes.byref(tp),
                              ctypes.byref(ns)), "pe_info")
-        name = {PATH_FP64: "fp64", PATH_MIX: "mix"}.get(path.value, "int")
+        name = {PATH_FP64: "fp64", PATH_MIX: "mix", PATH_INT32: "int32"}.get(path.value, "int")
         return {"path": name, "R": R.value, "warps": W.value,
                 "t_padded": tp.value, "n_slots": ns.value}
 

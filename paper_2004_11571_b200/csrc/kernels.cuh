@@ -15,7 +15,7 @@ namespace pe {
 constexpr int kMaxWarps = 16;
 constexpr int kSuper = 32;   // points per shared-memory super-group (one lane per point)
 
-enum PathKind { kInt4 = 0, kInt2 = 1, kFp64 = 2, kHyb = 3, kMix = 4 };
+enum PathKind { kInt4 = 0, kInt2 = 1, kFp64 = 2, kHyb = 3, kMix = 4, kInt32 = 5 };
 // kMix (p < 2^50): in every lane, chains r < R/2 run Alg. 2 on the FP64 pipe and chains
 // r >= R/2 run the Shoup-lazy product on the IMAD pipe, so both multiplier pipes work at once.
 // Max threads per CTA of k_step<PATH, R> (register budget: 65536 / threads per thread).
@@ -280,6 +280,7 @@ k_step(StepArgs args) {
   //      independent chain seeded by exponentiation)
   u64 a[R], m[R], w[R];
   double ad[R], md[R];   // FP64 path: a, m;  hybrid path: mp, msp
+  u32 a32[R], m32[R], w32[R];   // kInt32 path
   uint2 info = make_uint2(0, 0);
   if (active) {
     info = args.wt_info[wt];
@@ -294,6 +295,7 @@ k_step(StepArgs args) {
       if (fp_chain) { ad[r] = (double)a[r]; md[r] = (double)m[r]; }
       if (PATH == kHyb) { w[r] = __ldg(args.ms + q); md[r] = __ldg(args.mpd + q); ad[r] = __ldg(args.mspd + q); }
       if (PATH == kInt4 || PATH == kInt2 || (PATH == kMix && r >= R / 2)) w[r] = __ldg(args.w + q);
+      if (PATH == kInt32) { a32[r] = (u32)a[r]; m32[r] = (u32)m[r]; w32[r] = hi32(__ldg(args.w + q)); }
     }
   }
 
@@ -314,6 +316,14 @@ k_step(StepArgs args) {
             }
             const u64 si = __double2ull_rn(sum);
             acc[k].w0 = lo32(si); acc[k].w1 = hi32(si); acc[k].w2 = 0;
+          } else if (PATH == kInt32) {
+            u64 s64 = a32[0];                                  // R values < 2^32: no overflow
+#pragma unroll
+            for (int r = 1; r < R; ++r) s64 += a32[r];
+            acc[k].w0 = lo32(s64); acc[k].w1 = hi32(s64); acc[k].w2 = 0;
+            const u32 p32 = (u32)mp.p;
+#pragma unroll
+            for (int r = 0; r < R; ++r) a32[r] = mul_shoup32(a32[r], m32[r], w32[r], p32);
           } else if (PATH == kMix) {
             constexpr int RF = R / 2;
             double fs = ad[0];
@@ -343,7 +353,8 @@ k_step(StepArgs args) {
                                      : mul_shoup2(a[r], m[r], w[r], mp.np);
           }
         }
-        const U96 tot = PATH == kFp64 ? xpose_reduce8<2>(acc, lane) : xpose_reduce8<3>(acc, lane);
+        const U96 tot = (PATH == kFp64 || PATH == kInt32) ? xpose_reduce8<2>(acc, lane)
+                                                           : xpose_reduce8<3>(acc, lane);
         if ((lane & 3) == 0) sacc[buf][warp][s * 8 + (lane >> 2)] = tot;
       }
     }

@@ -176,6 +176,7 @@ static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStrea
     return cudaGetLastError();
   }
   if (path == kHyb) return launch_step_path<kHyb>(R, grid, block, s, a);
+  if (path == kInt32) return launch_step_path<kInt32>(R, grid, block, s, a);
   if (path == kInt4) return launch_step_path<kInt4>(R, grid, block, s, a);
   if (path == kInt2) return launch_step_path<kInt2>(R, grid, block, s, a);
   return launch_step_path<kFp64>(R, grid, block, s, a);
@@ -408,6 +409,8 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
     const bool hyb = core && !strcmp(core, "hyb");
     path = hyb ? kHyb : (p < (1ull << 62) ? kInt4 : kInt2);
     if (path_req == PE_PATH_AUTO && p < (1ull << 50) && (!core || !strcmp(core, "auto"))) path = kFp64;
+    // p < 2^31: 32-bit Shoup (4 IMAD slots per product instead of 14)
+    if (p < (1ull << 31) && (!core || !strcmp(core, "auto") || !strcmp(core, "int32"))) path = kInt32;
     if (core && !strcmp(core, "mix")) {
       if (p >= (1ull << 50)) { set_err(PE_ENOTSUP); return nullptr; }
       path = kMix;
@@ -592,7 +595,10 @@ extern "C" int pe_bucket_exps(const pe_ctx* h, uint32_t* dxdy) {
 extern "C" int pe_info(const pe_ctx* h, int32_t* path, int32_t* R, int32_t* warps, uint64_t* t_padded,
                        uint64_t* n_slots) {
   if (!h) return set_err(PE_EINVAL);
-  if (path) *path = h->path == kFp64 ? PE_PATH_FP64 : (h->path == kMix ? PE_PATH_MIX : PE_PATH_INT);
+  if (path)
+    *path = h->path == kFp64 ? PE_PATH_FP64
+          : h->path == kMix  ? PE_PATH_MIX
+          : h->path == kInt32 ? PE_PATH_INT32 : PE_PATH_INT;
   if (R) *R = h->R;
   if (warps) *warps = h->W;
   if (t_padded) *t_padded = h->t_pad;

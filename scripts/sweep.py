@@ -24,9 +24,15 @@ ap.add_argument("--core", default="shoup")
 ap.add_argument("--path", type=int, default=0)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--T", type=int, default=0)
+ap.add_argument("--p", type=int, default=0, help="override the prime (alpha redrawn in [1, p))")
 args = ap.parse_args()
-os.environ["PE_CORE"] = args.core
+if args.core != "auto":
+    os.environ["PE_CORE"] = args.core
 w = synth.gen_config(args.config)
+if args.p:
+    import numpy as np
+    w.p = args.p
+    w.alpha = synth.uniform_mod(np.random.default_rng(args.p), 1, args.p, w.n - 2)
 T = args.T or w.T
 out = torch.empty((1024 * 1024 * 64,), dtype=torch.int64, device="cuda")
 s = torch.cuda.current_stream()

@@ -257,3 +257,28 @@ def test_batch_config3_pair():
     inc_f = oracle.eval_incremental(f.p, f.n, f.coeffs, f.exps, f.alpha, f.j0, f.T)
     inc_h = oracle.eval_incremental(f.p, f.n, h.coeffs, h.exps, f.alpha, f.j0, f.T)
     assert np.array_equal(out[ro[0]:ro[1]], inc_f) and np.array_equal(out[ro[1]:ro[2]], inc_h)
+
+
+# ---------------------------------------------------------------- NEXT-3: 32-bit primes
+@pytest.mark.parametrize("p,R", [((1 << 31) - 1, 16), ((1 << 31) - 1, 8), (2_147_483_629, 4), (65_521, 2),
+                                 (3, 1), (1_000_003, 16)])
+def test_int32_path_parity(p, R):
+    """p < 2^31 -> 32-bit Shoup products (pe_info path 'int32'), bit-exact vs the oracle."""
+    w = synth.gen_config(3, t=40_000, T=77)
+    w.p = p
+    w.alpha = synth.uniform_mod(np.random.default_rng(p), 1, p, w.n - 2)
+    with pe.Context.from_workload(w, R=R) as ctx:
+        assert ctx.info()["path"] == "int32"
+    check_full(w, R=R)
+
+
+def test_int32_equals_int64_core():
+    """Same 31-bit instance through the 32-bit path and (PE_CORE=shoup) the 64-bit Shoup path."""
+    w = synth.random_small(310, (1 << 31) - 1, 7, 2000, 4, 66, 5, coeff_hi=2**64 - 1)
+    _, a = gpu_eval(w)
+    os.environ["PE_CORE"] = "shoup"
+    try:
+        _, b = gpu_eval(w)
+    finally:
+        del os.environ["PE_CORE"]
+    assert np.array_equal(a, b)
