@@ -136,6 +136,22 @@ int pe_set_timing(pe_ctx* h, int enable);
 int pe_kernel_stats(pe_ctx* h, uint64_t* step_launches, double* step_ms, double* fixup_ms,
                     double* term_points);
 
+/*
+ * Berlekamp-Massey per sequence (the sparse-interpolation step after the
+ * path; Ben-Or/Tiwari).  For each of the G sequences
+ * s_g(k) = d_seq[g*ld + k], k < T, values canonical in [0, p) (e.g. pe_eval_device output),
+ * computes the shortest connection polynomial C_g(z) = 1 + c_1 z + ... + c_L z^L with
+ * s_g(k) + sum_{i=1..L} c_i s_g(k-i) = 0 for L <= k < T:
+ *   d_lambda[g*ldl + i] = c_i (c_0 = 1, zeros beyond L), ldl >= T+1;   d_len[g] = L.
+ * For T >= 2 r_g it equals prod (1 - m_i z) over the bucket's distinct m_i with nonzero
+ * coefficient sum.  p prime, 3 <= p < 2^63.  Asynchronous on `stream` (device pointers);
+ * pe_bm is the synchronous host-array form.  Errors: PE_EINVAL, PE_ERANGE, PE_ENOMEM, PE_ECUDA.
+ */
+int pe_bm_device(uint64_t p, uint64_t G, uint64_t T, const uint64_t* d_seq, uint64_t ld,
+                 uint64_t* d_lambda, uint64_t ldl, uint32_t* d_len, void* stream);
+int pe_bm(uint64_t p, uint64_t G, uint64_t T, const uint64_t* seq /*[G*T]*/,
+          uint64_t* lambda /*[G*(T+1)]*/, uint32_t* len /*[G]*/);
+
 int pe_last_error(void);            /* thread-local code of the last failing call */
 const char* pe_strerror(int code);
 

@@ -27,7 +27,7 @@ CORE_SHOUP4, CORE_SHOUP2, CORE_MONT, CORE_FP64, CORE_FP64ADD, CORE_POW, CORE_SHO
 EXPORTS = ["pe_create", "pe_create_ex", "pe_eval", "pe_eval_device", "pe_destroy", "pe_num_buckets",
            "pe_bucket_exps", "pe_info", "pe_monomials", "pe_last_error", "pe_strerror",
            "pe_interp_bound_ok", "pe_test_core", "pe_bench_core", "pe_set_timing", "pe_kernel_stats",
-           "pe_create_batch", "pe_num_polys", "pe_poly_rows"]
+           "pe_create_batch", "pe_num_polys", "pe_poly_rows", "pe_bm_device", "pe_bm"]
 
 
 class PEError(RuntimeError):
@@ -95,6 +95,10 @@ def lib():
         L.pe_num_polys.restype = u32
         L.pe_poly_rows.argtypes = [vp, vp]
         L.pe_poly_rows.restype = ctypes.c_int
+        L.pe_bm_device.argtypes = [u64, u64, u64, vp, u64, vp, u64, vp, vp]
+        L.pe_bm_device.restype = ctypes.c_int
+        L.pe_bm.argtypes = [u64, u64, u64, vp, vp, vp]
+        L.pe_bm.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -234,6 +238,16 @@ def bench_core(variant: int, p: int, R: int, blocks: int, threads: int, iters: i
     _check(lib().pe_bench_core(variant, p, R, blocks, threads, iters, ctypes.byref(ms), ctypes.byref(steps),
                                ctypes.byref(cyc)), "pe_bench_core")
     return ms.value, steps.value, cyc.value
+
+
+def berlekamp_massey(p: int, seq: np.ndarray):
+    """pe_bm on host rows seq[G, T] -> (lengths uint32[G], connection polys uint64[G, T+1])."""
+    seq = np.ascontiguousarray(seq, dtype=np.uint64)
+    G, T = seq.shape
+    lam = np.zeros((G, T + 1), np.uint64)
+    ln = np.zeros(G, np.uint32)
+    _check(lib().pe_bm(p, G, T, _ptr(seq), _ptr(lam), _ptr(ln)), "pe_bm")
+    return ln, lam
 
 
 def interp_bound_ok(p: int, t: int) -> bool:

@@ -225,3 +225,67 @@ def test_scalar_core_random():
             e = int(rng.integers(0, 1 << 62))
             assert oracle.mulmod(a, b, p) == a * b % p
             assert oracle.powmod(a, e, p) == pow(a, e, p)
+
+
+# ---------------------------------------------------------------- Berlekamp-Massey oracle pins
+from oracle.bm import berlekamp_massey  # noqa: E402
+
+
+def _expand_prod_1_minus(ms, p):
+    c = [1]
+    for r in ms:                      # multiply by (1 - r z)
+        nc = c + [0]
+        for i in range(len(c)):
+            nc[i + 1] = (nc[i + 1] - r * c[i]) % p
+        c = nc
+    return c
+
+
+def test_bm_closed_forms():
+    p = 1_000_003
+    # Fibonacci: s_n = s_{n-1} + s_{n-2}  ->  C = 1 - z - z^2
+    fib = [0, 1]
+    for _ in range(30):
+        fib.append((fib[-1] + fib[-2]) % p)
+    assert berlekamp_massey(fib, p) == (2, [1, p - 1, p - 1])
+    # geometric c r^n -> C = 1 - r z
+    assert berlekamp_massey([5 * pow(7, n, p) % p for n in range(10)], p) == (1, [1, p - 7])
+    # zero sequence -> L = 0
+    assert berlekamp_massey([0] * 9, p) == (0, [1])
+    # impulse at the last position -> L = T (no shorter LFSR generates it)
+    L, C = berlekamp_massey([0] * 7 + [3], p)
+    assert L == 8
+
+
+def test_bm_power_sums_give_product():
+    """s_n = sum a_i m_i^n (distinct m_i, a_i != 0), T = 2r: C = prod (1 - m_i z)."""
+    p = (1 << 61) - 1
+    import random
+    rnd = random.Random(11)
+    for r in (1, 2, 5, 17):
+        ms = rnd.sample(range(2, p), r)
+        a = [rnd.randrange(1, p) for _ in range(r)]
+        seq = [sum(ai * pow(mi, n, p) for ai, mi in zip(a, ms)) % p for n in range(2 * r)]
+        L, C = berlekamp_massey(seq, p)
+        assert L == r and C == _expand_prod_1_minus(ms, p)
+
+
+def test_bm_on_oracle_output_matches_monomials():
+    """P9 through BM: every bucket of an oracle evaluation at j = 0.. (T >= 2 r_g) has connection
+    polynomial prod over its distinct m_i of (1 - m_i z)."""
+    p, n, T = (1 << 62) - 57, 5, 24
+    w = synth.random_small(31, p, n, 60, 3, T, 0)
+    w.exps[:, 0] = np.arange(60) % 9                    # 9 buckets of <= 7 terms
+    w.exps[:, 1] = 0
+    out = oracle.eval_direct(p, n, w.coeffs, w.exps, w.alpha, 0, T)
+    rows = oracle.buckets(w.exps, n).tolist()
+    for g, r in enumerate(rows):
+        members = [i for i in range(60) if int(w.exps[i, 0]) == r[0]]
+        coef = {}
+        for i in members:
+            m = _m_python(w.alpha, w.exps[i, 2:], p)
+            coef[m] = (coef.get(m, 0) + int(w.coeffs[i])) % p
+        ms = sorted(m for m, c in coef.items() if c)
+        L, C = berlekamp_massey(out[g].tolist(), p)
+        assert L == len(ms)
+        assert C == _expand_prod_1_minus(ms, p)
