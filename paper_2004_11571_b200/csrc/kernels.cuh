@@ -216,11 +216,12 @@ static __global__ void k_setup(const u32* __restrict__ exps, const u64* __restri
     c_out[q] = c;
     m_out[q] = m;
     w_out[q] = shoup_w(m, mp.p);
-    // mul_hyb constants: ms = m 2^32 mod p, mp = m/p, msp = ms/p (relative error <= 3u each)
-    const u64 ms = mulmod(m, (u64)(((unsigned __int128)1 << 32) % mp.p), mp);
-    ms_out[q] = ms;
-    mp_out[q] = __ddiv_rn(__ull2double_rn(m), __ull2double_rn(mp.p));
-    msp_out[q] = __ddiv_rn(__ull2double_rn(ms), __ull2double_rn(mp.p));
+    if (ms_out) {  // mul_hyb constants: ms = m 2^32 mod p, mp = m/p, msp = ms/p (rel. error <= 3u)
+      const u64 ms = mulmod(m, (u64)(((unsigned __int128)1 << 32) % mp.p), mp);
+      ms_out[q] = ms;
+      mp_out[q] = __ddiv_rn(__ull2double_rn(m), __ull2double_rn(mp.p));
+      msp_out[q] = __ddiv_rn(__ull2double_rn(ms), __ull2double_rn(mp.p));
+    }
     perm_out[q] = src;
   }
 }

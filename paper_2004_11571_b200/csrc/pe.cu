@@ -129,18 +129,35 @@ static void drop_recs(pe_ctx* h) {
 static void free_all(pe_ctx* h) {
   if (!h) return;
   drop_recs(h);
-  cudaFree(h->d_c); cudaFree(h->d_m); cudaFree(h->d_w); cudaFree(h->d_perm);
-  cudaFree(h->d_ms); cudaFree(h->d_mpd); cudaFree(h->d_mspd);
-  cudaFree(h->d_wt_info); cudaFree(h->d_slot_start); cudaFree(h->d_partial);
-  cudaFree(h->d_out_scratch);
+  // stream-ordered frees back into the (retained) device memory pool
+  cudaStream_t s = h->stream;
+  for (void* q : {(void*)h->d_c, (void*)h->d_m, (void*)h->d_w, (void*)h->d_perm, (void*)h->d_ms, (void*)h->d_mpd,
+                  (void*)h->d_mspd, (void*)h->d_wt_info, (void*)h->d_slot_start, (void*)h->d_partial,
+                  (void*)h->d_out_scratch})
+    if (q) cudaFreeAsync(q, s);
+  if (s) cudaStreamSynchronize(s);
   if (h->stream) cudaStreamDestroy(h->stream);
 }
 
+// All device buffers are stream-ordered allocations from the device's default memory pool,
+// whose release threshold is raised once per device so that repeated create / eval / destroy
+// cycles reuse memory instead of paying cudaMalloc / cudaFree each time.
+static thread_local cudaStream_t g_alloc_stream = nullptr;
+static void retain_pool_once(int dev) {
+  static bool done[64] = {};
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
 template <class T>
 static int dalloc(T** p, size_t n) {
   *p = nullptr;
   if (n == 0) n = 1;
-  CU(cudaMalloc((void**)p, n * sizeof(T)));
+  CU(cudaMallocAsync((void**)p, n * sizeof(T), g_alloc_stream));
   return PE_OK;
 }
 
@@ -196,6 +213,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   CU(cudaGetDevice(&h->device));
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   cudaStream_t s = h->stream;
+  retain_pool_once(h->device);
+  g_alloc_stream = s;
   if (t == 0) {
     h->G = 0;
     return PE_OK;
@@ -207,9 +226,11 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   if (dalloc(&d_coeffs, t) || dalloc(&d_exps, t * n) || dalloc(&d_alpha, nz + 1)) return g_last_error;
   struct Tmp {
     std::vector<void*> v;
-    ~Tmp() { for (void* p : v) cudaFree(p); }
+    cudaStream_t s = nullptr;
+    ~Tmp() { for (void* p : v) if (p) cudaFreeAsync(p, s); }
   } tmp;
   tmp.v = {d_coeffs, d_exps, d_alpha};
+  tmp.s = s;
   std::vector<u64> alpha_red(nz + 1, 1);
   for (u32 l = 0; l < nz; ++l) alpha_red[l] = alpha[l] % h->p;
   CU(cudaMemcpyAsync(d_coeffs, coeffs, t * sizeof(u64), cudaMemcpyHostToDevice, s));
@@ -359,8 +380,10 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   tmp.v.insert(tmp.v.end(), {d_poff, d_bstart});
   CU(cudaMemcpyAsync(d_poff, poff.data(), (G + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(d_bstart, bstart.data(), (G + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
+  if (h->path == kHyb &&  // hybrid-core constants only when that core runs
+      (dalloc(&h->d_ms, h->t_pad) || dalloc(&h->d_mpd, h->t_pad) || dalloc(&h->d_mspd, h->t_pad)))
+    return g_last_error;
   if (dalloc(&h->d_c, h->t_pad) || dalloc(&h->d_m, h->t_pad) || dalloc(&h->d_w, h->t_pad) ||
-      dalloc(&h->d_ms, h->t_pad) || dalloc(&h->d_mpd, h->t_pad) || dalloc(&h->d_mspd, h->t_pad) ||
       dalloc(&h->d_perm, h->t_pad) || dalloc(&h->d_wt_info, n_wt) || dalloc(&h->d_slot_start, G + 1))
     return g_last_error;
   k_setup<<<grid_for(h->t_pad, 256), 256, 0, s>>>(d_exps, d_coeffs, n, d_idxS, d_poff, d_bstart, (u32)G,
@@ -496,11 +519,10 @@ static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaSt
   Tp = std::min<u64>(Tp, 1u << 30);
   const size_t need = (size_t)nslots * Tp;
   if (need > h->partial_elems) {
-    CU(cudaStreamSynchronize(s));
-    cudaFree(h->d_partial);
+    if (h->d_partial) cudaFreeAsync(h->d_partial, s);
     h->d_partial = nullptr;
     h->partial_elems = 0;
-    CU(cudaMalloc((void**)&h->d_partial, need * sizeof(u64)));
+    CU(cudaMallocAsync((void**)&h->d_partial, need * sizeof(u64), s));
     h->partial_elems = need;
   }
   const int W = h->W;
@@ -567,10 +589,11 @@ extern "C" int pe_eval(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* out) {
   const size_t need = (size_t)h->G * T;
   int rc = PE_OK;
   if (need > h->out_scratch_elems) {
-    cudaFree(h->d_out_scratch);
+    if (h->d_out_scratch) cudaFreeAsync(h->d_out_scratch, h->stream);
     h->d_out_scratch = nullptr;
     h->out_scratch_elems = 0;
-    if (cudaMalloc((void**)&h->d_out_scratch, need * sizeof(u64)) != cudaSuccess) rc = set_err(PE_ENOMEM);
+    if (cudaMallocAsync((void**)&h->d_out_scratch, need * sizeof(u64), h->stream) != cudaSuccess)
+      rc = set_err(PE_ENOMEM);
     else h->out_scratch_elems = need;
   }
   if (rc == PE_OK) rc = eval_device_impl(h, j0, T, h->d_out_scratch, T, h->stream);
