@@ -533,9 +533,11 @@ static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaSt
     if (chunk == 0) {
       // cover the SMs: aim for >= 148 * 2 * 4 CTAs, but keep chunks long (seeding cost
       // ~ 2 log2(j) Montgomery products per term per chunk)
-      const u64 target = 148ull * 2 * 4;
+      // >= ~32 waves of 2 CTAs/SM keeps the last-wave tail small (config 5: 2 chunks, -1%);
+      // chunks stay >= 1024 points so the seed (~2 log2 j Montgomery products) is amortised
+      const u64 target = 148ull * 2 * 32;
       u64 nch = std::max<u64>(1, (target + n_cta - 1) / n_cta);
-      nch = std::min<u64>(nch, std::max<u64>(1, np / 512));
+      nch = std::min<u64>(nch, std::max<u64>(1, np / 1024));
       chunk = (u32)((np + nch - 1) / nch);
       chunk = (chunk + kSuper - 1) / kSuper * kSuper;
     }
