@@ -54,6 +54,17 @@ def peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def ncu_traffic(info):
+    """dram__bytes_read.sum + dram__bytes_write.sum per k_step launch from the committed
+    ncu --set full capture of this same bench launch (profiles/r01_kstep_summary.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_kstep_summary.json")) as f:
+            s = json.load(f)
+        return s["traffic_bytes_per_launch"] if info and info.get("path") == "int" else None
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 # ---------------------------------------------------------------- clocks sampling
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -264,7 +275,7 @@ def main():
     except pe.PEError:
         pass
     roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tterm-pt/s",
-            "frac": achieved / peak if peak else None, "traffic": None,
+            "frac": achieved / peak if peak else None, "traffic": ncu_traffic(info),
             "kernel": f"k_step<{info['path']},R={info['R']}>",
             "peak_basis": (f"IMAD-pipe model (DESIGN.md Roofline): {N_SM} SMs x {sm_mhz:.0f} MHz ({pk_kind} "
                            f"sm_max_mhz) x {IMAD_LANES_PER_CLK_SM} IMAD lanes/clk/SM / {IMAD_SLOTS_PER_TP} "

@@ -19,6 +19,30 @@ __device__ __forceinline__ void set96_sum(U96& x, u64 u, u64 v) {
       : "r"((u32)u), "r"((u32)(u >> 32)), "r"((u32)v), "r"((u32)(v >> 32)));
 }
 
+
+__device__ __forceinline__ void add96(U96& x, const U96& y) {
+  asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+      : "+r"(x.w0), "+r"(x.w1), "+r"(x.w2) : "r"(y.w0), "r"(y.w1), "r"(y.w2));
+}
+__device__ __forceinline__ U96 shfl96(const U96& x, int off) {
+  U96 r; r.w0 = __shfl_xor_sync(0xffffffffu, x.w0, off); r.w1 = __shfl_xor_sync(0xffffffffu, x.w1, off);
+  r.w2 = __shfl_xor_sync(0xffffffffu, x.w2, off); return r;
+}
+__device__ __forceinline__ U96 sel96(bool c, const U96& a, const U96& b) {
+  U96 r; r.w0 = c ? a.w0 : b.w0; r.w1 = c ? a.w1 : b.w1; r.w2 = c ? a.w2 : b.w2; return r;
+}
+__device__ __forceinline__ U96 xpose8(U96 (&v)[8], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  U96 t4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { U96 s = sel96(b4, v[i], v[i + 4]); t4[i] = sel96(b4, v[i + 4], v[i]); add96(t4[i], shfl96(s, 16)); }
+  U96 t2[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) { U96 s = sel96(b3, t4[i], t4[i + 2]); t2[i] = sel96(b3, t4[i + 2], t4[i]); add96(t2[i], shfl96(s, 8)); }
+  U96 s = sel96(b2, t2[0], t2[1]); U96 t1 = sel96(b2, t2[1], t2[0]); add96(t1, shfl96(s, 4));
+  add96(t1, shfl96(t1, 2)); add96(t1, shfl96(t1, 1)); return t1;
+}
+
 // V0: current library form
 __device__ __forceinline__ u64 mul_v0(u64 a, u64 m, u64 w, u64 np) {
   u64 r;
@@ -113,13 +137,13 @@ __device__ __forceinline__ u64 mulv(u64 a, u64 m, u64 w, u64 np) {
   if (V == 1) return mul_v1(a, m, w, np);
   if (V == 2) return mul_v2(a, m, w, np);
   if (V == 3) return mul_v3(a, m, w, np);
-  if (V == 5) return mul_v5(a, m, w, np);
+  if (V == 5 || V == 105) return mul_v5(a, m, w, np);
   if (V == 6) return mul_v6(a, m, w, np);
   return mul_v4(a, m, w, np);
 }
 
 template <int V, int R>
-__global__ void __launch_bounds__(256) kv(const u64* __restrict__ in, u64 np, int groups, u64* out) {
+__global__ void __launch_bounds__(256, 2) kv(const u64* __restrict__ in, u64 np, int groups, u64* out) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   u64 a[R], m[R], w[R];
 #pragma unroll
@@ -136,8 +160,13 @@ __global__ void __launch_bounds__(256) kv(const u64* __restrict__ in, u64 np, in
 #pragma unroll
       for (int r = 0; r < R; ++r) a[r] = mulv<V>(a[r], m[r], w[r], np);
     }
+    if (V >= 100) {
+      U96 x = xpose8(acc, threadIdx.x & 31);
+      tot.w0 ^= x.w0; tot.w1 += x.w1; tot.w2 ^= x.w2;
+    } else {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) { tot.w0 ^= acc[k].w0; tot.w1 += acc[k].w1; tot.w2 ^= acc[k].w2; }
+      for (int k = 0; k < 8; ++k) { tot.w0 ^= acc[k].w0; tot.w1 += acc[k].w1; tot.w2 ^= acc[k].w2; }
+    }
   }
   out[tid] = tot.w0 ^ ((u64)tot.w1 << 32) ^ tot.w2 ^ a[0];
 }
@@ -174,6 +203,7 @@ int main() {
     run<4>("v4_madc_q_wide_r", in, out, 2048);
     run<5>("v5_wide_cross", in, out, 2048);
     run<6>("v6_library", in, out, 2048);
+    run<105>("v5_plus_xpose", in, out, 2048);
   }
   printf("{\"status\": \"%s\"}\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
