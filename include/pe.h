@@ -47,7 +47,13 @@ enum {
   PE_ENOTSUP = -6    /* requested path / option not supported for this p               */
 };
 
-enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_MIX = 3, PE_PATH_INT32 = 4 };
+enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_MIX = 3, PE_PATH_INT32 = 4, PE_PATH_TC = 5 };
+/* PE_PATH_TC forces the tensor-core form of the step (p < 2^62, else PE_ENOTSUP): each bucket's
+ * block of T_c = 128 x 128 points is the product L * R of giant-step values c_i m_i^{j_s+128u} and
+ * baby-step values m_i^v (the Vandermonde structure M_i(beta^t) = m_i^t, PAPER.md:420-427,
+ * 465-478), computed exactly as 64 byte-by-byte int8 tcgen05 MMAs.  PE_PATH_AUTO
+ * selects it for 2^50 <= p < 2^62 when T >= 8192 (env PE_TC=0 off, 1 auto, 2 always);
+ * PE_PATH_INT never uses it.  Results are bit-identical either way. */
 /* PE_PATH_INT32 is reported by pe_info only: every p < 2^31 (any requested path except FP64)
  * uses 32-bit Shoup products. */
 /* PE_PATH_MIX is reported by pe_info only (env PE_CORE=mix, p < 2^50): half of every lane's
@@ -56,8 +62,8 @@ enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_MIX = 3, PE_
 
 /* Tuning knobs (0 = automatic).  They never change the result (pin P13). */
 typedef struct pe_config {
-  int32_t path;  /* PE_PATH_AUTO: FP64 Alg. 2 if p < 2^50 else INT64 Shoup; PE_PATH_FP64 / PE_PATH_INT
-                    force one.  env PE_PATH=int|fp64, PE_CORE=mix|fp64|hyb|shoup     */
+  int32_t path;  /* PE_PATH_AUTO: FP64 Alg. 2 if p < 2^50 else INT64 Shoup (tensor-core form for large
+                    T); PE_PATH_FP64 / PE_PATH_INT / PE_PATH_TC force one.  env PE_PATH=int|fp64, PE_CORE=mix|fp64|hyb|shoup     */
   int32_t R;     /* terms per lane: 1,2,4,8,16 (FP64: <= 8); auto picks by bucket sizes    */
   int32_t warps; /* warps per CTA, 1..16 (auto 8)                                          */
   int32_t chunk; /* points per CTA (multiple of 32; auto by grid coverage)                 */
@@ -122,6 +128,11 @@ int pe_bucket_exps(const pe_ctx* h, uint32_t* dxdy);        /* HOST uint32[2G]: 
 /* Introspection: values chosen at create. Any pointer may be NULL. */
 int pe_info(const pe_ctx* h, int32_t* path, int32_t* R, int32_t* warps, uint64_t* t_padded,
             uint64_t* n_slots);
+
+/* Tensor-core path state: *mode = 0 (not built for this handle), 1 (automatic: used by evaluations
+ * with T >= *min_T), 2 (forced, every T); *pieces = accumulation pieces (<= 4096 terms of one
+ * bucket each).  Any pointer may be NULL.  Errors: PE_EINVAL (h NULL). */
+int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint64_t* min_T);
 
 /* m_i = prod_l alpha_l^{e_i,l} mod p for every input term i (HOST uint64[t], input order). */
 int pe_monomials(const pe_ctx* h, uint64_t* m);

@@ -20,14 +20,14 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libpe.so")
 
 PE_OK, PE_EINVAL, PE_ENOTPRIME, PE_ERANGE, PE_ENOMEM, PE_ECUDA, PE_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
-PATH_AUTO, PATH_INT, PATH_FP64, PATH_MIX, PATH_INT32 = 0, 1, 2, 3, 4
+PATH_AUTO, PATH_INT, PATH_FP64, PATH_MIX, PATH_INT32, PATH_TC = 0, 1, 2, 3, 4, 5
 CORE_SHOUP4, CORE_SHOUP2, CORE_MONT, CORE_FP64, CORE_FP64ADD, CORE_POW, CORE_SHOUP4RAW, CORE_HYB, CORE_HYBRAW = range(9)
 
 #: every symbol include/pe.h and include/pe_test.h declare
 EXPORTS = ["pe_create", "pe_create_ex", "pe_eval", "pe_eval_device", "pe_destroy", "pe_num_buckets",
            "pe_bucket_exps", "pe_info", "pe_monomials", "pe_last_error", "pe_strerror",
            "pe_interp_bound_ok", "pe_test_core", "pe_bench_core", "pe_set_timing", "pe_kernel_stats",
-           "pe_create_batch", "pe_num_polys", "pe_poly_rows", "pe_bm_device", "pe_bm"]
+           "pe_create_batch", "pe_num_polys", "pe_poly_rows", "pe_bm_device", "pe_bm", "pe_tc_info"]
 
 
 class PEError(RuntimeError):
@@ -99,6 +99,8 @@ def lib():
         L.pe_bm_device.restype = ctypes.c_int
         L.pe_bm.argtypes = [u64, u64, u64, vp, vp, vp]
         L.pe_bm.restype = ctypes.c_int
+        L.pe_tc_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(u64), ctypes.POINTER(u64)]
+        L.pe_tc_info.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -193,8 +195,17 @@ class Context:
         _check(lib().pe_info(self._h, ctypes.byref(path), ctypes.byref(R), ctypes.byref(W), ctypes.byref(tp),
                              ctypes.byref(ns)), "pe_info")
         name = {PATH_FP64: "fp64", PATH_MIX: "mix", PATH_INT32: "int32"}.get(path.value, "int")
+        mode, pieces, min_t = ctypes.c_int32(), ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().pe_tc_info(self._h, ctypes.byref(mode), ctypes.byref(pieces), ctypes.byref(min_t)),
+               "pe_tc_info")
         return {"path": name, "R": R.value, "warps": W.value,
-                "t_padded": tp.value, "n_slots": ns.value}
+                "t_padded": tp.value, "n_slots": ns.value,
+                "tc_mode": mode.value, "tc_pieces": pieces.value, "tc_min_T": min_t.value}
+
+    def uses_tc(self, T: int) -> bool:
+        """True if an evaluation of T points runs the tensor-core kernel (PE_PATH_TC / auto)."""
+        i = self.info()
+        return i["tc_mode"] != 0 and T >= i["tc_min_T"]
 
     def monomials(self) -> np.ndarray:
         out = np.zeros(self.t, np.uint64)

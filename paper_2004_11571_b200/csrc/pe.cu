@@ -21,6 +21,7 @@
 
 #include "../../include/pe.h"
 #include "kernels.cuh"
+#include "tc.cuh"
 
 using namespace pe;
 
@@ -114,6 +115,16 @@ struct pe_ctx {
   size_t partial_elems = 0;
   u64* d_out_scratch = nullptr;
   size_t out_scratch_elems = 0;
+  // tensor-core path (tc.cuh): 0 off, 1 auto (T >= kTcMinT), 2 forced
+  int tc_mode = 0;
+  bool tc_ok = false;
+  u32 tc_npieces = 0, tc_nslots = 0;
+  int n_sm = 148;
+  u64 *d_m4 = nullptr, *d_w4 = nullptr, *d_mV = nullptr, *d_wV = nullptr, *d_mV4 = nullptr, *d_wV4 = nullptr;
+  uint4* d_piece = nullptr;
+  u32* d_tc_slot_start = nullptr;
+  u64* d_seed = nullptr;
+  size_t seed_elems = 0;
   size_t partial_cap_bytes = (size_t)1 << 30;
   // kernel timing (pe_set_timing / pe_kernel_stats)
   bool timing = false;
@@ -133,7 +144,9 @@ static void free_all(pe_ctx* h) {
   cudaStream_t s = h->stream;
   for (void* q : {(void*)h->d_c, (void*)h->d_m, (void*)h->d_w, (void*)h->d_perm, (void*)h->d_ms, (void*)h->d_mpd,
                   (void*)h->d_mspd, (void*)h->d_wt_info, (void*)h->d_slot_start, (void*)h->d_partial,
-                  (void*)h->d_out_scratch})
+                  (void*)h->d_out_scratch, (void*)h->d_m4, (void*)h->d_w4, (void*)h->d_mV, (void*)h->d_wV,
+                  (void*)h->d_mV4, (void*)h->d_wV4, (void*)h->d_piece, (void*)h->d_tc_slot_start,
+                  (void*)h->d_seed})
     if (q) cudaFreeAsync(q, s);
   if (s) cudaStreamSynchronize(s);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -198,6 +211,10 @@ static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStrea
   if (path == kInt2) return launch_step_path<kInt2>(R, grid, block, s, a);
   return launch_step_path<kFp64>(R, grid, block, s, a);
 }
+
+// automatic tensor-core path from this many points (a chunk is tc::kChunk = 16384 points; below
+// half a chunk the padding of the last chunk outweighs the gain)
+constexpr u64 kTcMinT = tc::kChunk / 2;
 
 static unsigned grid_for(u64 n, unsigned block) {
   u64 b = (n + block - 1) / block;
@@ -392,6 +409,41 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(h->d_wt_info, wt_info.data(), n_wt * sizeof(uint2), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(h->d_slot_start, slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
+
+  // ---- tensor-core path (tc.cuh): per-term strides + the piece plan
+  std::vector<uint4> pieces;
+  std::vector<u32> tc_slot_start(G + 1);
+  if (h->tc_mode != 0 && h->path == kInt4) {
+    const u64 tp = h->t_pad;
+    if (dalloc(&h->d_m4, tp) || dalloc(&h->d_w4, tp) || dalloc(&h->d_mV, tp) || dalloc(&h->d_wV, tp) ||
+        dalloc(&h->d_mV4, tp) || dalloc(&h->d_wV4, tp))
+      return g_last_error;
+    tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_m4, h->d_w4, h->d_mV, h->d_wV, h->d_mV4,
+                                                     h->d_wV4, h->mp);
+    CU(cudaGetLastError());
+    // pieces: each bucket's padded range split into ceil(n / kPieceMax) near-equal runs of whole
+    // K-blocks (<= kPieceMax terms keeps every int32 diagonal sum exact); slots contiguous per bucket
+    for (u64 g = 0; g < G; ++g) {
+      tc_slot_start[g] = (u32)pieces.size();
+      const u64 nkb = (poff[g + 1] - poff[g]) / tc::kKB;   // poff multiples of 32R
+      const u64 maxkb = tc::kPieceMax / tc::kKB;
+      const u64 np_g = (nkb + maxkb - 1) / maxkb;
+      u64 kb0 = 0;
+      for (u64 k = 0; k < np_g; ++k) {
+        const u64 len = nkb / np_g + (k < nkb % np_g ? 1 : 0);
+        pieces.push_back(make_uint4((u32)(poff[g] + kb0 * tc::kKB), (u32)len, (u32)pieces.size(), 0));
+        kb0 += len;
+      }
+    }
+    tc_slot_start[G] = (u32)pieces.size();
+    std::stable_sort(pieces.begin(), pieces.end(), [](const uint4& x, const uint4& y) { return x.y > y.y; });
+    h->tc_npieces = h->tc_nslots = (u32)pieces.size();
+    if (dalloc(&h->d_piece, pieces.size()) || dalloc(&h->d_tc_slot_start, G + 1)) return g_last_error;
+    CU(cudaMemcpyAsync(h->d_piece, pieces.data(), pieces.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(h->d_tc_slot_start, tc_slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
+    CU(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
+    h->tc_ok = true;
+  }
   CU(cudaStreamSynchronize(s));  // host vectors above must outlive the copies; tmp frees after
   return PE_OK;
 }
@@ -442,9 +494,19 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
       if (p >= (1ull << 50)) { set_err(PE_ENOTSUP); return nullptr; }
       path = kFp64;
     }
+  } else if (path_req == PE_PATH_TC) {
+    if (p >= (1ull << 62)) { set_err(PE_ENOTSUP); return nullptr; }
+    path = kInt4;
   } else {
     set_err(PE_EINVAL);
     return nullptr;
+  }
+  // tensor-core path: forced by PE_PATH_TC; automatic (large T) for the INT64 Shoup path when the
+  // caller asked for PE_PATH_AUTO; env PE_TC=0|1|2 overrides the automatic choice.
+  int tc_mode = path_req == PE_PATH_TC ? 2 : (path_req == PE_PATH_AUTO && path == kInt4 ? 1 : 0);
+  if (path_req == PE_PATH_AUTO && path == kInt4) {
+    const int e = env_int("PE_TC", 1);
+    tc_mode = e < 0 ? 0 : (e > 2 ? 2 : e);
   }
   int R = cfg && cfg->R ? cfg->R : env_int("PE_R", 0);
   int W = cfg && cfg->warps ? cfg->warps : env_int("PE_WARPS", 8);
@@ -458,6 +520,7 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
   h->p = p; h->t = t; h->n = n;
   h->mp = h_mod_params(p);
   h->path = path;
+  h->tc_mode = tc_mode;
   h->R = R; h->W = W; h->chunk_req = chunk;
   h->partial_cap_bytes = (size_t)env_int("PE_PARTIAL_MB", 1024) << 20;
   h->poly_off = poly_off;
@@ -510,14 +573,7 @@ extern "C" void pe_destroy(pe_ctx* h) {
 }
 
 // ---------------------------------------------------------------- eval
-static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s) {
-  if (T == 0 || h->G == 0) return PE_OK;
-  const u64 nslots = h->n_slots;
-  // pass size bounded by the partial-buffer cap
-  u64 Tp = std::max<u64>(kSuper, h->partial_cap_bytes / 8 / std::max<u64>(nslots, 1));
-  Tp = std::min<u64>(Tp, T);
-  Tp = std::min<u64>(Tp, 1u << 30);
-  const size_t need = (size_t)nslots * Tp;
+static int ensure_partial(pe_ctx* h, size_t need, cudaStream_t s) {
   if (need > h->partial_elems) {
     if (h->d_partial) cudaFreeAsync(h->d_partial, s);
     h->d_partial = nullptr;
@@ -525,6 +581,83 @@ static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaSt
     CU(cudaMallocAsync((void**)&h->d_partial, need * sizeof(u64), s));
     h->partial_elems = need;
   }
+  return PE_OK;
+}
+
+// Tensor-core evaluation (tc.cuh): per pass, chunk seeds -> k_tc (persistent, one CTA per SM)
+// -> k_fixup over the pieces' partial rows.
+static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s) {
+  const u64 nslots = h->tc_nslots;
+  u64 Tp = h->partial_cap_bytes / 8 / std::max<u64>(nslots, 1) / tc::kChunk * tc::kChunk;
+  Tp = std::max<u64>(Tp, tc::kChunk);
+  Tp = std::min<u64>(Tp, (T + tc::kChunk - 1) / tc::kChunk * tc::kChunk);
+  Tp = std::min<u64>(Tp, (u64)tc::kChunk * 4096);
+  if (ensure_partial(h, (size_t)nslots * std::min<u64>(Tp, T), s)) return g_last_error;
+  const u32 nch_max = (u32)(Tp / tc::kChunk);
+  if ((size_t)h->t_pad * nch_max > h->seed_elems) {
+    if (h->d_seed) cudaFreeAsync(h->d_seed, s);
+    h->d_seed = nullptr;
+    h->seed_elems = 0;
+    CU(cudaMallocAsync((void**)&h->d_seed, (size_t)h->t_pad * nch_max * sizeof(u64), s));
+    h->seed_elems = (size_t)h->t_pad * nch_max;
+  }
+  CU(cudaFuncSetAttribute(tc::k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
+  for (u64 k0 = 0; k0 < T; k0 += Tp) {
+    const u32 np = (u32)std::min<u64>(Tp, T - k0);
+    const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
+    tc::k_tc_seed<<<grid_for((u64)h->t_pad * nch, 256), 256, 0, s>>>(h->d_c, h->d_m, h->t_pad, nch, j0 + k0,
+                                                                      h->d_seed, h->mp);
+    CU(cudaGetLastError());
+    tc::TcArgs a;
+    a.S = h->d_seed;
+    a.m = h->d_m; a.w = h->d_w; a.m4 = h->d_m4; a.w4 = h->d_w4;
+    a.mV = h->d_mV; a.wV = h->d_wV; a.mV4 = h->d_mV4; a.wV4 = h->d_wV4;
+    a.piece = h->d_piece;
+    a.partial = h->d_partial;
+    a.ldp = np;
+    a.t_pad = h->t_pad;
+    a.npieces = h->tc_npieces;
+    a.nunits = h->tc_npieces * nch;
+    a.npts = np;
+    for (int d = 0; d < 15; ++d) a.Wd[d] = h_powmod(2, 8 * (u64)d, h->p);
+    a.mp = h->mp;
+    const unsigned grid = (unsigned)std::min<u64>(a.nunits, (u64)h->n_sm);
+    pe_ctx::Rec rec{};
+    if (h->timing) {
+      CU(cudaEventCreate(&rec.e0));
+      CU(cudaEventCreate(&rec.e1));
+      CU(cudaEventCreate(&rec.e2));
+      rec.tp = (double)h->t_pad * np;
+      CU(cudaEventRecord(rec.e0, s));
+    }
+    tc::k_tc<<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
+    CU(cudaGetLastError());
+    if (h->timing) CU(cudaEventRecord(rec.e1, s));
+    const u32 nkb = (np + 255) / 256;
+    k_fixup<<<(unsigned)(h->G * nkb), 256, 0, s>>>(h->d_partial, np, h->d_tc_slot_start, (u32)h->G, np, nkb,
+                                                   d_out + k0, ld, h->mp);
+    CU(cudaGetLastError());
+    if (h->timing) {
+      CU(cudaEventRecord(rec.e2, s));
+      h->recs.push_back(rec);
+    }
+  }
+  return PE_OK;
+}
+
+static bool use_tc(const pe_ctx* h, u64 T) {
+  return h->tc_ok && (h->tc_mode == 2 || (h->tc_mode == 1 && T >= kTcMinT));
+}
+
+static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s) {
+  if (T == 0 || h->G == 0) return PE_OK;
+  if (use_tc(h, T)) return eval_tc(h, j0, T, d_out, ld, s);
+  const u64 nslots = h->n_slots;
+  // pass size bounded by the partial-buffer cap
+  u64 Tp = std::max<u64>(kSuper, h->partial_cap_bytes / 8 / std::max<u64>(nslots, 1));
+  Tp = std::min<u64>(Tp, T);
+  Tp = std::min<u64>(Tp, 1u << 30);
+  if (ensure_partial(h, (size_t)nslots * Tp, s)) return g_last_error;
   const int W = h->W;
   const u32 n_cta = (h->n_wt + W - 1) / W;
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
@@ -628,6 +761,14 @@ extern "C" int pe_info(const pe_ctx* h, int32_t* path, int32_t* R, int32_t* warp
   if (warps) *warps = h->W;
   if (t_padded) *t_padded = h->t_pad;
   if (n_slots) *n_slots = h->n_slots;
+  return PE_OK;
+}
+
+extern "C" int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint64_t* min_T) {
+  if (!h) return set_err(PE_EINVAL);
+  if (mode) *mode = h->tc_ok ? h->tc_mode : 0;
+  if (pieces) *pieces = h->tc_npieces;
+  if (min_T) *min_T = h->tc_ok ? (h->tc_mode == 2 ? 1 : kTcMinT) : 0;
   return PE_OK;
 }
 

@@ -1,0 +1,360 @@
+// tc.cuh -- tensor-core form of the step-and-reduce (rows a5 + a6) for p < 2^62 (sm_100a).
+//
+// The matrix method's T x s evaluation matrix has the Vandermonde structure V[j][i] = m_i^j
+// ("M_i(beta^t) = m_i^t"; PAPER.md:465-478 transposed Vandermonde).  Writing a
+// chunk's points as j = j_s + u*V + v (u < U, v < V) factors every bucket's block of outputs
+// into one dense product per bucket g (baby-step / giant-step):
+//
+//     out[g][j_s + uV + v] = sum_{i in g} L[u][i] * R[i][v]   (mod p),
+//     L[u][i] = c_i m_i^{j_s + uV}   (giant steps: a_i <- a_i * m_i^V),
+//     R[i][v] = m_i^v                (baby steps:  a_i <- a_i * m_i),
+//
+// i.e. U + V modular products per term give U*V term-points, and the remaining work --
+// U*V*s multiply-adds -- is a dense contraction over the terms of a bucket, which is what
+// the 5th-generation tensor cores do.  Exactness: L and R are split into their 8 unsigned
+// bytes (L = sum_s 2^{8s} L_s), every byte product L_s R_t is an exact int8 MMA with int32
+// accumulation in TMEM, and the 64 (s, t) products are summed by diagonal d = s + t:
+//     X = sum_d 2^{8d} D_d,   D_d = sum_{s+t=d} L_s R_t,   D_d < 4096 * 8 * 255^2 < 2^31
+// for <= 4096 terms per accumulation (a "piece").  X mod p = sum_d D_d (2^{8d} mod p) mod p.
+//
+// Shapes: U = M = 128 (TMEM lanes), V = N = 128, K-block = 32 terms (one kind::i8 MMA).  The 15
+// diagonals do not fit TMEM at once (15 x 128 columns > 512), so a piece is evaluated in 4
+// rounds of <= 4 diagonals (16 digit-pair MMAs per K-block each), regenerating L and R per
+// round; rounds accumulate into the piece's partial row.  Measured on this B200: an
+// M=128, K=32 i8 MMA issues every ~136 clk for any N <= 256 (scripts/tc_probe.cu), so N = 128
+// costs 2x the N = 256 MACs/clk but balances the IMAD-bound generation.
+//
+// Warp roles (one CTA per SM, persistent, static round-robin over units = (piece, chunk)):
+//   warps 0-3  epilogue: tcgen05.ld the round's diagonals (TMEM lane = u), combine mod p,
+//              accumulate into partial[slot][chunk*16384 + u*128 + v]
+//   warp  4    TMEM allocator + single-thread MMA issuer (tcgen05.mma.cta_group::1.kind::i8)
+//   warps 5-10 producers, 3 pairs (one per smem stage): the L warp and the R warp of a pair
+//              generate one K-block's 128 giant-step / 128 baby-step values of 32 terms with
+//              Shoup products (4 chains per lane) and write their 8 byte planes in the
+//              no-swizzle K-major UMMA layout.
+#pragma once
+#include "modcore.cuh"
+
+namespace pe {
+namespace tc {
+
+constexpr int kU = 128;                   // giant steps per chunk  (MMA M / TMEM lanes)
+constexpr int kV = 128;                   // baby steps per chunk   (MMA N)
+constexpr u32 kChunk = kU * kV;           // points per chunk
+constexpr int kKB = 32;                   // terms per K-block (one i8 MMA K step)
+constexpr int kStages = 3;
+constexpr u32 kPieceMax = 4096;           // terms per accumulation: 4096 * 8 * 255^2 < 2^31
+constexpr u32 kLBO = 2048 + 64;           // bytes between the two 16-byte K chunks of a plane (+64: bank spread)
+constexpr u32 kPlane = 2 * kLBO;          // one digit plane: 128 rows x 32 bytes (+ pad)
+constexpr u32 kStageBytes = 16 * kPlane;  // 8 L planes + 8 R planes
+constexpr u32 kSmemBytes = kStages * kStageBytes + 1024;
+constexpr int kRounds = 4;
+constexpr int kThreads = 11 * 32;
+constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5;
+// diagonal groups: <= 4 diagonals (TMEM: 4 x 128 columns), 16 digit pairs each
+__device__ __constant__ const signed char kGroups[kRounds][4] = {
+    {7, 6, 0, -1}, {8, 5, 1, 14}, {9, 4, 2, 13}, {10, 3, 11, 12}};
+
+struct TcArgs {
+  const u64* S;     // [nch][t_pad] c_i m_i^{j_s(chunk)} mod p (chunk seeds)
+  const u64 *m, *w;      // m_i, Shoup w(m_i)            (baby-step seeds)
+  const u64 *m4, *w4;    // m_i^4                         (baby-step stride 4)
+  const u64 *mV, *wV;    // m_i^V                         (giant-step seeds)
+  const u64 *mV4, *wV4;  // m_i^{4V}                      (giant-step stride 4)
+  const uint4* piece;    // x = first padded term, y = K-blocks, z = partial slot (sorted by size desc)
+  u64* partial;          // [n_slots][ldp]
+  u64 ldp, t_pad;
+  u32 npieces, nunits, npts;
+  u64 Wd[15];            // 2^{8d} mod p
+  ModParams mp;
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t smem_desc(u32 saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((kLBO >> 4) & 0x3FFF) << 16;   // leading (K) byte offset
+  d |= (uint64_t)((128u >> 4) & 0x3FFF) << 32;   // stride (8-row group) byte offset
+  d |= (uint64_t)1 << 46;                        // sm_100 descriptor version; no swizzle
+  return d;
+}
+// kind::i8, D s32, A u8, B u8, both K-major, M = 128, N = 128
+constexpr u32 kIdesc = (2u << 4) | (0u << 7) | (0u << 10) | ((u32)(kV >> 3) << 17) | ((u32)(kU >> 4) << 24);
+
+__device__ __forceinline__ void mma_u8(u32 dtmem, uint64_t ad, uint64_t bd, u32 acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
+      :: "r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, u32 cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, u32 parity) {
+  u32 ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}\n"
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+// bounded wait: a protocol bug becomes a launch error instead of a hung GPU
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, u32 parity) {
+  for (u32 n = 0; !mbar_try(bar, parity); ++n)
+    if (n > (1u << 26)) __trap();
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld8(u32 taddr, u32 (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ u32 prmt(u32 a, u32 b, u32 sel) {
+  u32 r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// Byte-transpose 4 values (terms tq*4 + e, e < 4) into 8 digit-plane words (word s = byte s of
+// each value, value e in byte e = K position) and store them at row `row` of the stage.
+__device__ __forceinline__ void store_digits(uint8_t* planes, u32 off, const u64 (&x)[4]) {
+  const u32 l0 = lo32(x[0]), l1 = lo32(x[1]), l2 = lo32(x[2]), l3 = lo32(x[3]);
+  const u32 h0 = hi32(x[0]), h1 = hi32(x[1]), h2 = hi32(x[2]), h3 = hi32(x[3]);
+  u32 a = prmt(l0, l1, 0x5140), b = prmt(l2, l3, 0x5140);
+  u32 c = prmt(l0, l1, 0x7362), d = prmt(l2, l3, 0x7362);
+  *(u32*)(planes + 0 * kPlane + off) = prmt(a, b, 0x5410);
+  *(u32*)(planes + 1 * kPlane + off) = prmt(a, b, 0x7632);
+  *(u32*)(planes + 2 * kPlane + off) = prmt(c, d, 0x5410);
+  *(u32*)(planes + 3 * kPlane + off) = prmt(c, d, 0x7632);
+  a = prmt(h0, h1, 0x5140); b = prmt(h2, h3, 0x5140);
+  c = prmt(h0, h1, 0x7362); d = prmt(h2, h3, 0x7362);
+  *(u32*)(planes + 4 * kPlane + off) = prmt(a, b, 0x5410);
+  *(u32*)(planes + 5 * kPlane + off) = prmt(a, b, 0x7632);
+  *(u32*)(planes + 6 * kPlane + off) = prmt(c, d, 0x5410);
+  *(u32*)(planes + 7 * kPlane + off) = prmt(c, d, 0x7632);
+}
+
+__device__ __forceinline__ u32 plane_off(u32 row, u32 kbyte) {
+  return (kbyte >> 4) * kLBO + (row >> 3) * 128u + (row & 7u) * 16u + (kbyte & 15u);
+}
+
+// unit -> (piece, chunk): chunk-major over the size-sorted pieces
+__device__ __forceinline__ void unit_of(const TcArgs& a, u32 unit, uint4& pc, u32& chunk) {
+  chunk = unit / a.npieces;
+  pc = a.piece[unit % a.npieces];
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
+  extern __shared__ uint8_t dsm[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accf, acce;
+  __shared__ u32 tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 64); mbar_init(&empty[s], 1); }
+    mbar_init(&accf, 1);
+    mbar_init(&acce, 32 * kEpiWarps);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const u32 tb = tmem_base;
+
+  if (warp >= kProdWarp0) {
+    // ------------------------------------------------------------ producers
+    const int pw = warp - kProdWarp0;
+    const int pair = pw >> 1;
+    const bool giant = (pw & 1) == 0;  // L (giant steps) or R (baby steps)
+    const int tq = lane >> 2, rr = lane & 3;
+    uint8_t* planes_base = smem + (giant ? 0 : 8 * kPlane);
+    const u64 np = a.mp.np;
+    u32 it = 0;
+    for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
+      uint4 pc; u32 chunk;
+      unit_of(a, unit, pc, chunk);
+      for (int g = 0; g < kRounds; ++g) {
+        for (u32 kb = 0; kb < pc.y; ++kb, ++it) {
+          const u32 stage = it % kStages;
+          if ((int)stage != pair) continue;
+          const u32 use = it / kStages;
+          mbar_wait(&empty[stage], (use & 1) ^ 1);
+          const u64 q = (u64)pc.x + (u64)kb * kKB + (u64)tq * 4;
+          u64 x[4], sm[4], sw[4];
+          if (giant) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              x[e] = __ldg(a.S + (u64)chunk * a.t_pad + q + e);
+              const u64 bm = __ldg(a.mV + q + e), bw = __ldg(a.wV + q + e);
+              for (int r = 0; r < rr; ++r) x[e] = mul_shoup4(x[e], bm, bw, np);
+              sm[e] = __ldg(a.mV4 + q + e);
+              sw[e] = __ldg(a.wV4 + q + e);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              x[e] = 1;
+              const u64 bm = __ldg(a.m + q + e), bw = __ldg(a.w + q + e);
+              for (int r = 0; r < rr; ++r) x[e] = mul_shoup4(x[e], bm, bw, np);
+              sm[e] = __ldg(a.m4 + q + e);
+              sw[e] = __ldg(a.w4 + q + e);
+            }
+          }
+          uint8_t* planes = planes_base + stage * kStageBytes;
+#pragma unroll 1
+          for (int k = 0; k < 32; ++k) {
+            store_digits(planes, plane_off((u32)(rr + 4 * k), (u32)tq * 4), x);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] = mul_shoup4(x[e], sm[e], sw[e], np);
+          }
+          fence_async_smem();
+          mbar_arrive(&full[stage]);
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      u32 it = 0, round = 0;
+      const u32 sbase = smem_u32(smem);
+      for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
+        uint4 pc; u32 chunk;
+        unit_of(a, unit, pc, chunk);
+        for (int g = 0; g < kRounds; ++g, ++round) {
+          mbar_wait(&acce, (round & 1) ^ 1);
+          tc_fence_after();
+          for (u32 kb = 0; kb < pc.y; ++kb, ++it) {
+            const u32 stage = it % kStages, use = it / kStages;
+            mbar_wait(&full[stage], use & 1);
+            tc_fence_after();
+            const u32 st = sbase + stage * kStageBytes;
+#pragma unroll
+            for (int di = 0; di < 4; ++di) {
+              const int d = kGroups[g][di];
+              if (d < 0) continue;
+              const int s0 = d > 7 ? d - 7 : 0, s1 = d < 7 ? d : 7;
+              for (int s = s0; s <= s1; ++s)
+                mma_u8(tb + (u32)di * kV, smem_desc(st + (u32)s * kPlane),
+                       smem_desc(st + (u32)(8 + d - s) * kPlane), (kb > 0 || s > s0) ? 1u : 0u);
+            }
+            mma_commit(&empty[stage]);
+          }
+          mma_commit(&accf);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const u32 u = (u32)(warp * 32 + lane);
+    const u32 tl = tb + ((u32)(warp * 32) << 16);
+    const ModParams mp = a.mp;
+    u32 round = 0;
+    for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
+      uint4 pc; u32 chunk;
+      unit_of(a, unit, pc, chunk);
+      u64* prow = a.partial + (u64)pc.z * a.ldp;
+      const u64 kbase = (u64)chunk * kChunk + (u64)u * kV;
+      for (int g = 0; g < kRounds; ++g, ++round) {
+        mbar_wait(&accf, round & 1);
+        tc_fence_after();
+        int nd = 0;
+        u64 W[4];
+#pragma unroll
+        for (int di = 0; di < 4; ++di) {
+          const int d = kGroups[g][di];
+          W[di] = d >= 0 ? a.Wd[d] : 0;
+          nd += d >= 0;
+        }
+        for (u32 v0 = 0; v0 < (u32)kV; v0 += 8) {
+          u32 D[4][8];
+#pragma unroll
+          for (int di = 0; di < 4; ++di) {
+            if (di < nd) tmem_ld8(tl + (u32)di * kV + v0, D[di]);
+          }
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            // X = sum_d D_d * W_d < 4 * 2^31 * 2^62 (96-bit), then mod p
+            u64 lo = 0, hi = 0;
+#pragma unroll
+            for (int di = 0; di < 4; ++di) {
+              if (di < nd) {
+                const u64 w = W[di];
+                const u64 p0 = (u64)D[di][j] * lo32(w);
+                const u64 p1 = (u64)D[di][j] * hi32(w);
+                const u64 add_lo = p0 + (p1 << 32);
+                const u64 add_hi = (p1 >> 32) + (add_lo < p0 ? 1ull : 0ull);
+                lo += add_lo;
+                hi += add_hi + (lo < add_lo ? 1ull : 0ull);
+              }
+            }
+            u64 r = reduce128(hi, lo, mp);
+            const u64 k = kbase + v0 + j;
+            if (k < a.npts) {
+              if (g > 0) r = csub(r + prow[k], mp.p);
+              prow[k] = r;
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&acce);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tb));
+  }
+}
+
+// ---------------------------------------------------------------- setup kernels
+// Per padded term (pe_create): m^4, m^V, m^{4V} and their Shoup constants.
+__global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ m4, u64* __restrict__ w4,
+                           u64* __restrict__ mV, u64* __restrict__ wV, u64* __restrict__ mV4,
+                           u64* __restrict__ wV4, ModParams mp) {
+  for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
+    const u64 mm = to_mont(m[q], mp);
+    const u64 a4 = from_mont(mont_pow(mm, 4, mp), mp);
+    const u64 aV = from_mont(mont_pow(mm, kV, mp), mp);
+    const u64 aV4 = from_mont(mont_pow(mm, 4 * kV, mp), mp);
+    m4[q] = a4; w4[q] = shoup_w(a4, mp.p);
+    mV[q] = aV; wV[q] = shoup_w(aV, mp.p);
+    mV4[q] = aV4; wV4[q] = shoup_w(aV4, mp.p);
+  }
+}
+
+// Per evaluation pass: S[c][q] = c_q m_q^{js0 + c*kChunk}.
+__global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, u64 t_pad, u32 nch, u64 js0,
+                          u64* __restrict__ S, ModParams mp) {
+  const u64 total = t_pad * nch;
+  for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
+    const u64 ch = x / t_pad, q = x - ch * t_pad;
+    S[x] = seed_pow(c[q], m[q], js0 + ch * kChunk, mp);
+  }
+}
+
+}  // namespace tc
+}  // namespace pe
