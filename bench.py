@@ -13,10 +13,12 @@ value  = t*T / device time per step (max over ranks), inputs resident in HBM.
 e2e    = the same metric through the C ABI from pinned HOST inputs to a HOST result:
          pe_create (H2D of coeffs/exps/alpha + device planning + K1) + pe_eval(_device)
          + gather + D2H of the G x T result, every step.
-roofline = k_step (dominant kernel) term-points per launch / its CUDA-event launch time vs
-         the integer-pipe mulmod peak derived in DESIGN.md §Roofline (148 SMs x clock x 64
-         IMAD lanes/clk / 14 IMAD slots per 64-bit Shoup product), plus the register-resident
-         K5 ceiling of the same step measured in the same run.
+roofline = the dominant kernel.  Tensor-core path (default for config 5): k_tc's int8 tensor
+         ops per launch (128 per term-point: 64 exact byte-pair MACs) / its CUDA-event launch
+         time vs the int8 dense peak (2 x measured bf16), plus the tcgen05 i8 issue rate of the
+         same MMA shape measured in the same run.  Scalar path: k_step term-points per launch vs
+         the integer-pipe mulmod peak (148 SMs x clock x 64 IMAD lanes/clk /
+         14 IMAD slots per 64-bit Shoup product) plus the register-resident K5 ceiling.
 cpu_baseline / --impl reference = the CPU oracle (oracle/, direct definition) on a bounded
          column sample of the same workload, on this host's cores.
 """
@@ -37,6 +39,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "term-point modular evaluations/sec (62-bit p) at 1/2/4/8 B200; % mulmod roofline"
 UNIT = "term-points/s"
+OPS_PER_TP_TC = 128               # tensor-core path: 64 byte-pair MACs (2 ops each) per term-point
 IMAD_SLOTS_PER_TP = 14            # 4 low products x 1 + 5 full-width (HI/WIDE) x 2
 IMAD_LANES_PER_CLK_SM = 64        # measured IMAD lanes/clk/SM (profiles/r01_pipe_bench.jsonl)
 N_SM = 148
@@ -54,13 +57,12 @@ def peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def ncu_traffic(info):
-    """dram__bytes_read.sum + dram__bytes_write.sum per k_step launch from the committed
-    ncu --set full capture of this same bench launch (profiles/r01_kstep_summary.json)."""
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from the
+    committed ncu --set full capture of this same bench launch (profiles/r01_<kernel>_summary.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_kstep_summary.json")) as f:
-            s = json.load(f)
-        return s["traffic_bytes_per_launch"] if info and info.get("path") == "int" else None
+        with open(os.path.join(ROOT, "profiles", f"r01_{kernel}_summary.json")) as f:
+            return json.load(f)["traffic_bytes_per_launch"]
     except (OSError, KeyError, ValueError):
         return None
 
@@ -165,8 +167,9 @@ def workload_config(w, info):
            "term_points_per_step": w.t * w.T,
            "l2": "inputs larger than L2 (c, m, w: 3 x 8 B x t_padded; partials G x T)"}
     if info:
-        cfg.update({"path": info["path"], "R": info["R"], "warps": info["warps"], "t_padded": info["t_padded"],
-                    "n_slots": info["n_slots"], "G": info.get("G")})
+        cfg.update({"path": "tc" if info.get("uses_tc") else info["path"], "R": info["R"], "warps": info["warps"],
+                    "t_padded": info["t_padded"], "n_slots": info["n_slots"], "G": info.get("G"),
+                    "tc_pieces": info.get("tc_pieces")})
     return cfg
 
 
@@ -228,6 +231,7 @@ def main():
     info = ctx.info()
     info["G"] = ctx.G
     sh = ShardedEval(ctx.G, w.T, dev)
+    info["uses_tc"] = ctx.uses_tc(sh.cnt)
 
     def eval_local(j_first, cnt, out):
         ctx.eval_device(j_first, cnt, out.data_ptr(), out.shape[1], stream.cuda_stream)
@@ -257,38 +261,66 @@ def main():
     value = w.t * w.T / (ms * 1e-3)
     clocks = clk.summary()
 
-    # ---- roofline of k_step (dominant kernel)
+    # ---- roofline of the dominant kernel (k_tc on the tensor-core path, else k_step)
     pk, pk_kind = peaks()
     n_launch = max(ks["step_launches"], 1)                                 # passes x steps (rank 0)
-    step_ms = ks["step_ms"] / n_launch                                     # mean k_step launch time
+    step_ms = ks["step_ms"] / n_launch                                     # mean launch time
     launches_tp = ks["term_points"] / n_launch                             # padded term-points / launch
     algo_tp = w.t * sh.cnt * args.steps / n_launch if sh.cnt else 0        # algorithmic term-points / launch
-    achieved = algo_tp / (step_ms * 1e-3) if step_ms else 0.0
+    tp_rate = algo_tp / (step_ms * 1e-3) if step_ms else 0.0
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
-    peak = N_SM * sm_mhz * 1e6 * IMAD_LANES_PER_CLK_SM / IMAD_SLOTS_PER_TP
-    # register-resident ceiling of the same step (K5, no memory / reduction), measured now
-    k5 = None
-    try:
-        k5_ms, k5_steps, _ = pe.bench_core(pe.CORE_SHOUP4 if info["path"] == "int" else pe.CORE_FP64,
-                                           w.p, 8, N_SM * 2, 256, 4096)
-        k5 = k5_steps / (k5_ms * 1e-3)
-    except pe.PEError:
-        pass
-    roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tterm-pt/s",
-            "frac": achieved / peak if peak else None, "traffic": ncu_traffic(info),
-            "kernel": f"k_step<{info['path']},R={info['R']}>",
-            "peak_basis": (f"IMAD-pipe model (DESIGN.md Roofline): {N_SM} SMs x {sm_mhz:.0f} MHz ({pk_kind} "
-                           f"sm_max_mhz) x {IMAD_LANES_PER_CLK_SM} IMAD lanes/clk/SM / {IMAD_SLOTS_PER_TP} "
-                           "IMAD slots per 64-bit Shoup mulmod (4 low x 1 + 5 full-width x 2; measured "
-                           "IMAD 64, IMAD.HI 32 lanes/clk/SM, profiles/r01_pipe_bench.jsonl)"),
-            "frac_at_run_clock": (achieved / (peak * clocks["sm_mhz"] / sm_mhz)
-                                  if clocks.get("sm_mhz") else None),
-            "k5_register_resident_ceiling": k5 / 1e12 if k5 else None,
-            "frac_of_k5_ceiling": achieved / k5 if k5 else None,
-            "step_ms": step_ms, "fixup_ms": ks["fixup_ms"] / max(ks["step_launches"], 1),
-            "padded_term_points_per_launch": launches_tp, "term_points_per_launch": algo_tp,
-            "algorithmic_bytes_per_launch": 16 * w.t + 8 * ctx.G * sh.cnt}
-    gpu_launches = 2 * ks["step_launches"]           # k_step + k_fixup per pass (rank 0)
+    imad_peak = N_SM * sm_mhz * 1e6 * IMAD_LANES_PER_CLK_SM / IMAD_SLOTS_PER_TP
+    use_tc = ctx.uses_tc(sh.cnt)
+    if use_tc:
+        # 64 exact byte-pair multiply-accumulates per term-point: 128 int8 ops
+        ops = algo_tp * OPS_PER_TP_TC
+        achieved = ops / (step_ms * 1e-3)
+        peak = pk.get("bf16_tflops", 1590.0) * 1e12 * 2            # int8 dense = 2 x bf16 (guide nominal)
+        mma = {n: pe.bench_mma(n) for n in (64, 128)}                # same-run tcgen05 i8 issue rate
+        roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": ncu_traffic("ktc"),
+                "kernel": "k_tc (tcgen05.mma kind::i8 M=128 N=128 K=32, u8 x u8 -> s32 in TMEM)",
+                "peak_basis": (f"int8 dense tensor ops = 2 x {pk_kind} bf16_tflops "
+                               f"{pk.get('bf16_tflops', 1590.0):.1f} (guide nominal ratio 4.5/2.25 PFLOP/s); "
+                               f"sustained basis 2 x {pk.get('bf16_tflops_sustained', 1375.5):.1f}"),
+                "frac_of_sustained": achieved / (2e12 * pk.get("bf16_tflops_sustained", 1375.5)),
+                "mma_n128_ceiling": mma[128] / 1e12, "frac_of_mma_n128_ceiling": achieved / mma[128],
+                "mma_n64_ceiling": mma[64] / 1e12,
+                "term_points_per_s": tp_rate / 1e12,
+                "frac_of_imad_mulmod_roofline": tp_rate / imad_peak,
+                "imad_mulmod_roofline": imad_peak / 1e12,
+                "step_ms": step_ms, "fixup_ms": ks["fixup_ms"] / n_launch,
+                "padded_term_points_per_launch": launches_tp, "term_points_per_launch": algo_tp,
+                "int8_ops_per_launch": ops, "tc_pieces": info["tc_pieces"],
+                "algorithmic_bytes_per_launch": 16 * w.t + 8 * ctx.G * sh.cnt}
+        gpu_launches = 3 * ks["step_launches"]       # k_tc_seed + k_tc + k_fixup per pass (rank 0)
+    else:
+        achieved = tp_rate
+        peak = imad_peak
+        # register-resident ceiling of the same step (K5, no memory / reduction), measured now
+        k5 = None
+        try:
+            k5_ms, k5_steps, _ = pe.bench_core(pe.CORE_SHOUP4 if info["path"] == "int" else pe.CORE_FP64,
+                                               w.p, 8, N_SM * 2, 256, 4096)
+            k5 = k5_steps / (k5_ms * 1e-3)
+        except pe.PEError:
+            pass
+        roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tterm-pt/s",
+                "frac": achieved / peak if peak else None,
+                "traffic": ncu_traffic("kstep") if info["path"] == "int" else None,
+                "kernel": f"k_step<{info['path']},R={info['R']}>",
+                "peak_basis": (f"IMAD-pipe model (DESIGN.md Roofline): {N_SM} SMs x {sm_mhz:.0f} MHz ({pk_kind} "
+                               f"sm_max_mhz) x {IMAD_LANES_PER_CLK_SM} IMAD lanes/clk/SM / {IMAD_SLOTS_PER_TP} "
+                               "IMAD slots per 64-bit Shoup mulmod (4 low x 1 + 5 full-width x 2; measured "
+                               "IMAD 64, IMAD.HI 32 lanes/clk/SM, profiles/r01_pipe_bench.jsonl)"),
+                "frac_at_run_clock": (achieved / (peak * clocks["sm_mhz"] / sm_mhz)
+                                      if clocks.get("sm_mhz") else None),
+                "k5_register_resident_ceiling": k5 / 1e12 if k5 else None,
+                "frac_of_k5_ceiling": achieved / k5 if k5 else None,
+                "step_ms": step_ms, "fixup_ms": ks["fixup_ms"] / n_launch,
+                "padded_term_points_per_launch": launches_tp, "term_points_per_launch": algo_tp,
+                "algorithmic_bytes_per_launch": 16 * w.t + 8 * ctx.G * sh.cnt}
+        gpu_launches = 2 * ks["step_launches"]       # k_step + k_fixup per pass (rank 0)
 
     # ---- end-to-end: host inputs -> host result through the C ABI, every step
     e2e = None

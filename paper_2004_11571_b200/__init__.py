@@ -27,7 +27,7 @@ CORE_SHOUP4, CORE_SHOUP2, CORE_MONT, CORE_FP64, CORE_FP64ADD, CORE_POW, CORE_SHO
 EXPORTS = ["pe_create", "pe_create_ex", "pe_eval", "pe_eval_device", "pe_destroy", "pe_num_buckets",
            "pe_bucket_exps", "pe_info", "pe_monomials", "pe_last_error", "pe_strerror",
            "pe_interp_bound_ok", "pe_test_core", "pe_bench_core", "pe_set_timing", "pe_kernel_stats",
-           "pe_create_batch", "pe_num_polys", "pe_poly_rows", "pe_bm_device", "pe_bm", "pe_tc_info"]
+           "pe_create_batch", "pe_num_polys", "pe_poly_rows", "pe_bm_device", "pe_bm", "pe_tc_info", "pe_bench_mma"]
 
 
 class PEError(RuntimeError):
@@ -101,6 +101,9 @@ def lib():
         L.pe_bm.restype = ctypes.c_int
         L.pe_tc_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(u64), ctypes.POINTER(u64)]
         L.pe_tc_info.restype = ctypes.c_int
+        L.pe_bench_mma.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_float),
+                                   ctypes.POINTER(ctypes.c_double)]
+        L.pe_bench_mma.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -249,6 +252,13 @@ def bench_core(variant: int, p: int, R: int, blocks: int, threads: int, iters: i
     _check(lib().pe_bench_core(variant, p, R, blocks, threads, iters, ctypes.byref(ms), ctypes.byref(steps),
                                ctypes.byref(cyc)), "pe_bench_core")
     return ms.value, steps.value, cyc.value
+
+
+def bench_mma(N: int = 128, iters: int = 20000):
+    """pe_bench_mma: int8 tcgen05 MMA rate (M=128, N, K=32) -> int8 ops/s (2 per MAC)."""
+    ms, macs = ctypes.c_float(), ctypes.c_double()
+    _check(lib().pe_bench_mma(N, iters, ctypes.byref(ms), ctypes.byref(macs)), "pe_bench_mma")
+    return 2 * macs.value / (ms.value * 1e-3)
 
 
 def berlekamp_massey(p: int, seq: np.ndarray):

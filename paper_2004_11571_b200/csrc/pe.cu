@@ -121,6 +121,7 @@ struct pe_ctx {
   u32 tc_npieces = 0, tc_nslots = 0;
   int n_sm = 148;
   u64 *d_m4 = nullptr, *d_w4 = nullptr, *d_mV = nullptr, *d_wV = nullptr, *d_mV4 = nullptr, *d_wV4 = nullptr;
+  u64* d_m64 = nullptr;
   uint4* d_piece = nullptr;
   u32* d_tc_slot_start = nullptr;
   u64* d_seed = nullptr;
@@ -145,7 +146,7 @@ static void free_all(pe_ctx* h) {
   for (void* q : {(void*)h->d_c, (void*)h->d_m, (void*)h->d_w, (void*)h->d_perm, (void*)h->d_ms, (void*)h->d_mpd,
                   (void*)h->d_mspd, (void*)h->d_wt_info, (void*)h->d_slot_start, (void*)h->d_partial,
                   (void*)h->d_out_scratch, (void*)h->d_m4, (void*)h->d_w4, (void*)h->d_mV, (void*)h->d_wV,
-                  (void*)h->d_mV4, (void*)h->d_wV4, (void*)h->d_piece, (void*)h->d_tc_slot_start,
+                  (void*)h->d_mV4, (void*)h->d_wV4, (void*)h->d_m64, (void*)h->d_piece, (void*)h->d_tc_slot_start,
                   (void*)h->d_seed})
     if (q) cudaFreeAsync(q, s);
   if (s) cudaStreamSynchronize(s);
@@ -416,10 +417,10 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   if (h->tc_mode != 0 && h->path == kInt4) {
     const u64 tp = h->t_pad;
     if (dalloc(&h->d_m4, tp) || dalloc(&h->d_w4, tp) || dalloc(&h->d_mV, tp) || dalloc(&h->d_wV, tp) ||
-        dalloc(&h->d_mV4, tp) || dalloc(&h->d_wV4, tp))
+        dalloc(&h->d_mV4, tp) || dalloc(&h->d_wV4, tp) || dalloc(&h->d_m64, tp))
       return g_last_error;
     tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_m4, h->d_w4, h->d_mV, h->d_wV, h->d_mV4,
-                                                     h->d_wV4, h->mp);
+                                                     h->d_wV4, h->d_m64, h->mp);
     CU(cudaGetLastError());
     // pieces: each bucket's padded range split into ceil(n / kPieceMax) near-equal runs of whole
     // K-blocks (<= kPieceMax terms keeps every int32 diagonal sum exact); slots contiguous per bucket
@@ -594,23 +595,23 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
   Tp = std::min<u64>(Tp, (u64)tc::kChunk * 4096);
   if (ensure_partial(h, (size_t)nslots * std::min<u64>(Tp, T), s)) return g_last_error;
   const u32 nch_max = (u32)(Tp / tc::kChunk);
-  if ((size_t)h->t_pad * nch_max > h->seed_elems) {
+  if ((size_t)h->t_pad * nch_max * 2 > h->seed_elems) {
     if (h->d_seed) cudaFreeAsync(h->d_seed, s);
     h->d_seed = nullptr;
     h->seed_elems = 0;
-    CU(cudaMallocAsync((void**)&h->d_seed, (size_t)h->t_pad * nch_max * sizeof(u64), s));
-    h->seed_elems = (size_t)h->t_pad * nch_max;
+    CU(cudaMallocAsync((void**)&h->d_seed, (size_t)h->t_pad * nch_max * 2 * sizeof(u64), s));
+    h->seed_elems = (size_t)h->t_pad * nch_max * 2;
   }
   CU(cudaFuncSetAttribute(tc::k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
     const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
-    tc::k_tc_seed<<<grid_for((u64)h->t_pad * nch, 256), 256, 0, s>>>(h->d_c, h->d_m, h->t_pad, nch, j0 + k0,
+    tc::k_tc_seed<<<grid_for((u64)h->t_pad * nch * 2, 256), 256, 0, s>>>(h->d_c, h->d_m, h->t_pad, nch, j0 + k0,
                                                                       h->d_seed, h->mp);
     CU(cudaGetLastError());
     tc::TcArgs a;
     a.S = h->d_seed;
-    a.m = h->d_m; a.w = h->d_w; a.m4 = h->d_m4; a.w4 = h->d_w4;
+    a.m = h->d_m; a.w = h->d_w; a.m64 = h->d_m64; a.m4 = h->d_m4; a.w4 = h->d_w4;
     a.mV = h->d_mV; a.wV = h->d_wV; a.mV4 = h->d_mV4; a.wV4 = h->d_wV4;
     a.piece = h->d_piece;
     a.partial = h->d_partial;

@@ -7,6 +7,7 @@
 #include "../../include/pe.h"
 #include "../../include/pe_test.h"
 #include "kernels.cuh"
+#include "tc.cuh"
 
 using namespace pe;
 
@@ -262,5 +263,77 @@ extern "C" int pe_bench_core(int variant, uint64_t p, int R, int blocks, int thr
   cudaEventDestroy(e1);
   cudaFree(sink);
   cudaFree(cyc);
+  return rc;
+}
+
+// ---------------------------------------------------------------- int8 tcgen05 issue-rate probe
+// One CTA per SM issues `iters` M=128 x N x K=32 kind::i8 MMAs (u8 x u8 -> s32) from a fixed
+// shared-memory tile into 4 rotating TMEM accumulators: the same-run tensor ceiling that
+// bench.py quotes beside k_tc (the tc.cuh MMA shape is N = 128).
+__global__ void k_bench_mma(int iters, u32 idesc, u32 ncols) {
+  extern __shared__ uint8_t dsm[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ u32 tmem_base;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 2 * (int)tc::kPlane; i += blockDim.x) sm[i] = (uint8_t)(i * 13);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(tc::smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::fence_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const u32 tb = tmem_base;
+  if (threadIdx.x == 0) {
+    const uint64_t ad = tc::smem_desc(tc::smem_u32(sm)), bd = tc::smem_desc(tc::smem_u32(sm) + tc::kPlane);
+    for (int it = 0; it < iters; ++it)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "setp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
+          :: "r"(tb + (u32)(it & 3) * ncols), "l"(ad), "l"(bd), "r"(idesc), "r"(1u));
+    tc::mma_commit(&bar);
+  }
+  tc::mbar_wait(&bar, 0);
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tb));
+  }
+}
+
+extern "C" int pe_bench_mma(int N, int iters, float* ms, double* macs) {
+  if ((N != 64 && N != 128) || iters < 1 || !ms || !macs) return PE_EINVAL;
+  int dev = 0, nsm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return PE_ECUDA;
+  const u32 idesc = (2u << 4) | ((u32)(N >> 3) << 17) | ((u32)(128 >> 4) << 24);
+  const int smem = 2 * tc::kPlane + 1024;
+  if (cudaFuncSetAttribute(k_bench_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return PE_ECUDA;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
+    cudaEventRecord(e0);
+    k_bench_mma<<<nsm, 128, smem>>>(iters, idesc, (u32)N);
+    cudaEventRecord(e1);
+  }
+  int rc = PE_OK;
+  if (cudaGetLastError() != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess) rc = PE_ECUDA;
+  if (rc == PE_OK) {
+    cudaEventElapsedTime(ms, e0, e1);
+    *macs = (double)nsm * iters * 128.0 * N * 32.0;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   return rc;
 }

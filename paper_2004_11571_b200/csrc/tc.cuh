@@ -28,10 +28,10 @@
 //   warps 0-3  epilogue: tcgen05.ld the round's diagonals (TMEM lane = u), combine mod p,
 //              accumulate into partial[slot][chunk*16384 + u*128 + v]
 //   warp  4    TMEM allocator + single-thread MMA issuer (tcgen05.mma.cta_group::1.kind::i8)
-//   warps 5-10 producers, 3 pairs (one per smem stage): the L warp and the R warp of a pair
-//              generate one K-block's 128 giant-step / 128 baby-step values of 32 terms with
-//              Shoup products (4 chains per lane) and write their 8 byte planes in the
-//              no-swizzle K-major UMMA layout.
+//   warps 5-16 producers, 4 per smem stage: two L warps and two R warps generate one K-block's
+//              128 giant-step / 128 baby-step values of 32 terms (64 rows each) with Shoup
+//              products (4 chains per lane) and write their 8 byte planes in the no-swizzle
+//              K-major UMMA layout.
 #pragma once
 #include "modcore.cuh"
 
@@ -49,15 +49,17 @@ constexpr u32 kPlane = 2 * kLBO;          // one digit plane: 128 rows x 32 byte
 constexpr u32 kStageBytes = 16 * kPlane;  // 8 L planes + 8 R planes
 constexpr u32 kSmemBytes = kStages * kStageBytes + 1024;
 constexpr int kRounds = 4;
-constexpr int kThreads = 11 * 32;
+constexpr int kProdPerStage = 4;          // L rows 0-63, L rows 64-127, R rows 0-63, R rows 64-127
 constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5;
+constexpr int kThreads = (kProdWarp0 + kStages * kProdPerStage) * 32;
 // diagonal groups: <= 4 diagonals (TMEM: 4 x 128 columns), 16 digit pairs each
 __device__ __constant__ const signed char kGroups[kRounds][4] = {
     {7, 6, 0, -1}, {8, 5, 1, 14}, {9, 4, 2, 13}, {10, 3, 11, 12}};
 
 struct TcArgs {
-  const u64* S;     // [nch][t_pad] c_i m_i^{j_s(chunk)} mod p (chunk seeds)
+  const u64* S;     // [nch][2][t_pad] c_i m_i^{j_s(chunk)} and c_i m_i^{j_s(chunk) + 64V} (chunk seeds)
   const u64 *m, *w;      // m_i, Shoup w(m_i)            (baby-step seeds)
+  const u64* m64;        // m_i^64                        (baby-step seed of rows 64..127)
   const u64 *m4, *w4;    // m_i^4                         (baby-step stride 4)
   const u64 *mV, *wV;    // m_i^V                         (giant-step seeds)
   const u64 *mV4, *wV4;  // m_i^{4V}                      (giant-step stride 4)
@@ -132,21 +134,24 @@ __device__ __forceinline__ u32 prmt(u32 a, u32 b, u32 sel) {
 
 // Byte-transpose 4 values (terms tq*4 + e, e < 4) into 8 digit-plane words (word s = byte s of
 // each value, value e in byte e = K position) and store them at row `row` of the stage.
-__device__ __forceinline__ void store_digits(uint8_t* planes, u32 off, const u64 (&x)[4]) {
+__device__ __forceinline__ void sts32(u32 addr, u32 v) {
+  asm volatile("st.shared.b32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void store_digits(u32 planes, const u64 (&x)[4]) {
   const u32 l0 = lo32(x[0]), l1 = lo32(x[1]), l2 = lo32(x[2]), l3 = lo32(x[3]);
   const u32 h0 = hi32(x[0]), h1 = hi32(x[1]), h2 = hi32(x[2]), h3 = hi32(x[3]);
   u32 a = prmt(l0, l1, 0x5140), b = prmt(l2, l3, 0x5140);
   u32 c = prmt(l0, l1, 0x7362), d = prmt(l2, l3, 0x7362);
-  *(u32*)(planes + 0 * kPlane + off) = prmt(a, b, 0x5410);
-  *(u32*)(planes + 1 * kPlane + off) = prmt(a, b, 0x7632);
-  *(u32*)(planes + 2 * kPlane + off) = prmt(c, d, 0x5410);
-  *(u32*)(planes + 3 * kPlane + off) = prmt(c, d, 0x7632);
+  sts32(planes + 0 * kPlane, prmt(a, b, 0x5410));
+  sts32(planes + 1 * kPlane, prmt(a, b, 0x7632));
+  sts32(planes + 2 * kPlane, prmt(c, d, 0x5410));
+  sts32(planes + 3 * kPlane, prmt(c, d, 0x7632));
   a = prmt(h0, h1, 0x5140); b = prmt(h2, h3, 0x5140);
   c = prmt(h0, h1, 0x7362); d = prmt(h2, h3, 0x7362);
-  *(u32*)(planes + 4 * kPlane + off) = prmt(a, b, 0x5410);
-  *(u32*)(planes + 5 * kPlane + off) = prmt(a, b, 0x7632);
-  *(u32*)(planes + 6 * kPlane + off) = prmt(c, d, 0x5410);
-  *(u32*)(planes + 7 * kPlane + off) = prmt(c, d, 0x7632);
+  sts32(planes + 4 * kPlane, prmt(a, b, 0x5410));
+  sts32(planes + 5 * kPlane, prmt(a, b, 0x7632));
+  sts32(planes + 6 * kPlane, prmt(c, d, 0x5410));
+  sts32(planes + 7 * kPlane, prmt(c, d, 0x7632));
 }
 
 __device__ __forceinline__ u32 plane_off(u32 row, u32 kbyte) {
@@ -159,7 +164,7 @@ __device__ __forceinline__ void unit_of(const TcArgs& a, u32 unit, uint4& pc, u3
   pc = a.piece[unit % a.npieces];
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
+static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
   extern __shared__ uint8_t dsm[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accf, acce;
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 64); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 32 * kProdPerStage); mbar_init(&empty[s], 1); }
     mbar_init(&accf, 1);
     mbar_init(&acce, 32 * kEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -183,28 +188,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
 
   if (warp >= kProdWarp0) {
     // ------------------------------------------------------------ producers
+    // 4 warps per stage: (giant | baby) x (rows 0-63 | rows 64-127).  Lane = (tq, rr): terms
+    // tq*4 .. tq*4+3 of the K-block, rows half*64 + rr + 4k (k < 16), i.e. 4 independent
+    // Shoup chains of stride 4 per lane.
     const int pw = warp - kProdWarp0;
-    const int pair = pw >> 1;
-    const bool giant = (pw & 1) == 0;  // L (giant steps) or R (baby steps)
+    const int my_stage = pw / kProdPerStage, sub = pw % kProdPerStage;
+    const bool giant = sub < 2;
+    const u32 half = (u32)(sub & 1);
     const int tq = lane >> 2, rr = lane & 3;
-    uint8_t* planes_base = smem + (giant ? 0 : 8 * kPlane);
+    const u32 planes0 = smem_u32(smem) + (giant ? 0u : 8u * kPlane) + (u32)my_stage * kStageBytes +
+                        plane_off(half * 64 + (u32)rr, (u32)tq * 4);
     const u64 np = a.mp.np;
     u32 it = 0;
     for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
       uint4 pc; u32 chunk;
       unit_of(a, unit, pc, chunk);
+      const u64* Sx = a.S + ((u64)chunk * 2 + half) * a.t_pad;
       for (int g = 0; g < kRounds; ++g) {
         for (u32 kb = 0; kb < pc.y; ++kb, ++it) {
           const u32 stage = it % kStages;
-          if ((int)stage != pair) continue;
+          if ((int)stage != my_stage) continue;
           const u32 use = it / kStages;
-          mbar_wait(&empty[stage], (use & 1) ^ 1);
           const u64 q = (u64)pc.x + (u64)kb * kKB + (u64)tq * 4;
           u64 x[4], sm[4], sw[4];
           if (giant) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              x[e] = __ldg(a.S + (u64)chunk * a.t_pad + q + e);
+              x[e] = __ldg(Sx + q + e);
               const u64 bm = __ldg(a.mV + q + e), bw = __ldg(a.wV + q + e);
               for (int r = 0; r < rr; ++r) x[e] = mul_shoup4(x[e], bm, bw, np);
               sm[e] = __ldg(a.mV4 + q + e);
@@ -213,17 +223,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
           } else {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              x[e] = 1;
+              x[e] = half ? __ldg(a.m64 + q + e) : 1ull;
               const u64 bm = __ldg(a.m + q + e), bw = __ldg(a.w + q + e);
               for (int r = 0; r < rr; ++r) x[e] = mul_shoup4(x[e], bm, bw, np);
               sm[e] = __ldg(a.m4 + q + e);
               sw[e] = __ldg(a.w4 + q + e);
             }
           }
-          uint8_t* planes = planes_base + stage * kStageBytes;
-#pragma unroll 1
-          for (int k = 0; k < 32; ++k) {
-            store_digits(planes, plane_off((u32)(rr + 4 * k), (u32)tq * 4), x);
+          mbar_wait(&empty[stage], (use & 1) ^ 1);
+#pragma unroll 2
+          for (int k = 0; k < 16; ++k) {
+            // row half*64 + rr + 4k: +4 rows = +64 bytes inside the same 8-row core-matrix pair
+            store_digits(planes0 + (u32)(k >> 1) * 128u + (u32)(k & 1) * 64u, x);
 #pragma unroll
             for (int e = 0; e < 4; ++e) x[e] = mul_shoup4(x[e], sm[e], sw[e], np);
           }
@@ -332,27 +343,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
 
 // ---------------------------------------------------------------- setup kernels
 // Per padded term (pe_create): m^4, m^V, m^{4V} and their Shoup constants.
-__global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ m4, u64* __restrict__ w4,
+static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ m4, u64* __restrict__ w4,
                            u64* __restrict__ mV, u64* __restrict__ wV, u64* __restrict__ mV4,
-                           u64* __restrict__ wV4, ModParams mp) {
+                           u64* __restrict__ wV4, u64* __restrict__ m64, ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
     const u64 mm = to_mont(m[q], mp);
     const u64 a4 = from_mont(mont_pow(mm, 4, mp), mp);
     const u64 aV = from_mont(mont_pow(mm, kV, mp), mp);
     const u64 aV4 = from_mont(mont_pow(mm, 4 * kV, mp), mp);
+    m64[q] = from_mont(mont_pow(mm, 64, mp), mp);
     m4[q] = a4; w4[q] = shoup_w(a4, mp.p);
     mV[q] = aV; wV[q] = shoup_w(aV, mp.p);
     mV4[q] = aV4; wV4[q] = shoup_w(aV4, mp.p);
   }
 }
 
-// Per evaluation pass: S[c][q] = c_q m_q^{js0 + c*kChunk}.
-__global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, u64 t_pad, u32 nch, u64 js0,
+// Per evaluation pass: S[c][h][q] = c_q m_q^{js0 + c*kChunk + h*64V}, h = 0, 1 (the giant-step
+// seeds of rows 0 and 64 of chunk c).
+static __global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, u64 t_pad, u32 nch, u64 js0,
                           u64* __restrict__ S, ModParams mp) {
-  const u64 total = t_pad * nch;
+  const u64 total = t_pad * nch * 2;
   for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
-    const u64 ch = x / t_pad, q = x - ch * t_pad;
-    S[x] = seed_pow(c[q], m[q], js0 + ch * kChunk, mp);
+    const u64 ch = x / t_pad, q = x - ch * t_pad;   // ch = 2 * chunk + h
+    S[x] = seed_pow(c[q], m[q], js0 + (ch >> 1) * kChunk + (ch & 1) * (64ull * kV), mp);
   }
 }
 

@@ -62,11 +62,14 @@ def test_config4_fp64_equals_int_equals_mix():
     assert np.array_equal(a[:, 0:512:37], ref)
 
 
-def test_config5_sampled_and_edges():
-    """Full size (t = 10^7, T = 16384, the bench launch configuration): 8 columns against the
-    direct oracle, and the first/last 64 columns against the incremental checker."""
+@pytest.mark.parametrize("path", [pe.PATH_AUTO, pe.PATH_INT])
+def test_config5_sampled_and_edges(path):
+    """Full size (t = 10^7, T = 16384, the bench launch configuration: PATH_AUTO = the tensor-core
+    k_tc; PATH_INT = the scalar k_step): 8 columns against the direct oracle, and the first/last
+    64 columns against the incremental checker."""
     w = synth.gen_config(5)
-    with pe.Context.from_workload(w) as ctx:
+    with pe.Context.from_workload(w, path=path) as ctx:
+        assert ctx.uses_tc(w.T) == (path == pe.PATH_AUTO)
         out = ctx.eval(w.j0, w.T)
         rows = ctx.buckets()
     assert rows.tolist() == oracle.buckets(w.exps, w.n).tolist()

@@ -1,0 +1,150 @@
+"""GPU parity of the tensor-core path (PE_PATH_TC, csrc/tc.cuh) against the CPU oracle through
+the C ABI.  The path factors each bucket's 128 x 128-point chunk into giant-step x baby-step
+values (the Vandermonde structure m_i^{j} = m_i^{j_s + 128u} m_i^{v}) and sums
+their 64 byte-pair products on int8 tensor cores; results must be bit-identical to the oracle
+(canonical residues are unique, R14)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2004_11571_b200 as pe
+import synth
+
+pytestmark = pytest.mark.gpu
+
+P62 = synth.P62
+
+
+def tc_eval(w, j0=None, T=None, path=pe.PATH_TC):
+    with pe.Context.from_workload(w, path=path) as ctx:
+        T = w.T if T is None else T
+        assert ctx.uses_tc(T), ctx.info()
+        out = ctx.eval(w.j0 if j0 is None else j0, T)
+        rows = ctx.buckets()
+    return rows, out
+
+
+def check_tc(w, **kw):
+    rows, out = tc_eval(w, **kw)
+    assert rows.tolist() == oracle.buckets(w.exps, w.n).tolist()
+    ref = oracle.eval_workload(w)
+    bad = np.argwhere(out != ref)
+    assert bad.size == 0, f"{len(bad)} mismatches, first {bad[:5].tolist()}"
+
+
+@pytest.mark.parametrize("p,n,t,maxdeg,j0,T", [
+    (P62, 6, 300, 4, 1, 1),               # T = 1 (one column of a 16384-point chunk)
+    (P62, 6, 300, 4, 1, 129),             # ragged inside the first chunk (u = 1, v = 0)
+    (P62, 5, 500, 3, 0, 70),              # j0 = 0
+    (P62, 5, 200, 3, 2**64 - 40, 40),     # largest j range (seed exponents near 2^64)
+    (13, 4, 60, 3, 0, 50),                # tiny prime
+    (3, 5, 40, 2, 5, 20),                 # smallest prime
+    ((1 << 62) - 57, 2, 30, 6, 1, 10),    # n = 2 (m = 1: every column = coefficient sums)
+    (2**31 - 1, 3, 100, 9, 1, 64),        # n = 3, 31-bit p through the 64-bit tensor path
+    ((1 << 50) - 27, 7, 600, 4, 3, 77),   # 50-bit p (auto would take FP64 Alg. 2)
+])
+def test_tc_edge_shapes(p, n, t, maxdeg, j0, T):
+    w = synth.random_small(500 + t + n, p, n, t, maxdeg, T, j0, coeff_hi=2**64 - 1)
+    check_tc(w)
+
+
+def test_tc_two_chunks_and_tail():
+    """T = 2 x 16384 + 1000: three chunks (seeds at j0, j0 + 16384, j0 + 32768), ragged tail."""
+    w = synth.random_small(520, P62, 6, 2000, 4, 2 * 16384 + 1000, 7)
+    _, out = tc_eval(w)
+    ref = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
+    assert np.array_equal(out, ref)
+
+
+def test_tc_config1_and_config2_full():
+    check_tc(synth.gen_config(1))
+    check_tc(synth.gen_config(2))
+
+
+def test_tc_pieces_of_one_large_bucket():
+    """One (x,y) bucket of 20 000 terms: 5 accumulation pieces (<= 4096 terms each, the int32
+    exactness bound of DESIGN.md §7) summed by the fix-up; plus a 1-term and a 33-term bucket."""
+    w = synth.random_small(521, P62, 8, 20_034, 5, 300, 1)
+    w.exps[:, :2] = 4
+    w.exps[0, :2] = (9, 9)
+    w.exps[1:34, :2] = (0, 1)
+    with pe.Context.from_workload(w, path=pe.PATH_TC) as ctx:
+        assert ctx.info()["tc_pieces"] >= 7
+    _, out = tc_eval(w)
+    ref = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
+    assert np.array_equal(out, ref)
+    ks = np.array([0, 1, 127, 128, 299], np.uint64)
+    assert np.array_equal(out[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
+
+
+def test_tc_config3_full_incremental():
+    w = synth.gen_config(3)
+    _, out = tc_eval(w)
+    inc = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
+    assert np.array_equal(out, inc)
+
+
+def test_tc_multi_pass_partial_cap(monkeypatch):
+    """PE_PARTIAL_MB=1: the partial buffer holds one chunk, so T = 40000 runs as 3 passes."""
+    monkeypatch.setenv("PE_PARTIAL_MB", "1")
+    w = synth.random_small(522, P62, 5, 900, 4, 40_000, 2)
+    _, out = tc_eval(w)
+    ref = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
+    assert np.array_equal(out, ref)
+
+
+def test_tc_duplicates_zero_coeffs_alpha_ge_p():
+    w = synth.random_small(523, P62, 5, 400, 2, 50, 1, dup=True)
+    w.coeffs[::7] = 0
+    w.coeffs[1::11] = np.uint64(P62 + 5)
+    w.alpha = (w.alpha + np.uint64(P62)).astype(np.uint64)
+    check_tc(w)
+
+
+def test_tc_equals_scalar_step_and_fermat():
+    """The tensor path equals k_step on the same inputs (P13), and is Fermat-periodic (P5)."""
+    w = synth.gen_config(2, t=30_000, T=20_000)
+    _, a = tc_eval(w)
+    with pe.Context.from_workload(w, path=pe.PATH_INT) as ctx:
+        assert not ctx.uses_tc(w.T)
+        b = ctx.eval(w.j0, w.T)
+    assert np.array_equal(a, b)
+    _, c = tc_eval(w, j0=w.j0 + (w.p - 1))
+    assert np.array_equal(a, c)
+
+
+def test_tc_auto_selection():
+    """PE_PATH_AUTO: tensor path for 2^50 <= p < 2^62 and T >= 8192; never for p >= 2^62, p < 2^50
+    or PE_PATH_INT; PE_PATH_TC with p >= 2^62 is PE_ENOTSUP."""
+    w = synth.random_small(524, P62, 5, 100, 3, 10, 1)
+    with pe.Context.from_workload(w) as ctx:
+        assert ctx.uses_tc(8192) and not ctx.uses_tc(8191)
+    with pe.Context.from_workload(w, path=pe.PATH_INT) as ctx:
+        assert not ctx.uses_tc(10**6)
+    w50 = synth.random_small(525, (1 << 50) - 27, 5, 100, 3, 10, 1)
+    with pe.Context.from_workload(w50) as ctx:
+        assert ctx.info()["path"] == "fp64" and not ctx.uses_tc(10**6)
+    w63 = synth.random_small(526, (1 << 63) - 25, 5, 100, 3, 10, 1)
+    with pe.Context.from_workload(w63) as ctx:
+        assert not ctx.uses_tc(10**6)
+    with pytest.raises(pe.PEError) as ei:
+        pe.Context.from_workload(w63, path=pe.PATH_TC)
+    assert ei.value.code == pe.PE_ENOTSUP
+
+
+def test_tc_batch_polys():
+    """pe_create_batch through the tensor path: f and h of config-2 shape at the same points."""
+    f = synth.gen_config(2, t=20_000, T=300)
+    h = synth.gen_config(2, t=20_000, T=300, seed=77)
+    with pe.Context.batch(f.p, [(f.coeffs, f.exps), (h.coeffs, h.exps)], f.alpha, f.n,
+                          path=pe.PATH_TC) as ctx:
+        assert ctx.uses_tc(f.T)
+        ro = ctx.poly_rows().astype(np.int64)
+        out = ctx.eval(f.j0, f.T)
+    assert np.array_equal(out[ro[0]:ro[1]], oracle.eval_incremental(f.p, f.n, f.coeffs, f.exps, f.alpha, f.j0, f.T))
+    assert np.array_equal(out[ro[1]:ro[2]], oracle.eval_incremental(f.p, f.n, h.coeffs, h.exps, f.alpha, f.j0, f.T))
+
+
+def test_mma_probe_rate():
+    """pe_bench_mma runs and reports a plausible int8 rate (> 100 TOPS at N = 128)."""
+    assert pe.bench_mma(128, 4000) > 1e14
