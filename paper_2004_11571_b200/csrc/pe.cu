@@ -126,6 +126,7 @@ struct pe_ctx {
   u32* d_tc_slot_start = nullptr;
   u64* d_seed = nullptr;
   size_t seed_elems = 0;
+  u32* d_tc_scratch = nullptr;   // k_tc per-CTA 160-bit running sums (n_sm x 5 x 16384 u32)
   size_t partial_cap_bytes = (size_t)1 << 30;
   // kernel timing (pe_set_timing / pe_kernel_stats)
   bool timing = false;
@@ -146,7 +147,7 @@ static void free_all(pe_ctx* h) {
   for (void* q : {(void*)h->d_c, (void*)h->d_m, (void*)h->d_w, (void*)h->d_perm, (void*)h->d_ms, (void*)h->d_mpd,
                   (void*)h->d_mspd, (void*)h->d_wt_info, (void*)h->d_slot_start, (void*)h->d_partial,
                   (void*)h->d_out_scratch, (void*)h->d_m4, (void*)h->d_w4, (void*)h->d_mV, (void*)h->d_wV,
-                  (void*)h->d_mV4, (void*)h->d_wV4, (void*)h->d_m64, (void*)h->d_piece, (void*)h->d_tc_slot_start,
+                  (void*)h->d_mV4, (void*)h->d_wV4, (void*)h->d_m64, (void*)h->d_tc_scratch, (void*)h->d_piece, (void*)h->d_tc_slot_start,
                   (void*)h->d_seed})
     if (q) cudaFreeAsync(q, s);
   if (s) cudaStreamSynchronize(s);
@@ -593,7 +594,8 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
   Tp = std::max<u64>(Tp, tc::kChunk);
   Tp = std::min<u64>(Tp, (T + tc::kChunk - 1) / tc::kChunk * tc::kChunk);
   Tp = std::min<u64>(Tp, (u64)tc::kChunk * 4096);
-  if (ensure_partial(h, (size_t)nslots * std::min<u64>(Tp, T), s)) return g_last_error;
+  // partial rows padded to a multiple of 8 points (the epilogue's 64-byte vector accesses)
+  if (ensure_partial(h, (size_t)nslots * ((std::min<u64>(Tp, T) + 7) / 8 * 8), s)) return g_last_error;
   const u32 nch_max = (u32)(Tp / tc::kChunk);
   if ((size_t)h->t_pad * nch_max * 2 > h->seed_elems) {
     if (h->d_seed) cudaFreeAsync(h->d_seed, s);
@@ -602,7 +604,9 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     CU(cudaMallocAsync((void**)&h->d_seed, (size_t)h->t_pad * nch_max * 2 * sizeof(u64), s));
     h->seed_elems = (size_t)h->t_pad * nch_max * 2;
   }
-  CU(cudaFuncSetAttribute(tc::k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
+  if (!h->d_tc_scratch) CU(cudaMallocAsync((void**)&h->d_tc_scratch, (size_t)h->n_sm * 5 * tc::kChunk * sizeof(u32), s));
+  CU(cudaFuncSetAttribute(tc::k_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
+  CU(cudaFuncSetAttribute(tc::k_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
     const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
@@ -615,13 +619,16 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     a.mV = h->d_mV; a.wV = h->d_wV; a.mV4 = h->d_mV4; a.wV4 = h->d_wV4;
     a.piece = h->d_piece;
     a.partial = h->d_partial;
-    a.ldp = np;
+    a.ldp = (np + 7) / 8 * 8;
     a.t_pad = h->t_pad;
     a.npieces = h->tc_npieces;
     a.nunits = h->tc_npieces * nch;
     a.npts = np;
     for (int d = 0; d < 15; ++d) a.Wd[d] = h_powmod(2, 8 * (u64)d, h->p);
+    a.C128 = h_powmod(2, 128, h->p);
+    a.scratch = h->d_tc_scratch;
     a.mp = h->mp;
+    a.prof = nullptr;
     const unsigned grid = (unsigned)std::min<u64>(a.nunits, (u64)h->n_sm);
     pe_ctx::Rec rec{};
     if (h->timing) {
@@ -631,11 +638,34 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
       rec.tp = (double)h->t_pad * np;
       CU(cudaEventRecord(rec.e0, s));
     }
-    tc::k_tc<<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
+    unsigned long long* d_prof = nullptr;
+    const size_t nprof = (size_t)grid * (tc::kThreads / 32) * 5;
+    a.prof = nullptr;
+    if (env_int("PE_TC_PROF", 0)) {   // development: per-warp phase timers printed to stderr
+      CU(cudaMalloc(&d_prof, nprof * sizeof(unsigned long long)));
+      CU(cudaMemset(d_prof, 0, nprof * sizeof(unsigned long long)));
+      a.prof = d_prof;
+    }
+    if (d_prof) tc::k_tc<true><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
+    else tc::k_tc<false><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
     CU(cudaGetLastError());
+    if (d_prof) {
+      std::vector<unsigned long long> hp(nprof);
+      CU(cudaMemcpyAsync(hp.data(), d_prof, nprof * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+      cudaFree(d_prof);
+      const int nw = tc::kThreads / 32;
+      for (int wv = 0; wv < nw; ++wv) {
+        double acc[5] = {0, 0, 0, 0, 0};
+        for (unsigned b = 0; b < grid; ++b)
+          for (int i = 0; i < 5; ++i) acc[i] += (double)hp[((size_t)b * nw + wv) * 5 + i] / grid;
+        fprintf(stderr, "tcprof warp %2d: t0 %.0f t1 %.0f t2 %.0f n %.0f total %.0f\n", wv, acc[0], acc[1], acc[2],
+                acc[3], acc[4]);
+      }
+    }
     if (h->timing) CU(cudaEventRecord(rec.e1, s));
     const u32 nkb = (np + 255) / 256;
-    k_fixup<<<(unsigned)(h->G * nkb), 256, 0, s>>>(h->d_partial, np, h->d_tc_slot_start, (u32)h->G, np, nkb,
+    k_fixup<<<(unsigned)(h->G * nkb), 256, 0, s>>>(h->d_partial, a.ldp, h->d_tc_slot_start, (u32)h->G, np, nkb,
                                                    d_out + k0, ld, h->mp);
     CU(cudaGetLastError());
     if (h->timing) {

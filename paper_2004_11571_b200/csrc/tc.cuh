@@ -25,8 +25,9 @@
 // costs 2x the N = 256 MACs/clk but balances the IMAD-bound generation.
 //
 // Warp roles (one CTA per SM, persistent, static round-robin over units = (piece, chunk)):
-//   warps 0-3  epilogue: tcgen05.ld the round's diagonals (TMEM lane = u), combine mod p,
-//              accumulate into partial[slot][chunk*16384 + u*128 + v]
+//   warps 0-3  epilogue: tcgen05.ld the round's diagonals (TMEM lane = u), fold them exactly into
+//              160-bit running sums (shift/add, per-CTA L2-resident scratch), release TMEM; after
+//              the unit's last round one reduction mod p per point -> partial[slot][chunk*16384 + u*128 + v]
 //   warp  4    TMEM allocator + single-thread MMA issuer (tcgen05.mma.cta_group::1.kind::i8)
 //   warps 5-16 producers, 4 per smem stage: two L warps and two R warps generate one K-block's
 //              128 giant-step / 128 baby-step values of 32 terms (64 rows each) with Shoup
@@ -47,12 +48,24 @@ constexpr u32 kPieceMax = 4096;           // terms per accumulation: 4096 * 8 * 
 constexpr u32 kLBO = 2048 + 64;           // bytes between the two 16-byte K chunks of a plane (+64: bank spread)
 constexpr u32 kPlane = 2 * kLBO;          // one digit plane: 128 rows x 32 bytes (+ pad)
 constexpr u32 kStageBytes = 16 * kPlane;  // 8 L planes + 8 R planes
-constexpr u32 kSmemBytes = kStages * kStageBytes + 1024;
+// per-K-block term data streamed by the loader warp (TMA bulk copies): 11 arrays x 32 terms
+enum { kD_S0 = 0, kD_S1, kD_mV, kD_wV, kD_mV4, kD_wV4, kD_m, kD_w, kD_m4, kD_w4, kD_m64, kD_N };
+constexpr u32 kDataArr = kKB * 8;               // 256 B per array per K-block
+constexpr u32 kDataSlot = kD_N * kDataArr;      // 2816 B
+constexpr int kDataSlots = 2 * kStages;         // ring depth (2 K-blocks ahead per producer group)
+constexpr u32 kSmemBytes = kStages * kStageBytes + kDataSlots * kDataSlot + 1024;
 constexpr int kRounds = 4;
 constexpr int kProdPerStage = 4;          // L rows 0-63, L rows 64-127, R rows 0-63, R rows 64-127
 constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5;
-constexpr int kThreads = (kProdWarp0 + kStages * kProdPerStage) * 32;
+constexpr int kLoadWarp = kProdWarp0 + kStages * kProdPerStage;
+constexpr int kThreads = (kLoadWarp + 1) * 32;
 // diagonal groups: <= 4 diagonals (TMEM: 4 x 128 columns), 16 digit pairs each
+__host__ __device__ constexpr int group_diag(int g, int di) {
+  return g == 0 ? (di == 0 ? 7 : di == 1 ? 6 : di == 2 ? 0 : -1)
+       : g == 1 ? (di == 0 ? 8 : di == 1 ? 5 : di == 2 ? 1 : 14)
+       : g == 2 ? (di == 0 ? 9 : di == 1 ? 4 : di == 2 ? 2 : 13)
+                : (di == 0 ? 10 : di == 1 ? 3 : di == 2 ? 11 : 12);
+}
 __device__ __constant__ const signed char kGroups[kRounds][4] = {
     {7, 6, 0, -1}, {8, 5, 1, 14}, {9, 4, 2, 13}, {10, 3, 11, 12}};
 
@@ -67,8 +80,11 @@ struct TcArgs {
   u64* partial;          // [n_slots][ldp]
   u64 ldp, t_pad;
   u32 npieces, nunits, npts;
-  u64 Wd[15];            // 2^{8d} mod p
+  u64 Wd[15];            // 2^{8d} mod p  (Wd[8] = 2^64, Wd[12] = 2^96, Wd[14] -> see C128)
+  u64 C128;              // 2^128 mod p
+  u32* scratch;          // per CTA: 5 x kChunk u32 (160-bit exact running sums of a unit, L2-resident)
   ModParams mp;
+  unsigned long long* prof;  // optional phase timers [gridDim][warps][4] (PE_TC_PROF=1), else null
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -91,6 +107,35 @@ __device__ __forceinline__ void mma_u8(u32 dtmem, uint64_t ad, uint64_t bd, u32 
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
       :: "r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
 }
+__device__ __forceinline__ bool elect_one() {
+  u32 pred = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
+// warp-uniform value (lets the compiler keep it in the uniform datapath for tcgen05 operands)
+__device__ __forceinline__ u32 uni(u32 x) { return __shfl_sync(0xffffffffu, x, 0); }
+
+// The 16 digit-pair MMAs of round G on one smem stage (descriptor db = plane 0 of the stage),
+// round-robin over the round's diagonals so consecutive MMAs write different TMEM accumulators
+// (back-to-back MMAs into one accumulator serialise).  Fully unrolled: every operand offset is
+// a compile-time constant.
+template <int G>
+__device__ __forceinline__ void issue_round(u32 tb, uint64_t db, bool first_kb) {
+#pragma unroll
+  for (int step = 0; step < 8; ++step) {
+#pragma unroll
+    for (int di = 0; di < 4; ++di) {
+      const int d = group_diag(G, di);
+      const int s0 = d > 7 ? d - 7 : 0, s1 = d < 7 ? d : 7;
+      if (d >= 0 && s0 + step <= s1) {
+        const int sd = s0 + step;
+        mma_u8(tb + (u32)di * kV, db + (uint64_t)((u32)sd * (kPlane >> 4)),
+               db + (uint64_t)((u32)(8 + d - sd) * (kPlane >> 4)), (!first_kb || step > 0) ? 1u : 0u);
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                :: "r"(smem_u32(bar)) : "memory");
@@ -115,6 +160,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, u32 parity) {
   for (u32 n = 0; !mbar_try(bar, parity); ++n)
     if (n > (1u << 26)) __trap();
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on an mbarrier (complete_tx)
+__device__ __forceinline__ void bulk_g2s(u32 dst, const void* src, u32 bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(dst), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void lds4(u32 addr, u64 (&v)[4]) {
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%4];\n\tld.shared.v2.u64 {%2, %3}, [%4+16];"
+               : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "r"(addr) : "memory");
+}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -125,6 +182,12 @@ __device__ __forceinline__ void tmem_ld8(u32 taddr, u32 (&v)[8]) {
                : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Redefine registers written by tcgen05.ld after tcgen05.wait::ld: later (non-volatile) uses then
+// depend on this volatile statement and cannot be scheduled above the wait.
+__device__ __forceinline__ void tmem_reg_fence(u32 (&v)[8]) {
+  asm volatile("" : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7])
+               :: "memory");
+}
 
 __device__ __forceinline__ u32 prmt(u32 a, u32 b, u32 sel) {
   u32 r;
@@ -158,16 +221,95 @@ __device__ __forceinline__ u32 plane_off(u32 row, u32 kbyte) {
   return (kbyte >> 4) * kLBO + (row >> 3) * 128u + (row & 7u) * 16u + (kbyte & 15u);
 }
 
+// X (5 x 32-bit words, little endian) += D << 8d, exactly (X < 2^145 < 2^160 for the sum over all
+// 15 diagonals: D < 2^31, 8d <= 112).  Plain 128-bit C arithmetic: the compiler owns the carry
+// chain (carry flags are not preserved between separate inline-asm statements).
+template <int D8>
+__device__ __forceinline__ void fold_add(u32 (&X)[5], u32 Dv) {
+  typedef unsigned __int128 u128;
+  u128 lo = ((u128)(((u64)X[3] << 32) | X[2]) << 64) | (((u64)X[1] << 32) | X[0]);
+  const u128 add = (u128)Dv << D8;                                 // low 128 bits of D << 8d
+  const u32 spill = D8 > 96 ? (u32)(Dv >> (128 - D8 > 31 ? 31 : 128 - D8)) : 0u;  // bits >= 2^128
+  lo += add;
+  const u32 carry = lo < add ? 1u : 0u;
+  X[0] = (u32)lo;
+  X[1] = (u32)(lo >> 32);
+  X[2] = (u32)(lo >> 64);
+  X[3] = (u32)(lo >> 96);
+  X[4] += spill + carry;
+}
+
+// One round of the epilogue for thread row u: the round's diagonals (TMEM columns di*128 + v)
+// folded exactly into the unit's 160-bit running sums (scratch, SoA: word w at w*kChunk + u*128 + v).
+// TMEM is released (acce) as soon as the last block has been read.
+template <int G>
+__device__ __forceinline__ void epi_round(u32 tl, u32* __restrict__ sc, bool first, uint64_t* acce) {
+#pragma unroll 1
+  for (u32 v0 = 0; v0 < (u32)kV; v0 += 8) {
+    u32 X[5][8];
+    if (first) {
+#pragma unroll
+      for (int w = 0; w < 5; ++w)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) X[w][j] = 0;
+    } else {
+#pragma unroll
+      for (int w = 0; w < 5; ++w) {
+        const uint4* p4 = (const uint4*)(sc + (u32)w * kChunk + v0);
+        const uint4 q0 = p4[0], q1 = p4[1];
+        X[w][0] = q0.x; X[w][1] = q0.y; X[w][2] = q0.z; X[w][3] = q0.w;
+        X[w][4] = q1.x; X[w][5] = q1.y; X[w][6] = q1.z; X[w][7] = q1.w;
+      }
+    }
+    // TMEM loads after the scratch loads, waited on immediately: the destination registers must
+    // not be touched (even copied) before tcgen05.wait::ld
+    u32 D[4][8];
+#pragma unroll
+    for (int di = 0; di < 4; ++di)
+      if (group_diag(G, di) >= 0) tmem_ld8(tl + (u32)di * kV + v0, D[di]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int di = 0; di < 4; ++di)
+      if (group_diag(G, di) >= 0) tmem_reg_fence(D[di]);
+    if (v0 + 8 == (u32)kV) {   // TMEM drained: the MMA may start the next round
+      tc_fence_before();
+      mbar_arrive(acce);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      u32 x[5] = {X[0][j], X[1][j], X[2][j], X[3][j], X[4][j]};
+      if (group_diag(G, 0) >= 0) fold_add<8 * (group_diag(G, 0) < 0 ? 0 : group_diag(G, 0))>(x, D[0][j]);
+      if (group_diag(G, 1) >= 0) fold_add<8 * (group_diag(G, 1) < 0 ? 0 : group_diag(G, 1))>(x, D[1][j]);
+      if (group_diag(G, 2) >= 0) fold_add<8 * (group_diag(G, 2) < 0 ? 0 : group_diag(G, 2))>(x, D[2][j]);
+      if (group_diag(G, 3) >= 0) fold_add<8 * (group_diag(G, 3) < 0 ? 0 : group_diag(G, 3))>(x, D[3][j]);
+#pragma unroll
+      for (int w = 0; w < 5; ++w) X[w][j] = x[w];
+    }
+#pragma unroll
+    for (int w = 0; w < 5; ++w) {
+      uint4* p4 = (uint4*)(sc + (u32)w * kChunk + v0);
+      p4[0] = make_uint4(X[w][0], X[w][1], X[w][2], X[w][3]);
+      p4[1] = make_uint4(X[w][4], X[w][5], X[w][6], X[w][7]);
+    }
+  }
+}
+
+__device__ __forceinline__ long long clk() { return clock64(); }
+
 // unit -> (piece, chunk): chunk-major over the size-sorted pieces
 __device__ __forceinline__ void unit_of(const TcArgs& a, u32 unit, uint4& pc, u32& chunk) {
   chunk = unit / a.npieces;
   pc = a.piece[unit % a.npieces];
 }
 
+// PROF: per-warp phase timers (clock64) into a.prof -- a development build of the same kernel
+// (PE_TC_PROF=1); the production instantiation has no timers.
+template <bool PROF>
 static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
   extern __shared__ uint8_t dsm[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accf, acce;
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accf, acce, dfull[kDataSlots],
+      dempty[kDataSlots];
   __shared__ u32 tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -175,6 +317,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 32 * kProdPerStage); mbar_init(&empty[s], 1); }
     mbar_init(&accf, 1);
     mbar_init(&acce, 32 * kEpiWarps);
+    for (int s = 0; s < kDataSlots; ++s) { mbar_init(&dfull[s], 1); mbar_init(&dempty[s], 32 * kProdPerStage); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
@@ -185,12 +328,41 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const u32 tb = tmem_base;
+  long long T[4] = {0, 0, 0, 0};   // phase timers (a.prof)
+  const long long t_start = clk();
 
-  if (warp >= kProdWarp0) {
+  const u32 data0 = smem_u32(smem) + kStages * kStageBytes;
+  if (warp == kLoadWarp) {
+    // ------------------------------------------------------------ loader (TMA bulk copies)
+    if (lane == 0) {
+      u32 it = 0;
+      for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
+        uint4 pc; u32 chunk;
+        unit_of(a, unit, pc, chunk);
+        const u64* S0 = a.S + (u64)chunk * 2 * a.t_pad;
+        for (int g = 0; g < kRounds; ++g) {
+          for (u32 kb = 0; kb < pc.y; ++kb, ++it) {
+            const u32 slot = it % kDataSlots, use = it / kDataSlots;
+            long long c0 = clk();
+            mbar_wait(&dempty[slot], (use & 1) ^ 1);
+            if (PROF) T[0] += clk() - c0;
+            if (PROF) T[3] += 1;
+            mbar_expect_tx(&dfull[slot], kDataSlot);
+            const u64 q = (u64)pc.x + (u64)kb * kKB;
+            const u64* src[kD_N] = {S0 + q, S0 + a.t_pad + q, a.mV + q, a.wV + q, a.mV4 + q, a.wV4 + q,
+                                    a.m + q, a.w + q, a.m4 + q, a.w4 + q, a.m64 + q};
+            const u32 dst = data0 + slot * kDataSlot;
+#pragma unroll
+            for (int d = 0; d < kD_N; ++d) bulk_g2s(dst + (u32)d * kDataArr, src[d], kDataArr, &dfull[slot]);
+          }
+        }
+      }
+    }
+  } else if (warp >= kProdWarp0) {
     // ------------------------------------------------------------ producers
     // 4 warps per stage: (giant | baby) x (rows 0-63 | rows 64-127).  Lane = (tq, rr): terms
     // tq*4 .. tq*4+3 of the K-block, rows half*64 + rr + 4k (k < 16), i.e. 4 independent
-    // Shoup chains of stride 4 per lane.
+    // Shoup chains of stride 4 per lane.  Term data comes from the loader's smem ring.
     const int pw = warp - kProdWarp0;
     const int my_stage = pw / kProdPerStage, sub = pw % kProdPerStage;
     const bool giant = sub < 2;
@@ -198,39 +370,53 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
     const int tq = lane >> 2, rr = lane & 3;
     const u32 planes0 = smem_u32(smem) + (giant ? 0u : 8u * kPlane) + (u32)my_stage * kStageBytes +
                         plane_off(half * 64 + (u32)rr, (u32)tq * 4);
+    // this lane's 4 terms inside a data slot; seed / seed-step / chain-step arrays by role
+    const u32 toff = (u32)tq * 32;
+    const u32 a_seed = (giant ? (half ? kD_S1 : kD_S0) : kD_m64) * kDataArr + toff;
+    const u32 a_bm = (giant ? kD_mV : kD_m) * kDataArr + toff, a_bw = (giant ? kD_wV : kD_w) * kDataArr + toff;
+    const u32 a_sm = (giant ? kD_mV4 : kD_m4) * kDataArr + toff, a_sw = (giant ? kD_wV4 : kD_w4) * kDataArr + toff;
     const u64 np = a.mp.np;
     u32 it = 0;
     for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
       uint4 pc; u32 chunk;
       unit_of(a, unit, pc, chunk);
-      const u64* Sx = a.S + ((u64)chunk * 2 + half) * a.t_pad;
       for (int g = 0; g < kRounds; ++g) {
         for (u32 kb = 0; kb < pc.y; ++kb, ++it) {
           const u32 stage = it % kStages;
           if ((int)stage != my_stage) continue;
           const u32 use = it / kStages;
-          const u64 q = (u64)pc.x + (u64)kb * kKB + (u64)tq * 4;
-          u64 x[4], sm[4], sw[4];
-          if (giant) {
+          const u32 slot = it % kDataSlots, duse = it / kDataSlots;
+          const u32 dslot = data0 + slot * kDataSlot;
+          u64 x[4], bm[4], bw[4], sm[4], sw[4];
+          long long c0 = clk();
+          mbar_wait(&dfull[slot], duse & 1);
+          long long c1 = clk();
+          if (PROF) T[0] += c1 - c0;
+          lds4(dslot + a_seed, x);
+          lds4(dslot + a_bm, bm);
+          lds4(dslot + a_bw, bw);
+          lds4(dslot + a_sm, sm);
+          lds4(dslot + a_sw, sw);
+          if (!giant && !half) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              x[e] = __ldg(Sx + q + e);
-              const u64 bm = __ldg(a.mV + q + e), bw = __ldg(a.wV + q + e);
-              for (int r = 0; r < rr; ++r) x[e] = mul_shoup4(x[e], bm, bw, np);
-              sm[e] = __ldg(a.mV4 + q + e);
-              sw[e] = __ldg(a.wV4 + q + e);
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              x[e] = half ? __ldg(a.m64 + q + e) : 1ull;
-              const u64 bm = __ldg(a.m + q + e), bw = __ldg(a.w + q + e);
-              for (int r = 0; r < rr; ++r) x[e] = mul_shoup4(x[e], bm, bw, np);
-              sm[e] = __ldg(a.m4 + q + e);
-              sw[e] = __ldg(a.w4 + q + e);
-            }
+            for (int e = 0; e < 4; ++e) x[e] = 1;
           }
+          for (int r = 0; r < rr; ++r) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] = mul_shoup4(x[e], bm[e], bw[e], np);
+          }
+          // release the slot only after every value read from it has landed in registers, and
+          // order those generic-proxy reads before the loader's next async-proxy (bulk) write
+          {
+            u64 dep = sm[0] ^ sm[1] ^ sm[2] ^ sm[3] ^ sw[0] ^ sw[1] ^ sw[2] ^ sw[3] ^ x[0] ^ x[1] ^ x[2] ^ x[3];
+            asm volatile("" :: "l"(dep));
+          }
+          fence_async_smem();
+          mbar_arrive(&dempty[slot]);
+          c0 = clk();
           mbar_wait(&empty[stage], (use & 1) ^ 1);
+          c1 = clk();
+          if (PROF) T[1] += c1 - c0;
 #pragma unroll 2
           for (int k = 0; k < 16; ++k) {
             // row half*64 + rr + 4k: +4 rows = +64 bytes inside the same 8-row core-matrix pair
@@ -240,98 +426,130 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
           }
           fence_async_smem();
           mbar_arrive(&full[stage]);
+          if (PROF) T[2] += clk() - c1;
+          if (PROF) T[3] += 1;
         }
       }
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      u32 it = 0, round = 0;
-      const u32 sbase = smem_u32(smem);
-      for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
-        uint4 pc; u32 chunk;
-        unit_of(a, unit, pc, chunk);
-        for (int g = 0; g < kRounds; ++g, ++round) {
-          mbar_wait(&acce, (round & 1) ^ 1);
+    // The whole warp runs the control flow (operands stay warp-uniform); one elected lane issues.
+    u32 it = 0, round = 0;
+    const u32 tbu = uni(tb);
+    const uint64_t d0 = smem_desc(uni(smem_u32(smem)));
+    for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
+      uint4 pc; u32 chunk;
+      unit_of(a, unit, pc, chunk);
+      const u32 nkb = uni(pc.y);
+      for (int g = 0; g < kRounds; ++g, ++round) {
+        long long c0 = clk();
+        mbar_wait(&acce, (round & 1) ^ 1);
+        if (PROF) T[2] += clk() - c0;
+        tc_fence_after();
+        for (u32 kb = 0; kb < nkb; ++kb, ++it) {
+          const u32 stage = it % kStages, use = it / kStages;
+          c0 = clk();
+          mbar_wait(&full[stage], use & 1);
+          if (PROF) T[0] += clk() - c0;
+          if (PROF) T[3] += 1;
           tc_fence_after();
-          for (u32 kb = 0; kb < pc.y; ++kb, ++it) {
-            const u32 stage = it % kStages, use = it / kStages;
-            mbar_wait(&full[stage], use & 1);
-            tc_fence_after();
-            const u32 st = sbase + stage * kStageBytes;
-#pragma unroll
-            for (int di = 0; di < 4; ++di) {
-              const int d = kGroups[g][di];
-              if (d < 0) continue;
-              const int s0 = d > 7 ? d - 7 : 0, s1 = d < 7 ? d : 7;
-              for (int s = s0; s <= s1; ++s)
-                mma_u8(tb + (u32)di * kV, smem_desc(st + (u32)s * kPlane),
-                       smem_desc(st + (u32)(8 + d - s) * kPlane), (kb > 0 || s > s0) ? 1u : 0u);
+          const uint64_t db = d0 + (uint64_t)((stage * kStageBytes) >> 4);
+          // converge first so elect.sync picks the same leader (lane 0) every time: a
+          // tcgen05.commit tracks only the MMAs its own thread issued
+          __syncwarp();
+          // converge first so elect.sync picks the same leader (lane 0) every time: a
+          // tcgen05.commit tracks the MMAs its own thread issued
+          __syncwarp();
+          if (elect_one()) {
+            switch (g) {
+              case 0: issue_round<0>(tbu, db, kb == 0); break;
+              case 1: issue_round<1>(tbu, db, kb == 0); break;
+              case 2: issue_round<2>(tbu, db, kb == 0); break;
+              default: issue_round<3>(tbu, db, kb == 0); break;
             }
+            if (kb + 1 == nkb) mma_commit(&accf);   // accumulators complete after this K-block
             mma_commit(&empty[stage]);
           }
-          mma_commit(&accf);
+          __syncwarp();
         }
       }
     }
-    __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue
+    // Per round: TMEM -> exact 160-bit fold into this CTA's scratch (ALU only), release TMEM.
+    // After the unit's last round: one reduction mod p per point -> the piece's partial row,
+    // overlapping the next unit's first round of MMAs.
     const u32 u = (u32)(warp * 32 + lane);
     const u32 tl = tb + ((u32)(warp * 32) << 16);
     const ModParams mp = a.mp;
+    u32* sc = a.scratch + (u64)blockIdx.x * 5 * kChunk + (u64)u * kV;
+    const u64 C64 = a.Wd[8], C96 = a.Wd[12], C128 = a.C128;
     u32 round = 0;
     for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
       uint4 pc; u32 chunk;
       unit_of(a, unit, pc, chunk);
       u64* prow = a.partial + (u64)pc.z * a.ldp;
-      const u64 kbase = (u64)chunk * kChunk + (u64)u * kV;
+      const u64 kbase = (u64)chunk * kChunk + (u64)u * kV;   // multiple of 8; ldp multiple of 8
       for (int g = 0; g < kRounds; ++g, ++round) {
+        long long c0 = clk();
         mbar_wait(&accf, round & 1);
+        long long c1 = clk();
+        if (PROF) T[0] += c1 - c0;
         tc_fence_after();
-        int nd = 0;
-        u64 W[4];
-#pragma unroll
-        for (int di = 0; di < 4; ++di) {
-          const int d = kGroups[g][di];
-          W[di] = d >= 0 ? a.Wd[d] : 0;
-          nd += d >= 0;
+        switch (g) {
+          case 0: epi_round<0>(tl, sc, true, &acce); break;
+          case 1: epi_round<1>(tl, sc, false, &acce); break;
+          case 2: epi_round<2>(tl, sc, false, &acce); break;
+          default: epi_round<3>(tl, sc, false, &acce); break;
         }
-        for (u32 v0 = 0; v0 < (u32)kV; v0 += 8) {
-          u32 D[4][8];
-#pragma unroll
-          for (int di = 0; di < 4; ++di) {
-            if (di < nd) tmem_ld8(tl + (u32)di * kV + v0, D[di]);
-          }
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            // X = sum_d D_d * W_d < 4 * 2^31 * 2^62 (96-bit), then mod p
-            u64 lo = 0, hi = 0;
-#pragma unroll
-            for (int di = 0; di < 4; ++di) {
-              if (di < nd) {
-                const u64 w = W[di];
-                const u64 p0 = (u64)D[di][j] * lo32(w);
-                const u64 p1 = (u64)D[di][j] * hi32(w);
-                const u64 add_lo = p0 + (p1 << 32);
-                const u64 add_hi = (p1 >> 32) + (add_lo < p0 ? 1ull : 0ull);
-                lo += add_lo;
-                hi += add_hi + (lo < add_lo ? 1ull : 0ull);
-              }
-            }
-            u64 r = reduce128(hi, lo, mp);
-            const u64 k = kbase + v0 + j;
-            if (k < a.npts) {
-              if (g > 0) r = csub(r + prow[k], mp.p);
-              prow[k] = r;
-            }
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(&acce);
+        if (PROF) T[1] += clk() - c1;
+        if (PROF) T[3] += 1;
       }
+      // X mod p = (x0 + x1 2^32) + x2 (2^64 mod p) + x3 (2^96 mod p) + x4 (2^128 mod p)  (< 2^96)
+      long long c2 = clk();
+#pragma unroll 1
+      for (u32 v0 = 0; v0 < (u32)kV; v0 += 8) {
+        u32 X[5][8];
+#pragma unroll
+        for (int w = 0; w < 5; ++w) {
+          const uint4* p4 = (const uint4*)(sc + (u32)w * kChunk + v0);
+          const uint4 q0 = p4[0], q1 = p4[1];
+          X[w][0] = q0.x; X[w][1] = q0.y; X[w][2] = q0.z; X[w][3] = q0.w;
+          X[w][4] = q1.x; X[w][5] = q1.y; X[w][6] = q1.z; X[w][7] = q1.w;
+        }
+        u64 res[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          u64 lo = ((u64)X[1][j] << 32) | X[0][j], hi = 0;
+          const u64 terms[3][2] = {{X[2][j], C64}, {X[3][j], C96}, {X[4][j], C128}};
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const u64 p0 = terms[q][0] * lo32(terms[q][1]);
+            const u64 p1 = terms[q][0] * hi32(terms[q][1]);
+            const u64 add_lo = p0 + (p1 << 32);
+            const u64 add_hi = (p1 >> 32) + (add_lo < p0 ? 1ull : 0ull);
+            lo += add_lo;
+            hi += add_hi + (lo < add_lo ? 1ull : 0ull);
+          }
+          res[j] = reduce128(hi, lo, mp);
+        }
+        if (kbase + v0 + 8 <= a.npts) {
+          ulonglong2* dst = (ulonglong2*)(prow + kbase + v0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dst[j] = make_ulonglong2(res[2 * j], res[2 * j + 1]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (kbase + v0 + j < a.npts) prow[kbase + v0 + j] = res[j];
+        }
+      }
+      if (PROF) T[2] += clk() - c2;
     }
+  }
+  if (PROF && a.prof && lane == 0) {
+    unsigned long long* o = a.prof + ((u64)blockIdx.x * (kThreads / 32) + warp) * 5;
+    for (int i = 0; i < 4; ++i) o[i] = (unsigned long long)T[i];
+    o[4] = (unsigned long long)(clk() - t_start);
   }
   tc_fence_before();
   __syncthreads();
