@@ -221,22 +221,45 @@ __device__ __forceinline__ u32 plane_off(u32 row, u32 kbyte) {
   return (kbyte >> 4) * kLBO + (row >> 3) * 128u + (row & 7u) * 16u + (kbyte & 15u);
 }
 
-// X (5 x 32-bit words, little endian) += D << 8d, exactly (X < 2^145 < 2^160 for the sum over all
-// 15 diagonals: D < 2^31, 8d <= 112).  Plain 128-bit C arithmetic: the compiler owns the carry
-// chain (carry flags are not preserved between separate inline-asm statements).
+// X (5 x 32-bit words, little endian) += sum over the round's diagonals of D_d << 8d, exactly
+// (X < 2^145 < 2^160 for the sum over all 15 diagonals: D < 2^31, 8d <= 112).  The low 128 bits
+// are composed once per point; plain C 128-bit arithmetic lets the compiler own the carry chain
+// (carry flags are not preserved between separate inline-asm statements).
+typedef unsigned __int128 u128_t;
 template <int D8>
-__device__ __forceinline__ void fold_add(u32 (&X)[5], u32 Dv) {
-  typedef unsigned __int128 u128;
-  u128 lo = ((u128)(((u64)X[3] << 32) | X[2]) << 64) | (((u64)X[1] << 32) | X[0]);
-  const u128 add = (u128)Dv << D8;                                 // low 128 bits of D << 8d
-  const u32 spill = D8 > 96 ? (u32)(Dv >> (128 - D8 > 31 ? 31 : 128 - D8)) : 0u;  // bits >= 2^128
+__device__ __forceinline__ void fold_one(u128_t& lo, u32& x4, u32 Dv) {
+  if (D8 < 0) return;
+  constexpr int s = D8 < 0 ? 0 : D8;
+  const u128_t add = (u128_t)Dv << s;                                 // low 128 bits of D << 8d
+  const u32 spill = s > 96 ? (u32)(Dv >> (128 - s > 31 ? 31 : 128 - s)) : 0u;   // bits >= 2^128
   lo += add;
-  const u32 carry = lo < add ? 1u : 0u;
+  x4 += spill + (lo < add ? 1u : 0u);
+}
+template <int G>
+__device__ __forceinline__ void fold_point(u32 (&X)[5], u32 D0, u32 D1, u32 D2, u32 D3) {
+  u128_t lo = ((u128_t)(((u64)X[3] << 32) | X[2]) << 64) | (((u64)X[1] << 32) | X[0]);
+  u32 x4 = X[4];
+  fold_one<group_diag(G, 0) < 0 ? -1 : 8 * group_diag(G, 0)>(lo, x4, D0);
+  fold_one<group_diag(G, 1) < 0 ? -1 : 8 * group_diag(G, 1)>(lo, x4, D1);
+  fold_one<group_diag(G, 2) < 0 ? -1 : 8 * group_diag(G, 2)>(lo, x4, D2);
+  fold_one<group_diag(G, 3) < 0 ? -1 : 8 * group_diag(G, 3)>(lo, x4, D3);
   X[0] = (u32)lo;
   X[1] = (u32)(lo >> 32);
   X[2] = (u32)(lo >> 64);
   X[3] = (u32)(lo >> 96);
-  X[4] += spill + carry;
+  X[4] = x4;
+}
+// single-diagonal form (unit tests: scripts/fold_test.cu)
+template <int D8>
+__device__ __forceinline__ void fold_add(u32 (&X)[5], u32 Dv) {
+  u128_t lo = ((u128_t)(((u64)X[3] << 32) | X[2]) << 64) | (((u64)X[1] << 32) | X[0]);
+  u32 x4 = X[4];
+  fold_one<D8>(lo, x4, Dv);
+  X[0] = (u32)lo;
+  X[1] = (u32)(lo >> 32);
+  X[2] = (u32)(lo >> 64);
+  X[3] = (u32)(lo >> 96);
+  X[4] = x4;
 }
 
 // One round of the epilogue for thread row u: the round's diagonals (TMEM columns di*128 + v)
@@ -278,10 +301,7 @@ __device__ __forceinline__ void epi_round(u32 tl, u32* __restrict__ sc, bool fir
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       u32 x[5] = {X[0][j], X[1][j], X[2][j], X[3][j], X[4][j]};
-      if (group_diag(G, 0) >= 0) fold_add<8 * (group_diag(G, 0) < 0 ? 0 : group_diag(G, 0))>(x, D[0][j]);
-      if (group_diag(G, 1) >= 0) fold_add<8 * (group_diag(G, 1) < 0 ? 0 : group_diag(G, 1))>(x, D[1][j]);
-      if (group_diag(G, 2) >= 0) fold_add<8 * (group_diag(G, 2) < 0 ? 0 : group_diag(G, 2))>(x, D[2][j]);
-      if (group_diag(G, 3) >= 0) fold_add<8 * (group_diag(G, 3) < 0 ? 0 : group_diag(G, 3))>(x, D[3][j]);
+      fold_point<G>(x, D[0][j], D[1][j], D[2][j], group_diag(G, 3) >= 0 ? D[3][j] : 0u);
 #pragma unroll
       for (int w = 0; w < 5; ++w) X[w][j] = x[w];
     }
