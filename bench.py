@@ -202,7 +202,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2004_11571_b200 as pe
-    from paper_2004_11571_b200.dist import ShardedEval
+    from paper_2004_11571_b200.dist import ShardedEval, TermShardedEval, bucket_keys, term_partition
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
@@ -223,21 +223,44 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # ---- multi-GPU decomposition: the tensor-core path needs whole 16384-point chunks, so with
+    # N > 1 ranks shard bucket-contiguous TERM ranges (each rank: all T points of ~t/N terms,
+    # P2P row gather, boundary buckets summed mod p); the scalar path shards the point range.
+    probe = pe.Context(w.p, w.coeffs[:1], w.exps[:1], w.alpha, n=w.n)
+    term_shard = world > 1 and probe.uses_tc(w.T)
+    probe.close()
+    if term_shard:
+        order, bounds = term_partition(w.exps, world)
+        mine = np.sort(order[bounds[rank]:bounds[rank + 1]])
+        w_c, w_e = np.ascontiguousarray(w.coeffs[mine]), np.ascontiguousarray(w.exps[mine])
+    else:
+        w_c, w_e = w.coeffs, w.exps
+
     # ---- handle (pe_create) -- outside the device-timed region
     t0 = time.perf_counter()
-    ctx = pe.Context.from_workload(w)
+    ctx = pe.Context(w.p, w_c, w_e, w.alpha, n=w.n)
     torch.cuda.synchronize()
     create_s = time.perf_counter() - t0
     info = ctx.info()
     info["G"] = ctx.G
-    sh = ShardedEval(ctx.G, w.T, dev)
-    info["uses_tc"] = ctx.uses_tc(sh.cnt)
+    if term_shard:
+        sh = TermShardedEval(bucket_keys(w.exps)[order], bounds, w.T, w.p, dev)
+        info["G"] = sh.G
+        local_tp = w_c.size * w.T
+        info["uses_tc"] = ctx.uses_tc(w.T)
 
-    def eval_local(j_first, cnt, out):
-        ctx.eval_device(j_first, cnt, out.data_ptr(), out.shape[1], stream.cuda_stream)
+        def step():
+            return sh.run(lambda out: ctx.eval_device(w.j0, w.T, out.data_ptr(), w.T, stream.cuda_stream))
+    else:
+        sh = ShardedEval(ctx.G, w.T, dev)
+        local_tp = w.t * sh.cnt
+        info["uses_tc"] = ctx.uses_tc(sh.cnt)
 
-    def step():
-        return sh.run(eval_local, w.j0)
+        def eval_local(j_first, cnt, out):
+            ctx.eval_device(j_first, cnt, out.data_ptr(), out.shape[1], stream.cuda_stream)
+
+        def step():
+            return sh.run(eval_local, w.j0)
 
     # ---- device-timed region
     for _ in range(args.warmup):
@@ -266,11 +289,11 @@ def main():
     n_launch = max(ks["step_launches"], 1)                                 # passes x steps (rank 0)
     step_ms = ks["step_ms"] / n_launch                                     # mean launch time
     launches_tp = ks["term_points"] / n_launch                             # padded term-points / launch
-    algo_tp = w.t * sh.cnt * args.steps / n_launch if sh.cnt else 0        # algorithmic term-points / launch
+    algo_tp = local_tp * args.steps / n_launch if local_tp else 0         # algorithmic term-points / launch
     tp_rate = algo_tp / (step_ms * 1e-3) if step_ms else 0.0
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
     imad_peak = N_SM * sm_mhz * 1e6 * IMAD_LANES_PER_CLK_SM / IMAD_SLOTS_PER_TP
-    use_tc = ctx.uses_tc(sh.cnt)
+    use_tc = info["uses_tc"]
     if use_tc:
         # 64 exact byte-pair multiply-accumulates per term-point: 128 int8 ops
         ops = algo_tp * OPS_PER_TP_TC
@@ -292,7 +315,7 @@ def main():
                 "step_ms": step_ms, "fixup_ms": ks["fixup_ms"] / n_launch,
                 "padded_term_points_per_launch": launches_tp, "term_points_per_launch": algo_tp,
                 "int8_ops_per_launch": ops, "tc_pieces": info["tc_pieces"],
-                "algorithmic_bytes_per_launch": 16 * w.t + 8 * ctx.G * sh.cnt}
+                "algorithmic_bytes_per_launch": 16 * w_c.size + 8 * ctx.G * w.T}
         gpu_launches = 3 * ks["step_launches"]       # k_tc_seed + k_tc + k_fixup per pass (rank 0)
     else:
         achieved = tp_rate
@@ -327,13 +350,14 @@ def main():
     if not args.no_e2e:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64) if a.dtype == np.uint64
                                          else np.ascontiguousarray(a).view(np.int32)).pin_memory()
-        h_c, h_e, h_a = pin(w.coeffs), pin(w.exps), pin(w.alpha)
-        h_out = torch.empty((ctx.G, w.T), dtype=torch.int64).pin_memory() if sh.is_root else None
+        h_c, h_e, h_a = pin(w_c), pin(w_e), pin(w.alpha)          # this rank's terms (all for N = 1)
+        G_all = sh.G if term_shard else ctx.G
+        h_out = torch.empty((G_all, w.T), dtype=torch.int64).pin_memory() if sh.is_root else None
         L = pe.lib()
         import ctypes
 
         def e2e_step():
-            h = L.pe_create(w.p, w.t, w.n, ctypes.c_void_p(h_c.data_ptr()), ctypes.c_void_p(h_e.data_ptr()),
+            h = L.pe_create(w.p, w_c.size, w.n, ctypes.c_void_p(h_c.data_ptr()), ctypes.c_void_p(h_e.data_ptr()),
                             ctypes.c_void_p(h_a.data_ptr()))
             if not h:
                 raise pe.PEError(L.pe_last_error(), "pe_create")
@@ -342,6 +366,16 @@ def main():
                     rc = L.pe_eval(h, w.j0, w.T, ctypes.c_void_p(h_out.data_ptr()))
                     if rc:
                         raise pe.PEError(rc, "pe_eval")
+                elif term_shard:
+                    def ev_rows(out):
+                        rc = L.pe_eval_device(h, w.j0, w.T, ctypes.c_void_p(out.data_ptr()), w.T,
+                                              ctypes.c_void_p(stream.cuda_stream))
+                        if rc:
+                            raise pe.PEError(rc, "pe_eval_device")
+                    res = sh.run(ev_rows)
+                    if sh.is_root:
+                        h_out.copy_(res)
+                    torch.cuda.synchronize()
                 else:
                     def ev(j_first, cnt, out):
                         rc = L.pe_eval_device(h, j_first, cnt, ctypes.c_void_p(out.data_ptr()), out.shape[1],
@@ -368,9 +402,10 @@ def main():
             torch.cuda.synchronize()
             ts.append(max_over_ranks(time.perf_counter() - t0))
         e2e_s = statistics.median(ts)
-        h2d = w.coeffs.nbytes + w.exps.nbytes + w.alpha.nbytes
+        h2d = (w.coeffs.nbytes + w.exps.nbytes + w.alpha.nbytes * world if term_shard
+               else (w.coeffs.nbytes + w.exps.nbytes + w.alpha.nbytes) * world)
         e2e = {"value": w.t * w.T / e2e_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_s,
-               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": ctx.G * w.T * 8,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": G_all * w.T * 8,
                "includes": "pe_create (H2D + sort + plan + K1) + eval + gather + D2H, host wall clock, max over ranks"}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
@@ -390,7 +425,9 @@ def main():
                 "vs_baseline": None, "dtype": "u64", "data": "synthetic",
                 "config": workload_config(w, info), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": gpu_launches, "clocks": clocks,
-                "create_s": create_s, "parallelism": f"point-range shards x{world}, NCCL gather"}
+                "create_s": create_s,
+                "parallelism": (f"bucket-contiguous term ranges x{world}, NCCL P2P row gather" if term_shard
+                                else f"point-range shards x{world}, NCCL gather")}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
