@@ -48,7 +48,7 @@ int pe_bench_core(int variant, uint64_t p, int R, int blocks, int threads, int i
 
 /*
  * pe_bench_mma -- int8 tensor-core issue rate: one CTA per SM issues `iters` tcgen05.mma
- * kind::i8 (u8 x u8 -> s32, M = 128, N = 64 or 128, K = 32) from a fixed shared-memory tile
+ * kind::i8 (u8 x u8 -> s32, M = 128, N = 16, 32, 64 or 128, K = 32) from a fixed shared-memory tile
  * (the k_tc MMA shape, csrc/tc.cuh).  Writes the CUDA-event device time of the launch (ms) and
  * the multiply-accumulates executed.  Returns PE_OK / PE_EINVAL / PE_ECUDA.  Synchronous.
  */

@@ -120,8 +120,7 @@ struct pe_ctx {
   bool tc_ok = false;
   u32 tc_npieces = 0, tc_nslots = 0;
   int n_sm = 148;
-  u64 *d_m4 = nullptr, *d_w4 = nullptr, *d_mV = nullptr, *d_wV = nullptr, *d_mV4 = nullptr, *d_wV4 = nullptr;
-  u64* d_m64 = nullptr;
+  u64* d_tcC = nullptr;   // [t_pad][12] tensor-core path C records (tc.cuh)
   uint4* d_piece = nullptr;
   u32* d_tc_slot_start = nullptr;
   u64* d_seed = nullptr;
@@ -146,8 +145,8 @@ static void free_all(pe_ctx* h) {
   cudaStream_t s = h->stream;
   for (void* q : {(void*)h->d_c, (void*)h->d_m, (void*)h->d_w, (void*)h->d_perm, (void*)h->d_ms, (void*)h->d_mpd,
                   (void*)h->d_mspd, (void*)h->d_wt_info, (void*)h->d_slot_start, (void*)h->d_partial,
-                  (void*)h->d_out_scratch, (void*)h->d_m4, (void*)h->d_w4, (void*)h->d_mV, (void*)h->d_wV,
-                  (void*)h->d_mV4, (void*)h->d_wV4, (void*)h->d_m64, (void*)h->d_tc_scratch, (void*)h->d_piece, (void*)h->d_tc_slot_start,
+                  (void*)h->d_out_scratch, (void*)h->d_tcC,
+                  (void*)h->d_tc_scratch, (void*)h->d_piece, (void*)h->d_tc_slot_start,
                   (void*)h->d_seed})
     if (q) cudaFreeAsync(q, s);
   if (s) cudaStreamSynchronize(s);
@@ -417,11 +416,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   std::vector<u32> tc_slot_start(G + 1);
   if (h->tc_mode != 0 && h->path == kInt4) {
     const u64 tp = h->t_pad;
-    if (dalloc(&h->d_m4, tp) || dalloc(&h->d_w4, tp) || dalloc(&h->d_mV, tp) || dalloc(&h->d_wV, tp) ||
-        dalloc(&h->d_mV4, tp) || dalloc(&h->d_wV4, tp) || dalloc(&h->d_m64, tp))
-      return g_last_error;
-    tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_m4, h->d_w4, h->d_mV, h->d_wV, h->d_mV4,
-                                                     h->d_wV4, h->d_m64, h->mp);
+    if (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp)) return g_last_error;
+    tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_tcC, h->mp);
     CU(cudaGetLastError());
     // pieces: each bucket's padded range split into ceil(n / kPieceMax) near-equal runs of whole
     // K-blocks (<= kPieceMax terms keeps every int32 diagonal sum exact); slots contiguous per bucket
@@ -597,12 +593,12 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
   // partial rows padded to a multiple of 8 points (the epilogue's 64-byte vector accesses)
   if (ensure_partial(h, (size_t)nslots * ((std::min<u64>(Tp, T) + 7) / 8 * 8), s)) return g_last_error;
   const u32 nch_max = (u32)(Tp / tc::kChunk);
-  if ((size_t)h->t_pad * nch_max * 2 > h->seed_elems) {
+  if ((size_t)h->t_pad * nch_max * 8 > h->seed_elems) {
     if (h->d_seed) cudaFreeAsync(h->d_seed, s);
     h->d_seed = nullptr;
     h->seed_elems = 0;
-    CU(cudaMallocAsync((void**)&h->d_seed, (size_t)h->t_pad * nch_max * 2 * sizeof(u64), s));
-    h->seed_elems = (size_t)h->t_pad * nch_max * 2;
+    CU(cudaMallocAsync((void**)&h->d_seed, (size_t)h->t_pad * nch_max * 8 * sizeof(u64), s));
+    h->seed_elems = (size_t)h->t_pad * nch_max * 8;
   }
   if (!h->d_tc_scratch) CU(cudaMallocAsync((void**)&h->d_tc_scratch, (size_t)h->n_sm * 5 * tc::kChunk * sizeof(u32), s));
   CU(cudaFuncSetAttribute(tc::k_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
@@ -614,9 +610,8 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
                                                                       h->d_seed, h->mp);
     CU(cudaGetLastError());
     tc::TcArgs a;
-    a.S = h->d_seed;
-    a.m = h->d_m; a.w = h->d_w; a.m64 = h->d_m64; a.m4 = h->d_m4; a.w4 = h->d_w4;
-    a.mV = h->d_mV; a.wV = h->d_wV; a.mV4 = h->d_mV4; a.wV4 = h->d_wV4;
+    a.LS = h->d_seed;
+    a.C = h->d_tcC;
     a.piece = h->d_piece;
     a.partial = h->d_partial;
     a.ldp = (np + 7) / 8 * 8;
@@ -629,6 +624,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     a.scratch = h->d_tc_scratch;
     a.mp = h->mp;
     a.prof = nullptr;
+    a.dbg = env_int("PE_TC_DEBUG", 0);
     const unsigned grid = (unsigned)std::min<u64>(a.nunits, (u64)h->n_sm);
     pe_ctx::Rec rec{};
     if (h->timing) {

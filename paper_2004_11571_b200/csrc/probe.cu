@@ -270,7 +270,7 @@ extern "C" int pe_bench_core(int variant, uint64_t p, int R, int blocks, int thr
 // One CTA per SM issues `iters` M=128 x N x K=32 kind::i8 MMAs (u8 x u8 -> s32) from a fixed
 // shared-memory tile into 4 rotating TMEM accumulators: the same-run tensor ceiling that
 // bench.py quotes beside k_tc (the tc.cuh MMA shape is N = 128).
-__global__ void k_bench_mma(int iters, u32 idesc, u32 ncols) {
+__global__ void k_bench_mma(int iters, u32 idesc, u32 ncols, int nacc) {
   extern __shared__ uint8_t dsm[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t bar;
@@ -292,12 +292,14 @@ __global__ void k_bench_mma(int iters, u32 idesc, u32 ncols) {
   const u32 tb = tmem_base;
   if (threadIdx.x == 0) {
     const uint64_t ad = tc::smem_desc(tc::smem_u32(sm)), bd = tc::smem_desc(tc::smem_u32(sm) + tc::kPlane);
-    for (int it = 0; it < iters; ++it)
+    u32 acc_col = 0;
+    const u32 acc_end = (u32)nacc * ncols;
+    for (int it = 0; it < iters; ++it, acc_col = (acc_col + ncols == acc_end) ? 0u : acc_col + ncols)
       asm volatile(
           "{\n\t.reg .pred p;\n\t"
           "setp.ne.b32 p, %4, 0;\n\t"
           "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
-          :: "r"(tb + (u32)(it & 3) * ncols), "l"(ad), "l"(bd), "r"(idesc), "r"(1u));
+          :: "r"(tb + acc_col), "l"(ad), "l"(bd), "r"(idesc), "r"(1u));
     tc::mma_commit(&bar);
   }
   tc::mbar_wait(&bar, 0);
@@ -310,7 +312,8 @@ __global__ void k_bench_mma(int iters, u32 idesc, u32 ncols) {
 }
 
 extern "C" int pe_bench_mma(int N, int iters, float* ms, double* macs) {
-  if ((N != 64 && N != 128) || iters < 1 || !ms || !macs) return PE_EINVAL;
+  if ((N != 16 && N != 32 && N != 64 && N != 128) || iters < 1 || !ms || !macs) return PE_EINVAL;
+  const int nacc = (512 / N) < 16 ? 512 / N : 16;   // rotating independent accumulators
   int dev = 0, nsm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
@@ -324,7 +327,7 @@ extern "C" int pe_bench_mma(int N, int iters, float* ms, double* macs) {
   cudaEventCreate(&e1);
   for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
     cudaEventRecord(e0);
-    k_bench_mma<<<nsm, 128, smem>>>(iters, idesc, (u32)N);
+    k_bench_mma<<<nsm, 128, smem>>>(iters, idesc, (u32)N, nacc);
     cudaEventRecord(e1);
   }
   int rc = PE_OK;

@@ -14,8 +14,9 @@
 // the 5th-generation tensor cores do.  Exactness: L and R are split into their 8 unsigned
 // bytes (L = sum_s 2^{8s} L_s), every byte product L_s R_t is an exact int8 MMA with int32
 // accumulation in TMEM, and the 64 (s, t) products are summed by diagonal d = s + t:
-//     X = sum_d 2^{8d} D_d,   D_d = sum_{s+t=d} L_s R_t,   D_d < 4096 * 8 * 255^2 < 2^31
-// for <= 4096 terms per accumulation (a "piece").  X mod p = sum_d D_d (2^{8d} mod p) mod p.
+//     X = sum_d 2^{8d} D_d,   D_d = sum_{s+t=d} L_s R_t,   D_d < 8192 * 8 * 255^2 < 2^32
+// for <= 8192 terms per accumulation (a "piece"; the s32 TMEM accumulator wraps mod 2^32 without
+// saturation, so its bits read as u32 are exact).  X mod p = sum_d D_d (2^{8d} mod p) mod p.
 //
 // Shapes: U = M = 128 (TMEM lanes), V = N = 128, K-block = 32 terms (one kind::i8 MMA).  The 15
 // diagonals do not fit TMEM at once (15 x 128 columns > 512), so a piece is evaluated in 4
@@ -31,8 +32,10 @@
 //   warp  4    TMEM allocator + single-thread MMA issuer (tcgen05.mma.cta_group::1.kind::i8)
 //   warps 5-16 producers, 4 per smem stage: two L warps and two R warps generate one K-block's
 //              128 giant-step / 128 baby-step values of 32 terms (64 rows each) with Shoup
-//              products (4 chains per lane) and write their 8 byte planes in the no-swizzle
-//              K-major UMMA layout.
+//              products (4 chains per lane, seeded from precomputed chain seeds) and write their
+//              8 byte planes in the no-swizzle K-major UMMA layout.
+//   warp  17   loader: TMA bulk copies of each K-block's per-term seeds / multipliers into an
+//              smem ring ahead of the producers.
 #pragma once
 #include "modcore.cuh"
 
@@ -44,15 +47,21 @@ constexpr int kV = 128;                   // baby steps per chunk   (MMA N)
 constexpr u32 kChunk = kU * kV;           // points per chunk
 constexpr int kKB = 32;                   // terms per K-block (one i8 MMA K step)
 constexpr int kStages = 3;
-constexpr u32 kPieceMax = 4096;           // terms per accumulation: 4096 * 8 * 255^2 < 2^31
+constexpr u32 kPieceMax = 8192;           // terms per accumulation: 8192 * 8 * 255^2 < 2^32 (the s32
+                                          // accumulator wraps mod 2^32, saturate = 0; read as u32)
 constexpr u32 kLBO = 2048 + 64;           // bytes between the two 16-byte K chunks of a plane (+64: bank spread)
 constexpr u32 kPlane = 2 * kLBO;          // one digit plane: 128 rows x 32 bytes (+ pad)
 constexpr u32 kStageBytes = 16 * kPlane;  // 8 L planes + 8 R planes
 // per-K-block term data streamed by the loader warp (TMA bulk copies): 11 arrays x 32 terms
-enum { kD_S0 = 0, kD_S1, kD_mV, kD_wV, kD_mV4, kD_wV4, kD_m, kD_w, kD_m4, kD_w4, kD_m64, kD_N };
-constexpr u32 kDataArr = kKB * 8;               // 256 B per array per K-block
-constexpr u32 kDataSlot = kD_N * kDataArr;      // 2816 B
-constexpr int kDataSlots = 2 * kStages;         // ring depth (2 K-blocks ahead per producer group)
+// Per-term records (array of structs, so one K-block's data is two contiguous bulk copies):
+//   LS record (per chunk, 8 u64): giant-step chain seeds c m^{j_s + (64h + rr) V}, index h*4 + rr
+//   C  record (12 u64): baby-step chain seeds m^{64h + rr} (index h*4 + rr), m^4, w(m^4), m^{4V}, w(m^{4V})
+// (h = row half, rr = the lane's row residue mod 4)
+constexpr int kLSRec = 8, kCRec = 12;
+enum { kC_m4 = 8, kC_w4 = 9, kC_mV4 = 10, kC_wV4 = 11 };
+constexpr u32 kDataLS = kKB * kLSRec * 8;        // 2048 B
+constexpr u32 kDataSlot = kDataLS + kKB * kCRec * 8;   // 5120 B
+constexpr int kDataSlots = 5;                   // ring depth (K-blocks ahead of the producers)
 constexpr u32 kSmemBytes = kStages * kStageBytes + kDataSlots * kDataSlot + 1024;
 constexpr int kRounds = 4;
 constexpr int kProdPerStage = 4;          // L rows 0-63, L rows 64-127, R rows 0-63, R rows 64-127
@@ -70,12 +79,8 @@ __device__ __constant__ const signed char kGroups[kRounds][4] = {
     {7, 6, 0, -1}, {8, 5, 1, 14}, {9, 4, 2, 13}, {10, 3, 11, 12}};
 
 struct TcArgs {
-  const u64* S;     // [nch][2][t_pad] c_i m_i^{j_s(chunk)} and c_i m_i^{j_s(chunk) + 64V} (chunk seeds)
-  const u64 *m, *w;      // m_i, Shoup w(m_i)            (baby-step seeds)
-  const u64* m64;        // m_i^64                        (baby-step seed of rows 64..127)
-  const u64 *m4, *w4;    // m_i^4                         (baby-step stride 4)
-  const u64 *mV, *wV;    // m_i^V                         (giant-step seeds)
-  const u64 *mV4, *wV4;  // m_i^{4V}                      (giant-step stride 4)
+  const u64* LS;         // [nch][t_pad][8] LS records (giant-step chain seeds of each chunk)
+  const u64* C;          // [t_pad][12] C records (baby-step seeds, stride-4 multipliers)
   const uint4* piece;    // x = first padded term, y = K-blocks, z = partial slot (sorted by size desc)
   u64* partial;          // [n_slots][ldp]
   u64 ldp, t_pad;
@@ -85,6 +90,8 @@ struct TcArgs {
   u32* scratch;          // per CTA: 5 x kChunk u32 (160-bit exact running sums of a unit, L2-resident)
   ModParams mp;
   unsigned long long* prof;  // optional phase timers [gridDim][warps][4] (PE_TC_PROF=1), else null
+  int dbg;                   // development only (PE_TC_DEBUG, PROF build): 1 = skip the MMAs,
+                             // 2 = producers skip generation, 3 = epilogue skips its scratch loads
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -155,10 +162,14 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, u32 parity) {
       : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   return ok != 0;
 }
-// bounded wait: a protocol bug becomes a launch error instead of a hung GPU
+// bounded wait: a protocol bug becomes a launch error instead of a hung GPU.  SLEEP_NS > 0 backs
+// off between polls so a waiting warp stops taking issue slots from the producers on its SMSP.
+template <int SLEEP_NS = 0>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, u32 parity) {
-  for (u32 n = 0; !mbar_try(bar, parity); ++n)
+  for (u32 n = 0; !mbar_try(bar, parity); ++n) {
+    if (SLEEP_NS) __nanosleep(SLEEP_NS);
     if (n > (1u << 26)) __trap();
+  }
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, u32 bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
@@ -167,6 +178,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, u32 bytes) {
 __device__ __forceinline__ void bulk_g2s(u32 dst, const void* src, u32 bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                :: "r"(dst), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ u64 lds64(u32 addr) {
+  u64 v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void lds2(u32 addr, u64& a, u64& b) {
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr) : "memory");
 }
 __device__ __forceinline__ void lds4(u32 addr, u64 (&v)[4]) {
   asm volatile("ld.shared.v2.u64 {%0, %1}, [%4];\n\tld.shared.v2.u64 {%2, %3}, [%4+16];"
@@ -325,7 +344,7 @@ __device__ __forceinline__ void unit_of(const TcArgs& a, u32 unit, uint4& pc, u3
 // PROF: per-warp phase timers (clock64) into a.prof -- a development build of the same kernel
 // (PE_TC_PROF=1); the production instantiation has no timers.
 template <bool PROF>
-static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
+static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 18 warps: <= 96 regs/thread (per-SMSP register file)
   extern __shared__ uint8_t dsm[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accf, acce, dfull[kDataSlots],
@@ -359,21 +378,19 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
       for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
         uint4 pc; u32 chunk;
         unit_of(a, unit, pc, chunk);
-        const u64* S0 = a.S + (u64)chunk * 2 * a.t_pad;
+        const u64* LSc = a.LS + (u64)chunk * a.t_pad * kLSRec;
         for (int g = 0; g < kRounds; ++g) {
           for (u32 kb = 0; kb < pc.y; ++kb, ++it) {
             const u32 slot = it % kDataSlots, use = it / kDataSlots;
             long long c0 = clk();
-            mbar_wait(&dempty[slot], (use & 1) ^ 1);
+            mbar_wait<256>(&dempty[slot], (use & 1) ^ 1);
             if (PROF) T[0] += clk() - c0;
             if (PROF) T[3] += 1;
             mbar_expect_tx(&dfull[slot], kDataSlot);
             const u64 q = (u64)pc.x + (u64)kb * kKB;
-            const u64* src[kD_N] = {S0 + q, S0 + a.t_pad + q, a.mV + q, a.wV + q, a.mV4 + q, a.wV4 + q,
-                                    a.m + q, a.w + q, a.m4 + q, a.w4 + q, a.m64 + q};
             const u32 dst = data0 + slot * kDataSlot;
-#pragma unroll
-            for (int d = 0; d < kD_N; ++d) bulk_g2s(dst + (u32)d * kDataArr, src[d], kDataArr, &dfull[slot]);
+            bulk_g2s(dst, LSc + q * kLSRec, kDataLS, &dfull[slot]);
+            bulk_g2s(dst + kDataLS, a.C + q * kCRec, kDataSlot - kDataLS, &dfull[slot]);
           }
         }
       }
@@ -390,11 +407,11 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
     const int tq = lane >> 2, rr = lane & 3;
     const u32 planes0 = smem_u32(smem) + (giant ? 0u : 8u * kPlane) + (u32)my_stage * kStageBytes +
                         plane_off(half * 64 + (u32)rr, (u32)tq * 4);
-    // this lane's 4 terms inside a data slot; seed / seed-step / chain-step arrays by role
-    const u32 toff = (u32)tq * 32;
-    const u32 a_seed = (giant ? (half ? kD_S1 : kD_S0) : kD_m64) * kDataArr + toff;
-    const u32 a_bm = (giant ? kD_mV : kD_m) * kDataArr + toff, a_bw = (giant ? kD_wV : kD_w) * kDataArr + toff;
-    const u32 a_sm = (giant ? kD_mV4 : kD_m4) * kDataArr + toff, a_sw = (giant ? kD_wV4 : kD_w4) * kDataArr + toff;
+    // this lane's 4 terms inside a data slot: its chain seed (record index half*4 + rr) and the
+    // stride-4 multiplier + Shoup constant (adjacent in the C record)
+    const u32 seed_off = giant ? ((u32)tq * 4 * kLSRec + half * 4 + (u32)rr) * 8
+                               : kDataLS + ((u32)tq * 4 * kCRec + half * 4 + (u32)rr) * 8;
+    const u32 mul_off = kDataLS + ((u32)tq * 4 * kCRec + (giant ? kC_mV4 : kC_m4)) * 8;
     const u64 np = a.mp.np;
     u32 it = 0;
     for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
@@ -407,23 +424,15 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
           const u32 use = it / kStages;
           const u32 slot = it % kDataSlots, duse = it / kDataSlots;
           const u32 dslot = data0 + slot * kDataSlot;
-          u64 x[4], bm[4], bw[4], sm[4], sw[4];
+          u64 x[4], sm[4], sw[4];
           long long c0 = clk();
-          mbar_wait(&dfull[slot], duse & 1);
+          mbar_wait<64>(&dfull[slot], duse & 1);
           long long c1 = clk();
           if (PROF) T[0] += c1 - c0;
-          lds4(dslot + a_seed, x);
-          lds4(dslot + a_bm, bm);
-          lds4(dslot + a_bw, bw);
-          lds4(dslot + a_sm, sm);
-          lds4(dslot + a_sw, sw);
-          if (!giant && !half) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) x[e] = 1;
-          }
-          for (int r = 0; r < rr; ++r) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) x[e] = mul_shoup4(x[e], bm[e], bw[e], np);
+          for (int e = 0; e < 4; ++e) {
+            x[e] = lds64(dslot + seed_off + (u32)e * kLSRec * 8 * (giant ? 1u : 0u) + (u32)e * kCRec * 8 * (giant ? 0u : 1u));
+            lds2(dslot + mul_off + (u32)e * kCRec * 8, sm[e], sw[e]);
           }
           // release the slot only after every value read from it has landed in registers, and
           // order those generic-proxy reads before the loader's next async-proxy (bulk) write
@@ -434,11 +443,11 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
           fence_async_smem();
           mbar_arrive(&dempty[slot]);
           c0 = clk();
-          mbar_wait(&empty[stage], (use & 1) ^ 1);
+          mbar_wait<64>(&empty[stage], (use & 1) ^ 1);
           c1 = clk();
           if (PROF) T[1] += c1 - c0;
 #pragma unroll 2
-          for (int k = 0; k < 16; ++k) {
+          for (int k = 0; k < ((PROF && a.dbg == 2) ? 0 : 16); ++k) {
             // row half*64 + rr + 4k: +4 rows = +64 bytes inside the same 8-row core-matrix pair
             store_digits(planes0 + (u32)(k >> 1) * 128u + (u32)(k & 1) * 64u, x);
 #pragma unroll
@@ -463,13 +472,13 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
       const u32 nkb = uni(pc.y);
       for (int g = 0; g < kRounds; ++g, ++round) {
         long long c0 = clk();
-        mbar_wait(&acce, (round & 1) ^ 1);
+        mbar_wait<64>(&acce, (round & 1) ^ 1);
         if (PROF) T[2] += clk() - c0;
         tc_fence_after();
         for (u32 kb = 0; kb < nkb; ++kb, ++it) {
           const u32 stage = it % kStages, use = it / kStages;
           c0 = clk();
-          mbar_wait(&full[stage], use & 1);
+          mbar_wait<32>(&full[stage], use & 1);
           if (PROF) T[0] += clk() - c0;
           if (PROF) T[3] += 1;
           tc_fence_after();
@@ -481,7 +490,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
           // tcgen05.commit tracks the MMAs its own thread issued
           __syncwarp();
           if (elect_one()) {
-            switch (g) {
+            if (!(PROF && a.dbg == 1)) switch (g) {
               case 0: issue_round<0>(tbu, db, kb == 0); break;
               case 1: issue_round<1>(tbu, db, kb == 0); break;
               case 2: issue_round<2>(tbu, db, kb == 0); break;
@@ -512,15 +521,16 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
       const u64 kbase = (u64)chunk * kChunk + (u64)u * kV;   // multiple of 8; ldp multiple of 8
       for (int g = 0; g < kRounds; ++g, ++round) {
         long long c0 = clk();
-        mbar_wait(&accf, round & 1);
+        mbar_wait<128>(&accf, round & 1);
         long long c1 = clk();
         if (PROF) T[0] += c1 - c0;
         tc_fence_after();
+        const bool nold = PROF && a.dbg == 3;   // debug: no scratch loads (timing only)
         switch (g) {
           case 0: epi_round<0>(tl, sc, true, &acce); break;
-          case 1: epi_round<1>(tl, sc, false, &acce); break;
-          case 2: epi_round<2>(tl, sc, false, &acce); break;
-          default: epi_round<3>(tl, sc, false, &acce); break;
+          case 1: epi_round<1>(tl, sc, nold, &acce); break;
+          case 2: epi_round<2>(tl, sc, nold, &acce); break;
+          default: epi_round<3>(tl, sc, nold, &acce); break;
         }
         if (PROF) T[1] += clk() - c1;
         if (PROF) T[3] += 1;
@@ -580,30 +590,40 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {
 }
 
 // ---------------------------------------------------------------- setup kernels
-// Per padded term (pe_create): m^4, m^V, m^{4V} and their Shoup constants.
-static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ m4, u64* __restrict__ w4,
-                           u64* __restrict__ mV, u64* __restrict__ wV, u64* __restrict__ mV4,
-                           u64* __restrict__ wV4, u64* __restrict__ m64, ModParams mp) {
+// Per padded term (pe_create): the C record -- baby-step chain seeds m^{64h + rr} (h*4 + rr), the
+// stride-4 chain multipliers m^4, m^{4V} and their Shoup constants.
+static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ C, ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
     const u64 mm = to_mont(m[q], mp);
     const u64 a4 = from_mont(mont_pow(mm, 4, mp), mp);
-    const u64 aV = from_mont(mont_pow(mm, kV, mp), mp);
     const u64 aV4 = from_mont(mont_pow(mm, 4 * kV, mp), mp);
-    m64[q] = from_mont(mont_pow(mm, 64, mp), mp);
-    m4[q] = a4; w4[q] = shoup_w(a4, mp.p);
-    mV[q] = aV; wV[q] = shoup_w(aV, mp.p);
-    mV4[q] = aV4; wV4[q] = shoup_w(aV4, mp.p);
+    u64* rec = C + q * kCRec;
+    u64 x = mp.r1;                                      // mont(1)
+    const u64 x64 = mont_pow(mm, 64, mp);
+    for (int rr = 0; rr < 4; ++rr) {
+      rec[rr] = from_mont(x, mp);
+      rec[4 + rr] = from_mont(mont_mul(x, x64, mp), mp);
+      x = mont_mul(x, mm, mp);
+    }
+    rec[kC_m4] = a4; rec[kC_w4] = shoup_w(a4, mp.p);
+    rec[kC_mV4] = aV4; rec[kC_wV4] = shoup_w(aV4, mp.p);
   }
 }
 
-// Per evaluation pass: S[c][h][q] = c_q m_q^{js0 + c*kChunk + h*64V}, h = 0, 1 (the giant-step
-// seeds of rows 0 and 64 of chunk c).
+// Per evaluation pass: LS records of chunk c: LS[c][q][h*4 + rr] = c_q m_q^{js0 + c*kChunk + (64h + rr) V}.
 static __global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, u64 t_pad, u32 nch, u64 js0,
-                          u64* __restrict__ S, ModParams mp) {
+                                 u64* __restrict__ LS, ModParams mp) {
   const u64 total = t_pad * nch * 2;
   for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
     const u64 ch = x / t_pad, q = x - ch * t_pad;   // ch = 2 * chunk + h
-    S[x] = seed_pow(c[q], m[q], js0 + (ch >> 1) * kChunk + (ch & 1) * (64ull * kV), mp);
+    const u64 chunk = ch >> 1, h = ch & 1;
+    u64 s = to_mont(seed_pow(c[q], m[q], js0 + chunk * kChunk + h * (64ull * kV), mp), mp);
+    const u64 mV = mont_pow(to_mont(m[q], mp), kV, mp);
+    u64* dst = LS + (chunk * t_pad + q) * kLSRec + h * 4;
+    for (int rr = 0; rr < 4; ++rr) {
+      dst[rr] = from_mont(s, mp);
+      s = mont_mul(s, mV, mp);
+    }
   }
 }
 
