@@ -62,14 +62,14 @@ def test_tc_config1_and_config2_full():
 
 
 def test_tc_pieces_of_one_large_bucket():
-    """One (x,y) bucket of 20 000 terms: 5 accumulation pieces (<= 4096 terms each, the int32
+    """One (x,y) bucket of 20 000 terms: 3 accumulation pieces (<= 8192 terms each, the u32
     exactness bound of DESIGN.md §7) summed by the fix-up; plus a 1-term and a 33-term bucket."""
     w = synth.random_small(521, P62, 8, 20_034, 5, 300, 1)
     w.exps[:, :2] = 4
     w.exps[0, :2] = (9, 9)
     w.exps[1:34, :2] = (0, 1)
     with pe.Context.from_workload(w, path=pe.PATH_TC) as ctx:
-        assert ctx.info()["tc_pieces"] >= 7
+        assert ctx.info()["tc_pieces"] == 5
     _, out = tc_eval(w)
     ref = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
     assert np.array_equal(out, ref)
