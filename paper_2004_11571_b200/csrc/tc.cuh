@@ -122,22 +122,69 @@ __device__ __forceinline__ bool elect_one() {
 // warp-uniform value (lets the compiler keep it in the uniform datapath for tcgen05 operands)
 __device__ __forceinline__ u32 uni(u32 x) { return __shfl_sync(0xffffffffu, x, 0); }
 
+// MMA with an A-operand collector mode: 0 = read A (no keep), 1 = read A and keep it in the
+// collector buffer (fill), 2 = reuse the collector's A and keep it (use), 3 = reuse and release
+// (lastuse).  Reusing A removes its 4 KB shared-memory read from all but the first MMA of a run.
+template <int COL>
+__device__ __forceinline__ void mma_u8c(u32 dtmem, uint64_t ad, uint64_t bd, u32 acc) {
+  if (COL == 0)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
+                 :: "r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
+  else if (COL == 1)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n\t}\n"
+                 :: "r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
+  else if (COL == 2)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::use [%0], %1, %2, %3, p;\n\t}\n"
+                 :: "r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
+  else
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}\n"
+                 :: "r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
+}
+
+// digit pair (s, t = d - s) of diagonal slot di exists in round G
+__host__ __device__ constexpr bool pair_ok(int G, int di, int sd) {
+  return group_diag(G, di) >= 0 && group_diag(G, di) - sd >= 0 && group_diag(G, di) - sd <= 7;
+}
+__host__ __device__ constexpr int run_len(int G, int sd) {
+  return (pair_ok(G, 0, sd) ? 1 : 0) + (pair_ok(G, 1, sd) ? 1 : 0) + (pair_ok(G, 2, sd) ? 1 : 0) +
+         (pair_ok(G, 3, sd) ? 1 : 0);
+}
+// position of slot di inside the run of plane sd when the slots are visited in the rotated order
+// di = (sd + k) & 3, k = 0..3 (rotation keeps consecutive MMAs on different accumulators)
+__host__ __device__ constexpr int run_pos(int G, int sd, int di) {
+  return ((pair_ok(G, (sd + 0) & 3, sd) && ((sd + 0) & 3) != di && (((di - sd) & 3) > 0)) ? 1 : 0) +
+         ((pair_ok(G, (sd + 1) & 3, sd) && ((sd + 1) & 3) != di && (((di - sd) & 3) > 1)) ? 1 : 0) +
+         ((pair_ok(G, (sd + 2) & 3, sd) && ((sd + 2) & 3) != di && (((di - sd) & 3) > 2)) ? 1 : 0);
+}
+
 // The 16 digit-pair MMAs of round G on one smem stage (descriptor db = plane 0 of the stage),
-// round-robin over the round's diagonals so consecutive MMAs write different TMEM accumulators
-// (back-to-back MMAs into one accumulator serialise).  Fully unrolled: every operand offset is
-// a compile-time constant.
+// grouped by L plane s so the A operand (L_s) is read from shared memory once per K-block and
+// reused from the collector buffer; within a plane's run the round's diagonals are visited in a
+// rotated order so consecutive MMAs write different TMEM accumulators.  Fully unrolled: every
+// operand offset and collector mode is a compile-time constant.
 template <int G>
 __device__ __forceinline__ void issue_round(u32 tb, uint64_t db, bool first_kb) {
 #pragma unroll
-  for (int step = 0; step < 8; ++step) {
+  for (int sd = 0; sd < 8; ++sd) {
 #pragma unroll
-    for (int di = 0; di < 4; ++di) {
-      const int d = group_diag(G, di);
-      const int s0 = d > 7 ? d - 7 : 0, s1 = d < 7 ? d : 7;
-      if (d >= 0 && s0 + step <= s1) {
-        const int sd = s0 + step;
-        mma_u8(tb + (u32)di * kV, db + (uint64_t)((u32)sd * (kPlane >> 4)),
-               db + (uint64_t)((u32)(8 + d - sd) * (kPlane >> 4)), (!first_kb || step > 0) ? 1u : 0u);
+    for (int k = 0; k < 4; ++k) {
+      const int di = (sd + k) & 3;
+      if (pair_ok(G, di, sd)) {
+        const int d = group_diag(G, di);
+        const int n = run_len(G, sd), pos = run_pos(G, sd, di);
+        const int s0 = d > 7 ? d - 7 : 0;
+        const u32 acc = (!first_kb || sd > s0) ? 1u : 0u;   // first pair of diagonal d at kb 0 overwrites
+        const u32 dt = tb + (u32)di * kV;
+        const uint64_t ad = db + (uint64_t)((u32)sd * (kPlane >> 4));
+        const uint64_t bd = db + (uint64_t)((u32)(8 + d - sd) * (kPlane >> 4));
+        if (n == 1) mma_u8c<0>(dt, ad, bd, acc);
+        else if (pos == 0) mma_u8c<1>(dt, ad, bd, acc);
+        else if (pos == n - 1) mma_u8c<3>(dt, ad, bd, acc);
+        else mma_u8c<2>(dt, ad, bd, acc);
       }
     }
   }
