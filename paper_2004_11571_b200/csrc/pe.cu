@@ -125,7 +125,7 @@ struct pe_ctx {
   u32* d_tc_slot_start = nullptr;
   u64* d_seed = nullptr;
   size_t seed_elems = 0;
-  u32* d_tc_scratch = nullptr;   // k_tc per-CTA 160-bit running sums (n_sm x 5 x 16384 u32)
+  u32* d_tc_scratch = nullptr;   // k_tc per-CTA drained diagonal sums (n_sm x 2 x 15 x 16384 u32)
   size_t partial_cap_bytes = (size_t)1 << 30;
   // kernel timing (pe_set_timing / pe_kernel_stats)
   bool timing = false;
@@ -600,7 +600,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     CU(cudaMallocAsync((void**)&h->d_seed, (size_t)h->t_pad * nch_max * 8 * sizeof(u64), s));
     h->seed_elems = (size_t)h->t_pad * nch_max * 8;
   }
-  if (!h->d_tc_scratch) CU(cudaMallocAsync((void**)&h->d_tc_scratch, (size_t)h->n_sm * 5 * tc::kChunk * sizeof(u32), s));
+  if (!h->d_tc_scratch) CU(cudaMallocAsync((void**)&h->d_tc_scratch, (size_t)h->n_sm * 2 * 15 * tc::kChunk * sizeof(u32), s));
   CU(cudaFuncSetAttribute(tc::k_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   CU(cudaFuncSetAttribute(tc::k_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   for (u64 k0 = 0; k0 < T; k0 += Tp) {

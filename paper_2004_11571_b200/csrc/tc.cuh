@@ -25,17 +25,18 @@
 // M=128, K=32 i8 MMA issues every ~136 clk for any N <= 256 (scripts/tc_probe.cu), so N = 128
 // costs 2x the N = 256 MACs/clk but balances the IMAD-bound generation.
 //
-// Warp roles (one CTA per SM, persistent, static round-robin over units = (piece, chunk)):
+// Warp roles (one CTA per SM, 16 warps = 4 per SMSP, persistent, static round-robin over units =
+// (piece, chunk)):
 //   warps 0-3  epilogue: tcgen05.ld the round's diagonals (TMEM lane = u), fold them exactly into
 //              160-bit running sums (shift/add, per-CTA L2-resident scratch), release TMEM; after
-//              the unit's last round one reduction mod p per point -> partial[slot][chunk*16384 + u*128 + v]
-//   warp  4    TMEM allocator + single-thread MMA issuer (tcgen05.mma.cta_group::1.kind::i8)
-//   warps 5-16 producers, 4 per smem stage: two L warps and two R warps generate one K-block's
+//              the unit's last round one reduction mod p per point -> partial[slot][chunk*16384 + u*128 + v].
+//              Warp 0 is also the TMEM allocator and the MMA issuer (tcgen05.mma.cta_group::1.kind::i8,
+//              elect.sync leader): a round's MMAs and its epilogue cannot overlap anyway.
+//   warps 4-15 producers, 4 per smem stage: two L warps and two R warps generate one K-block's
 //              128 giant-step / 128 baby-step values of 32 terms (64 rows each) with Shoup
 //              products (4 chains per lane, seeded from precomputed chain seeds) and write their
-//              8 byte planes in the no-swizzle K-major UMMA layout.
-//   warp  17   loader: TMA bulk copies of each K-block's per-term seeds / multipliers into an
-//              smem ring ahead of the producers.
+//              8 byte planes in the no-swizzle K-major UMMA layout; each group's first lane also
+//              issues the TMA bulk copies of the group's next K-block of per-term records.
 #pragma once
 #include "modcore.cuh"
 
@@ -50,7 +51,7 @@ constexpr int kStages = 3;
 constexpr u32 kPieceMax = 8192;           // terms per accumulation: 8192 * 8 * 255^2 < 2^32 (the s32
                                           // accumulator wraps mod 2^32, saturate = 0; read as u32)
 constexpr u32 kLBO = 2048 + 64;           // bytes between the two 16-byte K chunks of a plane (+64: bank spread)
-constexpr u32 kPlane = 2 * kLBO;          // one digit plane: 128 rows x 32 bytes (+ pad)
+constexpr u32 kPlane = kLBO + 2048;       // one digit plane: 128 rows x 32 bytes (+ pad between the chunks)
 constexpr u32 kStageBytes = 16 * kPlane;  // 8 L planes + 8 R planes
 // per-K-block term data streamed by the loader warp (TMA bulk copies): 11 arrays x 32 terms
 // Per-term records (array of structs, so one K-block's data is two contiguous bulk copies):
@@ -61,13 +62,13 @@ constexpr int kLSRec = 8, kCRec = 12;
 enum { kC_m4 = 8, kC_w4 = 9, kC_mV4 = 10, kC_wV4 = 11 };
 constexpr u32 kDataLS = kKB * kLSRec * 8;        // 2048 B
 constexpr u32 kDataSlot = kDataLS + kKB * kCRec * 8;   // 5120 B
-constexpr int kDataSlots = 5;                   // ring depth (K-blocks ahead of the producers)
+constexpr int kDataSlots = 6;                   // 2 per producer group: current + next K-block
 constexpr u32 kSmemBytes = kStages * kStageBytes + kDataSlots * kDataSlot + 1024;
 constexpr int kRounds = 4;
 constexpr int kProdPerStage = 4;          // L rows 0-63, L rows 64-127, R rows 0-63, R rows 64-127
-constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5;
-constexpr int kLoadWarp = kProdWarp0 + kStages * kProdPerStage;
-constexpr int kThreads = (kLoadWarp + 1) * 32;
+constexpr int kEpiWarps = 4, kMmaWarp = 0, kProdWarp0 = 4;   // warp 0: epilogue + MMA issue
+constexpr int kThreads = (kProdWarp0 + kStages * kProdPerStage) * 32;   // 16 warps: 4 per SMSP
+static_assert(kRounds == kEpiWarps, "round g's MMAs are issued by epilogue warp g");
 // diagonal groups: <= 4 diagonals (TMEM: 4 x 128 columns), 16 digit pairs each
 __host__ __device__ constexpr int group_diag(int g, int di) {
   return g == 0 ? (di == 0 ? 7 : di == 1 ? 6 : di == 2 ? 0 : -1)
@@ -87,7 +88,7 @@ struct TcArgs {
   u32 npieces, nunits, npts;
   u64 Wd[15];            // 2^{8d} mod p  (Wd[8] = 2^64, Wd[12] = 2^96, Wd[14] -> see C128)
   u64 C128;              // 2^128 mod p
-  u32* scratch;          // per CTA: 5 x kChunk u32 (160-bit exact running sums of a unit, L2-resident)
+  u32* scratch;          // per CTA: 2 (ping-pong by unit) x 15 diagonals x kChunk u32 drained diagonal sums
   ModParams mp;
   unsigned long long* prof;  // optional phase timers [gridDim][warps][4] (PE_TC_PROF=1), else null
   int dbg;                   // development only (PE_TC_DEBUG, PROF build): 1 = skip the MMAs,
@@ -328,30 +329,14 @@ __device__ __forceinline__ void fold_add(u32 (&X)[5], u32 Dv) {
   X[4] = x4;
 }
 
-// One round of the epilogue for thread row u: the round's diagonals (TMEM columns di*128 + v)
-// folded exactly into the unit's 160-bit running sums (scratch, SoA: word w at w*kChunk + u*128 + v).
-// TMEM is released (acce) as soon as the last block has been read.
+// Epilogue critical part: drain round G's diagonals of thread row u from TMEM into the unit's raw
+// buffer (raw[d][u][v], u32: the diagonal sums themselves) and release TMEM (acce) as soon as the
+// last block is in registers -- only tcgen05.ld and fire-and-forget stores, so the MMA warp can
+// start the next round almost at once.
 template <int G>
-__device__ __forceinline__ void epi_round(u32 tl, u32* __restrict__ sc, bool first, uint64_t* acce) {
+__device__ __forceinline__ void epi_drain(u32 tl, u32* __restrict__ raw_u, uint64_t* acce) {
 #pragma unroll 1
   for (u32 v0 = 0; v0 < (u32)kV; v0 += 8) {
-    u32 X[5][8];
-    if (first) {
-#pragma unroll
-      for (int w = 0; w < 5; ++w)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) X[w][j] = 0;
-    } else {
-#pragma unroll
-      for (int w = 0; w < 5; ++w) {
-        const uint4* p4 = (const uint4*)(sc + (u32)w * kChunk + v0);
-        const uint4 q0 = p4[0], q1 = p4[1];
-        X[w][0] = q0.x; X[w][1] = q0.y; X[w][2] = q0.z; X[w][3] = q0.w;
-        X[w][4] = q1.x; X[w][5] = q1.y; X[w][6] = q1.z; X[w][7] = q1.w;
-      }
-    }
-    // TMEM loads after the scratch loads, waited on immediately: the destination registers must
-    // not be touched (even copied) before tcgen05.wait::ld
     u32 D[4][8];
 #pragma unroll
     for (int di = 0; di < 4; ++di)
@@ -365,19 +350,26 @@ __device__ __forceinline__ void epi_round(u32 tl, u32* __restrict__ sc, bool fir
       mbar_arrive(acce);
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      u32 x[5] = {X[0][j], X[1][j], X[2][j], X[3][j], X[4][j]};
-      fold_point<G>(x, D[0][j], D[1][j], D[2][j], group_diag(G, 3) >= 0 ? D[3][j] : 0u);
-#pragma unroll
-      for (int w = 0; w < 5; ++w) X[w][j] = x[w];
-    }
-#pragma unroll
-    for (int w = 0; w < 5; ++w) {
-      uint4* p4 = (uint4*)(sc + (u32)w * kChunk + v0);
-      p4[0] = make_uint4(X[w][0], X[w][1], X[w][2], X[w][3]);
-      p4[1] = make_uint4(X[w][4], X[w][5], X[w][6], X[w][7]);
+    for (int di = 0; di < 4; ++di) {
+      constexpr int dummy = 0;
+      (void)dummy;
+      if (group_diag(G, di) >= 0) {
+        uint4* p4 = (uint4*)(raw_u + (u32)group_diag(G, di) * (kU * kV) + v0);
+        p4[0] = make_uint4(D[di][0], D[di][1], D[di][2], D[di][3]);
+        p4[1] = make_uint4(D[di][4], D[di][5], D[di][6], D[di][7]);
+      }
     }
   }
+}
+
+// X (160-bit, 5 x u32) = sum_{d<15} D_d 2^{8d}, exactly (< 2^145): composed in 128-bit C
+// arithmetic (the compiler owns the carries) + a top word.
+template <int D8>
+__device__ __forceinline__ void fold_in(u128_t& lo, u32& x4, u32 Dv) {
+  const u128_t add = (u128_t)Dv << D8;
+  const u32 spill = D8 > 96 ? (u32)(Dv >> (128 - D8 > 31 ? 31 : 128 - D8)) : 0u;
+  lo += add;
+  x4 += spill + (lo < add ? 1u : 0u);
 }
 
 __device__ __forceinline__ long long clk() { return clock64(); }
@@ -390,12 +382,43 @@ __device__ __forceinline__ void unit_of(const TcArgs& a, u32 unit, uint4& pc, u3
 
 // PROF: per-warp phase timers (clock64) into a.prof -- a development build of the same kernel
 // (PE_TC_PROF=1); the production instantiation has no timers.
+// Walks one CTA's K-block sequence: units blockIdx.x, +gridDim.x, ...; per unit 4 rounds; per round
+// the piece's K-blocks.
+struct KIter {
+  u32 unit, kb, nkb, q0, chunk;
+  int g;
+  bool valid;
+  __device__ __forceinline__ void load(const TcArgs& a) {
+    valid = unit < a.nunits;
+    if (valid) {
+      uint4 pc;
+      unit_of(a, unit, pc, chunk);
+      nkb = pc.y;
+      q0 = pc.x;
+    }
+  }
+  __device__ __forceinline__ void init(const TcArgs& a) { unit = blockIdx.x; kb = 0; g = 0; load(a); }
+  __device__ __forceinline__ void next(const TcArgs& a) {
+    if (++kb == nkb) {
+      kb = 0;
+      if (++g == kRounds) { g = 0; unit += gridDim.x; load(a); }
+    }
+  }
+};
+
+// The two TMA bulk copies of one K-block's per-term records into a data slot.
+__device__ __forceinline__ void load_kblock(const TcArgs& a, const KIter& k, u32 dst, uint64_t* bar) {
+  const u64 q = (u64)k.q0 + (u64)k.kb * kKB;
+  mbar_expect_tx(bar, kDataSlot);
+  bulk_g2s(dst, a.LS + ((u64)k.chunk * a.t_pad + q) * kLSRec, kDataLS, bar);
+  bulk_g2s(dst + kDataLS, a.C + q * kCRec, kDataSlot - kDataLS, bar);
+}
+
 template <bool PROF>
-static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 18 warps: <= 96 regs/thread (per-SMSP register file)
+static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 warps: <= 128 regs/thread
   extern __shared__ uint8_t dsm[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accf, acce, dfull[kDataSlots],
-      dempty[kDataSlots];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accf, acce, dfull[kDataSlots];
   __shared__ u32 tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -403,7 +426,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 18 w
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 32 * kProdPerStage); mbar_init(&empty[s], 1); }
     mbar_init(&accf, 1);
     mbar_init(&acce, 32 * kEpiWarps);
-    for (int s = 0; s < kDataSlots; ++s) { mbar_init(&dfull[s], 1); mbar_init(&dempty[s], 32 * kProdPerStage); }
+    for (int s = 0; s < kDataSlots; ++s) mbar_init(&dfull[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
@@ -416,208 +439,196 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 18 w
   const u32 tb = tmem_base;
   long long T[4] = {0, 0, 0, 0};   // phase timers (a.prof)
   const long long t_start = clk();
-
   const u32 data0 = smem_u32(smem) + kStages * kStageBytes;
-  if (warp == kLoadWarp) {
-    // ------------------------------------------------------------ loader (TMA bulk copies)
-    if (lane == 0) {
-      u32 it = 0;
-      for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
-        uint4 pc; u32 chunk;
-        unit_of(a, unit, pc, chunk);
-        const u64* LSc = a.LS + (u64)chunk * a.t_pad * kLSRec;
-        for (int g = 0; g < kRounds; ++g) {
-          for (u32 kb = 0; kb < pc.y; ++kb, ++it) {
-            const u32 slot = it % kDataSlots, use = it / kDataSlots;
-            long long c0 = clk();
-            mbar_wait<256>(&dempty[slot], (use & 1) ^ 1);
-            if (PROF) T[0] += clk() - c0;
-            if (PROF) T[3] += 1;
-            mbar_expect_tx(&dfull[slot], kDataSlot);
-            const u64 q = (u64)pc.x + (u64)kb * kKB;
-            const u32 dst = data0 + slot * kDataSlot;
-            bulk_g2s(dst, LSc + q * kLSRec, kDataLS, &dfull[slot]);
-            bulk_g2s(dst + kDataLS, a.C + q * kCRec, kDataSlot - kDataLS, &dfull[slot]);
-          }
-        }
-      }
-    }
-  } else if (warp >= kProdWarp0) {
+
+  if (warp >= kProdWarp0) {
     // ------------------------------------------------------------ producers
     // 4 warps per stage: (giant | baby) x (rows 0-63 | rows 64-127).  Lane = (tq, rr): terms
     // tq*4 .. tq*4+3 of the K-block, rows half*64 + rr + 4k (k < 16), i.e. 4 independent
-    // Shoup chains of stride 4 per lane.  Term data comes from the loader's smem ring.
+    // Shoup chains of stride 4 per lane.  Each group owns two data slots; its first warp's lane 0
+    // brings the group's NEXT K-block's per-term records in with TMA while the current one is
+    // being generated (no loader warp: the 16 warps fill the 4 SMSPs evenly).
     const int pw = warp - kProdWarp0;
     const int my_stage = pw / kProdPerStage, sub = pw % kProdPerStage;
     const bool giant = sub < 2;
     const u32 half = (u32)(sub & 1);
+    const bool leader = sub == 0 && lane == 0;
     const int tq = lane >> 2, rr = lane & 3;
     const u32 planes0 = smem_u32(smem) + (giant ? 0u : 8u * kPlane) + (u32)my_stage * kStageBytes +
                         plane_off(half * 64 + (u32)rr, (u32)tq * 4);
-    // this lane's 4 terms inside a data slot: its chain seed (record index half*4 + rr) and the
-    // stride-4 multiplier + Shoup constant (adjacent in the C record)
     const u32 seed_off = giant ? ((u32)tq * 4 * kLSRec + half * 4 + (u32)rr) * 8
                                : kDataLS + ((u32)tq * 4 * kCRec + half * 4 + (u32)rr) * 8;
     const u32 mul_off = kDataLS + ((u32)tq * 4 * kCRec + (giant ? kC_mV4 : kC_m4)) * 8;
+    const u32 slot0 = (u32)my_stage * 2;
     const u64 np = a.mp.np;
-    u32 it = 0;
-    for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
-      uint4 pc; u32 chunk;
-      unit_of(a, unit, pc, chunk);
-      for (int g = 0; g < kRounds; ++g) {
-        for (u32 kb = 0; kb < pc.y; ++kb, ++it) {
-          const u32 stage = it % kStages;
-          if ((int)stage != my_stage) continue;
-          const u32 use = it / kStages;
-          const u32 slot = it % kDataSlots, duse = it / kDataSlots;
-          const u32 dslot = data0 + slot * kDataSlot;
-          u64 x[4], sm[4], sw[4];
-          long long c0 = clk();
-          mbar_wait<64>(&dfull[slot], duse & 1);
-          long long c1 = clk();
-          if (PROF) T[0] += c1 - c0;
+    KIter cur, ahead;
+    cur.init(a);
+    ahead.init(a);
+    for (int i = 0; i < my_stage; ++i) ahead.next(a);                 // the group's first K-block
+    if (leader && ahead.valid) load_kblock(a, ahead, data0 + slot0 * kDataSlot, &dfull[slot0]);
+    for (int i = 0; i < kStages; ++i) ahead.next(a);                  // ... and its second
+    u32 guse = 0;
+    for (u32 it = 0; cur.valid; ++it, cur.next(a)) {
+      const u32 stage = it % kStages;
+      if ((int)stage != my_stage) continue;
+      const u32 use = it / kStages;
+      long long c0 = clk();
+      mbar_wait<64>(&empty[stage], (use & 1) ^ 1);
+      long long c1 = clk();
+      if (PROF) T[1] += c1 - c0;
+      // the other slot held K-block guse-1, which every warp of the group consumed before the
+      // stage could be released: refill it with the group's next K-block
+      if (leader && ahead.valid)
+        load_kblock(a, ahead, data0 + (slot0 + ((guse + 1) & 1)) * kDataSlot, &dfull[slot0 + ((guse + 1) & 1)]);
+      const u32 slot = slot0 + (guse & 1);
+      const u32 dslot = data0 + slot * kDataSlot;
+      u64 x[4], sm[4], sw[4];
+      c0 = clk();
+      mbar_wait<64>(&dfull[slot], (guse >> 1) & 1);
+      c1 = clk();
+      if (PROF) T[0] += c1 - c0;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            x[e] = lds64(dslot + seed_off + (u32)e * kLSRec * 8 * (giant ? 1u : 0u) + (u32)e * kCRec * 8 * (giant ? 0u : 1u));
-            lds2(dslot + mul_off + (u32)e * kCRec * 8, sm[e], sw[e]);
-          }
-          // release the slot only after every value read from it has landed in registers, and
-          // order those generic-proxy reads before the loader's next async-proxy (bulk) write
-          {
-            u64 dep = sm[0] ^ sm[1] ^ sm[2] ^ sm[3] ^ sw[0] ^ sw[1] ^ sw[2] ^ sw[3] ^ x[0] ^ x[1] ^ x[2] ^ x[3];
-            asm volatile("" :: "l"(dep));
-          }
-          fence_async_smem();
-          mbar_arrive(&dempty[slot]);
-          c0 = clk();
-          mbar_wait<64>(&empty[stage], (use & 1) ^ 1);
-          c1 = clk();
-          if (PROF) T[1] += c1 - c0;
+      for (int e = 0; e < 4; ++e) {
+        x[e] = lds64(dslot + seed_off + (u32)e * kLSRec * 8 * (giant ? 1u : 0u) + (u32)e * kCRec * 8 * (giant ? 0u : 1u));
+        lds2(dslot + mul_off + (u32)e * kCRec * 8, sm[e], sw[e]);
+      }
 #pragma unroll 2
-          for (int k = 0; k < ((PROF && a.dbg == 2) ? 0 : 16); ++k) {
-            // row half*64 + rr + 4k: +4 rows = +64 bytes inside the same 8-row core-matrix pair
-            store_digits(planes0 + (u32)(k >> 1) * 128u + (u32)(k & 1) * 64u, x);
+      for (int k = 0; k < ((PROF && a.dbg == 2) ? 0 : 16); ++k) {
+        // row half*64 + rr + 4k: +4 rows = +64 bytes inside the same 8-row core-matrix pair
+        store_digits(planes0 + (u32)(k >> 1) * 128u + (u32)(k & 1) * 64u, x);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) x[e] = mul_shoup4(x[e], sm[e], sw[e], np);
-          }
-          fence_async_smem();
-          mbar_arrive(&full[stage]);
-          if (PROF) T[2] += clk() - c1;
-          if (PROF) T[3] += 1;
-        }
+        for (int e = 0; e < 4; ++e) x[e] = mul_shoup4(x[e], sm[e], sw[e], np);
       }
-    }
-  } else if (warp == kMmaWarp) {
-    // ------------------------------------------------------------ MMA issuer
-    // The whole warp runs the control flow (operands stay warp-uniform); one elected lane issues.
-    u32 it = 0, round = 0;
-    const u32 tbu = uni(tb);
-    const uint64_t d0 = smem_desc(uni(smem_u32(smem)));
-    for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
-      uint4 pc; u32 chunk;
-      unit_of(a, unit, pc, chunk);
-      const u32 nkb = uni(pc.y);
-      for (int g = 0; g < kRounds; ++g, ++round) {
-        long long c0 = clk();
-        mbar_wait<64>(&acce, (round & 1) ^ 1);
-        if (PROF) T[2] += clk() - c0;
-        tc_fence_after();
-        for (u32 kb = 0; kb < nkb; ++kb, ++it) {
-          const u32 stage = it % kStages, use = it / kStages;
-          c0 = clk();
-          mbar_wait<32>(&full[stage], use & 1);
-          if (PROF) T[0] += clk() - c0;
-          if (PROF) T[3] += 1;
-          tc_fence_after();
-          const uint64_t db = d0 + (uint64_t)((stage * kStageBytes) >> 4);
-          // converge first so elect.sync picks the same leader (lane 0) every time: a
-          // tcgen05.commit tracks only the MMAs its own thread issued
-          __syncwarp();
-          // converge first so elect.sync picks the same leader (lane 0) every time: a
-          // tcgen05.commit tracks the MMAs its own thread issued
-          __syncwarp();
-          if (elect_one()) {
-            if (!(PROF && a.dbg == 1)) switch (g) {
-              case 0: issue_round<0>(tbu, db, kb == 0); break;
-              case 1: issue_round<1>(tbu, db, kb == 0); break;
-              case 2: issue_round<2>(tbu, db, kb == 0); break;
-              default: issue_round<3>(tbu, db, kb == 0); break;
-            }
-            if (kb + 1 == nkb) mma_commit(&accf);   // accumulators complete after this K-block
-            mma_commit(&empty[stage]);
-          }
-          __syncwarp();
-        }
-      }
+      fence_async_smem();
+      mbar_arrive(&full[stage]);
+      if (PROF) T[2] += clk() - c1;
+      if (PROF) T[3] += 1;
+      for (int i = 0; i < kStages; ++i) ahead.next(a);
+      ++guse;
     }
   } else {
-    // ------------------------------------------------------------ epilogue
-    // Per round: TMEM -> exact 160-bit fold into this CTA's scratch (ALU only), release TMEM.
-    // After the unit's last round: one reduction mod p per point -> the piece's partial row,
-    // overlapping the next unit's first round of MMAs.
+    // ------------------------------------------------------------ epilogue (+ MMA issue in warp 0)
+    // MMA issue and TMEM drain alternate (TMEM holds one round), so warp 0 issues a round's MMAs
+    // (converged warp, elect.sync leader) and then drains its lane quarter.  Per round every
+    // epilogue warp only moves its 4 diagonals from TMEM to the unit's raw buffer (ping-pong by
+    // unit) and releases TMEM.  After the unit's 4 rounds warps 1-3 fold all 15 diagonals
+    // exactly (X = sum D_d 2^{8d}) and reduce mod p into the piece's partial row -- warp 1 also
+    // for warp 0's rows -- while warp 0 is already issuing the next unit's MMAs.
     const u32 u = (u32)(warp * 32 + lane);
     const u32 tl = tb + ((u32)(warp * 32) << 16);
     const ModParams mp = a.mp;
-    u32* sc = a.scratch + (u64)blockIdx.x * 5 * kChunk + (u64)u * kV;
+    u32* raw_cta = a.scratch + (u64)blockIdx.x * 2 * 15 * (kU * kV);
     const u64 C64 = a.Wd[8], C96 = a.Wd[12], C128 = a.C128;
-    u32 round = 0;
-    for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
+    const u32 tbu = uni(tb);
+    const uint64_t d0 = smem_desc(uni(smem_u32(smem)));
+    u32 round = 0, it = 0, nunit = 0;
+    for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x, ++nunit) {
       uint4 pc; u32 chunk;
       unit_of(a, unit, pc, chunk);
+      const u32 nkb = uni(pc.y);
       u64* prow = a.partial + (u64)pc.z * a.ldp;
-      const u64 kbase = (u64)chunk * kChunk + (u64)u * kV;   // multiple of 8; ldp multiple of 8
+      u32* raw = raw_cta + (u64)(nunit & 1) * 15 * (kU * kV);
       for (int g = 0; g < kRounds; ++g, ++round) {
+        // round g's MMAs are issued by epilogue warp g (one per SMSP: the issue cost rotates over
+        // the 4 SMSPs instead of slowing the producers that share SMSP 0)
+        if (warp != g) it += nkb;
+        if (warp == g) {
+          long long c0 = clk();
+          mbar_wait<32>(&acce, (round & 1) ^ 1);
+          if (PROF) T[2] += clk() - c0;
+          tc_fence_after();
+          for (u32 kb = 0; kb < nkb; ++kb, ++it) {
+            const u32 stage = it % kStages, use = it / kStages;
+            c0 = clk();
+            mbar_wait<32>(&full[stage], use & 1);
+            if (PROF) T[1] += clk() - c0;
+            tc_fence_after();
+            const uint64_t db = d0 + (uint64_t)((stage * kStageBytes) >> 4);
+            // converge first so elect.sync picks the same leader (lane 0) every time: a
+            // tcgen05.commit tracks the MMAs its own thread issued
+            __syncwarp();
+            if (elect_one()) {
+              if (!(PROF && a.dbg == 1)) switch (g) {
+                case 0: issue_round<0>(tbu, db, kb == 0); break;
+                case 1: issue_round<1>(tbu, db, kb == 0); break;
+                case 2: issue_round<2>(tbu, db, kb == 0); break;
+                default: issue_round<3>(tbu, db, kb == 0); break;
+              }
+              if (kb + 1 == nkb) mma_commit(&accf);   // accumulators complete after this K-block
+              mma_commit(&empty[stage]);
+            }
+            __syncwarp();
+          }
+          // (this raw buffer was last read two units ago by warp 1's fold of warp 0's rows; that
+          // fold precedes warp 1's drain of the previous unit's last round, which this warp has
+          // already waited for through acce -- no extra barrier needed)
+        }
         long long c0 = clk();
-        mbar_wait<128>(&accf, round & 1);
+        mbar_wait<64>(&accf, round & 1);
         long long c1 = clk();
         if (PROF) T[0] += c1 - c0;
         tc_fence_after();
-        const bool nold = PROF && a.dbg == 3;   // debug: no scratch loads (timing only)
+        u32* raw_u = raw + (u64)u * kV;
         switch (g) {
-          case 0: epi_round<0>(tl, sc, true, &acce); break;
-          case 1: epi_round<1>(tl, sc, nold, &acce); break;
-          case 2: epi_round<2>(tl, sc, nold, &acce); break;
-          default: epi_round<3>(tl, sc, nold, &acce); break;
+          case 0: epi_drain<0>(tl, raw_u, &acce); break;
+          case 1: epi_drain<1>(tl, raw_u, &acce); break;
+          case 2: epi_drain<2>(tl, raw_u, &acce); break;
+          default: epi_drain<3>(tl, raw_u, &acce); break;
         }
-        if (PROF) T[1] += clk() - c1;
+        if (PROF && warp != g) T[1] += clk() - c1;
         if (PROF) T[3] += 1;
       }
       // X mod p = (x0 + x1 2^32) + x2 (2^64 mod p) + x3 (2^96 mod p) + x4 (2^128 mod p)  (< 2^96)
       long long c2 = clk();
+      for (int pass = 0; pass < (warp == 1 ? 2 : (warp == kMmaWarp ? 0 : 1)); ++pass) {
+        u32 ur = u;
+        if (pass == 1) {                 // warp 1: warp 0's rows, once all 4 warps drained round 3
+          mbar_wait<32>(&acce, (round - 1) & 1);
+          ur = (u32)lane;
+        }
+        const u32* rr_ = raw + (u64)ur * kV;
+        const u64 kbase = (u64)chunk * kChunk + (u64)ur * kV;   // multiple of 8; ldp multiple of 8
 #pragma unroll 1
-      for (u32 v0 = 0; v0 < (u32)kV; v0 += 8) {
-        u32 X[5][8];
+        for (u32 v0 = 0; v0 < (u32)kV; v0 += 4) {
+          u32 D[15][4];
 #pragma unroll
-        for (int w = 0; w < 5; ++w) {
-          const uint4* p4 = (const uint4*)(sc + (u32)w * kChunk + v0);
-          const uint4 q0 = p4[0], q1 = p4[1];
-          X[w][0] = q0.x; X[w][1] = q0.y; X[w][2] = q0.z; X[w][3] = q0.w;
-          X[w][4] = q1.x; X[w][5] = q1.y; X[w][6] = q1.z; X[w][7] = q1.w;
-        }
-        u64 res[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          u64 lo = ((u64)X[1][j] << 32) | X[0][j], hi = 0;
-          const u64 terms[3][2] = {{X[2][j], C64}, {X[3][j], C96}, {X[4][j], C128}};
-#pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            const u64 p0 = terms[q][0] * lo32(terms[q][1]);
-            const u64 p1 = terms[q][0] * hi32(terms[q][1]);
-            const u64 add_lo = p0 + (p1 << 32);
-            const u64 add_hi = (p1 >> 32) + (add_lo < p0 ? 1ull : 0ull);
-            lo += add_lo;
-            hi += add_hi + (lo < add_lo ? 1ull : 0ull);
+          for (int d = 0; d < 15; ++d) {
+            const uint4 q = *(const uint4*)(rr_ + (u32)d * (kU * kV) + v0);
+            D[d][0] = q.x; D[d][1] = q.y; D[d][2] = q.z; D[d][3] = q.w;
           }
-          res[j] = reduce128(hi, lo, mp);
-        }
-        if (kbase + v0 + 8 <= a.npts) {
-          ulonglong2* dst = (ulonglong2*)(prow + kbase + v0);
+          u64 res[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dst[j] = make_ulonglong2(res[2 * j], res[2 * j + 1]);
-        } else {
+          for (int j = 0; j < 4; ++j) {
+            u128_t acc = 0;
+            u32 x4 = 0;
+            fold_in<0>(acc, x4, D[0][j]);   fold_in<8>(acc, x4, D[1][j]);   fold_in<16>(acc, x4, D[2][j]);
+            fold_in<24>(acc, x4, D[3][j]);  fold_in<32>(acc, x4, D[4][j]);  fold_in<40>(acc, x4, D[5][j]);
+            fold_in<48>(acc, x4, D[6][j]);  fold_in<56>(acc, x4, D[7][j]);  fold_in<64>(acc, x4, D[8][j]);
+            fold_in<72>(acc, x4, D[9][j]);  fold_in<80>(acc, x4, D[10][j]); fold_in<88>(acc, x4, D[11][j]);
+            fold_in<96>(acc, x4, D[12][j]); fold_in<104>(acc, x4, D[13][j]); fold_in<112>(acc, x4, D[14][j]);
+            u64 lo = (u64)acc, hi = 0;
+            const u64 x2 = (u64)(acc >> 64) & 0xffffffffull, x3 = (u64)(acc >> 96);
+            const u64 terms[3][2] = {{x2, C64}, {x3, C96}, {(u64)x4, C128}};
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (kbase + v0 + j < a.npts) prow[kbase + v0 + j] = res[j];
+            for (int q = 0; q < 3; ++q) {
+              const u64 p0 = terms[q][0] * lo32(terms[q][1]);
+              const u64 p1 = terms[q][0] * hi32(terms[q][1]);
+              const u64 add_lo = p0 + (p1 << 32);
+              const u64 add_hi = (p1 >> 32) + (add_lo < p0 ? 1ull : 0ull);
+              lo += add_lo;
+              hi += add_hi + (lo < add_lo ? 1ull : 0ull);
+            }
+            res[j] = reduce128(hi, lo, mp);
+          }
+          if (kbase + v0 + 4 <= a.npts) {
+            ulonglong2* dst = (ulonglong2*)(prow + kbase + v0);
+            dst[0] = make_ulonglong2(res[0], res[1]);
+            dst[1] = make_ulonglong2(res[2], res[3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (kbase + v0 + j < a.npts) prow[kbase + v0 + j] = res[j];
+          }
         }
       }
       if (PROF) T[2] += clk() - c2;
