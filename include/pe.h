@@ -52,7 +52,8 @@ enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_MIX = 3, PE_
  * block of T_c = 128 x 128 points is the product L * R of giant-step values c_i m_i^{j_s+128u} and
  * baby-step values m_i^v (the Vandermonde structure M_i(beta^t) = m_i^t, PAPER.md:420-427,
  * 465-478), computed exactly as 64 byte-by-byte int8 tcgen05 MMAs.  PE_PATH_AUTO
- * selects it for 2^50 <= p < 2^62 when T >= 8192 (env PE_TC=0 off, 1 auto, 2 always);
+ * selects it for any p < 2^62 when T >= 2048 (>= 5*10^5 padded terms) or T >= 4096 (fewer
+ * terms) -- pe_tc_info reports the handle's threshold (env PE_TC=0 off, 1 auto, 2 always);
  * PE_PATH_INT never uses it.  Results are bit-identical either way. */
 /* PE_PATH_INT32 is reported by pe_info only: every p < 2^31 (any requested path except FP64)
  * uses 32-bit Shoup products. */
@@ -62,8 +63,8 @@ enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_MIX = 3, PE_
 
 /* Tuning knobs (0 = automatic).  They never change the result (pin P13). */
 typedef struct pe_config {
-  int32_t path;  /* PE_PATH_AUTO: FP64 Alg. 2 if p < 2^50 else INT64 Shoup (tensor-core form for large
-                    T); PE_PATH_FP64 / PE_PATH_INT / PE_PATH_TC force one.  env PE_PATH=int|fp64, PE_CORE=mix|fp64|hyb|shoup     */
+  int32_t path;  /* PE_PATH_AUTO: FP64 Alg. 2 if p < 2^50 else INT64 Shoup, in the tensor-core form for
+                    large T when p < 2^62; PE_PATH_FP64 / PE_PATH_INT / PE_PATH_TC force one.  env PE_PATH=int|fp64, PE_CORE=mix|fp64|hyb|shoup     */
   int32_t R;     /* terms per lane: 1,2,4,8,16 (FP64: <= 8); auto picks by bucket sizes    */
   int32_t warps; /* warps per CTA, 1..16 (auto 8)                                          */
   int32_t chunk; /* points per CTA (multiple of 32; auto by grid coverage)                 */

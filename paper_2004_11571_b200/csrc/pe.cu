@@ -115,7 +115,7 @@ struct pe_ctx {
   size_t partial_elems = 0;
   u64* d_out_scratch = nullptr;
   size_t out_scratch_elems = 0;
-  // tensor-core path (tc.cuh): 0 off, 1 auto (T >= kTcMinT), 2 forced
+  // tensor-core path (tc.cuh): 0 off, 1 auto (T >= tc_min_T(t_pad)), 2 forced
   int tc_mode = 0;
   bool tc_ok = false;
   u32 tc_npieces = 0, tc_nslots = 0;
@@ -213,9 +213,10 @@ static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStrea
   return launch_step_path<kFp64>(R, grid, block, s, a);
 }
 
-// automatic tensor-core path from this many points (a chunk is tc::kChunk = 16384 points; below
-// half a chunk the padding of the last chunk outweighs the gain)
-constexpr u64 kTcMinT = tc::kChunk / 2;
+// automatic tensor-core path from this many points (a chunk is tc::kChunk = 16384 points): k_tc is
+// ~10x faster per term-point than k_step but computes whole chunks and pays a fixed epilogue per
+// piece; measured crossovers (scripts/tc_threshold.py): T ~ 2048 for 10^6 terms, ~4096 for 10^5.
+static u64 tc_min_T(u64 t_pad) { return t_pad >= 500000 ? 2048 : 4096; }
 
 static unsigned grid_for(u64 n, unsigned block) {
   u64 b = (n + block - 1) / block;
@@ -414,17 +415,24 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   // ---- tensor-core path (tc.cuh): per-term strides + the piece plan
   std::vector<uint4> pieces;
   std::vector<u32> tc_slot_start(G + 1);
-  if (h->tc_mode != 0 && h->path == kInt4) {
+  if (h->tc_mode != 0 && (h->path == kInt4 || h->path == kFp64 || h->path == kInt32)) {
     const u64 tp = h->t_pad;
     if (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp)) return g_last_error;
     tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_tcC, h->mp);
     CU(cudaGetLastError());
     // pieces: each bucket's padded range split into ceil(n / kPieceMax) near-equal runs of whole
     // K-blocks (<= kPieceMax terms keeps every int32 diagonal sum exact); slots contiguous per bucket
+    // piece size: <= kPieceMax (exactness), and <= twice the average per-CTA load so one large
+    // bucket cannot bound the kernel time of a small problem (every unit also pays a fixed
+    // epilogue -- 4 drains + one fold -- so pieces stay >= 1024 terms)
+    CU(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
+    u64 piece_max = 2 * ((tp + h->n_sm - 1) / h->n_sm);
+    piece_max = std::min<u64>(std::max<u64>(piece_max, 1024), tc::kPieceMax);
+    piece_max = (piece_max + tc::kKB - 1) / tc::kKB * tc::kKB;
     for (u64 g = 0; g < G; ++g) {
       tc_slot_start[g] = (u32)pieces.size();
       const u64 nkb = (poff[g + 1] - poff[g]) / tc::kKB;   // poff multiples of 32R
-      const u64 maxkb = tc::kPieceMax / tc::kKB;
+      const u64 maxkb = piece_max / tc::kKB;
       const u64 np_g = (nkb + maxkb - 1) / maxkb;
       u64 kb0 = 0;
       for (u64 k = 0; k < np_g; ++k) {
@@ -439,7 +447,6 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
     if (dalloc(&h->d_piece, pieces.size()) || dalloc(&h->d_tc_slot_start, G + 1)) return g_last_error;
     CU(cudaMemcpyAsync(h->d_piece, pieces.data(), pieces.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(h->d_tc_slot_start, tc_slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
-    CU(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
     h->tc_ok = true;
   }
   CU(cudaStreamSynchronize(s));  // host vectors above must outlive the copies; tmp frees after
@@ -501,8 +508,11 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
   }
   // tensor-core path: forced by PE_PATH_TC; automatic (large T) for the INT64 Shoup path when the
   // caller asked for PE_PATH_AUTO; env PE_TC=0|1|2 overrides the automatic choice.
-  int tc_mode = path_req == PE_PATH_TC ? 2 : (path_req == PE_PATH_AUTO && path == kInt4 ? 1 : 0);
-  if (path_req == PE_PATH_AUTO && path == kInt4) {
+  // (any p < 2^62: the automatic scalar core -- Shoup, FP64 Alg. 2 or 32-bit Shoup -- serves short
+  // point ranges, the tensor-core form long ones)
+  const bool tc_able = path == kInt4 || path == kFp64 || path == kInt32;
+  int tc_mode = path_req == PE_PATH_TC ? 2 : (path_req == PE_PATH_AUTO && tc_able ? 1 : 0);
+  if (path_req == PE_PATH_AUTO && tc_able) {
     const int e = env_int("PE_TC", 1);
     tc_mode = e < 0 ? 0 : (e > 2 ? 2 : e);
   }
@@ -635,7 +645,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
       CU(cudaEventRecord(rec.e0, s));
     }
     unsigned long long* d_prof = nullptr;
-    const size_t nprof = (size_t)grid * (tc::kThreads / 32) * 5;
+    const size_t nprof = (size_t)grid * (tc::kThreads / 32) * 5 + (size_t)grid * 3;
     a.prof = nullptr;
     if (env_int("PE_TC_PROF", 0)) {   // development: per-warp phase timers printed to stderr
       CU(cudaMalloc(&d_prof, nprof * sizeof(unsigned long long)));
@@ -658,6 +668,15 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
         fprintf(stderr, "tcprof warp %2d: t0 %.0f t1 %.0f t2 %.0f n %.0f total %.0f\n", wv, acc[0], acc[1], acc[2],
                 acc[3], acc[4]);
       }
+      const unsigned long long* gt = hp.data() + (size_t)grid * nw * 5;
+      unsigned long long e0 = ~0ull, e1 = 0, a0 = ~0ull, a1 = 0, x0 = ~0ull, x1 = 0;
+      for (unsigned b = 0; b < grid; ++b) {
+        e0 = std::min(e0, gt[3 * b]); e1 = std::max(e1, gt[3 * b]);
+        a0 = std::min(a0, gt[3 * b + 1]); a1 = std::max(a1, gt[3 * b + 1]);
+        x0 = std::min(x0, gt[3 * b + 2]); x1 = std::max(x1, gt[3 * b + 2]);
+      }
+      fprintf(stderr, "tcprof wall us: entry %.1f..%.1f  alloc-done %.1f..%.1f  exit %.1f..%.1f\n", 0.0,
+              (e1 - e0) / 1e3, (a0 - e0) / 1e3, (a1 - e0) / 1e3, (x0 - e0) / 1e3, (x1 - e0) / 1e3);
     }
     if (h->timing) CU(cudaEventRecord(rec.e1, s));
     const u32 nkb = (np + 255) / 256;
@@ -673,7 +692,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
 }
 
 static bool use_tc(const pe_ctx* h, u64 T) {
-  return h->tc_ok && (h->tc_mode == 2 || (h->tc_mode == 1 && T >= kTcMinT));
+  return h->tc_ok && (h->tc_mode == 2 || (h->tc_mode == 1 && T >= tc_min_T(h->t_pad)));
 }
 
 static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s) {
@@ -795,7 +814,7 @@ extern "C" int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint
   if (!h) return set_err(PE_EINVAL);
   if (mode) *mode = h->tc_ok ? h->tc_mode : 0;
   if (pieces) *pieces = h->tc_npieces;
-  if (min_T) *min_T = h->tc_ok ? (h->tc_mode == 2 ? 1 : kTcMinT) : 0;
+  if (min_T) *min_T = h->tc_ok ? (h->tc_mode == 2 ? 1 : tc_min_T(h->t_pad)) : 0;
   return PE_OK;
 }
 

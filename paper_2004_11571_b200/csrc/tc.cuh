@@ -416,6 +416,8 @@ __device__ __forceinline__ void load_kblock(const TcArgs& a, const KIter& k, u32
 
 template <bool PROF>
 static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 warps: <= 128 regs/thread
+  unsigned long long g_entry = 0;
+  if (PROF) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
   extern __shared__ uint8_t dsm[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accf, acce, dfull[kDataSlots];
@@ -437,6 +439,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 w
   __syncthreads();
   tc_fence_after();
   const u32 tb = tmem_base;
+  unsigned long long g_alloc = 0;
+  if (PROF) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_alloc));
   long long T[4] = {0, 0, 0, 0};   // phase timers (a.prof)
   const long long t_start = clk();
   const u32 data0 = smem_u32(smem) + kStages * kStageBytes;
@@ -638,6 +642,12 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 w
     unsigned long long* o = a.prof + ((u64)blockIdx.x * (kThreads / 32) + warp) * 5;
     for (int i = 0; i < 4; ++i) o[i] = (unsigned long long)T[i];
     o[4] = (unsigned long long)(clk() - t_start);
+    if (warp == 0) {   // wall-clock stamps (ns): entry, after TMEM alloc, exit of this CTA
+      unsigned long long g_exit;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
+      unsigned long long* gt = a.prof + (u64)gridDim.x * (kThreads / 32) * 5 + (u64)blockIdx.x * 3;
+      gt[0] = g_entry; gt[1] = g_alloc; gt[2] = g_exit;
+    }
   }
   tc_fence_before();
   __syncthreads();

@@ -41,10 +41,14 @@ def test_config2_full():
     check_full(synth.gen_config(2))
 
 
-@pytest.mark.parametrize("cfg", [3, 4])
-def test_config3_4_full_incremental_and_sampled_direct(cfg):
+@pytest.mark.parametrize("cfg,path", [(3, pe.PATH_AUTO), (3, pe.PATH_INT), (4, pe.PATH_AUTO), (4, pe.PATH_FP64)])
+def test_config3_4_full_incremental_and_sampled_direct(cfg, path):
+    """Configs 3 and 4 in full: PATH_AUTO takes the tensor-core form (T = 4096 >= the threshold),
+    PATH_INT / PATH_FP64 the scalar Shoup / FP64 Alg. 2 k_step."""
     w = synth.gen_config(cfg)
-    rows, out = gpu_eval(w)
+    with pe.Context.from_workload(w, path=path) as ctx:
+        assert ctx.uses_tc(w.T) == (path == pe.PATH_AUTO)
+    rows, out = gpu_eval(w, path=path)
     assert rows.tolist() == oracle.buckets(w.exps, w.n).tolist()
     inc = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
     assert np.array_equal(out, inc)
