@@ -121,6 +121,7 @@ struct pe_ctx {
   u32 tc_npieces = 0, tc_nslots = 0;
   int n_sm = 148;
   u64* d_tcC = nullptr;   // [t_pad][12] tensor-core path C records (tc.cuh)
+  u64* d_tcMH = nullptr;  // [t_pad] Montgomery m^{64*128} (row-half-1 seed factor, k_tc_seed)
   uint4* d_piece = nullptr;
   u32* d_tc_slot_start = nullptr;
   u64* d_seed = nullptr;
@@ -145,7 +146,7 @@ static void free_all(pe_ctx* h) {
   cudaStream_t s = h->stream;
   for (void* q : {(void*)h->d_c, (void*)h->d_m, (void*)h->d_w, (void*)h->d_perm, (void*)h->d_ms, (void*)h->d_mpd,
                   (void*)h->d_mspd, (void*)h->d_wt_info, (void*)h->d_slot_start, (void*)h->d_partial,
-                  (void*)h->d_out_scratch, (void*)h->d_tcC,
+                  (void*)h->d_out_scratch, (void*)h->d_tcC, (void*)h->d_tcMH,
                   (void*)h->d_tc_scratch, (void*)h->d_piece, (void*)h->d_tc_slot_start,
                   (void*)h->d_seed})
     if (q) cudaFreeAsync(q, s);
@@ -417,8 +418,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   std::vector<u32> tc_slot_start(G + 1);
   if (h->tc_mode != 0 && (h->path == kInt4 || h->path == kFp64 || h->path == kInt32)) {
     const u64 tp = h->t_pad;
-    if (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp)) return g_last_error;
-    tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_tcC, h->mp);
+    if (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp) || dalloc(&h->d_tcMH, tp)) return g_last_error;
+    tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_tcC, h->d_tcMH, h->mp);
     CU(cudaGetLastError());
     // pieces: each bucket's padded range split into ceil(n / kPieceMax) near-equal runs of whole
     // K-blocks (<= kPieceMax terms keeps every int32 diagonal sum exact); slots contiguous per bucket
@@ -616,7 +617,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
     const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
-    tc::k_tc_seed<<<grid_for((u64)h->t_pad * nch * 2, 256), 256, 0, s>>>(h->d_c, h->d_m, h->t_pad, nch, j0 + k0,
+    tc::k_tc_seed<<<grid_for((u64)h->t_pad * nch, 256), 256, 0, s>>>(h->d_c, h->d_m, h->d_tcMH, h->t_pad, nch, j0 + k0,
                                                                       h->d_seed, h->mp);
     CU(cudaGetLastError());
     tc::TcArgs a;

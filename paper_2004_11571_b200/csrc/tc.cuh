@@ -660,9 +660,11 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 w
 // ---------------------------------------------------------------- setup kernels
 // Per padded term (pe_create): the C record -- baby-step chain seeds m^{64h + rr} (h*4 + rr), the
 // stride-4 chain multipliers m^4, m^{4V} and their Shoup constants.
-static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ C, ModParams mp) {
+static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ C,
+                                  u64* __restrict__ mH, ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
     const u64 mm = to_mont(m[q], mp);
+    mH[q] = mont_pow(mm, 64ull * kV, mp);             // Montgomery form of m^{64V} (seed of row half 1)
     const u64 a4 = from_mont(mont_pow(mm, 4, mp), mp);
     const u64 aV4 = from_mont(mont_pow(mm, 4 * kV, mp), mp);
     u64* rec = C + q * kCRec;
@@ -678,19 +680,23 @@ static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __r
   }
 }
 
-// Per evaluation pass: LS records of chunk c: LS[c][q][h*4 + rr] = c_q m_q^{js0 + c*kChunk + (64h + rr) V}.
-static __global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, u64 t_pad, u32 nch, u64 js0,
-                                 u64* __restrict__ LS, ModParams mp) {
-  const u64 total = t_pad * nch * 2;
+// Per evaluation pass: LS records of chunk c: LS[c][q][h*4 + rr] = c_q m_q^{js0 + c*kChunk + (64h + rr) V}
+// (one exponentiation per term and chunk; the row-half-1 seeds by one product with m^{64V}).
+static __global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, const u64* __restrict__ mH,
+                                 u64 t_pad, u32 nch, u64 js0, u64* __restrict__ LS, ModParams mp) {
+  const u64 total = t_pad * nch;
   for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
-    const u64 ch = x / t_pad, q = x - ch * t_pad;   // ch = 2 * chunk + h
-    const u64 chunk = ch >> 1, h = ch & 1;
-    u64 s = to_mont(seed_pow(c[q], m[q], js0 + chunk * kChunk + h * (64ull * kV), mp), mp);
+    const u64 chunk = x / t_pad, q = x - chunk * t_pad;
+    const u64 s0 = to_mont(seed_pow(c[q], m[q], js0 + chunk * kChunk, mp), mp);
     const u64 mV = mont_pow(to_mont(m[q], mp), kV, mp);
-    u64* dst = LS + (chunk * t_pad + q) * kLSRec + h * 4;
-    for (int rr = 0; rr < 4; ++rr) {
-      dst[rr] = from_mont(s, mp);
-      s = mont_mul(s, mV, mp);
+    u64* dst = LS + (chunk * t_pad + q) * kLSRec;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      u64 s = h ? mont_mul(s0, mH[q], mp) : s0;
+      for (int rr = 0; rr < 4; ++rr) {
+        dst[h * 4 + rr] = from_mont(s, mp);
+        s = mont_mul(s, mV, mp);
+      }
     }
   }
 }
