@@ -120,13 +120,13 @@ struct pe_ctx {
   bool tc_ok = false;
   u32 tc_npieces = 0, tc_nslots = 0;
   int n_sm = 148;
-  u64* d_tcC = nullptr;   // [t_pad][12] tensor-core path C records (tc.cuh)
-  u64* d_tcMH = nullptr;  // [t_pad] Montgomery m^{64*128} (row-half-1 seed factor, k_tc_seed)
+  u64* d_tcC = nullptr;   // [t_pad][2] tensor-core path C records (tc.cuh)
+  uint8_t* d_tcR = nullptr;   // [t_pad / 32][tc::kRBytes] baby-step byte planes m^v, v < 64 (tc.cuh)
   uint4* d_piece = nullptr;
   u32* d_tc_slot_start = nullptr;
   u64* d_seed = nullptr;
   size_t seed_elems = 0;
-  u32* d_tc_scratch = nullptr;   // k_tc per-CTA drained diagonal sums (n_sm x 2 x 15 x 16384 u32)
+  u32* d_tc_scratch = nullptr;   // k_tc per-CTA drained diagonal sums (n_sm x 2 x 15 x kChunk u32)
   size_t partial_cap_bytes = (size_t)1 << 30;
   // kernel timing (pe_set_timing / pe_kernel_stats)
   bool timing = false;
@@ -146,7 +146,7 @@ static void free_all(pe_ctx* h) {
   cudaStream_t s = h->stream;
   for (void* q : {(void*)h->d_c, (void*)h->d_m, (void*)h->d_w, (void*)h->d_perm, (void*)h->d_ms, (void*)h->d_mpd,
                   (void*)h->d_mspd, (void*)h->d_wt_info, (void*)h->d_slot_start, (void*)h->d_partial,
-                  (void*)h->d_out_scratch, (void*)h->d_tcC, (void*)h->d_tcMH,
+                  (void*)h->d_out_scratch, (void*)h->d_tcC, (void*)h->d_tcR,
                   (void*)h->d_tc_scratch, (void*)h->d_piece, (void*)h->d_tc_slot_start,
                   (void*)h->d_seed})
     if (q) cudaFreeAsync(q, s);
@@ -214,7 +214,7 @@ static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStrea
   return launch_step_path<kFp64>(R, grid, block, s, a);
 }
 
-// automatic tensor-core path from this many points (a chunk is tc::kChunk = 16384 points): k_tc is
+// automatic tensor-core path from this many points (a chunk is tc::kChunk = 8192 points): k_tc is
 // ~10x faster per term-point than k_step but computes whole chunks and pays a fixed epilogue per
 // piece; measured crossovers (scripts/tc_threshold.py): T ~ 2048 for 10^6 terms, ~4096 for 10^5.
 static u64 tc_min_T(u64 t_pad) { return t_pad >= 500000 ? 2048 : 4096; }
@@ -418,14 +418,17 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   std::vector<u32> tc_slot_start(G + 1);
   if (h->tc_mode != 0 && (h->path == kInt4 || h->path == kFp64 || h->path == kInt32)) {
     const u64 tp = h->t_pad;
-    if (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp) || dalloc(&h->d_tcMH, tp)) return g_last_error;
-    tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_tcC, h->d_tcMH, h->mp);
+    if (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp) || dalloc(&h->d_tcR, (size_t)tp / tc::kKB * tc::kRBytes))
+      return g_last_error;
+    tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_tcC, h->mp);
+    CU(cudaGetLastError());
+    tc::k_tc_rplanes<<<grid_for(tp / 4 * (tc::kV / 8), 256), 256, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
     CU(cudaGetLastError());
     // pieces: each bucket's padded range split into ceil(n / kPieceMax) near-equal runs of whole
     // K-blocks (<= kPieceMax terms keeps every int32 diagonal sum exact); slots contiguous per bucket
     // piece size: <= kPieceMax (exactness), and <= twice the average per-CTA load so one large
     // bucket cannot bound the kernel time of a small problem (every unit also pays a fixed
-    // epilogue -- 4 drains + one fold -- so pieces stay >= 1024 terms)
+    // epilogue -- 2 drains + one fold -- so pieces stay >= 1024 terms)
     CU(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
     u64 piece_max = 2 * ((tp + h->n_sm - 1) / h->n_sm);
     piece_max = std::min<u64>(std::max<u64>(piece_max, 1024), tc::kPieceMax);
@@ -604,12 +607,12 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
   // partial rows padded to a multiple of 8 points (the epilogue's 64-byte vector accesses)
   if (ensure_partial(h, (size_t)nslots * ((std::min<u64>(Tp, T) + 7) / 8 * 8), s)) return g_last_error;
   const u32 nch_max = (u32)(Tp / tc::kChunk);
-  if ((size_t)h->t_pad * nch_max * 8 > h->seed_elems) {
+  if ((size_t)h->t_pad * nch_max * tc::kLSRec > h->seed_elems) {
     if (h->d_seed) cudaFreeAsync(h->d_seed, s);
     h->d_seed = nullptr;
     h->seed_elems = 0;
-    CU(cudaMallocAsync((void**)&h->d_seed, (size_t)h->t_pad * nch_max * 8 * sizeof(u64), s));
-    h->seed_elems = (size_t)h->t_pad * nch_max * 8;
+    CU(cudaMallocAsync((void**)&h->d_seed, (size_t)h->t_pad * nch_max * tc::kLSRec * sizeof(u64), s));
+    h->seed_elems = (size_t)h->t_pad * nch_max * tc::kLSRec;
   }
   if (!h->d_tc_scratch) CU(cudaMallocAsync((void**)&h->d_tc_scratch, (size_t)h->n_sm * 2 * 15 * tc::kChunk * sizeof(u32), s));
   CU(cudaFuncSetAttribute(tc::k_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
@@ -617,12 +620,13 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
     const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
-    tc::k_tc_seed<<<grid_for((u64)h->t_pad * nch, 256), 256, 0, s>>>(h->d_c, h->d_m, h->d_tcMH, h->t_pad, nch, j0 + k0,
+    tc::k_tc_seed<<<grid_for((u64)h->t_pad * nch, 256), 256, 0, s>>>(h->d_c, h->d_m, h->t_pad, nch, j0 + k0,
                                                                       h->d_seed, h->mp);
     CU(cudaGetLastError());
     tc::TcArgs a;
     a.LS = h->d_seed;
     a.C = h->d_tcC;
+    a.Rp = h->d_tcR;
     a.piece = h->d_piece;
     a.partial = h->d_partial;
     a.ldp = (np + 7) / 8 * 8;

@@ -269,14 +269,14 @@ extern "C" int pe_bench_core(int variant, uint64_t p, int R, int blocks, int thr
 // ---------------------------------------------------------------- int8 tcgen05 issue-rate probe
 // One CTA per SM issues `iters` M=128 x N x K=32 kind::i8 MMAs (u8 x u8 -> s32) from a fixed
 // shared-memory tile into 4 rotating TMEM accumulators: the same-run tensor ceiling that
-// bench.py quotes beside k_tc (the tc.cuh MMA shape is N = 128).
+// bench.py quotes beside k_tc (the tc.cuh MMA shape is N = tc::kV = 64).
 __global__ void k_bench_mma(int iters, u32 idesc, u32 ncols, int nacc) {
   extern __shared__ uint8_t dsm[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t bar;
   __shared__ u32 tmem_base;
   const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 2 * (int)tc::kPlane; i += blockDim.x) sm[i] = (uint8_t)(i * 13);
+  for (int i = threadIdx.x; i < 2 * (int)tc::kPlaneA; i += blockDim.x) sm[i] = (uint8_t)(i * 13);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(tc::smem_u32(&tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -291,7 +291,8 @@ __global__ void k_bench_mma(int iters, u32 idesc, u32 ncols, int nacc) {
   tc::tc_fence_after();
   const u32 tb = tmem_base;
   if (threadIdx.x == 0) {
-    const uint64_t ad = tc::smem_desc(tc::smem_u32(sm)), bd = tc::smem_desc(tc::smem_u32(sm) + tc::kPlane);
+    const uint64_t ad = tc::smem_desc(tc::smem_u32(sm), tc::kLBOA),
+                   bd = tc::smem_desc(tc::smem_u32(sm) + tc::kPlaneA, tc::kLBOA);
     u32 acc_col = 0;
     const u32 acc_end = (u32)nacc * ncols;
     for (int it = 0; it < iters; ++it, acc_col = (acc_col + ncols == acc_end) ? 0u : acc_col + ncols)
@@ -319,7 +320,7 @@ extern "C" int pe_bench_mma(int N, int iters, float* ms, double* macs) {
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return PE_ECUDA;
   const u32 idesc = (2u << 4) | ((u32)(N >> 3) << 17) | ((u32)(128 >> 4) << 24);
-  const int smem = 2 * tc::kPlane + 1024;
+  const int smem = 2 * tc::kPlaneA + 1024;
   if (cudaFuncSetAttribute(k_bench_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return PE_ECUDA;
   cudaEvent_t e0, e1;

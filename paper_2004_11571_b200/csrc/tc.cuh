@@ -18,25 +18,28 @@
 // for <= 8192 terms per accumulation (a "piece"; the s32 TMEM accumulator wraps mod 2^32 without
 // saturation, so its bits read as u32 are exact).  X mod p = sum_d D_d (2^{8d} mod p) mod p.
 //
-// Shapes: U = M = 128 (TMEM lanes), V = N = 128, K-block = 32 terms (one kind::i8 MMA).  The 15
-// diagonals do not fit TMEM at once (15 x 128 columns > 512), so a piece is evaluated in 4
-// rounds of <= 4 diagonals (16 digit-pair MMAs per K-block each), regenerating L and R per
-// round; rounds accumulate into the piece's partial row.  Measured on this B200: an
-// M=128, K=32 i8 MMA issues every ~136 clk for any N <= 256 (scripts/tc_probe.cu), so N = 128
-// costs 2x the N = 256 MACs/clk but balances the IMAD-bound generation.
+// Shapes: U = M = 128 (TMEM lanes), V = N = 64, K-block = 32 terms (one kind::i8 MMA).  The 15
+// diagonals do not fit TMEM at once (15 x 64 columns > 512), so a piece is evaluated in 2 rounds
+// of <= 8 diagonals (30 and 34 digit-pair MMAs per K-block), regenerating L and R per round;
+// rounds accumulate into the unit's raw diagonal buffer.  Measured on this B200: an M=128, K=32
+// i8 MMA costs ~64 clk for any N <= 128 (pe_bench_mma), so N = 64 runs the tensor pipe at half
+// its N = 128 rate -- but with 2 rounds instead of 4 the generation per point falls from 2 to
+// 1.5 modular products, and the smaller stage (49.7 KB) lets 4 stages fit shared memory, which
+// decouples the producers from the in-order MMA.
 //
-// Warp roles (one CTA per SM, 16 warps = 4 per SMSP, persistent, static round-robin over units =
+// Warp roles (one CTA per SM, 12 warps = 3 per SMSP, persistent, static round-robin over units =
 // (piece, chunk)):
-//   warps 0-3  epilogue: tcgen05.ld the round's diagonals (TMEM lane = u), fold them exactly into
-//              160-bit running sums (shift/add, per-CTA L2-resident scratch), release TMEM; after
-//              the unit's last round one reduction mod p per point -> partial[slot][chunk*16384 + u*128 + v].
-//              Warp 0 is also the TMEM allocator and the MMA issuer (tcgen05.mma.cta_group::1.kind::i8,
-//              elect.sync leader): a round's MMAs and its epilogue cannot overlap anyway.
-//   warps 4-15 producers, 4 per smem stage: two L warps and two R warps generate one K-block's
-//              128 giant-step / 128 baby-step values of 32 terms (64 rows each) with Shoup
-//              products (4 chains per lane, seeded from precomputed chain seeds) and write their
-//              8 byte planes in the no-swizzle K-major UMMA layout; each group's first lane also
-//              issues the TMA bulk copies of the group's next K-block of per-term records.
+//   warps 0-3  epilogue: tcgen05.ld the round's diagonals (TMEM lane = u) into the unit's raw
+//              buffer (per-CTA, L2-resident), release TMEM; after the unit's last round an exact
+//              160-bit fold of the 15 diagonals and one reduction mod p per point ->
+//              partial[slot][chunk*kChunk + u*kV + v].  Warps 0 / 1 also issue rounds 0 / 1's MMAs
+//              (tcgen05.mma.cta_group::1.kind::i8, elect.sync leader); warp 0 allocates TMEM.
+//   warps 4-11 producers, 2 per smem stage: each generates 16 terms x 128 giant-step rows of one
+//              K-block with Shoup products (4 chains per lane, seeded from per-chunk chain seeds)
+//              and writes their 8 byte planes in the no-swizzle K-major UMMA layout.  The baby-step
+//              planes R = m^v do not depend on the points: they are written once per handle and
+//              the group's first lane copies each K-block's planes into the stage with TMA (as it
+//              does the group's next K-block of per-term records).
 #pragma once
 #include "modcore.cuh"
 
@@ -44,44 +47,50 @@ namespace pe {
 namespace tc {
 
 constexpr int kU = 128;                   // giant steps per chunk  (MMA M / TMEM lanes)
-constexpr int kV = 128;                   // baby steps per chunk   (MMA N)
+constexpr int kV = 64;                    // baby steps per chunk   (MMA N)
 constexpr u32 kChunk = kU * kV;           // points per chunk
 constexpr int kKB = 32;                   // terms per K-block (one i8 MMA K step)
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr u32 kPieceMax = 8192;           // terms per accumulation: 8192 * 8 * 255^2 < 2^32 (the s32
                                           // accumulator wraps mod 2^32, saturate = 0; read as u32)
-constexpr u32 kLBO = 2048 + 64;           // bytes between the two 16-byte K chunks of a plane (+64: bank spread)
-constexpr u32 kPlane = kLBO + 2048;       // one digit plane: 128 rows x 32 bytes (+ pad between the chunks)
-constexpr u32 kStageBytes = 16 * kPlane;  // 8 L planes + 8 R planes
-// per-K-block term data streamed by the loader warp (TMA bulk copies): 11 arrays x 32 terms
+// Digit planes in the no-swizzle K-major UMMA layout: 8-row x 16-byte core matrices, rows of a
+// core-matrix column 128 B apart (SBO), the two 16-byte K halves LBO apart.
+constexpr u32 kLBOA = 2048;               // L planes (A, 128 rows): writes are conflict-free unpadded
+constexpr u32 kPlaneA = kLBOA + 2048;
+constexpr u32 kLBOB = 1024 + 64;          // R planes (B, 64 rows): +64 B spreads the K halves over banks
+constexpr u32 kPlaneB = kLBOB + 1024;
+constexpr u32 kStageBytes = 8 * kPlaneA + 8 * kPlaneB;   // 8 L planes + 8 R planes (49664 B)
 // Per-term records (array of structs, so one K-block's data is two contiguous bulk copies):
-//   LS record (per chunk, 8 u64): giant-step chain seeds c m^{j_s + (64h + rr) V}, index h*4 + rr
-//   C  record (12 u64): baby-step chain seeds m^{64h + rr} (index h*4 + rr), m^4, w(m^4), m^{4V}, w(m^{4V})
-// (h = row half, rr = the lane's row residue mod 4)
-constexpr int kLSRec = 8, kCRec = 12;
-enum { kC_m4 = 8, kC_w4 = 9, kC_mV4 = 10, kC_wV4 = 11 };
-constexpr u32 kDataLS = kKB * kLSRec * 8;        // 2048 B
-constexpr u32 kDataSlot = kDataLS + kKB * kCRec * 8;   // 5120 B
-constexpr int kDataSlots = 6;                   // 2 per producer group: current + next K-block
-constexpr u32 kSmemBytes = kStages * kStageBytes + kDataSlots * kDataSlot + 1024;
-constexpr int kRounds = 4;
-constexpr int kProdPerStage = 4;          // L rows 0-63, L rows 64-127, R rows 0-63, R rows 64-127
+//   LS record (per chunk, 8 u64): giant-step chain seeds c m^{j_s + rr V}, rr < 8
+//   C  record (2 u64): the giant-step chain multiplier m^{8V} and its Shoup constant
+// The baby-step factors R[i][v] = m_i^v do not depend on the points: pe_create writes their byte
+// planes once per handle, in the stage's R-plane layout ([t_pad / 32][kRBytes], k_tc_rplanes),
+// and each K-block's 16.5 KB is one TMA bulk copy into the stage.
+constexpr int kLSRec = 8, kCRec = 2;
+enum { kC_mL = 0, kC_wL = 1 };
+constexpr u32 kRBytes = 8 * kPlaneB;                  // one K-block's R planes (16896 B)
+constexpr u32 kDataLS = kKB * kLSRec * 8;             // 2048 B
+constexpr u32 kDataSlot = kDataLS + kKB * kCRec * 8;  // 2560 B
+constexpr int kDataSlots = 2 * kStages;               // 2 per producer group: current + next K-block
+constexpr u32 kSmemBytes = kStages * kStageBytes + kDataSlots * kDataSlot + 128;
+constexpr int kRounds = 2;
+constexpr int kDiag = 8;                  // diagonal accumulators per round: 8 x 64 TMEM columns
+constexpr int kProdPerStage = 2;          // L terms 0-15, L terms 16-31 (128 rows each)
 constexpr int kEpiWarps = 4, kMmaWarp = 0, kProdWarp0 = 4;   // warp 0: epilogue + MMA issue
-constexpr int kThreads = (kProdWarp0 + kStages * kProdPerStage) * 32;   // 16 warps: 4 per SMSP
-static_assert(kRounds == kEpiWarps, "round g's MMAs are issued by epilogue warp g");
-// diagonal groups: <= 4 diagonals (TMEM: 4 x 128 columns), 16 digit pairs each
+constexpr int kThreads = (kProdWarp0 + kStages * kProdPerStage) * 32;   // 12 warps: 3 per SMSP
+static_assert(kRounds <= kEpiWarps, "round g's MMAs are issued by epilogue warp g");
+static_assert(kDiag * kV == 512, "a round's accumulators fill TMEM");
+static_assert(kSmemBytes + 256 <= 232448, "shared memory");
+// diagonal groups: 8 + 7 diagonals, 30 + 34 digit pairs
 __host__ __device__ constexpr int group_diag(int g, int di) {
-  return g == 0 ? (di == 0 ? 7 : di == 1 ? 6 : di == 2 ? 0 : -1)
-       : g == 1 ? (di == 0 ? 8 : di == 1 ? 5 : di == 2 ? 1 : 14)
-       : g == 2 ? (di == 0 ? 9 : di == 1 ? 4 : di == 2 ? 2 : 13)
-                : (di == 0 ? 10 : di == 1 ? 3 : di == 2 ? 11 : 12);
+  return g == 0 ? (di == 0 ? 7 : di == 1 ? 6 : di == 2 ? 5 : di == 3 ? 0 : di == 4 ? 1 : di == 5 ? 2 : di == 6 ? 14 : 13)
+                : (di == 0 ? 8 : di == 1 ? 4 : di == 2 ? 9 : di == 3 ? 3 : di == 4 ? 10 : di == 5 ? 11 : di == 6 ? 12 : -1);
 }
-__device__ __constant__ const signed char kGroups[kRounds][4] = {
-    {7, 6, 0, -1}, {8, 5, 1, 14}, {9, 4, 2, 13}, {10, 3, 11, 12}};
 
 struct TcArgs {
   const u64* LS;         // [nch][t_pad][8] LS records (giant-step chain seeds of each chunk)
-  const u64* C;          // [t_pad][12] C records (baby-step seeds, stride-4 multipliers)
+  const u64* C;          // [t_pad][2] C records (giant-step chain multiplier)
+  const uint8_t* Rp;     // [t_pad / 32][kRBytes] baby-step byte planes (k_tc_rplanes)
   const uint4* piece;    // x = first padded term, y = K-blocks, z = partial slot (sorted by size desc)
   u64* partial;          // [n_slots][ldp]
   u64 ldp, t_pad;
@@ -98,14 +107,14 @@ struct TcArgs {
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ uint64_t smem_desc(u32 saddr) {
+__device__ __forceinline__ uint64_t smem_desc(u32 saddr, u32 lbo) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((kLBO >> 4) & 0x3FFF) << 16;   // leading (K) byte offset
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;    // leading (K) byte offset
   d |= (uint64_t)((128u >> 4) & 0x3FFF) << 32;   // stride (8-row group) byte offset
   d |= (uint64_t)1 << 46;                        // sm_100 descriptor version; no swizzle
   return d;
 }
-// kind::i8, D s32, A u8, B u8, both K-major, M = 128, N = 128
+// kind::i8, D s32, A u8, B u8, both K-major, M = kU = 128, N = kV = 64
 constexpr u32 kIdesc = (2u << 4) | (0u << 7) | (0u << 10) | ((u32)(kV >> 3) << 17) | ((u32)(kU >> 4) << 24);
 
 __device__ __forceinline__ void mma_u8(u32 dtmem, uint64_t ad, uint64_t bd, u32 acc) {
@@ -151,37 +160,37 @@ __host__ __device__ constexpr bool pair_ok(int G, int di, int sd) {
   return group_diag(G, di) >= 0 && group_diag(G, di) - sd >= 0 && group_diag(G, di) - sd <= 7;
 }
 __host__ __device__ constexpr int run_len(int G, int sd) {
-  return (pair_ok(G, 0, sd) ? 1 : 0) + (pair_ok(G, 1, sd) ? 1 : 0) + (pair_ok(G, 2, sd) ? 1 : 0) +
-         (pair_ok(G, 3, sd) ? 1 : 0);
+  int n = 0;
+  for (int di = 0; di < kDiag; ++di) n += pair_ok(G, di, sd) ? 1 : 0;
+  return n;
 }
-// position of slot di inside the run of plane sd when the slots are visited in the rotated order
-// di = (sd + k) & 3, k = 0..3 (rotation keeps consecutive MMAs on different accumulators)
-__host__ __device__ constexpr int run_pos(int G, int sd, int di) {
-  return ((pair_ok(G, (sd + 0) & 3, sd) && ((sd + 0) & 3) != di && (((di - sd) & 3) > 0)) ? 1 : 0) +
-         ((pair_ok(G, (sd + 1) & 3, sd) && ((sd + 1) & 3) != di && (((di - sd) & 3) > 1)) ? 1 : 0) +
-         ((pair_ok(G, (sd + 2) & 3, sd) && ((sd + 2) & 3) != di && (((di - sd) & 3) > 2)) ? 1 : 0);
+// position of the k-th visited slot inside the run of plane sd (slots visited in the rotated
+// order di = (sd + k) mod kDiag, which keeps consecutive MMAs on different accumulators)
+__host__ __device__ constexpr int run_pos(int G, int sd, int k) {
+  int n = 0;
+  for (int j = 0; j < k; ++j) n += pair_ok(G, (sd + j) % kDiag, sd) ? 1 : 0;
+  return n;
 }
 
-// The 16 digit-pair MMAs of round G on one smem stage (descriptor db = plane 0 of the stage),
-// grouped by L plane s so the A operand (L_s) is read from shared memory once per K-block and
-// reused from the collector buffer; within a plane's run the round's diagonals are visited in a
-// rotated order so consecutive MMAs write different TMEM accumulators.  Fully unrolled: every
-// operand offset and collector mode is a compile-time constant.
+// The digit-pair MMAs of round G on one smem stage (da / db = descriptors of L plane 0 / R plane
+// 0), grouped by L plane s so the A operand (L_s) is read from shared memory once per K-block and
+// reused from the collector buffer.  Fully unrolled: every operand offset and collector mode is a
+// compile-time constant.
 template <int G>
-__device__ __forceinline__ void issue_round(u32 tb, uint64_t db, bool first_kb) {
+__device__ __forceinline__ void issue_round(u32 tb, uint64_t da, uint64_t db, bool first_kb) {
 #pragma unroll
   for (int sd = 0; sd < 8; ++sd) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int di = (sd + k) & 3;
+    for (int k = 0; k < kDiag; ++k) {
+      const int di = (sd + k) % kDiag;
       if (pair_ok(G, di, sd)) {
         const int d = group_diag(G, di);
-        const int n = run_len(G, sd), pos = run_pos(G, sd, di);
+        const int n = run_len(G, sd), pos = run_pos(G, sd, k);
         const int s0 = d > 7 ? d - 7 : 0;
         const u32 acc = (!first_kb || sd > s0) ? 1u : 0u;   // first pair of diagonal d at kb 0 overwrites
         const u32 dt = tb + (u32)di * kV;
-        const uint64_t ad = db + (uint64_t)((u32)sd * (kPlane >> 4));
-        const uint64_t bd = db + (uint64_t)((u32)(8 + d - sd) * (kPlane >> 4));
+        const uint64_t ad = da + (uint64_t)((u32)sd * (kPlaneA >> 4));
+        const uint64_t bd = db + (uint64_t)((u32)(d - sd) * (kPlaneB >> 4));
         if (n == 1) mma_u8c<0>(dt, ad, bd, acc);
         else if (pos == 0) mma_u8c<1>(dt, ad, bd, acc);
         else if (pos == n - 1) mma_u8c<3>(dt, ad, bd, acc);
@@ -267,25 +276,27 @@ __device__ __forceinline__ u32 prmt(u32 a, u32 b, u32 sel) {
 __device__ __forceinline__ void sts32(u32 addr, u32 v) {
   asm volatile("st.shared.b32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
 }
+template <u32 PS>
 __device__ __forceinline__ void store_digits(u32 planes, const u64 (&x)[4]) {
   const u32 l0 = lo32(x[0]), l1 = lo32(x[1]), l2 = lo32(x[2]), l3 = lo32(x[3]);
   const u32 h0 = hi32(x[0]), h1 = hi32(x[1]), h2 = hi32(x[2]), h3 = hi32(x[3]);
   u32 a = prmt(l0, l1, 0x5140), b = prmt(l2, l3, 0x5140);
   u32 c = prmt(l0, l1, 0x7362), d = prmt(l2, l3, 0x7362);
-  sts32(planes + 0 * kPlane, prmt(a, b, 0x5410));
-  sts32(planes + 1 * kPlane, prmt(a, b, 0x7632));
-  sts32(planes + 2 * kPlane, prmt(c, d, 0x5410));
-  sts32(planes + 3 * kPlane, prmt(c, d, 0x7632));
+  sts32(planes + 0 * PS, prmt(a, b, 0x5410));
+  sts32(planes + 1 * PS, prmt(a, b, 0x7632));
+  sts32(planes + 2 * PS, prmt(c, d, 0x5410));
+  sts32(planes + 3 * PS, prmt(c, d, 0x7632));
   a = prmt(h0, h1, 0x5140); b = prmt(h2, h3, 0x5140);
   c = prmt(h0, h1, 0x7362); d = prmt(h2, h3, 0x7362);
-  sts32(planes + 4 * kPlane, prmt(a, b, 0x5410));
-  sts32(planes + 5 * kPlane, prmt(a, b, 0x7632));
-  sts32(planes + 6 * kPlane, prmt(c, d, 0x5410));
-  sts32(planes + 7 * kPlane, prmt(c, d, 0x7632));
+  sts32(planes + 4 * PS, prmt(a, b, 0x5410));
+  sts32(planes + 5 * PS, prmt(a, b, 0x7632));
+  sts32(planes + 6 * PS, prmt(c, d, 0x5410));
+  sts32(planes + 7 * PS, prmt(c, d, 0x7632));
 }
 
+template <u32 LBO>
 __device__ __forceinline__ u32 plane_off(u32 row, u32 kbyte) {
-  return (kbyte >> 4) * kLBO + (row >> 3) * 128u + (row & 7u) * 16u + (kbyte & 15u);
+  return (kbyte >> 4) * LBO + (row >> 3) * 128u + (row & 7u) * 16u + (kbyte & 15u);
 }
 
 // X (5 x 32-bit words, little endian) += sum over the round's diagonals of D_d << 8d, exactly
@@ -301,20 +312,6 @@ __device__ __forceinline__ void fold_one(u128_t& lo, u32& x4, u32 Dv) {
   const u32 spill = s > 96 ? (u32)(Dv >> (128 - s > 31 ? 31 : 128 - s)) : 0u;   // bits >= 2^128
   lo += add;
   x4 += spill + (lo < add ? 1u : 0u);
-}
-template <int G>
-__device__ __forceinline__ void fold_point(u32 (&X)[5], u32 D0, u32 D1, u32 D2, u32 D3) {
-  u128_t lo = ((u128_t)(((u64)X[3] << 32) | X[2]) << 64) | (((u64)X[1] << 32) | X[0]);
-  u32 x4 = X[4];
-  fold_one<group_diag(G, 0) < 0 ? -1 : 8 * group_diag(G, 0)>(lo, x4, D0);
-  fold_one<group_diag(G, 1) < 0 ? -1 : 8 * group_diag(G, 1)>(lo, x4, D1);
-  fold_one<group_diag(G, 2) < 0 ? -1 : 8 * group_diag(G, 2)>(lo, x4, D2);
-  fold_one<group_diag(G, 3) < 0 ? -1 : 8 * group_diag(G, 3)>(lo, x4, D3);
-  X[0] = (u32)lo;
-  X[1] = (u32)(lo >> 32);
-  X[2] = (u32)(lo >> 64);
-  X[3] = (u32)(lo >> 96);
-  X[4] = x4;
 }
 // single-diagonal form (unit tests: scripts/fold_test.cu)
 template <int D8>
@@ -332,32 +329,54 @@ __device__ __forceinline__ void fold_add(u32 (&X)[5], u32 Dv) {
 // Epilogue critical part: drain round G's diagonals of thread row u from TMEM into the unit's raw
 // buffer (raw[d][u][v], u32: the diagonal sums themselves) and release TMEM (acce) as soon as the
 // last block is in registers -- only tcgen05.ld and fire-and-forget stores, so the MMA warp can
-// start the next round almost at once.
+// start the next round almost at once.  Four accumulators (32 registers) per tcgen05.wait.
+template <int G, int H>
+__device__ __forceinline__ void drain_ld(u32 tl, u32 v0, u32 (&D)[4][8]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (group_diag(G, 4 * H + j) >= 0) tmem_ld8(tl + (u32)(4 * H + j) * kV + v0, D[j]);
+}
+template <int G, int H>
+__device__ __forceinline__ void drain_fence(u32 (&D)[4][8]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (group_diag(G, 4 * H + j) >= 0) tmem_reg_fence(D[j]);
+}
+template <int G, int H>
+__device__ __forceinline__ void drain_st(u32 v0, u32* __restrict__ raw_u, const u32 (&D)[4][8]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (group_diag(G, 4 * H + j) >= 0) {
+      uint4* p4 = (uint4*)(raw_u + (u32)group_diag(G, 4 * H + j) * (kU * kV) + v0);
+      p4[0] = make_uint4(D[j][0], D[j][1], D[j][2], D[j][3]);
+      p4[1] = make_uint4(D[j][4], D[j][5], D[j][6], D[j][7]);
+    }
+  }
+}
+// Software-pipelined: the tcgen05.ld of the next 4 accumulators x 8 columns is in flight while
+// the previous block is stored; TMEM is released (acce) right after the last load completes.
 template <int G>
 __device__ __forceinline__ void epi_drain(u32 tl, u32* __restrict__ raw_u, uint64_t* acce) {
+  u32 A[4][8], B[4][8];
+  drain_ld<G, 0>(tl, 0, A);
+  tmem_wait_ld();
+  drain_fence<G, 0>(A);
 #pragma unroll 1
   for (u32 v0 = 0; v0 < (u32)kV; v0 += 8) {
-    u32 D[4][8];
-#pragma unroll
-    for (int di = 0; di < 4; ++di)
-      if (group_diag(G, di) >= 0) tmem_ld8(tl + (u32)di * kV + v0, D[di]);
+    drain_ld<G, 1>(tl, v0, B);
+    drain_st<G, 0>(v0, raw_u, A);
     tmem_wait_ld();
-#pragma unroll
-    for (int di = 0; di < 4; ++di)
-      if (group_diag(G, di) >= 0) tmem_reg_fence(D[di]);
-    if (v0 + 8 == (u32)kV) {   // TMEM drained: the MMA may start the next round
+    drain_fence<G, 1>(B);
+    if (v0 + 8 < (u32)kV) {
+      drain_ld<G, 0>(tl, v0 + 8, A);
+    } else {   // TMEM drained: the MMA may start the next round
       tc_fence_before();
       mbar_arrive(acce);
     }
-#pragma unroll
-    for (int di = 0; di < 4; ++di) {
-      constexpr int dummy = 0;
-      (void)dummy;
-      if (group_diag(G, di) >= 0) {
-        uint4* p4 = (uint4*)(raw_u + (u32)group_diag(G, di) * (kU * kV) + v0);
-        p4[0] = make_uint4(D[di][0], D[di][1], D[di][2], D[di][3]);
-        p4[1] = make_uint4(D[di][4], D[di][5], D[di][6], D[di][7]);
-      }
+    drain_st<G, 1>(v0, raw_u, B);
+    if (v0 + 8 < (u32)kV) {
+      tmem_wait_ld();
+      drain_fence<G, 0>(A);
     }
   }
 }
@@ -382,7 +401,7 @@ __device__ __forceinline__ void unit_of(const TcArgs& a, u32 unit, uint4& pc, u3
 
 // PROF: per-warp phase timers (clock64) into a.prof -- a development build of the same kernel
 // (PE_TC_PROF=1); the production instantiation has no timers.
-// Walks one CTA's K-block sequence: units blockIdx.x, +gridDim.x, ...; per unit 4 rounds; per round
+// Walks one CTA's K-block sequence: units blockIdx.x, +gridDim.x, ...; per unit kRounds rounds; per round
 // the piece's K-blocks.
 struct KIter {
   u32 unit, kb, nkb, q0, chunk;
@@ -415,17 +434,18 @@ __device__ __forceinline__ void load_kblock(const TcArgs& a, const KIter& k, u32
 }
 
 template <bool PROF>
-static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 warps: <= 128 regs/thread
+static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 warps: <= 168 regs/thread
   unsigned long long g_entry = 0;
   if (PROF) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
   extern __shared__ uint8_t dsm[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = (uint8_t*)(((uintptr_t)dsm + 127) & ~(uintptr_t)127);   // kSmemBytes holds 128 B of slack
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accf, acce, dfull[kDataSlots];
   __shared__ u32 tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 32 * kProdPerStage); mbar_init(&empty[s], 1); }
+    // full: the group's threads + the leader's expect_tx arrival for the R planes
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 32 * kProdPerStage + 1); mbar_init(&empty[s], 1); }
     mbar_init(&accf, 1);
     mbar_init(&acce, 32 * kEpiWarps);
     for (int s = 0; s < kDataSlots; ++s) mbar_init(&dfull[s], 1);
@@ -447,22 +467,20 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 w
 
   if (warp >= kProdWarp0) {
     // ------------------------------------------------------------ producers
-    // 4 warps per stage: (giant | baby) x (rows 0-63 | rows 64-127).  Lane = (tq, rr): terms
-    // tq*4 .. tq*4+3 of the K-block, rows half*64 + rr + 4k (k < 16), i.e. 4 independent
-    // Shoup chains of stride 4 per lane.  Each group owns two data slots; its first warp's lane 0
-    // brings the group's NEXT K-block's per-term records in with TMA while the current one is
-    // being generated (no loader warp: the 16 warps fill the 4 SMSPs evenly).
+    // 2 warps per stage generate the 128 giant-step rows of 16 terms each: lane = (tq < 4,
+    // rr < 8), terms sub*16 + tq*4 .. +3, rows rr + 8k (k < 16) -- 4 Shoup chains of stride 8 per
+    // lane; one store instruction covers 8 rows x 16 bytes = all 32 banks.  The group's first
+    // lane brings in, with TMA, the K-block's baby-step planes (straight into the stage, counted
+    // on its full barrier) and the group's NEXT K-block's per-term records (two data slots).
     const int pw = warp - kProdWarp0;
     const int my_stage = pw / kProdPerStage, sub = pw % kProdPerStage;
-    const bool giant = sub < 2;
-    const u32 half = (u32)(sub & 1);
     const bool leader = sub == 0 && lane == 0;
-    const int tq = lane >> 2, rr = lane & 3;
-    const u32 planes0 = smem_u32(smem) + (giant ? 0u : 8u * kPlane) + (u32)my_stage * kStageBytes +
-                        plane_off(half * 64 + (u32)rr, (u32)tq * 4);
-    const u32 seed_off = giant ? ((u32)tq * 4 * kLSRec + half * 4 + (u32)rr) * 8
-                               : kDataLS + ((u32)tq * 4 * kCRec + half * 4 + (u32)rr) * 8;
-    const u32 mul_off = kDataLS + ((u32)tq * 4 * kCRec + (giant ? kC_mV4 : kC_m4)) * 8;
+    const u32 tq = (u32)(lane >> 3), rr = (u32)(lane & 7);
+    const u32 term0 = (u32)sub * 16 + tq * 4;     // first of the lane's 4 terms
+    const u32 stage0 = smem_u32(smem) + (u32)my_stage * kStageBytes;
+    const u32 planes0 = stage0 + plane_off<kLBOA>(rr, term0);
+    const u32 seed_off = (term0 * kLSRec + rr) * 8;
+    const u32 mul_off = kDataLS + (term0 * kCRec + kC_mL) * 8;
     const u32 slot0 = (u32)my_stage * 2;
     const u64 np = a.mp.np;
     KIter cur, ahead;
@@ -482,8 +500,12 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 w
       if (PROF) T[1] += c1 - c0;
       // the other slot held K-block guse-1, which every warp of the group consumed before the
       // stage could be released: refill it with the group's next K-block
-      if (leader && ahead.valid)
-        load_kblock(a, ahead, data0 + (slot0 + ((guse + 1) & 1)) * kDataSlot, &dfull[slot0 + ((guse + 1) & 1)]);
+      if (leader) {
+        mbar_expect_tx(&full[stage], kRBytes);
+        bulk_g2s(stage0 + 8 * kPlaneA, a.Rp + ((u64)cur.q0 / kKB + cur.kb) * kRBytes, kRBytes, &full[stage]);
+        if (ahead.valid)
+          load_kblock(a, ahead, data0 + (slot0 + ((guse + 1) & 1)) * kDataSlot, &dfull[slot0 + ((guse + 1) & 1)]);
+      }
       const u32 slot = slot0 + (guse & 1);
       const u32 dslot = data0 + slot * kDataSlot;
       u64 x[4], sm[4], sw[4];
@@ -493,13 +515,13 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 w
       if (PROF) T[0] += c1 - c0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        x[e] = lds64(dslot + seed_off + (u32)e * kLSRec * 8 * (giant ? 1u : 0u) + (u32)e * kCRec * 8 * (giant ? 0u : 1u));
+        x[e] = lds64(dslot + seed_off + (u32)e * kLSRec * 8);
         lds2(dslot + mul_off + (u32)e * kCRec * 8, sm[e], sw[e]);
       }
 #pragma unroll 2
       for (int k = 0; k < ((PROF && a.dbg == 2) ? 0 : 16); ++k) {
-        // row half*64 + rr + 4k: +4 rows = +64 bytes inside the same 8-row core-matrix pair
-        store_digits(planes0 + (u32)(k >> 1) * 128u + (u32)(k & 1) * 64u, x);
+        // row rr + 8k: the next 8-row core-matrix group, +128 bytes
+        store_digits<kPlaneA>(planes0 + (u32)k * 128u, x);
 #pragma unroll
         for (int e = 0; e < 4; ++e) x[e] = mul_shoup4(x[e], sm[e], sw[e], np);
       }
@@ -514,8 +536,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 w
     // ------------------------------------------------------------ epilogue (+ MMA issue in warp 0)
     // MMA issue and TMEM drain alternate (TMEM holds one round), so warp 0 issues a round's MMAs
     // (converged warp, elect.sync leader) and then drains its lane quarter.  Per round every
-    // epilogue warp only moves its 4 diagonals from TMEM to the unit's raw buffer (ping-pong by
-    // unit) and releases TMEM.  After the unit's 4 rounds warps 1-3 fold all 15 diagonals
+    // epilogue warp only moves its rows of the round's diagonals from TMEM to the unit's raw buffer (ping-pong by
+    // unit) and releases TMEM.  After the unit's last round warps 1-3 fold all 15 diagonals
     // exactly (X = sum D_d 2^{8d}) and reduce mod p into the piece's partial row -- warp 1 also
     // for warp 0's rows -- while warp 0 is already issuing the next unit's MMAs.
     const u32 u = (u32)(warp * 32 + lane);
@@ -524,7 +546,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 w
     u32* raw_cta = a.scratch + (u64)blockIdx.x * 2 * 15 * (kU * kV);
     const u64 C64 = a.Wd[8], C96 = a.Wd[12], C128 = a.C128;
     const u32 tbu = uni(tb);
-    const uint64_t d0 = smem_desc(uni(smem_u32(smem)));
+    const uint64_t dA0 = smem_desc(uni(smem_u32(smem)), kLBOA);
+    const uint64_t dB0 = smem_desc(uni(smem_u32(smem)) + 8 * kPlaneA, kLBOB);
     u32 round = 0, it = 0, nunit = 0;
     for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x, ++nunit) {
       uint4 pc; u32 chunk;
@@ -547,16 +570,15 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 w
             mbar_wait<32>(&full[stage], use & 1);
             if (PROF) T[1] += clk() - c0;
             tc_fence_after();
-            const uint64_t db = d0 + (uint64_t)((stage * kStageBytes) >> 4);
+            const uint64_t da = dA0 + (uint64_t)((stage * kStageBytes) >> 4);
+            const uint64_t db = dB0 + (uint64_t)((stage * kStageBytes) >> 4);
             // converge first so elect.sync picks the same leader (lane 0) every time: a
             // tcgen05.commit tracks the MMAs its own thread issued
             __syncwarp();
             if (elect_one()) {
-              if (!(PROF && a.dbg == 1)) switch (g) {
-                case 0: issue_round<0>(tbu, db, kb == 0); break;
-                case 1: issue_round<1>(tbu, db, kb == 0); break;
-                case 2: issue_round<2>(tbu, db, kb == 0); break;
-                default: issue_round<3>(tbu, db, kb == 0); break;
+              if (!(PROF && a.dbg == 1)) {
+                if (g == 0) issue_round<0>(tbu, da, db, kb == 0);
+                else issue_round<1>(tbu, da, db, kb == 0);
               }
               if (kb + 1 == nkb) mma_commit(&accf);   // accumulators complete after this K-block
               mma_commit(&empty[stage]);
@@ -573,12 +595,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 w
         if (PROF) T[0] += c1 - c0;
         tc_fence_after();
         u32* raw_u = raw + (u64)u * kV;
-        switch (g) {
-          case 0: epi_drain<0>(tl, raw_u, &acce); break;
-          case 1: epi_drain<1>(tl, raw_u, &acce); break;
-          case 2: epi_drain<2>(tl, raw_u, &acce); break;
-          default: epi_drain<3>(tl, raw_u, &acce); break;
-        }
+        if (g == 0) epi_drain<0>(tl, raw_u, &acce);
+        else epi_drain<1>(tl, raw_u, &acce);
         if (PROF && warp != g) T[1] += clk() - c1;
         if (PROF) T[3] += 1;
       }
@@ -586,7 +604,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 w
       long long c2 = clk();
       for (int pass = 0; pass < (warp == 1 ? 2 : (warp == kMmaWarp ? 0 : 1)); ++pass) {
         u32 ur = u;
-        if (pass == 1) {                 // warp 1: warp 0's rows, once all 4 warps drained round 3
+        if (pass == 1) {                 // warp 1: warp 0's rows, once all 4 warps drained the last round
           mbar_wait<32>(&acce, (round - 1) & 1);
           ur = (u32)lane;
         }
@@ -658,45 +676,65 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 16 w
 }
 
 // ---------------------------------------------------------------- setup kernels
-// Per padded term (pe_create): the C record -- baby-step chain seeds m^{64h + rr} (h*4 + rr), the
-// stride-4 chain multipliers m^4, m^{4V} and their Shoup constants.
-static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ C,
-                                  u64* __restrict__ mH, ModParams mp) {
+// Per padded term (pe_create): the C record -- the giant-step chain multiplier m^{8V} (stride 8
+// rows of L) and its Shoup constant.
+static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ C, ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
-    const u64 mm = to_mont(m[q], mp);
-    mH[q] = mont_pow(mm, 64ull * kV, mp);             // Montgomery form of m^{64V} (seed of row half 1)
-    const u64 a4 = from_mont(mont_pow(mm, 4, mp), mp);
-    const u64 aV4 = from_mont(mont_pow(mm, 4 * kV, mp), mp);
-    u64* rec = C + q * kCRec;
-    u64 x = mp.r1;                                      // mont(1)
-    const u64 x64 = mont_pow(mm, 64, mp);
-    for (int rr = 0; rr < 4; ++rr) {
-      rec[rr] = from_mont(x, mp);
-      rec[4 + rr] = from_mont(mont_mul(x, x64, mp), mp);
-      x = mont_mul(x, mm, mp);
-    }
-    rec[kC_m4] = a4; rec[kC_w4] = shoup_w(a4, mp.p);
-    rec[kC_mV4] = aV4; rec[kC_wV4] = shoup_w(aV4, mp.p);
+    const u64 aL = from_mont(mont_pow(to_mont(m[q], mp), 8 * kV, mp), mp);
+    C[q * kCRec + kC_mL] = aL;
+    C[q * kCRec + kC_wL] = shoup_w(aL, mp.p);
   }
 }
 
-// Per evaluation pass: LS records of chunk c: LS[c][q][h*4 + rr] = c_q m_q^{js0 + c*kChunk + (64h + rr) V}
-// (one exponentiation per term and chunk; the row-half-1 seeds by one product with m^{64V}).
-static __global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, const u64* __restrict__ mH,
-                                 u64 t_pad, u32 nch, u64 js0, u64* __restrict__ LS, ModParams mp) {
+// Per handle (pe_create): the baby-step byte planes R_t[i][v] = byte t of m_i^v (v < V), in the
+// stage layout of each K-block.  Thread = (4 terms, 8 consecutive v): one exponentiation m^{8o},
+// then 8 products; the 4 terms' digits are byte-transposed into 8 plane words per v.
+static __global__ void k_tc_rplanes(const u64* __restrict__ m, u64 t_pad, uint8_t* __restrict__ Rp, ModParams mp) {
+  const u64 total = t_pad / 4 * (kV / 8);
+  for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
+    const u64 quad = x / (kV / 8);
+    const u32 o = (u32)(x - quad * (kV / 8));
+    u64 mm[4], y[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      mm[e] = to_mont(m[quad * 4 + e], mp);
+      y[e] = mont_pow(mm[e], 8ull * o, mp);
+    }
+    uint8_t* kb = Rp + (quad * 4 / kKB) * kRBytes;
+    const u32 kbyte = (u32)(quad * 4 % kKB);
+#pragma unroll 1
+    for (u32 k = 0; k < 8; ++k) {
+      u64 v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = from_mont(y[e], mp);
+      const u32 off = plane_off<kLBOB>(8 * o + k, kbyte);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        u32 w = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) w |= (u32)((v[e] >> (8 * t)) & 0xff) << (8 * e);
+        *(u32*)(kb + t * kPlaneB + off) = w;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) y[e] = mont_mul(y[e], mm[e], mp);
+    }
+  }
+}
+
+// Per evaluation pass: LS records of chunk c: LS[c][q][rr] = c_q m_q^{js0 + c*kChunk + rr V}, rr < 8
+// (one exponentiation per term and chunk, then 7 products with m^V).
+static __global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, u64 t_pad, u32 nch, u64 js0,
+                                 u64* __restrict__ LS, ModParams mp) {
   const u64 total = t_pad * nch;
   for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
     const u64 chunk = x / t_pad, q = x - chunk * t_pad;
-    const u64 s0 = to_mont(seed_pow(c[q], m[q], js0 + chunk * kChunk, mp), mp);
+    u64 s = to_mont(seed_pow(c[q], m[q], js0 + chunk * kChunk, mp), mp);
     const u64 mV = mont_pow(to_mont(m[q], mp), kV, mp);
     u64* dst = LS + (chunk * t_pad + q) * kLSRec;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      u64 s = h ? mont_mul(s0, mH[q], mp) : s0;
-      for (int rr = 0; rr < 4; ++rr) {
-        dst[h * 4 + rr] = from_mont(s, mp);
-        s = mont_mul(s, mV, mp);
-      }
+    for (int rr = 0; rr < kLSRec; ++rr) {
+      dst[rr] = from_mont(s, mp);
+      s = mont_mul(s, mV, mp);
     }
   }
 }
