@@ -69,7 +69,7 @@ def ncu_traffic(kernel: str):
 
 # ---------------------------------------------------------------- clocks sampling
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -97,13 +97,24 @@ class ClockSampler:
                 out, _ = self.p.communicate()
             self.lines = [l for l in out.splitlines() if l.strip()]
 
-    def summary(self):
+    def summary(self, t0: float = None, t1: float = None):
+        """Samples taken while the GPU was loaded: wall-clock window [t0, t1] (warm-up start to the
+        end of the timed region; nvidia-smi needs ~0.1-0.3 s to start, so the window opens at the
+        warm-up)."""
+        import datetime
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for l in getattr(self, "lines", []):
             f = [x.strip() for x in l.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            if ts is not None and t0 is not None and not (t0 - 0.05 <= ts <= t1 + 0.05):
+                continue
+            f = f[1:]
             try:
                 sm.append(float(f[1]))
                 mx = max(mx, float(f[2]))
@@ -177,7 +188,7 @@ def workload_config(w, info):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -262,27 +273,30 @@ def main():
         def step():
             return sh.run(eval_local, w.j0)
 
-    # ---- device-timed region
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    ctx.kernel_stats()                      # drop anything recorded so far
-    barrier()
-    torch.cuda.synchronize()
-    ctx.set_timing(True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # ---- device-timed region (clock samples from the warm-up on: nvidia-smi starts slowly)
     with ClockSampler(local_rank) as clk:
+        t_load0 = time.time()
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        ctx.kernel_stats()                      # drop anything recorded so far
+        barrier()
+        torch.cuda.synchronize()
+        ctx.set_timing(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
+        t_load1 = time.time()
+        time.sleep(0.15)                        # let the sampler flush its last line
     barrier()
     ctx.set_timing(False)
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     ks = ctx.kernel_stats()
     value = w.t * w.T / (ms * 1e-3)
-    clocks = clk.summary()
+    clocks = clk.summary(t_load0, t_load1)
 
     # ---- roofline of the dominant kernel (k_tc on the tensor-core path, else k_step)
     pk, pk_kind = peaks()
@@ -302,13 +316,13 @@ def main():
         mma = {n: pe.bench_mma(n) for n in (64, 128)}                # same-run tcgen05 i8 issue rate
         roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": ncu_traffic("ktc"),
-                "kernel": "k_tc (tcgen05.mma kind::i8 M=128 N=128 K=32, u8 x u8 -> s32 in TMEM)",
+                "kernel": "k_tc (tcgen05.mma kind::i8 M=128 N=64 K=32, u8 x u8 -> s32 in TMEM)",
                 "peak_basis": (f"int8 dense tensor ops = 2 x {pk_kind} bf16_tflops "
                                f"{pk.get('bf16_tflops', 1590.0):.1f} (guide nominal ratio 4.5/2.25 PFLOP/s); "
                                f"sustained basis 2 x {pk.get('bf16_tflops_sustained', 1375.5):.1f}"),
                 "frac_of_sustained": achieved / (2e12 * pk.get("bf16_tflops_sustained", 1375.5)),
-                "mma_n128_ceiling": mma[128] / 1e12, "frac_of_mma_n128_ceiling": achieved / mma[128],
-                "mma_n64_ceiling": mma[64] / 1e12,
+                "mma_n64_ceiling": mma[64] / 1e12, "frac_of_mma_n64_ceiling": achieved / mma[64],
+                "mma_n128_ceiling": mma[128] / 1e12,
                 "term_points_per_s": tp_rate / 1e12,
                 "frac_of_imad_mulmod_roofline": tp_rate / imad_peak,
                 "imad_mulmod_roofline": imad_peak / 1e12,

@@ -121,6 +121,7 @@ struct pe_ctx {
   u32 tc_npieces = 0, tc_nslots = 0;
   int n_sm = 148;
   u64* d_tcC = nullptr;   // [t_pad][2] tensor-core path C records (tc.cuh)
+  u64* d_tcMS = nullptr;  // [t_pad][2] Montgomery m^V, m^{kChunk} (k_tc_seed)
   uint8_t* d_tcR = nullptr;   // [t_pad / 32][tc::kRBytes] baby-step byte planes m^v, v < 64 (tc.cuh)
   uint4* d_piece = nullptr;
   u32* d_tc_slot_start = nullptr;
@@ -146,7 +147,7 @@ static void free_all(pe_ctx* h) {
   cudaStream_t s = h->stream;
   for (void* q : {(void*)h->d_c, (void*)h->d_m, (void*)h->d_w, (void*)h->d_perm, (void*)h->d_ms, (void*)h->d_mpd,
                   (void*)h->d_mspd, (void*)h->d_wt_info, (void*)h->d_slot_start, (void*)h->d_partial,
-                  (void*)h->d_out_scratch, (void*)h->d_tcC, (void*)h->d_tcR,
+                  (void*)h->d_out_scratch, (void*)h->d_tcC, (void*)h->d_tcR, (void*)h->d_tcMS,
                   (void*)h->d_tc_scratch, (void*)h->d_piece, (void*)h->d_tc_slot_start,
                   (void*)h->d_seed})
     if (q) cudaFreeAsync(q, s);
@@ -418,11 +419,14 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   std::vector<u32> tc_slot_start(G + 1);
   if (h->tc_mode != 0 && (h->path == kInt4 || h->path == kFp64 || h->path == kInt32)) {
     const u64 tp = h->t_pad;
-    if (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp) || dalloc(&h->d_tcR, (size_t)tp / tc::kKB * tc::kRBytes))
+    if (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp) || dalloc(&h->d_tcMS, (size_t)2 * tp) ||
+        dalloc(&h->d_tcR, (size_t)((tp + 2 * tc::kKB - 1) / (2 * tc::kKB)) * 2 * tc::kRBytes))
       return g_last_error;
-    tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_tcC, h->mp);
+    tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
     CU(cudaGetLastError());
-    tc::k_tc_rplanes<<<grid_for(tp / 4 * (tc::kV / 8), 256), 256, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
+    const u64 nrp = (tp + 2 * tc::kKB - 1) / (2 * tc::kKB);   // blocks of 2 K-blocks
+    tc::k_tc_rplanes<<<(unsigned)std::max<u64>(1, std::min<u64>(nrp, 148ull * 16)), tc::kRpThreads, 0, s>>>(
+        h->d_m, tp, h->d_tcR, h->mp);
     CU(cudaGetLastError());
     // pieces: each bucket's padded range split into ceil(n / kPieceMax) near-equal runs of whole
     // K-blocks (<= kPieceMax terms keeps every int32 diagonal sum exact); slots contiguous per bucket
@@ -620,8 +624,9 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
     const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
-    tc::k_tc_seed<<<grid_for((u64)h->t_pad * nch, 256), 256, 0, s>>>(h->d_c, h->d_m, h->t_pad, nch, j0 + k0,
-                                                                      h->d_seed, h->mp);
+    const u64 nseed = (u64)h->t_pad * ((nch + tc::kSeedChunks - 1) / tc::kSeedChunks);
+    tc::k_tc_seed<<<grid_for(nseed, 256), 256, 0, s>>>(h->d_c, h->d_m, h->d_tcMS, h->t_pad, nch, j0 + k0, h->d_seed,
+                                                       h->mp);
     CU(cudaGetLastError());
     tc::TcArgs a;
     a.LS = h->d_seed;

@@ -640,7 +640,9 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
               lo += add_lo;
               hi += add_hi + (lo < add_lo ? 1ull : 0ull);
             }
-            res[j] = reduce128(hi, lo, mp);
+            // the baby-step planes hold Montgomery residues m^v 2^64 (k_tc_rplanes), so the sum is
+            // 2^64 X: one REDC (x 2^-64) is the reduction; REDC needs its high word < p
+            res[j] = redc(hi < mp.p ? hi : hi % mp.p, lo, mp);
           }
           if (kbase + v0 + 4 <= a.npts) {
             ulonglong2* dst = (ulonglong2*)(prow + kbase + v0);
@@ -677,64 +679,91 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
 
 // ---------------------------------------------------------------- setup kernels
 // Per padded term (pe_create): the C record -- the giant-step chain multiplier m^{8V} (stride 8
-// rows of L) and its Shoup constant.
-static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ C, ModParams mp) {
+// rows of L) and its Shoup constant -- and, for the per-pass seeds, Montgomery m^V and m^{kChunk}.
+static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ C, u64* __restrict__ MS,
+                                  ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
-    const u64 aL = from_mont(mont_pow(to_mont(m[q], mp), 8 * kV, mp), mp);
+    const u64 mV = mont_pow(to_mont(m[q], mp), kV, mp);
+    const u64 aL = from_mont(mont_pow(mV, 8, mp), mp);
     C[q * kCRec + kC_mL] = aL;
     C[q * kCRec + kC_wL] = shoup_w(aL, mp.p);
+    MS[2 * q] = mV;
+    MS[2 * q + 1] = mont_pow(mV, kU, mp);              // m^{kChunk}
   }
 }
 
-// Per handle (pe_create): the baby-step byte planes R_t[i][v] = byte t of m_i^v (v < V), in the
-// stage layout of each K-block.  Thread = (4 terms, 8 consecutive v): one exponentiation m^{8o},
-// then 8 products; the 4 terms' digits are byte-transposed into 8 plane words per v.
-static __global__ void k_tc_rplanes(const u64* __restrict__ m, u64 t_pad, uint8_t* __restrict__ Rp, ModParams mp) {
-  const u64 total = t_pad / 4 * (kV / 8);
-  for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
-    const u64 quad = x / (kV / 8);
-    const u32 o = (u32)(x - quad * (kV / 8));
-    u64 mm[4], y[4];
+// Per handle (pe_create): the baby-step byte planes R_t[i][v] = byte t of the Montgomery residue
+// m_i^v 2^64 mod p (v < V) in the stage layout of each K-block (any representative < 2^64 gives
+// exact byte products; the epilogue's REDC removes the 2^64).  Block = 2 K-blocks staged in
+// shared memory; thread = (4 terms, rows r + 8j): one warp's stores cover 8 consecutive rows x
+// 16 bytes, and the block leaves with 16-byte coalesced stores.
+constexpr int kRpThreads = 128;
+static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __restrict__ m, u64 t_pad,
+                                                                  uint8_t* __restrict__ Rp, ModParams mp) {
+  __shared__ __align__(16) uint8_t st[2 * kRBytes];
+  const u64 nblk = (t_pad + 2 * kKB - 1) / (2 * kKB);   // Rp is allocated for a whole last block
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const u32 ql = (u32)(lane >> 3), r = (u32)(lane & 7);
+  const u32 kbl = (u32)warp >> 1, h = (u32)warp & 1;
+  const u32 base = kbl * kRBytes + h * kLBOB + r * 16u + ql * 4u;
+  for (u64 blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const u64 q0 = blk * 2 * kKB + kbl * kKB + h * 16 + ql * 4;
+    u64 y[4], m8[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      mm[e] = to_mont(m[quad * 4 + e], mp);
-      y[e] = mont_pow(mm[e], 8ull * o, mp);
+      const u64 mm = to_mont(q0 + e < t_pad ? m[q0 + e] : 0ull, mp);
+      const u64 m2 = mont_mul(mm, mm, mp), m4 = mont_mul(m2, m2, mp);
+      m8[e] = mont_mul(m4, m4, mp);
+      u64 x = mp.r1;                                     // Montgomery 1 = m^0
+      if (r & 1) x = mm;
+      if (r & 2) x = mont_mul(x, m2, mp);
+      if (r & 4) x = mont_mul(x, m4, mp);
+      y[e] = x;                                          // m^r
     }
-    uint8_t* kb = Rp + (quad * 4 / kKB) * kRBytes;
-    const u32 kbyte = (u32)(quad * 4 % kKB);
 #pragma unroll 1
-    for (u32 k = 0; k < 8; ++k) {
-      u64 v[4];
+    for (u32 j = 0; j < (u32)kV / 8; ++j) {              // row r + 8j
+      const u32 l0 = lo32(y[0]), l1 = lo32(y[1]), l2 = lo32(y[2]), l3 = lo32(y[3]);
+      const u32 h0 = hi32(y[0]), h1 = hi32(y[1]), h2 = hi32(y[2]), h3 = hi32(y[3]);
+      u32 wd[8];
+      u32 a = prmt(l0, l1, 0x5140), b = prmt(l2, l3, 0x5140), c = prmt(l0, l1, 0x7362), d = prmt(l2, l3, 0x7362);
+      wd[0] = prmt(a, b, 0x5410); wd[1] = prmt(a, b, 0x7632); wd[2] = prmt(c, d, 0x5410); wd[3] = prmt(c, d, 0x7632);
+      a = prmt(h0, h1, 0x5140); b = prmt(h2, h3, 0x5140); c = prmt(h0, h1, 0x7362); d = prmt(h2, h3, 0x7362);
+      wd[4] = prmt(a, b, 0x5410); wd[5] = prmt(a, b, 0x7632); wd[6] = prmt(c, d, 0x5410); wd[7] = prmt(c, d, 0x7632);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = from_mont(y[e], mp);
-      const u32 off = plane_off<kLBOB>(8 * o + k, kbyte);
+      for (int t = 0; t < 8; ++t) *(u32*)(st + base + (u32)t * kPlaneB + j * 128u) = wd[t];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        u32 w = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) w |= (u32)((v[e] >> (8 * t)) & 0xff) << (8 * e);
-        *(u32*)(kb + t * kPlaneB + off) = w;
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) y[e] = mont_mul(y[e], mm[e], mp);
+      for (int e = 0; e < 4; ++e) y[e] = mont_mul(y[e], m8[e], mp);
     }
+    __syncthreads();
+    uint4* dst = (uint4*)(Rp + blk * 2 * kRBytes);
+    const uint4* src = (const uint4*)st;
+    for (u32 i = threadIdx.x; i < 2 * kRBytes / 16; i += kRpThreads) dst[i] = src[i];
+    __syncthreads();
   }
 }
 
-// Per evaluation pass: LS records of chunk c: LS[c][q][rr] = c_q m_q^{js0 + c*kChunk + rr V}, rr < 8
-// (one exponentiation per term and chunk, then 7 products with m^V).
-static __global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, u64 t_pad, u32 nch, u64 js0,
-                                 u64* __restrict__ LS, ModParams mp) {
-  const u64 total = t_pad * nch;
+// Per evaluation pass: LS records of chunk c: LS[c][q][rr] = c_q m_q^{js0 + c*kChunk + rr V}, rr < 8.
+// Thread = (term, kSeedChunks consecutive chunks): one exponentiation, then products with the
+// precomputed m^V (within a chunk) and m^{kChunk} (between chunks).
+constexpr u32 kSeedChunks = 4;
+static __global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, const u64* __restrict__ MS,
+                                 u64 t_pad, u32 nch, u64 js0, u64* __restrict__ LS, ModParams mp) {
+  const u32 ngrp = (nch + kSeedChunks - 1) / kSeedChunks;
+  const u64 total = t_pad * ngrp;
   for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
-    const u64 chunk = x / t_pad, q = x - chunk * t_pad;
-    u64 s = to_mont(seed_pow(c[q], m[q], js0 + chunk * kChunk, mp), mp);
-    const u64 mV = mont_pow(to_mont(m[q], mp), kV, mp);
-    u64* dst = LS + (chunk * t_pad + q) * kLSRec;
+    const u64 grp = x / t_pad, q = x - grp * t_pad;
+    const u32 ch0 = (u32)grp * kSeedChunks, ch1 = min(nch, ch0 + kSeedChunks);
+    const u64 mV = MS[2 * q], mC = MS[2 * q + 1];
+    u64 s0 = to_mont(seed_pow(c[q], m[q], js0 + (u64)ch0 * kChunk, mp), mp);
+    for (u32 ch = ch0; ch < ch1; ++ch) {
+      u64* dst = LS + ((u64)ch * t_pad + q) * kLSRec;
+      u64 s = s0;
 #pragma unroll
-    for (int rr = 0; rr < kLSRec; ++rr) {
-      dst[rr] = from_mont(s, mp);
-      s = mont_mul(s, mV, mp);
+      for (int rr = 0; rr < kLSRec; ++rr) {
+        dst[rr] = from_mont(s, mp);
+        s = mont_mul(s, mV, mp);
+      }
+      s0 = mont_mul(s0, mC, mp);
     }
   }
 }

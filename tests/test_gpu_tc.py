@@ -153,6 +153,18 @@ def test_tc_batch_polys():
     assert np.array_equal(out[ro[1]:ro[2]], oracle.eval_incremental(f.p, f.n, h.coeffs, h.exps, f.alpha, f.j0, f.T))
 
 
+@pytest.mark.parametrize("R", [1, 2])
+def test_tc_small_tiles_odd_kblocks(R):
+    """R = 1 / 2 pads buckets to 32 / 64 terms only, so the padded term count can be an odd number
+    of K-blocks (the baby-step plane builder works in pairs of K-blocks)."""
+    w = synth.random_small(530 + R, P62, 4, 33, 2, 200, 3)
+    with pe.Context.from_workload(w, path=pe.PATH_TC, R=R) as ctx:
+        assert ctx.info()["R"] == R and ctx.uses_tc(w.T)
+        assert (ctx.info()["t_padded"] // 32) % 2 == 1 or R == 2
+        out = ctx.eval(w.j0, w.T)
+    assert np.array_equal(out, oracle.eval_workload(w))
+
+
 def test_mma_probe_rate():
     """pe_bench_mma runs and reports a plausible int8 rate (> 100 TOPS at N = 128)."""
     assert pe.bench_mma(128, 4000) > 1e14
