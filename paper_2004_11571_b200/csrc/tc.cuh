@@ -101,7 +101,7 @@ struct TcArgs {
   ModParams mp;
   unsigned long long* prof;  // optional phase timers [gridDim][warps][4] (PE_TC_PROF=1), else null
   int dbg;                   // development only (PE_TC_DEBUG, PROF build): 1 = skip the MMAs,
-                             // 2 = producers skip generation, 3 = epilogue skips its scratch loads
+                             // 2 = producers skip generation, 3 = the TMEM drain skips its stores
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -327,7 +327,7 @@ __device__ __forceinline__ void fold_add(u32 (&X)[5], u32 Dv) {
 }
 
 // Epilogue critical part: drain round G's diagonals of thread row u from TMEM into the unit's raw
-// buffer (raw[d][u][v], u32: the diagonal sums themselves) and release TMEM (acce) as soon as the
+// buffer (raw[d][v/4][u][v%4], u32: the diagonal sums themselves) and release TMEM (acce) as soon as the
 // last block is in registers -- only tcgen05.ld and fire-and-forget stores, so the MMA warp can
 // start the next round almost at once.  Four accumulators (32 registers) per tcgen05.wait.
 template <int G, int H>
@@ -347,16 +347,17 @@ __device__ __forceinline__ void drain_st(u32 v0, u32* __restrict__ raw_u, const 
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     if (group_diag(G, 4 * H + j) >= 0) {
-      uint4* p4 = (uint4*)(raw_u + (u32)group_diag(G, 4 * H + j) * (kU * kV) + v0);
+      // raw[d][v / 4][u][v % 4]: a warp's 16-byte stores cover 512 contiguous bytes
+      uint4* p4 = (uint4*)(raw_u + (u32)group_diag(G, 4 * H + j) * (kU * kV) + (v0 >> 2) * (kU * 4));
       p4[0] = make_uint4(D[j][0], D[j][1], D[j][2], D[j][3]);
-      p4[1] = make_uint4(D[j][4], D[j][5], D[j][6], D[j][7]);
+      p4[kU] = make_uint4(D[j][4], D[j][5], D[j][6], D[j][7]);
     }
   }
 }
 // Software-pipelined: the tcgen05.ld of the next 4 accumulators x 8 columns is in flight while
 // the previous block is stored; TMEM is released (acce) right after the last load completes.
 template <int G>
-__device__ __forceinline__ void epi_drain(u32 tl, u32* __restrict__ raw_u, uint64_t* acce) {
+__device__ __forceinline__ void epi_drain(u32 tl, u32* __restrict__ raw_u, uint64_t* acce, bool st = true) {
   u32 A[4][8], B[4][8];
   drain_ld<G, 0>(tl, 0, A);
   tmem_wait_ld();
@@ -364,7 +365,7 @@ __device__ __forceinline__ void epi_drain(u32 tl, u32* __restrict__ raw_u, uint6
 #pragma unroll 1
   for (u32 v0 = 0; v0 < (u32)kV; v0 += 8) {
     drain_ld<G, 1>(tl, v0, B);
-    drain_st<G, 0>(v0, raw_u, A);
+    if (st) drain_st<G, 0>(v0, raw_u, A);
     tmem_wait_ld();
     drain_fence<G, 1>(B);
     if (v0 + 8 < (u32)kV) {
@@ -373,7 +374,7 @@ __device__ __forceinline__ void epi_drain(u32 tl, u32* __restrict__ raw_u, uint6
       tc_fence_before();
       mbar_arrive(acce);
     }
-    drain_st<G, 1>(v0, raw_u, B);
+    if (st) drain_st<G, 1>(v0, raw_u, B);
     if (v0 + 8 < (u32)kV) {
       tmem_wait_ld();
       drain_fence<G, 0>(A);
@@ -594,9 +595,10 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
         long long c1 = clk();
         if (PROF) T[0] += c1 - c0;
         tc_fence_after();
-        u32* raw_u = raw + (u64)u * kV;
-        if (g == 0) epi_drain<0>(tl, raw_u, &acce);
-        else epi_drain<1>(tl, raw_u, &acce);
+        u32* raw_u = raw + (u64)u * 4;
+        const bool st = !(PROF && a.dbg == 3);
+        if (g == 0) epi_drain<0>(tl, raw_u, &acce, st);
+        else epi_drain<1>(tl, raw_u, &acce, st);
         if (PROF && warp != g) T[1] += clk() - c1;
         if (PROF) T[3] += 1;
       }
@@ -608,14 +610,14 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
           mbar_wait<32>(&acce, (round - 1) & 1);
           ur = (u32)lane;
         }
-        const u32* rr_ = raw + (u64)ur * kV;
+        const u32* rr_ = raw + (u64)ur * 4;
         const u64 kbase = (u64)chunk * kChunk + (u64)ur * kV;   // multiple of 8; ldp multiple of 8
 #pragma unroll 1
         for (u32 v0 = 0; v0 < (u32)kV; v0 += 4) {
           u32 D[15][4];
 #pragma unroll
           for (int d = 0; d < 15; ++d) {
-            const uint4 q = *(const uint4*)(rr_ + (u32)d * (kU * kV) + v0);
+            const uint4 q = *(const uint4*)(rr_ + (u32)d * (kU * kV) + (v0 >> 2) * (kU * 4));
             D[d][0] = q.x; D[d][1] = q.y; D[d][2] = q.z; D[d][3] = q.w;
           }
           u64 res[4];
