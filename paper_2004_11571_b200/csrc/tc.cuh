@@ -61,16 +61,17 @@ constexpr u32 kLBOB = 1024 + 64;          // R planes (B, 64 rows): +64 B spread
 constexpr u32 kPlaneB = kLBOB + 1024;
 constexpr u32 kStageBytes = 8 * kPlaneA + 8 * kPlaneB;   // 8 L planes + 8 R planes (49664 B)
 // Per-term records (array of structs, so one K-block's data is two contiguous bulk copies):
-//   LS record (per chunk, 8 u64): giant-step chain seeds c m^{j_s + rr V}, rr < 8
-//   C  record (2 u64): the giant-step chain multiplier m^{8V} and its Shoup constant
+//   LS record (per chunk, 1 u64): the chunk seed c m^{j_s}
+//   C  record (10 u64): the giant-step chain multiplier m^{8V} and its Shoup constant, and the
+//      Montgomery residues of m^{rr V} (rr < 8) that turn the chunk seed into the 8 chain seeds
 // The baby-step factors R[i][v] = m_i^v do not depend on the points: pe_create writes their byte
 // planes once per handle, in the stage's R-plane layout ([t_pad / 32][kRBytes], k_tc_rplanes),
 // and each K-block's 16.5 KB is one TMA bulk copy into the stage.
-constexpr int kLSRec = 8, kCRec = 2;
-enum { kC_mL = 0, kC_wL = 1 };
+constexpr int kLSRec = 1, kCRec = 10;
+enum { kC_mL = 0, kC_wL = 1, kC_g0 = 2 };
 constexpr u32 kRBytes = 8 * kPlaneB;                  // one K-block's R planes (16896 B)
-constexpr u32 kDataLS = kKB * kLSRec * 8;             // 2048 B
-constexpr u32 kDataSlot = kDataLS + kKB * kCRec * 8;  // 2560 B
+constexpr u32 kDataLS = kKB * kLSRec * 8;             // 256 B
+constexpr u32 kDataSlot = kDataLS + kKB * kCRec * 8;  // 2816 B
 constexpr int kDataSlots = 2 * kStages;               // 2 per producer group: current + next K-block
 constexpr u32 kSmemBytes = kStages * kStageBytes + kDataSlots * kDataSlot + 128;
 constexpr int kRounds = 2;
@@ -88,8 +89,8 @@ __host__ __device__ constexpr int group_diag(int g, int di) {
 }
 
 struct TcArgs {
-  const u64* LS;         // [nch][t_pad][8] LS records (giant-step chain seeds of each chunk)
-  const u64* C;          // [t_pad][2] C records (giant-step chain multiplier)
+  const u64* LS;         // [nch][t_pad] chunk seeds c m^{j_s}
+  const u64* C;          // [t_pad][10] C records (giant-step chain multiplier, m^{rr V} table)
   const uint8_t* Rp;     // [t_pad / 32][kRBytes] baby-step byte planes (k_tc_rplanes)
   const uint4* piece;    // x = first padded term, y = K-blocks, z = partial slot (sorted by size desc)
   u64* partial;          // [n_slots][ldp]
@@ -101,7 +102,8 @@ struct TcArgs {
   ModParams mp;
   unsigned long long* prof;  // optional phase timers [gridDim][warps][4] (PE_TC_PROF=1), else null
   int dbg;                   // development only (PE_TC_DEBUG, PROF build): 1 = skip the MMAs,
-                             // 2 = producers skip generation, 3 = the TMEM drain skips its stores
+                             // 2 = producers skip generation, 3 = the TMEM drain skips its stores,
+                             // 4 = no baby-step plane copies, 6 = 2 + 4, 7 = 6 without the A collector
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -176,7 +178,7 @@ __host__ __device__ constexpr int run_pos(int G, int sd, int k) {
 // 0), grouped by L plane s so the A operand (L_s) is read from shared memory once per K-block and
 // reused from the collector buffer.  Fully unrolled: every operand offset and collector mode is a
 // compile-time constant.
-template <int G>
+template <int G, bool NOCOL = false>
 __device__ __forceinline__ void issue_round(u32 tb, uint64_t da, uint64_t db, bool first_kb) {
 #pragma unroll
   for (int sd = 0; sd < 8; ++sd) {
@@ -191,7 +193,7 @@ __device__ __forceinline__ void issue_round(u32 tb, uint64_t da, uint64_t db, bo
         const u32 dt = tb + (u32)di * kV;
         const uint64_t ad = da + (uint64_t)((u32)sd * (kPlaneA >> 4));
         const uint64_t bd = db + (uint64_t)((u32)(d - sd) * (kPlaneB >> 4));
-        if (n == 1) mma_u8c<0>(dt, ad, bd, acc);
+        if (n == 1 || NOCOL) mma_u8c<0>(dt, ad, bd, acc);
         else if (pos == 0) mma_u8c<1>(dt, ad, bd, acc);
         else if (pos == n - 1) mma_u8c<3>(dt, ad, bd, acc);
         else mma_u8c<2>(dt, ad, bd, acc);
@@ -424,6 +426,15 @@ struct KIter {
       if (++g == kRounds) { g = 0; unit += gridDim.x; load(a); }
     }
   }
+  // n K-blocks ahead (a producer group's next K-block is kStages ahead): one add and compare
+  // unless a round or unit boundary is crossed
+  __device__ __forceinline__ void advance(const TcArgs& a, u32 n) {
+    kb += n;
+    while (valid && kb >= nkb) {
+      kb -= nkb;
+      if (++g == kRounds) { g = 0; unit += gridDim.x; load(a); }
+    }
+  }
 };
 
 // The two TMA bulk copies of one K-block's per-term records into a data slot.
@@ -480,47 +491,56 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
     const u32 term0 = (u32)sub * 16 + tq * 4;     // first of the lane's 4 terms
     const u32 stage0 = smem_u32(smem) + (u32)my_stage * kStageBytes;
     const u32 planes0 = stage0 + plane_off<kLBOA>(rr, term0);
-    const u32 seed_off = (term0 * kLSRec + rr) * 8;
+    const u32 seed_off = term0 * kLSRec * 8;
     const u32 mul_off = kDataLS + (term0 * kCRec + kC_mL) * 8;
+    const u32 g_off = kDataLS + (term0 * kCRec + kC_g0 + rr) * 8;
+    const ModParams mp = a.mp;
     const u32 slot0 = (u32)my_stage * 2;
     const u64 np = a.mp.np;
+    // the group owns K-blocks my_stage, my_stage + kStages, ... of the CTA's sequence
     KIter cur, ahead;
     cur.init(a);
-    ahead.init(a);
-    for (int i = 0; i < my_stage; ++i) ahead.next(a);                 // the group's first K-block
-    if (leader && ahead.valid) load_kblock(a, ahead, data0 + slot0 * kDataSlot, &dfull[slot0]);
-    for (int i = 0; i < kStages; ++i) ahead.next(a);                  // ... and its second
+    cur.advance(a, (u32)my_stage);                                   // the group's first K-block
+    ahead = cur;
+    ahead.advance(a, kStages);                                       // ... and its second
+    if (leader && cur.valid) load_kblock(a, cur, data0 + slot0 * kDataSlot, &dfull[slot0]);
     u32 guse = 0;
-    for (u32 it = 0; cur.valid; ++it, cur.next(a)) {
-      const u32 stage = it % kStages;
-      if ((int)stage != my_stage) continue;
-      const u32 use = it / kStages;
+    // the lane's chain seeds and multipliers of the group's K-block number g (data slot g & 1)
+    u64 x[4], sm[4], sw[4];
+    auto fetch = [&](u32 g) {
+      const u32 dslot = data0 + (slot0 + (g & 1)) * kDataSlot;
+      const long long f0 = clk();
+      mbar_wait<64>(&dfull[slot0 + (g & 1)], (g >> 1) & 1);
+      if (PROF) T[0] += clk() - f0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        // chain seed of row rr: c m^{j_s} (normal) x Montgomery m^{rr V} -> c m^{j_s + rr V}
+        x[e] = mont_mul(lds64(dslot + seed_off + (u32)e * kLSRec * 8), lds64(dslot + g_off + (u32)e * kCRec * 8), mp);
+        lds2(dslot + mul_off + (u32)e * kCRec * 8, sm[e], sw[e]);
+      }
+    };
+    if (cur.valid) fetch(0);
+    for (; cur.valid; cur = ahead, ahead.advance(a, kStages)) {
+      const u32 stage = (u32)my_stage;
+      const u32 use = guse;
       long long c0 = clk();
       mbar_wait<64>(&empty[stage], (use & 1) ^ 1);
       long long c1 = clk();
       if (PROF) T[1] += c1 - c0;
-      // the other slot held K-block guse-1, which every warp of the group consumed before the
-      // stage could be released: refill it with the group's next K-block
+      // the other slot held K-block guse-1, which every warp of the group read (at the end of
+      // K-block guse-2) before arriving on that stage fill: refill it with the group's next K-block
       if (leader) {
-        mbar_expect_tx(&full[stage], kRBytes);
-        bulk_g2s(stage0 + 8 * kPlaneA, a.Rp + ((u64)cur.q0 / kKB + cur.kb) * kRBytes, kRBytes, &full[stage]);
+        if (PROF && (a.dbg == 4 || a.dbg == 6 || a.dbg == 7)) {
+          mbar_arrive(&full[stage]);
+        } else {
+          mbar_expect_tx(&full[stage], kRBytes);
+          bulk_g2s(stage0 + 8 * kPlaneA, a.Rp + ((u64)cur.q0 / kKB + cur.kb) * kRBytes, kRBytes, &full[stage]);
+        }
         if (ahead.valid)
           load_kblock(a, ahead, data0 + (slot0 + ((guse + 1) & 1)) * kDataSlot, &dfull[slot0 + ((guse + 1) & 1)]);
       }
-      const u32 slot = slot0 + (guse & 1);
-      const u32 dslot = data0 + slot * kDataSlot;
-      u64 x[4], sm[4], sw[4];
-      c0 = clk();
-      mbar_wait<64>(&dfull[slot], (guse >> 1) & 1);
-      c1 = clk();
-      if (PROF) T[0] += c1 - c0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        x[e] = lds64(dslot + seed_off + (u32)e * kLSRec * 8);
-        lds2(dslot + mul_off + (u32)e * kCRec * 8, sm[e], sw[e]);
-      }
 #pragma unroll 2
-      for (int k = 0; k < ((PROF && a.dbg == 2) ? 0 : 16); ++k) {
+      for (int k = 0; k < ((PROF && (a.dbg == 2 || a.dbg >= 6)) ? 0 : 16); ++k) {
         // row rr + 8k: the next 8-row core-matrix group, +128 bytes
         store_digits<kPlaneA>(planes0 + (u32)k * 128u, x);
 #pragma unroll
@@ -530,8 +550,10 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       mbar_arrive(&full[stage]);
       if (PROF) T[2] += clk() - c1;
       if (PROF) T[3] += 1;
-      for (int i = 0; i < kStages; ++i) ahead.next(a);
       ++guse;
+      // next K-block's seeds while this stage is being consumed (its data arrived during this
+      // K-block); the product latency hides in the wait for the stage
+      if (ahead.valid) fetch(guse);
     }
   } else {
     // ------------------------------------------------------------ epilogue (+ MMA issue in warp 0)
@@ -577,7 +599,10 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
             // tcgen05.commit tracks the MMAs its own thread issued
             __syncwarp();
             if (elect_one()) {
-              if (!(PROF && a.dbg == 1)) {
+              if (PROF && a.dbg == 7) {
+                if (g == 0) issue_round<0, true>(tbu, da, db, kb == 0);
+                else issue_round<1, true>(tbu, da, db, kb == 0);
+              } else if (!(PROF && a.dbg == 1)) {
                 if (g == 0) issue_round<0>(tbu, da, db, kb == 0);
                 else issue_round<1>(tbu, da, db, kb == 0);
               }
@@ -681,12 +706,18 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
 
 // ---------------------------------------------------------------- setup kernels
 // Per padded term (pe_create): the C record -- the giant-step chain multiplier m^{8V} (stride 8
-// rows of L) and its Shoup constant -- and, for the per-pass seeds, Montgomery m^V and m^{kChunk}.
+// rows of L), its Shoup constant and the Montgomery table m^{rr V} (rr < 8) -- and, for the
+// per-pass chunk seeds, Montgomery m^V and m^{kChunk}.
 static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ C, u64* __restrict__ MS,
                                   ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
     const u64 mV = mont_pow(to_mont(m[q], mp), kV, mp);
-    const u64 aL = from_mont(mont_pow(mV, 8, mp), mp);
+    u64 g = mp.r1;                                     // Montgomery m^{rr V}
+    for (int rr = 0; rr < 8; ++rr) {
+      C[q * kCRec + kC_g0 + rr] = g;
+      g = mont_mul(g, mV, mp);
+    }
+    const u64 aL = from_mont(g, mp);                   // m^{8V}
     C[q * kCRec + kC_mL] = aL;
     C[q * kCRec + kC_wL] = shoup_w(aL, mp.p);
     MS[2 * q] = mV;
@@ -744,9 +775,8 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
   }
 }
 
-// Per evaluation pass: LS records of chunk c: LS[c][q][rr] = c_q m_q^{js0 + c*kChunk + rr V}, rr < 8.
-// Thread = (term, kSeedChunks consecutive chunks): one exponentiation, then products with the
-// precomputed m^V (within a chunk) and m^{kChunk} (between chunks).
+// Per evaluation pass: the chunk seeds LS[c][q] = c_q m_q^{js0 + c*kChunk}.  Thread = (term,
+// kSeedChunks consecutive chunks): one exponentiation, then products with m^{kChunk}.
 constexpr u32 kSeedChunks = 4;
 static __global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, const u64* __restrict__ MS,
                                  u64 t_pad, u32 nch, u64 js0, u64* __restrict__ LS, ModParams mp) {
@@ -755,17 +785,11 @@ static __global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restric
   for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
     const u64 grp = x / t_pad, q = x - grp * t_pad;
     const u32 ch0 = (u32)grp * kSeedChunks, ch1 = min(nch, ch0 + kSeedChunks);
-    const u64 mV = MS[2 * q], mC = MS[2 * q + 1];
-    u64 s0 = to_mont(seed_pow(c[q], m[q], js0 + (u64)ch0 * kChunk, mp), mp);
+    const u64 mC = MS[2 * q + 1];                        // Montgomery m^{kChunk}
+    u64 s = seed_pow(c[q], m[q], js0 + (u64)ch0 * kChunk, mp);   // normal form, < p
     for (u32 ch = ch0; ch < ch1; ++ch) {
-      u64* dst = LS + ((u64)ch * t_pad + q) * kLSRec;
-      u64 s = s0;
-#pragma unroll
-      for (int rr = 0; rr < kLSRec; ++rr) {
-        dst[rr] = from_mont(s, mp);
-        s = mont_mul(s, mV, mp);
-      }
-      s0 = mont_mul(s0, mC, mp);
+      LS[(u64)ch * t_pad + q] = s;
+      s = mont_mul(s, mC, mp);                           // normal x Montgomery -> normal
     }
   }
 }
