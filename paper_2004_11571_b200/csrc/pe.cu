@@ -638,6 +638,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     a.t_pad = h->t_pad;
     a.npieces = h->tc_npieces;
     a.nunits = h->tc_npieces * nch;
+    a.nch = nch;
     a.npts = np;
     for (int d = 0; d < 15; ++d) a.Wd[d] = h_powmod(2, 8 * (u64)d, h->p);
     a.C128 = h_powmod(2, 128, h->p);

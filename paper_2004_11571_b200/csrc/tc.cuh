@@ -95,7 +95,7 @@ struct TcArgs {
   const uint4* piece;    // x = first padded term, y = K-blocks, z = partial slot (sorted by size desc)
   u64* partial;          // [n_slots][ldp]
   u64 ldp, t_pad;
-  u32 npieces, nunits, npts;
+  u32 npieces, nunits, npts, nch;
   u64 Wd[15];            // 2^{8d} mod p  (Wd[8] = 2^64, Wd[12] = 2^96, Wd[14] -> see C128)
   u64 C128;              // 2^128 mod p
   u32* scratch;          // per CTA: 2 (ping-pong by unit) x 15 diagonals x kChunk u32 drained diagonal sums
@@ -396,10 +396,12 @@ __device__ __forceinline__ void fold_in(u128_t& lo, u32& x4, u32 Dv) {
 
 __device__ __forceinline__ long long clk() { return clock64(); }
 
-// unit -> (piece, chunk): chunk-major over the size-sorted pieces
+// unit -> (piece, chunk), piece-major over the size-sorted pieces
 __device__ __forceinline__ void unit_of(const TcArgs& a, u32 unit, uint4& pc, u32& chunk) {
-  chunk = unit / a.npieces;
-  pc = a.piece[unit % a.npieces];
+  // piece-major: the chunks of one piece run at the same time on neighbouring CTAs, so the
+  // second reader of a K-block's baby-step planes and C records finds them in L2
+  chunk = unit % a.nch;
+  pc = a.piece[unit / a.nch];
 }
 
 // PROF: per-warp phase timers (clock64) into a.prof -- a development build of the same kernel
