@@ -127,7 +127,7 @@ struct pe_ctx {
   u32* d_tc_slot_start = nullptr;
   u64* d_seed = nullptr;
   size_t seed_elems = 0;
-  u32* d_tc_scratch = nullptr;   // k_tc per-CTA drained diagonal sums (n_sm x 2 x 15 x kChunk u32)
+  u32* d_tc_scratch = nullptr;   // k_tc per-CTA drained diagonal sums (n_sm x 2 x kDiag x kChunk u32)
   size_t partial_cap_bytes = (size_t)1 << 30;
   // kernel timing (pe_set_timing / pe_kernel_stats)
   bool timing = false;
@@ -451,7 +451,10 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
     }
     tc_slot_start[G] = (u32)pieces.size();
     std::stable_sort(pieces.begin(), pieces.end(), [](const uint4& x, const uint4& y) { return x.y > y.y; });
-    h->tc_npieces = h->tc_nslots = (u32)pieces.size();
+    // one partial row per (piece, diagonal round): k_tc reduces each round's part on its own
+    h->tc_npieces = (u32)pieces.size();
+    h->tc_nslots = (u32)pieces.size() * tc::kRounds;
+    for (auto& x : tc_slot_start) x *= tc::kRounds;
     if (dalloc(&h->d_piece, pieces.size()) || dalloc(&h->d_tc_slot_start, G + 1)) return g_last_error;
     CU(cudaMemcpyAsync(h->d_piece, pieces.data(), pieces.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(h->d_tc_slot_start, tc_slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
@@ -618,7 +621,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     CU(cudaMallocAsync((void**)&h->d_seed, (size_t)h->t_pad * nch_max * tc::kLSRec * sizeof(u64), s));
     h->seed_elems = (size_t)h->t_pad * nch_max * tc::kLSRec;
   }
-  if (!h->d_tc_scratch) CU(cudaMallocAsync((void**)&h->d_tc_scratch, (size_t)h->n_sm * 2 * 15 * tc::kChunk * sizeof(u32), s));
+  if (!h->d_tc_scratch) CU(cudaMallocAsync((void**)&h->d_tc_scratch, (size_t)h->n_sm * 2 * tc::kDiag * tc::kChunk * sizeof(u32), s));
   CU(cudaFuncSetAttribute(tc::k_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   CU(cudaFuncSetAttribute(tc::k_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
@@ -637,7 +640,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     a.ldp = (np + 7) / 8 * 8;
     a.t_pad = h->t_pad;
     a.npieces = h->tc_npieces;
-    a.nunits = h->tc_npieces * nch;
+    a.nunits = h->tc_npieces * nch * tc::kRounds;
     a.nch = nch;
     a.npts = np;
     for (int d = 0; d < 15; ++d) a.Wd[d] = h_powmod(2, 8 * (u64)d, h->p);

@@ -98,7 +98,7 @@ struct TcArgs {
   u32 npieces, nunits, npts, nch;
   u64 Wd[15];            // 2^{8d} mod p  (Wd[8] = 2^64, Wd[12] = 2^96, Wd[14] -> see C128)
   u64 C128;              // 2^128 mod p
-  u32* scratch;          // per CTA: 2 (ping-pong by unit) x 15 diagonals x kChunk u32 drained diagonal sums
+  u32* scratch;          // per CTA: 2 (ping-pong by unit) x kDiag accumulators x kChunk u32 drained diagonal sums
   ModParams mp;
   unsigned long long* prof;  // optional phase timers [gridDim][warps][4] (PE_TC_PROF=1), else null
   int dbg;                   // development only (PE_TC_DEBUG, PROF build): 1 = skip the MMAs,
@@ -329,7 +329,7 @@ __device__ __forceinline__ void fold_add(u32 (&X)[5], u32 Dv) {
 }
 
 // Epilogue critical part: drain round G's diagonals of thread row u from TMEM into the unit's raw
-// buffer (raw[d][v/4][u][v%4], u32: the diagonal sums themselves) and release TMEM (acce) as soon as the
+// buffer (raw[slot][v/4][u][v%4], u32: the diagonal sums themselves) and release TMEM (acce) as soon as the
 // last block is in registers -- only tcgen05.ld and fire-and-forget stores, so the MMA warp can
 // start the next round almost at once.  Four accumulators (32 registers) per tcgen05.wait.
 template <int G, int H>
@@ -350,7 +350,7 @@ __device__ __forceinline__ void drain_st(u32 v0, u32* __restrict__ raw_u, const 
   for (int j = 0; j < 4; ++j) {
     if (group_diag(G, 4 * H + j) >= 0) {
       // raw[d][v / 4][u][v % 4]: a warp's 16-byte stores cover 512 contiguous bytes
-      uint4* p4 = (uint4*)(raw_u + (u32)group_diag(G, 4 * H + j) * (kU * kV) + (v0 >> 2) * (kU * 4));
+      uint4* p4 = (uint4*)(raw_u + (u32)(4 * H + j) * (kU * kV) + (v0 >> 2) * (kU * 4));
       p4[0] = make_uint4(D[j][0], D[j][1], D[j][2], D[j][3]);
       p4[kU] = make_uint4(D[j][4], D[j][5], D[j][6], D[j][7]);
     }
@@ -394,47 +394,112 @@ __device__ __forceinline__ void fold_in(u128_t& lo, u32& x4, u32 Dv) {
   x4 += spill + (lo < add ? 1u : 0u);
 }
 
+// X_G += sum over round G's accumulator slots DI.. of D[slot] << 8 d(slot)  (compile-time shifts)
+template <int G, int DI>
+__device__ __forceinline__ void fold_group(u128_t& acc, u32& x4, const u32 (&D)[kDiag][4], int j) {
+  if constexpr (DI < kDiag) {
+    if constexpr (group_diag(G, DI) >= 0) fold_in<8 * group_diag(G, DI)>(acc, x4, D[DI][j]);
+    fold_group<G, DI + 1>(acc, x4, D, j);
+  }
+}
+
+// One TMEM row (giant step ur) of a unit: fold round G's diagonals of each of the kV points into
+// X_G (< 2^145), reduce the 2^64..2^128 words with 2^{32k} mod p into 128 bits, and finish with
+// one REDC into the unit's partial row.
+template <int G>
+__device__ __forceinline__ void fold_row(const u32* __restrict__ rr_, u64* __restrict__ prow, u64 kbase, u32 npts,
+                                         u64 C64, u64 C96, u64 C128, const ModParams& mp) {
+#pragma unroll 1
+  for (u32 v0 = 0; v0 < (u32)kV; v0 += 4) {
+    u32 D[kDiag][4];
+#pragma unroll
+    for (int di = 0; di < kDiag; ++di) {
+      if (group_diag(G, di) >= 0) {
+        const uint4 q = *(const uint4*)(rr_ + (u32)di * (kU * kV) + (v0 >> 2) * (kU * 4));
+        D[di][0] = q.x; D[di][1] = q.y; D[di][2] = q.z; D[di][3] = q.w;
+      }
+    }
+    u64 res[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      u128_t acc = 0;
+      u32 x4 = 0;
+      fold_group<G, 0>(acc, x4, D, j);
+      // X mod p = (x0 + x1 2^32) + x2 (2^64 mod p) + x3 (2^96 mod p) + x4 (2^128 mod p)  (< 2^98)
+      u64 lo = (u64)acc, hi = 0;
+      const u64 x2 = (u64)(acc >> 64) & 0xffffffffull, x3 = (u64)(acc >> 96);
+      const u64 terms[3][2] = {{x2, C64}, {x3, C96}, {(u64)x4, C128}};
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const u64 p0 = terms[q][0] * lo32(terms[q][1]);
+        const u64 p1 = terms[q][0] * hi32(terms[q][1]);
+        const u64 add_lo = p0 + (p1 << 32);
+        const u64 add_hi = (p1 >> 32) + (add_lo < p0 ? 1ull : 0ull);
+        lo += add_lo;
+        hi += add_hi + (lo < add_lo ? 1ull : 0ull);
+      }
+      // the baby-step planes hold Montgomery residues m^v 2^64 (k_tc_rplanes), so the sum is
+      // 2^64 X: one REDC (x 2^-64) is the reduction; REDC needs its high word < p
+      res[j] = redc(hi < mp.p ? hi : hi % mp.p, lo, mp);
+    }
+    if (kbase + v0 + 4 <= npts) {
+      ulonglong2* dst = (ulonglong2*)(prow + kbase + v0);
+      dst[0] = make_ulonglong2(res[0], res[1]);
+      dst[1] = make_ulonglong2(res[2], res[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (kbase + v0 + j < npts) prow[kbase + v0 + j] = res[j];
+    }
+  }
+}
+
 __device__ __forceinline__ long long clk() { return clock64(); }
 
-// unit -> (piece, chunk), piece-major over the size-sorted pieces
-__device__ __forceinline__ void unit_of(const TcArgs& a, u32 unit, uint4& pc, u32& chunk) {
-  // piece-major: the chunks of one piece run at the same time on neighbouring CTAs, so the
-  // second reader of a K-block's baby-step planes and C records finds them in L2
-  chunk = unit % a.nch;
-  pc = a.piece[unit / a.nch];
+// unit -> (piece, chunk, diagonal round g), piece-major over the size-sorted pieces: the
+// kRounds x nch units of one piece run at the same time on neighbouring CTAs, so all but the
+// first reader of a K-block's baby-step planes and C records find them in L2.  X mod p is the
+// sum of the rounds' parts (X = sum_g X_g), so each unit reduces its own part into its own
+// partial row (slot = piece slot * kRounds + g) and k_fixup adds them.
+// The i-th unit of this CTA: units are dealt to the CTAs in snake order (row i of gridDim units
+// left to right for even i, right to left for odd i), so with size-sorted units every CTA gets a
+// large and a small one in turn; ids grow with i, so the first id >= nunits ends the sequence.
+__device__ __forceinline__ u32 unit_id(u32 i) {
+  return i * gridDim.x + ((i & 1) ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
+}
+__device__ __forceinline__ void unit_of(const TcArgs& a, u32 unit, uint4& pc, u32& chunk, u32& g) {
+  g = unit % kRounds;
+  const u32 r = unit / kRounds;
+  chunk = r % a.nch;
+  pc = a.piece[r / a.nch];
 }
 
 // PROF: per-warp phase timers (clock64) into a.prof -- a development build of the same kernel
 // (PE_TC_PROF=1); the production instantiation has no timers.
-// Walks one CTA's K-block sequence: units blockIdx.x, +gridDim.x, ...; per unit kRounds rounds; per round
-// the piece's K-blocks.
+// Walks one CTA's K-block sequence: units unit_id(0), unit_id(1), ...; per unit the piece's K-blocks.
 struct KIter {
-  u32 unit, kb, nkb, q0, chunk;
-  int g;
+  u32 ord, unit, kb, nkb, q0, chunk;
   bool valid;
   __device__ __forceinline__ void load(const TcArgs& a) {
+    unit = unit_id(ord);
     valid = unit < a.nunits;
     if (valid) {
       uint4 pc;
-      unit_of(a, unit, pc, chunk);
+      u32 g;
+      unit_of(a, unit, pc, chunk, g);
       nkb = pc.y;
       q0 = pc.x;
     }
   }
-  __device__ __forceinline__ void init(const TcArgs& a) { unit = blockIdx.x; kb = 0; g = 0; load(a); }
-  __device__ __forceinline__ void next(const TcArgs& a) {
-    if (++kb == nkb) {
-      kb = 0;
-      if (++g == kRounds) { g = 0; unit += gridDim.x; load(a); }
-    }
-  }
+  __device__ __forceinline__ void init(const TcArgs& a) { ord = 0; kb = 0; load(a); }
   // n K-blocks ahead (a producer group's next K-block is kStages ahead): one add and compare
-  // unless a round or unit boundary is crossed
+  // unless a unit boundary is crossed
   __device__ __forceinline__ void advance(const TcArgs& a, u32 n) {
     kb += n;
     while (valid && kb >= nkb) {
       kb -= nkb;
-      if (++g == kRounds) { g = 0; unit += gridDim.x; load(a); }
+      ++ord;
+      load(a);
     }
   }
 };
@@ -568,121 +633,75 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
     const u32 u = (u32)(warp * 32 + lane);
     const u32 tl = tb + ((u32)(warp * 32) << 16);
     const ModParams mp = a.mp;
-    u32* raw_cta = a.scratch + (u64)blockIdx.x * 2 * 15 * (kU * kV);
+    u32* raw_cta = a.scratch + (u64)blockIdx.x * 2 * kDiag * (kU * kV);
     const u64 C64 = a.Wd[8], C96 = a.Wd[12], C128 = a.C128;
     const u32 tbu = uni(tb);
     const uint64_t dA0 = smem_desc(uni(smem_u32(smem)), kLBOA);
     const uint64_t dB0 = smem_desc(uni(smem_u32(smem)) + 8 * kPlaneA, kLBOB);
-    u32 round = 0, it = 0, nunit = 0;
-    for (u32 unit = blockIdx.x; unit < a.nunits; unit += gridDim.x, ++nunit) {
-      uint4 pc; u32 chunk;
-      unit_of(a, unit, pc, chunk);
+    u32 it = 0;
+    for (u32 nunit = 0, unit = unit_id(0); unit < a.nunits; unit = unit_id(++nunit)) {
+      uint4 pc; u32 chunk, g;
+      unit_of(a, unit, pc, chunk, g);
       const u32 nkb = uni(pc.y);
-      u64* prow = a.partial + (u64)pc.z * a.ldp;
-      u32* raw = raw_cta + (u64)(nunit & 1) * 15 * (kU * kV);
-      for (int g = 0; g < kRounds; ++g, ++round) {
-        // round g's MMAs are issued by epilogue warp g (one per SMSP: the issue cost rotates over
-        // the 4 SMSPs instead of slowing the producers that share SMSP 0)
-        if (warp != g) it += nkb;
-        if (warp == g) {
-          long long c0 = clk();
-          mbar_wait<32>(&acce, (round & 1) ^ 1);
-          if (PROF) T[2] += clk() - c0;
-          tc_fence_after();
-          for (u32 kb = 0; kb < nkb; ++kb, ++it) {
-            const u32 stage = it % kStages, use = it / kStages;
-            c0 = clk();
-            mbar_wait<32>(&full[stage], use & 1);
-            if (PROF) T[1] += clk() - c0;
-            tc_fence_after();
-            const uint64_t da = dA0 + (uint64_t)((stage * kStageBytes) >> 4);
-            const uint64_t db = dB0 + (uint64_t)((stage * kStageBytes) >> 4);
-            // converge first so elect.sync picks the same leader (lane 0) every time: a
-            // tcgen05.commit tracks the MMAs its own thread issued
-            __syncwarp();
-            if (elect_one()) {
-              if (PROF && a.dbg == 7) {
-                if (g == 0) issue_round<0, true>(tbu, da, db, kb == 0);
-                else issue_round<1, true>(tbu, da, db, kb == 0);
-              } else if (!(PROF && a.dbg == 1)) {
-                if (g == 0) issue_round<0>(tbu, da, db, kb == 0);
-                else issue_round<1>(tbu, da, db, kb == 0);
-              }
-              if (kb + 1 == nkb) mma_commit(&accf);   // accumulators complete after this K-block
-              mma_commit(&empty[stage]);
-            }
-            __syncwarp();
-          }
-          // (this raw buffer was last read two units ago by warp 1's fold of warp 0's rows; that
-          // fold precedes warp 1's drain of the previous unit's last round, which this warp has
-          // already waited for through acce -- no extra barrier needed)
-        }
+      g = uni(g);
+      u64* prow = a.partial + ((u64)pc.z * kRounds + g) * a.ldp;
+      u32* raw = raw_cta + (u64)(nunit & 1) * kDiag * (kU * kV);
+      if (warp == kMmaWarp) {
+        // (this raw buffer was last read two units ago by warp 1's fold of warp 0's rows; that
+        // fold precedes warp 1's drain of the previous unit, which this warp has waited for
+        // through acce -- no extra barrier needed)
         long long c0 = clk();
-        mbar_wait<64>(&accf, round & 1);
-        long long c1 = clk();
-        if (PROF) T[0] += c1 - c0;
+        mbar_wait<32>(&acce, (nunit & 1) ^ 1);
+        if (PROF) T[2] += clk() - c0;
         tc_fence_after();
-        u32* raw_u = raw + (u64)u * 4;
-        const bool st = !(PROF && a.dbg == 3);
-        if (g == 0) epi_drain<0>(tl, raw_u, &acce, st);
-        else epi_drain<1>(tl, raw_u, &acce, st);
-        if (PROF && warp != g) T[1] += clk() - c1;
-        if (PROF) T[3] += 1;
+        for (u32 kb = 0; kb < nkb; ++kb, ++it) {
+          const u32 stage = it % kStages, use = it / kStages;
+          c0 = clk();
+          mbar_wait<32>(&full[stage], use & 1);
+          if (PROF) T[1] += clk() - c0;
+          tc_fence_after();
+          const uint64_t da = dA0 + (uint64_t)((stage * kStageBytes) >> 4);
+          const uint64_t db = dB0 + (uint64_t)((stage * kStageBytes) >> 4);
+          // converge first so elect.sync picks the same leader (lane 0) every time: a
+          // tcgen05.commit tracks the MMAs its own thread issued
+          __syncwarp();
+          if (elect_one()) {
+            if (PROF && a.dbg == 7) {
+              if (g == 0) issue_round<0, true>(tbu, da, db, kb == 0);
+              else issue_round<1, true>(tbu, da, db, kb == 0);
+            } else if (!(PROF && a.dbg == 1)) {
+              if (g == 0) issue_round<0>(tbu, da, db, kb == 0);
+              else issue_round<1>(tbu, da, db, kb == 0);
+            }
+            if (kb + 1 == nkb) mma_commit(&accf);   // accumulators complete after this K-block
+            mma_commit(&empty[stage]);
+          }
+          __syncwarp();
+        }
       }
-      // X mod p = (x0 + x1 2^32) + x2 (2^64 mod p) + x3 (2^96 mod p) + x4 (2^128 mod p)  (< 2^96)
+      long long c0 = clk();
+      mbar_wait<64>(&accf, nunit & 1);
+      long long c1 = clk();
+      if (PROF) T[0] += c1 - c0;
+      tc_fence_after();
+      u32* raw_u = raw + (u64)u * 4;
+      const bool st = !(PROF && a.dbg == 3);
+      if (g == 0) epi_drain<0>(tl, raw_u, &acce, st);
+      else epi_drain<1>(tl, raw_u, &acce, st);
+      if (PROF && warp != kMmaWarp) T[1] += clk() - c1;
+      if (PROF) T[3] += 1;
+      // warps 1-3 fold the unit while warp 0 issues the next one's MMAs
       long long c2 = clk();
       for (int pass = 0; pass < (warp == 1 ? 2 : (warp == kMmaWarp ? 0 : 1)); ++pass) {
         u32 ur = u;
-        if (pass == 1) {                 // warp 1: warp 0's rows, once all 4 warps drained the last round
-          mbar_wait<32>(&acce, (round - 1) & 1);
+        if (pass == 1) {                 // warp 1: warp 0's rows, once all 4 warps drained the unit
+          mbar_wait<32>(&acce, nunit & 1);
           ur = (u32)lane;
         }
         const u32* rr_ = raw + (u64)ur * 4;
         const u64 kbase = (u64)chunk * kChunk + (u64)ur * kV;   // multiple of 8; ldp multiple of 8
-#pragma unroll 1
-        for (u32 v0 = 0; v0 < (u32)kV; v0 += 4) {
-          u32 D[15][4];
-#pragma unroll
-          for (int d = 0; d < 15; ++d) {
-            const uint4 q = *(const uint4*)(rr_ + (u32)d * (kU * kV) + (v0 >> 2) * (kU * 4));
-            D[d][0] = q.x; D[d][1] = q.y; D[d][2] = q.z; D[d][3] = q.w;
-          }
-          u64 res[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            u128_t acc = 0;
-            u32 x4 = 0;
-            fold_in<0>(acc, x4, D[0][j]);   fold_in<8>(acc, x4, D[1][j]);   fold_in<16>(acc, x4, D[2][j]);
-            fold_in<24>(acc, x4, D[3][j]);  fold_in<32>(acc, x4, D[4][j]);  fold_in<40>(acc, x4, D[5][j]);
-            fold_in<48>(acc, x4, D[6][j]);  fold_in<56>(acc, x4, D[7][j]);  fold_in<64>(acc, x4, D[8][j]);
-            fold_in<72>(acc, x4, D[9][j]);  fold_in<80>(acc, x4, D[10][j]); fold_in<88>(acc, x4, D[11][j]);
-            fold_in<96>(acc, x4, D[12][j]); fold_in<104>(acc, x4, D[13][j]); fold_in<112>(acc, x4, D[14][j]);
-            u64 lo = (u64)acc, hi = 0;
-            const u64 x2 = (u64)(acc >> 64) & 0xffffffffull, x3 = (u64)(acc >> 96);
-            const u64 terms[3][2] = {{x2, C64}, {x3, C96}, {(u64)x4, C128}};
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-              const u64 p0 = terms[q][0] * lo32(terms[q][1]);
-              const u64 p1 = terms[q][0] * hi32(terms[q][1]);
-              const u64 add_lo = p0 + (p1 << 32);
-              const u64 add_hi = (p1 >> 32) + (add_lo < p0 ? 1ull : 0ull);
-              lo += add_lo;
-              hi += add_hi + (lo < add_lo ? 1ull : 0ull);
-            }
-            // the baby-step planes hold Montgomery residues m^v 2^64 (k_tc_rplanes), so the sum is
-            // 2^64 X: one REDC (x 2^-64) is the reduction; REDC needs its high word < p
-            res[j] = redc(hi < mp.p ? hi : hi % mp.p, lo, mp);
-          }
-          if (kbase + v0 + 4 <= a.npts) {
-            ulonglong2* dst = (ulonglong2*)(prow + kbase + v0);
-            dst[0] = make_ulonglong2(res[0], res[1]);
-            dst[1] = make_ulonglong2(res[2], res[3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (kbase + v0 + j < a.npts) prow[kbase + v0 + j] = res[j];
-          }
-        }
+        if (g == 0) fold_row<0>(rr_, prow, kbase, a.npts, C64, C96, C128, mp);
+        else fold_row<1>(rr_, prow, kbase, a.npts, C64, C96, C128, mp);
       }
       if (PROF) T[2] += clk() - c2;
     }
