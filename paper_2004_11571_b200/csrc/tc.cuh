@@ -408,9 +408,9 @@ __device__ __forceinline__ void fold_group(u128_t& acc, u32& x4, const u32 (&D)[
 // one REDC into the unit's partial row.
 template <int G>
 __device__ __forceinline__ void fold_row(const u32* __restrict__ rr_, u64* __restrict__ prow, u64 kbase, u32 npts,
-                                         u64 C64, u64 C96, u64 C128, const ModParams& mp) {
+                                         u64 C64, u64 C96, u64 C128, const ModParams& mp, u32 vbeg, u32 vend) {
 #pragma unroll 1
-  for (u32 v0 = 0; v0 < (u32)kV; v0 += 4) {
+  for (u32 v0 = vbeg; v0 < vend; v0 += 4) {
     u32 D[kDiag][4];
 #pragma unroll
     for (int di = 0; di < kDiag; ++di) {
@@ -553,7 +553,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
     // on its full barrier) and the group's NEXT K-block's per-term records (two data slots).
     const int pw = warp - kProdWarp0;
     const int my_stage = pw / kProdPerStage, sub = pw % kProdPerStage;
-    const bool leader = sub == 0 && lane == 0;
+    const bool leader = sub == 0 && lane == 0;            // issues the baby-step plane copies
+    const bool loader = sub == 1 && lane == 0;            // issues the per-term record prefetches
     const u32 tq = (u32)(lane >> 3), rr = (u32)(lane & 7);
     const u32 term0 = (u32)sub * 16 + tq * 4;     // first of the lane's 4 terms
     const u32 stage0 = smem_u32(smem) + (u32)my_stage * kStageBytes;
@@ -570,7 +571,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
     cur.advance(a, (u32)my_stage);                                   // the group's first K-block
     ahead = cur;
     ahead.advance(a, kStages);                                       // ... and its second
-    if (leader && cur.valid) load_kblock(a, cur, data0 + slot0 * kDataSlot, &dfull[slot0]);
+    if (loader && cur.valid) load_kblock(a, cur, data0 + slot0 * kDataSlot, &dfull[slot0]);
     u32 guse = 0;
     // the lane's chain seeds and multipliers of the group's K-block number g (data slot g & 1)
     u64 x[4], sm[4], sw[4];
@@ -603,9 +604,9 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
           mbar_expect_tx(&full[stage], kRBytes);
           bulk_g2s(stage0 + 8 * kPlaneA, a.Rp + ((u64)cur.q0 / kKB + cur.kb) * kRBytes, kRBytes, &full[stage]);
         }
-        if (ahead.valid)
-          load_kblock(a, ahead, data0 + (slot0 + ((guse + 1) & 1)) * kDataSlot, &dfull[slot0 + ((guse + 1) & 1)]);
       }
+      if (loader && ahead.valid)
+        load_kblock(a, ahead, data0 + (slot0 + ((guse + 1) & 1)) * kDataSlot, &dfull[slot0 + ((guse + 1) & 1)]);
 #pragma unroll 2
       for (int k = 0; k < ((PROF && (a.dbg == 2 || a.dbg >= 6)) ? 0 : 16); ++k) {
         // row rr + 8k: the next 8-row core-matrix group, +128 bytes
@@ -628,7 +629,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
     // (converged warp, elect.sync leader) and then drains its lane quarter.  Per round every
     // epilogue warp only moves its rows of the round's diagonals from TMEM to the unit's raw buffer (ping-pong by
     // unit) and releases TMEM.  After the unit's last round warps 1-3 fold all 15 diagonals
-    // exactly (X = sum D_d 2^{8d}) and reduce mod p into the piece's partial row -- warp 1 also
+    // exactly (X = sum D_d 2^{8d}) and reduce mod p into the piece's partial row -- warps 2 and 3 also
     // for warp 0's rows -- while warp 0 is already issuing the next unit's MMAs.
     const u32 u = (u32)(warp * 32 + lane);
     const u32 tl = tb + ((u32)(warp * 32) << 16);
@@ -647,8 +648,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       u64* prow = a.partial + ((u64)pc.z * kRounds + g) * a.ldp;
       u32* raw = raw_cta + (u64)(nunit & 1) * kDiag * (kU * kV);
       if (warp == kMmaWarp) {
-        // (this raw buffer was last read two units ago by warp 1's fold of warp 0's rows; that
-        // fold precedes warp 1's drain of the previous unit, which this warp has waited for
+        // (this raw buffer was last read two units ago by warps 2 / 3's fold of warp 0's rows;
+        // that fold precedes their drain of the previous unit, which this warp has waited for
         // through acce -- no extra barrier needed)
         long long c0 = clk();
         mbar_wait<32>(&acce, (nunit & 1) ^ 1);
@@ -658,7 +659,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
           const u32 stage = it % kStages, use = it / kStages;
           c0 = clk();
           mbar_wait<32>(&full[stage], use & 1);
-          if (PROF) T[1] += clk() - c0;
+          if (PROF) T[kb < (u32)kStages ? 0 : 1] += clk() - c0;   // unit start vs steady state
           tc_fence_after();
           const uint64_t da = dA0 + (uint64_t)((stage * kStageBytes) >> 4);
           const uint64_t db = dB0 + (uint64_t)((stage * kStageBytes) >> 4);
@@ -690,18 +691,22 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       else epi_drain<1>(tl, raw_u, &acce, st);
       if (PROF && warp != kMmaWarp) T[1] += clk() - c1;
       if (PROF) T[3] += 1;
-      // warps 1-3 fold the unit while warp 0 issues the next one's MMAs
+      // warps 1-3 fold the unit while warp 0 issues the next one's MMAs; warp 0's rows are
+      // split by v between warps 2 and 3 (1.5 row-sets each on SMSPs 2 / 3, 1 on SMSP 1: the fold
+      // shares those SMSPs with producer warps)
       long long c2 = clk();
-      for (int pass = 0; pass < (warp == 1 ? 2 : (warp == kMmaWarp ? 0 : 1)); ++pass) {
-        u32 ur = u;
-        if (pass == 1) {                 // warp 1: warp 0's rows, once all 4 warps drained the unit
+      for (int pass = 0; pass < (warp == kMmaWarp ? 0 : (warp == 1 ? 1 : 2)); ++pass) {
+        u32 ur = u, vbeg = 0, vend = (u32)kV;
+        if (pass == 1) {                 // warp 0's rows, once all 4 warps drained the unit
           mbar_wait<32>(&acce, nunit & 1);
           ur = (u32)lane;
+          vbeg = warp == 2 ? 0u : (u32)kV / 2;
+          vend = vbeg + (u32)kV / 2;
         }
         const u32* rr_ = raw + (u64)ur * 4;
         const u64 kbase = (u64)chunk * kChunk + (u64)ur * kV;   // multiple of 8; ldp multiple of 8
-        if (g == 0) fold_row<0>(rr_, prow, kbase, a.npts, C64, C96, C128, mp);
-        else fold_row<1>(rr_, prow, kbase, a.npts, C64, C96, C128, mp);
+        if (g == 0) fold_row<0>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
+        else fold_row<1>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
       }
       if (PROF) T[2] += clk() - c2;
     }
