@@ -420,7 +420,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   if (h->tc_mode != 0 && (h->path == kInt4 || h->path == kFp64 || h->path == kInt32)) {
     const u64 tp = h->t_pad;
     if (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp) || dalloc(&h->d_tcMS, (size_t)2 * tp) ||
-        dalloc(&h->d_tcR, (size_t)((tp + 2 * tc::kKB - 1) / (2 * tc::kKB)) * 4 * tc::kRBytes))
+        dalloc(&h->d_tcR, (size_t)((tp + 2 * tc::kKB - 1) / (2 * tc::kKB)) * 2 * tc::kRBytes))
       return g_last_error;
     tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
     CU(cudaGetLastError());
@@ -607,15 +607,13 @@ static int ensure_partial(pe_ctx* h, size_t need, cudaStream_t s) {
 // -> k_fixup over the pieces' partial rows.
 static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s) {
   const u64 nslots = h->tc_nslots;
-  // a CTA pair evaluates 2 x kChunk points per unit: passes are whole pair chunks
-  const u64 kPair = 2 * (u64)tc::kChunk;
-  u64 Tp = h->partial_cap_bytes / 8 / std::max<u64>(nslots, 1) / kPair * kPair;
-  Tp = std::max<u64>(Tp, kPair);
-  Tp = std::min<u64>(Tp, (T + kPair - 1) / kPair * kPair);
-  Tp = std::min<u64>(Tp, kPair * 2048);
+  u64 Tp = h->partial_cap_bytes / 8 / std::max<u64>(nslots, 1) / tc::kChunk * tc::kChunk;
+  Tp = std::max<u64>(Tp, tc::kChunk);
+  Tp = std::min<u64>(Tp, (T + tc::kChunk - 1) / tc::kChunk * tc::kChunk);
+  Tp = std::min<u64>(Tp, (u64)tc::kChunk * 4096);
   // partial rows padded to a multiple of 8 points (the epilogue's 64-byte vector accesses)
   if (ensure_partial(h, (size_t)nslots * ((std::min<u64>(Tp, T) + 7) / 8 * 8), s)) return g_last_error;
-  const u32 nch_max = (u32)(Tp / tc::kChunk);   // 8192-point chunks (seeds), even
+  const u32 nch_max = (u32)(Tp / tc::kChunk);
   if ((size_t)h->t_pad * nch_max * tc::kLSRec > h->seed_elems) {
     if (h->d_seed) cudaFreeAsync(h->d_seed, s);
     h->d_seed = nullptr;
@@ -628,10 +626,10 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
   CU(cudaFuncSetAttribute(tc::k_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
-    const u32 nch = (u32)((np + kPair - 1) / kPair);   // pair chunks
-    const u64 nseed = (u64)h->t_pad * ((2 * nch + tc::kSeedChunks - 1) / tc::kSeedChunks);
-    tc::k_tc_seed<<<grid_for(nseed, 256), 256, 0, s>>>(h->d_c, h->d_m, h->d_tcMS, h->t_pad, 2 * nch, j0 + k0,
-                                                       h->d_seed, h->mp);
+    const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
+    const u64 nseed = (u64)h->t_pad * ((nch + tc::kSeedChunks - 1) / tc::kSeedChunks);
+    tc::k_tc_seed<<<grid_for(nseed, 256), 256, 0, s>>>(h->d_c, h->d_m, h->d_tcMS, h->t_pad, nch, j0 + k0, h->d_seed,
+                                                       h->mp);
     CU(cudaGetLastError());
     tc::TcArgs a;
     a.LS = h->d_seed;
@@ -651,8 +649,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     a.mp = h->mp;
     a.prof = nullptr;
     a.dbg = env_int("PE_TC_DEBUG", 0);
-    // CTA pairs (clusters of 2, cta_group::2 MMAs): an even grid, one pair per unit at most
-    const unsigned grid = (unsigned)std::min<u64>(2 * (u64)a.nunits, (u64)(h->n_sm & ~1));
+    const unsigned grid = (unsigned)std::min<u64>(a.nunits, (u64)h->n_sm);
     pe_ctx::Rec rec{};
     if (h->timing) {
       CU(cudaEventCreate(&rec.e0));
@@ -678,14 +675,13 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
       CU(cudaStreamSynchronize(s));
       cudaFree(d_prof);
       const int nw = tc::kThreads / 32;
-      for (int rk = 0; rk < 2; ++rk)   // leader (rank 0) and peer (rank 1) CTAs of the pairs
-        for (int wv = 0; wv < nw; ++wv) {
-          double acc[5] = {0, 0, 0, 0, 0};
-          for (unsigned b = (unsigned)rk; b < grid; b += 2)
-            for (int i = 0; i < 5; ++i) acc[i] += (double)hp[((size_t)b * nw + wv) * 5 + i] / (grid / 2);
-          fprintf(stderr, "tcprof rank %d warp %2d: t0 %.0f t1 %.0f t2 %.0f n %.0f total %.0f\n", rk, wv, acc[0],
-                  acc[1], acc[2], acc[3], acc[4]);
-        }
+      for (int wv = 0; wv < nw; ++wv) {
+        double acc[5] = {0, 0, 0, 0, 0};
+        for (unsigned b = 0; b < grid; ++b)
+          for (int i = 0; i < 5; ++i) acc[i] += (double)hp[((size_t)b * nw + wv) * 5 + i] / grid;
+        fprintf(stderr, "tcprof warp %2d: t0 %.0f t1 %.0f t2 %.0f n %.0f total %.0f\n", wv, acc[0], acc[1], acc[2],
+                acc[3], acc[4]);
+      }
       const unsigned long long* gt = hp.data() + (size_t)grid * nw * 5;
       unsigned long long e0 = ~0ull, e1 = 0, a0 = ~0ull, a1 = 0, x0 = ~0ull, x1 = 0;
       for (unsigned b = 0; b < grid; ++b) {

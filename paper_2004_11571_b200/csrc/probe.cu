@@ -301,7 +301,7 @@ __global__ void k_bench_mma(int iters, u32 idesc, u32 ncols, int nacc) {
           "setp.ne.b32 p, %4, 0;\n\t"
           "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
           :: "r"(tb + acc_col), "l"(ad), "l"(bd), "r"(idesc), "r"(1u));
-    tc::mma_commit1(&bar);
+    tc::mma_commit(&bar);
   }
   tc::mbar_wait(&bar, 0);
   tc::tc_fence_before();

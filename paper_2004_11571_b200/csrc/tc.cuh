@@ -33,7 +33,7 @@
 //              buffer (per-CTA, L2-resident), release TMEM; after the unit's last round an exact
 //              160-bit fold of the 15 diagonals and one reduction mod p per point ->
 //              partial[slot][chunk*kChunk + u*kV + v].  Warps 0 / 1 also issue rounds 0 / 1's MMAs
-//              (tcgen05.mma.cta_group::2.kind::i8, elect.sync leader); warp 0 allocates TMEM.
+//              (tcgen05.mma.cta_group::1.kind::i8, elect.sync leader); warp 0 allocates TMEM.
 //   warps 4-11 producers, 2 per smem stage: each generates 16 terms x 128 giant-step rows of one
 //              K-block with Shoup products (4 chains per lane, seeded from per-chunk chain seeds)
 //              and writes their 8 byte planes in the no-swizzle K-major UMMA layout.  The baby-step
@@ -50,17 +50,16 @@ constexpr int kU = 128;                   // giant steps per chunk  (MMA M / TME
 constexpr int kV = 64;                    // baby steps per chunk   (MMA N)
 constexpr u32 kChunk = kU * kV;           // points per chunk
 constexpr int kKB = 32;                   // terms per K-block (one i8 MMA K step)
-constexpr int kStages = 5;
+constexpr int kStages = 4;
 constexpr u32 kPieceMax = 8192;           // terms per accumulation: 8192 * 8 * 255^2 < 2^32 (the s32
                                           // accumulator wraps mod 2^32, saturate = 0; read as u32)
 // Digit planes in the no-swizzle K-major UMMA layout: 8-row x 16-byte core matrices, rows of a
 // core-matrix column 128 B apart (SBO), the two 16-byte K halves LBO apart.
 constexpr u32 kLBOA = 2048;               // L planes (A, 128 rows): writes are conflict-free unpadded
 constexpr u32 kPlaneA = kLBOA + 2048;
-constexpr u32 kVh = kV / 2;               // B rows held by each CTA of the pair (cta_group::2 splits N)
-constexpr u32 kLBOB = kVh * 16;           // R half-planes (B, 32 rows), written by TMA only
-constexpr u32 kPlaneB = 2 * kLBOB;
-constexpr u32 kStageBytes = 8 * kPlaneA + 8 * kPlaneB;   // 8 L planes + 8 R half-planes (40960 B)
+constexpr u32 kLBOB = 1024 + 64;          // R planes (B, 64 rows): +64 B spreads the K halves over banks
+constexpr u32 kPlaneB = kLBOB + 1024;
+constexpr u32 kStageBytes = 8 * kPlaneA + 8 * kPlaneB;   // 8 L planes + 8 R planes (49664 B)
 // Per-term records (array of structs, so one K-block's data is two contiguous bulk copies):
 //   LS record (per chunk, 1 u64): the chunk seed c m^{j_s}
 //   C  record (10 u64): the giant-step chain multiplier m^{8V} and its Shoup constant, and the
@@ -70,19 +69,16 @@ constexpr u32 kStageBytes = 8 * kPlaneA + 8 * kPlaneB;   // 8 L planes + 8 R hal
 // and each K-block's 16.5 KB is one TMA bulk copy into the stage.
 constexpr int kLSRec = 1, kCRec = 10;
 enum { kC_mL = 0, kC_wL = 1, kC_g0 = 2 };
-constexpr u32 kRBytes = 8 * kPlaneB;                  // one K-block's R half-planes of one CTA (8192 B)
+constexpr u32 kRBytes = 8 * kPlaneB;                  // one K-block's R planes (16896 B)
 constexpr u32 kDataLS = kKB * kLSRec * 8;             // 256 B
 constexpr u32 kDataSlot = kDataLS + kKB * kCRec * 8;  // 2816 B
-constexpr int kDataSlots = kStages;                   // 1 per producer group (read into registers one
-                                                      // K-block ahead, then refilled)
+constexpr int kDataSlots = 2 * kStages;               // 2 per producer group: current + next K-block
 constexpr u32 kSmemBytes = kStages * kStageBytes + kDataSlots * kDataSlot + 128;
 constexpr int kRounds = 2;
 constexpr int kDiag = 8;                  // diagonal accumulators per round: 8 x 64 TMEM columns
 constexpr int kProdPerStage = 2;          // L terms 0-15, L terms 16-31 (128 rows each)
 constexpr int kEpiWarps = 4, kMmaWarp = 0, kProdWarp0 = 4;   // warp 0: epilogue + MMA issue
-constexpr int kRelayWarp = kProdWarp0 + kStages * kProdPerStage;       // peer CTA: forwards the
-                                                                        // baby-step copies' completion
-constexpr int kThreads = (kRelayWarp + 1) * 32;                         // 15 warps
+constexpr int kThreads = (kProdWarp0 + kStages * kProdPerStage) * 32;   // 12 warps: 3 per SMSP
 static_assert(kRounds <= kEpiWarps, "round g's MMAs are issued by epilogue warp g");
 static_assert(kDiag * kV == 512, "a round's accumulators fill TMEM");
 static_assert(kSmemBytes + 256 <= 232448, "shared memory");
@@ -99,7 +95,7 @@ struct TcArgs {
   const uint4* piece;    // x = first padded term, y = K-blocks, z = partial slot (sorted by size desc)
   u64* partial;          // [n_slots][ldp]
   u64 ldp, t_pad;
-  u32 npieces, nunits, npts, nch;   // nch: 16384-point chunks (one per CTA pair and unit)
+  u32 npieces, nunits, npts, nch;
   u64 Wd[15];            // 2^{8d} mod p  (Wd[8] = 2^64, Wd[12] = 2^96, Wd[14] -> see C128)
   u64 C128;              // 2^128 mod p
   u32* scratch;          // per CTA: 2 (ping-pong by unit) x kDiag accumulators x kChunk u32 drained diagonal sums
@@ -120,14 +116,14 @@ __device__ __forceinline__ uint64_t smem_desc(u32 saddr, u32 lbo) {
   d |= (uint64_t)1 << 46;                        // sm_100 descriptor version; no swizzle
   return d;
 }
-// kind::i8, D s32, A u8, B u8, both K-major, M = 2 kU = 256 (the CTA pair), N = kV = 64
-constexpr u32 kIdesc = (2u << 4) | (0u << 7) | (0u << 10) | ((u32)(kV >> 3) << 17) | ((u32)(2 * kU >> 4) << 24);
+// kind::i8, D s32, A u8, B u8, both K-major, M = kU = 128, N = kV = 64
+constexpr u32 kIdesc = (2u << 4) | (0u << 7) | (0u << 10) | ((u32)(kV >> 3) << 17) | ((u32)(kU >> 4) << 24);
 
 __device__ __forceinline__ void mma_u8(u32 dtmem, uint64_t ad, uint64_t bd, u32 acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
       :: "r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
 }
 __device__ __forceinline__ bool elect_one() {
@@ -145,19 +141,19 @@ template <int COL>
 __device__ __forceinline__ void mma_u8c(u32 dtmem, uint64_t ad, uint64_t bd, u32 acc) {
   if (COL == 0)
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
+                 "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
                  :: "r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
   else if (COL == 1)
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::2.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n\t}\n"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n\t}\n"
                  :: "r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
   else if (COL == 2)
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::2.kind::i8.collector::a::use [%0], %1, %2, %3, p;\n\t}\n"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::use [%0], %1, %2, %3, p;\n\t}\n"
                  :: "r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
   else
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::2.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}\n"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}\n"
                  :: "r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
 }
 
@@ -206,32 +202,9 @@ __device__ __forceinline__ void issue_round(u32 tb, uint64_t da, uint64_t db, bo
   }
 }
 
-// single-CTA commit (pe_bench_mma's cta_group::1 probe)
-__device__ __forceinline__ void mma_commit1(uint64_t* bar) {
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                :: "r"(smem_u32(bar)) : "memory");
-}
-// completion of the leader's MMAs, signalled on the barrier at the same offset in both CTAs
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-               :: "r"(smem_u32(bar)), "h"((unsigned short)3) : "memory");
-}
-__device__ __forceinline__ u32 cluster_rank() {
-  u32 r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// the shared::cluster address of a local shared variable's copy in CTA `rank`
-__device__ __forceinline__ u32 peer_addr(const void* p, u32 rank) {
-  u32 r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive_remote(u32 cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, u32 cnt) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(cnt));
@@ -243,7 +216,7 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, u32 parity) {
   u32 ok;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, P1;\n\t}\n"
       : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   return ok != 0;
@@ -386,7 +359,7 @@ __device__ __forceinline__ void drain_st(u32 v0, u32* __restrict__ raw_u, const 
 // Software-pipelined: the tcgen05.ld of the next 4 accumulators x 8 columns is in flight while
 // the previous block is stored; TMEM is released (acce) right after the last load completes.
 template <int G>
-__device__ __forceinline__ void epi_drain(u32 tl, u32* __restrict__ raw_u, uint64_t* acce, u32 acce_remote, bool st = true) {
+__device__ __forceinline__ void epi_drain(u32 tl, u32* __restrict__ raw_u, uint64_t* acce, bool st = true) {
   u32 A[4][8], B[4][8];
   drain_ld<G, 0>(tl, 0, A);
   tmem_wait_ld();
@@ -399,10 +372,9 @@ __device__ __forceinline__ void epi_drain(u32 tl, u32* __restrict__ raw_u, uint6
     drain_fence<G, 1>(B);
     if (v0 + 8 < (u32)kV) {
       drain_ld<G, 0>(tl, v0 + 8, A);
-    } else {   // TMEM drained: the MMA may start the next unit
+    } else {   // TMEM drained: the MMA may start the next round
       tc_fence_before();
       mbar_arrive(acce);
-      if (acce_remote) mbar_arrive_remote(acce_remote);   // peer CTA: tell the leader too
     }
     if (st) drain_st<G, 1>(v0, raw_u, B);
     if (v0 + 8 < (u32)kV) {
@@ -493,15 +465,12 @@ __device__ __forceinline__ long long clk() { return clock64(); }
 // left to right for even i, right to left for odd i), so with size-sorted units every CTA gets a
 // large and a small one in turn; ids grow with i, so the first id >= nunits ends the sequence.
 __device__ __forceinline__ u32 unit_id(u32 i) {
-  const u32 ncl = gridDim.x >> 1, cid = blockIdx.x >> 1;   // clusters (CTA pairs) deal the units
-  return i * ncl + ((i & 1) ? ncl - 1 - cid : cid);
+  return i * gridDim.x + ((i & 1) ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
 }
-// chunk = this CTA's 8192-point chunk: the pair's 16384-point chunk c covers chunks 2c (rank 0,
-// giant steps u < 128) and 2c + 1 (rank 1, u = 128..255).
 __device__ __forceinline__ void unit_of(const TcArgs& a, u32 unit, uint4& pc, u32& chunk, u32& g) {
   g = unit % kRounds;
   const u32 r = unit / kRounds;
-  chunk = 2 * (r % a.nch) + (blockIdx.x & 1);
+  chunk = r % a.nch;
   pc = a.piece[r / a.nch];
 }
 
@@ -544,41 +513,29 @@ __device__ __forceinline__ void load_kblock(const TcArgs& a, const KIter& k, u32
 }
 
 template <bool PROF>
-static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 15 warps: <= 136 regs/thread
+static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 warps: <= 168 regs/thread
   unsigned long long g_entry = 0;
   if (PROF) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
   extern __shared__ uint8_t dsm[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)dsm + 127) & ~(uintptr_t)127);   // kSmemBytes holds 128 B of slack
-  // CTA pair (cluster of 2): rank 0 (the leader) issues the pair's MMAs; its full barrier counts
-  // both CTAs' producers (the peer's arrive remotely once their baby-step half-planes have landed,
-  // rfull) and its own expect_tx arrival; acce2 counts the peer's TMEM drains.
-  __shared__ __align__(8) uint64_t full[kStages], rfull[kStages], empty[kStages], accf, acce, acce2,
-      dfull[kDataSlots];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accf, acce, dfull[kDataSlots];
   __shared__ u32 tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const u32 rank = cluster_rank();
-  const bool lead = rank == 0;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      // leader: its producers' threads + its copy's expect_tx arrival + the peer's relay; peer:
-      // rfull = its producers' threads + its copy's expect_tx arrival (forwarded by the relay)
-      mbar_init(&full[s], 32 * kProdPerStage + 1 + 1);
-      mbar_init(&rfull[s], 32 * kProdPerStage + 1);
-      mbar_init(&empty[s], 1);
-    }
+    // full: the group's threads + the leader's expect_tx arrival for the R planes
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 32 * kProdPerStage + 1); mbar_init(&empty[s], 1); }
     mbar_init(&accf, 1);
     mbar_init(&acce, 32 * kEpiWarps);
-    mbar_init(&acce2, 32 * kEpiWarps);
     for (int s = 0; s < kDataSlots; ++s) mbar_init(&dfull[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(smem_u32(&tmem_base)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
-  cluster_sync_all();
+  __syncthreads();
   tc_fence_after();
   const u32 tb = tmem_base;
   unsigned long long g_alloc = 0;
@@ -587,21 +544,7 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) 
   const long long t_start = clk();
   const u32 data0 = smem_u32(smem) + kStages * kStageBytes;
 
-  if (warp == kRelayWarp) {
-    // ------------------------------------------------------------ relay (peer CTA only)
-    // The peer's stages complete on its own barrier (rfull: producers + the baby-step copy);
-    // forward each completion to the leader's full barrier in K-block order.
-    if (!lead && lane == 0) {
-      const u32 full_leader = peer_addr(&full[0], 0);
-      KIter cur;
-      cur.init(a);
-      for (u32 it = 0; cur.valid; ++it, cur.advance(a, 1)) {
-        mbar_wait<64>(&rfull[it % kStages], (it / kStages) & 1);
-        mbar_arrive_remote(full_leader + (it % kStages) * 8);
-      }
-    }
-    __syncwarp();
-  } else if (warp >= kProdWarp0) {
+  if (warp >= kProdWarp0) {
     // ------------------------------------------------------------ producers
     // 2 warps per stage generate the 128 giant-step rows of 16 terms each: lane = (tq < 4,
     // rr < 8), terms sub*16 + tq*4 .. +3, rows rr + 8k (k < 16) -- 4 Shoup chains of stride 8 per
@@ -620,7 +563,7 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) 
     const u32 mul_off = kDataLS + (term0 * kCRec + kC_mL) * 8;
     const u32 g_off = kDataLS + (term0 * kCRec + kC_g0 + rr) * 8;
     const ModParams mp = a.mp;
-    const u32 slot0 = (u32)my_stage;
+    const u32 slot0 = (u32)my_stage * 2;
     const u64 np = a.mp.np;
     // the group owns K-blocks my_stage, my_stage + kStages, ... of the CTA's sequence
     KIter cur, ahead;
@@ -628,15 +571,14 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) 
     cur.advance(a, (u32)my_stage);                                   // the group's first K-block
     ahead = cur;
     ahead.advance(a, kStages);                                       // ... and its second
+    if (loader && cur.valid) load_kblock(a, cur, data0 + slot0 * kDataSlot, &dfull[slot0]);
     u32 guse = 0;
-    // The group's single data slot holds its next K-block's per-term records: both warps read
-    // them into registers (fetch, one K-block ahead, while they wait for their stage), sync on
-    // the group's named barrier, and the loader lane refills the slot with the K-block after.
+    // the lane's chain seeds and multipliers of the group's K-block number g (data slot g & 1)
     u64 x[4], sm[4], sw[4];
-    const u32 dslot = data0 + slot0 * kDataSlot;
-    auto fetch = [&](u32 g) {   // g = the group's K-block number = the slot's fill number
+    auto fetch = [&](u32 g) {
+      const u32 dslot = data0 + (slot0 + (g & 1)) * kDataSlot;
       const long long f0 = clk();
-      mbar_wait<64>(&dfull[slot0], g & 1);
+      mbar_wait<64>(&dfull[slot0 + (g & 1)], (g >> 1) & 1);
       if (PROF) T[0] += clk() - f0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -644,33 +586,27 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) 
         x[e] = mont_mul(lds64(dslot + seed_off + (u32)e * kLSRec * 8), lds64(dslot + g_off + (u32)e * kCRec * 8), mp);
         lds2(dslot + mul_off + (u32)e * kCRec * 8, sm[e], sw[e]);
       }
-      // the loaded values are in registers before the slot is handed back to the async proxy
-#pragma unroll
-      for (int e = 0; e < 4; ++e) asm volatile("" :: "l"(x[e]), "l"(sm[e]), "l"(sw[e]));
-      fence_async_smem();
-      asm volatile("bar.sync %0, %1;" :: "r"(1 + my_stage), "r"(32 * kProdPerStage) : "memory");
     };
-    if (loader && cur.valid) load_kblock(a, cur, dslot, &dfull[slot0]);
-    if (cur.valid) {
-      fetch(0);
-      if (loader && ahead.valid) load_kblock(a, ahead, dslot, &dfull[slot0]);
-    }
-    for (; cur.valid;) {
+    if (cur.valid) fetch(0);
+    for (; cur.valid; cur = ahead, ahead.advance(a, kStages)) {
       const u32 stage = (u32)my_stage;
       const u32 use = guse;
       long long c0 = clk();
       mbar_wait<64>(&empty[stage], (use & 1) ^ 1);
       long long c1 = clk();
       if (PROF) T[1] += c1 - c0;
-      if (leader) {   // this CTA's half of the K-block's baby-step planes (v = 32 rank .. +31)
-        uint64_t* rb = lead ? &full[stage] : &rfull[stage];
+      // the other slot held K-block guse-1, which every warp of the group read (at the end of
+      // K-block guse-2) before arriving on that stage fill: refill it with the group's next K-block
+      if (leader) {
         if (PROF && (a.dbg == 4 || a.dbg == 6 || a.dbg == 7)) {
-          mbar_arrive(rb);
+          mbar_arrive(&full[stage]);
         } else {
-          mbar_expect_tx(rb, kRBytes);
-          bulk_g2s(stage0 + 8 * kPlaneA, a.Rp + (((u64)cur.q0 / kKB + cur.kb) * 2 + rank) * kRBytes, kRBytes, rb);
+          mbar_expect_tx(&full[stage], kRBytes);
+          bulk_g2s(stage0 + 8 * kPlaneA, a.Rp + ((u64)cur.q0 / kKB + cur.kb) * kRBytes, kRBytes, &full[stage]);
         }
       }
+      if (loader && ahead.valid)
+        load_kblock(a, ahead, data0 + (slot0 + ((guse + 1) & 1)) * kDataSlot, &dfull[slot0 + ((guse + 1) & 1)]);
 #pragma unroll 2
       for (int k = 0; k < ((PROF && (a.dbg == 2 || a.dbg >= 6)) ? 0 : 16); ++k) {
         // row rr + 8k: the next 8-row core-matrix group, +128 bytes
@@ -679,19 +615,13 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) 
         for (int e = 0; e < 4; ++e) x[e] = mul_shoup4(x[e], sm[e], sw[e], np);
       }
       fence_async_smem();
-      // peer CTA: a local arrival; the relay forwards the completed stage to the leader (a
-      // cluster-scope release from a thread with fresh stores costs ~1k clk)
-      mbar_arrive(lead ? &full[stage] : &rfull[stage]);
+      mbar_arrive(&full[stage]);
       if (PROF) T[2] += clk() - c1;
       if (PROF) T[3] += 1;
       ++guse;
-      cur = ahead;
-      ahead.advance(a, kStages);
-      // next K-block's seeds while this stage is being consumed; then refill the slot
-      if (cur.valid) {
-        fetch(guse);
-        if (loader && ahead.valid) load_kblock(a, ahead, dslot, &dfull[slot0]);
-      }
+      // next K-block's seeds while this stage is being consumed (its data arrived during this
+      // K-block); the product latency hides in the wait for the stage
+      if (ahead.valid) fetch(guse);
     }
   } else {
     // ------------------------------------------------------------ epilogue (+ MMA issue in warp 0)
@@ -717,13 +647,12 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) 
       g = uni(g);
       u64* prow = a.partial + ((u64)pc.z * kRounds + g) * a.ldp;
       u32* raw = raw_cta + (u64)(nunit & 1) * kDiag * (kU * kV);
-      if (lead && warp == kMmaWarp) {
+      if (warp == kMmaWarp) {
         // (this raw buffer was last read two units ago by warps 2 / 3's fold of warp 0's rows;
         // that fold precedes their drain of the previous unit, which this warp has waited for
         // through acce -- no extra barrier needed)
         long long c0 = clk();
         mbar_wait<32>(&acce, (nunit & 1) ^ 1);
-        mbar_wait<32>(&acce2, (nunit & 1) ^ 1);   // and the peer CTA's drain
         if (PROF) T[2] += clk() - c0;
         tc_fence_after();
         for (u32 kb = 0; kb < nkb; ++kb, ++it) {
@@ -758,17 +687,15 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) 
       tc_fence_after();
       u32* raw_u = raw + (u64)u * 4;
       const bool st = !(PROF && a.dbg == 3);
-      const u32 acce_remote = lead ? 0u : peer_addr(&acce2, 0);
-      if (g == 0) epi_drain<0>(tl, raw_u, &acce, acce_remote, st);
-      else epi_drain<1>(tl, raw_u, &acce, acce_remote, st);
+      if (g == 0) epi_drain<0>(tl, raw_u, &acce, st);
+      else epi_drain<1>(tl, raw_u, &acce, st);
       if (PROF && warp != kMmaWarp) T[1] += clk() - c1;
       if (PROF) T[3] += 1;
       // warps 1-3 fold the unit while warp 0 issues the next one's MMAs; warp 0's rows are
       // split by v between warps 2 and 3 (1.5 row-sets each on SMSPs 2 / 3, 1 on SMSP 1: the fold
       // shares those SMSPs with producer warps)
       long long c2 = clk();
-      // (the peer CTA issues no MMAs: there every warp folds its own rows)
-      for (int pass = 0; pass < (!lead ? 1 : warp == kMmaWarp ? 0 : (warp == 1 ? 1 : 2)); ++pass) {
+      for (int pass = 0; pass < (warp == kMmaWarp ? 0 : (warp == 1 ? 1 : 2)); ++pass) {
         u32 ur = u, vbeg = 0, vend = (u32)kV;
         if (pass == 1) {                 // warp 0's rows, once all 4 warps drained the unit
           mbar_wait<32>(&acce, nunit & 1);
@@ -796,10 +723,10 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) 
     }
   }
   tc_fence_before();
-  cluster_sync_all();
+  __syncthreads();
   if (warp == kMmaWarp) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" :: "r"(tb));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tb));
   }
 }
 
@@ -825,20 +752,19 @@ static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __r
 }
 
 // Per handle (pe_create): the baby-step byte planes R_t[i][v] = byte t of the Montgomery residue
-// m_i^v 2^64 mod p (v < V) in the stage layout of each K-block, split into the two CTAs' halves
-// (v < 32: rank 0, v >= 32: rank 1; kRBytes each) -- any representative < 2^64 gives exact byte
-// products; the epilogue's REDC removes the 2^64.  Block = 2 K-blocks staged in shared memory;
-// thread = (4 terms, rows r + 8j): one warp's stores cover 8 consecutive rows x 16 bytes, and
-// the block leaves with 16-byte coalesced stores.
+// m_i^v 2^64 mod p (v < V) in the stage layout of each K-block (any representative < 2^64 gives
+// exact byte products; the epilogue's REDC removes the 2^64).  Block = 2 K-blocks staged in
+// shared memory; thread = (4 terms, rows r + 8j): one warp's stores cover 8 consecutive rows x
+// 16 bytes, and the block leaves with 16-byte coalesced stores.
 constexpr int kRpThreads = 128;
 static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __restrict__ m, u64 t_pad,
                                                                   uint8_t* __restrict__ Rp, ModParams mp) {
-  __shared__ __align__(16) uint8_t st[4 * kRBytes];
+  __shared__ __align__(16) uint8_t st[2 * kRBytes];
   const u64 nblk = (t_pad + 2 * kKB - 1) / (2 * kKB);   // Rp is allocated for a whole last block
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const u32 ql = (u32)(lane >> 3), r = (u32)(lane & 7);
   const u32 kbl = (u32)warp >> 1, h = (u32)warp & 1;
-  const u32 base = kbl * 2 * kRBytes + h * kLBOB + r * 16u + ql * 4u;
+  const u32 base = kbl * kRBytes + h * kLBOB + r * 16u + ql * 4u;
   for (u64 blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const u64 q0 = blk * 2 * kKB + kbl * kKB + h * 16 + ql * 4;
     u64 y[4], m8[4];
@@ -863,15 +789,14 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
       a = prmt(h0, h1, 0x5140); b = prmt(h2, h3, 0x5140); c = prmt(h0, h1, 0x7362); d = prmt(h2, h3, 0x7362);
       wd[4] = prmt(a, b, 0x5410); wd[5] = prmt(a, b, 0x7632); wd[6] = prmt(c, d, 0x5410); wd[7] = prmt(c, d, 0x7632);
 #pragma unroll
-      for (int t = 0; t < 8; ++t)   // row v = r + 8j: half j / 4, 8-row group j % 4 of the half
-        *(u32*)(st + base + (j >> 2) * kRBytes + (u32)t * kPlaneB + (j & 3) * 128u) = wd[t];
+      for (int t = 0; t < 8; ++t) *(u32*)(st + base + (u32)t * kPlaneB + j * 128u) = wd[t];
 #pragma unroll
       for (int e = 0; e < 4; ++e) y[e] = mont_mul(y[e], m8[e], mp);
     }
     __syncthreads();
-    uint4* dst = (uint4*)(Rp + blk * 4 * kRBytes);
+    uint4* dst = (uint4*)(Rp + blk * 2 * kRBytes);
     const uint4* src = (const uint4*)st;
-    for (u32 i = threadIdx.x; i < 4 * kRBytes / 16; i += kRpThreads) dst[i] = src[i];
+    for (u32 i = threadIdx.x; i < 2 * kRBytes / 16; i += kRpThreads) dst[i] = src[i];
     __syncthreads();
   }
 }
