@@ -22,7 +22,7 @@ def dev_ms(w, path, T, reps=5):
         return e0.elapsed_time(e1) / reps
 
 
-for cfg, Ts in ((2, (1000, 2048, 4096, 8192)), (3, (1024, 2048, 4096, 8192, 16384)), (4, (4096,))):
+for cfg, Ts in ((2, (256, 512, 1000, 2048, 4096)), (3, (256, 512, 1024, 2048, 4096)), (4, (1024, 2048, 4096))):
     w = synth.gen_config(cfg)
     base = pe.PATH_AUTO if cfg == 4 else pe.PATH_INT
     for T in Ts:
