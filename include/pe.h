@@ -49,12 +49,14 @@ enum {
 
 enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_MIX = 3, PE_PATH_INT32 = 4, PE_PATH_TC = 5 };
 /* PE_PATH_TC forces the tensor-core form of the step (p < 2^62, else PE_ENOTSUP): each bucket's
- * block of T_c = 128 x 128 points is the product L * R of giant-step values c_i m_i^{j_s+128u} and
+ * block of T_c = 128 x 64 points is the product L * R of giant-step values c_i m_i^{j_s+64u} and
  * baby-step values m_i^v (the Vandermonde structure M_i(beta^t) = m_i^t, PAPER.md:420-427,
- * 465-478), computed exactly as 64 byte-by-byte int8 tcgen05 MMAs.  PE_PATH_AUTO
- * selects it for any p < 2^62 when T >= 2048 (>= 5*10^5 padded terms) or T >= 4096 (fewer
- * terms) -- pe_tc_info reports the handle's threshold (env PE_TC=0 off, 1 auto, 2 always);
- * PE_PATH_INT never uses it.  Results are bit-identical either way. */
+ * 465-478), computed exactly as 64 byte-by-byte int8 tcgen05 MMAs; the baby-step
+ * planes are built once per handle (about 530 B per padded term of device memory).
+ * PE_PATH_AUTO selects it for any p < 2^62 when T >= 512 (>= 5*10^5 padded terms) or
+ * T >= 8.6e7 / t_pad clamped to [512, 8192] (fewer terms) -- pe_tc_info reports the handle's
+ * threshold (env PE_TC=0 off, 1 auto, 2 always); PE_PATH_INT never uses it.  Results are
+ * bit-identical either way. */
 /* PE_PATH_INT32 is reported by pe_info only: every p < 2^31 (any requested path except FP64)
  * uses 32-bit Shoup products. */
 /* PE_PATH_MIX is reported by pe_info only (env PE_CORE=mix, p < 2^50): half of every lane's

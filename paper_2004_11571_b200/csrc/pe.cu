@@ -215,10 +215,14 @@ static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStrea
   return launch_step_path<kFp64>(R, grid, block, s, a);
 }
 
-// automatic tensor-core path from this many points (a chunk is tc::kChunk = 8192 points): k_tc is
-// ~10x faster per term-point than k_step but computes whole chunks and pays a fixed epilogue per
-// piece; measured crossovers (scripts/tc_threshold.py): T ~ 2048 for 10^6 terms, ~4096 for 10^5.
-static u64 tc_min_T(u64 t_pad) { return t_pad >= 500000 ? 2048 : 4096; }
+// automatic tensor-core path from this many points (a chunk is tc::kChunk = 8192 points): k_tc
+// costs a flat ~0.11 ms + 0.42 ns per padded term for any T <= 8192, k_step grows with t * T.
+// Measured crossovers (scripts/tc_threshold.py, profiles/r01_tc_threshold.jsonl): T ~ 860 for
+// 10^5 terms, ~480 for 10^6 (k_step INT), 512 vs FP64 Alg. 2 -- i.e. T* ~ 8.6e7 / t_pad, >= 512.
+static u64 tc_min_T(u64 t_pad) {
+  if (t_pad >= 500000) return 512;
+  return std::min<u64>(8192, std::max<u64>(512, 86000000ull / std::max<u64>(t_pad, 1)));
+}
 
 static unsigned grid_for(u64 n, unsigned block) {
   u64 b = (n + block - 1) / block;

@@ -115,16 +115,20 @@ def test_tc_equals_scalar_step_and_fermat():
 
 
 def test_tc_auto_selection():
-    """PE_PATH_AUTO: tensor path for p < 2^62 and T >= the handle's threshold (4096 for small
-    t, 2048 from 5*10^5 padded terms); never for p >= 2^62, PE_PATH_INT or PE_PATH_FP64; PE_PATH_TC with
-    p >= 2^62 is PE_ENOTSUP."""
+    """PE_PATH_AUTO: tensor path for p < 2^62 and T >= the handle's threshold (8.6e7 / t_pad
+    clamped to [512, 8192]; 512 from 5*10^5 padded terms); never for p >= 2^62, PE_PATH_INT or
+    PE_PATH_FP64; PE_PATH_TC with p >= 2^62 is PE_ENOTSUP."""
     w = synth.random_small(524, P62, 5, 100, 3, 10, 1)
     with pe.Context.from_workload(w) as ctx:
-        assert ctx.info()["tc_min_T"] == 4096
-        assert ctx.uses_tc(4096) and not ctx.uses_tc(4095)
+        assert ctx.info()["tc_min_T"] == 8192
+        assert ctx.uses_tc(8192) and not ctx.uses_tc(8191)
+    w2 = synth.gen_config(2, T=10)
+    with pe.Context.from_workload(w2) as ctx:
+        tp = ctx.info()["t_padded"]
+        assert ctx.info()["tc_min_T"] == max(512, 86_000_000 // tp) and ctx.uses_tc(1000)   # config 2
     w3 = synth.gen_config(3, t=600_000, T=10)
     with pe.Context.from_workload(w3) as ctx:
-        assert ctx.info()["tc_min_T"] == 2048 and ctx.uses_tc(2048) and not ctx.uses_tc(2047)
+        assert ctx.info()["tc_min_T"] == 512 and ctx.uses_tc(512) and not ctx.uses_tc(511)
     with pe.Context.from_workload(w, path=pe.PATH_INT) as ctx:
         assert not ctx.uses_tc(10**6)
     w50 = synth.random_small(525, (1 << 50) - 27, 5, 100, 3, 10, 1)
