@@ -129,6 +129,8 @@ struct pe_ctx {
   size_t seed_elems = 0;
   u32* d_tc_scratch = nullptr;   // k_tc per-CTA drained diagonal sums (n_sm x 2 x kDiag x kChunk u32)
   size_t partial_cap_bytes = (size_t)1 << 30;
+  cudaStream_t copy_stream = nullptr;   // pe_eval: device->host copy of a column block
+  cudaEvent_t copy_done = nullptr;
   // kernel timing (pe_set_timing / pe_kernel_stats)
   bool timing = false;
   struct Rec { cudaEvent_t e0, e1, e2; double tp; };
@@ -152,6 +154,8 @@ static void free_all(pe_ctx* h) {
                   (void*)h->d_seed})
     if (q) cudaFreeAsync(q, s);
   if (s) cudaStreamSynchronize(s);
+  if (h->copy_stream) cudaStreamSynchronize(h->copy_stream), cudaStreamDestroy(h->copy_stream);
+  if (h->copy_done) cudaEventDestroy(h->copy_done);
   if (h->stream) cudaStreamDestroy(h->stream);
 }
 
@@ -795,11 +799,34 @@ extern "C" int pe_eval(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* out) {
       rc = set_err(PE_ENOMEM);
     else h->out_scratch_elems = need;
   }
-  if (rc == PE_OK) rc = eval_device_impl(h, j0, T, h->d_out_scratch, T, h->stream);
-  if (rc == PE_OK) {
-    if (cudaMemcpyAsync(out, h->d_out_scratch, need * sizeof(u64), cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
-        cudaStreamSynchronize(h->stream) != cudaSuccess)
+  // Long ranges on the tensor-core path: two column blocks of whole chunks, the first block's
+  // device->host copy (pitched: rows of the [G][T] result) overlapping the second's evaluation.
+  const u64 half = (T / 2 + tc::kChunk - 1) / tc::kChunk * tc::kChunk;
+  const bool split = rc == PE_OK && use_tc(h, T) && T >= 2 * (u64)tc::kChunk && half < T && use_tc(h, T - half);
+  if (split) {
+    if (!h->copy_stream && cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
       rc = set_err(PE_ECUDA);
+    if (rc == PE_OK && !h->copy_done && cudaEventCreateWithFlags(&h->copy_done, cudaEventDisableTiming) != cudaSuccess)
+      rc = set_err(PE_ECUDA);
+    const u64 blk[2][2] = {{0, half}, {half, T - half}};
+    for (int b = 0; b < 2 && rc == PE_OK; ++b) {
+      rc = eval_device_impl(h, j0 + blk[b][0], blk[b][1], h->d_out_scratch + blk[b][0], T, h->stream);
+      if (rc != PE_OK) break;
+      if (cudaEventRecord(h->copy_done, h->stream) != cudaSuccess ||
+          cudaStreamWaitEvent(h->copy_stream, h->copy_done, 0) != cudaSuccess ||
+          cudaMemcpy2DAsync(out + blk[b][0], T * sizeof(u64), h->d_out_scratch + blk[b][0], T * sizeof(u64),
+                            blk[b][1] * sizeof(u64), h->G, cudaMemcpyDeviceToHost, h->copy_stream) != cudaSuccess)
+        rc = set_err(PE_ECUDA);
+    }
+    if (cudaStreamSynchronize(h->copy_stream) != cudaSuccess || cudaStreamSynchronize(h->stream) != cudaSuccess)
+      if (rc == PE_OK) rc = set_err(PE_ECUDA);
+  } else {
+    if (rc == PE_OK) rc = eval_device_impl(h, j0, T, h->d_out_scratch, T, h->stream);
+    if (rc == PE_OK) {
+      if (cudaMemcpyAsync(out, h->d_out_scratch, need * sizeof(u64), cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+          cudaStreamSynchronize(h->stream) != cudaSuccess)
+        rc = set_err(PE_ECUDA);
+    }
   }
   if (cur != h->device) cudaSetDevice(cur);
   return rc;
