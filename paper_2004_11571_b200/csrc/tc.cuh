@@ -57,9 +57,11 @@ constexpr u32 kPieceMax = 8192;           // terms per accumulation: 8192 * 8 * 
 // core-matrix column 128 B apart (SBO), the two 16-byte K halves LBO apart.
 constexpr u32 kLBOA = 2048;               // L planes (A, 128 rows): writes are conflict-free unpadded
 constexpr u32 kPlaneA = kLBOA + 2048;
-constexpr u32 kLBOB = 1024 + 64;          // R planes (B, 64 rows): +64 B spreads the K halves over banks
-constexpr u32 kPlaneB = kLBOB + 1024;
-constexpr u32 kStageBytes = 8 * kPlaneA + 8 * kPlaneB;   // 8 L planes + 8 R planes (49664 B)
+// R planes (B, 64 rows, written by TMA only): [K half][plane t][64 rows x 16 B], so planes
+// t .. t+k-1 are one B operand of N = 64k rows (SBO 128) -- one MMA covers k diagonals
+constexpr u32 kPlaneB = kV * 16;          // one plane's rows in one K half (1 KB)
+constexpr u32 kLBOB = 8 * kPlaneB;        // K-half stride (8 KB)
+constexpr u32 kStageBytes = 8 * kPlaneA + 2 * kLBOB;     // 8 L planes + 8 R planes (49152 B)
 // Per-term records (array of structs, so one K-block's data is two contiguous bulk copies):
 //   LS record (per chunk, 1 u64): the chunk seed c m^{j_s}
 //   C  record (10 u64): the giant-step chain multiplier m^{8V} and its Shoup constant, and the
@@ -69,7 +71,7 @@ constexpr u32 kStageBytes = 8 * kPlaneA + 8 * kPlaneB;   // 8 L planes + 8 R pla
 // and each K-block's 16.5 KB is one TMA bulk copy into the stage.
 constexpr int kLSRec = 1, kCRec = 10;
 enum { kC_mL = 0, kC_wL = 1, kC_g0 = 2 };
-constexpr u32 kRBytes = 8 * kPlaneB;                  // one K-block's R planes (16896 B)
+constexpr u32 kRBytes = 2 * kLBOB;                    // one K-block's R planes (16384 B)
 constexpr u32 kDataLS = kKB * kLSRec * 8;             // 256 B
 constexpr u32 kDataSlot = kDataLS + kKB * kCRec * 8;  // 2816 B
 constexpr int kDataSlots = 2 * kStages;               // 2 per producer group: current + next K-block
@@ -82,10 +84,11 @@ constexpr int kThreads = (kProdWarp0 + kStages * kProdPerStage) * 32;   // 12 wa
 static_assert(kRounds <= kEpiWarps, "round g's MMAs are issued by epilogue warp g");
 static_assert(kDiag * kV == 512, "a round's accumulators fill TMEM");
 static_assert(kSmemBytes + 256 <= 232448, "shared memory");
-// diagonal groups: 8 + 7 diagonals, 30 + 34 digit pairs
+// diagonal rounds: d = 0..7 and d = 8..14 (36 + 28 digit pairs); accumulator slot = d - d_lo, so
+// for one L plane s the round's pairs (s, t) have consecutive t and land in consecutive slots:
+// one wide MMA (B = planes t..t+k-1, N = 64k <= 256) covers k of them
 __host__ __device__ constexpr int group_diag(int g, int di) {
-  return g == 0 ? (di == 0 ? 7 : di == 1 ? 6 : di == 2 ? 5 : di == 3 ? 0 : di == 4 ? 1 : di == 5 ? 2 : di == 6 ? 14 : 13)
-                : (di == 0 ? 8 : di == 1 ? 4 : di == 2 ? 9 : di == 3 ? 3 : di == 4 ? 10 : di == 5 ? 11 : di == 6 ? 12 : -1);
+  return g == 0 ? di : (di < 7 ? 8 + di : -1);
 }
 
 struct TcArgs {
@@ -155,6 +158,57 @@ __device__ __forceinline__ void mma_u8c(u32 dtmem, uint64_t ad, uint64_t bd, u32
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}\n"
                  :: "r"(dtmem), "l"(ad), "l"(bd), "r"(kIdesc), "r"(acc));
+}
+
+template <int COL>
+__device__ __forceinline__ void mma_u8n(u32 dtmem, uint64_t ad, uint64_t bd, u32 idesc, u32 acc) {
+  if (COL == 0)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
+                 :: "r"(dtmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+  else if (COL == 1)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n\t}\n"
+                 :: "r"(dtmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+  else
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}\n"
+                 :: "r"(dtmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__host__ __device__ constexpr u32 idesc_n(int n) {
+  return (2u << 4) | ((u32)(n >> 3) << 17) | ((u32)(kU >> 4) << 24);
+}
+
+// Round G on one stage as wide MMAs: for each L plane s the round's partners t form one range
+// [t_lo, t_hi]; it is issued as MMAs of <= 4 consecutive R planes (N = 64k), D = slots
+// s + t - d_lo ...  The plane whose range covers every slot of the round (s = 0 for d = 0..7,
+// s = 7 for d = 8..14) goes first, so at K-block 0 it initialises all accumulators (acc = 0) and
+// every later MMA accumulates.  A plane issued as two MMAs keeps A in the collector.
+template <int G>
+__device__ __forceinline__ void issue_round_wide(u32 tb, uint64_t da, uint64_t db, bool first_kb) {
+  constexpr int d_lo = G == 0 ? 0 : 8, d_hi = G == 0 ? 7 : 14;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int sd = G == 0 ? k : 7 - k;
+    const int t_lo = d_lo - sd > 0 ? d_lo - sd : 0;
+    const int t_hi = d_hi - sd < 7 ? d_hi - sd : 7;
+    if (t_lo > t_hi) continue;
+    const int nmma = (t_hi - t_lo) / 4 + 1;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      if (c >= nmma) continue;
+      const int ta = t_lo + 4 * c;
+      const int tb2 = ta + 3 < t_hi ? ta + 3 : t_hi;
+      const int n = 64 * (tb2 - ta + 1);
+      const u32 acc = (!first_kb || k > 0) ? 1u : 0u;
+      const u32 dt = tb + (u32)((sd + ta - d_lo) * kV);
+      const uint64_t ad = da + (uint64_t)((u32)sd * (kPlaneA >> 4));
+      const uint64_t bd = db + (uint64_t)((u32)ta * (kPlaneB >> 4));
+      if (nmma == 1) mma_u8n<0>(dt, ad, bd, idesc_n(n), acc);
+      else if (c == 0) mma_u8n<1>(dt, ad, bd, idesc_n(n), acc);
+      else mma_u8n<2>(dt, ad, bd, idesc_n(n), acc);
+    }
+  }
 }
 
 // digit pair (s, t = d - s) of diagonal slot di exists in round G
@@ -667,12 +721,12 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
           // tcgen05.commit tracks the MMAs its own thread issued
           __syncwarp();
           if (elect_one()) {
-            if (PROF && a.dbg == 7) {
+            if (PROF && a.dbg == 7) {   // one N = 64 MMA per digit pair (the previous issue form)
               if (g == 0) issue_round<0, true>(tbu, da, db, kb == 0);
               else issue_round<1, true>(tbu, da, db, kb == 0);
             } else if (!(PROF && a.dbg == 1)) {
-              if (g == 0) issue_round<0>(tbu, da, db, kb == 0);
-              else issue_round<1>(tbu, da, db, kb == 0);
+              if (g == 0) issue_round_wide<0>(tbu, da, db, kb == 0);
+              else issue_round_wide<1>(tbu, da, db, kb == 0);
             }
             if (kb + 1 == nkb) mma_commit(&accf);   // accumulators complete after this K-block
             mma_commit(&empty[stage]);
