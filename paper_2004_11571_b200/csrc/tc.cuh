@@ -18,28 +18,29 @@
 // for <= 8192 terms per accumulation (a "piece"; the s32 TMEM accumulator wraps mod 2^32 without
 // saturation, so its bits read as u32 are exact).  X mod p = sum_d D_d (2^{8d} mod p) mod p.
 //
-// Shapes: U = M = 128 (TMEM lanes), V = N = 64, K-block = 32 terms (one kind::i8 MMA).  The 15
-// diagonals do not fit TMEM at once (15 x 64 columns > 512), so a piece is evaluated in 2 rounds
-// of <= 8 diagonals (30 and 34 digit-pair MMAs per K-block), regenerating L and R per round;
-// rounds accumulate into the unit's raw diagonal buffer.  Measured on this B200: an M=128, K=32
-// i8 MMA costs ~64 clk for any N <= 128 (pe_bench_mma), so N = 64 runs the tensor pipe at half
-// its N = 128 rate -- but with 2 rounds instead of 4 the generation per point falls from 2 to
-// 1.5 modular products, and the smaller stage (49.7 KB) lets 4 stages fit shared memory, which
-// decouples the producers from the in-order MMA.
+// Shapes: U = M = 128 (TMEM lanes), V = 64, K-block = 32 terms (one kind::i8 MMA K step).  The
+// 15 diagonals do not fit TMEM at once (15 x 64 columns > 512), so a piece is evaluated in 2
+// rounds, d = 0..7 and d = 8..14 (slot = d - d_lo); a unit is (piece, chunk, round) and reduces
+// its own part X_g into its own partial row (X mod p = sum of the parts).  Because the round's
+// partners t of one L plane s are consecutive, and the baby-step planes sit plane after plane in
+// each K half, each (s, run of t) is ONE MMA with N = 64k <= 256 (22 MMAs per K-block for both
+// rounds).  The baby-step planes R = m^v do not depend on the points: they are built once per
+// handle and streamed into the stages by TMA, so per evaluation only the giant steps are
+// generated (1 modular product per 32 term-points).
 //
-// Warp roles (one CTA per SM, 12 warps = 3 per SMSP, persistent, static round-robin over units =
-// (piece, chunk)):
-//   warps 0-3  epilogue: tcgen05.ld the round's diagonals (TMEM lane = u) into the unit's raw
-//              buffer (per-CTA, L2-resident), release TMEM; after the unit's last round an exact
-//              160-bit fold of the 15 diagonals and one reduction mod p per point ->
-//              partial[slot][chunk*kChunk + u*kV + v].  Warps 0 / 1 also issue rounds 0 / 1's MMAs
-//              (tcgen05.mma.cta_group::1.kind::i8, elect.sync leader); warp 0 allocates TMEM.
+// Warp roles (one CTA per SM, 12 warps = 3 per SMSP, persistent; units are piece-major and dealt
+// to the CTAs in snake order):
+//   warps 0-3  epilogue: tcgen05.ld the unit's diagonals (TMEM lane = u) into the unit's raw
+//              buffer (per-CTA, L2-resident), release TMEM; then an exact 160-bit fold of the
+//              round's diagonals and one reduction mod p per point (warps 1-3; warps 2 / 3 also
+//              cover warp 0's rows) -> partial[slot][chunk*kChunk + u*kV + v].  Warp 0 issues
+//              every unit's MMAs (tcgen05.mma.cta_group::1.kind::i8, elect.sync leader) and
+//              allocates TMEM.
 //   warps 4-11 producers, 2 per smem stage: each generates 16 terms x 128 giant-step rows of one
-//              K-block with Shoup products (4 chains per lane, seeded from per-chunk chain seeds)
-//              and writes their 8 byte planes in the no-swizzle K-major UMMA layout.  The baby-step
-//              planes R = m^v do not depend on the points: they are written once per handle and
-//              the group's first lane copies each K-block's planes into the stage with TMA (as it
-//              does the group's next K-block of per-term records).
+//              K-block with Shoup products (4 chains per lane, seeded from the chunk seed) and
+//              writes their 8 byte planes in the no-swizzle K-major UMMA layout; one warp's first
+//              lane copies the K-block's baby-step planes into the stage with TMA, the other's
+//              prefetches the group's next K-block of per-term records.
 #pragma once
 #include "modcore.cuh"
 
