@@ -172,3 +172,35 @@ def test_tc_small_tiles_odd_kblocks(R):
 def test_mma_probe_rate():
     """pe_bench_mma runs and reports a plausible int8 rate (> 100 TOPS at N = 128)."""
     assert pe.bench_mma(128, 4000) > 1e14
+
+
+@pytest.mark.parametrize("T", [16385, 2 * 8192, 3 * 8192 + 5])
+def test_tc_host_eval_column_blocks(T):
+    """pe_eval on the tensor path splits long ranges into two column blocks of whole chunks and
+    overlaps the first block's pitched device->host copy with the second's evaluation: the
+    result equals pe_eval_device's (single pass) and the oracle's incremental evaluation."""
+    import torch
+    w = synth.random_small(540 + T % 97, P62, 6, 900, 4, T, 11)
+    with pe.Context.from_workload(w, path=pe.PATH_TC) as ctx:
+        host = ctx.eval(w.j0, w.T)
+        d = torch.empty((ctx.G, w.T), dtype=torch.int64, device="cuda")
+        ctx.eval_device(w.j0, w.T, d.data_ptr())
+        torch.cuda.synchronize()
+        dev = d.cpu().numpy().view(np.uint64)
+    assert np.array_equal(host, dev)
+    assert np.array_equal(host, oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T))
+
+
+@pytest.mark.parametrize("nbig", [8192, 8193, 16384 + 33])
+def test_tc_piece_boundaries_and_max_tile(nbig):
+    """A bucket of exactly one / just over one / two pieces (8192 terms each: the u32 exactness
+    bound) with the largest tile (R = 16, buckets padded to 512 terms), many units per CTA."""
+    t = nbig + 300
+    w = synth.random_small(550 + nbig % 101, P62, 8, t, 5, 200, 2)
+    w.exps[:, :2] = 3
+    w.exps[:nbig, :2] = (7, 7)
+    with pe.Context.from_workload(w, path=pe.PATH_TC, R=16) as ctx:
+        assert ctx.info()["R"] == 16
+        out = ctx.eval(w.j0, w.T)
+    ref = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
+    assert np.array_equal(out, ref)
