@@ -1,0 +1,91 @@
+"""CPU checks of the arithmetic the tensor-core path rests on (csrc/tc.cuh), from
+the definitions -- not from the kernel:
+
+* byte-diagonal identity: for 64-bit L, R split into bytes L = sum_s 2^{8s} L_s,
+  sum_i L_i R_i = sum_d 2^{8d} D_d with D_d = sum_i sum_{s+t=d} L_{i,s} R_{i,t} (exact integers);
+* the accumulator bound: D_d <= 8 * 255^2 * 8192 < 2^32 for a piece of 8192 terms, so a
+  wrapping u32/s32 accumulator holds it exactly;
+* the round split: X mod p = (X_0 + X_1) mod p with X_g = sum over round g's diagonals
+  (d = 0..7, d = 8..14), so each round can be reduced on its own;
+* the epilogue reduction: the 160-bit X is cut into 32-bit words x0..x4, x2..x4 are folded with
+  2^{32k} mod p into a 128-bit (hi, lo) with hi < p, and one Montgomery REDC gives X 2^-64 mod p --
+  which is sum_i L_i m_i^v when the baby-step factors are Montgomery residues m^v 2^64 mod p.
+"""
+import random
+
+import pytest
+
+P62 = (1 << 62) - 57
+
+
+def bytes_of(x):
+    return [(x >> (8 * s)) & 0xFF for s in range(8)]
+
+
+def diagonals(Ls, Rs):
+    D = [0] * 15
+    for L, R in zip(Ls, Rs):
+        lb, rb = bytes_of(L), bytes_of(R)
+        for s in range(8):
+            for t in range(8):
+                D[s + t] += lb[s] * rb[t]
+    return D
+
+
+def redc(hi, lo, p):
+    """Montgomery reduction of hi*2^64 + lo (hi < p): returns (hi*2^64 + lo) * 2^-64 mod p."""
+    assert hi < p
+    pinv = (-pow(p, -1, 1 << 64)) % (1 << 64)
+    u = (lo * pinv) % (1 << 64)
+    t = (hi * (1 << 64) + lo + u * p) >> 64
+    return t - p if t >= p else t
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_byte_diagonal_identity(seed):
+    rng = random.Random(seed)
+    n = 97
+    Ls = [rng.getrandbits(64) for _ in range(n)]
+    Rs = [rng.getrandbits(64) for _ in range(n)]
+    D = diagonals(Ls, Rs)
+    assert sum(a * b for a, b in zip(Ls, Rs)) == sum(D[d] << (8 * d) for d in range(15))
+
+
+def test_accumulator_bound_at_piece_size():
+    """All-0xFF bytes maximise every diagonal: the 8-pair diagonal over 8192 terms stays < 2^32."""
+    npairs = [min(d, 14 - d) + 1 for d in range(15)]
+    assert max(npairs) == 8
+    worst = 8 * 255 * 255 * 8192
+    assert worst < (1 << 32) and worst >= (1 << 31)     # tight: read as u32, not s32
+    D = diagonals([2**64 - 1] * 3, [2**64 - 1] * 3)
+    assert D == [3 * 255 * 255 * k for k in npairs]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_round_split_and_epilogue_reduction(seed):
+    rng = random.Random(100 + seed)
+    p = P62
+    R64 = (1 << 64) % p
+    n = 64
+    c = [rng.randrange(p) for _ in range(n)]
+    m = [rng.randrange(1, p) for _ in range(n)]
+    j, v = rng.randrange(1, 1 << 40), rng.randrange(64)
+    # giant-step values (lazy representatives < 4p, as the Shoup chains leave them) and
+    # Montgomery baby-step residues m^v 2^64 mod p
+    Ls = [(ci * pow(mi, j, p)) % p + rng.randrange(4) * p for ci, mi in zip(c, m)]
+    Ls = [x if x < (1 << 64) else x - p for x in Ls]
+    Rs = [(pow(mi, v, p) * R64) % p for mi in m]
+    want = sum(ci * pow(mi, j + v, p) for ci, mi in zip(c, m)) % p
+    D = diagonals(Ls, Rs)
+    parts = []
+    for rnd in (range(0, 8), range(8, 15)):
+        X = sum(D[d] << (8 * d) for d in rnd)
+        assert X < (1 << 145)
+        x = [(X >> (32 * k)) & 0xFFFFFFFF for k in range(5)]
+        lo, hi = x[0] | (x[1] << 32), 0
+        acc = lo
+        for k, xk in ((2, x[2]), (3, x[3]), (4, x[4])):
+            acc += xk * pow(2, 32 * k, p)                  # x_k * (2^{32k} mod p), 128-bit sum
+        hi, lo = acc >> 64, acc & ((1 << 64) - 1)
+        parts.append(redc(hi % p, lo, p))                  # = X_g 2^-64 mod p
+    assert (parts[0] + parts[1]) % p == want
