@@ -662,12 +662,15 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       }
       if (loader && ahead.valid)
         load_kblock(a, ahead, data0 + (slot0 + ((guse + 1) & 1)) * kDataSlot, &dfull[slot0 + ((guse + 1) & 1)]);
-#pragma unroll 2
-      for (int k = 0; k < ((PROF && (a.dbg == 2 || a.dbg >= 6)) ? 0 : 16); ++k) {
-        // row rr + 8k: the next 8-row core-matrix group, +128 bytes
-        store_digits<kPlaneA>(planes0 + (u32)k * 128u, x);
+      if (!(PROF && (a.dbg == 2 || a.dbg >= 6))) {
+#pragma unroll 3
+        for (int k = 0; k < 15; ++k) {
+          // row rr + 8k: the next 8-row core-matrix group, +128 bytes
+          store_digits<kPlaneA>(planes0 + (u32)k * 128u, x);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) x[e] = mul_shoup4(x[e], sm[e], sw[e], np);
+          for (int e = 0; e < 4; ++e) x[e] = mul_shoup4(x[e], sm[e], sw[e], np);
+        }
+        store_digits<kPlaneA>(planes0 + 15u * 128u, x);   // last row: no product after it
       }
       fence_async_smem();
       mbar_arrive(&full[stage]);
