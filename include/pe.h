@@ -48,12 +48,13 @@ enum {
 };
 
 enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_MIX = 3, PE_PATH_INT32 = 4, PE_PATH_TC = 5 };
-/* PE_PATH_TC forces the tensor-core form of the step (p < 2^62, else PE_ENOTSUP): each bucket's
+/* PE_PATH_TC forces the tensor-core form of the step (any p < 2^63; for 2^62 <= p the giant-step
+ * chains use the exact-quotient Shoup product so every value keeps 8 bytes): each bucket's
  * block of T_c = 128 x 64 points is the product L * R of giant-step values c_i m_i^{j_s+64u} and
  * baby-step values m_i^v (the Vandermonde structure M_i(beta^t) = m_i^t, PAPER.md:420-427,
  * 465-478), computed exactly as 64 byte-by-byte int8 tcgen05 MMAs; the baby-step
  * planes are built once per handle (about 530 B per padded term of device memory).
- * PE_PATH_AUTO selects it for any p < 2^62 when T >= 512 (>= 5*10^5 padded terms) or
+ * PE_PATH_AUTO selects it for any p < 2^63 when T >= 512 (>= 5*10^5 padded terms) or
  * T >= 8.6e7 / t_pad clamped to [512, 8192] (fewer terms) -- pe_tc_info reports the handle's
  * threshold (env PE_TC=0 off, 1 auto, 2 always); PE_PATH_INT never uses it.  Results are
  * bit-identical either way. */
@@ -66,7 +67,7 @@ enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_MIX = 3, PE_
 /* Tuning knobs (0 = automatic).  They never change the result (pin P13). */
 typedef struct pe_config {
   int32_t path;  /* PE_PATH_AUTO: FP64 Alg. 2 if p < 2^50 else INT64 Shoup, in the tensor-core form for
-                    large T when p < 2^62; PE_PATH_FP64 / PE_PATH_INT / PE_PATH_TC force one.  env PE_PATH=int|fp64, PE_CORE=mix|fp64|hyb|shoup     */
+                    large T (any p < 2^63); PE_PATH_FP64 / PE_PATH_INT / PE_PATH_TC force one.  env PE_PATH=int|fp64, PE_CORE=mix|fp64|hyb|shoup     */
   int32_t R;     /* terms per lane: 1,2,4,8,16 (FP64: <= 8); auto picks by bucket sizes    */
   int32_t warps; /* warps per CTA, 1..16 (auto 8)                                          */
   int32_t chunk; /* points per CTA (multiple of 32; auto by grid coverage)                 */

@@ -425,7 +425,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   // ---- tensor-core path (tc.cuh): per-term strides + the piece plan
   std::vector<uint4> pieces;
   std::vector<u32> tc_slot_start(G + 1);
-  if (h->tc_mode != 0 && (h->path == kInt4 || h->path == kFp64 || h->path == kInt32)) {
+  if (h->tc_mode != 0 && (h->path == kInt4 || h->path == kInt2 || h->path == kFp64 || h->path == kInt32)) {
     const u64 tp = h->t_pad;
     if (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp) || dalloc(&h->d_tcMS, (size_t)2 * tp) ||
         dalloc(&h->d_tcR, (size_t)((tp + 2 * tc::kKB - 1) / (2 * tc::kKB)) * 2 * tc::kRBytes))
@@ -519,17 +519,16 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
       path = kFp64;
     }
   } else if (path_req == PE_PATH_TC) {
-    if (p >= (1ull << 62)) { set_err(PE_ENOTSUP); return nullptr; }
-    path = kInt4;
+    path = p < (1ull << 62) ? kInt4 : kInt2;
   } else {
     set_err(PE_EINVAL);
     return nullptr;
   }
   // tensor-core path: forced by PE_PATH_TC; automatic (large T) for the INT64 Shoup path when the
   // caller asked for PE_PATH_AUTO; env PE_TC=0|1|2 overrides the automatic choice.
-  // (any p < 2^62: the automatic scalar core -- Shoup, FP64 Alg. 2 or 32-bit Shoup -- serves short
+  // (any p < 2^63: the automatic scalar core -- Shoup, FP64 Alg. 2 or 32-bit Shoup -- serves short
   // point ranges, the tensor-core form long ones)
-  const bool tc_able = path == kInt4 || path == kFp64 || path == kInt32;
+  const bool tc_able = path == kInt4 || path == kInt2 || path == kFp64 || path == kInt32;
   int tc_mode = path_req == PE_PATH_TC ? 2 : (path_req == PE_PATH_AUTO && tc_able ? 1 : 0);
   if (path_req == PE_PATH_AUTO && tc_able) {
     const int e = env_int("PE_TC", 1);
@@ -630,8 +629,10 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     h->seed_elems = (size_t)h->t_pad * nch_max * tc::kLSRec;
   }
   if (!h->d_tc_scratch) CU(cudaMallocAsync((void**)&h->d_tc_scratch, (size_t)h->n_sm * 2 * tc::kDiag * tc::kChunk * sizeof(u32), s));
-  CU(cudaFuncSetAttribute(tc::k_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
-  CU(cudaFuncSetAttribute(tc::k_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
+  const bool wide = h->p >= (1ull << 62);   // exact-quotient chains (values < 2p < 2^64)
+  CU(cudaFuncSetAttribute(tc::k_tc<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
+  CU(cudaFuncSetAttribute(tc::k_tc<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
+  CU(cudaFuncSetAttribute(tc::k_tc<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
     const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
@@ -674,8 +675,9 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
       CU(cudaMemset(d_prof, 0, nprof * sizeof(unsigned long long)));
       a.prof = d_prof;
     }
-    if (d_prof) tc::k_tc<true><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
-    else tc::k_tc<false><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
+    if (d_prof && !wide) tc::k_tc<true, false><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
+    else if (wide) tc::k_tc<false, true><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
+    else tc::k_tc<false, false><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
     CU(cudaGetLastError());
     if (d_prof) {
       std::vector<unsigned long long> hp(nprof);

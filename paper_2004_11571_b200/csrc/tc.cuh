@@ -1,4 +1,4 @@
-// tc.cuh -- tensor-core form of the step-and-reduce (rows a5 + a6) for p < 2^62 (sm_100a).
+// tc.cuh -- tensor-core form of the step-and-reduce (rows a5 + a6) for p < 2^63 (sm_100a).
 //
 // The matrix method's T x s evaluation matrix has the Vandermonde structure V[j][i] = m_i^j
 // ("M_i(beta^t) = m_i^t"; PAPER.md:465-478 transposed Vandermonde).  Writing a
@@ -567,7 +567,9 @@ __device__ __forceinline__ void load_kblock(const TcArgs& a, const KIter& k, u32
   bulk_g2s(dst + kDataLS, a.C + q * kCRec, kDataSlot - kDataLS, bar);
 }
 
-template <bool PROF>
+// WIDE: 2^62 <= p < 2^63 -- the giant-step chains use the exact-quotient Shoup product (output
+// < 2p < 2^64, so every value still has 8 bytes); otherwise the lazy one (output < 4p < 2^64).
+template <bool PROF, bool WIDE>
 static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 warps: <= 168 regs/thread
   unsigned long long g_entry = 0;
   if (PROF) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
@@ -668,7 +670,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
           // row rr + 8k: the next 8-row core-matrix group, +128 bytes
           store_digits<kPlaneA>(planes0 + (u32)k * 128u, x);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) x[e] = mul_shoup4(x[e], sm[e], sw[e], np);
+          for (int e = 0; e < 4; ++e) x[e] = WIDE ? mul_shoup2(x[e], sm[e], sw[e], np) : mul_shoup4(x[e], sm[e], sw[e], np);
         }
         store_digits<kPlaneA>(planes0 + 15u * 128u, x);   // last row: no product after it
       }

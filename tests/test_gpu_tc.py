@@ -42,6 +42,8 @@ def check_tc(w, **kw):
     ((1 << 62) - 57, 2, 30, 6, 1, 10),    # n = 2 (m = 1: every column = coefficient sums)
     (2**31 - 1, 3, 100, 9, 1, 64),        # n = 3, 31-bit p through the 64-bit tensor path
     ((1 << 50) - 27, 7, 600, 4, 3, 77),   # 50-bit p (auto would take FP64 Alg. 2)
+    ((1 << 63) - 25, 6, 700, 4, 5, 300),  # largest supported p: exact-quotient giant-step chains
+    ((1 << 62) + 135, 5, 400, 3, 1, 129), # just above 2^62
 ])
 def test_tc_edge_shapes(p, n, t, maxdeg, j0, T):
     w = synth.random_small(500 + t + n, p, n, t, maxdeg, T, j0, coeff_hi=2**64 - 1)
@@ -115,9 +117,8 @@ def test_tc_equals_scalar_step_and_fermat():
 
 
 def test_tc_auto_selection():
-    """PE_PATH_AUTO: tensor path for p < 2^62 and T >= the handle's threshold (8.6e7 / t_pad
-    clamped to [512, 8192]; 512 from 5*10^5 padded terms); never for p >= 2^62, PE_PATH_INT or
-    PE_PATH_FP64; PE_PATH_TC with p >= 2^62 is PE_ENOTSUP."""
+    """PE_PATH_AUTO: tensor path for any p < 2^63 and T >= the handle's threshold (8.6e7 / t_pad
+    clamped to [512, 8192]; 512 from 5*10^5 padded terms); never for PE_PATH_INT or PE_PATH_FP64."""
     w = synth.random_small(524, P62, 5, 100, 3, 10, 1)
     with pe.Context.from_workload(w) as ctx:
         assert ctx.info()["tc_min_T"] == 8192
@@ -137,11 +138,10 @@ def test_tc_auto_selection():
     with pe.Context.from_workload(w50, path=pe.PATH_FP64) as ctx:
         assert not ctx.uses_tc(10**6)
     w63 = synth.random_small(526, (1 << 63) - 25, 5, 100, 3, 10, 1)
-    with pe.Context.from_workload(w63) as ctx:
+    with pe.Context.from_workload(w63) as ctx:           # 2^62 <= p < 2^63: exact-quotient chains
+        assert ctx.uses_tc(10**6) and not ctx.uses_tc(100)
+    with pe.Context.from_workload(w63, path=pe.PATH_INT) as ctx:
         assert not ctx.uses_tc(10**6)
-    with pytest.raises(pe.PEError) as ei:
-        pe.Context.from_workload(w63, path=pe.PATH_TC)
-    assert ei.value.code == pe.PE_ENOTSUP
 
 
 def test_tc_batch_polys():
@@ -204,3 +204,18 @@ def test_tc_piece_boundaries_and_max_tile(nbig):
         out = ctx.eval(w.j0, w.T)
     ref = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
     assert np.array_equal(out, ref)
+
+
+def test_tc_63bit_prime_equals_scalar_step():
+    """2^62 <= p < 2^63 (exact-quotient giant-step chains, values < 2p < 2^64): the tensor path
+    equals k_step's lazy-2 Shoup path on a config-2-shaped instance spanning several chunks."""
+    w = synth.random_small(560, (1 << 63) - 25, 8, 20_000, 6, 17_000, 3)
+    with pe.Context.from_workload(w) as ctx:
+        assert ctx.uses_tc(w.T)
+        a = ctx.eval(w.j0, w.T)
+    with pe.Context.from_workload(w, path=pe.PATH_INT) as ctx:
+        assert not ctx.uses_tc(w.T)
+        b = ctx.eval(w.j0, w.T)
+    assert np.array_equal(a, b)
+    ks = np.array([0, 1, 8191, 8192, 16999], np.uint64)
+    assert np.array_equal(a[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
