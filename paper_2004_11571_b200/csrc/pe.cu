@@ -461,8 +461,9 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
     std::stable_sort(pieces.begin(), pieces.end(), [](const uint4& x, const uint4& y) { return x.y > y.y; });
     // one partial row per (piece, diagonal round): k_tc reduces each round's part on its own
     h->tc_npieces = (u32)pieces.size();
-    h->tc_nslots = (u32)pieces.size() * tc::kRounds;
-    for (auto& x : tc_slot_start) x *= tc::kRounds;
+    const u32 rounds = h->p < (1ull << 31) ? 1 : tc::kRounds;   // 4-byte digits: one round
+    h->tc_nslots = (u32)pieces.size() * rounds;
+    for (auto& x : tc_slot_start) x *= rounds;
     if (dalloc(&h->d_piece, pieces.size()) || dalloc(&h->d_tc_slot_start, G + 1)) return g_last_error;
     CU(cudaMemcpyAsync(h->d_piece, pieces.data(), pieces.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(h->d_tc_slot_start, tc_slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
@@ -629,10 +630,13 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     h->seed_elems = (size_t)h->t_pad * nch_max * tc::kLSRec;
   }
   if (!h->d_tc_scratch) CU(cudaMallocAsync((void**)&h->d_tc_scratch, (size_t)h->n_sm * 2 * tc::kDiag * tc::kChunk * sizeof(u32), s));
-  const bool wide = h->p >= (1ull << 62);   // exact-quotient chains (values < 2p < 2^64)
-  CU(cudaFuncSetAttribute(tc::k_tc<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
-  CU(cudaFuncSetAttribute(tc::k_tc<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
-  CU(cudaFuncSetAttribute(tc::k_tc<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
+  // kernel mode: 0 = lazy chains, 8 digits; 1 = p >= 2^62, exact chains, 8 digits; 2 = p < 2^31,
+  // exact chains (values < 2^32), 4 digits, one round
+  const int mode = h->p < (1ull << 31) ? 2 : (h->p >= (1ull << 62) ? 1 : 0);
+  CU(cudaFuncSetAttribute(tc::k_tc<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
+  CU(cudaFuncSetAttribute(tc::k_tc<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
+  CU(cudaFuncSetAttribute(tc::k_tc<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
+  CU(cudaFuncSetAttribute(tc::k_tc<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
     const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
@@ -649,7 +653,8 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     a.ldp = (np + 7) / 8 * 8;
     a.t_pad = h->t_pad;
     a.npieces = h->tc_npieces;
-    a.nunits = h->tc_npieces * nch * tc::kRounds;
+    a.rounds = h->p < (1ull << 31) ? 1 : tc::kRounds;
+    a.nunits = h->tc_npieces * nch * a.rounds;
     a.nch = nch;
     a.npts = np;
     for (int d = 0; d < 15; ++d) a.Wd[d] = h_powmod(2, 8 * (u64)d, h->p);
@@ -675,9 +680,10 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
       CU(cudaMemset(d_prof, 0, nprof * sizeof(unsigned long long)));
       a.prof = d_prof;
     }
-    if (d_prof && !wide) tc::k_tc<true, false><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
-    else if (wide) tc::k_tc<false, true><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
-    else tc::k_tc<false, false><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
+    if (d_prof && mode == 0) tc::k_tc<true, 0><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
+    else if (mode == 1) tc::k_tc<false, 1><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
+    else if (mode == 2) tc::k_tc<false, 2><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
+    else tc::k_tc<false, 0><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
     CU(cudaGetLastError());
     if (d_prof) {
       std::vector<unsigned long long> hp(nprof);

@@ -88,8 +88,9 @@ static_assert(kSmemBytes + 256 <= 232448, "shared memory");
 // diagonal rounds: d = 0..7 and d = 8..14 (36 + 28 digit pairs); accumulator slot = d - d_lo, so
 // for one L plane s the round's pairs (s, t) have consecutive t and land in consecutive slots:
 // one wide MMA (B = planes t..t+k-1, N = 64k <= 256) covers k of them
+// group 2: the single round of the 4-digit mode (p < 2^31: values < 2^32), d = 0..6
 __host__ __device__ constexpr int group_diag(int g, int di) {
-  return g == 0 ? di : (di < 7 ? 8 + di : -1);
+  return g == 0 ? di : g == 1 ? (di < 7 ? 8 + di : -1) : (di < 7 ? di : -1);
 }
 
 struct TcArgs {
@@ -100,6 +101,7 @@ struct TcArgs {
   u64* partial;          // [n_slots][ldp]
   u64 ldp, t_pad;
   u32 npieces, nunits, npts, nch;
+  u32 rounds;            // diagonal rounds per (piece, chunk): 2 (8-byte digits) or 1 (4-byte, p < 2^31)
   u64 Wd[15];            // 2^{8d} mod p  (Wd[8] = 2^64, Wd[12] = 2^96, Wd[14] -> see C128)
   u64 C128;              // 2^128 mod p
   u32* scratch;          // per CTA: 2 (ping-pong by unit) x kDiag accumulators x kChunk u32 drained diagonal sums
@@ -210,6 +212,18 @@ __device__ __forceinline__ void issue_round_wide(u32 tb, uint64_t da, uint64_t d
       else mma_u8n<2>(dt, ad, bd, idesc_n(n), acc);
     }
   }
+}
+
+// The 4-digit mode (p < 2^31): 16 digit pairs, diagonals 0..6 in one round, as 5 MMAs.  No L plane
+// meets every diagonal, so at K-block 0 the two MMAs that overwrite cover disjoint slots
+// (s = 0: slots 0..3; s = 3, t = 1..3: slots 4..6) and every later MMA accumulates.
+__device__ __forceinline__ void issue_round4(u32 tb, uint64_t da, uint64_t db, bool first_kb) {
+  const u32 ini = first_kb ? 0u : 1u;
+  mma_u8n<0>(tb + 0 * kV, da + 0 * (kPlaneA >> 4), db + 0 * (kPlaneB >> 4), idesc_n(256), ini);
+  mma_u8n<1>(tb + 4 * kV, da + 3 * (kPlaneA >> 4), db + 1 * (kPlaneB >> 4), idesc_n(192), ini);
+  mma_u8n<2>(tb + 3 * kV, da + 3 * (kPlaneA >> 4), db + 0 * (kPlaneB >> 4), idesc_n(64), 1u);
+  mma_u8n<0>(tb + 1 * kV, da + 1 * (kPlaneA >> 4), db + 0 * (kPlaneB >> 4), idesc_n(256), 1u);
+  mma_u8n<0>(tb + 2 * kV, da + 2 * (kPlaneA >> 4), db + 0 * (kPlaneB >> 4), idesc_n(256), 1u);
 }
 
 // digit pair (s, t = d - s) of diagonal slot di exists in round G
@@ -332,6 +346,17 @@ __device__ __forceinline__ u32 prmt(u32 a, u32 b, u32 sel) {
 // each value, value e in byte e = K position) and store them at row `row` of the stage.
 __device__ __forceinline__ void sts32(u32 addr, u32 v) {
   asm volatile("st.shared.b32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+// values < 2^32 (4-digit mode): only the low 4 byte planes
+template <u32 PS>
+__device__ __forceinline__ void store_digits4(u32 planes, const u64 (&x)[4]) {
+  const u32 l0 = lo32(x[0]), l1 = lo32(x[1]), l2 = lo32(x[2]), l3 = lo32(x[3]);
+  const u32 a = prmt(l0, l1, 0x5140), b = prmt(l2, l3, 0x5140);
+  const u32 c = prmt(l0, l1, 0x7362), d = prmt(l2, l3, 0x7362);
+  sts32(planes + 0 * PS, prmt(a, b, 0x5410));
+  sts32(planes + 1 * PS, prmt(a, b, 0x7632));
+  sts32(planes + 2 * PS, prmt(c, d, 0x5410));
+  sts32(planes + 3 * PS, prmt(c, d, 0x7632));
 }
 template <u32 PS>
 __device__ __forceinline__ void store_digits(u32 planes, const u64 (&x)[4]) {
@@ -515,7 +540,7 @@ __device__ __forceinline__ long long clk() { return clock64(); }
 // kRounds x nch units of one piece run at the same time on neighbouring CTAs, so all but the
 // first reader of a K-block's baby-step planes and C records find them in L2.  X mod p is the
 // sum of the rounds' parts (X = sum_g X_g), so each unit reduces its own part into its own
-// partial row (slot = piece slot * kRounds + g) and k_fixup adds them.
+// partial row (slot = piece slot * rounds + g) and k_fixup adds them.
 // The i-th unit of this CTA: units are dealt to the CTAs in snake order (row i of gridDim units
 // left to right for even i, right to left for odd i), so with size-sorted units every CTA gets a
 // large and a small one in turn; ids grow with i, so the first id >= nunits ends the sequence.
@@ -523,8 +548,8 @@ __device__ __forceinline__ u32 unit_id(u32 i) {
   return i * gridDim.x + ((i & 1) ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
 }
 __device__ __forceinline__ void unit_of(const TcArgs& a, u32 unit, uint4& pc, u32& chunk, u32& g) {
-  g = unit % kRounds;
-  const u32 r = unit / kRounds;
+  g = unit % a.rounds;
+  const u32 r = unit / a.rounds;
   chunk = r % a.nch;
   pc = a.piece[r / a.nch];
 }
@@ -567,9 +592,10 @@ __device__ __forceinline__ void load_kblock(const TcArgs& a, const KIter& k, u32
   bulk_g2s(dst + kDataLS, a.C + q * kCRec, kDataSlot - kDataLS, bar);
 }
 
-// WIDE: 2^62 <= p < 2^63 -- the giant-step chains use the exact-quotient Shoup product (output
-// < 2p < 2^64, so every value still has 8 bytes); otherwise the lazy one (output < 4p < 2^64).
-template <bool PROF, bool WIDE>
+// MODE 0: p < 2^62, lazy Shoup chains (values < 4p < 2^64), 8 byte digits, 2 rounds.
+// MODE 1: 2^62 <= p < 2^63, exact-quotient chains (values < 2p < 2^64), 8 digits, 2 rounds.
+// MODE 2: p < 2^31, exact-quotient chains (values < 2p < 2^32), 4 digits, 1 round of 5 MMAs.
+template <bool PROF, int MODE>
 static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 warps: <= 168 regs/thread
   unsigned long long g_entry = 0;
   if (PROF) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
@@ -668,11 +694,13 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
 #pragma unroll 3
         for (int k = 0; k < 15; ++k) {
           // row rr + 8k: the next 8-row core-matrix group, +128 bytes
-          store_digits<kPlaneA>(planes0 + (u32)k * 128u, x);
+          if (MODE == 2) store_digits4<kPlaneA>(planes0 + (u32)k * 128u, x);
+          else store_digits<kPlaneA>(planes0 + (u32)k * 128u, x);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) x[e] = WIDE ? mul_shoup2(x[e], sm[e], sw[e], np) : mul_shoup4(x[e], sm[e], sw[e], np);
+          for (int e = 0; e < 4; ++e) x[e] = MODE ? mul_shoup2(x[e], sm[e], sw[e], np) : mul_shoup4(x[e], sm[e], sw[e], np);
         }
-        store_digits<kPlaneA>(planes0 + 15u * 128u, x);   // last row: no product after it
+        if (MODE == 2) store_digits4<kPlaneA>(planes0 + 15u * 128u, x);   // last row: no product after it
+        else store_digits<kPlaneA>(planes0 + 15u * 128u, x);
       }
       fence_async_smem();
       mbar_arrive(&full[stage]);
@@ -705,7 +733,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       unit_of(a, unit, pc, chunk, g);
       const u32 nkb = uni(pc.y);
       g = uni(g);
-      u64* prow = a.partial + ((u64)pc.z * kRounds + g) * a.ldp;
+      u64* prow = a.partial + ((u64)pc.z * a.rounds + g) * a.ldp;
+      if (MODE == 2) g = 2;   // the 4-digit mode's single round
       u32* raw = raw_cta + (u64)(nunit & 1) * kDiag * (kU * kV);
       if (warp == kMmaWarp) {
         // (this raw buffer was last read two units ago by warps 2 / 3's fold of warp 0's rows;
@@ -731,7 +760,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
               if (g == 0) issue_round<0, true>(tbu, da, db, kb == 0);
               else issue_round<1, true>(tbu, da, db, kb == 0);
             } else if (!(PROF && a.dbg == 1)) {
-              if (g == 0) issue_round_wide<0>(tbu, da, db, kb == 0);
+              if (MODE == 2) issue_round4(tbu, da, db, kb == 0);
+              else if (g == 0) issue_round_wide<0>(tbu, da, db, kb == 0);
               else issue_round_wide<1>(tbu, da, db, kb == 0);
             }
             if (kb + 1 == nkb) mma_commit(&accf);   // accumulators complete after this K-block
@@ -747,7 +777,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       tc_fence_after();
       u32* raw_u = raw + (u64)u * 4;
       const bool st = !(PROF && a.dbg == 3);
-      if (g == 0) epi_drain<0>(tl, raw_u, &acce, st);
+      if (MODE == 2) epi_drain<2>(tl, raw_u, &acce, st);
+      else if (g == 0) epi_drain<0>(tl, raw_u, &acce, st);
       else epi_drain<1>(tl, raw_u, &acce, st);
       if (PROF && warp != kMmaWarp) T[1] += clk() - c1;
       if (PROF) T[3] += 1;
@@ -765,7 +796,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
         }
         const u32* rr_ = raw + (u64)ur * 4;
         const u64 kbase = (u64)chunk * kChunk + (u64)ur * kV;   // multiple of 8; ldp multiple of 8
-        if (g == 0) fold_row<0>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
+        if (MODE == 2) fold_row<2>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
+        else if (g == 0) fold_row<0>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
         else fold_row<1>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
       }
       if (PROF) T[2] += clk() - c2;

@@ -219,3 +219,18 @@ def test_tc_63bit_prime_equals_scalar_step():
     assert np.array_equal(a, b)
     ks = np.array([0, 1, 8191, 8192, 16999], np.uint64)
     assert np.array_equal(a[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
+
+
+def test_tc_31bit_prime_equals_scalar_step():
+    """p < 2^31: exact-quotient chains keep every value below 2^32, so the tensor path uses 4 byte
+    digits (16 pairs, diagonals 0..6, one round of 5 MMAs); equals k_step's 32-bit Shoup path."""
+    w = synth.random_small(570, (1 << 31) - 1, 8, 20_000, 6, 17_000, 3)
+    with pe.Context.from_workload(w) as ctx:
+        assert ctx.uses_tc(w.T)
+        a = ctx.eval(w.j0, w.T)
+    with pe.Context.from_workload(w, path=pe.PATH_INT) as ctx:
+        assert not ctx.uses_tc(w.T)
+        b = ctx.eval(w.j0, w.T)
+    assert np.array_equal(a, b)
+    ks = np.array([0, 1, 8191, 8192, 16999], np.uint64)
+    assert np.array_equal(a[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
