@@ -632,10 +632,12 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
   if (!h->d_tc_scratch) CU(cudaMallocAsync((void**)&h->d_tc_scratch, (size_t)h->n_sm * 2 * tc::kDiag * tc::kChunk * sizeof(u32), s));
   // kernel mode: 0 = lazy chains, 8 digits; 1 = p >= 2^62, exact chains, 8 digits; 2 = p < 2^31,
   // exact chains (values < 2^32), 4 digits, one round
-  const int mode = h->p < (1ull << 31) ? 2 : (h->p >= (1ull << 62) ? 1 : 0);
+  // 3 = 2^31 <= p < 2^54: lazy chains (values < 2^56), 7 digits, two rounds of 12 + 6 MMAs
+  const int mode = h->p < (1ull << 31) ? 2 : h->p < (1ull << 54) ? 3 : (h->p >= (1ull << 62) ? 1 : 0);
   CU(cudaFuncSetAttribute(tc::k_tc<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   CU(cudaFuncSetAttribute(tc::k_tc<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   CU(cudaFuncSetAttribute(tc::k_tc<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
+  CU(cudaFuncSetAttribute(tc::k_tc<false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   CU(cudaFuncSetAttribute(tc::k_tc<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
@@ -683,6 +685,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     if (d_prof && mode == 0) tc::k_tc<true, 0><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
     else if (mode == 1) tc::k_tc<false, 1><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
     else if (mode == 2) tc::k_tc<false, 2><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
+    else if (mode == 3) tc::k_tc<false, 3><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
     else tc::k_tc<false, 0><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
     CU(cudaGetLastError());
     if (d_prof) {

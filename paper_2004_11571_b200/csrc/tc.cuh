@@ -89,8 +89,9 @@ static_assert(kSmemBytes + 256 <= 232448, "shared memory");
 // for one L plane s the round's pairs (s, t) have consecutive t and land in consecutive slots:
 // one wide MMA (B = planes t..t+k-1, N = 64k <= 256) covers k of them
 // group 2: the single round of the 4-digit mode (p < 2^31: values < 2^32), d = 0..6
+// group 4: the 7-digit mode's second round, d = 8..12
 __host__ __device__ constexpr int group_diag(int g, int di) {
-  return g == 0 ? di : g == 1 ? (di < 7 ? 8 + di : -1) : (di < 7 ? di : -1);
+  return g == 0 ? di : g == 1 ? (di < 7 ? 8 + di : -1) : g == 2 ? (di < 7 ? di : -1) : (di < 5 ? 8 + di : -1);
 }
 
 struct TcArgs {
@@ -173,9 +174,13 @@ __device__ __forceinline__ void mma_u8n(u32 dtmem, uint64_t ad, uint64_t bd, u32
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n\t}\n"
                  :: "r"(dtmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
-  else
+  else if (COL == 2)
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}\n"
+                 :: "r"(dtmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+  else
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::use [%0], %1, %2, %3, p;\n\t}\n"
                  :: "r"(dtmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
 }
 __host__ __device__ constexpr u32 idesc_n(int n) {
@@ -225,6 +230,27 @@ __device__ __forceinline__ void issue_round4(u32 tb, uint64_t da, uint64_t db, b
   mma_u8n<0>(tb + 1 * kV, da + 1 * (kPlaneA >> 4), db + 0 * (kPlaneB >> 4), idesc_n(256), 1u);
   mma_u8n<0>(tb + 2 * kV, da + 2 * (kPlaneA >> 4), db + 0 * (kPlaneB >> 4), idesc_n(256), 1u);
 }
+
+// The 7-digit mode (p < 2^54: lazy values < 4p < 2^56): 49 pairs, rounds d = 0..7 (34 pairs, 12
+// MMAs) and d = 8..12 (15 pairs, 6 MMAs).  Round 0 has no L plane meeting all 8 diagonals: the MMAs
+// that overwrite at K-block 0 cover disjoint slots (s=0: 0..3 and 4..6, s=1 t=6: 7); in round 1,
+// s = 6 meets all five and goes first.  Runs of one L plane keep A in the collector.
+#define TC7(COL, S, T0, N, SLOT, ACC) \
+  mma_u8n<COL>(tb + (SLOT) * kV, da + (S) * (kPlaneA >> 4), db + (T0) * (kPlaneB >> 4), idesc_n(N), ACC)
+__device__ __forceinline__ void issue_round7_0(u32 tb, uint64_t da, uint64_t db, bool first_kb) {
+  const u32 ini = first_kb ? 0u : 1u;
+  TC7(1, 0, 0, 256, 0, ini); TC7(2, 0, 4, 192, 4, ini);
+  TC7(1, 1, 6, 64, 7, ini);  TC7(3, 1, 0, 256, 1, 1u); TC7(2, 1, 4, 128, 5, 1u);
+  TC7(1, 2, 0, 256, 2, 1u);  TC7(2, 2, 4, 128, 6, 1u);
+  TC7(1, 3, 0, 256, 3, 1u);  TC7(2, 3, 4, 64, 7, 1u);
+  TC7(0, 4, 0, 256, 4, 1u);  TC7(0, 5, 0, 192, 5, 1u);  TC7(0, 6, 0, 128, 6, 1u);
+}
+__device__ __forceinline__ void issue_round7_1(u32 tb, uint64_t da, uint64_t db, bool first_kb) {
+  const u32 ini = first_kb ? 0u : 1u;
+  TC7(1, 6, 2, 256, 0, ini); TC7(2, 6, 6, 64, 4, ini);
+  TC7(0, 5, 3, 256, 0, 1u);  TC7(0, 4, 4, 192, 0, 1u);  TC7(0, 3, 5, 128, 0, 1u);  TC7(0, 2, 6, 64, 0, 1u);
+}
+#undef TC7
 
 // digit pair (s, t = d - s) of diagonal slot di exists in round G
 __host__ __device__ constexpr bool pair_ok(int G, int di, int sd) {
@@ -595,6 +621,7 @@ __device__ __forceinline__ void load_kblock(const TcArgs& a, const KIter& k, u32
 // MODE 0: p < 2^62, lazy Shoup chains (values < 4p < 2^64), 8 byte digits, 2 rounds.
 // MODE 1: 2^62 <= p < 2^63, exact-quotient chains (values < 2p < 2^64), 8 digits, 2 rounds.
 // MODE 2: p < 2^31, exact-quotient chains (values < 2p < 2^32), 4 digits, 1 round of 5 MMAs.
+// MODE 3: 2^31 <= p < 2^54, lazy chains (values < 4p < 2^56), 7 digits, 2 rounds of 12 + 6 MMAs.
 template <bool PROF, int MODE>
 static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 warps: <= 168 regs/thread
   unsigned long long g_entry = 0;
@@ -697,7 +724,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
           if (MODE == 2) store_digits4<kPlaneA>(planes0 + (u32)k * 128u, x);
           else store_digits<kPlaneA>(planes0 + (u32)k * 128u, x);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) x[e] = MODE ? mul_shoup2(x[e], sm[e], sw[e], np) : mul_shoup4(x[e], sm[e], sw[e], np);
+          for (int e = 0; e < 4; ++e)
+            x[e] = (MODE == 1 || MODE == 2) ? mul_shoup2(x[e], sm[e], sw[e], np) : mul_shoup4(x[e], sm[e], sw[e], np);
         }
         if (MODE == 2) store_digits4<kPlaneA>(planes0 + 15u * 128u, x);   // last row: no product after it
         else store_digits<kPlaneA>(planes0 + 15u * 128u, x);
@@ -761,7 +789,10 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
               else issue_round<1, true>(tbu, da, db, kb == 0);
             } else if (!(PROF && a.dbg == 1)) {
               if (MODE == 2) issue_round4(tbu, da, db, kb == 0);
-              else if (g == 0) issue_round_wide<0>(tbu, da, db, kb == 0);
+              else if (MODE == 3) {
+                if (g == 0) issue_round7_0(tbu, da, db, kb == 0);
+                else issue_round7_1(tbu, da, db, kb == 0);
+              } else if (g == 0) issue_round_wide<0>(tbu, da, db, kb == 0);
               else issue_round_wide<1>(tbu, da, db, kb == 0);
             }
             if (kb + 1 == nkb) mma_commit(&accf);   // accumulators complete after this K-block
@@ -778,6 +809,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       u32* raw_u = raw + (u64)u * 4;
       const bool st = !(PROF && a.dbg == 3);
       if (MODE == 2) epi_drain<2>(tl, raw_u, &acce, st);
+      else if (MODE == 3 && g == 1) epi_drain<4>(tl, raw_u, &acce, st);
       else if (g == 0) epi_drain<0>(tl, raw_u, &acce, st);
       else epi_drain<1>(tl, raw_u, &acce, st);
       if (PROF && warp != kMmaWarp) T[1] += clk() - c1;
@@ -797,6 +829,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
         const u32* rr_ = raw + (u64)ur * 4;
         const u64 kbase = (u64)chunk * kChunk + (u64)ur * kV;   // multiple of 8; ldp multiple of 8
         if (MODE == 2) fold_row<2>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
+        else if (MODE == 3 && g == 1) fold_row<4>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
         else if (g == 0) fold_row<0>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
         else fold_row<1>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
       }

@@ -43,6 +43,8 @@ def check_tc(w, **kw):
     (2**31 - 1, 3, 100, 9, 1, 64),        # n = 3, 31-bit p through the 64-bit tensor path
     ((1 << 50) - 27, 7, 600, 4, 3, 77),   # 50-bit p (auto would take FP64 Alg. 2)
     ((1 << 63) - 25, 6, 700, 4, 5, 300),  # largest supported p: exact-quotient giant-step chains
+    ((1 << 54) - 33, 6, 700, 4, 2, 300),  # largest 7-digit-mode p (lazy values < 4p < 2^56)
+    ((1 << 31) + 11, 6, 700, 4, 2, 300),  # smallest 7-digit-mode p
     ((1 << 62) + 135, 5, 400, 3, 1, 129), # just above 2^62
 ])
 def test_tc_edge_shapes(p, n, t, maxdeg, j0, T):
@@ -233,4 +235,18 @@ def test_tc_31bit_prime_equals_scalar_step():
         b = ctx.eval(w.j0, w.T)
     assert np.array_equal(a, b)
     ks = np.array([0, 1, 8191, 8192, 16999], np.uint64)
+    assert np.array_equal(a[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
+
+
+def test_tc_7digit_mode_equals_scalar_step():
+    """2^31 <= p < 2^54 (here config 4's 2^50 - 27): 7 byte digits, 49 pairs in rounds of 12 + 6
+    MMAs; equals k_step's FP64 Alg. 2 path on a config-4-shaped instance."""
+    w = synth.gen_config(4, t=60_000, T=9000)
+    with pe.Context.from_workload(w, path=pe.PATH_TC) as ctx:
+        a = ctx.eval(w.j0, w.T)
+    with pe.Context.from_workload(w, path=pe.PATH_FP64) as ctx:
+        assert not ctx.uses_tc(w.T)
+        b = ctx.eval(w.j0, w.T)
+    assert np.array_equal(a, b)
+    ks = np.array([0, 1, 8191, 8192, 8999], np.uint64)
     assert np.array_equal(a[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
