@@ -223,9 +223,13 @@ static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStrea
 // costs a flat ~0.11 ms + 0.42 ns per padded term for any T <= 8192, k_step grows with t * T.
 // Measured crossovers (scripts/tc_threshold.py, profiles/r01_tc_threshold.jsonl): T ~ 860 for
 // 10^5 terms, ~480 for 10^6 (k_step INT), 512 vs FP64 Alg. 2 -- i.e. T* ~ 8.6e7 / t_pad, >= 512.
-static u64 tc_min_T(u64 t_pad) {
+// p < 2^31 competes with the 4-IMAD-slot 32-bit Shoup k_step instead: crossovers T ~ 770 (10^6
+// terms) and ~930 (10^5) against k_tc's 4-digit mode (scripts/tc_threshold_p31.py).
+static u64 tc_min_T(u64 t_pad, u64 p) {
+  const u64 tp = std::max<u64>(t_pad, 1);
+  if (p < (1ull << 31)) return std::min<u64>(8192, std::max<u64>(768, 95000000ull / tp));
   if (t_pad >= 500000) return 512;
-  return std::min<u64>(8192, std::max<u64>(512, 86000000ull / std::max<u64>(t_pad, 1)));
+  return std::min<u64>(8192, std::max<u64>(512, 86000000ull / tp));
 }
 
 static unsigned grid_for(u64 n, unsigned block) {
@@ -725,7 +729,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
 }
 
 static bool use_tc(const pe_ctx* h, u64 T) {
-  return h->tc_ok && (h->tc_mode == 2 || (h->tc_mode == 1 && T >= tc_min_T(h->t_pad)));
+  return h->tc_ok && (h->tc_mode == 2 || (h->tc_mode == 1 && T >= tc_min_T(h->t_pad, h->p)));
 }
 
 static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s) {
@@ -870,7 +874,7 @@ extern "C" int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint
   if (!h) return set_err(PE_EINVAL);
   if (mode) *mode = h->tc_ok ? h->tc_mode : 0;
   if (pieces) *pieces = h->tc_npieces;
-  if (min_T) *min_T = h->tc_ok ? (h->tc_mode == 2 ? 1 : tc_min_T(h->t_pad)) : 0;
+  if (min_T) *min_T = h->tc_ok ? (h->tc_mode == 2 ? 1 : tc_min_T(h->t_pad, h->p)) : 0;
   return PE_OK;
 }
 

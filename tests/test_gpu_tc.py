@@ -132,6 +132,10 @@ def test_tc_auto_selection():
     w3 = synth.gen_config(3, t=600_000, T=10)
     with pe.Context.from_workload(w3) as ctx:
         assert ctx.info()["tc_min_T"] == 512 and ctx.uses_tc(512) and not ctx.uses_tc(511)
+    w31 = synth.random_small(527, (1 << 31) - 1, 6, 600_000 // 8, 9, 10, 1)   # p < 2^31: vs 32-bit k_step
+    with pe.Context.from_workload(w31) as ctx:
+        tp = ctx.info()["t_padded"]
+        assert ctx.info()["tc_min_T"] == min(8192, max(768, 95_000_000 // tp))
     with pe.Context.from_workload(w, path=pe.PATH_INT) as ctx:
         assert not ctx.uses_tc(10**6)
     w50 = synth.random_small(525, (1 << 50) - 27, 5, 100, 3, 10, 1)
