@@ -59,12 +59,30 @@ def peaks():
 
 def ncu_traffic(kernel: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from the
-    committed ncu --set full capture of this same bench launch (profiles/r01_<kernel>_summary.json)."""
+    newest committed ncu --set full capture of this same bench launch
+    (profiles/rNN_<kernel>_summary.json), with the file and the commit the capture was taken at.
+    Returns (bytes or None, source dict or None)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{kernel}_summary.json")), reverse=True):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+            return d["traffic_bytes_per_launch"], {"file": os.path.relpath(path, ROOT),
+                                                   "commit": d.get("commit"), "when": d.get("when")}
+        except (OSError, KeyError, ValueError):
+            continue
+    return None, None
+
+
+def cpu_model() -> str:
     try:
-        with open(os.path.join(ROOT, "profiles", f"r01_{kernel}_summary.json")) as f:
-            return json.load(f)["traffic_bytes_per_launch"]
-    except (OSError, KeyError, ValueError):
-        return None
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for l in out.splitlines():
+            if l.startswith("Model name:"):
+                return l.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
 
 
 # ---------------------------------------------------------------- clocks sampling
@@ -129,6 +147,16 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU oracle leg
+def incremental_sample(w, ncols: int):
+    """Time the Alg. 1 incremental checker (oracle/, as it stands) on the first ncols columns of the
+    workload: the fair analogue of the paper's scalar-integer reference."""
+    import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, ncols)
+    return w.t * ncols, time.perf_counter() - t0
+
+
 def oracle_sample(w, ncols: int, seed: int = 0):
     """Time the direct oracle (as it stands) on ncols sampled columns of the workload."""
     import oracle
@@ -167,21 +195,25 @@ def run_reference(args, w, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": workload_config(w, None),
+            "config": workload_config(w),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def workload_config(w, info):
-    cfg = {"workload": w.name, "t": w.t, "n": w.n, "T": w.T, "j0": w.j0, "p": w.p,
-           "term_points_per_step": w.t * w.T,
-           "l2": "inputs larger than L2 (c, m, w: 3 x 8 B x t_padded; partials G x T)"}
-    if info:
-        cfg.update({"path": "tc" if info.get("uses_tc") else info["path"], "R": info["R"], "warps": info["warps"],
-                    "t_padded": info["t_padded"], "n_slots": info["n_slots"], "G": info.get("G"),
-                    "tc_pieces": info.get("tc_pieces")})
-    return cfg
+def workload_config(w):
+    """The workload only (identical in both arms); implementation details go to impl_config."""
+    return {"workload": w.name, "t": w.t, "n": w.n, "T": w.T, "j0": w.j0, "p": w.p,
+            "term_points_per_step": w.t * w.T,
+            "l2": ("inputs larger than L2 (126 MB): the tensor-core step streams 5.2 GB of baby-step "
+                   "planes + 0.8 GB of per-term records per launch (config 5); the scalar step reads "
+                   "c, m, w (3 x 8 B x t_padded)")}
+
+
+def impl_config(info):
+    return {"kernel": "k_tc" if info.get("uses_tc") else "k_step", "scalar_core": info["path"], "R": info["R"],
+            "warps": info["warps"], "t_padded": info["t_padded"], "n_slots": info["n_slots"], "G": info.get("G"),
+            "tc_pieces": info.get("tc_pieces")}
 
 
 # ---------------------------------------------------------------- GPU leg
@@ -195,6 +227,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-cols", type=int, default=0, help="oracle sample columns (0 = 4 x cores)")
+    ap.add_argument("--sustain-s", type=float, default=0.0,
+                    help="also run the device step back to back for this many seconds (power-capped figure)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -298,6 +332,26 @@ def main():
     value = w.t * w.T / (ms * 1e-3)
     clocks = clk.summary(t_load0, t_load1)
 
+    # ---- optional sustained leg: back-to-back steps for >= args.sustain_s seconds (power-capped clock)
+    sustained = None
+    if args.sustain_s > 0:
+        n_s = max(1, int(args.sustain_s * 1e3 / ms))
+        with ClockSampler(local_rank) as clk2:
+            barrier()
+            torch.cuda.synchronize()
+            ts0 = time.time()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            for _ in range(n_s):
+                step()
+            f1.record(stream)
+            torch.cuda.synchronize()
+            ts1 = time.time()
+            time.sleep(0.15)
+        ms_s = max_over_ranks(f0.elapsed_time(f1) / n_s)
+        sustained = {"steps": n_s, "seconds": n_s * ms_s / 1e3, "ms_per_step": ms_s,
+                     "value": w.t * w.T / (ms_s * 1e-3), "clocks": clk2.summary(ts0, ts1)}
+
     # ---- roofline of the dominant kernel (k_tc on the tensor-core path, else k_step)
     pk, pk_kind = peaks()
     n_launch = max(ks["step_launches"], 1)                                 # passes x steps (rank 0)
@@ -314,8 +368,9 @@ def main():
         achieved = ops / (step_ms * 1e-3)
         peak = pk.get("bf16_tflops", 1590.0) * 1e12 * 2            # int8 dense = 2 x bf16 (guide nominal)
         mma = {n: pe.bench_mma(n) for n in (64, 128)}                # same-run tcgen05 i8 issue rate
+        traffic, traffic_src = ncu_traffic("ktc")
         roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": ncu_traffic("ktc"),
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "k_tc (tcgen05.mma kind::i8 M=128 N=64..256 K=32, u8 x u8 -> s32 in TMEM)",
                 "peak_basis": (f"int8 dense tensor ops = 2 x {pk_kind} bf16_tflops "
                                f"{pk.get('bf16_tflops', 1590.0):.1f} (guide nominal ratio 4.5/2.25 PFLOP/s); "
@@ -324,7 +379,7 @@ def main():
                 "mma_n128_ceiling": mma[128] / 1e12, "frac_of_mma_n128_ceiling": achieved / mma[128],
                 "mma_n64_ceiling": mma[64] / 1e12,
                 "term_points_per_s": tp_rate / 1e12,
-                "frac_of_imad_mulmod_roofline": tp_rate / imad_peak,
+                "speedup_vs_imad_mulmod_roofline": tp_rate / imad_peak,
                 "imad_mulmod_roofline": imad_peak / 1e12,
                 "step_ms": step_ms, "fixup_ms": ks["fixup_ms"] / n_launch,
                 "padded_term_points_per_launch": launches_tp, "term_points_per_launch": algo_tp,
@@ -342,9 +397,10 @@ def main():
             k5 = k5_steps / (k5_ms * 1e-3)
         except pe.PEError:
             pass
+        traffic, traffic_src = ncu_traffic("kstep") if info["path"] == "int" else (None, None)
         roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tterm-pt/s",
                 "frac": achieved / peak if peak else None,
-                "traffic": ncu_traffic("kstep") if info["path"] == "int" else None,
+                "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": f"k_step<{info['path']},R={info['R']}>",
                 "peak_basis": (f"IMAD-pipe model (DESIGN.md Roofline): {N_SM} SMs x {sm_mhz:.0f} MHz ({pk_kind} "
                                f"sm_max_mhz) x {IMAD_LANES_PER_CLK_SM} IMAD lanes/clk/SM / {IMAD_SLOTS_PER_TP} "
@@ -429,19 +485,26 @@ def main():
         os.environ.setdefault("OMP_NUM_THREADS", str(cores))
         ncols = args.cpu_cols or 4 * cores
         n_tp, dt, _ = oracle_sample(w, ncols)
-        cpu = {"value": n_tp / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+        inc_cols = max(1, args.cpu_cols or 64)
+        i_tp, i_dt = incremental_sample(w, inc_cols)
+        cpu = {"value": n_tp / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"{w.name}: all {w.t} terms x {ncols} random columns of T={w.T} "
-                         f"(direct definition, OpenMP over columns), {dt:.1f} s"}
+                         f"(direct definition, OpenMP over columns), {dt:.1f} s",
+               "incremental": {"value": i_tp / i_dt, "unit": UNIT, "cores": cores,
+                               "sample": f"Alg. 1 checker (oracle incr_eval, OpenMP over rows): all {w.t} terms x "
+                                         f"the first {inc_cols} columns, {i_dt:.1f} s"}}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-                "config": workload_config(w, info), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": gpu_launches, "clocks": clocks,
+                "config": workload_config(w), "impl_config": impl_config(info), "roofline": roof,
+                "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": gpu_launches, "clocks": clocks, "sustained": sustained,
                 "create_s": create_s,
-                "parallelism": (f"bucket-contiguous term ranges x{world}, NCCL P2P row gather" if term_shard
-                                else f"point-range shards x{world}, NCCL gather")}
+                "parallelism": ("single GPU (no collective)" if world == 1 else
+                                f"bucket-contiguous term ranges x{world}, NCCL P2P row gather + pe_rows_addmod"
+                                if term_shard else f"point-range shards x{world}, NCCL gather + pe_unshard_columns")}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -47,27 +47,30 @@ enum {
   PE_ENOTSUP = -6    /* requested path / option not supported for this p               */
 };
 
-enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_MIX = 3, PE_PATH_INT32 = 4, PE_PATH_TC = 5 };
+enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_INT32 = 4, PE_PATH_TC = 5 };  /* 3: retired */
 /* PE_PATH_TC forces the tensor-core form of the step (any p < 2^63; for 2^62 <= p the giant-step
  * chains use the exact-quotient Shoup product so every value keeps 8 bytes): each bucket's
  * block of T_c = 128 x 64 points is the product L * R of giant-step values c_i m_i^{j_s+64u} and
  * baby-step values m_i^v (the Vandermonde structure M_i(beta^t) = m_i^t, PAPER.md:420-427,
  * 465-478), computed exactly as 64 byte-by-byte int8 tcgen05 MMAs; the baby-step
  * planes are built once per handle (about 530 B per padded term of device memory).
- * PE_PATH_AUTO selects it for any p < 2^63 when T >= 512 (>= 5*10^5 padded terms) or
- * T >= 8.6e7 / t_pad clamped to [512, 8192] (fewer terms) -- pe_tc_info reports the handle's
- * threshold (env PE_TC=0 off, 1 auto, 2 always); PE_PATH_INT never uses it.  Results are
- * bit-identical either way. */
+ * PE_PATH_AUTO selects it for any p < 2^63 once T reaches the handle's measured threshold
+ * (pe_tc_info): for 2^31 <= p, T >= 512 with >= 5*10^5 padded terms, else T >= 8.6e7 / t_pad clamped
+ * to [512, 8192]; for p < 2^31 (against the 32-bit scalar core) T >= 9.5e7 / t_pad clamped to
+ * [768, 8192].  It also needs one 8192-point chunk of partial rows (8 B x pieces x rounds per point)
+ * to fit the partial-buffer cap (env PE_PARTIAL_MB, default 1024), and its handle memory to fit the
+ * device (and env PE_TC_MEM_MB if set): otherwise an automatic handle degrades to the scalar
+ * k_step (same results).  env PE_TC=0 off, 1 auto, 2 always; PE_PATH_INT never uses it.  Results
+ * are bit-identical either way. */
 /* PE_PATH_INT32 is reported by pe_info only: every p < 2^31 (any requested path except FP64)
  * uses 32-bit Shoup products. */
-/* PE_PATH_MIX is reported by pe_info only (env PE_CORE=mix, p < 2^50): half of every lane's
- * chains run FP64 Alg. 2 (FP64 pipe), half integer Shoup (IMAD pipe).  Correct but not faster
- * than pure Alg. 2 on B200 (both are issue-bound), so the automatic path for p < 2^50 is FP64. */
 
 /* Tuning knobs (0 = automatic).  They never change the result (pin P13). */
 typedef struct pe_config {
-  int32_t path;  /* PE_PATH_AUTO: FP64 Alg. 2 if p < 2^50 else INT64 Shoup, in the tensor-core form for
-                    large T (any p < 2^63); PE_PATH_FP64 / PE_PATH_INT / PE_PATH_TC force one.  env PE_PATH=int|fp64, PE_CORE=mix|fp64|hyb|shoup     */
+  int32_t path;  /* PE_PATH_AUTO: scalar core = 32-bit Shoup if p < 2^31, FP64 Alg. 2 if p < 2^50, else
+                    INT64 Shoup; the tensor-core form instead for T >= the handle's threshold (any
+                    p < 2^63).  PE_PATH_FP64 / PE_PATH_INT / PE_PATH_TC force one.
+                    env PE_PATH=int|fp64, PE_CORE=fp64|shoup|int32               */
   int32_t R;     /* terms per lane: 1,2,4,8,16 (FP64: <= 8); auto picks by bucket sizes    */
   int32_t warps; /* warps per CTA, 1..16 (auto 8)                                          */
   int32_t chunk; /* points per CTA (multiple of 32; auto by grid coverage)                 */
@@ -84,7 +87,7 @@ typedef struct pe_config {
  *   alpha   HOST uint64[n-2] (may be NULL iff n == 2), reduced mod p, must be != 0 mod p.
  * Deep-copies everything; the caller may free its arrays on return.
  * Returns NULL on error and sets pe_last_error() (PE_EINVAL / PE_ENOTPRIME / PE_ERANGE /
- * PE_ENOMEM / PE_ECUDA).  Validation happens before any CUDA call.
+ * PE_ENOMEM / PE_ECUDA).  Validation happens before any CUDA call.  t <= 2^31 - 1 (PE_ERANGE).
  */
 pe_ctx* pe_create(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs,
                   const uint32_t* exps, const uint64_t* alpha);
@@ -119,7 +122,10 @@ int pe_eval(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* out);
  * pe_eval_device -- T images into DEVICE memory: d_out[g*ld + k], ld >= T (elements).
  * Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream): returns after
  * enqueueing.  The handle's scratch is reused by the next call on the same handle, so calls
- * on one handle must be stream-ordered (same stream, or synchronised).
+ * on one handle must be stream-ordered (same stream, or synchronised).  Runs on the handle's
+ * device whatever device is current (restored on return).  If an earlier tensor-core launch of
+ * the handle timed out in a pipeline wait (a protocol fault, never a legitimate stall), every
+ * later call returns PE_ECUDA.
  */
 int pe_eval_device(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* d_out, uint64_t ld,
                    void* stream);
@@ -133,19 +139,26 @@ int pe_bucket_exps(const pe_ctx* h, uint32_t* dxdy);        /* HOST uint32[2G]: 
 int pe_info(const pe_ctx* h, int32_t* path, int32_t* R, int32_t* warps, uint64_t* t_padded,
             uint64_t* n_slots);
 
-/* Tensor-core path state: *mode = 0 (not built for this handle), 1 (automatic: used by evaluations
- * with T >= *min_T), 2 (forced, every T); *pieces = accumulation pieces (<= 4096 terms of one
- * bucket each).  Any pointer may be NULL.  Errors: PE_EINVAL (h NULL). */
+/* Tensor-core path state: *mode = 0 (not built for this handle, or degraded for lack of memory), 1
+ * (automatic: used by evaluations with T >= *min_T), 2 (forced, every T); *pieces = accumulation
+ * pieces (<= 8192 terms of one bucket each; env PE_TC_PIECE caps them lower, for tests).  Any
+ * pointer may be NULL.  Errors: PE_EINVAL (h NULL). */
 int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint64_t* min_T);
+
+/* Which hot kernel an evaluation of T points on this handle runs: 0 = the scalar k_step, 1 = the
+ * tensor-core k_tc (the automatic choice: threshold, partial-buffer cap, memory).  PE_EINVAL if h
+ * is NULL. */
+int pe_eval_kernel(const pe_ctx* h, uint64_t T);
 
 /* m_i = prod_l alpha_l^{e_i,l} mod p for every input term i (HOST uint64[t], input order). */
 int pe_monomials(const pe_ctx* h, uint64_t* m);
 
 /*
  * Kernel timing (for bench.py's roofline): when enabled, pe_eval_device records CUDA events
- * on its stream around every k_step (hot loop) and k_fixup launch.  pe_kernel_stats waits for
- * the recorded events, returns the accumulated launch count, device milliseconds of each
- * kernel and the term-points k_step processed (padded terms x points), then resets them.
+ * on its stream around every hot-loop launch (k_step, or k_tc on the tensor-core path) and the
+ * k_fixup that follows it.  pe_kernel_stats waits for the recorded events, returns the
+ * accumulated launch count, device milliseconds of the hot kernel and of k_fixup, and the
+ * term-points processed (padded terms x points), then resets them.
  */
 int pe_set_timing(pe_ctx* h, int enable);
 int pe_kernel_stats(pe_ctx* h, uint64_t* step_launches, double* step_ms, double* fixup_ms,
@@ -166,6 +179,26 @@ int pe_bm_device(uint64_t p, uint64_t G, uint64_t T, const uint64_t* d_seq, uint
                  uint64_t* d_lambda, uint64_t ldl, uint32_t* d_len, void* stream);
 int pe_bm(uint64_t p, uint64_t G, uint64_t T, const uint64_t* seq /*[G*T]*/,
           uint64_t* lambda /*[G*(T+1)]*/, uint32_t* len /*[G]*/);
+
+/*
+ * Multi-GPU assembly (BASELINE.json north_star "sharding ... one gather"), so the
+ * Python plumbing does no modular arithmetic and no per-rank copy loops.  Device pointers,
+ * asynchronous on `stream`.
+ *
+ * pe_rows_addmod -- d_dst[r*ld_dst + k] = (d_dst[r*ld_dst + k] + d_src[r*ld_src + k]) mod p for
+ *   r < rows, k < cols.  Both operands canonical residues in [0, p), 3 <= p < 2^63 (the u64 sum
+ *   cannot wrap).  The root's coefficient reduction of a bucket whose terms two ranks share
+ *   (PAPER.md:489-503 across ranks).  Errors: PE_ERANGE (p), PE_EINVAL (NULL, ld < cols), PE_ECUDA.
+ *
+ * pe_unshard_columns -- point-range shards back into rows: d_blocks is [P][G][Tr] (rank r's
+ *   columns r*Tr .. r*Tr + Tr - 1, the gathered buffer), d_out is [G][ld] with ld >= T;
+ *   d_out[g*ld + r*Tr + k] = d_blocks[(r*G + g)*Tr + k] for r*Tr + k < T.  Errors: PE_EINVAL
+ *   (NULL, ld < T, P*Tr < T), PE_ECUDA.
+ */
+int pe_rows_addmod(uint64_t p, uint64_t* d_dst, uint64_t ld_dst, const uint64_t* d_src, uint64_t ld_src,
+                   uint64_t rows, uint64_t cols, void* stream);
+int pe_unshard_columns(uint64_t* d_out, uint64_t ld, const uint64_t* d_blocks, uint64_t P, uint64_t G,
+                       uint64_t Tr, uint64_t T, void* stream);
 
 int pe_last_error(void);            /* thread-local code of the last failing call */
 const char* pe_strerror(int code);

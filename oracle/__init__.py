@@ -6,7 +6,9 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baselin
 
 * ``oracle.c``  -- the direct definition with ``unsigned
   __int128`` square-and-multiply, OpenMP over points; and ``incr_eval``, Alg. 1
-   as the incremental companion checker.
+   as the incremental companion checker (``incr_eval_blocked``: the same
+  checker with the points cut into blocks, each seeded at its first point, for load balance on
+  Zipf-skewed rows).
 * ``brute.py``  -- Python big-integer literal substitution for tiny inputs.
 
 Pins: tests/test_oracle_pins.py (DESIGN.md "Oracle pins" P1-P13).
@@ -49,6 +51,8 @@ def _load():
         lib.oracle_eval.restype = ctypes.c_int
         lib.incr_eval.argtypes = [u64, u64, u32, vp, vp, vp, u64, u64, vp]
         lib.incr_eval.restype = ctypes.c_int
+        lib.incr_eval_blocked.argtypes = [u64, u64, u32, vp, vp, vp, u64, u64, u64, vp]
+        lib.incr_eval_blocked.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -107,6 +111,19 @@ def eval_incremental(p, n, coeffs, exps, alpha, j0, T) -> np.ndarray:
     out = np.zeros((G, int(T)), np.uint64)
     if G and T:
         rc = _load().incr_eval(p, coeffs.size, n, _ptr(coeffs), _ptr(exps), _ptr(alpha), j0, T, _ptr(out))
+        assert rc == 0
+    return out
+
+
+def eval_incremental_blocked(p, n, coeffs, exps, alpha, j0, T, block=512) -> np.ndarray:
+    """Alg. 1 checker with the points split into blocks (each task seeded at its first point by
+    exponentiation): same values as eval_incremental, balanced over (row, block) tasks."""
+    coeffs, exps, alpha = _prep(coeffs, exps, alpha, n)
+    G = buckets(exps, n).shape[0]
+    out = np.zeros((G, int(T)), np.uint64)
+    if G and T:
+        rc = _load().incr_eval_blocked(p, coeffs.size, n, _ptr(coeffs), _ptr(exps), _ptr(alpha), j0, T, block,
+                                       _ptr(out))
         assert rc == 0
     return out
 

@@ -176,3 +176,68 @@ int incr_eval(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs, const 
     free(start); free(a); free(m);
     return 0;
 }
+
+/*
+ * Same Alg. 1 checker, with the points cut into blocks of `block` columns so that the work
+ * is spread over (row, block) pairs rather than rows alone (a Zipf-skewed config-5 row of
+ * 1.3M terms would otherwise run 16384 points on one thread).  Each (row, block) task seeds its
+ * a-vector at its first point, a_i = c_i * m_i^{j0+k0} -- the seed incr_eval uses at j0, i.e. the
+ * Lambda/Gamma seeding of PAPER.md:559-565 -- then runs Alg. 1 over the block.
+ * Only the task split differs from incr_eval; the arithmetic per point is the same.
+ */
+int incr_eval_blocked(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs, const uint32_t* exps,
+                      const uint64_t* alpha, uint64_t j0, uint64_t T, uint64_t block, uint64_t* out) {
+    if (p < 2 || n < 2 || block == 0) return -1;
+    uint64_t* keys;
+    uint64_t* row = (uint64_t*)malloc((t ? t : 1) * sizeof(uint64_t));
+    uint64_t G = build_rows(t, n, exps, &keys, row);
+    free(keys);
+    uint64_t* start = (uint64_t*)calloc(G + 1, sizeof(uint64_t));
+    for (uint64_t i = 0; i < t; ++i) start[row[i] + 1]++;
+    for (uint64_t g = 0; g < G; ++g) start[g + 1] += start[g];
+    uint64_t* fill = (uint64_t*)malloc((G + 1) * sizeof(uint64_t));
+    memcpy(fill, start, (G + 1) * sizeof(uint64_t));
+    uint64_t* c = (uint64_t*)malloc((t ? t : 1) * sizeof(uint64_t));
+    uint64_t* m = (uint64_t*)malloc((t ? t : 1) * sizeof(uint64_t));
+    for (uint64_t i = 0; i < t; ++i) {                 /* m_i = prod_l alpha_l^{e_il} */
+        uint64_t mi = 1 % p;
+        for (uint32_t l = 0; l + 2 < n; ++l) mi = mulmod(mi, oracle_powmod(alpha[l], exps[i * n + 2 + l], p), p);
+        uint64_t pos = fill[row[i]]++;
+        m[pos] = mi;
+        c[pos] = coeffs[i] % p;
+    }
+    free(fill);
+    free(row);
+    const uint64_t nb = (T + block - 1) / block;
+    int fail = 0;
+#pragma omp parallel
+    {
+        uint64_t cap = 0;
+        uint64_t* a = NULL;
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t task = 0; task < (int64_t)(G * nb); ++task) {
+            const uint64_t g = (uint64_t)task / nb, b = (uint64_t)task % nb;
+            const uint64_t k0 = b * block, k1 = k0 + block < T ? k0 + block : T;
+            const uint64_t s0 = start[g], len = start[g + 1] - s0;
+            if (len > cap) {
+                free(a);
+                cap = len;
+                a = (uint64_t*)malloc(cap * sizeof(uint64_t));
+                if (!a) { fail = 1; cap = 0; continue; }
+            }
+            for (uint64_t i = 0; i < len; ++i)         /* a_i = c_i m_i^{j0 + k0} */
+                a[i] = mulmod(c[s0 + i], oracle_powmod(m[s0 + i], j0 + k0, p), p);
+            for (uint64_t k = k0; k < k1; ++k) {
+                uint64_t acc = 0;
+                for (uint64_t i = 0; i < len; ++i) {
+                    acc = addmod(acc, a[i], p);        /* c <- c (+) a[j] */
+                    a[i] = mulmod(a[i], m[s0 + i], p); /* a[j] <- a[j] (x) m[j] */
+                }
+                out[g * T + k] = acc;
+            }
+        }
+        free(a);
+    }
+    free(start); free(c); free(m);
+    return fail ? -2 : 0;
+}

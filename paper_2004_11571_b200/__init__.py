@@ -18,16 +18,20 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libpe.so")
+TEST_LIB_PATH = os.path.join(_PKG, "libpe_test.so")   # include/pe_test.h: probes, not the product
 
 PE_OK, PE_EINVAL, PE_ENOTPRIME, PE_ERANGE, PE_ENOMEM, PE_ECUDA, PE_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
-PATH_AUTO, PATH_INT, PATH_FP64, PATH_MIX, PATH_INT32, PATH_TC = 0, 1, 2, 3, 4, 5
+PATH_AUTO, PATH_INT, PATH_FP64, PATH_INT32, PATH_TC = 0, 1, 2, 4, 5
 CORE_SHOUP4, CORE_SHOUP2, CORE_MONT, CORE_FP64, CORE_FP64ADD, CORE_POW, CORE_SHOUP4RAW, CORE_HYB, CORE_HYBRAW = range(9)
 
-#: every symbol include/pe.h and include/pe_test.h declare
+#: every symbol include/pe.h declares (libpe.so)
 EXPORTS = ["pe_create", "pe_create_ex", "pe_eval", "pe_eval_device", "pe_destroy", "pe_num_buckets",
            "pe_bucket_exps", "pe_info", "pe_monomials", "pe_last_error", "pe_strerror",
-           "pe_interp_bound_ok", "pe_test_core", "pe_bench_core", "pe_set_timing", "pe_kernel_stats",
-           "pe_create_batch", "pe_num_polys", "pe_poly_rows", "pe_bm_device", "pe_bm", "pe_tc_info", "pe_bench_mma"]
+           "pe_interp_bound_ok", "pe_set_timing", "pe_kernel_stats",
+           "pe_create_batch", "pe_num_polys", "pe_poly_rows", "pe_bm_device", "pe_bm", "pe_tc_info",
+           "pe_rows_addmod", "pe_unshard_columns", "pe_eval_kernel"]
+#: every symbol include/pe_test.h declares (libpe_test.so)
+TEST_EXPORTS = ["pe_test_core", "pe_bench_core", "pe_bench_mma"]
 
 
 class PEError(RuntimeError):
@@ -78,12 +82,6 @@ def lib():
         L.pe_strerror.restype = ctypes.c_char_p
         L.pe_interp_bound_ok.argtypes = [u64, u64]
         L.pe_interp_bound_ok.restype = ctypes.c_int
-        L.pe_test_core.argtypes = [ctypes.c_int, u64, u64, vp, vp, vp, vp]
-        L.pe_test_core.restype = ctypes.c_int
-        L.pe_bench_core.argtypes = [ctypes.c_int, u64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                    ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double),
-                                    ctypes.POINTER(ctypes.c_double)]
-        L.pe_bench_core.restype = ctypes.c_int
         L.pe_set_timing.argtypes = [vp, ctypes.c_int]
         L.pe_set_timing.restype = ctypes.c_int
         L.pe_kernel_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double),
@@ -101,11 +99,38 @@ def lib():
         L.pe_bm.restype = ctypes.c_int
         L.pe_tc_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(u64), ctypes.POINTER(u64)]
         L.pe_tc_info.restype = ctypes.c_int
+        L.pe_eval_kernel.argtypes = [vp, u64]
+        L.pe_eval_kernel.restype = ctypes.c_int
+        L.pe_rows_addmod.argtypes = [u64, vp, u64, vp, u64, u64, u64, vp]
+        L.pe_rows_addmod.restype = ctypes.c_int
+        L.pe_unshard_columns.argtypes = [vp, u64, vp, u64, u64, u64, u64, vp]
+        L.pe_unshard_columns.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+_test_lib = None
+
+
+def test_lib():
+    """Load libpe_test.so (include/pe_test.h: modular-core probes, roofline microbenchmarks)."""
+    global _test_lib
+    if _test_lib is None:
+        if not os.path.exists(TEST_LIB_PATH):
+            raise RuntimeError(f"{TEST_LIB_PATH} missing: run `python -m paper_2004_11571_b200.build`")
+        L = ctypes.CDLL(TEST_LIB_PATH)
+        u64, vp = ctypes.c_uint64, ctypes.c_void_p
+        L.pe_test_core.argtypes = [ctypes.c_int, u64, u64, vp, vp, vp, vp]
+        L.pe_test_core.restype = ctypes.c_int
+        L.pe_bench_core.argtypes = [ctypes.c_int, u64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_double)]
+        L.pe_bench_core.restype = ctypes.c_int
         L.pe_bench_mma.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_float),
                                    ctypes.POINTER(ctypes.c_double)]
         L.pe_bench_mma.restype = ctypes.c_int
-        _lib = L
-    return _lib
+        _test_lib = L
+    return _test_lib
 
 
 def _ptr(a):
@@ -197,7 +222,7 @@ class Context:
         tp, ns = ctypes.c_uint64(), ctypes.c_uint64()
         _check(lib().pe_info(self._h, ctypes.byref(path), ctypes.byref(R), ctypes.byref(W), ctypes.byref(tp),
                              ctypes.byref(ns)), "pe_info")
-        name = {PATH_FP64: "fp64", PATH_MIX: "mix", PATH_INT32: "int32"}.get(path.value, "int")
+        name = {PATH_FP64: "fp64", PATH_INT32: "int32"}.get(path.value, "int")
         mode, pieces, min_t = ctypes.c_int32(), ctypes.c_uint64(), ctypes.c_uint64()
         _check(lib().pe_tc_info(self._h, ctypes.byref(mode), ctypes.byref(pieces), ctypes.byref(min_t)),
                "pe_tc_info")
@@ -205,10 +230,16 @@ class Context:
                 "t_padded": tp.value, "n_slots": ns.value,
                 "tc_mode": mode.value, "tc_pieces": pieces.value, "tc_min_T": min_t.value}
 
+    def eval_kernel(self, T: int) -> str:
+        """Hot kernel an evaluation of T points runs (pe_eval_kernel): "k_step" or "k_tc"."""
+        k = lib().pe_eval_kernel(self._h, T)
+        if k < 0:
+            raise PEError(k, "pe_eval_kernel")
+        return {0: "k_step", 1: "k_tc"}[k]
+
     def uses_tc(self, T: int) -> bool:
         """True if an evaluation of T points runs the tensor-core kernel (PE_PATH_TC / auto)."""
-        i = self.info()
-        return i["tc_mode"] != 0 and T >= i["tc_min_T"]
+        return self.eval_kernel(T) == "k_tc"
 
     def monomials(self) -> np.ndarray:
         out = np.zeros(self.t, np.uint64)
@@ -243,13 +274,13 @@ def test_core(variant: int, p: int, a, b, extra=None) -> np.ndarray:
     b = np.ascontiguousarray(b, dtype=np.uint64)
     out = np.zeros(a.size, np.uint64)
     x = None if extra is None else np.ascontiguousarray(extra, dtype=np.uint64)
-    _check(lib().pe_test_core(variant, p, a.size, _ptr(a), _ptr(b), _ptr(x), _ptr(out)), "pe_test_core")
+    _check(test_lib().pe_test_core(variant, p, a.size, _ptr(a), _ptr(b), _ptr(x), _ptr(out)), "pe_test_core")
     return out
 
 
 def bench_core(variant: int, p: int, R: int, blocks: int, threads: int, iters: int):
     ms, steps, cyc = ctypes.c_float(), ctypes.c_double(), ctypes.c_double()
-    _check(lib().pe_bench_core(variant, p, R, blocks, threads, iters, ctypes.byref(ms), ctypes.byref(steps),
+    _check(test_lib().pe_bench_core(variant, p, R, blocks, threads, iters, ctypes.byref(ms), ctypes.byref(steps),
                                ctypes.byref(cyc)), "pe_bench_core")
     return ms.value, steps.value, cyc.value
 
@@ -257,7 +288,7 @@ def bench_core(variant: int, p: int, R: int, blocks: int, threads: int, iters: i
 def bench_mma(N: int = 128, iters: int = 20000):
     """pe_bench_mma: int8 tcgen05 MMA rate (M=128, N, K=32) -> int8 ops/s (2 per MAC)."""
     ms, macs = ctypes.c_float(), ctypes.c_double()
-    _check(lib().pe_bench_mma(N, iters, ctypes.byref(ms), ctypes.byref(macs)), "pe_bench_mma")
+    _check(test_lib().pe_bench_mma(N, iters, ctypes.byref(ms), ctypes.byref(macs)), "pe_bench_mma")
     return 2 * macs.value / (ms.value * 1e-3)
 
 
@@ -273,3 +304,15 @@ def berlekamp_massey(p: int, seq: np.ndarray):
 
 def interp_bound_ok(p: int, t: int) -> bool:
     return bool(lib().pe_interp_bound_ok(p, t))
+
+
+def rows_addmod(p: int, d_dst: int, ld_dst: int, d_src: int, ld_src: int, rows: int, cols: int, stream: int = 0):
+    """pe_rows_addmod on device pointers: dst = (dst + src) mod p, element-wise over rows x cols."""
+    _check(lib().pe_rows_addmod(p, ctypes.c_void_p(d_dst), ld_dst, ctypes.c_void_p(d_src), ld_src, rows, cols,
+                                ctypes.c_void_p(stream)), "pe_rows_addmod")
+
+
+def unshard_columns(d_out: int, ld: int, d_blocks: int, P: int, G: int, Tr: int, T: int, stream: int = 0):
+    """pe_unshard_columns: [P][G][Tr] point-range blocks -> rows of [G][ld]."""
+    _check(lib().pe_unshard_columns(ctypes.c_void_p(d_out), ld, ctypes.c_void_p(d_blocks), P, G, Tr, T,
+                                    ctypes.c_void_p(stream)), "pe_unshard_columns")

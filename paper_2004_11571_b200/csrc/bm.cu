@@ -126,39 +126,53 @@ ModParams bm_params(u64 p) {
   mp.r2 = (u64)(((u128)mp.r1 * mp.r1) % p);
   mp.pd = (double)p;
   mp.u = 1.0 / (double)p;
-  mp.hc = hyb_C(p);
   return mp;
 }
 
 }  // namespace
 
+namespace pe {
+int set_last_error(int e);   // pe.cu: thread-local code read by pe_last_error
+}
+
 extern "C" int pe_bm_device(uint64_t p, uint64_t G, uint64_t T, const uint64_t* d_seq, uint64_t ld,
                             uint64_t* d_lambda, uint64_t ldl, uint32_t* d_len, void* stream) {
-  if (p < 3 || p >= (1ull << 63) || (p & 1) == 0) return PE_ERANGE;
+  set_last_error(PE_OK);
+  if (p < 3 || p >= (1ull << 63) || (p & 1) == 0) return set_last_error(PE_ERANGE);
   if (G == 0 || T == 0) return PE_OK;
   if (!d_seq || !d_lambda || !d_len || ld < T || ldl < T + 1 || T >= 0xffffffffull || G >= 0x7fffffffull)
-    return PE_EINVAL;
+    return set_last_error(PE_EINVAL);
   cudaStream_t s = (cudaStream_t)stream;
   u64* scratch = nullptr;
-  if (cudaMallocAsync((void**)&scratch, G * 3 * (T + 1) * sizeof(u64), s) != cudaSuccess) return PE_ENOMEM;
+  if (cudaMallocAsync((void**)&scratch, G * 3 * (T + 1) * sizeof(u64), s) != cudaSuccess) {
+    cudaGetLastError();
+    return set_last_error(PE_ENOMEM);
+  }
   k_bm<<<(unsigned)G, 256, 0, s>>>(d_seq, ld, (u32)T, d_lambda, ldl, d_len, scratch, bm_params(p));
   cudaError_t e = cudaGetLastError();
   cudaFreeAsync(scratch, s);
-  return e == cudaSuccess ? PE_OK : PE_ECUDA;
+  return e == cudaSuccess ? PE_OK : set_last_error(PE_ECUDA);
 }
 
 extern "C" int pe_bm(uint64_t p, uint64_t G, uint64_t T, const uint64_t* seq, uint64_t* lambda, uint32_t* len) {
+  set_last_error(PE_OK);
   if (G == 0 || T == 0) return PE_OK;
-  if (!seq || !lambda || !len) return PE_EINVAL;
-  u64 *ds, *dl;
-  u32* dn;
-  if (cudaMalloc(&ds, G * T * 8) || cudaMalloc(&dl, G * (T + 1) * 8) || cudaMalloc(&dn, G * 4)) return PE_ENOMEM;
+  if (!seq || !lambda || !len) return set_last_error(PE_EINVAL);
+  u64 *ds = nullptr, *dl = nullptr;
+  u32* dn = nullptr;
   int rc = PE_OK;
-  if (cudaMemcpy(ds, seq, G * T * 8, cudaMemcpyHostToDevice) != cudaSuccess) rc = PE_ECUDA;
+  if (cudaMalloc(&ds, G * T * 8) != cudaSuccess || cudaMalloc(&dl, G * (T + 1) * 8) != cudaSuccess ||
+      cudaMalloc(&dn, G * 4) != cudaSuccess) {
+    cudaGetLastError();
+    rc = PE_ENOMEM;
+  }
+  if (rc == PE_OK && cudaMemcpy(ds, seq, G * T * 8, cudaMemcpyHostToDevice) != cudaSuccess) rc = PE_ECUDA;
   if (rc == PE_OK) rc = pe_bm_device(p, G, T, ds, T, dl, T + 1, dn, nullptr);
   if (rc == PE_OK && (cudaMemcpy(lambda, dl, G * (T + 1) * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
                       cudaMemcpy(len, dn, G * 4, cudaMemcpyDeviceToHost) != cudaSuccess))
     rc = PE_ECUDA;
-  cudaFree(ds); cudaFree(dl); cudaFree(dn);
-  return rc;
+  if (ds) cudaFree(ds);   // also on the failure paths: no partial allocation leaks
+  if (dl) cudaFree(dl);
+  if (dn) cudaFree(dn);
+  return rc == PE_OK ? PE_OK : set_last_error(rc);
 }

@@ -15,12 +15,12 @@ namespace pe {
 constexpr int kMaxWarps = 16;
 constexpr int kSuper = 32;   // points per shared-memory super-group (one lane per point)
 
-enum PathKind { kInt4 = 0, kInt2 = 1, kFp64 = 2, kHyb = 3, kMix = 4, kInt32 = 5 };
-// kMix (p < 2^50): in every lane, chains r < R/2 run Alg. 2 on the FP64 pipe and chains
-// r >= R/2 run the Shoup-lazy product on the IMAD pipe, so both multiplier pipes work at once.
+// Scalar cores of k_step (the hybrid FP64-quotient and the mixed FP64/IMAD variants measured in
+// round 1 were not faster and live only in the test library, csrc/probe.cu).
+enum PathKind { kInt4 = 0, kInt2 = 1, kFp64 = 2, kInt32 = 5 };
 // Max threads per CTA of k_step<PATH, R> (register budget: 65536 / threads per thread).
 __host__ __device__ constexpr int step_max_threads(int path, int R) {
-  return (R >= 16 || (path == kHyb && R >= 8)) ? 256 : 512;
+  return R >= 16 ? 256 : 512;
 }
 
 // ---------------------------------------------------------------- 96-bit accumulators
@@ -182,7 +182,6 @@ static __global__ void k_setup(const u32* __restrict__ exps, const u64* __restri
                         const u64* __restrict__ bstart, u32 G, u64 t_pad,
                         const u64* __restrict__ table, u32 D, const u64* __restrict__ alpha,
                         u64* __restrict__ c_out, u64* __restrict__ m_out, u64* __restrict__ w_out,
-                        u64* __restrict__ ms_out, double* __restrict__ mp_out, double* __restrict__ msp_out,
                         u32* __restrict__ perm_out, ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
     // bucket g: poff[g] <= q < poff[g+1]
@@ -216,12 +215,6 @@ static __global__ void k_setup(const u32* __restrict__ exps, const u64* __restri
     c_out[q] = c;
     m_out[q] = m;
     w_out[q] = shoup_w(m, mp.p);
-    if (ms_out) {  // mul_hyb constants: ms = m 2^32 mod p, mp = m/p, msp = ms/p (rel. error <= 3u)
-      const u64 ms = mulmod(m, (u64)(((unsigned __int128)1 << 32) % mp.p), mp);
-      ms_out[q] = ms;
-      mp_out[q] = __ddiv_rn(__ull2double_rn(m), __ull2double_rn(mp.p));
-      msp_out[q] = __ddiv_rn(__ull2double_rn(ms), __ull2double_rn(mp.p));
-    }
     perm_out[q] = src;
   }
 }
@@ -239,9 +232,6 @@ struct StepArgs {
   const u64* c;          // [t_pad] reduced coefficients (tile layout)
   const u64* m;          // [t_pad] m_i
   const u64* w;          // [t_pad] floor(m_i 2^64 / p)           (Shoup paths)
-  const u64* ms;         // [t_pad] m_i 2^32 mod p                 (hybrid path)
-  const double* mpd;     // [t_pad] RN(m_i / p)                    (hybrid path)
-  const double* mspd;    // [t_pad] RN(ms_i / p)                   (hybrid path)
   const uint2* wt_info;  // [n_wt] x = partial slot, y = run length if run leader else 0
   u64* partial;          // [n_slots][ldp]
   u64 ldp;               // leading dimension of partial (points of this pass)
@@ -280,7 +270,7 @@ k_step(StepArgs args) {
   // ---- load the lane's R terms and seed a_r = c_r * m_r^{js} (each
   //      independent chain seeded by exponentiation)
   u64 a[R], m[R], w[R];
-  double ad[R], md[R];   // FP64 path: a, m;  hybrid path: mp, msp
+  double ad[R], md[R];   // FP64 path: a, m
   u32 a32[R], m32[R], w32[R];   // kInt32 path
   uint2 info = make_uint2(0, 0);
   if (active) {
@@ -292,10 +282,8 @@ k_step(StepArgs args) {
       const u64 c = __ldg(args.c + q);
       m[r] = __ldg(args.m + q);
       a[r] = seed_pow(c, m[r], js, mp);
-      const bool fp_chain = PATH == kFp64 || (PATH == kMix && r < R / 2);
-      if (fp_chain) { ad[r] = (double)a[r]; md[r] = (double)m[r]; }
-      if (PATH == kHyb) { w[r] = __ldg(args.ms + q); md[r] = __ldg(args.mpd + q); ad[r] = __ldg(args.mspd + q); }
-      if (PATH == kInt4 || PATH == kInt2 || (PATH == kMix && r >= R / 2)) w[r] = __ldg(args.w + q);
+      if (PATH == kFp64) { ad[r] = (double)a[r]; md[r] = (double)m[r]; }
+      if (PATH == kInt4 || PATH == kInt2) w[r] = __ldg(args.w + q);
       if (PATH == kInt32) { a32[r] = (u32)a[r]; m32[r] = (u32)m[r]; w32[r] = hi32(__ldg(args.w + q)); }
     }
   }
@@ -325,20 +313,6 @@ k_step(StepArgs args) {
             const u32 p32 = (u32)mp.p;
 #pragma unroll
             for (int r = 0; r < R; ++r) a32[r] = mul_shoup32(a32[r], m32[r], w32[r], p32);
-          } else if (PATH == kMix) {
-            constexpr int RF = R / 2;
-            double fs = ad[0];
-#pragma unroll
-            for (int r = 1; r < RF; ++r) fs = __dadd_rn(fs, ad[r]);          // exact: RF*p < 2^52
-            // fs < 2^52 is an integer: bits(2^52 + fs) = 0x4330000000000000 | fs
-            const u64 fb = (u64)__double_as_longlong(__dadd_rn(fs, 4503599627370496.0)) & 0x000fffffffffffffull;
-            set96_sum(acc[k], fb, a[RF]);
-#pragma unroll
-            for (int r = RF + 1; r < R; ++r) add96_64(acc[k], a[r]);
-#pragma unroll
-            for (int r = 0; r < RF; ++r) ad[r] = mul_fp(ad[r], md[r], mp.pd, mp.u);
-#pragma unroll
-            for (int r = RF; r < R; ++r) a[r] = mul_shoup4(a[r], m[r], w[r], mp.np);
           } else {
             if (R == 1) {
               acc[k].w0 = lo32(a[0]); acc[k].w1 = hi32(a[0]); acc[k].w2 = 0;
@@ -349,9 +323,7 @@ k_step(StepArgs args) {
             for (int r = 2; r < R; ++r) add96_64(acc[k], a[r]);
 #pragma unroll
             for (int r = 0; r < R; ++r)
-              a[r] = PATH == kHyb ? mul_hyb(a[r], m[r], w[r], md[r], ad[r], mp.np, mp.hc)
-                     : PATH == kInt4 ? mul_shoup4(a[r], m[r], w[r], mp.np)
-                                     : mul_shoup2(a[r], m[r], w[r], mp.np);
+              a[r] = PATH == kInt4 ? mul_shoup4(a[r], m[r], w[r], mp.np) : mul_shoup2(a[r], m[r], w[r], mp.np);
           }
         }
         const U96 tot = (PATH == kFp64 || PATH == kInt32) ? xpose_reduce8<2>(acc, lane)
@@ -388,6 +360,19 @@ static __global__ void k_fixup(const u64* __restrict__ partial, u64 ldp, const u
     hi += (lo < v);
   }
   out[(u64)g * ld + k] = reduce128(hi, lo, mp);
+}
+
+// Multi-GPU assembly (pe_rows_addmod): dst[r][k] = (dst[r][k] + src[r][k]) mod p for canonical
+// residues (< p < 2^63, so the u64 sum cannot wrap) -- the root's sum of a bucket split between
+// two term ranges, i.e. the coefficient reduction of PAPER.md:489-503 across ranks.
+static __global__ void k_rows_addmod(u64* __restrict__ dst, u64 ldd, const u64* __restrict__ src, u64 lds, u64 rows,
+                                     u64 cols, u64 p) {
+  const u64 n = rows * cols;
+  for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < n; x += (u64)gridDim.x * blockDim.x) {
+    const u64 r = x / cols, k = x - r * cols;
+    const u64 s = dst[r * ldd + k] + src[r * lds + k];
+    dst[r * ldd + k] = s >= p ? s - p : s;
+  }
 }
 
 }  // namespace pe

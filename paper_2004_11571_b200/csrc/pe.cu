@@ -28,6 +28,9 @@ using namespace pe;
 // ---------------------------------------------------------------- errors
 static thread_local int g_last_error = PE_OK;
 static int set_err(int e) { g_last_error = e; return e; }
+namespace pe {
+int set_last_error(int e) { return set_err(e); }   // bm.cu's calls report through pe_last_error too
+}
 
 #define CU(call)                                                                  \
   do {                                                                            \
@@ -87,7 +90,6 @@ static ModParams h_mod_params(u64 p) {
   mp.r2 = h_mulmod(mp.r1, mp.r1, p);
   mp.pd = (double)p;
   mp.u = 1.0 / (double)p;  // RN(1/p) (host IEEE division, default rounding)
-  mp.hc = hyb_C(p);
   return mp;
 }
 
@@ -106,8 +108,7 @@ struct pe_ctx {
   std::vector<u64> poly_off{0, 0};   // term offsets of the batched polynomials [npoly+1]
   std::vector<u64> poly_rows{0, 0};  // first output row of each polynomial [npoly+1]
   // device
-  u64 *d_c = nullptr, *d_m = nullptr, *d_w = nullptr, *d_ms = nullptr;
-  double *d_mpd = nullptr, *d_mspd = nullptr;
+  u64 *d_c = nullptr, *d_m = nullptr, *d_w = nullptr;
   u32* d_perm = nullptr;
   uint2* d_wt_info = nullptr;
   u32* d_slot_start = nullptr;
@@ -128,6 +129,7 @@ struct pe_ctx {
   u64* d_seed = nullptr;
   size_t seed_elems = 0;
   u32* d_tc_scratch = nullptr;   // k_tc per-CTA drained diagonal sums (n_sm x 2 x kDiag x kChunk u32)
+  u32* h_status = nullptr;       // mapped host word: k_tc sets it when a pipeline wait times out
   size_t partial_cap_bytes = (size_t)1 << 30;
   cudaStream_t copy_stream = nullptr;   // pe_eval: device->host copy of a column block
   cudaEvent_t copy_done = nullptr;
@@ -147,8 +149,7 @@ static void free_all(pe_ctx* h) {
   drop_recs(h);
   // stream-ordered frees back into the (retained) device memory pool
   cudaStream_t s = h->stream;
-  for (void* q : {(void*)h->d_c, (void*)h->d_m, (void*)h->d_w, (void*)h->d_perm, (void*)h->d_ms, (void*)h->d_mpd,
-                  (void*)h->d_mspd, (void*)h->d_wt_info, (void*)h->d_slot_start, (void*)h->d_partial,
+  for (void* q : {(void*)h->d_c, (void*)h->d_m, (void*)h->d_w, (void*)h->d_perm, (void*)h->d_wt_info, (void*)h->d_slot_start, (void*)h->d_partial,
                   (void*)h->d_out_scratch, (void*)h->d_tcC, (void*)h->d_tcR, (void*)h->d_tcMS,
                   (void*)h->d_tc_scratch, (void*)h->d_piece, (void*)h->d_tc_slot_start,
                   (void*)h->d_seed})
@@ -156,6 +157,7 @@ static void free_all(pe_ctx* h) {
   if (s) cudaStreamSynchronize(s);
   if (h->copy_stream) cudaStreamSynchronize(h->copy_stream), cudaStreamDestroy(h->copy_stream);
   if (h->copy_done) cudaEventDestroy(h->copy_done);
+  if (h->h_status) cudaFreeHost(h->h_status);
   if (h->stream) cudaStreamDestroy(h->stream);
 }
 
@@ -203,16 +205,6 @@ static cudaError_t launch_step_path(int R, dim3 grid, dim3 block, cudaStream_t s
   return cudaGetLastError();
 }
 static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStream_t s, const StepArgs& a) {
-  if (path == kMix) {
-    switch (R) {
-      case 2: k_step<kMix, 2><<<grid, block, 0, s>>>(a); break;
-      case 4: k_step<kMix, 4><<<grid, block, 0, s>>>(a); break;
-      case 8: k_step<kMix, 8><<<grid, block, 0, s>>>(a); break;
-      default: return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
-  }
-  if (path == kHyb) return launch_step_path<kHyb>(R, grid, block, s, a);
   if (path == kInt32) return launch_step_path<kInt32>(R, grid, block, s, a);
   if (path == kInt4) return launch_step_path<kInt4>(R, grid, block, s, a);
   if (path == kInt2) return launch_step_path<kInt2>(R, grid, block, s, a);
@@ -252,7 +244,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
     h->G = 0;
     return PE_OK;
   }
-  if (t >= 0xffffffffull) return set_err(PE_ERANGE);
+  if (t > 0x7fffffffull) return set_err(PE_ERANGE);   // CUB sort / select take int num_items
 
   // ---- upload (a1)
   u64* d_coeffs; u32* d_exps; u64* d_alpha;
@@ -350,7 +342,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   for (u32 k = npoly; k-- > 0;) h->poly_rows[k] = std::min(h->poly_rows[k], h->poly_rows[k + 1]);
 
   // ---- host tile plan from the G bucket sizes
-  const int maxR = (h->path == kFp64 || h->path == kMix) ? 8 : 16;
+  const int maxR = h->path == kFp64 ? 8 : 16;
   int R = h->R;
   if (R == 0) {
     // largest R whose per-bucket padding wastes <= 6% of the terms (and R <= 8 by default)
@@ -363,7 +355,6 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   }
   if (R != 1 && R != 2 && R != 4 && R != 8 && R != 16) return set_err(PE_EINVAL);
   if (R > maxR) return set_err(PE_ENOTSUP);
-  if (h->path == kMix && R == 1) h->path = kFp64;   // a single chain cannot be split
   if (32 * h->W > step_max_threads(h->path, R)) return set_err(PE_EINVAL);
   h->R = R;
   const u64 tile = 32ull * R;
@@ -413,15 +404,12 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   tmp.v.insert(tmp.v.end(), {d_poff, d_bstart});
   CU(cudaMemcpyAsync(d_poff, poff.data(), (G + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(d_bstart, bstart.data(), (G + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
-  if (h->path == kHyb &&  // hybrid-core constants only when that core runs
-      (dalloc(&h->d_ms, h->t_pad) || dalloc(&h->d_mpd, h->t_pad) || dalloc(&h->d_mspd, h->t_pad)))
-    return g_last_error;
   if (dalloc(&h->d_c, h->t_pad) || dalloc(&h->d_m, h->t_pad) || dalloc(&h->d_w, h->t_pad) ||
       dalloc(&h->d_perm, h->t_pad) || dalloc(&h->d_wt_info, n_wt) || dalloc(&h->d_slot_start, G + 1))
     return g_last_error;
   k_setup<<<grid_for(h->t_pad, 256), 256, 0, s>>>(d_exps, d_coeffs, n, d_idxS, d_poff, d_bstart, (u32)G,
                                                    h->t_pad, d_table, D, d_alpha, h->d_c, h->d_m, h->d_w,
-                                                   h->d_ms, h->d_mpd, h->d_mspd, h->d_perm, h->mp);
+                                                   h->d_perm, h->mp);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(h->d_wt_info, wt_info.data(), n_wt * sizeof(uint2), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(h->d_slot_start, slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
@@ -431,9 +419,27 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   std::vector<u32> tc_slot_start(G + 1);
   if (h->tc_mode != 0 && (h->path == kInt4 || h->path == kInt2 || h->path == kFp64 || h->path == kInt32)) {
     const u64 tp = h->t_pad;
-    if (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp) || dalloc(&h->d_tcMS, (size_t)2 * tp) ||
-        dalloc(&h->d_tcR, (size_t)((tp + 2 * tc::kKB - 1) / (2 * tc::kKB)) * 2 * tc::kRBytes))
-      return g_last_error;
+    // handle memory of the tensor-core form: C records + seed powers + baby-step planes (DESIGN.md
+    // §6, ~624 B per padded term).  If it does not fit (the device, or the env cap PE_TC_MEM_MB),
+    // an automatic handle degrades to the scalar k_step; a forced one (PE_PATH_TC) fails.
+    const u64 nrblk = (tp + 2 * tc::kKB - 1) / (2 * tc::kKB);
+    const u64 tc_bytes = (u64)tc::kCRec * 8 * tp + 16 * tp + nrblk * 2 * tc::kRBytes;
+    const u64 cap = (u64)std::max(0, env_int("PE_TC_MEM_MB", 0)) << 20;
+    int rc = PE_OK;
+    if (cap && tc_bytes > cap) rc = PE_ENOMEM;
+    if (rc == PE_OK && (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp) || dalloc(&h->d_tcMS, (size_t)2 * tp) ||
+                        dalloc(&h->d_tcR, (size_t)nrblk * 2 * tc::kRBytes)))
+      rc = g_last_error;
+    if (rc != PE_OK) {
+      if (h->tc_mode == 2 || rc != PE_ENOMEM) return set_err(rc);
+      for (void** q : {(void**)&h->d_tcC, (void**)&h->d_tcMS, (void**)&h->d_tcR})
+        if (*q) { cudaFreeAsync(*q, s); *q = nullptr; }
+      cudaGetLastError();               // allocation failures are not sticky; clear the record
+      g_last_error = PE_OK;
+      h->tc_mode = 0;
+      CU(cudaStreamSynchronize(s));
+      return PE_OK;
+    }
     tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
     CU(cudaGetLastError());
     const u64 nrp = (tp + 2 * tc::kKB - 1) / (2 * tc::kKB);   // blocks of 2 K-blocks
@@ -448,6 +454,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
     CU(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
     u64 piece_max = 2 * ((tp + h->n_sm - 1) / h->n_sm);
     piece_max = std::min<u64>(std::max<u64>(piece_max, 1024), tc::kPieceMax);
+    const int pm_env = env_int("PE_TC_PIECE", 0);   // testing: force small pieces (many units per CTA)
+    if (pm_env > 0) piece_max = std::min<u64>((u64)pm_env, tc::kPieceMax);
     piece_max = (piece_max + tc::kKB - 1) / tc::kKB * tc::kKB;
     for (u64 g = 0; g < G; ++g) {
       tc_slot_start[g] = (u32)pieces.size();
@@ -471,6 +479,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
     if (dalloc(&h->d_piece, pieces.size()) || dalloc(&h->d_tc_slot_start, G + 1)) return g_last_error;
     CU(cudaMemcpyAsync(h->d_piece, pieces.data(), pieces.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(h->d_tc_slot_start, tc_slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
+    if (cudaHostAlloc((void**)&h->h_status, sizeof(u32), cudaHostAllocMapped) != cudaSuccess) return set_err(PE_ENOMEM);
+    *h->h_status = 0;
     h->tc_ok = true;
   }
   CU(cudaStreamSynchronize(s));  // host vectors above must outlive the copies; tmp frees after
@@ -507,18 +517,12 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
     if (p >= (1ull << 50)) { set_err(PE_ENOTSUP); return nullptr; }
     path = kFp64;
   } else if (path_req == PE_PATH_INT || path_req == PE_PATH_AUTO) {
-    // INT64 family: the 32-bit-IMAD Shoup core by default (lazy-4 for p < 2^62, lazy-2
-    // above); PE_CORE=hyb selects the hybrid FP64-quotient core.
+    // INT64 family: the 32-bit-IMAD Shoup core (lazy-4 for p < 2^62, lazy-2 above)
     const char* core = getenv("PE_CORE");
-    const bool hyb = core && !strcmp(core, "hyb");
-    path = hyb ? kHyb : (p < (1ull << 62) ? kInt4 : kInt2);
+    path = p < (1ull << 62) ? kInt4 : kInt2;
     if (path_req == PE_PATH_AUTO && p < (1ull << 50) && (!core || !strcmp(core, "auto"))) path = kFp64;
     // p < 2^31: 32-bit Shoup (4 IMAD slots per product instead of 14)
     if (p < (1ull << 31) && (!core || !strcmp(core, "auto") || !strcmp(core, "int32"))) path = kInt32;
-    if (core && !strcmp(core, "mix")) {
-      if (p >= (1ull << 50)) { set_err(PE_ENOTSUP); return nullptr; }
-      path = kMix;
-    }
     if (core && !strcmp(core, "fp64")) {
       if (p >= (1ull << 50)) { set_err(PE_ENOTSUP); return nullptr; }
       path = kFp64;
@@ -623,6 +627,8 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
   Tp = std::max<u64>(Tp, tc::kChunk);
   Tp = std::min<u64>(Tp, (T + tc::kChunk - 1) / tc::kChunk * tc::kChunk);
   Tp = std::min<u64>(Tp, (u64)tc::kChunk * 4096);
+  // every allocation of the evaluation comes before its first launch, so an automatic handle can
+  // still fall back to k_step on PE_ENOMEM (eval_device_impl)
   // partial rows padded to a multiple of 8 points (the epilogue's 64-byte vector accesses)
   if (ensure_partial(h, (size_t)nslots * ((std::min<u64>(Tp, T) + 7) / 8 * 8), s)) return g_last_error;
   const u32 nch_max = (u32)(Tp / tc::kChunk);
@@ -634,6 +640,8 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     h->seed_elems = (size_t)h->t_pad * nch_max * tc::kLSRec;
   }
   if (!h->d_tc_scratch) CU(cudaMallocAsync((void**)&h->d_tc_scratch, (size_t)h->n_sm * 2 * tc::kDiag * tc::kChunk * sizeof(u32), s));
+  u32* d_status = nullptr;
+  CU(cudaHostGetDevicePointer((void**)&d_status, h->h_status, 0));
   // kernel mode: 0 = lazy chains, 8 digits; 1 = p >= 2^62, exact chains, 8 digits; 2 = p < 2^31,
   // exact chains (values < 2^32), 4 digits, one round
   // 3 = 2^31 <= p < 2^54: lazy chains (values < 2^56), 7 digits, two rounds of 12 + 6 MMAs
@@ -667,6 +675,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     a.C128 = h_powmod(2, 128, h->p);
     a.scratch = h->d_tc_scratch;
     a.mp = h->mp;
+    a.status = d_status;
     a.prof = nullptr;
     a.dbg = env_int("PE_TC_DEBUG", 0);
     const unsigned grid = (unsigned)std::min<u64>(a.nunits, (u64)h->n_sm);
@@ -728,13 +737,27 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
   return PE_OK;
 }
 
+// Tensor-core form for this T?  Forced handles always; automatic ones from the measured threshold,
+// and only while one chunk's partial rows (one per piece and diagonal round, T_pass >= one chunk)
+// fit the partial-buffer cap -- a handle with very many buckets stays on k_step, whose partial
+// rows are per CTA run and need far less.
 static bool use_tc(const pe_ctx* h, u64 T) {
-  return h->tc_ok && (h->tc_mode == 2 || (h->tc_mode == 1 && T >= tc_min_T(h->t_pad, h->p)));
+  if (!h->tc_ok) return false;
+  if (h->tc_mode == 2) return true;
+  if (h->tc_mode != 1 || T < tc_min_T(h->t_pad, h->p)) return false;
+  const u64 row = (std::min<u64>(T, tc::kChunk) + 7) / 8 * 8;
+  return (u64)h->tc_nslots * row * sizeof(u64) <= h->partial_cap_bytes;
 }
 
 static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s) {
   if (T == 0 || h->G == 0) return PE_OK;
-  if (use_tc(h, T)) return eval_tc(h, j0, T, d_out, ld, s);
+  if (use_tc(h, T)) {
+    const int rc = eval_tc(h, j0, T, d_out, ld, s);
+    if (rc != PE_ENOMEM || h->tc_mode == 2) return rc;
+    // automatic handle and the evaluation's scratch does not fit: degrade to k_step
+    cudaGetLastError();
+    g_last_error = PE_OK;
+  }
   const u64 nslots = h->n_slots;
   // pass size bounded by the partial-buffer cap
   u64 Tp = std::max<u64>(kSuper, h->partial_cap_bytes / 8 / std::max<u64>(nslots, 1));
@@ -759,7 +782,6 @@ static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaSt
     }
     StepArgs a;
     a.c = h->d_c; a.m = h->d_m; a.w = h->d_w; a.wt_info = h->d_wt_info;
-    a.ms = h->d_ms; a.mpd = h->d_mpd; a.mspd = h->d_mspd;
     a.partial = h->d_partial; a.ldp = np; a.js0 = j0 + k0; a.n_wt = h->n_wt; a.npts = np;
     a.chunk = chunk; a.mp = h->mp;
     dim3 grid(n_cta, (np + chunk - 1) / chunk), block(32 * W);
@@ -786,13 +808,23 @@ static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaSt
   return PE_OK;
 }
 
+// A k_tc pipeline wait that timed out (bounded waits) leaves the handle's status
+// word set; every later call on the handle reports PE_ECUDA.
+static bool tc_failed(const pe_ctx* h) { return h->h_status && *(volatile u32*)h->h_status != 0; }
+
 extern "C" int pe_eval_device(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* d_out, uint64_t ld,
                               void* stream) {
   g_last_error = PE_OK;
   if (!h) return set_err(PE_EINVAL);
   if (T && j0 + (T - 1) < j0) return set_err(PE_ERANGE);
   if (T && h->G && (!d_out || ld < T)) return set_err(PE_EINVAL);
-  return eval_device_impl(h, j0, T, d_out, ld, (cudaStream_t)stream);
+  if (tc_failed(h)) return set_err(PE_ECUDA);
+  int cur = 0;
+  CU(cudaGetDevice(&cur));
+  if (cur != h->device) CU(cudaSetDevice(h->device));   // kernels and stream-ordered allocations go to the handle's device
+  const int rc = eval_device_impl(h, j0, T, d_out, ld, (cudaStream_t)stream);
+  if (cur != h->device) cudaSetDevice(cur);
+  return rc;
 }
 
 extern "C" int pe_eval(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* out) {
@@ -843,6 +875,7 @@ extern "C" int pe_eval(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* out) {
         rc = set_err(PE_ECUDA);
     }
   }
+  if (rc == PE_OK && tc_failed(h)) rc = set_err(PE_ECUDA);
   if (cur != h->device) cudaSetDevice(cur);
   return rc;
 }
@@ -860,9 +893,7 @@ extern "C" int pe_info(const pe_ctx* h, int32_t* path, int32_t* R, int32_t* warp
                        uint64_t* n_slots) {
   if (!h) return set_err(PE_EINVAL);
   if (path)
-    *path = h->path == kFp64 ? PE_PATH_FP64
-          : h->path == kMix  ? PE_PATH_MIX
-          : h->path == kInt32 ? PE_PATH_INT32 : PE_PATH_INT;
+    *path = h->path == kFp64 ? PE_PATH_FP64 : h->path == kInt32 ? PE_PATH_INT32 : PE_PATH_INT;
   if (R) *R = h->R;
   if (warps) *warps = h->W;
   if (t_padded) *t_padded = h->t_pad;
@@ -876,6 +907,11 @@ extern "C" int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint
   if (pieces) *pieces = h->tc_npieces;
   if (min_T) *min_T = h->tc_ok ? (h->tc_mode == 2 ? 1 : tc_min_T(h->t_pad, h->p)) : 0;
   return PE_OK;
+}
+
+extern "C" int pe_eval_kernel(const pe_ctx* h, uint64_t T) {
+  if (!h) return set_err(PE_EINVAL);
+  return use_tc(h, T) ? 1 : 0;
 }
 
 extern "C" int pe_monomials(const pe_ctx* h, uint64_t* m) {
@@ -915,6 +951,32 @@ extern "C" int pe_kernel_stats(pe_ctx* h, uint64_t* step_launches, double* step_
   if (fixup_ms) *fixup_ms = f_ms;
   if (term_points) *term_points = tp;
   drop_recs(h);
+  return PE_OK;
+}
+
+// ---------------------------------------------------------------- multi-GPU assembly
+extern "C" int pe_rows_addmod(uint64_t p, uint64_t* d_dst, uint64_t ld_dst, const uint64_t* d_src, uint64_t ld_src,
+                              uint64_t rows, uint64_t cols, void* stream) {
+  g_last_error = PE_OK;
+  if (p < 3 || p >= (1ull << 63)) return set_err(PE_ERANGE);
+  if (rows == 0 || cols == 0) return PE_OK;
+  if (!d_dst || !d_src || ld_dst < cols || ld_src < cols) return set_err(PE_EINVAL);
+  k_rows_addmod<<<grid_for(rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(d_dst, ld_dst, d_src, ld_src, rows,
+                                                                            cols, p);
+  CU(cudaGetLastError());
+  return PE_OK;
+}
+
+extern "C" int pe_unshard_columns(uint64_t* d_out, uint64_t ld, const uint64_t* d_blocks, uint64_t P, uint64_t G,
+                                  uint64_t Tr, uint64_t T, void* stream) {
+  g_last_error = PE_OK;
+  if (G == 0 || T == 0 || P == 0) return PE_OK;
+  if (!d_out || !d_blocks || ld < T || Tr == 0 || P * Tr < T) return set_err(PE_EINVAL);
+  for (u64 r = 0; r < P && r * Tr < T; ++r) {
+    const u64 cnt = std::min<u64>(Tr, T - r * Tr);
+    CU(cudaMemcpy2DAsync(d_out + r * Tr, ld * sizeof(u64), d_blocks + r * G * Tr, Tr * sizeof(u64),
+                         cnt * sizeof(u64), G, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  }
   return PE_OK;
 }
 

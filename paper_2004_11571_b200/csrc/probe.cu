@@ -303,7 +303,9 @@ __global__ void k_bench_mma(int iters, u32 idesc, u32 ncols, int nacc) {
           :: "r"(tb + acc_col), "l"(ad), "l"(bd), "r"(idesc), "r"(1u));
     tc::mma_commit(&bar);
   }
-  tc::mbar_wait(&bar, 0);
+  __shared__ u32 abort_flag;
+  abort_flag = 0;
+  tc::mbar_wait(&bar, 0, tc::Abort{&abort_flag, nullptr});
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 0) {

@@ -107,6 +107,7 @@ struct TcArgs {
   u64 C128;              // 2^128 mod p
   u32* scratch;          // per CTA: 2 (ping-pong by unit) x kDiag accumulators x kChunk u32 drained diagonal sums
   ModParams mp;
+  u32* status;           // mapped host word (pe_ctx::h_status): set to 1 if a pipeline wait timed out
   unsigned long long* prof;  // optional phase timers [gridDim][warps][4] (PE_TC_PROF=1), else null
   int dbg;                   // development only (PE_TC_DEBUG, PROF build): 1 = skip the MMAs,
                              // 2 = producers skip generation, 3 = the TMEM drain skips its stores,
@@ -316,13 +317,37 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, u32 parity) {
       : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   return ok != 0;
 }
-// bounded wait: a protocol bug becomes a launch error instead of a hung GPU.  SLEEP_NS > 0 backs
-// off between polls so a waiting warp stops taking issue slots from the producers on its SMSP.
+// Bounded wait.  A wait that has not completed after kWaitTimeoutNs of %globaltimer (far beyond any
+// legitimate stall: a whole config-5 launch takes ~9 ms) marks the CTA aborted and the handle's
+// status word failed, and returns; once a CTA is aborted every wait returns at once, so all its
+// warps run out of their loops (producing garbage, never hanging) and the host reports PE_ECUDA
+// (pe.cu tc_failed) instead of a trapped context.  SLEEP_NS > 0 backs off between polls so a
+// waiting warp stops taking issue slots from the producers on its SMSP.
+constexpr unsigned long long kWaitTimeoutNs = 20ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct Abort {
+  volatile u32* cta;   // shared word: this CTA gave up
+  u32* status;         // mapped host word
+};
 template <int SLEEP_NS = 0>
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, u32 parity) {
-  for (u32 n = 0; !mbar_try(bar, parity); ++n) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, u32 parity, const Abort& ab) {
+  if (mbar_try(bar, parity) || *ab.cta) return;
+  const unsigned long long t0 = gtimer();
+  for (u32 n = 1;; ++n) {
     if (SLEEP_NS) __nanosleep(SLEEP_NS);
-    if (n > (1u << 26)) __trap();
+    if (mbar_try(bar, parity)) return;
+    if ((n & 255) == 0) {
+      if (*ab.cta) return;
+      if (gtimer() - t0 > kWaitTimeoutNs) {
+        *ab.cta = 1;
+        if (ab.status) atomicExch(ab.status, 1u);
+        return;
+      }
+    }
   }
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, u32 bytes) {
@@ -630,6 +655,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
   uint8_t* smem = (uint8_t*)(((uintptr_t)dsm + 127) & ~(uintptr_t)127);   // kSmemBytes holds 128 B of slack
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accf, acce, dfull[kDataSlots];
   __shared__ u32 tmem_base;
+  __shared__ u32 abort_flag;
+  const Abort ab{&abort_flag, a.status};
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -639,6 +666,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
     mbar_init(&acce, 32 * kEpiWarps);
     for (int s = 0; s < kDataSlots; ++s) mbar_init(&dfull[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    abort_flag = 0;
   }
   if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(smem_u32(&tmem_base)));
@@ -688,7 +716,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
     auto fetch = [&](u32 g) {
       const u32 dslot = data0 + (slot0 + (g & 1)) * kDataSlot;
       const long long f0 = clk();
-      mbar_wait<64>(&dfull[slot0 + (g & 1)], (g >> 1) & 1);
+      mbar_wait<64>(&dfull[slot0 + (g & 1)], (g >> 1) & 1, ab);
       if (PROF) T[0] += clk() - f0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -702,7 +730,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       const u32 stage = (u32)my_stage;
       const u32 use = guse;
       long long c0 = clk();
-      mbar_wait<64>(&empty[stage], (use & 1) ^ 1);
+      mbar_wait<64>(&empty[stage], (use & 1) ^ 1, ab);
       long long c1 = clk();
       if (PROF) T[1] += c1 - c0;
       // the other slot held K-block guse-1, which every warp of the group read (at the end of
@@ -769,13 +797,13 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
         // that fold precedes their drain of the previous unit, which this warp has waited for
         // through acce -- no extra barrier needed)
         long long c0 = clk();
-        mbar_wait<32>(&acce, (nunit & 1) ^ 1);
+        mbar_wait<32>(&acce, (nunit & 1) ^ 1, ab);
         if (PROF) T[2] += clk() - c0;
         tc_fence_after();
         for (u32 kb = 0; kb < nkb; ++kb, ++it) {
           const u32 stage = it % kStages, use = it / kStages;
           c0 = clk();
-          mbar_wait<32>(&full[stage], use & 1);
+          mbar_wait<32>(&full[stage], use & 1, ab);
           if (PROF) T[kb < (u32)kStages ? 0 : 1] += clk() - c0;   // unit start vs steady state
           tc_fence_after();
           const uint64_t da = dA0 + (uint64_t)((stage * kStageBytes) >> 4);
@@ -802,7 +830,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
         }
       }
       long long c0 = clk();
-      mbar_wait<64>(&accf, nunit & 1);
+      mbar_wait<64>(&accf, nunit & 1, ab);
       long long c1 = clk();
       if (PROF) T[0] += c1 - c0;
       tc_fence_after();
@@ -821,7 +849,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       for (int pass = 0; pass < (warp == kMmaWarp ? 0 : (warp == 1 ? 1 : 2)); ++pass) {
         u32 ur = u, vbeg = 0, vend = (u32)kV;
         if (pass == 1) {                 // warp 0's rows, once all 4 warps drained the unit
-          mbar_wait<32>(&acce, nunit & 1);
+          mbar_wait<32>(&acce, nunit & 1, ab);
           ur = (u32)lane;
           vbeg = warp == 2 ? 0u : (u32)kV / 2;
           vend = vbeg + (u32)kV / 2;

@@ -1,18 +1,28 @@
-"""Multi-GPU point-range sharding (PAPER.md:557-573 HM16 "N evaluations at a
-time", in its contiguous-range form).
+"""Multi-GPU plumbing: one process per GPU, torch.distributed for
+the process group and the NCCL transfers, libpe (C ABI) for everything that touches the values.
 
-Every rank holds the full, replicated term set (its own ``Context``), evaluates a contiguous
-block of the T points -- seeding a_i at its own first point by exponentiation inside k_step --
-and the only collective is one gather of the G x T_r output blocks to the root over NCCL.
-Arbitrary term sharding (MT18's 1D decomposition) would need a *modular*
-all-reduce, which NCCL's wrapping uint64 sum cannot do exactly; the bucket-contiguous term
-ranges of ``TermShardedEval`` (below, used by the tensor-core path) avoid it.
+Two decompositions, each with one gather to the root as the only collective:
 
-``eval_sharded`` is device-agnostic plumbing: ``eval_local(j_first, T_r, out_view)`` fills a
-``[G, T_r]`` int64 tensor (the CUDA path on GPUs; the tests inject the CPU oracle under gloo).
+* ``ShardedEval`` -- point ranges (HM16 "N evaluations at a time", in its
+  contiguous-range form): every rank holds the full replicated term set (its own handle),
+  evaluates a contiguous block of the T points -- seeding at its own first point -- and the
+  root gathers the G x T_r blocks and puts them back into rows with ``pe_unshard_columns``.
+* ``TermShardedEval`` -- bucket-contiguous term ranges (the matrix method's own sorted order,
+  PAPER.md:495-503): rank r evaluates all T points of ~t/P consecutive terms; the root receives
+  every rank's rows straight into place, and the <= P-1 buckets cut by a range boundary are
+  summed mod p by ``pe_rows_addmod`` (PAPER.md:489-503's coefficient reduction across ranks).
+
+This module does no modular arithmetic and no per-column copies itself: the two libpe calls
+above do that on the device.  ``addmod`` / ``unshard`` may be injected (the CPU gloo tests pass
+host implementations, since libpe needs a GPU); the defaults call libpe and require CUDA tensors.
+
+``world`` / ``rank`` may be given explicitly (no process group): ``TermShardedEval.assemble`` and
+``ShardedEval.assemble`` then run the root's placement on per-rank outputs held by one process,
+which is how the single-GPU tests drive exactly this bookkeeping.
 """
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -28,13 +38,47 @@ def shard_width(T: int, world: int) -> int:
     return -(-T // world) if T else 0
 
 
-class ShardedEval:
-    """Buffers for one (G, T, world) shape; reused across steps."""
+def _world_rank(group, world, rank):
+    if world is not None:
+        return world, (0 if rank is None else rank)
+    if dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
 
-    def __init__(self, G: int, T: int, device, group=None, root: int = 0):
+
+def _stream_of(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def libpe_addmod(p: int):
+    """dst <- (dst + src) mod p on device rows (pe_rows_addmod)."""
+    import paper_2004_11571_b200 as pe
+
+    def f(dst: torch.Tensor, src: torch.Tensor):
+        if not (dst.is_cuda and src.is_cuda):
+            raise RuntimeError("pe_rows_addmod needs device tensors (inject addmod= for CPU tests)")
+        pe.rows_addmod(p, dst.data_ptr(), dst.stride(0), src.data_ptr(), src.stride(0), dst.shape[0], dst.shape[1],
+                       _stream_of(dst))
+    return f
+
+
+def libpe_unshard(out: torch.Tensor, blocks: torch.Tensor, T: int):
+    """out[:, r*Tr + k] <- blocks[r, :, k] (pe_unshard_columns)."""
+    import paper_2004_11571_b200 as pe
+    if not (out.is_cuda and blocks.is_cuda):
+        raise RuntimeError("pe_unshard_columns needs device tensors (inject unshard= for CPU tests)")
+    P, G, Tr = blocks.shape
+    pe.unshard_columns(out.data_ptr(), out.stride(0), blocks.data_ptr(), P, G, Tr, T, _stream_of(out))
+
+
+class ShardedEval:
+    """Point-range sharding: buffers for one (G, T, world) shape, reused across steps."""
+
+    def __init__(self, G: int, T: int, device, group=None, root: int = 0, world=None, rank=None,
+                 unshard=None):
         self.G, self.T, self.root, self.group = G, T, root, group
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world, self.rank = _world_rank(group, world, rank)
+        self.unshard = unshard or libpe_unshard
         self.Tr = shard_width(T, self.world)
         self.off, self.cnt = shard_range(T, self.world, self.rank)
         self.is_root = self.rank == root
@@ -53,32 +97,36 @@ class ShardedEval:
             return self.out
         if not gather:
             return None
-        dist.gather(self.local, [t for t in self.gathered] if self.is_root else None, dst=self.root,
+        dist.gather(self.local, list(self.gathered.unbind(0)) if self.is_root else None, dst=self.root,
                     group=self.group)
         if not self.is_root:
             return None
-        for r in range(self.world):                     # [P][G][T_r] -> [G][T]
+        self.unshard(self.out, self.gathered, self.T)
+        return self.out
+
+    def assemble(self, eval_rank, j0: int):
+        """Single process, no process group: rank r's block is produced by
+        ``eval_rank(r, j_first, cnt, out_view)`` straight into the gather buffer, then the root's
+        placement runs as in ``run``."""
+        assert self.is_root and self.world > 1
+        for r in range(self.world):
             off, cnt = shard_range(self.T, self.world, r)
             if cnt:
-                self.out[:, off: off + cnt].copy_(self.gathered[r, :, :cnt])
+                eval_rank(r, j0 + off, cnt, self.gathered[r])
+        self.unshard(self.out, self.gathered, self.T)
         return self.out
 
 
 # ---------------------------------------------------------------------------------------------
-# Bucket-contiguous term-range sharding (the tensor-core path's multi-GPU form).
-#
-# The tensor-core step (csrc/tc.cuh) evaluates 128 x 128-point chunks; with BASELINE config 5's
-# T = 16384 "sharded across 1/2/4/8 GPUs", point ranges of 2048-8192 points per rank would fall
-# below one chunk.  So ranks shard the TERMS instead, in the matrix method's own bucket order
-# (terms sorted by (x, y) exponent): the terms, sorted by (dx, dy) descending,
-# are cut into `world` contiguous ranges of ~t/world terms; every rank evaluates all T points of
-# its range with its own handle (full T: whole chunks) and sends its G_r output rows to the root.
-# Because the ranges are contiguous in bucket order, consecutive ranks share at most ONE bucket
-# (the one cut by the boundary); the root adds those boundary rows mod p (values < p < 2^62, so
-# the int64 sum cannot overflow).  No modular all-reduce is needed (MT18).
+# Bucket-contiguous term-range sharding (the tensor-core path's multi-GPU form, DESIGN.md §9).
+# The terms, sorted by (dx, dy) descending, are cut into `world` contiguous ranges of ~t/world
+# terms; every rank evaluates all T points of its range with its own handle (whole 8192-point
+# chunks, so the tensor-core kernel keeps its full 128 x 64 tiles) and sends its G_r output rows
+# to the root.  Consecutive ranks share at most ONE bucket (the one cut by the boundary); the root
+# adds those rows mod p with pe_rows_addmod.  No modular all-reduce is needed (cf. PAPER.md:
+# 574-576, MT18's 1D block decomposition).
 # ---------------------------------------------------------------------------------------------
-def bucket_keys(exps) -> "np.ndarray":
-    import numpy as np
+def bucket_keys(exps) -> np.ndarray:
     e = np.asarray(exps)
     return (e[:, 0].astype(np.uint64) << np.uint64(32)) | e[:, 1].astype(np.uint64)
 
@@ -86,7 +134,6 @@ def bucket_keys(exps) -> "np.ndarray":
 def term_partition(exps, world: int):
     """Stable descending sort of the terms by (dx, dy) and the rank boundaries.
     Returns (order, bounds): rank r owns terms order[bounds[r]:bounds[r+1]] (~t/world each)."""
-    import numpy as np
     key = bucket_keys(exps)
     order = np.argsort(~key, kind="stable")                  # descending (dx, dy)
     t = key.size
@@ -103,11 +150,11 @@ class TermShardedEval:
     first one is shared with rank r-1 when ``overlap[r]``.
     """
 
-    def __init__(self, keys_sorted, bounds, T: int, p: int, device, group=None, root: int = 0):
-        import numpy as np
+    def __init__(self, keys_sorted, bounds, T: int, p: int, device, group=None, root: int = 0, world=None,
+                 rank=None, addmod=None):
         self.T, self.p, self.root, self.group = T, int(p), root, group
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world, self.rank = _world_rank(group, world, rank)
+        self.addmod = addmod or libpe_addmod(self.p)
         assert len(bounds) == self.world + 1
         ks = np.asarray(keys_sorted, dtype=np.uint64)
         new_row = np.ones(ks.size, dtype=bool)
@@ -131,6 +178,32 @@ class TermShardedEval:
         self.shared = (torch.empty((self.world, T), dtype=torch.int64, device=device)
                        if self.is_root and self.world > 1 else None)
 
+    def _slices(self, r):
+        """Row blocks of rank r's output sent separately: the shared boundary row on its own."""
+        g = self.G_r[r]
+        if not g:
+            return []
+        if not self.overlap[r]:
+            return [slice(0, g)]
+        return [slice(0, 1)] + ([slice(1, g)] if g > 1 else [])
+
+    def _targets(self, r):
+        """Where the root puts rank r's rows: [(row slice of r's output, destination view)]."""
+        off, t = self.row_off[r], []
+        for sl in self._slices(r):
+            if self.overlap[r] and sl.start == 0:
+                t.append((sl, self.shared[r:r + 1]))             # boundary row: summed afterwards
+            else:
+                t.append((sl, self.out[off + sl.start:off + sl.stop]))
+        return t
+
+    def _combine(self):
+        """Boundary buckets, in rank order: out[row_off[r]] += shared[r] (mod p, on the device)."""
+        for r in range(self.world):
+            if self.G_r[r] and self.overlap[r]:
+                o = self.row_off[r]
+                self.addmod(self.out[o:o + 1], self.shared[r:r + 1])
+
     def run(self, eval_local, gather: bool = True):
         """eval_local(out_view [G_r, T]) fills this rank's rows; then the root receives every
         rank's rows straight into place and adds the shared boundary rows mod p."""
@@ -140,39 +213,29 @@ class TermShardedEval:
             return self.out if self.world == 1 else None
         ops = []
         if not self.is_root:
-            g = self.G_r[self.rank]
-            if g:
-                if self.overlap[self.rank]:
-                    ops.append(dist.P2POp(dist.isend, self.local[:1], self.root, self.group))
-                    if g > 1:
-                        ops.append(dist.P2POp(dist.isend, self.local[1:], self.root, self.group))
-                else:
-                    ops.append(dist.P2POp(dist.isend, self.local, self.root, self.group))
+            for sl in self._slices(self.rank):
+                ops.append(dist.P2POp(dist.isend, self.local[sl], self.root, self.group))
         else:
             for r in range(self.world):
-                g, off = self.G_r[r], self.row_off[r]
-                if not g:
-                    continue
-                if r == self.rank:
-                    dst0 = self.shared[r:r + 1] if self.overlap[r] else self.out[off:off + 1]
-                    dst0.copy_(self.local[:1])
-                    if g > 1:
-                        self.out[off + 1:off + g].copy_(self.local[1:])
-                    continue
-                if self.overlap[r]:
-                    ops.append(dist.P2POp(dist.irecv, self.shared[r:r + 1], r, self.group))
-                    if g > 1:
-                        ops.append(dist.P2POp(dist.irecv, self.out[off + 1:off + g], r, self.group))
-                else:
-                    ops.append(dist.P2POp(dist.irecv, self.out[off:off + g], r, self.group))
+                for sl, dst in self._targets(r):
+                    if r == self.rank:
+                        dst.copy_(self.local[sl])                # root's own rows (device copy)
+                    else:
+                        ops.append(dist.P2POp(dist.irecv, dst, r, self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
         if not self.is_root:
             return None
-        for r in range(self.world):                              # boundary buckets, in rank order
-            if self.G_r[r] and self.overlap[r]:
-                row = self.out[self.row_off[r]]
-                s = row + self.shared[r]
-                row.copy_(torch.where(s >= self.p, s - self.p, s))
+        self._combine()
+        return self.out
+
+    def assemble(self, locals_):
+        """Single process, no process group: ``locals_[r]`` is rank r's [G_r, T] output; the
+        root's placement and boundary sums run exactly as in ``run``."""
+        assert self.is_root and self.world > 1
+        for r in range(self.world):
+            for sl, dst in self._targets(r):
+                dst.copy_(locals_[r][sl])
+        self._combine()
         return self.out

@@ -2,8 +2,10 @@
 
 The per-rank evaluation is injected: here each rank evaluates its column block with the CPU
 oracle (test infrastructure), so this checks the host logic -- shard ranges, uneven tails,
-empty ranks, the gather and the [P][G][T_r] -> [G][T] permutation -- against one
-single-process oracle call.  On GPUs the same object drives pe_eval_device over NCCL.
+empty ranks, the gather and the root's placement -- against one single-process oracle call.
+libpe's device calls (pe_unshard_columns, pe_rows_addmod) need a GPU, so the CPU runs inject host
+stand-ins for them (``_unshard_host`` / ``_addmod_host``, Python integers); on GPUs the same
+objects drive pe_eval_device and the libpe calls over NCCL (tests/test_gpu_dist.py).
 """
 import os
 import socket
@@ -15,6 +17,22 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2004_11571_b200.dist import ShardedEval, shard_range
+
+
+def _unshard_host(out, blocks, T):
+    P, G, Tr = blocks.shape
+    for r in range(P):
+        cnt = max(0, min(Tr, T - r * Tr))
+        if cnt:
+            out[:, r * Tr:r * Tr + cnt] = blocks[r, :, :cnt]
+
+
+def _addmod_host(p):
+    def f(dst, src):
+        a = dst.numpy().view(np.uint64).astype(object)
+        b = src.numpy().view(np.uint64).astype(object)
+        dst.copy_(torch.from_numpy(((a + b) % p).astype(np.uint64).view(np.int64)))
+    return f
 
 
 def _free_port():
@@ -33,7 +51,7 @@ def _worker(rank, world, port, T, q):
         import synth
         w = synth.random_small(42, synth.P62, 6, 300, 3, T, 5)
         G = oracle.buckets(w.exps, w.n).shape[0]
-        sh = ShardedEval(G, T, torch.device("cpu"))
+        sh = ShardedEval(G, T, torch.device("cpu"), unshard=_unshard_host)
 
         def eval_local(j_first, cnt, out):
             r = oracle.eval_direct(w.p, w.n, w.coeffs, w.exps, w.alpha, j_first, cnt)
@@ -83,12 +101,13 @@ def _term_worker(rank, world, port, args, q):
         import oracle
         import synth
         from paper_2004_11571_b200.dist import TermShardedEval, bucket_keys, term_partition
-        seed, t, T, big = args
-        w = synth.random_small(seed, synth.P62, 6, t, 3, T, 5)
+        seed, t, T, big, p = args
+        w = synth.random_small(seed, p, 6, t, 3, T, 5)
         if big:   # one bucket holding most terms: it spans several ranks (middle ranks: 1 row)
             w.exps[: int(0.8 * t), :2] = (2, 2)
         order, bounds = term_partition(w.exps, world)
-        sh = TermShardedEval(bucket_keys(w.exps)[order], bounds, T, w.p, torch.device("cpu"))
+        sh = TermShardedEval(bucket_keys(w.exps)[order], bounds, T, w.p, torch.device("cpu"),
+                             addmod=_addmod_host(w.p))
         mine = order[bounds[rank]:bounds[rank + 1]]
 
         def eval_local(out):      # rank's own handle: here the CPU oracle on its terms
@@ -103,22 +122,24 @@ def _term_worker(rank, world, port, args, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,t,T,big", [(2, 300, 9, False), (3, 301, 7, False), (4, 250, 5, True),
-                                           (3, 2, 4, False), (2, 1, 3, False)])
-def test_term_sharded_matches_single(world, t, T, big):
+@pytest.mark.parametrize("world,t,T,big,p", [(2, 300, 9, False, (1 << 62) - 57), (3, 301, 7, False, (1 << 62) - 57),
+                                             (4, 250, 5, True, (1 << 62) - 57), (3, 2, 4, False, (1 << 62) - 57),
+                                             (2, 1, 3, False, (1 << 62) - 57), (4, 250, 5, True, (1 << 63) - 25)])
+def test_term_sharded_matches_single(world, t, T, big, p):
     """Bucket-contiguous term ranges + P2P row gather + boundary rows summed mod p reproduce the
-    single-process oracle, including a bucket spanning several ranks and empty ranks (t < world)."""
+    single-process oracle, including a bucket spanning several ranks, empty ranks (t < world) and
+    a prime above 2^62 (boundary sums up to 2p - 2 >= 2^63)."""
     import oracle
     import synth
     seed = 77
-    w = synth.random_small(seed, synth.P62, 6, t, 3, T, 5)
+    w = synth.random_small(seed, p, 6, t, 3, T, 5)
     if big:
         w.exps[: int(0.8 * t), :2] = (2, 2)
     ref = oracle.eval_direct(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, T)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_term_worker, args=(r, world, port, (seed, t, T, big), q)) for r in range(world)]
+    procs = [ctx.Process(target=_term_worker, args=(r, world, port, (seed, t, T, big, p), q)) for r in range(world)]
     for p in procs:
         p.start()
     got = q.get(timeout=120)

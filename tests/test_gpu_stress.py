@@ -1,0 +1,91 @@
+"""Repeated-launch determinism of the tensor-core kernel (k_tc, csrc/tc.cuh) and graceful
+degradation when its memory does not fit.
+
+compute-sanitizer is closed on this GPU pool, so races in k_tc's warp-specialised pipeline (the
+mbarrier ring, the TMEM hand-off between MMA issue and drain, the per-CTA raw-scratch ping-pong)
+are hunted by repetition instead: a race shows up as a run whose output differs from the others.
+Every run must equal the first bit for bit, and the first must equal the CPU oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2004_11571_b200 as pe
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _repeat_equal(ctx, w, runs):
+    G, T = ctx.G, w.T
+    s = torch.cuda.current_stream()
+    ref = torch.empty((G, T), dtype=torch.int64, device="cuda")
+    out = torch.empty_like(ref)
+    ctx.eval_device(w.j0, T, ref.data_ptr(), T, s.cuda_stream)
+    diffs = []
+    for i in range(runs):
+        out.fill_(-1)
+        ctx.eval_device(w.j0, T, out.data_ptr(), T, s.cuda_stream)
+        n = int((out != ref).sum())
+        if n:
+            diffs.append((i, n))
+    torch.cuda.synchronize()
+    assert not diffs, f"runs differing from the first (run, elements): {diffs[:10]}"
+    return ref.cpu().numpy().view(np.uint64)
+
+
+def test_config5_repeated_launches_bitwise():
+    """50 back-to-back evaluations of BASELINE config 5 (t = 10^7, T = 16384: ~49 units per CTA,
+    the bench launch configuration) are bitwise identical; the first is checked on sampled columns
+    (the full G x T comparison is test_gpu_parity.py::test_config5_full)."""
+    w = synth.gen_config(5)
+    with pe.Context.from_workload(w) as ctx:
+        assert ctx.uses_tc(w.T)
+        first = _repeat_equal(ctx, w, 50)
+    ks = np.array([0, 2591, 8192 + 40 * 64 + 7, 16383], np.uint64)
+    assert np.array_equal(first[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
+
+
+@pytest.mark.parametrize("piece", [1024, 256])
+def test_small_pieces_many_units_per_cta(monkeypatch, piece):
+    """Config-3 shape (10^6 terms, T = 4096) with pieces capped at `piece` terms (PE_TC_PIECE) and
+    R = 16 tiles: thousands of units, so every CTA cycles its raw-scratch ping-pong and TMEM
+    hand-off tens of times per launch; 50 runs bitwise equal, the first equal to the full
+    incremental checker."""
+    monkeypatch.setenv("PE_TC_PIECE", str(piece))
+    w = synth.gen_config(3)
+    with pe.Context.from_workload(w, path=pe.PATH_TC, R=16) as ctx:
+        info = ctx.info()
+        assert info["tc_pieces"] >= w.t // piece
+        first = _repeat_equal(ctx, w, 50)
+    ref = oracle.eval_incremental_blocked(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
+    assert np.array_equal(first, ref)
+
+
+def test_tc_memory_cap_degrades_to_k_step(monkeypatch):
+    """PE_TC_MEM_MB below the tensor path's handle memory: an automatic handle falls back to the
+    scalar k_step (pe_tc_info mode 0) and stays bit-exact; a forced PE_PATH_TC handle fails with
+    PE_ENOMEM instead."""
+    w = synth.gen_config(2, t=60_000, T=2000)
+    with pe.Context.from_workload(w) as ctx:
+        assert ctx.uses_tc(w.T)                       # without the cap: tensor path
+    monkeypatch.setenv("PE_TC_MEM_MB", "8")           # ~624 B/term x 6e4 terms ~ 37 MB > 8 MB
+    with pe.Context.from_workload(w) as ctx:
+        assert ctx.info()["tc_mode"] == 0 and not ctx.uses_tc(w.T)
+        out = ctx.eval(w.j0, w.T)
+    assert np.array_equal(out, oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T))
+    with pytest.raises(pe.PEError) as ei:
+        pe.Context.from_workload(w, path=pe.PATH_TC)
+    assert ei.value.code == pe.PE_ENOMEM
+
+
+def test_many_buckets_partial_cap_uses_k_step(monkeypatch):
+    """A chunk of partial rows (pieces x rounds x 8192 x 8 B) above the partial-buffer cap: the
+    automatic path keeps k_step (10^6 buckets would need > 100 GB on k_tc)."""
+    w = synth.random_small(611, synth.P62, 6, 20_000, 9, 2000, 1)
+    w.exps[:, 0] = np.arange(w.t, dtype=np.uint32) % 5000      # 5000 buckets of ~4 terms
+    monkeypatch.setenv("PE_PARTIAL_MB", "64")                  # 5000 pieces x 2 rounds x 2000 x 8 B = 160 MB > 64 MB
+    with pe.Context.from_workload(w) as ctx:
+        assert ctx.info()["tc_mode"] == 1 and not ctx.uses_tc(w.T)
+        out = ctx.eval(w.j0, w.T)
+    assert np.array_equal(out, oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T))

@@ -139,6 +139,8 @@ def test_incremental_equals_direct(seed, p, n, j0, T):
     d = oracle.eval_direct(p, n, w.coeffs, w.exps, w.alpha, j0, T)
     i = oracle.eval_incremental(p, n, w.coeffs, w.exps, w.alpha, j0, T)
     assert np.array_equal(d, i)
+    for block in (1, 4, T, T + 3):       # the blocked checker (re-seeded per block) is the same
+        assert np.array_equal(d, oracle.eval_incremental_blocked(p, n, w.coeffs, w.exps, w.alpha, j0, T, block))
 
 
 def _m_python(alpha, e, p):
