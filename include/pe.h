@@ -47,7 +47,15 @@ enum {
   PE_ENOTSUP = -6    /* requested path / option not supported for this p               */
 };
 
-enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_INT32 = 4, PE_PATH_TC = 5 };  /* 3: retired */
+enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_INT32 = 4, PE_PATH_TC = 5,
+       PE_PATH_FAST = 6 };  /* 3: retired */
+/* PE_PATH_FAST forces the asymptotically fast method (HL13)
+ * for every T, p < 2^62 (PE_ENOTSUP above), T <= 2^20 (PE_ERANGE above): per bucket the T outputs
+ * are the first T coefficients of sum_i a_i / (1 - m_i z) = N(z)/D(z), a_i = c_i m_i^{j0}, computed
+ * by a product tree of (N, D) pairs and a Newton power-series inversion, with polynomial products
+ * done exactly by NTTs over five 30-bit primes and CRT (O(s log^2 T) operations instead of s T).
+ * PE_PATH_AUTO takes it for p < 2^62 once T reaches the measured crossover with the tensor-core
+ * form (pe_eval_kernel reports the choice; env PE_FAST=0 off, 2 always). Bit-identical results. */
 /* PE_PATH_TC forces the tensor-core form of the step (any p < 2^63; for 2^62 <= p the giant-step
  * chains use the exact-quotient Shoup product so every value keeps 8 bytes): each bucket's
  * block of T_c = 128 x 64 points is the product L * R of giant-step values c_i m_i^{j_s+64u} and
@@ -146,8 +154,8 @@ int pe_info(const pe_ctx* h, int32_t* path, int32_t* R, int32_t* warps, uint64_t
 int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint64_t* min_T);
 
 /* Which hot kernel an evaluation of T points on this handle runs: 0 = the scalar k_step, 1 = the
- * tensor-core k_tc (the automatic choice: threshold, partial-buffer cap, memory).  PE_EINVAL if h
- * is NULL. */
+ * tensor-core k_tc, 2 = the fast product-tree method (the automatic choice: thresholds,
+ * partial-buffer cap, memory).  PE_EINVAL if h is NULL. */
 int pe_eval_kernel(const pe_ctx* h, uint64_t T);
 
 /* m_i = prod_l alpha_l^{e_i,l} mod p for every input term i (HOST uint64[t], input order). */

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_PKG, "libpe.so")
 TEST_LIB_PATH = os.path.join(_PKG, "libpe_test.so")   # include/pe_test.h: probes, not the product
 
 PE_OK, PE_EINVAL, PE_ENOTPRIME, PE_ERANGE, PE_ENOMEM, PE_ECUDA, PE_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
-PATH_AUTO, PATH_INT, PATH_FP64, PATH_INT32, PATH_TC = 0, 1, 2, 4, 5
+PATH_AUTO, PATH_INT, PATH_FP64, PATH_INT32, PATH_TC, PATH_FAST = 0, 1, 2, 4, 5, 6
 CORE_SHOUP4, CORE_SHOUP2, CORE_MONT, CORE_FP64, CORE_FP64ADD, CORE_POW, CORE_SHOUP4RAW, CORE_HYB, CORE_HYBRAW = range(9)
 
 #: every symbol include/pe.h declares (libpe.so)
@@ -235,7 +235,7 @@ class Context:
         k = lib().pe_eval_kernel(self._h, T)
         if k < 0:
             raise PEError(k, "pe_eval_kernel")
-        return {0: "k_step", 1: "k_tc"}[k]
+        return {0: "k_step", 1: "k_tc", 2: "fast"}[k]
 
     def uses_tc(self, T: int) -> bool:
         """True if an evaluation of T points runs the tensor-core kernel (PE_PATH_TC / auto)."""

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpe.so")
 TEST_LIB = os.path.join(PKG, "libpe_test.so")
-LIBS = {LIB: [os.path.join(CSRC, "pe.cu"), os.path.join(CSRC, "bm.cu")],
+LIBS = {LIB: [os.path.join(CSRC, "pe.cu"), os.path.join(CSRC, "bm.cu"), os.path.join(CSRC, "fast.cu")],
         TEST_LIB: [os.path.join(CSRC, "probe.cu")]}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/pe.h"
+#include "fast.h"
 #include "kernels.cuh"
 #include "tc.cuh"
 
@@ -130,6 +131,11 @@ struct pe_ctx {
   size_t seed_elems = 0;
   u32* d_tc_scratch = nullptr;   // k_tc per-CTA drained diagonal sums (n_sm x 2 x kDiag x kChunk u32)
   u32* h_status = nullptr;       // mapped host word: k_tc sets it when a pipeline wait times out
+  // asymptotically fast method (fast.cu, NEXT-4): 0 off, 1 automatic (T >= fast_min_T), 2 forced
+  int fast_mode = 0;
+  u64 fast_min_T = 0;
+  fast::Plan* fast = nullptr;
+  std::vector<u64> h_poff;       // padded bucket offsets [G+1] (the fast path's tree shape)
   size_t partial_cap_bytes = (size_t)1 << 30;
   cudaStream_t copy_stream = nullptr;   // pe_eval: device->host copy of a column block
   cudaEvent_t copy_done = nullptr;
@@ -158,6 +164,7 @@ static void free_all(pe_ctx* h) {
   if (h->copy_stream) cudaStreamSynchronize(h->copy_stream), cudaStreamDestroy(h->copy_stream);
   if (h->copy_done) cudaEventDestroy(h->copy_done);
   if (h->h_status) cudaFreeHost(h->h_status);
+  if (h->fast) fast::destroy(h->fast, s), h->fast = nullptr;
   if (h->stream) cudaStreamDestroy(h->stream);
 }
 
@@ -223,6 +230,9 @@ static u64 tc_min_T(u64 t_pad, u64 p) {
   if (t_pad >= 500000) return 512;
   return std::min<u64>(8192, std::max<u64>(512, 86000000ull / tp));
 }
+
+// automatic fast-method threshold (points): from the measured crossover with k_tc
+static const u64 kFastMinT = ~0ull;
 
 static unsigned grid_for(u64 n, unsigned block) {
   u64 b = (n + block - 1) / block;
@@ -365,6 +375,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
     poff[g + 1] = poff[g] + (counts[g] + tile - 1) / tile * tile;
   }
   h->t_pad = poff[G];
+  h->h_poff = poff;
   const u64 n_wt = h->t_pad / tile;
   if (n_wt >= 0x7fffffffull) return set_err(PE_ERANGE);
   h->n_wt = (u32)n_wt;
@@ -483,6 +494,10 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
     *h->h_status = 0;
     h->tc_ok = true;
   }
+  if (h->fast_mode == 2) {
+    const int rc = fast::create(h->h_poff, h->mp, s, &h->fast);
+    if (rc != PE_OK) return set_err(rc);
+  }
   CU(cudaStreamSynchronize(s));  // host vectors above must outlive the copies; tmp frees after
   return PE_OK;
 }
@@ -529,6 +544,9 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
     }
   } else if (path_req == PE_PATH_TC) {
     path = p < (1ull << 62) ? kInt4 : kInt2;
+  } else if (path_req == PE_PATH_FAST) {
+    if (p >= (1ull << 62)) { set_err(PE_ENOTSUP); return nullptr; }
+    path = kInt4;
   } else {
     set_err(PE_EINVAL);
     return nullptr;
@@ -539,6 +557,13 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
   // point ranges, the tensor-core form long ones)
   const bool tc_able = path == kInt4 || path == kInt2 || path == kFp64 || path == kInt32;
   int tc_mode = path_req == PE_PATH_TC ? 2 : (path_req == PE_PATH_AUTO && tc_able ? 1 : 0);
+  // fast method: forced by PE_PATH_FAST; automatic (p < 2^62, T >= the measured crossover) unless
+  // env PE_FAST=0; PE_FAST=2 forces it for PE_PATH_AUTO handles
+  int fast_mode = path_req == PE_PATH_FAST ? 2 : 0;
+  if (path_req == PE_PATH_AUTO && p < (1ull << 62)) {
+    const int e = env_int("PE_FAST", 1);
+    fast_mode = e <= 0 ? 0 : (e >= 2 ? 2 : 1);
+  }
   if (path_req == PE_PATH_AUTO && tc_able) {
     const int e = env_int("PE_TC", 1);
     tc_mode = e < 0 ? 0 : (e > 2 ? 2 : e);
@@ -556,6 +581,7 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
   h->mp = h_mod_params(p);
   h->path = path;
   h->tc_mode = tc_mode;
+  h->fast_mode = fast_mode;
   h->R = R; h->W = W; h->chunk_req = chunk;
   h->partial_cap_bytes = (size_t)env_int("PE_PARTIAL_MB", 1024) << 20;
   h->poly_off = poly_off;
@@ -676,6 +702,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     a.scratch = h->d_tc_scratch;
     a.mp = h->mp;
     a.status = d_status;
+    a.discard = env_int("PE_TC_DISCARD", 1);
     a.prof = nullptr;
     a.dbg = env_int("PE_TC_DEBUG", 0);
     const unsigned grid = (unsigned)std::min<u64>(a.nunits, (u64)h->n_sm);
@@ -749,8 +776,53 @@ static bool use_tc(const pe_ctx* h, u64 T) {
   return (u64)h->tc_nslots * row * sizeof(u64) <= h->partial_cap_bytes;
 }
 
+// automatic fast-method threshold: the measured crossover against k_tc (fast method)
+static u64 fast_min_T(const pe_ctx* h) {
+  (void)h;
+  const int e = env_int("PE_FAST_MIN_T", 0);
+  return e > 0 ? (u64)e : kFastMinT;
+}
+static bool use_fast(const pe_ctx* h, u64 T) {
+  if (h->fast_mode == 2) return true;
+  return h->fast_mode == 1 && T >= fast_min_T(h) && T <= fast::kTMax;
+}
+enum { kKStep = 0, kKTc = 1, kKFast = 2 };
+static int choose_kernel(const pe_ctx* h, u64 T) {
+  if (use_fast(h, T)) return kKFast;
+  return use_tc(h, T) ? kKTc : kKStep;
+}
+
+static int eval_fast(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s) {
+  if (!h->fast) {
+    const int rc = fast::create(h->h_poff, h->mp, s, &h->fast);
+    if (rc != PE_OK) return set_err(rc);
+  }
+  pe_ctx::Rec rec{};
+  if (h->timing) {
+    CU(cudaEventCreate(&rec.e0));
+    CU(cudaEventCreate(&rec.e1));
+    CU(cudaEventCreate(&rec.e2));
+    rec.tp = (double)h->t_pad * T;
+    CU(cudaEventRecord(rec.e0, s));
+  }
+  const int rc = fast::eval(h->fast, h->d_c, h->d_m, h->mp, j0, T, d_out, ld, s);
+  if (rc != PE_OK) return set_err(rc);
+  if (h->timing) {
+    CU(cudaEventRecord(rec.e1, s));
+    CU(cudaEventRecord(rec.e2, s));
+    h->recs.push_back(rec);
+  }
+  return PE_OK;
+}
+
 static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s) {
   if (T == 0 || h->G == 0) return PE_OK;
+  if (choose_kernel(h, T) == kKFast) {
+    const int rc = eval_fast(h, j0, T, d_out, ld, s);
+    if (rc != PE_ENOMEM || h->fast_mode == 2) return rc;
+    cudaGetLastError();            // automatic handle: degrade to the matrix method
+    g_last_error = PE_OK;
+  }
   if (use_tc(h, T)) {
     const int rc = eval_tc(h, j0, T, d_out, ld, s);
     if (rc != PE_ENOMEM || h->tc_mode == 2) return rc;
@@ -849,7 +921,8 @@ extern "C" int pe_eval(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* out) {
   // Long ranges on the tensor-core path: two column blocks of whole chunks, the first block's
   // device->host copy (pitched: rows of the [G][T] result) overlapping the second's evaluation.
   const u64 half = (T / 2 + tc::kChunk - 1) / tc::kChunk * tc::kChunk;
-  const bool split = rc == PE_OK && use_tc(h, T) && T >= 2 * (u64)tc::kChunk && half < T && use_tc(h, T - half);
+  const bool split = rc == PE_OK && choose_kernel(h, T) == kKTc && T >= 2 * (u64)tc::kChunk && half < T &&
+                     choose_kernel(h, T - half) == kKTc;
   if (split) {
     if (!h->copy_stream && cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
       rc = set_err(PE_ECUDA);
@@ -911,7 +984,7 @@ extern "C" int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint
 
 extern "C" int pe_eval_kernel(const pe_ctx* h, uint64_t T) {
   if (!h) return set_err(PE_EINVAL);
-  return use_tc(h, T) ? 1 : 0;
+  return choose_kernel(h, T);
 }
 
 extern "C" int pe_monomials(const pe_ctx* h, uint64_t* m) {

@@ -107,6 +107,7 @@ struct TcArgs {
   u64 C128;              // 2^128 mod p
   u32* scratch;          // per CTA: 2 (ping-pong by unit) x kDiag accumulators x kChunk u32 drained diagonal sums
   ModParams mp;
+  int discard;           // 1: discard the raw scratch lines from L2 once folded (PE_TC_DISCARD, default 1)
   u32* status;           // mapped host word (pe_ctx::h_status): set to 1 if a pipeline wait timed out
   unsigned long long* prof;  // optional phase timers [gridDim][warps][4] (PE_TC_PROF=1), else null
   int dbg;                   // development only (PE_TC_DEBUG, PROF build): 1 = skip the MMAs,
@@ -537,9 +538,19 @@ __device__ __forceinline__ void fold_group(u128_t& acc, u32& x4, const u32 (&D)[
 // One TMEM row (giant step ur) of a unit: fold round G's diagonals of each of the kV points into
 // X_G (< 2^145), reduce the 2^64..2^128 words with 2^{32k} mod p into 128 bits, and finish with
 // one REDC into the unit's partial row.
+// discard.global.L2: drop a 128-byte L2 line without writing it back (a weak write of an undefined
+// value, ordered by the same release/acquire as a store).  The drained diagonal sums are dead once
+// folded; without this the dirty scratch lines are evicted to DRAM by the streaming baby-step
+// planes before the ping-pong rewrites them (round 1: ~1.8 GB of the 8.5 GB per config-5 launch).
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" :: "l"(p) : "memory");
+}
+
 template <int G>
 __device__ __forceinline__ void fold_row(const u32* __restrict__ rr_, u64* __restrict__ prow, u64 kbase, u32 npts,
-                                         u64 C64, u64 C96, u64 C128, const ModParams& mp, u32 vbeg, u32 vend) {
+                                         u64 C64, u64 C96, u64 C128, const ModParams& mp, u32 vbeg, u32 vend,
+                                         bool disc) {
+  const bool line_head = (threadIdx.x & 7) == 0;   // 8 consecutive rows x 16 B = one 128-B line
 #pragma unroll 1
   for (u32 v0 = vbeg; v0 < vend; v0 += 4) {
     u32 D[kDiag][4];
@@ -572,6 +583,16 @@ __device__ __forceinline__ void fold_row(const u32* __restrict__ rr_, u64* __res
       // the baby-step planes hold Montgomery residues m^v 2^64 (k_tc_rplanes), so the sum is
       // 2^64 X: one REDC (x 2^-64) is the reduction; REDC needs its high word < p
       res[j] = redc(hi < mp.p ? hi : hi % mp.p, lo, mp);
+    }
+    if (disc) {
+      // every lane's loads of this v0 group were consumed above; once the warp has converged, the
+      // warp's 4 lines per diagonal (its 32 rows x 16 B) are dead
+      __syncwarp();
+      if (line_head) {
+#pragma unroll
+        for (int di = 0; di < kDiag; ++di)
+          if (group_diag(G, di) >= 0) discard_l2(rr_ + (u32)di * (kU * kV) + (v0 >> 2) * (kU * 4));
+      }
     }
     if (kbase + v0 + 4 <= npts) {
       ulonglong2* dst = (ulonglong2*)(prow + kbase + v0);
@@ -856,10 +877,10 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
         }
         const u32* rr_ = raw + (u64)ur * 4;
         const u64 kbase = (u64)chunk * kChunk + (u64)ur * kV;   // multiple of 8; ldp multiple of 8
-        if (MODE == 2) fold_row<2>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
-        else if (MODE == 3 && g == 1) fold_row<4>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
-        else if (g == 0) fold_row<0>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
-        else fold_row<1>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend);
+        if (MODE == 2) fold_row<2>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
+        else if (MODE == 3 && g == 1) fold_row<4>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
+        else if (g == 0) fold_row<0>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
+        else fold_row<1>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
       }
       if (PROF) T[2] += clk() - c2;
     }
