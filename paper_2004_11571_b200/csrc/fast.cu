@@ -53,7 +53,7 @@ struct PrimeC {
 struct Consts {
   PrimeC pr[kNP];
   uint2 ginv[kNP][kNP];   // Garner: q_i^{-1} mod q_j (i < j) and its Shoup companion
-  u64 qmodp[kNP];         // q_i mod p
+  u64 qmodp[kNP];         // q_i 2^64 mod p (Montgomery form of q_i mod p)
 };
 
 // ---------------------------------------------------------------- 32-bit modular helpers
@@ -76,38 +76,76 @@ __device__ __forceinline__ u32 reduce_q(u64 x, const PrimeC& P) {
 }
 
 // ---------------------------------------------------------------- shared-memory NTTs
-// X holds `nunits` transforms of S points each (S = 2^lg), values in [0, 2q).  Forward: DIF
-// (Gentleman-Sande), natural order in, bit-reversed out.  Twiddles tw[len + i] = w_{2len}^i.
-__device__ __forceinline__ void ntt_dif(u32* X, int lg, u32 npts, const uint2* __restrict__ tw, u32 q) {
+// X holds transforms of S = 2^lg points each (npts points in all), values in [0, 2q), stored with
+// one pad word per 32 (phys): every pass below reads each thread's elements at a power-of-two stride,
+// and the pad makes the warp's 32 accesses hit 32 distinct banks for every stride.
+// Forward: DIF (Gentleman-Sande), natural order in, bit-reversed out, twiddles tw[len + i] =
+// w_{2len}^i.  Inverse: DIT (Cooley-Tukey), bit-reversed in, natural out, inverse twiddles.
+// Stages run in passes of up to 4: a thread loads 16 elements (indices base + c 2^{s_bot}), does the
+// pass's stages in registers and stores them back -- 4 shared-memory round trips and barriers for
+// an 8192-point transform instead of 13.
+__device__ __forceinline__ u32 phys(u32 i) { return i + (i >> 5); }
+constexpr u32 padded(u32 n) { return n + (n >> 5); }
+
+template <int R, bool FWD>
+__device__ __forceinline__ void ntt_pass(u32* X, int s_bot, u32 npts, const uint2* __restrict__ tw, u32 q) {
+  constexpr int E = 1 << R;
   const u32 q2 = 2 * q;
-  for (int s = lg - 1; s >= 0; --s) {
-    const u32 len = 1u << s;
-    for (u32 b = threadIdx.x; b < npts / 2; b += blockDim.x) {
-      const u32 i = b & (len - 1);
-      const u32 pos = ((b >> s) << (s + 1)) | i;   // unit * S + block * 2len + i
-      const u32 u = X[pos], v = X[pos + len];
-      const uint2 w = tw[len + i];
-      X[pos] = red2q(u + v, q2);
-      X[pos + len] = shoup32(u - v + q2, w.x, w.y, q);
+  const u32 ngroups = npts >> R;
+  for (u32 gi = threadIdx.x; gi < ngroups; gi += blockDim.x) {
+    const u32 lo = gi & ((1u << s_bot) - 1);
+    const u32 base = ((gi >> s_bot) << (s_bot + R)) | lo;   // R zero bits inserted at s_bot
+    u32 v[E];
+#pragma unroll
+    for (int c = 0; c < E; ++c) v[c] = X[phys(base + ((u32)c << s_bot))];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int st = FWD ? R - 1 - k : k;               // DIF: top stage first; DIT: bottom first
+      const int s = s_bot + st;
+      const u32 len = 1u << s;
+#pragma unroll
+      for (int c = 0; c < E; ++c) {
+        if (c & (1 << st)) continue;
+        const int c2 = c | (1 << st);
+        const u32 i = (base + ((u32)c << s_bot)) & (len - 1);
+        const uint2 w = tw[len + i];
+        const u32 u = v[c], x = v[c2];
+        if (FWD) {
+          v[c] = red2q(u + x, q2);
+          v[c2] = shoup32(u - x + q2, w.x, w.y, q);
+        } else {
+          const u32 t = shoup32(x, w.x, w.y, q);
+          v[c] = red2q(u + t, q2);
+          v[c2] = red2q(u - t + q2, q2);
+        }
+      }
     }
-    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < E; ++c) X[phys(base + ((u32)c << s_bot))] = v[c];
+  }
+  __syncthreads();
+}
+template <bool FWD>
+__device__ __forceinline__ void ntt_run(u32* X, int s_bot, int R, u32 npts, const uint2* tw, u32 q) {
+  switch (R) {
+    case 4: ntt_pass<4, FWD>(X, s_bot, npts, tw, q); break;
+    case 3: ntt_pass<3, FWD>(X, s_bot, npts, tw, q); break;
+    case 2: ntt_pass<2, FWD>(X, s_bot, npts, tw, q); break;
+    default: ntt_pass<1, FWD>(X, s_bot, npts, tw, q); break;
   }
 }
-// Inverse: DIT (Cooley-Tukey), bit-reversed in, natural out, inverse twiddles.
+__device__ __forceinline__ void ntt_dif(u32* X, int lg, u32 npts, const uint2* __restrict__ tw, u32 q) {
+  for (int top = lg - 1; top >= 0;) {
+    const int R = top + 1 < 4 ? top + 1 : 4;
+    ntt_run<true>(X, top - R + 1, R, npts, tw, q);
+    top -= R;
+  }
+}
 __device__ __forceinline__ void ntt_dit(u32* X, int lg, u32 npts, const uint2* __restrict__ tw, u32 q) {
-  const u32 q2 = 2 * q;
-  for (int s = 0; s < lg; ++s) {
-    const u32 len = 1u << s;
-    for (u32 b = threadIdx.x; b < npts / 2; b += blockDim.x) {
-      const u32 i = b & (len - 1);
-      const u32 pos = ((b >> s) << (s + 1)) | i;
-      const u32 u = X[pos];
-      const uint2 w = tw[len + i];
-      const u32 t = shoup32(X[pos + len], w.x, w.y, q);
-      X[pos] = red2q(u + t, q2);
-      X[pos + len] = red2q(u - t + q2, q2);
-    }
-    __syncthreads();
+  for (int bot = 0; bot < lg;) {
+    const int R = lg - bot < 4 ? lg - bot : 4;
+    ntt_run<false>(X, bot, R, npts, tw, q);
+    bot += R;
   }
 }
 
@@ -121,6 +159,7 @@ struct Call {
   u64 rstride;
   u32 nops, nouts, njobs;
   u32 Lc, Lo, Bk, nb, nbo, lg;          // operand length, output length, block, blocks, out blocks, log2 S
+  u32 lgnb, lgnops, lgnouts, lgnbo, lgLo, lgBk;   // the same as shifts (all powers of two)
   int kind;                             // kMerge / kMul / kTwoMinus
   // outputs
   u64* dst[2];
@@ -151,19 +190,19 @@ __global__ void __launch_bounds__(512) k_fast_fwd(Call a) {
   const u32 u0 = blockIdx.x * per;
   const u32 nu = min(per, nunits - u0), npts = nu * S;
   for (u32 x = threadIdx.x; x < npts; x += blockDim.x) {
-    const u32 u = u0 + x / S, i = x % S;
-    const u32 blk = u % a.nb, o = (u / a.nb) % a.nops, job = u / (a.nb * a.nops);
+    const u32 u = u0 + (x >> a.lg), i = x & (S - 1);
+    const u32 blk = u & (a.nb - 1), o = (u >> a.lgnb) & (a.nops - 1), job = u >> (a.lgnb + a.lgnops);
     u32 v = 0;
     if (i < a.Bk) {
       const u64* src = op_ptr(a, job, o);
       if (src) v = reduce_q(src[(u64)blk * a.Bk + i], P);
     }
-    X[x] = v;
+    X[phys(x)] = v;
   }
   __syncthreads();
   ntt_dif(X, a.lg, npts, a.twf + (u64)j * kSmax, P.q);
   u32* out = a.spec + ((u64)j * nunits + u0) * S;
-  for (u32 x = threadIdx.x; x < npts; x += blockDim.x) out[x] = X[x];
+  for (u32 x = threadIdx.x; x < npts; x += blockDim.x) out[x] = X[phys(x)];
 }
 
 // Pointwise products + inverse: unit = (job, out, out block c) of prime blockIdx.y.
@@ -180,8 +219,8 @@ __global__ void __launch_bounds__(512) k_fast_pwinv(Call a) {
   const u64 opstride = (u64)a.nb * S;                       // one operand's spectra
   const u32* spec = a.spec + (u64)j * a.njobs * a.nops * opstride;
   for (u32 x = threadIdx.x; x < npts; x += blockDim.x) {
-    const u32 u = u0 + x / S, i = x % S;
-    const u32 c = u % a.nbo, out = (u / a.nbo) % a.nouts, job = u / (a.nbo * a.nouts);
+    const u32 u = u0 + (x >> a.lg), i = x & (S - 1);
+    const u32 c = u & (a.nbo - 1), out = (u >> a.lgnbo) & (a.nouts - 1), job = u >> (a.lgnbo + a.lgnouts);
     const u32* J = spec + (u64)job * a.nops * opstride + i;
     u32 acc = 0;
     const int npair = (a.kind == kMerge && out == 0) ? 2 : 1;
@@ -200,14 +239,14 @@ __global__ void __launch_bounds__(512) k_fast_pwinv(Call a) {
         acc = red2q(acc + mont32(A, B, P.q, P.qinv_neg), q2);
       }
     }
-    X[x] = acc;
+    X[phys(x)] = acc;
   }
   __syncthreads();
   ntt_dit(X, a.lg, npts, a.twi + (u64)j * kSmax, P.q);
   const uint2 sc = a.scale[j * (kLgMax + 1) + a.lg];       // S^-1 2^32: undoes the transform and mont32
   u32* out = a.res + ((u64)j * nunits + u0) * S;
   for (u32 x = threadIdx.x; x < npts; x += blockDim.x) {
-    u32 v = red2q(shoup32(X[x], sc.x, sc.y, P.q), P.q);
+    u32 v = red2q(shoup32(X[phys(x)], sc.x, sc.y, P.q), P.q);
     out[x] = v;
   }
 }
@@ -231,7 +270,7 @@ __device__ __forceinline__ u64 crt_modp(const u32 (&r)[kNP], const Consts& C, co
   u64 y = v[kNP - 1] < mp.p ? v[kNP - 1] : v[kNP - 1] % mp.p;
 #pragma unroll
   for (int i = kNP - 2; i >= 0; --i) {
-    y = mulmod(y, C.qmodp[i], mp);
+    y = mont_mul(y, C.qmodp[i], mp);   // y q_i mod p (qmodp in Montgomery form)
     const u64 vi = v[i] < mp.p ? v[i] : v[i] % mp.p;
     y += vi;
     y = y >= mp.p ? y - mp.p : y;
@@ -249,7 +288,7 @@ __global__ void k_fast_crt(Call a) {
   const u32 S = 1u << a.lg;
   const u64 p = a.mp.p;
   for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
-    const u32 job = (u32)(x / a.Lo), k = (u32)(x % a.Lo);
+    const u32 job = (u32)(x >> a.lgLo), k = (u32)(x & (a.Lo - 1));
     u64 conv[2];
     const int shift = a.kind == kMerge ? 1 : 0;
     for (u32 o = 0; o < a.nouts; ++o) {
@@ -260,11 +299,11 @@ __global__ void k_fast_crt(Call a) {
       for (int jj = 0; jj < kNP; ++jj) {
         const u32 q = a.C.pr[jj].q;
         const u32* R = a.res + (((u64)jj * a.njobs + job) * a.nouts + o) * a.nbo * S;
-        const u32 c = K / a.Bk;
+        const u32 c = K >> a.lgBk;
         u32 acc = 0;
-        if (c < a.nbo) acc = R[(u64)c * S + (K - c * a.Bk)];
+        if (c < a.nbo) acc = R[(u64)c * S + (K - (c << a.lgBk))];
         if (c >= 1 && c - 1 < a.nbo) {
-          acc += R[(u64)(c - 1) * S + (K - (c - 1) * a.Bk)];
+          acc += R[(u64)(c - 1) * S + (K - ((c - 1) << a.lgBk))];
           acc = acc >= q ? acc - q : acc;
         }
         r[jj] = acc;
@@ -294,6 +333,74 @@ __global__ void k_fast_crt(Call a) {
   }
 }
 
+// Fused tree merge for short operands (S = 2 Lc <= kFusedS): a CTA holds kFusedS / S jobs and runs
+// the whole product in shared memory -- per prime the 4 operands mod q (one array of 4 x npts
+// points: DIF over every S-point unit at once), pointwise P = N1 E2 + N2 E1 and Q = E1 E2, the 2
+// inverse transforms, residues kept in shared memory -- then Garner CRT and the merge epilogue
+// straight into the next level.  Global traffic: the children (L2-resident across the 5 primes)
+// and the parents, instead of spectra and residues.
+constexpr u32 kFusedS = 1024;
+constexpr u32 kFusedSmem = (padded(4 * kFusedS) + 2 * kNP * kFusedS) * sizeof(u32);   // 58 KB: 3 CTAs per SM
+__global__ void __launch_bounds__(512) k_fast_merge_fused(Call a) {
+  extern __shared__ u32 sm[];
+  u32* W = sm;                       // [4][npts]: N1, E1, N2, E2 of the CTA's jobs (P, Q after the products)
+  u32* Rz = sm + padded(4 * kFusedS);   // [kNP][2][npts] residues of P and Q (W is padded: phys)
+  const u32 S = 1u << a.lg, per = kFusedS >> a.lg;
+  const u32 job0 = blockIdx.x * per;
+  const u32 nj = min(per, a.njobs - job0), npts = nj * S;
+  for (int jp = 0; jp < kNP; ++jp) {
+    const PrimeC P = a.C.pr[jp];
+    for (u32 x = threadIdx.x; x < 4 * npts; x += blockDim.x) {
+      const u32 o = x >= 2 * npts ? (x >= 3 * npts ? 3u : 2u) : (x >= npts ? 1u : 0u);
+      const u32 r = x - o * npts, jj = r >> a.lg, i = r & (S - 1);
+      u32 v = 0;
+      if (i < a.Lc) {
+        const u64* src = op_ptr(a, job0 + jj, o);
+        if (src) v = reduce_q(src[i], P);
+      }
+      W[phys(x)] = v;
+    }
+    __syncthreads();
+    ntt_dif(W, a.lg, 4 * npts, a.twf + (u64)jp * kSmax, P.q);
+    const u32 q2 = 2 * P.q;
+    for (u32 x = threadIdx.x; x < npts; x += blockDim.x) {
+      const u32 n1 = W[phys(x)], e1 = W[phys(npts + x)], n2 = W[phys(2 * npts + x)], e2 = W[phys(3 * npts + x)];
+      W[phys(x)] = red2q(mont32(n1, e2, P.q, P.qinv_neg) + mont32(n2, e1, P.q, P.qinv_neg), q2);
+      W[phys(npts + x)] = mont32(e1, e2, P.q, P.qinv_neg);
+    }
+    __syncthreads();
+    ntt_dit(W, a.lg, 2 * npts, a.twi + (u64)jp * kSmax, P.q);
+    const uint2 sc = a.scale[jp * (kLgMax + 1) + a.lg];
+    for (u32 x = threadIdx.x; x < 2 * npts; x += blockDim.x)
+      Rz[(u32)jp * 2 * kFusedS + x] = red2q(shoup32(W[phys(x)], sc.x, sc.y, P.q), P.q);
+    __syncthreads();
+  }
+  const u64 p = a.mp.p;
+  for (u32 x = threadIdx.x; x < nj * a.Lo; x += blockDim.x) {
+    const u32 jj = x >> a.lgLo, k = x & (a.Lo - 1), job = job0 + jj;
+    u64 conv[2] = {0, 0};
+    if (k >= 1) {
+      for (int o = 0; o < 2; ++o) {
+        u32 r[kNP];
+#pragma unroll
+        for (int jp = 0; jp < kNP; ++jp) r[jp] = Rz[(u32)jp * 2 * kFusedS + (u32)o * npts + jj * S + k - 1];
+        conv[o] = crt_modp(r, a.C, a.mp);
+      }
+    }
+    const u64* N1 = op_ptr(a, job, 0);
+    const u64* E1 = op_ptr(a, job, 1);
+    const u64* N2 = op_ptr(a, job, 2);
+    const u64* E2 = op_ptr(a, job, 3);
+    u64 n = conv[0], e = conv[1];
+    if (k < a.Lc) {
+      if (N1) { n = addp(n, N1[k], p); e = addp(e, E1[k], p); }
+      if (N2) { n = addp(n, N2[k], p); e = addp(e, E2[k], p); }
+    }
+    a.dst[0][(u64)job * a.dstride + k] = n;
+    a.dst[1][(u64)job * a.dstride + k] = e;
+  }
+}
+
 // Leaves to level 5: warp w of the CTA owns padded terms 32 g .. 32 g + 31 (g = global group); a_i =
 // c_i m_i^{j0}, leaf (N, E) = (a_i, -m_i); five levels of pairwise merges in shared memory by
 // schoolbook products mod p; the level-5 node (length min(32, T2)) goes to N5[g], E5[g].
@@ -306,8 +413,9 @@ __global__ void __launch_bounds__(128) k_fast_leaf(const u64* __restrict__ c, co
   for (u64 g = blockIdx.x * 4ull + w; g < ngroups; g += (u64)gridDim.x * 4) {
     const u64 q = g * 32 + lane;
     const u64 mi = m[q];
-    sN[w][0][lane] = seed_pow(c[q], mi, j0, mp);
-    sE[w][0][lane] = mi == 0 ? 0 : p - mi;
+    // Montgomery form inside the warp (one REDC per product), normal form out
+    sN[w][0][lane] = to_mont(seed_pow(c[q], mi, j0, mp), mp);
+    sE[w][0][lane] = to_mont(mi == 0 ? 0 : p - mi, mp);
     __syncwarp();
     int cur = 0;
     for (int lc = 1; lc < 32; lc <<= 1) {   // child length lc, output length 2 lc
@@ -322,9 +430,9 @@ __global__ void __launch_bounds__(128) k_fast_leaf(const u64* __restrict__ c, co
       for (int x = 0; x < lc && x <= k - 1; ++x) {
         const int y = k - 1 - x;
         if (y >= lc) continue;
-        n = addp(n, mulmod(n1[x], e2[y], mp), p);
-        n = addp(n, mulmod(n2[x], e1[y], mp), p);
-        e = addp(e, mulmod(e1[x], e2[y], mp), p);
+        n = addp(n, mont_mul(n1[x], e2[y], mp), p);
+        n = addp(n, mont_mul(n2[x], e1[y], mp), p);
+        e = addp(e, mont_mul(e1[x], e2[y], mp), p);
       }
       sN[w][cur ^ 1][lane] = n;
       sE[w][cur ^ 1][lane] = e;
@@ -332,8 +440,8 @@ __global__ void __launch_bounds__(128) k_fast_leaf(const u64* __restrict__ c, co
       cur ^= 1;
     }
     if ((u32)lane < L5) {
-      N5[g * L5 + lane] = sN[w][cur][lane];
-      E5[g * L5 + lane] = sE[w][cur][lane];
+      N5[g * L5 + lane] = from_mont(sN[w][cur][lane], mp);
+      E5[g * L5 + lane] = from_mont(sE[w][cur][lane], mp);
     }
     __syncwarp();
   }
@@ -525,7 +633,7 @@ int create(const std::vector<u64>& poff, const ModParams& mp, cudaStream_t s, Pl
     pc.qinv_neg = (u32)0 - inv;
     pc.bar = (u64)(((u128)1 << 64) / q);
     for (int i = 0; i < j; ++i) P->C.ginv[j][i] = shoup_pair(hpow(kQ[i] % q, q - 2, q), q);
-    P->C.qmodp[j] = kQ[j] % mp.p;
+    P->C.qmodp[j] = (u64)((((u128)(kQ[j] % mp.p)) << 64) % mp.p);
   }
   if (rc == PE_OK) {
     if (cudaMallocAsync((void**)&P->d_twf, twf.size() * sizeof(uint2), s) != cudaSuccess ||
@@ -566,23 +674,36 @@ static int run_call(Plan* P, Call& a, cudaStream_t s) {
   a.nb = a.Lc / a.Bk;
   a.lg = ilog2(2ull * a.Bk);
   const u32 S = 1u << a.lg;
+  // output blocks: the block-pair sums a + b = c needed for coefficients < Lo (c <= 2nb - 2; a
+  // power of two so the kernels split unit indices with shifts -- an extra c = 2nb - 1 has no pairs)
   if (a.nb == 1) a.nbo = 1;
-  else a.nbo = std::min<u32>((a.Lo + a.Bk - 1) / a.Bk, 2 * a.nb - 1);
+  else a.nbo = std::min<u32>((a.Lo + a.Bk - 1) / a.Bk, 2 * a.nb);
+  a.lgnb = ilog2(a.nb); a.lgnops = ilog2(a.nops); a.lgnouts = ilog2(a.nouts); a.lgnbo = ilog2(a.nbo);
+  a.lgLo = ilog2(a.Lo); a.lgBk = ilog2(a.Bk);
+  a.twf = P->d_twf;
+  a.twi = P->d_twi;
+  a.scale = P->d_scale;
+  a.C = P->C;
+  if (a.kind == kMerge && S <= kFusedS && !getenv("PE_FAST_NOFUSE")) {   // short operands: one fused kernel
+    if (a.njobs == 0) return PE_OK;
+    const u32 per = kFusedS / S;
+    FCU(cudaFuncSetAttribute(k_fast_merge_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem));
+    k_fast_merge_fused<<<(a.njobs + per - 1) / per, 512, kFusedSmem, s>>>(a);
+    FCU(cudaGetLastError());
+    return PE_OK;
+  }
+
   if (a.njobs == 0) return PE_OK;
   const u64 nspec = (u64)kNP * a.njobs * a.nops * a.nb * S;
   const u64 nres = (u64)kNP * a.njobs * a.nouts * a.nbo * S;
   if (grow(&P->d_spec, P->spec_elems, nspec, s) || grow(&P->d_res, P->res_elems, nres, s)) return PE_ENOMEM;
   a.spec = P->d_spec;
   a.res = P->d_res;
-  a.twf = P->d_twf;
-  a.twi = P->d_twi;
-  a.scale = P->d_scale;
-  a.C = P->C;
   const u32 per = std::max<u32>(1, kTile >> a.lg);
-  const u32 smem = per * S * sizeof(u32);
+  const u32 smem = padded(per * S) * sizeof(u32);
   const u32 threads = std::min<u32>(512, std::max<u32>(32, per * S / 2));
-  FCU(cudaFuncSetAttribute(k_fast_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * 4));
-  FCU(cudaFuncSetAttribute(k_fast_pwinv, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * 4));
+  FCU(cudaFuncSetAttribute(k_fast_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, padded(kTile) * 4));
+  FCU(cudaFuncSetAttribute(k_fast_pwinv, cudaFuncAttributeMaxDynamicSharedMemorySize, padded(kTile) * 4));
   const u32 nu_f = a.njobs * a.nops * a.nb, nu_i = a.njobs * a.nouts * a.nbo;
   k_fast_fwd<<<dim3((nu_f + per - 1) / per, kNP), threads, smem, s>>>(a);
   FCU(cudaGetLastError());

@@ -12,6 +12,7 @@
 #include <cub/iterator/counting_input_iterator.cuh>
 
 #include <algorithm>
+#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -120,17 +121,26 @@ struct pe_ctx {
   // tensor-core path (tc.cuh): 0 off, 1 auto (T >= tc_min_T(t_pad)), 2 forced
   int tc_mode = 0;
   bool tc_ok = false;
-  u32 tc_npieces = 0, tc_nslots = 0;
+  u32 tc_rounds = 2;
   int n_sm = 148;
   u64* d_tcC = nullptr;   // [t_pad][2] tensor-core path C records (tc.cuh)
   u64* d_tcMS = nullptr;  // [t_pad][2] Montgomery m^V, m^{kChunk} (k_tc_seed)
   uint8_t* d_tcR = nullptr;   // [t_pad / 32][tc::kRBytes] baby-step byte planes m^v, v < 64 (tc.cuh)
-  uint4* d_piece = nullptr;
-  u32* d_tc_slot_start = nullptr;
   u64* d_seed = nullptr;
   size_t seed_elems = 0;
   u32* d_tc_scratch = nullptr;   // k_tc per-CTA drained diagonal sums (n_sm x 2 x kDiag x kChunk u32)
   u32* h_status = nullptr;       // mapped host word: k_tc sets it when a pipeline wait times out
+  // k_tc piece plans, one per chunk count of a pass (tc_plan): pieces, partial slots, unit schedule
+  struct TcPlan {
+    u32 npieces = 0, nslots = 0, grid = 0;
+    std::vector<uint4> pieces;       // x = first padded term, y = K-blocks, z = slot (size-sorted)
+    std::vector<u32> slot_start;     // [G+1] partial slots of bucket g (x rounds)
+    std::vector<u32> sched;          // [nunits] units per CTA, then [grid + 1] offsets
+    uint4* d_piece = nullptr;
+    u32* d_slot_start = nullptr;
+    u32* d_sched = nullptr;
+  };
+  std::map<u32, TcPlan> tc_plans;
   // asymptotically fast method (fast.cu, NEXT-4): 0 off, 1 automatic (T >= fast_min_T), 2 forced
   int fast_mode = 0;
   u64 fast_min_T = 0;
@@ -157,9 +167,12 @@ static void free_all(pe_ctx* h) {
   cudaStream_t s = h->stream;
   for (void* q : {(void*)h->d_c, (void*)h->d_m, (void*)h->d_w, (void*)h->d_perm, (void*)h->d_wt_info, (void*)h->d_slot_start, (void*)h->d_partial,
                   (void*)h->d_out_scratch, (void*)h->d_tcC, (void*)h->d_tcR, (void*)h->d_tcMS,
-                  (void*)h->d_tc_scratch, (void*)h->d_piece, (void*)h->d_tc_slot_start,
-                  (void*)h->d_seed})
+                  (void*)h->d_tc_scratch, (void*)h->d_seed})
     if (q) cudaFreeAsync(q, s);
+  for (auto& kv : h->tc_plans)
+    for (void* q : {(void*)kv.second.d_piece, (void*)kv.second.d_slot_start, (void*)kv.second.d_sched})
+      if (q) cudaFreeAsync(q, s);
+  h->tc_plans.clear();
   if (s) cudaStreamSynchronize(s);
   if (h->copy_stream) cudaStreamSynchronize(h->copy_stream), cudaStreamDestroy(h->copy_stream);
   if (h->copy_done) cudaEventDestroy(h->copy_done);
@@ -426,8 +439,6 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   CU(cudaMemcpyAsync(h->d_slot_start, slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
 
   // ---- tensor-core path (tc.cuh): per-term strides + the piece plan
-  std::vector<uint4> pieces;
-  std::vector<u32> tc_slot_start(G + 1);
   if (h->tc_mode != 0 && (h->path == kInt4 || h->path == kInt2 || h->path == kFp64 || h->path == kInt32)) {
     const u64 tp = h->t_pad;
     // handle memory of the tensor-core form: C records + seed powers + baby-step planes (DESIGN.md
@@ -457,39 +468,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
     tc::k_tc_rplanes<<<(unsigned)std::max<u64>(1, std::min<u64>(nrp, 148ull * 16)), tc::kRpThreads, 0, s>>>(
         h->d_m, tp, h->d_tcR, h->mp);
     CU(cudaGetLastError());
-    // pieces: each bucket's padded range split into ceil(n / kPieceMax) near-equal runs of whole
-    // K-blocks (<= kPieceMax terms keeps every int32 diagonal sum exact); slots contiguous per bucket
-    // piece size: <= kPieceMax (exactness), and <= twice the average per-CTA load so one large
-    // bucket cannot bound the kernel time of a small problem (every unit also pays a fixed
-    // epilogue -- 2 drains + one fold -- so pieces stay >= 1024 terms)
     CU(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
-    u64 piece_max = 2 * ((tp + h->n_sm - 1) / h->n_sm);
-    piece_max = std::min<u64>(std::max<u64>(piece_max, 1024), tc::kPieceMax);
-    const int pm_env = env_int("PE_TC_PIECE", 0);   // testing: force small pieces (many units per CTA)
-    if (pm_env > 0) piece_max = std::min<u64>((u64)pm_env, tc::kPieceMax);
-    piece_max = (piece_max + tc::kKB - 1) / tc::kKB * tc::kKB;
-    for (u64 g = 0; g < G; ++g) {
-      tc_slot_start[g] = (u32)pieces.size();
-      const u64 nkb = (poff[g + 1] - poff[g]) / tc::kKB;   // poff multiples of 32R
-      const u64 maxkb = piece_max / tc::kKB;
-      const u64 np_g = (nkb + maxkb - 1) / maxkb;
-      u64 kb0 = 0;
-      for (u64 k = 0; k < np_g; ++k) {
-        const u64 len = nkb / np_g + (k < nkb % np_g ? 1 : 0);
-        pieces.push_back(make_uint4((u32)(poff[g] + kb0 * tc::kKB), (u32)len, (u32)pieces.size(), 0));
-        kb0 += len;
-      }
-    }
-    tc_slot_start[G] = (u32)pieces.size();
-    std::stable_sort(pieces.begin(), pieces.end(), [](const uint4& x, const uint4& y) { return x.y > y.y; });
-    // one partial row per (piece, diagonal round): k_tc reduces each round's part on its own
-    h->tc_npieces = (u32)pieces.size();
-    const u32 rounds = h->p < (1ull << 31) ? 1 : tc::kRounds;   // 4-byte digits: one round
-    h->tc_nslots = (u32)pieces.size() * rounds;
-    for (auto& x : tc_slot_start) x *= rounds;
-    if (dalloc(&h->d_piece, pieces.size()) || dalloc(&h->d_tc_slot_start, G + 1)) return g_last_error;
-    CU(cudaMemcpyAsync(h->d_piece, pieces.data(), pieces.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(h->d_tc_slot_start, tc_slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
+    h->tc_rounds = h->p < (1ull << 31) ? 1 : tc::kRounds;   // 4-byte digits: one round
     if (cudaHostAlloc((void**)&h->h_status, sizeof(u32), cudaHostAllocMapped) != cudaSuccess) return set_err(PE_ENOMEM);
     *h->h_status = 0;
     h->tc_ok = true;
@@ -645,10 +625,131 @@ static int ensure_partial(pe_ctx* h, size_t need, cudaStream_t s) {
   return PE_OK;
 }
 
+// k_tc piece plan for a pass of nch chunks (host part cached per nch; device copies on first use).
+// Pieces: each bucket's padded range cut into near-equal runs of whole K-blocks of at most maxkb
+// K-blocks -- <= kPieceMax terms keeps every int32 diagonal sum exact (tc.cuh) -- with maxkb chosen
+// so the launch has about kUnitsPerCta units (piece, chunk, round) per CTA: enough to balance a
+// small launch (a 1/8 term shard of config 5), while a large one keeps the 8192-term maximum.
+// Schedule (longest processing time first, by piece): pieces in decreasing size, the nch x rounds
+// units of a piece dealt to the currently least-loaded CTAs (cost = K-blocks + ~4 for the unit's
+// epilogue and pipeline fill), so the units sharing a piece's baby-step planes sit at the same
+// load level of neighbouring CTAs and run side by side (one DRAM read of the planes, L2 for the
+// rest -- the round-1 snake order's property).  env PE_TC_PIECE (terms) / PE_TC_UPC override.
+static const u32 kUnitsPerCta = 6;
+static int tc_plan(pe_ctx* h, u32 nch, bool upload, cudaStream_t s, pe_ctx::TcPlan** out) {
+  auto it = h->tc_plans.find(nch);
+  pe_ctx::TcPlan* P = nullptr;
+  if (it == h->tc_plans.end()) {
+    P = &h->tc_plans[nch];
+    const u64 G = h->G, tkb = h->t_pad / tc::kKB;
+    const u32 rounds = h->tc_rounds;
+    u64 maxkb;
+    const int pm_env = env_int("PE_TC_PIECE", 0), upc = env_int("PE_TC_UPC", (int)kUnitsPerCta);
+    if (pm_env > 0) {
+      maxkb = std::max<u64>(1, (u64)pm_env / tc::kKB);
+    } else if (upc <= 0) {   // round-1 rule: pieces of up to twice the per-SM share
+      maxkb = 2 * ((h->t_pad + h->n_sm - 1) / h->n_sm) / tc::kKB;
+      maxkb = std::max<u64>(maxkb, 1024 / tc::kKB);
+    } else {
+      maxkb = (tkb * nch * rounds + (u64)h->n_sm * upc - 1) / ((u64)h->n_sm * upc);
+      maxkb = std::max<u64>(maxkb, 1024 / tc::kKB);
+    }
+    maxkb = std::min<u64>(maxkb, tc::kPieceMax / tc::kKB);
+    std::vector<u32> slot(G + 1);
+    for (u64 g = 0; g < G; ++g) {
+      slot[g] = (u32)P->pieces.size();
+      const u64 nkb = (h->h_poff[g + 1] - h->h_poff[g]) / tc::kKB;   // poff multiples of 32R
+      const u64 np_g = (nkb + maxkb - 1) / maxkb;
+      u64 kb0 = 0;
+      for (u64 k = 0; k < np_g; ++k) {
+        const u64 len = nkb / np_g + (k < nkb % np_g ? 1 : 0);
+        P->pieces.push_back(make_uint4((u32)(h->h_poff[g] + kb0 * tc::kKB), (u32)len, (u32)P->pieces.size(), 0));
+        kb0 += len;
+      }
+    }
+    slot[G] = (u32)P->pieces.size();
+    std::stable_sort(P->pieces.begin(), P->pieces.end(), [](const uint4& x, const uint4& y) { return x.y > y.y; });
+    // one partial row per (piece, diagonal round): k_tc reduces each round's part on its own
+    P->npieces = (u32)P->pieces.size();
+    P->nslots = P->npieces * rounds;
+    for (auto& x : slot) x *= rounds;
+    P->slot_start = std::move(slot);
+    // schedule
+    const u32 upp = nch * rounds, nunits = P->npieces * upp;
+    const u32 grid = (u32)std::min<u64>(nunits, (u64)h->n_sm);
+    P->grid = grid;
+    std::vector<std::pair<u64, u32>> heap;   // (load, cta), min-heap
+    for (u32 b = 0; b < grid; ++b) heap.push_back({0, b});
+    auto cmp = [](const std::pair<u64, u32>& x, const std::pair<u64, u32>& y) {
+      return x.first != y.first ? x.first > y.first : x.second > y.second;
+    };
+    std::make_heap(heap.begin(), heap.end(), cmp);
+    // (a) snake: units in piece-major order, row r of `grid` units dealt left to right for even r,
+    //     right to left for odd r (the round-1 order: with ~50 units per CTA its makespan is within
+    //     0.5 % of the mean and a piece's units start together);
+    // (b) LPT by piece (below).  The cost model picks (b) only when it shortens the makespan by > 3 %
+    //     -- launches with few units per CTA, e.g. one term shard of a multi-GPU run.
+    std::vector<std::vector<u32>> snake(grid), lists(grid);
+    std::vector<u64> sload(grid, 0);
+    for (u32 u = 0; u < nunits; ++u) {
+      const u32 row = u / grid, col = u % grid, b = (row & 1) ? grid - 1 - col : col;
+      snake[b].push_back(u);
+      sload[b] += (u64)P->pieces[u / upp].y + 4;
+    }
+    std::vector<std::pair<u64, u32>> took;
+    for (u32 pc = 0; pc < P->npieces; ++pc) {   // pieces are size-sorted: LPT order
+      const u64 cost = (u64)P->pieces[pc].y + 4;
+      took.clear();
+      for (u32 k = 0; k < upp; ++k) {
+        if (took.size() == grid) {              // more units than CTAs: reuse the least loaded again
+          for (auto& x : took) { heap.push_back(x); std::push_heap(heap.begin(), heap.end(), cmp); }
+          took.clear();
+        }
+        std::pop_heap(heap.begin(), heap.end(), cmp);
+        auto top = heap.back();
+        heap.pop_back();
+        lists[top.second].push_back(pc * upp + k);   // unit = (piece * nch + chunk) * rounds + g
+        top.first += cost;
+        took.push_back(top);
+      }
+      for (auto& x : took) { heap.push_back(x); std::push_heap(heap.begin(), heap.end(), cmp); }
+    }
+    u64 lpt_max = 0, snake_max = 0;
+    for (auto& x : heap) lpt_max = std::max(lpt_max, x.first);
+    for (u64 x : sload) snake_max = std::max(snake_max, x);
+    const int sch = env_int("PE_TC_SCHED", -1);   // testing: 0 snake, 1 LPT
+    if (sch == 0 || (sch < 0 && !(lpt_max * 100 < snake_max * 97))) lists.swap(snake);
+    P->sched.assign(nunits + grid + 1, 0);
+    u32 o = 0;
+    for (u32 b = 0; b < grid; ++b) {
+      P->sched[nunits + b] = o;
+      for (u32 u : lists[b]) P->sched[o++] = u;
+    }
+    P->sched[nunits + grid] = o;
+  } else {
+    P = &it->second;
+  }
+  if (upload && !P->d_piece) {
+    CU(cudaMallocAsync((void**)&P->d_piece, std::max<size_t>(1, P->pieces.size()) * sizeof(uint4), s));
+    CU(cudaMallocAsync((void**)&P->d_slot_start, P->slot_start.size() * sizeof(u32), s));
+    CU(cudaMallocAsync((void**)&P->d_sched, P->sched.size() * sizeof(u32), s));
+    CU(cudaMemcpyAsync(P->d_piece, P->pieces.data(), P->pieces.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(P->d_slot_start, P->slot_start.data(), P->slot_start.size() * sizeof(u32),
+                       cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(P->d_sched, P->sched.data(), P->sched.size() * sizeof(u32), cudaMemcpyHostToDevice, s));
+  }
+  *out = P;
+  return PE_OK;
+}
+
 // Tensor-core evaluation (tc.cuh): per pass, chunk seeds -> k_tc (persistent, one CTA per SM)
 // -> k_fixup over the pieces' partial rows.
 static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s) {
-  const u64 nslots = h->tc_nslots;
+  // pass length from the one-chunk plan: it has the most pieces (plans with more chunks per pass
+  // use larger pieces), so its slot count bounds every pass's partial rows
+  pe_ctx::TcPlan* P1 = nullptr;
+  if (tc_plan(h, 1, false, s, &P1)) return g_last_error;
+  const u64 nslots = P1->nslots;
   u64 Tp = h->partial_cap_bytes / 8 / std::max<u64>(nslots, 1) / tc::kChunk * tc::kChunk;
   Tp = std::max<u64>(Tp, tc::kChunk);
   Tp = std::min<u64>(Tp, (T + tc::kChunk - 1) / tc::kChunk * tc::kChunk);
@@ -684,17 +785,19 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     tc::k_tc_seed<<<grid_for(nseed, 256), 256, 0, s>>>(h->d_c, h->d_m, h->d_tcMS, h->t_pad, nch, j0 + k0, h->d_seed,
                                                        h->mp);
     CU(cudaGetLastError());
+    pe_ctx::TcPlan* P = nullptr;
+    if (tc_plan(h, nch, true, s, &P)) return g_last_error;
     tc::TcArgs a;
     a.LS = h->d_seed;
     a.C = h->d_tcC;
     a.Rp = h->d_tcR;
-    a.piece = h->d_piece;
+    a.piece = P->d_piece;
     a.partial = h->d_partial;
     a.ldp = (np + 7) / 8 * 8;
     a.t_pad = h->t_pad;
-    a.npieces = h->tc_npieces;
-    a.rounds = h->p < (1ull << 31) ? 1 : tc::kRounds;
-    a.nunits = h->tc_npieces * nch * a.rounds;
+    a.npieces = P->npieces;
+    a.rounds = h->tc_rounds;
+    a.nunits = P->npieces * nch * a.rounds;
     a.nch = nch;
     a.npts = np;
     for (int d = 0; d < 15; ++d) a.Wd[d] = h_powmod(2, 8 * (u64)d, h->p);
@@ -705,7 +808,9 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     a.discard = env_int("PE_TC_DISCARD", 1);
     a.prof = nullptr;
     a.dbg = env_int("PE_TC_DEBUG", 0);
-    const unsigned grid = (unsigned)std::min<u64>(a.nunits, (u64)h->n_sm);
+    const unsigned grid = P->grid;
+    a.sched = P->d_sched;
+    a.sched_off = P->d_sched + a.nunits;
     pe_ctx::Rec rec{};
     if (h->timing) {
       CU(cudaEventCreate(&rec.e0));
@@ -753,7 +858,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     }
     if (h->timing) CU(cudaEventRecord(rec.e1, s));
     const u32 nkb = (np + 255) / 256;
-    k_fixup<<<(unsigned)(h->G * nkb), 256, 0, s>>>(h->d_partial, a.ldp, h->d_tc_slot_start, (u32)h->G, np, nkb,
+    k_fixup<<<(unsigned)(h->G * nkb), 256, 0, s>>>(h->d_partial, a.ldp, P->d_slot_start, (u32)h->G, np, nkb,
                                                    d_out + k0, ld, h->mp);
     CU(cudaGetLastError());
     if (h->timing) {
@@ -773,7 +878,9 @@ static bool use_tc(const pe_ctx* h, u64 T) {
   if (h->tc_mode == 2) return true;
   if (h->tc_mode != 1 || T < tc_min_T(h->t_pad, h->p)) return false;
   const u64 row = (std::min<u64>(T, tc::kChunk) + 7) / 8 * 8;
-  return (u64)h->tc_nslots * row * sizeof(u64) <= h->partial_cap_bytes;
+  pe_ctx::TcPlan* P1 = nullptr;
+  if (tc_plan(const_cast<pe_ctx*>(h), 1, false, nullptr, &P1)) return false;   // host-only: no CUDA call
+  return (u64)P1->nslots * row * sizeof(u64) <= h->partial_cap_bytes;
 }
 
 // automatic fast-method threshold: the measured crossover against k_tc (fast method)
@@ -977,7 +1084,10 @@ extern "C" int pe_info(const pe_ctx* h, int32_t* path, int32_t* R, int32_t* warp
 extern "C" int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint64_t* min_T) {
   if (!h) return set_err(PE_EINVAL);
   if (mode) *mode = h->tc_ok ? h->tc_mode : 0;
-  if (pieces) *pieces = h->tc_npieces;
+  if (pieces) {
+    pe_ctx::TcPlan* P1 = nullptr;
+    *pieces = h->tc_ok && tc_plan(const_cast<pe_ctx*>(h), 1, false, nullptr, &P1) == PE_OK ? P1->npieces : 0;
+  }
   if (min_T) *min_T = h->tc_ok ? (h->tc_mode == 2 ? 1 : tc_min_T(h->t_pad, h->p)) : 0;
   return PE_OK;
 }

@@ -99,6 +99,8 @@ struct TcArgs {
   const u64* C;          // [t_pad][10] C records (giant-step chain multiplier, m^{rr V} table)
   const uint8_t* Rp;     // [t_pad / 32][kRBytes] baby-step byte planes (k_tc_rplanes)
   const uint4* piece;    // x = first padded term, y = K-blocks, z = partial slot (sorted by size desc)
+  const u32* sched;      // units of CTA b: sched[sched_off[b] .. sched_off[b+1])  (host LPT schedule)
+  const u32* sched_off;  // [gridDim.x + 1]
   u64* partial;          // [n_slots][ldp]
   u64 ldp, t_pad;
   u32 npieces, nunits, npts, nch;
@@ -613,11 +615,12 @@ __device__ __forceinline__ long long clk() { return clock64(); }
 // first reader of a K-block's baby-step planes and C records find them in L2.  X mod p is the
 // sum of the rounds' parts (X = sum_g X_g), so each unit reduces its own part into its own
 // partial row (slot = piece slot * rounds + g) and k_fixup adds them.
-// The i-th unit of this CTA: units are dealt to the CTAs in snake order (row i of gridDim units
-// left to right for even i, right to left for odd i), so with size-sorted units every CTA gets a
-// large and a small one in turn; ids grow with i, so the first id >= nunits ends the sequence.
-__device__ __forceinline__ u32 unit_id(u32 i) {
-  return i * gridDim.x + ((i & 1) ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
+// The i-th unit of this CTA, from the host's schedule (pe.cu tc_schedule: longest-processing-time
+// dealing of the size-sorted units over the CTAs, so a launch with few units per CTA -- a shard of
+// a multi-GPU run -- stays balanced); past the CTA's list it returns 0xffffffff (>= nunits).
+__device__ __forceinline__ u32 unit_id(const TcArgs& a, u32 i) {
+  const u32 o = a.sched_off[blockIdx.x] + i;
+  return o < a.sched_off[blockIdx.x + 1] ? a.sched[o] : 0xffffffffu;
 }
 __device__ __forceinline__ void unit_of(const TcArgs& a, u32 unit, uint4& pc, u32& chunk, u32& g) {
   g = unit % a.rounds;
@@ -633,7 +636,7 @@ struct KIter {
   u32 ord, unit, kb, nkb, q0, chunk;
   bool valid;
   __device__ __forceinline__ void load(const TcArgs& a) {
-    unit = unit_id(ord);
+    unit = unit_id(a, ord);
     valid = unit < a.nunits;
     if (valid) {
       uint4 pc;
@@ -805,7 +808,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
     const uint64_t dA0 = smem_desc(uni(smem_u32(smem)), kLBOA);
     const uint64_t dB0 = smem_desc(uni(smem_u32(smem)) + 8 * kPlaneA, kLBOB);
     u32 it = 0;
-    for (u32 nunit = 0, unit = unit_id(0); unit < a.nunits; unit = unit_id(++nunit)) {
+    for (u32 nunit = 0, unit = unit_id(a, 0); unit < a.nunits; unit = unit_id(a, ++nunit)) {
       uint4 pc; u32 chunk, g;
       unit_of(a, unit, pc, chunk, g);
       const u32 nkb = uni(pc.y);

@@ -34,6 +34,8 @@ def timed(ctx, j0, T, out, reps):
 
 def main():
     reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 3
+    only_tc = "--only-tc" in sys.argv
+    Tsel = [int(x) for x in sys.argv[sys.argv.index("--T") + 1].split(",")] if "--T" in sys.argv else None
     cfgs = [int(x) for x in (sys.argv[sys.argv.index("--cfg") + 1] if "--cfg" in sys.argv else "3,5").split(",")]
     Ts = {3: [512, 1024, 2048, 4096, 8192, 16384, 32768, 65536, 131072, 262144],
           5: [4096, 16384, 32768, 65536]}
@@ -41,12 +43,12 @@ def main():
         w = synth.gen_config(cfg)
         with pe.Context.from_workload(w, path=pe.PATH_TC) as tc, pe.Context.from_workload(w, path=pe.PATH_FAST) as fa:
             G = tc.G
-            for T in Ts[cfg]:
+            for T in (Tsel or Ts[cfg]):
                 a = torch.empty((G, T), dtype=torch.int64, device="cuda")
                 b = torch.empty_like(a)
                 t_tc = timed(tc, w.j0, T, a, reps)
-                t_fa = timed(fa, w.j0, T, b, reps)
-                same = bool(torch.equal(a, b))
+                t_fa = float("nan") if only_tc else timed(fa, w.j0, T, b, reps)
+                same = None if only_tc else bool(torch.equal(a, b))
                 print(json.dumps({"workload": w.name, "t": w.t, "G": G, "T": T, "k_tc_ms": t_tc, "fast_ms": t_fa,
                                   "fast_over_tc": t_fa / t_tc, "bitwise_equal": same,
                                   "k_tc_term_points_per_s": w.t * T / (t_tc * 1e-3),

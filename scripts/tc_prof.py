@@ -13,7 +13,7 @@ import synth  # noqa: E402
 t = int(sys.argv[sys.argv.index("--t") + 1]) if "--t" in sys.argv else None
 cfg = int(sys.argv[sys.argv.index("--cfg") + 1]) if "--cfg" in sys.argv else 5
 T = int(sys.argv[sys.argv.index("--T") + 1]) if "--T" in sys.argv else None
-path = pe.PATH_INT if "--int" in sys.argv else pe.PATH_TC
+path = pe.PATH_INT if "--int" in sys.argv else pe.PATH_FAST if "--fast" in sys.argv else pe.PATH_TC
 w = synth.gen_config(cfg, t=t, T=T)
 with pe.Context.from_workload(w, path=path) as ctx:
     d = torch.empty((ctx.G, w.T), dtype=torch.int64, device="cuda")
