@@ -181,7 +181,8 @@ __device__ __forceinline__ const u64* op_ptr(const Call& a, u32 job, u32 o) {
 }
 
 // Forward transforms: unit = (job, op, block) of prime blockIdx.y; a CTA holds kTile / S units.
-__global__ void __launch_bounds__(512) k_fast_fwd(Call a) {
+constexpr u32 kNttThreads = 256;
+__global__ void __launch_bounds__(kNttThreads, 3) k_fast_fwd(Call a) {
   extern __shared__ u32 X[];
   const int j = blockIdx.y;
   const PrimeC P = a.C.pr[j];
@@ -189,15 +190,25 @@ __global__ void __launch_bounds__(512) k_fast_fwd(Call a) {
   const u32 nunits = a.njobs * a.nops * a.nb;
   const u32 u0 = blockIdx.x * per;
   const u32 nu = min(per, nunits - u0), npts = nu * S;
-  for (u32 x = threadIdx.x; x < npts; x += blockDim.x) {
-    const u32 u = u0 + (x >> a.lg), i = x & (S - 1);
-    const u32 blk = u & (a.nb - 1), o = (u >> a.lgnb) & (a.nops - 1), job = u >> (a.lgnb + a.lgnops);
-    u32 v = 0;
-    if (i < a.Bk) {
-      const u64* src = op_ptr(a, job, o);
-      if (src) v = reduce_q(src[(u64)blk * a.Bk + i], P);
+  // 4 independent loads in flight per thread before any reduction (the loads are the latency)
+  for (u32 x0 = threadIdx.x; x0 < npts; x0 += 4 * blockDim.x) {
+    u64 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const u32 x = x0 + k * blockDim.x;
+      v[k] = 0;
+      const u32 u = u0 + (x >> a.lg), i = x & (S - 1);
+      if (x < npts && i < a.Bk) {
+        const u32 blk = u & (a.nb - 1), o = (u >> a.lgnb) & (a.nops - 1), job = u >> (a.lgnb + a.lgnops);
+        const u64* src = op_ptr(a, job, o);
+        if (src) v[k] = __ldg(src + (u64)blk * a.Bk + i);
+      }
     }
-    X[phys(x)] = v;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const u32 x = x0 + k * blockDim.x;
+      if (x < npts) X[phys(x)] = reduce_q(v[k], P);
+    }
   }
   __syncthreads();
   ntt_dif(X, a.lg, npts, a.twf + (u64)j * kSmax, P.q);
@@ -207,7 +218,7 @@ __global__ void __launch_bounds__(512) k_fast_fwd(Call a) {
 
 // Pointwise products + inverse: unit = (job, out, out block c) of prime blockIdx.y.
 // out 0 of kMerge: N1 E2 + N2 E1 (ops 0,3 and 2,1); out 1: E1 E2 (ops 1,3); kMul: op0 op1.
-__global__ void __launch_bounds__(512) k_fast_pwinv(Call a) {
+__global__ void __launch_bounds__(kNttThreads, 3) k_fast_pwinv(Call a) {
   extern __shared__ u32 X[];
   const int j = blockIdx.y;
   const PrimeC P = a.C.pr[j];
@@ -340,25 +351,29 @@ __global__ void k_fast_crt(Call a) {
 // straight into the next level.  Global traffic: the children (L2-resident across the 5 primes)
 // and the parents, instead of spectra and residues.
 constexpr u32 kFusedS = 1024;
-constexpr u32 kFusedSmem = (padded(4 * kFusedS) + 2 * kNP * kFusedS) * sizeof(u32);   // 58 KB: 3 CTAs per SM
-__global__ void __launch_bounds__(512) k_fast_merge_fused(Call a) {
+constexpr u32 kFusedThreads = 256;
+// W (padded) + residues of P, Q for the 5 primes + the 4 operands as u64 (read from global once)
+constexpr u32 kFusedSmem = (padded(4 * kFusedS) + 2 * kNP * kFusedS) * sizeof(u32) + 4 * (kFusedS / 2) * sizeof(u64);
+__global__ void __launch_bounds__(kFusedThreads, 3) k_fast_merge_fused(Call a) {
   extern __shared__ u32 sm[];
   u32* W = sm;                       // [4][npts]: N1, E1, N2, E2 of the CTA's jobs (P, Q after the products)
   u32* Rz = sm + padded(4 * kFusedS);   // [kNP][2][npts] residues of P and Q (W is padded: phys)
+  u64* Op = (u64*)(Rz + 2 * kNP * kFusedS);   // [4][nj * Lc] the operands, canonical mod p
   const u32 S = 1u << a.lg, per = kFusedS >> a.lg;
   const u32 job0 = blockIdx.x * per;
   const u32 nj = min(per, a.njobs - job0), npts = nj * S;
+  const u32 lgLc = a.lg - 1, nop = nj << lgLc;     // Lc = S / 2 coefficients per operand
+  for (u32 x = threadIdx.x; x < 4 * nop; x += blockDim.x) {
+    const u32 o = x / nop, r = x - o * nop, jj = r >> lgLc, i = r & (a.Lc - 1);
+    const u64* src = op_ptr(a, job0 + jj, o);
+    Op[x] = src ? src[i] : 0;
+  }
+  __syncthreads();
   for (int jp = 0; jp < kNP; ++jp) {
     const PrimeC P = a.C.pr[jp];
     for (u32 x = threadIdx.x; x < 4 * npts; x += blockDim.x) {
-      const u32 o = x >= 2 * npts ? (x >= 3 * npts ? 3u : 2u) : (x >= npts ? 1u : 0u);
-      const u32 r = x - o * npts, jj = r >> a.lg, i = r & (S - 1);
-      u32 v = 0;
-      if (i < a.Lc) {
-        const u64* src = op_ptr(a, job0 + jj, o);
-        if (src) v = reduce_q(src[i], P);
-      }
-      W[phys(x)] = v;
+      const u32 unit = x >> a.lg, i = x & (S - 1);            // unit = o * nj + jj
+      W[phys(x)] = i < a.Lc ? reduce_q(Op[(unit << lgLc) + i], P) : 0u;
     }
     __syncthreads();
     ntt_dif(W, a.lg, 4 * npts, a.twf + (u64)jp * kSmax, P.q);
@@ -387,14 +402,11 @@ __global__ void __launch_bounds__(512) k_fast_merge_fused(Call a) {
         conv[o] = crt_modp(r, a.C, a.mp);
       }
     }
-    const u64* N1 = op_ptr(a, job, 0);
-    const u64* E1 = op_ptr(a, job, 1);
-    const u64* N2 = op_ptr(a, job, 2);
-    const u64* E2 = op_ptr(a, job, 3);
     u64 n = conv[0], e = conv[1];
-    if (k < a.Lc) {
-      if (N1) { n = addp(n, N1[k], p); e = addp(e, E1[k], p); }
-      if (N2) { n = addp(n, N2[k], p); e = addp(e, E2[k], p); }
+    if (k < a.Lc) {   // children from the shared-memory copy (absent children read as zero)
+      const u32 b = (jj << lgLc) + k;
+      n = addp(addp(n, Op[b], p), Op[2 * nop + b], p);
+      e = addp(addp(e, Op[nop + b], p), Op[3 * nop + b], p);
     }
     a.dst[0][(u64)job * a.dstride + k] = n;
     a.dst[1][(u64)job * a.dstride + k] = e;
@@ -688,7 +700,7 @@ static int run_call(Plan* P, Call& a, cudaStream_t s) {
     if (a.njobs == 0) return PE_OK;
     const u32 per = kFusedS / S;
     FCU(cudaFuncSetAttribute(k_fast_merge_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem));
-    k_fast_merge_fused<<<(a.njobs + per - 1) / per, 512, kFusedSmem, s>>>(a);
+    k_fast_merge_fused<<<(a.njobs + per - 1) / per, kFusedThreads, kFusedSmem, s>>>(a);
     FCU(cudaGetLastError());
     return PE_OK;
   }
@@ -701,7 +713,7 @@ static int run_call(Plan* P, Call& a, cudaStream_t s) {
   a.res = P->d_res;
   const u32 per = std::max<u32>(1, kTile >> a.lg);
   const u32 smem = padded(per * S) * sizeof(u32);
-  const u32 threads = std::min<u32>(512, std::max<u32>(32, per * S / 2));
+  const u32 threads = std::min<u32>(kNttThreads, std::max<u32>(32, per * S / 2));
   FCU(cudaFuncSetAttribute(k_fast_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, padded(kTile) * 4));
   FCU(cudaFuncSetAttribute(k_fast_pwinv, cudaFuncAttributeMaxDynamicSharedMemorySize, padded(kTile) * 4));
   const u32 nu_f = a.njobs * a.nops * a.nb, nu_i = a.njobs * a.nouts * a.nbo;

@@ -889,9 +889,13 @@ static u64 fast_min_T(const pe_ctx* h) {
   const int e = env_int("PE_FAST_MIN_T", 0);
   return e > 0 ? (u64)e : kFastMinT;
 }
+// Automatic choice: the fast method beats the scalar matrix method (k_step) from T ~ kFastMinT on,
+// but never the tensor-core form within its supported T (profiles/r02_fast_sweep*.jsonl, DESIGN.md
+// §7), so an automatic handle takes it only when its tensor-core form is off (PE_TC=0, or it
+// degraded for lack of memory).
 static bool use_fast(const pe_ctx* h, u64 T) {
   if (h->fast_mode == 2) return true;
-  return h->fast_mode == 1 && T >= fast_min_T(h) && T <= fast::kTMax;
+  return h->fast_mode == 1 && !h->tc_ok && T >= fast_min_T(h) && T <= fast::kTMax;
 }
 enum { kKStep = 0, kKTc = 1, kKFast = 2 };
 static int choose_kernel(const pe_ctx* h, u64 T) {
