@@ -244,8 +244,12 @@ static u64 tc_min_T(u64 t_pad, u64 p) {
   return std::min<u64>(8192, std::max<u64>(512, 86000000ull / tp));
 }
 
-// automatic fast-method threshold (points): from the measured crossover with k_tc
-static const u64 kFastMinT = ~0ull;
+// automatic fast-method threshold against the scalar matrix method (points; profiles/
+// r02_fast_sweep_*.jsonl): fast/k_step = 1.05 at T = 4096 and 0.72 at 8192 on config 3 (3.9k terms
+// per bucket), 0.81 at 4096 on config 5 (10k per bucket).  Its per-bucket Newton inversion costs
+// O(T log T) whatever the bucket size, so it also needs >= kFastMinTermsPerBucket terms per bucket.
+static const u64 kFastMinT = 8192;
+static const u64 kFastMinTermsPerBucket = 2048;
 
 static unsigned grid_for(u64 n, unsigned block) {
   u64 b = (n + block - 1) / block;
@@ -806,6 +810,11 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     a.mp = h->mp;
     a.status = d_status;
     a.discard = env_int("PE_TC_DISCARD", 1);
+    a.sleep_ns[0] = 32; a.sleep_ns[1] = 64; a.sleep_ns[2] = 64;
+    if (const char* e = getenv("PE_TC_SLEEP")) {
+      unsigned x, y, z;
+      if (sscanf(e, "%u,%u,%u", &x, &y, &z) == 3) { a.sleep_ns[0] = x; a.sleep_ns[1] = y; a.sleep_ns[2] = z; }
+    }
     a.prof = nullptr;
     a.dbg = env_int("PE_TC_DEBUG", 0);
     const unsigned grid = P->grid;
@@ -895,7 +904,8 @@ static u64 fast_min_T(const pe_ctx* h) {
 // degraded for lack of memory).
 static bool use_fast(const pe_ctx* h, u64 T) {
   if (h->fast_mode == 2) return true;
-  return h->fast_mode == 1 && !h->tc_ok && T >= fast_min_T(h) && T <= fast::kTMax;
+  return h->fast_mode == 1 && !h->tc_ok && T >= fast_min_T(h) && T <= fast::kTMax &&
+         h->t >= kFastMinTermsPerBucket * h->G;
 }
 enum { kKStep = 0, kKTc = 1, kKFast = 2 };
 static int choose_kernel(const pe_ctx* h, u64 T) {

@@ -110,6 +110,8 @@ struct TcArgs {
   u32* scratch;          // per CTA: 2 (ping-pong by unit) x kDiag accumulators x kChunk u32 drained diagonal sums
   ModParams mp;
   int discard;           // 1: discard the raw scratch lines from L2 once folded (PE_TC_DISCARD, default 1)
+  u32 sleep_ns[3];       // poll back-off (ns) of the MMA warp's stage wait, the producers' stage wait and
+                         // the epilogue's accumulator wait (32 / 64 / 64; env PE_TC_SLEEP=a,b,c)
   u32* status;           // mapped host word (pe_ctx::h_status): set to 1 if a pipeline wait timed out
   unsigned long long* prof;  // optional phase timers [gridDim][warps][4] (PE_TC_PROF=1), else null
   int dbg;                   // development only (PE_TC_DEBUG, PROF build): 1 = skip the MMAs,
@@ -337,11 +339,11 @@ struct Abort {
   u32* status;         // mapped host word
 };
 template <int SLEEP_NS = 0>
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, u32 parity, const Abort& ab) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, u32 parity, const Abort& ab, u32 sleep_ns = SLEEP_NS) {
   if (mbar_try(bar, parity) || *ab.cta) return;
   const unsigned long long t0 = gtimer();
   for (u32 n = 1;; ++n) {
-    if (SLEEP_NS) __nanosleep(SLEEP_NS);
+    if (sleep_ns) __nanosleep(sleep_ns);
     if (mbar_try(bar, parity)) return;
     if ((n & 255) == 0) {
       if (*ab.cta) return;
@@ -754,7 +756,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       const u32 stage = (u32)my_stage;
       const u32 use = guse;
       long long c0 = clk();
-      mbar_wait<64>(&empty[stage], (use & 1) ^ 1, ab);
+      mbar_wait<64>(&empty[stage], (use & 1) ^ 1, ab, a.sleep_ns[1]);
       long long c1 = clk();
       if (PROF) T[1] += c1 - c0;
       // the other slot held K-block guse-1, which every warp of the group read (at the end of
@@ -827,7 +829,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
         for (u32 kb = 0; kb < nkb; ++kb, ++it) {
           const u32 stage = it % kStages, use = it / kStages;
           c0 = clk();
-          mbar_wait<32>(&full[stage], use & 1, ab);
+          mbar_wait<32>(&full[stage], use & 1, ab, a.sleep_ns[0]);
           if (PROF) T[kb < (u32)kStages ? 0 : 1] += clk() - c0;   // unit start vs steady state
           tc_fence_after();
           const uint64_t da = dA0 + (uint64_t)((stage * kStageBytes) >> 4);
@@ -854,7 +856,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
         }
       }
       long long c0 = clk();
-      mbar_wait<64>(&accf, nunit & 1, ab);
+      mbar_wait<64>(&accf, nunit & 1, ab, a.sleep_ns[2]);
       long long c1 = clk();
       if (PROF) T[0] += c1 - c0;
       tc_fence_after();

@@ -111,3 +111,20 @@ def test_fast_limits():
         with pytest.raises(pe.PEError) as ei:
             ctx.eval(1, (1 << 20) + 1)
         assert ei.value.code == pe.PE_ERANGE
+
+
+def test_fast_automatic_choice_without_tensor_path(monkeypatch):
+    """With the tensor-core form off (PE_TC=0), an automatic handle takes the fast method for
+    T >= 8192 when buckets hold >= 2048 terms on average (its measured crossover with k_step,
+    profiles/r02_fast_sweep_config3.jsonl), and k_step otherwise; bit-exact either way."""
+    monkeypatch.setenv("PE_TC", "0")
+    w = synth.gen_config(3, t=300_000, T=8192)             # 256 buckets of ~1170 terms: k_step
+    with pe.Context.from_workload(w) as ctx:
+        assert ctx.eval_kernel(w.T) == "k_step"
+    w = synth.gen_config(3, t=600_000, T=8192)             # ~2340 terms per bucket: fast from T = 8192
+    w.exps[:, :2] %= np.uint32(14)                         # 196 buckets
+    with pe.Context.from_workload(w) as ctx:
+        assert ctx.eval_kernel(8191) == "k_step" and ctx.eval_kernel(w.T) == "fast"
+        out = ctx.eval(w.j0, w.T)
+    ks = np.array([0, 1, 4097, 8191], np.uint64)
+    assert np.array_equal(out[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
