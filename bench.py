@@ -268,9 +268,10 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- multi-GPU decomposition: the tensor-core path needs whole 16384-point chunks, so with
+    # ---- multi-GPU decomposition: the tensor-core path works in whole 8192-point chunks, so with
     # N > 1 ranks shard bucket-contiguous TERM ranges (each rank: all T points of ~t/N terms,
-    # P2P row gather, boundary buckets summed mod p); the scalar path shards the point range.
+    # P2P row gather, boundary buckets summed mod p by pe_rows_addmod) -- measured 6.5x vs 1.55x
+    # for point ranges at 8 ranks; the scalar path shards the point range.
     probe = pe.Context(w.p, w.coeffs[:1], w.exps[:1], w.alpha, n=w.n)
     term_shard = world > 1 and probe.uses_tc(w.T)
     probe.close()

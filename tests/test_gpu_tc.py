@@ -1,7 +1,7 @@
 """GPU parity of the tensor-core path (PE_PATH_TC, csrc/tc.cuh) against the CPU oracle through
-the C ABI.  The path factors each bucket's 128 x 128-point chunk into giant-step x baby-step
-values (the Vandermonde structure m_i^{j} = m_i^{j_s + 128u} m_i^{v}) and sums
-their 64 byte-pair products on int8 tensor cores; results must be bit-identical to the oracle
+the C ABI.  The path factors each bucket's 128 x 64-point chunk into giant-step x baby-step
+values (the Vandermonde structure m_i^{j} = m_i^{j_s + 64u} m_i^{v}, u < 128, v < 64,
+PAPER.md:420-427) and sums their 64 byte-pair products on int8 tensor cores; results must be bit-identical to the oracle
 (canonical residues are unique, R14)."""
 import numpy as np
 import pytest
@@ -33,7 +33,7 @@ def check_tc(w, **kw):
 
 
 @pytest.mark.parametrize("p,n,t,maxdeg,j0,T", [
-    (P62, 6, 300, 4, 1, 1),               # T = 1 (one column of a 16384-point chunk)
+    (P62, 6, 300, 4, 1, 1),               # T = 1 (one column of an 8192-point chunk)
     (P62, 6, 300, 4, 1, 129),             # ragged inside the first chunk (u = 1, v = 0)
     (P62, 5, 500, 3, 0, 70),              # j0 = 0
     (P62, 5, 200, 3, 2**64 - 40, 40),     # largest j range (seed exponents near 2^64)
