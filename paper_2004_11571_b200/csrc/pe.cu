@@ -271,7 +271,6 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
     h->G = 0;
     return PE_OK;
   }
-  if (t > 0x7fffffffull) return set_err(PE_ERANGE);   // CUB sort / select take int num_items
 
   // ---- upload (a1)
   u64* d_coeffs; u32* d_exps; u64* d_alpha;
@@ -499,6 +498,7 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
   }
   const u64 t = poly_off[npoly];
   if (n < 2 || n > 66) { set_err(PE_EINVAL); return nullptr; }
+  if (t > 0x7fffffffull) { set_err(PE_ERANGE); return nullptr; }   // CUB sort / select take int num_items
   if (t > 0 && (!coeffs || !exps)) { set_err(PE_EINVAL); return nullptr; }
   if (n > 2 && !alpha) { set_err(PE_EINVAL); return nullptr; }
   if (p < 3 || p >= (1ull << 63)) { set_err(PE_ERANGE); return nullptr; }

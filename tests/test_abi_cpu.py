@@ -79,6 +79,9 @@ def test_validation_before_cuda(L):
     assert L.pe_last_error() == pe.PE_EINVAL
     assert not _create(L, P62, 2, 4, cp, ep, None)       # alpha NULL with n > 2
     assert L.pe_last_error() == pe.PE_EINVAL
+    # t > 2^31 - 1 (the device sort takes int counts): rejected before the arrays are read
+    assert not _create(L, P62, 1 << 31, 4, cp, ep, ap)
+    assert L.pe_last_error() == pe.PE_ERANGE
     z = np.array([2, P62 * 2], np.uint64)                 # alpha_2 == 0 mod p
     assert not _create(L, P62, 2, 4, cp, ep, z.ctypes.data_as(ctypes.c_void_p))
     assert L.pe_last_error() == pe.PE_ERANGE
