@@ -741,6 +741,7 @@ static int tc_plan(pe_ctx* h, u32 nch, bool upload, cudaStream_t s, pe_ctx::TcPl
     CU(cudaMemcpyAsync(P->d_slot_start, P->slot_start.data(), P->slot_start.size() * sizeof(u32),
                        cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(P->d_sched, P->sched.data(), P->sched.size() * sizeof(u32), cudaMemcpyHostToDevice, s));
+    CU(cudaStreamSynchronize(s));   // once per (handle, chunk count): later calls may use another stream
   }
   *out = P;
   return PE_OK;

@@ -51,6 +51,8 @@ def check_incremental(w):
     (2**31 - 1, 3, 100, 9, 1, 64),
     ((1 << 50) - 27, 7, 600, 4, 3, 77),
     ((1 << 62) - 87, 6, 700, 4, 5, 300),   # near the top of the supported range
+    (P62, 6, 300, 4, 1, 4097),             # T2 = 8192: the first block-convolved length
+    (P62, 6, 5000, 4, 1, 2048),            # buckets longer than T2 (truncated upper levels)
 ])
 def test_fast_edge_shapes(p, n, t, maxdeg, j0, T):
     check_direct(synth.random_small(800 + t + n, p, n, t, maxdeg, T, j0, coeff_hi=2**64 - 1))
@@ -128,3 +130,17 @@ def test_fast_automatic_choice_without_tensor_path(monkeypatch):
         out = ctx.eval(w.j0, w.T)
     ks = np.array([0, 1, 4097, 8191], np.uint64)
     assert np.array_equal(out[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
+
+
+def test_fast_batched_polynomials():
+    """pe_create_batch with the fast method: f and h of config-3 shape at the same points (the gcd
+    workload), rows per polynomial equal to the incremental checker."""
+    f = synth.gen_config(3, t=60_000, T=3000)
+    h = synth.gen_config(3, t=40_000, T=3000, seed=77)
+    with pe.Context.batch(f.p, [(f.coeffs, f.exps), (h.coeffs, h.exps)], f.alpha, f.n, path=pe.PATH_FAST) as ctx:
+        assert ctx.eval_kernel(f.T) == "fast"
+        ro = ctx.poly_rows().astype(np.int64)
+        out = ctx.eval(f.j0, f.T)
+    inc_f = oracle.eval_incremental(f.p, f.n, f.coeffs, f.exps, f.alpha, f.j0, f.T)
+    inc_h = oracle.eval_incremental(f.p, f.n, h.coeffs, h.exps, f.alpha, f.j0, f.T)
+    assert np.array_equal(out[ro[0]:ro[1]], inc_f) and np.array_equal(out[ro[1]:ro[2]], inc_h)

@@ -89,3 +89,17 @@ def test_many_buckets_partial_cap_uses_k_step(monkeypatch):
         assert ctx.info()["tc_mode"] == 1 and not ctx.uses_tc(w.T)
         out = ctx.eval(w.j0, w.T)
     assert np.array_equal(out, oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T))
+
+
+def test_schedule_orders_agree(monkeypatch):
+    """The k_tc result does not depend on the host's unit schedule: the snake order and the
+    longest-processing-time order (PE_TC_SCHED=0/1, pe.cu tc_plan) give identical bits on a
+    config-3 instance with ~6 units per CTA, equal to the incremental checker."""
+    w = synth.gen_config(3, t=400_000, T=9000)
+    outs = []
+    for sched in ("0", "1"):
+        monkeypatch.setenv("PE_TC_SCHED", sched)
+        with pe.Context.from_workload(w, path=pe.PATH_TC) as ctx:
+            outs.append(ctx.eval(w.j0, w.T))
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], oracle.eval_incremental_blocked(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T))
