@@ -160,6 +160,8 @@ struct Call {
   u32 nops, nouts, njobs;
   u32 Lc, Lo, Bk, nb, nbo, lg;          // operand length, output length, block, blocks, out blocks, log2 S
   u32 lgnb, lgnops, lgnouts, lgnbo, lgLo, lgBk;   // the same as shifts (all powers of two)
+  u32 nbz[4];           // op o has nonzero coefficients only in its first nbz[o] blocks (others: skipped)
+  u32 keep;             // bit o: op o's spectra are already in place from the previous call (not redone)
   int kind;                             // kMerge / kMul / kTwoMinus
   // outputs
   u64* dst[2];
@@ -190,6 +192,11 @@ __global__ void __launch_bounds__(kNttThreads, 3) k_fast_fwd(Call a) {
   const u32 nunits = a.njobs * a.nops * a.nb;
   const u32 u0 = blockIdx.x * per;
   const u32 nu = min(per, nunits - u0), npts = nu * S;
+  auto skipped = [&](u32 u) {
+    const u32 blk = u & (a.nb - 1), o = (u >> a.lgnb) & (a.nops - 1);
+    return ((a.keep >> o) & 1u) || blk >= a.nbz[o];
+  };
+  if (nu == 1 && skipped(u0)) return;          // whole CTA (one 8192-point unit) not needed
   // 4 independent loads in flight per thread before any reduction (the loads are the latency)
   for (u32 x0 = threadIdx.x; x0 < npts; x0 += 4 * blockDim.x) {
     u64 v[4];
@@ -213,7 +220,8 @@ __global__ void __launch_bounds__(kNttThreads, 3) k_fast_fwd(Call a) {
   __syncthreads();
   ntt_dif(X, a.lg, npts, a.twf + (u64)j * kSmax, P.q);
   u32* out = a.spec + ((u64)j * nunits + u0) * S;
-  for (u32 x = threadIdx.x; x < npts; x += blockDim.x) out[x] = X[phys(x)];
+  for (u32 x = threadIdx.x; x < npts; x += blockDim.x)
+    if (!skipped(u0 + (x >> a.lg))) out[x] = X[phys(x)];
 }
 
 // Pointwise products + inverse: unit = (job, out, out block c) of prime blockIdx.y.
@@ -243,7 +251,8 @@ __global__ void __launch_bounds__(kNttThreads, 3) k_fast_pwinv(Call a) {
       } else {
         oa = 0u; ob = 1u;
       }
-      const u32 blo = c + 1 > a.nb ? c + 1 - a.nb : 0, bhi = min(c, a.nb - 1);
+      const u32 na = a.nbz[oa], nbb = a.nbz[ob];        // blocks beyond nbz are zero: no product
+      const u32 blo = c + 1 > nbb ? c + 1 - nbb : 0, bhi = min(c, na - 1);
       for (u32 ba = blo; ba <= bhi; ++ba) {
         const u32 bb = c - ba;
         const u32 A = J[(u64)oa * opstride + (u64)ba * S], B = J[(u64)ob * opstride + (u64)bb * S];
@@ -692,6 +701,8 @@ static int run_call(Plan* P, Call& a, cudaStream_t s) {
   else a.nbo = std::min<u32>((a.Lo + a.Bk - 1) / a.Bk, 2 * a.nb);
   a.lgnb = ilog2(a.nb); a.lgnops = ilog2(a.nops); a.lgnouts = ilog2(a.nouts); a.lgnbo = ilog2(a.nbo);
   a.lgLo = ilog2(a.Lo); a.lgBk = ilog2(a.Bk);
+  for (int o = 0; o < 4; ++o)   // callers give nonzero lengths in coefficients (0: the whole operand)
+    a.nbz[o] = a.nbz[o] ? std::min<u32>(a.nb, (a.nbz[o] + a.Bk - 1) / a.Bk) : a.nb;
   a.twf = P->d_twf;
   a.twi = P->d_twi;
   a.scale = P->d_scale;
@@ -776,9 +787,14 @@ int eval(Plan* P, const u64* d_c, const u64* d_m, const ModParams& mp, u64 j0, u
     a.base[0] = D; a.base[1] = Y; a.idx = nullptr; a.nidx = 1; a.ish = 0; a.rstride = T2;
     a.nops = 2; a.nouts = 1; a.njobs = (u32)P->G; a.Lc = 2 * k; a.Lo = 2 * k;
     a.kind = kTwoMinus; a.dst[0] = W; a.dstride = T2; a.mp = mp;
+    a.nbz[0] = 0; a.nbz[1] = k;               // Y has k coefficients: its upper blocks are zero
     if (int rc = run_call(P, a, s)) return rc;
-    Call b = a;
-    b.base[0] = Y; b.base[1] = W; b.kind = kMul; b.dst[0] = Y;
+    // Y <- Y W: op 1 is Y again, same length: its spectra from the call above are reused
+    Call b{};
+    b.base[0] = W; b.base[1] = Y; b.idx = nullptr; b.nidx = 1; b.ish = 0; b.rstride = T2;
+    b.nops = 2; b.nouts = 1; b.njobs = (u32)P->G; b.Lc = 2 * k; b.Lo = 2 * k;
+    b.kind = kMul; b.dst[0] = Y; b.dstride = T2; b.mp = mp;
+    b.nbz[0] = 0; b.nbz[1] = k; b.keep = 2u;
     if (int rc = run_call(P, b, s)) return rc;
   }
   // out = N Y mod z^T
