@@ -140,7 +140,7 @@ struct pe_ctx {
     u32* d_slot_start = nullptr;
     u32* d_sched = nullptr;
   };
-  std::map<u32, TcPlan> tc_plans;
+  mutable std::map<u32, TcPlan> tc_plans;   // lazily built cache (also from const queries)
   // asymptotically fast method (fast.cu, NEXT-4): 0 off, 1 automatic (T >= fast_min_T), 2 forced
   int fast_mode = 0;
   u64 fast_min_T = 0;
@@ -640,7 +640,7 @@ static int ensure_partial(pe_ctx* h, size_t need, cudaStream_t s) {
 // load level of neighbouring CTAs and run side by side (one DRAM read of the planes, L2 for the
 // rest -- the round-1 snake order's property).  env PE_TC_PIECE (terms) / PE_TC_UPC override.
 static const u32 kUnitsPerCta = 6;
-static int tc_plan(pe_ctx* h, u32 nch, bool upload, cudaStream_t s, pe_ctx::TcPlan** out) {
+static int tc_plan(const pe_ctx* h, u32 nch, bool upload, cudaStream_t s, pe_ctx::TcPlan** out) {
   auto it = h->tc_plans.find(nch);
   pe_ctx::TcPlan* P = nullptr;
   if (it == h->tc_plans.end()) {
@@ -889,7 +889,7 @@ static bool use_tc(const pe_ctx* h, u64 T) {
   if (h->tc_mode != 1 || T < tc_min_T(h->t_pad, h->p)) return false;
   const u64 row = (std::min<u64>(T, tc::kChunk) + 7) / 8 * 8;
   pe_ctx::TcPlan* P1 = nullptr;
-  if (tc_plan(const_cast<pe_ctx*>(h), 1, false, nullptr, &P1)) return false;   // host-only: no CUDA call
+  if (tc_plan(h, 1, false, nullptr, &P1)) return false;   // host-only: no CUDA call
   return (u64)P1->nslots * row * sizeof(u64) <= h->partial_cap_bytes;
 }
 
@@ -1101,7 +1101,7 @@ extern "C" int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint
   if (mode) *mode = h->tc_ok ? h->tc_mode : 0;
   if (pieces) {
     pe_ctx::TcPlan* P1 = nullptr;
-    *pieces = h->tc_ok && tc_plan(const_cast<pe_ctx*>(h), 1, false, nullptr, &P1) == PE_OK ? P1->npieces : 0;
+    *pieces = h->tc_ok && tc_plan(h, 1, false, nullptr, &P1) == PE_OK ? P1->npieces : 0;
   }
   if (min_T) *min_T = h->tc_ok ? (h->tc_mode == 2 ? 1 : tc_min_T(h->t_pad, h->p)) : 0;
   return PE_OK;
