@@ -120,7 +120,7 @@ class ClockSampler:
         end of the timed region; nvidia-smi needs ~0.1-0.3 s to start, so the window opens at the
         warm-up)."""
         import datetime
-        sm, mx, reasons = [], 0.0, set()
+        sm, mx, reasons, pw = [], 0.0, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for l in getattr(self, "lines", []):
             f = [x.strip() for x in l.split(",")]
@@ -136,6 +136,7 @@ class ClockSampler:
             try:
                 sm.append(float(f[1]))
                 mx = max(mx, float(f[2]))
+                pw.append(float(f[3]))
             except ValueError:
                 continue
             for name, v in zip(names, f[5:9]):
@@ -143,7 +144,8 @@ class ClockSampler:
                     reasons.add(name)
         load = [s for s in sm if s > 0.5 * mx] if mx else sm
         return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_median": statistics.median(pw) if pw else None, "power_w_max": max(pw) if pw else None}
 
 
 # ---------------------------------------------------------------- CPU oracle leg
