@@ -108,9 +108,10 @@ __device__ __forceinline__ U96 xpose_reduce8(U96 (&v)[8], int lane) {
 }
 
 // ---------------------------------------------------------------- setup kernels
-static __global__ void k_keys(const u32* __restrict__ exps, u64 t, u32 n, u64* __restrict__ key,
+// Terms [a, b) (one upload chunk): bucket key and input index.
+static __global__ void k_keys(const u32* __restrict__ exps, u64 a, u64 b, u32 n, u64* __restrict__ key,
                        u32* __restrict__ idx) {
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < t; i += (u64)gridDim.x * blockDim.x) {
+  for (u64 i = a + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < b; i += (u64)gridDim.x * blockDim.x) {
     key[i] = ((u64)exps[i * n + 0] << 32) | exps[i * n + 1];
     idx[i] = (u32)i;
   }
@@ -154,15 +155,9 @@ static __global__ void k_gather_runs(const u32* __restrict__ starts, u32 G, cons
   }
 }
 
-static __global__ void k_max_exp(const u32* __restrict__ exps, u64 t, u32 n, u32* __restrict__ dmax) {
-  u32 mx = 0;
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < t; i += (u64)gridDim.x * blockDim.x)
-    for (u32 l = 2; l < n; ++l) mx = max(mx, exps[i * n + l]);
-  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(dmax, mx);
-}
-
-// table[l*(D+1) + e] = mont(alpha_l^e), one thread per entry (independent exponentiations).
+// table[l*(D+1) + e] = mont(alpha_l^e), one thread per entry (independent exponentiations); D + 1 =
+// kTab entries per variable (exponents beyond take direct powers in k_monomials).
+constexpr u32 kTab = 256;
 static __global__ void k_power_table(const u64* __restrict__ alpha, u32 nz, u32 D, u64* __restrict__ table,
                               ModParams mp) {
   u64 total = (u64)nz * (D + 1);
@@ -172,20 +167,36 @@ static __global__ void k_power_table(const u64* __restrict__ alpha, u32 nz, u32 
   }
 }
 
-// One thread per padded slot q.  Bucket g of the padded layout owns [poff[g], poff[g+1]);
-// its first cnt[g] slots are the sorted terms bstart[g] .. bstart[g]+cnt[g]-1, the rest are
-// padding (c = 0, m = 1: contributes 0 at every point).
-// m_i = prod_l alpha_l^{e_il} with n-3 Montgomery products from the power tables
-// ("n-3 multiplications for each m_i thanks to the tables of powers").
-static __global__ void k_setup(const u32* __restrict__ exps, const u64* __restrict__ coeffs, u32 n,
+// m_i = prod_l alpha_l^{e_il} mod p for the input terms [a, b) of one upload chunk (input order), with
+// n-3 Montgomery products from the power tables ("n-3 multiplications for each m_i
+// thanks to the tables of powers"); an exponent beyond the table takes a direct power.  Runs while
+// later chunks are still crossing PCIe.
+static __global__ void k_monomials(const u32* __restrict__ exps, u64 a, u64 b, u32 n,
+                                   const u64* __restrict__ table, const u64* __restrict__ alpha,
+                                   u64* __restrict__ m_in, ModParams mp) {
+  for (u64 i = a + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < b; i += (u64)gridDim.x * blockDim.x) {
+    const u32* e = exps + i * n;
+    u64 acc = mp.r1;   // Montgomery 1
+    for (u32 l = 0; l + 2 < n; ++l) {
+      const u32 x = e[2 + l];
+      const u64 f = x < kTab ? table[(u64)l * kTab + x] : mont_pow(to_mont(alpha[l], mp), x, mp);
+      acc = l == 0 ? f : mont_mul(acc, f, mp);
+    }
+    m_in[i] = from_mont(acc, mp);
+  }
+}
+
+// One thread per padded slot q.  Bucket g of the padded layout owns [poff[g], poff[g+1]); its first
+// cnt[g] slots are the sorted terms bstart[g] .. bstart[g]+cnt[g]-1, the rest are padding (c = 0,
+// m = 1: contributes 0 at every point).  Coefficients reduced mod p (reading R5), m_i from
+// k_monomials, Shoup constant w_i = floor(m_i 2^64 / p).
+static __global__ void k_setup(const u64* __restrict__ coeffs, const u64* __restrict__ m_in,
                         const u32* __restrict__ sorted_idx, const u64* __restrict__ poff,
                         const u64* __restrict__ bstart, u32 G, u64 t_pad,
-                        const u64* __restrict__ table, u32 D, const u64* __restrict__ alpha,
                         u64* __restrict__ c_out, u64* __restrict__ m_out, u64* __restrict__ w_out,
                         u32* __restrict__ perm_out, ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
-    // bucket g: poff[g] <= q < poff[g+1]
-    u32 lo = 0, hi = G;
+    u32 lo = 0, hi = G;   // bucket g: poff[g] <= q < poff[g+1]
     while (hi - lo > 1) {
       u32 mid = (lo + hi) >> 1;
       if (poff[mid] <= q) lo = mid; else hi = mid;
@@ -198,19 +209,7 @@ static __global__ void k_setup(const u32* __restrict__ exps, const u64* __restri
     if (r < cnt) {
       src = sorted_idx[bstart[g] + r];
       c = coeffs[src] % mp.p;
-      const u32* e = exps + (u64)src * n;
-      if (n > 2) {
-        u64 acc;
-        if (table) {
-          acc = table[e[2]];
-          for (u32 l = 1; l + 2 < n; ++l) acc = mont_mul(acc, table[(u64)l * (D + 1) + e[2 + l]], mp);
-        } else {  // exponents too large for tables: direct powers
-          acc = mont_pow(to_mont(alpha[0], mp), e[2], mp);
-          for (u32 l = 1; l + 2 < n; ++l)
-            acc = mont_mul(acc, mont_pow(to_mont(alpha[l], mp), e[2 + l], mp), mp);
-        }
-        m = from_mont(acc, mp);
-      }
+      m = m_in[src];
     }
     c_out[q] = c;
     m_out[q] = m;

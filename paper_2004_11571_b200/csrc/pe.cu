@@ -258,6 +258,30 @@ static unsigned grid_for(u64 n, unsigned block) {
 }
 
 // ---------------------------------------------------------------- create
+// Development: env PE_CREATE_PROF=1 prints the device time between pe_create's phases (CUDA events on
+// the handle stream; host waits show up as gaps).
+struct CreateProf {
+  bool on = false;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  void mark(const char* what, cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.push_back({what, e});
+  }
+  ~CreateProf() {
+    if (!on || ev.empty()) return;
+    cudaEventSynchronize(ev.back().second);
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+      fprintf(stderr, "pe_create %-28s %8.3f ms\n", ev[i].first, ms);
+    }
+    for (auto& x : ev) cudaEventDestroy(x.second);
+  }
+};
+
 static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64* alpha) {
   const u64 t = h->t;
   const u32 n = h->n;
@@ -267,6 +291,9 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   cudaStream_t s = h->stream;
   retain_pool_once(h->device);
   g_alloc_stream = s;
+  CreateProf prof;
+  prof.on = env_int("PE_CREATE_PROF", 0) != 0;
+  prof.mark("start", s);
   if (t == 0) {
     h->G = 0;
     return PE_OK;
@@ -284,16 +311,52 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   tmp.s = s;
   std::vector<u64> alpha_red(nz + 1, 1);
   for (u32 l = 0; l < nz; ++l) alpha_red[l] = alpha[l] % h->p;
-  CU(cudaMemcpyAsync(d_coeffs, coeffs, t * sizeof(u64), cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(d_exps, exps, t * n * sizeof(u32), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(d_alpha, alpha_red.data(), (nz + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
+  // power tables alpha_l^e, e < kTab (a3), ready before the first chunk lands
+  u64* d_table = nullptr;
+  if (nz) {
+    if (dalloc(&d_table, (size_t)nz * kTab)) return g_last_error;
+    tmp.v.push_back(d_table);
+    k_power_table<<<grid_for((u64)nz * kTab, 128), 128, 0, s>>>(d_alpha, nz, kTab - 1, d_table, h->mp);
+    CU(cudaGetLastError());
+  }
 
-  // ---- keys, sort descending (a2); batched polynomials: stable re-sort by polynomial id
-  u64 *d_key, *d_key2; u32 *d_idx, *d_idx2;
-  if (dalloc(&d_key, t) || dalloc(&d_key2, t) || dalloc(&d_idx, t) || dalloc(&d_idx2, t)) return g_last_error;
-  tmp.v.insert(tmp.v.end(), {d_key, d_key2, d_idx, d_idx2});
-  k_keys<<<grid_for(t, 256), 256, 0, s>>>(d_exps, t, n, d_key, d_idx);
-  CU(cudaGetLastError());
+  // ---- upload in chunks on a copy stream; keys (a2) and monomials (a3) of each chunk run on the
+  // handle's stream as soon as it lands, while the next chunks are still crossing PCIe
+  u64 *d_key, *d_key2, *d_m_in; u32 *d_idx, *d_idx2;
+  if (dalloc(&d_key, t) || dalloc(&d_key2, t) || dalloc(&d_idx, t) || dalloc(&d_idx2, t) || dalloc(&d_m_in, t))
+    return g_last_error;
+  tmp.v.insert(tmp.v.end(), {d_key, d_key2, d_idx, d_idx2, d_m_in});
+  {
+    cudaStream_t cs = nullptr;
+    CU(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    const u64 nchunk = t >= (1u << 20) ? 8 : 1;
+    std::vector<cudaEvent_t> ev(nchunk, nullptr);
+    int rc = PE_OK;
+    cudaEvent_t ready = nullptr;   // the copy stream starts after the handle stream's allocations
+    if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ready, s) != cudaSuccess || cudaStreamWaitEvent(cs, ready, 0) != cudaSuccess)
+      rc = PE_ECUDA;
+    for (u64 k = 0; k < nchunk && rc == PE_OK; ++k) {
+      const u64 a = t * k / nchunk, b = t * (k + 1) / nchunk;
+      if (cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming) != cudaSuccess ||
+          cudaMemcpyAsync(d_coeffs + a, coeffs + a, (b - a) * sizeof(u64), cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+          cudaMemcpyAsync(d_exps + a * n, exps + a * n, (b - a) * n * sizeof(u32), cudaMemcpyHostToDevice, cs) !=
+              cudaSuccess ||
+          cudaEventRecord(ev[k], cs) != cudaSuccess || cudaStreamWaitEvent(s, ev[k], 0) != cudaSuccess) {
+        rc = PE_ECUDA;
+        break;
+      }
+      k_keys<<<grid_for(b - a, 256), 256, 0, s>>>(d_exps, a, b, n, d_key, d_idx);
+      k_monomials<<<grid_for(b - a, 256), 256, 0, s>>>(d_exps, a, b, n, d_table, d_alpha, d_m_in, h->mp);
+      if (cudaGetLastError() != cudaSuccess) rc = PE_ECUDA;
+    }
+    for (auto e : ev) if (e) cudaEventDestroy(e);   // destruction is deferred until the events complete
+    if (ready) cudaEventDestroy(ready);
+    cudaStreamDestroy(cs);                           // likewise: returns at once, the copies still run
+    if (rc != PE_OK) return set_err(rc);
+  }
+  prof.mark("upload+keys+monomials", s);
   const u32 npoly = (u32)h->poly_off.size() - 1;
   size_t sort_bytes = 0, sort2_bytes = 0, sel_bytes = 0;
   unsigned char* d_flags;
@@ -332,18 +395,9 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   CU(cudaGetLastError());
   CU(cub::DeviceSelect::Flagged(d_cub, sel_bytes, counting, d_flags, d_starts, d_nruns, (int)t, s));
 
-  // max evaluated exponent -> power-table size
-  u32* d_dmax;
-  if (dalloc(&d_dmax, 1)) return g_last_error;
-  tmp.v.push_back(d_dmax);
-  CU(cudaMemsetAsync(d_dmax, 0, sizeof(u32), s));
-  if (nz) {
-    k_max_exp<<<grid_for(t, 256), 256, 0, s>>>(d_exps, t, n, d_dmax);
-    CU(cudaGetLastError());
-  }
-  u32 nruns = 0, D = 0;
+  prof.mark("sort+runs", s);
+  u32 nruns = 0;
   CU(cudaMemcpyAsync(&nruns, d_nruns, sizeof(u32), cudaMemcpyDeviceToHost, s));
-  CU(cudaMemcpyAsync(&D, d_dmax, sizeof(u32), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   const u64 G = nruns;
   h->G = G;
@@ -416,15 +470,6 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   slot_start[G] = slot;
   h->n_slots = slot;
 
-  // ---- power tables (a3)
-  u64* d_table = nullptr;
-  const u64 tab_entries = (u64)nz * ((u64)D + 1);
-  if (nz && tab_entries <= (1ull << 22)) {
-    if (dalloc(&d_table, tab_entries)) return g_last_error;
-    tmp.v.push_back(d_table);
-    k_power_table<<<grid_for(tab_entries, 128), 128, 0, s>>>(d_alpha, nz, D, d_table, h->mp);
-    CU(cudaGetLastError());
-  }
   // ---- padded layout + monomials
   u64 *d_poff, *d_bstart;
   if (dalloc(&d_poff, G + 1) || dalloc(&d_bstart, G + 1)) return g_last_error;
@@ -434,9 +479,9 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   if (dalloc(&h->d_c, h->t_pad) || dalloc(&h->d_m, h->t_pad) || dalloc(&h->d_w, h->t_pad) ||
       dalloc(&h->d_perm, h->t_pad) || dalloc(&h->d_wt_info, n_wt) || dalloc(&h->d_slot_start, G + 1))
     return g_last_error;
-  k_setup<<<grid_for(h->t_pad, 256), 256, 0, s>>>(d_exps, d_coeffs, n, d_idxS, d_poff, d_bstart, (u32)G,
-                                                   h->t_pad, d_table, D, d_alpha, h->d_c, h->d_m, h->d_w,
-                                                   h->d_perm, h->mp);
+  prof.mark("host plan (+gaps)", s);
+  k_setup<<<grid_for(h->t_pad, 256), 256, 0, s>>>(d_coeffs, d_m_in, d_idxS, d_poff, d_bstart, (u32)G, h->t_pad,
+                                                   h->d_c, h->d_m, h->d_w, h->d_perm, h->mp);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(h->d_wt_info, wt_info.data(), n_wt * sizeof(uint2), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(h->d_slot_start, slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
@@ -465,12 +510,32 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
       CU(cudaStreamSynchronize(s));
       return PE_OK;
     }
-    tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
-    CU(cudaGetLastError());
-    const u64 nrp = (tp + 2 * tc::kKB - 1) / (2 * tc::kKB);   // blocks of 2 K-blocks
-    tc::k_tc_rplanes<<<(unsigned)std::max<u64>(1, std::min<u64>(nrp, 148ull * 16)), tc::kRpThreads, 0, s>>>(
-        h->d_m, tp, h->d_tcR, h->mp);
-    CU(cudaGetLastError());
+    prof.mark("k_setup (+copies)", s);
+    // the C records (k_tc_setup) and the baby-step planes (k_tc_rplanes) both depend only on m:
+    // the former runs on a side stream beside the latter
+    {
+      cudaStream_t s2 = nullptr;
+      cudaEvent_t e_m = nullptr, e_done = nullptr;
+      CU(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+      int rc = PE_OK;
+      if (cudaEventCreateWithFlags(&e_m, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&e_done, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventRecord(e_m, s) != cudaSuccess || cudaStreamWaitEvent(s2, e_m, 0) != cudaSuccess)
+        rc = PE_ECUDA;
+      if (rc == PE_OK) {
+        tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s2>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
+        const u64 nrp = (tp + 2 * tc::kKB - 1) / (2 * tc::kKB);   // blocks of 2 K-blocks
+        tc::k_tc_rplanes<<<(unsigned)std::max<u64>(1, std::min<u64>(nrp, 148ull * 16)), tc::kRpThreads, 0, s>>>(
+            h->d_m, tp, h->d_tcR, h->mp);
+        if (cudaGetLastError() != cudaSuccess || cudaEventRecord(e_done, s2) != cudaSuccess ||
+            cudaStreamWaitEvent(s, e_done, 0) != cudaSuccess)
+          rc = PE_ECUDA;
+      }
+      if (e_m) cudaEventDestroy(e_m);
+      if (e_done) cudaEventDestroy(e_done);
+      cudaStreamDestroy(s2);
+      if (rc != PE_OK) return set_err(rc);
+    }
     CU(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
     h->tc_rounds = h->p < (1ull << 31) ? 1 : tc::kRounds;   // 4-byte digits: one round
     if (cudaHostAlloc((void**)&h->h_status, sizeof(u32), cudaHostAllocMapped) != cudaSuccess) return set_err(PE_ENOMEM);
@@ -481,6 +546,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
     const int rc = fast::create(h->h_poff, h->mp, s, &h->fast);
     if (rc != PE_OK) return set_err(rc);
   }
+  prof.mark("tc setup + rplanes", s);
   CU(cudaStreamSynchronize(s));  // host vectors above must outlive the copies; tmp frees after
   return PE_OK;
 }
