@@ -17,8 +17,8 @@
 //   root (N, E)         Y = D^-1 mod z^T2 by Newton (Y <- Y (2 - D Y), precision doubling), then
 //                       out = N Y mod z^T.
 //
-// Polynomial products over F_p (any p < 2^62) are exact integer convolutions recovered by CRT from
-// 5 NTT primes q_j < 2^30 (q_j = c 2^20 + 1; prod q_j > 2^149 > 2 L p^2 for L <= 2^20); operands
+// Polynomial products over F_p (any p < 2^63) are exact integer convolutions recovered by CRT from
+// 5 NTT primes q_j < 2^30 (q_j = c 2^20 + 1; prod q_j > 2^149 > 2 L p^2 = 2^147 for L <= 2^20); operands
 // longer than 4096 are cut into 4096-coefficient blocks whose 8192-point transforms are multiplied
 // block-pairwise in the transform domain (a + b = c) and overlap-added -- so one shared-memory NTT
 // of at most 8192 points serves every length.  Three batched kernels per product call:
@@ -298,7 +298,7 @@ __device__ __forceinline__ u64 crt_modp(const u32 (&r)[kNP], const Consts& C, co
   return y;
 }
 __device__ __forceinline__ u64 addp(u64 x, u64 y, u64 p) {
-  const u64 s = x + y;   // x, y < p < 2^62
+  const u64 s = x + y;   // x, y < p < 2^63: no wrap
   return s >= p ? s - p : s;
 }
 
@@ -575,7 +575,6 @@ void destroy(Plan* P, cudaStream_t s) {
 
 int create(const std::vector<u64>& poff, const ModParams& mp, cudaStream_t s, Plan** out) {
   *out = nullptr;
-  if (mp.p >= (1ull << 62)) return PE_ENOTSUP;   // CRT bound: 2 L p^2 < prod q_j needs p < 2^62
   Plan* P = new Plan();
   P->G = poff.size() - 1;
   P->t_pad = poff.back();

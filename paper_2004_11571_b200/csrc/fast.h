@@ -15,11 +15,11 @@ constexpr int kLgMax = 13;          // largest shared-memory transform: 2^13 poi
 constexpr unsigned kSmax = 1u << kLgMax;
 constexpr unsigned kBkMax = kSmax / 2;   // operand block (block convolution above this length)
 constexpr unsigned kTile = kSmax;        // points per CTA in the transform kernels
-constexpr unsigned long long kTMax = 1ull << 20;   // CRT bound: prod q_j > 2 T2 p^2 for p < 2^62
+constexpr unsigned long long kTMax = 1ull << 20;   // CRT bound: prod q_j (2^149.7) > 2 T2 p^2 (< 2^147)
 
 struct Plan;
-// Tree shape from the padded bucket offsets (multiples of 32): PE_OK / PE_ENOTSUP (p >= 2^62) /
-// PE_ENOMEM / PE_ECUDA.
+// Tree shape from the padded bucket offsets (multiples of 32), any p < 2^63: PE_OK / PE_ENOMEM /
+// PE_ECUDA.
 int create(const std::vector<u64>& poff, const ModParams& mp, cudaStream_t s, Plan** out);
 // out[g*ld + k] = sum_{i in g} c_i m_i^{j0+k}, k < T (padded-layout c, m on the device).
 int eval(Plan* P, const u64* d_c, const u64* d_m, const ModParams& mp, u64 j0, u64 T, u64* d_out, u64 ld,

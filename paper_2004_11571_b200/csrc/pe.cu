@@ -595,8 +595,7 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
   } else if (path_req == PE_PATH_TC) {
     path = p < (1ull << 62) ? kInt4 : kInt2;
   } else if (path_req == PE_PATH_FAST) {
-    if (p >= (1ull << 62)) { set_err(PE_ENOTSUP); return nullptr; }
-    path = kInt4;
+    path = p < (1ull << 62) ? kInt4 : kInt2;
   } else {
     set_err(PE_EINVAL);
     return nullptr;
@@ -610,7 +609,7 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
   // fast method: forced by PE_PATH_FAST; automatic (p < 2^62, T >= the measured crossover) unless
   // env PE_FAST=0; PE_FAST=2 forces it for PE_PATH_AUTO handles
   int fast_mode = path_req == PE_PATH_FAST ? 2 : 0;
-  if (path_req == PE_PATH_AUTO && p < (1ull << 62)) {
+  if (path_req == PE_PATH_AUTO) {
     const int e = env_int("PE_FAST", 1);
     fast_mode = e <= 0 ? 0 : (e >= 2 ? 2 : 1);
   }

@@ -50,7 +50,9 @@ def check_incremental(w):
     (P62, 2, 30, 6, 1, 10),                # n = 2: m = 1, D = (1 - z)^s
     (2**31 - 1, 3, 100, 9, 1, 64),
     ((1 << 50) - 27, 7, 600, 4, 3, 77),
-    ((1 << 62) - 87, 6, 700, 4, 5, 300),   # near the top of the supported range
+    ((1 << 62) - 87, 6, 700, 4, 5, 300),
+    ((1 << 62) + 135, 5, 400, 3, 1, 129),   # just above 2^62
+    ((1 << 63) - 25, 6, 700, 4, 5, 300),    # largest supported p: 2 L p^2 < 2^147 < prod q_j
     (P62, 6, 300, 4, 1, 4097),             # T2 = 8192: the first block-convolved length
     (P62, 6, 5000, 4, 1, 2048),            # buckets longer than T2 (truncated upper levels)
 ])
@@ -104,10 +106,6 @@ def test_fast_equals_tc_and_step():
 
 
 def test_fast_limits():
-    w = synth.random_small(823, (1 << 62) + 135, 5, 50, 3, 10, 1)
-    with pytest.raises(pe.PEError) as ei:
-        pe.Context.from_workload(w, path=pe.PATH_FAST)
-    assert ei.value.code == pe.PE_ENOTSUP
     w = synth.random_small(824, P62, 5, 50, 3, 10, 1)
     with pe.Context.from_workload(w, path=pe.PATH_FAST) as ctx:
         with pytest.raises(pe.PEError) as ei:
