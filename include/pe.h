@@ -106,6 +106,15 @@ pe_ctx* pe_create_ex(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs,
                      const uint32_t* exps, const uint64_t* alpha, const pe_config* cfg);
 
 /*
+ * pe_create_compact -- pe_create_ex with exponents as HOST uint8[t*n] (same row-major layout; every
+ * degree < 256, which covers every BASELINE config and the paper's workloads).
+ * A quarter of the bytes to move over PCIe for the same polynomial: the upload is most of an
+ * end-to-end evaluation.  Same results, errors and ownership as pe_create_ex.
+ */
+pe_ctx* pe_create_compact(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs, const uint8_t* exps,
+                          const uint64_t* alpha, const pe_config* cfg);
+
+/*
  * pe_create_batch -- several polynomials f_0..f_{npoly-1} evaluated at the SAME points beta^j in
  * one launch (the gcd workload: images of f and h at the same beta^t;
  * SURVEY.md §8(f) NEXT-1).  Polynomial k owns terms [sum_{q<k} t_per_poly[q], ... + t_per_poly[k])

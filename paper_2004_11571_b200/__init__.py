@@ -29,7 +29,7 @@ EXPORTS = ["pe_create", "pe_create_ex", "pe_eval", "pe_eval_device", "pe_destroy
            "pe_bucket_exps", "pe_info", "pe_monomials", "pe_last_error", "pe_strerror",
            "pe_interp_bound_ok", "pe_set_timing", "pe_kernel_stats",
            "pe_create_batch", "pe_num_polys", "pe_poly_rows", "pe_bm_device", "pe_bm", "pe_tc_info",
-           "pe_rows_addmod", "pe_unshard_columns", "pe_eval_kernel"]
+           "pe_rows_addmod", "pe_unshard_columns", "pe_eval_kernel", "pe_create_compact"]
 #: every symbol include/pe_test.h declares (libpe_test.so)
 TEST_EXPORTS = ["pe_test_core", "pe_bench_core", "pe_bench_mma"]
 
@@ -87,6 +87,8 @@ def lib():
         L.pe_kernel_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         L.pe_kernel_stats.restype = ctypes.c_int
+        L.pe_create_compact.argtypes = [u64, u64, u32, vp, vp, vp, ctypes.POINTER(Config)]
+        L.pe_create_compact.restype = vp
         L.pe_create_batch.argtypes = [u64, u32, vp, u32, vp, vp, vp, ctypes.POINTER(Config)]
         L.pe_create_batch.restype = vp
         L.pe_num_polys.argtypes = [vp]
@@ -146,16 +148,24 @@ class Context:
     """An evaluation handle (``pe_create_ex``).  Arrays are host numpy arrays."""
 
     def __init__(self, p: int, coeffs, exps, alpha, n: int | None = None, path: int = PATH_AUTO,
-                 R: int = 0, warps: int = 0, chunk: int = 0):
+                 R: int = 0, warps: int = 0, chunk: int = 0, compact: bool = False):
+        """compact=True: exponents passed as uint8 (pe_create_compact; every degree must be < 256)."""
         coeffs = np.ascontiguousarray(coeffs, dtype=np.uint64).ravel()
-        exps = np.ascontiguousarray(exps, dtype=np.uint32)
+        if compact:
+            e = np.asarray(exps)
+            if e.size and int(e.max()) > 255:
+                raise ValueError("compact exponents must be < 256")
+            exps = np.ascontiguousarray(e, dtype=np.uint8)
+        else:
+            exps = np.ascontiguousarray(exps, dtype=np.uint32)
         n = exps.shape[1] if n is None else n
-        exps = exps.reshape(-1, n) if exps.size else np.zeros((0, n), np.uint32)
+        exps = exps.reshape(-1, n) if exps.size else np.zeros((0, n), exps.dtype)
         alpha = np.ascontiguousarray(alpha, dtype=np.uint64).ravel()
         self.p, self.n, self.t = int(p), int(n), int(coeffs.size)
         cfg = Config(path, R, warps, chunk)
         L = lib()
-        h = L.pe_create_ex(self.p, self.t, self.n, _ptr(coeffs), _ptr(exps), _ptr(alpha), ctypes.byref(cfg))
+        create = L.pe_create_compact if compact else L.pe_create_ex
+        h = create(self.p, self.t, self.n, _ptr(coeffs), _ptr(exps), _ptr(alpha), ctypes.byref(cfg))
         if not h:
             raise PEError(L.pe_last_error(), "pe_create")
         self._h = ctypes.c_void_p(h)

@@ -108,8 +108,10 @@ __device__ __forceinline__ U96 xpose_reduce8(U96 (&v)[8], int lane) {
 }
 
 // ---------------------------------------------------------------- setup kernels
-// Terms [a, b) (one upload chunk): bucket key and input index.
-static __global__ void k_keys(const u32* __restrict__ exps, u64 a, u64 b, u32 n, u64* __restrict__ key,
+// Terms [a, b) (one upload chunk): bucket key and input index.  E: exponent type of the input
+// (u32, or u8 for pe_create_compact).
+template <class E>
+static __global__ void k_keys(const E* __restrict__ exps, u64 a, u64 b, u32 n, u64* __restrict__ key,
                        u32* __restrict__ idx) {
   for (u64 i = a + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < b; i += (u64)gridDim.x * blockDim.x) {
     key[i] = ((u64)exps[i * n + 0] << 32) | exps[i * n + 1];
@@ -171,11 +173,12 @@ static __global__ void k_power_table(const u64* __restrict__ alpha, u32 nz, u32 
 // n-3 Montgomery products from the power tables ("n-3 multiplications for each m_i
 // thanks to the tables of powers"); an exponent beyond the table takes a direct power.  Runs while
 // later chunks are still crossing PCIe.
-static __global__ void k_monomials(const u32* __restrict__ exps, u64 a, u64 b, u32 n,
+template <class E>
+static __global__ void k_monomials(const E* __restrict__ exps, u64 a, u64 b, u32 n,
                                    const u64* __restrict__ table, const u64* __restrict__ alpha,
                                    u64* __restrict__ m_in, ModParams mp) {
   for (u64 i = a + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < b; i += (u64)gridDim.x * blockDim.x) {
-    const u32* e = exps + i * n;
+    const E* e = exps + i * n;
     u64 acc = mp.r1;   // Montgomery 1
     for (u32 l = 0; l + 2 < n; ++l) {
       const u32 x = e[2 + l];

@@ -282,7 +282,8 @@ struct CreateProf {
   }
 };
 
-static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64* alpha) {
+template <class E>
+static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* alpha) {
   const u64 t = h->t;
   const u32 n = h->n;
   const u32 nz = n - 2;
@@ -300,7 +301,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   }
 
   // ---- upload (a1)
-  u64* d_coeffs; u32* d_exps; u64* d_alpha;
+  u64* d_coeffs; E* d_exps; u64* d_alpha;
   if (dalloc(&d_coeffs, t) || dalloc(&d_exps, t * n) || dalloc(&d_alpha, nz + 1)) return g_last_error;
   struct Tmp {
     std::vector<void*> v;
@@ -341,7 +342,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
       const u64 a = t * k / nchunk, b = t * (k + 1) / nchunk;
       if (cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming) != cudaSuccess ||
           cudaMemcpyAsync(d_coeffs + a, coeffs + a, (b - a) * sizeof(u64), cudaMemcpyHostToDevice, cs) != cudaSuccess ||
-          cudaMemcpyAsync(d_exps + a * n, exps + a * n, (b - a) * n * sizeof(u32), cudaMemcpyHostToDevice, cs) !=
+          cudaMemcpyAsync(d_exps + a * n, exps + a * n, (b - a) * n * sizeof(E), cudaMemcpyHostToDevice, cs) !=
               cudaSuccess ||
           cudaEventRecord(ev[k], cs) != cudaSuccess || cudaStreamWaitEvent(s, ev[k], 0) != cudaSuccess) {
         rc = PE_ECUDA;
@@ -551,8 +552,9 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const u32* exps, const u64*
   return PE_OK;
 }
 
+template <class E>
 static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_poly, uint32_t n,
-                             const uint64_t* coeffs, const uint32_t* exps, const uint64_t* alpha,
+                             const uint64_t* coeffs, const E* exps, const uint64_t* alpha,
                              const pe_config* cfg) {
   g_last_error = PE_OK;
   // ---- validation before any CUDA call
@@ -660,6 +662,11 @@ extern "C" pe_ctx* pe_create_batch(uint64_t p, uint32_t npoly, const uint64_t* t
                                    const uint64_t* coeffs, const uint32_t* exps, const uint64_t* alpha,
                                    const pe_config* cfg) {
   return create_common(p, npoly, t_per_poly, n, coeffs, exps, alpha, cfg);
+}
+
+extern "C" pe_ctx* pe_create_compact(uint64_t p, uint64_t t, uint32_t n, const uint64_t* coeffs,
+                                     const uint8_t* exps, const uint64_t* alpha, const pe_config* cfg) {
+  return create_common(p, 1, &t, n, coeffs, exps, alpha, cfg);
 }
 
 extern "C" uint32_t pe_num_polys(const pe_ctx* h) { return h ? (uint32_t)h->poly_off.size() - 1 : 0; }

@@ -37,10 +37,11 @@ def test_random_shapes_all_kernels(seed):
     paths = [pe.PATH_AUTO, pe.PATH_INT, pe.PATH_TC, pe.PATH_FAST]
     if w.p < (1 << 50):
         paths.append(pe.PATH_FP64)
-    for path in paths:
-        with pe.Context.from_workload(w, path=path) as ctx:
+    variants = [(path, False) for path in paths] + [(pe.PATH_AUTO, True)]   # + uint8 exponents
+    for path, compact in variants:
+        with pe.Context.from_workload(w, path=path, compact=compact) as ctx:
             out = ctx.eval(w.j0, w.T)
             kern = ctx.eval_kernel(w.T)
         bad = np.argwhere(out != ref)
-        assert bad.size == 0, (f"p={w.p} n={w.n} t={w.t} T={w.T} j0={w.j0} path={path} ({kern}): "
+        assert bad.size == 0, (f"p={w.p} n={w.n} t={w.t} T={w.T} j0={w.j0} path={path} compact={compact} ({kern}): "
                                f"{len(bad)} mismatches, first {bad[:3].tolist()}")

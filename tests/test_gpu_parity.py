@@ -76,14 +76,15 @@ def config5_ref():
     return w, full
 
 
-@pytest.mark.parametrize("path", [pe.PATH_AUTO, pe.PATH_INT])
-def test_config5_full(path, config5_ref):
+@pytest.mark.parametrize("path,compact", [(pe.PATH_AUTO, False), (pe.PATH_INT, False), (pe.PATH_AUTO, True)])
+def test_config5_full(path, compact, config5_ref):
     """Full size in the bench launch configuration (PATH_AUTO = the tensor-core k_tc; PATH_INT = the
-    scalar k_step), compared over the WHOLE G x T output with the incremental checker, plus 24
+    scalar k_step; compact = the uint8-exponent entry pe_create_compact), compared over the WHOLE
+    G x T output with the incremental checker, plus 24
     columns against the direct definition -- chosen to hit every TMEM lane quarter (u = 0..127 in
     groups of 32) of both 8192-point chunks, the chunk edges and v = 0 / 63."""
     w, full = config5_ref
-    with pe.Context.from_workload(w, path=path) as ctx:
+    with pe.Context.from_workload(w, path=path, compact=compact) as ctx:
         assert ctx.uses_tc(w.T) == (path == pe.PATH_AUTO)
         out = ctx.eval(w.j0, w.T)
         rows = ctx.buckets()
