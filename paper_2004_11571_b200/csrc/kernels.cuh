@@ -112,10 +112,27 @@ __device__ __forceinline__ U96 xpose_reduce8(U96 (&v)[8], int lane) {
 // (u32, or u8 for pe_create_compact).
 template <class E>
 static __global__ void k_keys(const E* __restrict__ exps, u64 a, u64 b, u32 n, u64* __restrict__ key,
-                       u32* __restrict__ idx) {
+                       u32* __restrict__ idx, u32* __restrict__ kmax) {
+  u32 mx = 0, my = 0;
   for (u64 i = a + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < b; i += (u64)gridDim.x * blockDim.x) {
-    key[i] = ((u64)exps[i * n + 0] << 32) | exps[i * n + 1];
+    const u32 dx = exps[i * n + 0], dy = exps[i * n + 1];
+    key[i] = ((u64)dx << 32) | dy;
     idx[i] = (u32)i;
+    mx = max(mx, dx);
+    my = max(my, dy);
+  }
+  for (int o = 16; o; o >>= 1) {   // the largest degrees in x and y (the sort's key width)
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    my = max(my, __shfl_xor_sync(0xffffffffu, my, o));
+  }
+  if ((threadIdx.x & 31) == 0) { atomicMax(kmax, mx); atomicMax(kmax + 1, my); }
+}
+// Keys (dx << 32 | dy) -> (dx << bd | dy) with dy < 2^bd: the same order in bx + bd bits, so the
+// radix sort runs ceil((bx + bd) / 8) passes instead of 8 (config 5: 2).
+static __global__ void k_pack_keys(u64* __restrict__ key, u64 t, u32 bd) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < t; i += (u64)gridDim.x * blockDim.x) {
+    const u64 k = key[i];
+    key[i] = ((k >> 32) << bd) | (k & 0xffffffffull);
   }
 }
 

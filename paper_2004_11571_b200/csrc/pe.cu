@@ -324,10 +324,12 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
 
   // ---- upload in chunks on a copy stream; keys (a2) and monomials (a3) of each chunk run on the
   // handle's stream as soon as it lands, while the next chunks are still crossing PCIe
-  u64 *d_key, *d_key2, *d_m_in; u32 *d_idx, *d_idx2;
-  if (dalloc(&d_key, t) || dalloc(&d_key2, t) || dalloc(&d_idx, t) || dalloc(&d_idx2, t) || dalloc(&d_m_in, t))
+  u64 *d_key, *d_key2, *d_m_in; u32 *d_idx, *d_idx2, *d_kmax;
+  if (dalloc(&d_key, t) || dalloc(&d_key2, t) || dalloc(&d_idx, t) || dalloc(&d_idx2, t) || dalloc(&d_m_in, t) ||
+      dalloc(&d_kmax, 2))
     return g_last_error;
-  tmp.v.insert(tmp.v.end(), {d_key, d_key2, d_idx, d_idx2, d_m_in});
+  tmp.v.insert(tmp.v.end(), {d_key, d_key2, d_idx, d_idx2, d_m_in, d_kmax});
+  CU(cudaMemsetAsync(d_kmax, 0, 2 * sizeof(u32), s));
   {
     cudaStream_t cs = nullptr;
     CU(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -348,7 +350,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
         rc = PE_ECUDA;
         break;
       }
-      k_keys<<<grid_for(b - a, 256), 256, 0, s>>>(d_exps, a, b, n, d_key, d_idx);
+      k_keys<<<grid_for(b - a, 256), 256, 0, s>>>(d_exps, a, b, n, d_key, d_idx, d_kmax);
       k_monomials<<<grid_for(b - a, 256), 256, 0, s>>>(d_exps, a, b, n, d_table, d_alpha, d_m_in, h->mp);
       if (cudaGetLastError() != cudaSuccess) rc = PE_ECUDA;
     }
@@ -358,6 +360,14 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
     if (rc != PE_OK) return set_err(rc);
   }
   prof.mark("upload+keys+monomials", s);
+  // key width: the largest x and y degrees (the host waits here for the upload it cannot pass)
+  u32 kmax[2] = {0, 0};
+  CU(cudaMemcpyAsync(kmax, d_kmax, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  auto nbits = [](u32 x) { int b = 0; while (b < 32 && (x >> b)) ++b; return b; };
+  const int bd = nbits(kmax[1]), key_bits = std::max(1, nbits(kmax[0]) + bd);
+  k_pack_keys<<<grid_for(t, 256), 256, 0, s>>>(d_key, t, (u32)bd);
+  CU(cudaGetLastError());
   const u32 npoly = (u32)h->poly_off.size() - 1;
   size_t sort_bytes = 0, sort2_bytes = 0, sel_bytes = 0;
   unsigned char* d_flags;
@@ -375,7 +385,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
   void* d_cub;
   if (dalloc((char**)&d_cub, std::max(std::max(sort_bytes, sort2_bytes), sel_bytes))) return g_last_error;
   tmp.v.push_back(d_cub);
-  CU(cub::DeviceRadixSort::SortPairsDescending(d_cub, sort_bytes, d_key, d_key2, d_idx, d_idx2, (int)t, 0, 64, s));
+  CU(cub::DeviceRadixSort::SortPairsDescending(d_cub, sort_bytes, d_key, d_key2, d_idx, d_idx2, (int)t, 0,
+                                               key_bits, s));
   u64* d_keyS = d_key2;   // final order: (polynomial asc, dx desc, dy desc)
   u32* d_idxS = d_idx2;
   if (npoly > 1) {
@@ -417,7 +428,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
   starts[G] = (u32)t;
   for (u64 g = 0; g < G; ++g) counts[g] = starts[g + 1] - starts[g];
   h->dxdy.resize(2 * G);
-  for (u64 g = 0; g < G; ++g) { h->dxdy[2 * g] = (u32)(ukeys[g] >> 32); h->dxdy[2 * g + 1] = (u32)ukeys[g]; }
+  const u64 ymask = bd >= 64 ? ~0ull : ((1ull << bd) - 1);
+  for (u64 g = 0; g < G; ++g) { h->dxdy[2 * g] = (u32)(ukeys[g] >> bd); h->dxdy[2 * g + 1] = (u32)(ukeys[g] & ymask); }
   h->poly_rows.assign(npoly + 1, G);
   for (u64 g = G; g-- > 0;) h->poly_rows[upid[g]] = g;            // first row of each polynomial
   for (u32 k = npoly; k-- > 0;) h->poly_rows[k] = std::min(h->poly_rows[k], h->poly_rows[k + 1]);
