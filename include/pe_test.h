@@ -21,7 +21,9 @@ enum {
   PE_CORE_POW = 5,     /* a * b^e mod p via Montgomery square-and-multiply: e = extra[i]      */
   PE_CORE_SHOUP4RAW = 6, /* raw lazy output of SHOUP4 (must be < 4p and == a*b mod p)         */
   PE_CORE_HYB = 7,       /* hybrid FP64-quotient product, p < 2^63; probe canonicalises        */
-  PE_CORE_HYBRAW = 8     /* raw output of HYB (must be in (0, 2p) and == a*b mod p)            */
+  PE_CORE_HYBRAW = 8,    /* raw output of HYB (must be in (0, 2p) and == a*b mod p)            */
+  PE_CORE_SHOUPW = 9     /* shoup_w_fast(b) XOR shoup_w(b): 0 iff the Montgomery form of the Shoup
+                            constant floor(b 2^64 / p) agrees with the bit-loop division       */
 };
 
 /*

@@ -22,7 +22,8 @@ TEST_LIB_PATH = os.path.join(_PKG, "libpe_test.so")   # include/pe_test.h: probe
 
 PE_OK, PE_EINVAL, PE_ENOTPRIME, PE_ERANGE, PE_ENOMEM, PE_ECUDA, PE_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
 PATH_AUTO, PATH_INT, PATH_FP64, PATH_INT32, PATH_TC, PATH_FAST = 0, 1, 2, 4, 5, 6
-CORE_SHOUP4, CORE_SHOUP2, CORE_MONT, CORE_FP64, CORE_FP64ADD, CORE_POW, CORE_SHOUP4RAW, CORE_HYB, CORE_HYBRAW = range(9)
+(CORE_SHOUP4, CORE_SHOUP2, CORE_MONT, CORE_FP64, CORE_FP64ADD, CORE_POW, CORE_SHOUP4RAW, CORE_HYB, CORE_HYBRAW,
+ CORE_SHOUPW) = range(10)
 
 #: every symbol include/pe.h declares (libpe.so)
 EXPORTS = ["pe_create", "pe_create_ex", "pe_eval", "pe_eval_device", "pe_destroy", "pe_num_buckets",

@@ -233,7 +233,7 @@ static __global__ void k_setup(const u64* __restrict__ coeffs, const u64* __rest
     }
     c_out[q] = c;
     m_out[q] = m;
-    w_out[q] = shoup_w(m, mp.p);
+    w_out[q] = shoup_w_fast(m, mp);
     perm_out[q] = src;
   }
 }

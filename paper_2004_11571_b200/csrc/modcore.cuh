@@ -230,6 +230,13 @@ __device__ __forceinline__ u64 shoup_w(u64 m, u64 p) {
   return q;
 }
 
+// floor(m * 2^64 / p) for m < p without the bit loop: with rem = m 2^64 mod p (= to_mont(m)),
+// m 2^64 = w p + rem, so w p == -rem (mod 2^64) and w = rem * (-p^{-1}) mod 2^64 = rem * mp.pinv --
+// exact because 0 <= w < 2^64.  One Montgomery product and one 64-bit multiply.
+__device__ __forceinline__ u64 shoup_w_fast(u64 m, const ModParams& mp) {
+  return to_mont(m, mp) * mp.pinv;
+}
+
 // ---------------------------------------------------------------- FP64 Alg. 2 / Alg. 3
 // Alg. 2, p < 2^50, x,y in [0,p) as exact doubles; returns [0,p).
 __device__ __forceinline__ double mul_fp(double x, double y, double p, double u) {

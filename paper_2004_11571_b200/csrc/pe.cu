@@ -538,8 +538,11 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
       if (rc == PE_OK) {
         tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s2>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
         const u64 nrp = (tp + 2 * tc::kKB - 1) / (2 * tc::kKB);   // blocks of 2 K-blocks
-        tc::k_tc_rplanes<<<(unsigned)std::max<u64>(1, std::min<u64>(nrp, 148ull * 16)), tc::kRpThreads, 0, s>>>(
-            h->d_m, tp, h->d_tcR, h->mp);
+        const unsigned rpg = (unsigned)std::max<u64>(1, std::min<u64>(nrp, 148ull * 16));
+        if (h->p >= (1ull << 31) && h->p < (1ull << 62))
+          tc::k_tc_rplanes<true><<<rpg, tc::kRpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
+        else
+          tc::k_tc_rplanes<false><<<rpg, tc::kRpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
         if (cudaGetLastError() != cudaSuccess || cudaEventRecord(e_done, s2) != cudaSuccess ||
             cudaStreamWaitEvent(s, e_done, 0) != cudaSuccess)
           rc = PE_ECUDA;

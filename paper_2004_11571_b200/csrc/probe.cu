@@ -45,6 +45,7 @@ __global__ void k_probe(int variant, u64 N, const u64* a, const u64* b, const u6
         break;
       }
       case PE_CORE_SHOUP2: r = csub(mul_shoup2(ai, bi, shoup_w(bi, mp.p), mp.np), mp.p); break;
+      case PE_CORE_SHOUPW: r = shoup_w_fast(bi, mp) ^ shoup_w(bi, mp.p); break;   // 0 iff the two agree
       case PE_CORE_MONT: r = mulmod(ai, bi, mp); break;
       case PE_CORE_FP64: {
         double g = mul_fp((double)ai, (double)bi, mp.pd, mp.u);
@@ -76,7 +77,7 @@ extern "C" int pe_test_core(int variant, uint64_t p, uint64_t N, const uint64_t*
   if (p < 3 || p >= (1ull << 63) || (p & 1) == 0) return PE_ERANGE;
   if ((variant == PE_CORE_SHOUP4 || variant == PE_CORE_SHOUP4RAW) && p >= (1ull << 62)) return PE_ENOTSUP;
   if ((variant == PE_CORE_FP64 || variant == PE_CORE_FP64ADD) && p >= (1ull << 50)) return PE_ENOTSUP;
-  if (variant < 0 || variant > 8 || (N && (!a || !b || !out)) || (variant == PE_CORE_POW && N && !extra))
+  if (variant < 0 || variant > 9 || (N && (!a || !b || !out)) || (variant == PE_CORE_POW && N && !extra))
     return PE_EINVAL;
   if (N == 0) return PE_OK;
   u64 *da, *db, *dx = nullptr, *dout;

@@ -924,7 +924,7 @@ static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __r
     }
     const u64 aL = from_mont(g, mp);                   // m^{8V}
     C[q * kCRec + kC_mL] = aL;
-    C[q * kCRec + kC_wL] = shoup_w(aL, mp.p);
+    C[q * kCRec + kC_wL] = shoup_w_fast(aL, mp);
     MS[2 * q] = mV;
     MS[2 * q + 1] = mont_pow(mV, kU, mp);              // m^{kChunk}
   }
@@ -936,6 +936,11 @@ static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __r
 // shared memory; thread = (4 terms, rows r + 8j): one warp's stores cover 8 consecutive rows x
 // 16 bytes, and the block leaves with 16-byte coalesced stores.
 constexpr int kRpThreads = 128;
+// The stride-8 chain of a lane (rows r, r + 8, ...) multiplies by the fixed m^8 with Shoup products
+// (its constant is m8_mont * (-p^-1) mod 2^64, modcore.cuh shoup_w_fast): any representative below
+// 2^digits is exact for the MMAs, so LAZY chains (values < 4p) serve 2^31 <= p < 2^62 (8 digits, or 7
+// when p < 2^54: 4p < 2^56) and exact-quotient ones (< 2p) the 4-digit (p < 2^31) and p >= 2^62 modes.
+template <bool LAZY>
 static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __restrict__ m, u64 t_pad,
                                                                   uint8_t* __restrict__ Rp, ModParams mp) {
   __shared__ __align__(16) uint8_t st[2 * kRBytes];
@@ -946,17 +951,19 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
   const u32 base = kbl * kRBytes + h * kLBOB + r * 16u + ql * 4u;
   for (u64 blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const u64 q0 = blk * 2 * kKB + kbl * kKB + h * 16 + ql * 4;
-    u64 y[4], m8[4];
+    u64 y[4], m8[4], w8[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const u64 mm = to_mont(q0 + e < t_pad ? m[q0 + e] : 0ull, mp);
       const u64 m2 = mont_mul(mm, mm, mp), m4 = mont_mul(m2, m2, mp);
-      m8[e] = mont_mul(m4, m4, mp);
+      const u64 m8m = mont_mul(m4, m4, mp);              // Montgomery m^8 = m^8 2^64 mod p
+      m8[e] = from_mont(m8m, mp);                        // normal m^8: the chain's fixed multiplier
+      w8[e] = m8m * mp.pinv;                             // its Shoup constant floor(m^8 2^64 / p)
       u64 x = mp.r1;                                     // Montgomery 1 = m^0
       if (r & 1) x = mm;
       if (r & 2) x = mont_mul(x, m2, mp);
       if (r & 4) x = mont_mul(x, m4, mp);
-      y[e] = x;                                          // m^r
+      y[e] = x;                                          // m^r (Montgomery residue)
     }
 #pragma unroll 1
     for (u32 j = 0; j < (u32)kV / 8; ++j) {              // row r + 8j
@@ -969,8 +976,11 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
       wd[4] = prmt(a, b, 0x5410); wd[5] = prmt(a, b, 0x7632); wd[6] = prmt(c, d, 0x5410); wd[7] = prmt(c, d, 0x7632);
 #pragma unroll
       for (int t = 0; t < 8; ++t) *(u32*)(st + base + (u32)t * kPlaneB + j * 128u) = wd[t];
+      if (j + 1 < (u32)kV / 8) {                         // row r + 8(j+1) = row r + 8j times m^8
 #pragma unroll
-      for (int e = 0; e < 4; ++e) y[e] = mont_mul(y[e], m8[e], mp);
+        for (int e = 0; e < 4; ++e)
+          y[e] = LAZY ? mul_shoup4(y[e], m8[e], w8[e], mp.np) : mul_shoup2(y[e], m8[e], w8[e], mp.np);
+      }
     }
     __syncthreads();
     uint4* dst = (uint4*)(Rp + blk * 2 * kRBytes);

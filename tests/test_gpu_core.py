@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import paper_2004_11571_b200 as pe
+import synth
 
 pytestmark = pytest.mark.gpu
 
@@ -133,3 +134,17 @@ def test_seed_pow():
         out = pe.test_core(pe.CORE_POW, p, c, m, e)
         want = [(int(x) * pow(int(y), int(z), p)) % p for x, y, z in zip(c, m, e)]
         assert out.tolist() == want, p
+
+
+def test_shoup_constant_fast_form():
+    """shoup_w_fast (w = (m 2^64 mod p) * (-p^-1) mod 2^64, used by k_setup and k_tc_setup) equals
+    the bit-loop division floor(m 2^64 / p) on every residue of small primes and on random and edge
+    residues of 20- to 63-bit primes."""
+    rng = np.random.default_rng(77)
+    for p in (3, 5, 7, 13, 251, 509):
+        b = np.arange(p, dtype=np.uint64)
+        assert not np.any(pe.test_core(pe.CORE_SHOUPW, p, b, b))
+    for p in (1_000_003, (1 << 31) - 1, (1 << 50) - 27, (1 << 62) - 57, (1 << 62) + 135, (1 << 63) - 25):
+        b = np.concatenate([synth.uniform_mod(rng, 0, p, 20000),
+                            np.array([0, 1, 2, p - 2, p - 1, p // 2, p // 2 + 1], np.uint64)])
+        assert not np.any(pe.test_core(pe.CORE_SHOUPW, p, b, b)), p

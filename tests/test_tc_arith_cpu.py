@@ -89,3 +89,16 @@ def test_round_split_and_epilogue_reduction(seed):
         hi, lo = acc >> 64, acc & ((1 << 64) - 1)
         parts.append(redc(hi % p, lo, p))                  # = X_g 2^-64 mod p
     assert (parts[0] + parts[1]) % p == want
+
+
+def test_shoup_constant_identity():
+    """The identity behind shoup_w_fast (csrc/modcore.cuh): for m < p, floor(m 2^64 / p) equals
+    (m 2^64 mod p) * (-p^-1 mod 2^64) mod 2^64 (m 2^64 = w p + rem, so w p == -rem mod 2^64, and
+    0 <= w < 2^64 makes the congruence an equality).  Python integers, no kernel code."""
+    import random
+    rnd = random.Random(5)
+    for p in (3, 13, 509, 1_000_003, (1 << 31) - 1, (1 << 62) - 57, (1 << 63) - 25):
+        ninv = (-pow(p, -1, 1 << 64)) % (1 << 64)
+        for m in [0, 1, p - 1] + [rnd.randrange(p) for _ in range(200)]:
+            rem = (m << 64) % p
+            assert (rem * ninv) % (1 << 64) == (m << 64) // p
