@@ -462,27 +462,6 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
   const u64 n_wt = h->t_pad / tile;
   if (n_wt >= 0x7fffffffull) return set_err(PE_ERANGE);
   h->n_wt = (u32)n_wt;
-  const int W = h->W;
-  std::vector<uint2> wt_info(n_wt);
-  std::vector<u32> wt_bucket(n_wt), slot_start(G + 1);
-  for (u64 g = 0; g < G; ++g)
-    for (u64 x = poff[g] / tile; x < poff[g + 1] / tile; ++x) wt_bucket[x] = (u32)g;
-  u32 slot = 0;
-  for (u64 x = 0; x < n_wt; ++x) {
-    bool start = (x % W == 0) || wt_bucket[x] != wt_bucket[x - 1];
-    if (start) {
-      if (x == 0 || wt_bucket[x] != wt_bucket[x - 1]) slot_start[wt_bucket[x]] = slot;
-      u32 len = 1;
-      while ((x + len) % W != 0 && x + len < n_wt && wt_bucket[x + len] == wt_bucket[x]) ++len;
-      wt_info[x] = make_uint2(slot, len);
-      ++slot;
-    } else {
-      wt_info[x] = make_uint2(slot - 1, 0);
-    }
-  }
-  slot_start[G] = slot;
-  h->n_slots = slot;
-
   // ---- padded layout + monomials
   u64 *d_poff, *d_bstart;
   if (dalloc(&d_poff, G + 1) || dalloc(&d_bstart, G + 1)) return g_last_error;
@@ -496,8 +475,6 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
   k_setup<<<grid_for(h->t_pad, 256), 256, 0, s>>>(d_coeffs, d_m_in, d_idxS, d_poff, d_bstart, (u32)G, h->t_pad,
                                                    h->d_c, h->d_m, h->d_w, h->d_perm, h->mp);
   CU(cudaGetLastError());
-  CU(cudaMemcpyAsync(h->d_wt_info, wt_info.data(), n_wt * sizeof(uint2), cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(h->d_slot_start, slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
 
   // ---- tensor-core path (tc.cuh): per-term strides + the piece plan
   if (h->tc_mode != 0 && (h->path == kInt4 || h->path == kInt2 || h->path == kFp64 || h->path == kInt32)) {
@@ -519,10 +496,11 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
         if (*q) { cudaFreeAsync(*q, s); *q = nullptr; }
       cudaGetLastError();               // allocation failures are not sticky; clear the record
       g_last_error = PE_OK;
-      h->tc_mode = 0;
-      CU(cudaStreamSynchronize(s));
-      return PE_OK;
+      h->tc_mode = 0;                   // the rest of the tensor-path setup is skipped below
     }
+  }
+  if (h->tc_mode != 0 && (h->path == kInt4 || h->path == kInt2 || h->path == kFp64 || h->path == kInt32)) {
+    const u64 tp = h->t_pad;
     prof.mark("k_setup (+copies)", s);
     // the C records (k_tc_setup) and the baby-step planes (k_tc_rplanes) both depend only on m:
     // the former runs on a side stream beside the latter
@@ -558,6 +536,31 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
     *h->h_status = 0;
     h->tc_ok = true;
   }
+  // ---- k_step's warp-tile plan (host), computed while the setup kernels above run
+  const int W = h->W;
+  std::vector<uint2> wt_info(n_wt);
+  std::vector<u32> wt_bucket(n_wt), slot_start(G + 1);
+  for (u64 g = 0; g < G; ++g)
+    for (u64 x = poff[g] / tile; x < poff[g + 1] / tile; ++x) wt_bucket[x] = (u32)g;
+  u32 slot = 0;
+  for (u64 x = 0; x < n_wt; ++x) {
+    bool start = (x % W == 0) || wt_bucket[x] != wt_bucket[x - 1];
+    if (start) {
+      if (x == 0 || wt_bucket[x] != wt_bucket[x - 1]) slot_start[wt_bucket[x]] = slot;
+      u32 len = 1;
+      while ((x + len) % W != 0 && x + len < n_wt && wt_bucket[x + len] == wt_bucket[x]) ++len;
+      wt_info[x] = make_uint2(slot, len);
+      ++slot;
+    } else {
+      wt_info[x] = make_uint2(slot - 1, 0);
+    }
+  }
+  slot_start[G] = slot;
+  h->n_slots = slot;
+
+  CU(cudaMemcpyAsync(h->d_wt_info, wt_info.data(), n_wt * sizeof(uint2), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(h->d_slot_start, slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
+
   if (h->fast_mode == 2) {
     const int rc = fast::create(h->h_poff, h->mp, s, &h->fast);
     if (rc != PE_OK) return set_err(rc);

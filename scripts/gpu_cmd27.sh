@@ -1,0 +1,5 @@
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/r27_smoke.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/r27_tests.log 2>&1
+echo "rc=$?" >> gpurun_out/r27_tests.log
+PE_CREATE_PROF=1 timeout 300 python scripts/e2e_breakdown.py > gpurun_out/r27_e2e.txt 2>&1
+echo done
