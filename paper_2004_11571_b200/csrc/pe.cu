@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <map>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -139,8 +140,11 @@ struct pe_ctx {
     uint4* d_piece = nullptr;
     u32* d_slot_start = nullptr;
     u32* d_sched = nullptr;
+    cudaEvent_t uploaded = nullptr;  // the device copies are complete (any stream may wait on it)
   };
-  mutable std::map<u32, TcPlan> tc_plans;   // lazily built cache (also from const queries)
+  u64 split_g1 = 0;                  // pe_eval's row split for the tensor path (0: no split)
+  // lazily built cache (also from const queries), keyed by (chunks per pass, first row, end row)
+  mutable std::map<std::tuple<u32, u64, u64>, TcPlan> tc_plans;
   // asymptotically fast method (fast.cu, NEXT-4): 0 off, 1 automatic (T >= fast_min_T), 2 forced
   int fast_mode = 0;
   u64 fast_min_T = 0;
@@ -169,9 +173,11 @@ static void free_all(pe_ctx* h) {
                   (void*)h->d_out_scratch, (void*)h->d_tcC, (void*)h->d_tcR, (void*)h->d_tcMS,
                   (void*)h->d_tc_scratch, (void*)h->d_seed})
     if (q) cudaFreeAsync(q, s);
-  for (auto& kv : h->tc_plans)
+  for (auto& kv : h->tc_plans) {
     for (void* q : {(void*)kv.second.d_piece, (void*)kv.second.d_slot_start, (void*)kv.second.d_sched})
       if (q) cudaFreeAsync(q, s);
+    if (kv.second.uploaded) cudaEventDestroy(kv.second.uploaded);
+  }
   h->tc_plans.clear();
   if (s) cudaStreamSynchronize(s);
   if (h->copy_stream) cudaStreamSynchronize(h->copy_stream), cudaStreamDestroy(h->copy_stream);
@@ -258,6 +264,27 @@ static unsigned grid_for(u64 n, unsigned block) {
 }
 
 // ---------------------------------------------------------------- create
+static int tc_plan(const pe_ctx* h, u32 nch, u64 g0, u64 g1, bool upload, cudaStream_t s, pe_ctx::TcPlan** out);
+
+// pe_eval's row split for the tensor path: rows [0, G1) then [G1, G), the first block's device->host
+// copy overlapping the second's evaluation.  G1 minimises E1 + max(E2, D1) + D2 under a simple model
+// -- evaluation ~ padded terms x T at ~2e13 term-points/s, copy ~ rows x T x 8 B at ~50 GB/s (PCIe 5)
+// -- in which T cancels, so the split is a property of the handle (config 5: ~22 % of the terms in
+// the second block, whose copy, the exposed tail, is ~1/4 of the result).  0 = no split.
+static u64 tc_row_split(const pe_ctx* h) {
+  if (h->G < 2) return 0;
+  const double ce = 1.0 / 2e13, cd = 8.0 / 5e10, tp = (double)h->t_pad;
+  double best = tp * ce + (double)h->G * cd;   // no split
+  u64 G1 = 0;
+  for (u64 g = 1; g < h->G; ++g) {
+    const double e1 = (double)h->h_poff[g] * ce, e2 = (tp - (double)h->h_poff[g]) * ce;
+    const double d1 = (double)g * cd, d2 = (double)(h->G - g) * cd;
+    const double tot = e1 + std::max(e2, d1) + d2;
+    if (tot < best) { best = tot; G1 = g; }
+  }
+  return G1;
+}
+
 // Development: env PE_CREATE_PROF=1 prints the device time between pe_create's phases (CUDA events on
 // the handle stream; host waits show up as gaps).
 struct CreateProf {
@@ -561,6 +588,18 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
   CU(cudaMemcpyAsync(h->d_wt_info, wt_info.data(), n_wt * sizeof(uint2), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(h->d_slot_start, slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
 
+  // k_tc plans of the common evaluation shapes (1 or 2 chunks per pass; all rows, and pe_eval's two
+  // row blocks), built on the host while the setup kernels run and uploaded behind them
+  if (h->tc_ok) {
+    h->split_g1 = tc_row_split(h);
+    const u64 ranges[3][2] = {{0, h->G}, {0, h->split_g1}, {h->split_g1, h->G}};
+    for (u32 nch = 1; nch <= 2; ++nch)
+      for (auto& r : ranges) {
+        if (r[0] >= r[1]) continue;
+        pe_ctx::TcPlan* P = nullptr;
+        if (tc_plan(h, nch, r[0], r[1], true, s, &P)) return g_last_error;
+      }
+  }
   if (h->fast_mode == 2) {
     const int rc = fast::create(h->h_poff, h->mp, s, &h->fast);
     if (rc != PE_OK) return set_err(rc);
@@ -730,28 +769,44 @@ static int ensure_partial(pe_ctx* h, size_t need, cudaStream_t s) {
 // load level of neighbouring CTAs and run side by side (one DRAM read of the planes, L2 for the
 // rest -- the round-1 snake order's property).  env PE_TC_PIECE (terms) / PE_TC_UPC override.
 static const u32 kUnitsPerCta = 6;
-static int tc_plan(const pe_ctx* h, u32 nch, bool upload, cudaStream_t s, pe_ctx::TcPlan** out) {
-  auto it = h->tc_plans.find(nch);
+// Largest piece (K-blocks) of a plan for rows [g0, g1) and nch chunks.
+static u64 tc_maxkb(const pe_ctx* h, u32 nch, u64 g0, u64 g1) {
+  const u64 tkb = (h->h_poff[g1] - h->h_poff[g0]) / tc::kKB;
+  const u32 rounds = h->tc_rounds;
+  u64 maxkb;
+  const int pm_env = env_int("PE_TC_PIECE", 0), upc = env_int("PE_TC_UPC", (int)kUnitsPerCta);
+  if (pm_env > 0) {
+    maxkb = std::max<u64>(1, (u64)pm_env / tc::kKB);
+  } else if (upc <= 0) {   // round-1 rule: pieces of up to twice the per-SM share
+    maxkb = 2 * ((h->t_pad + h->n_sm - 1) / h->n_sm) / tc::kKB;
+    maxkb = std::max<u64>(maxkb, 1024 / tc::kKB);
+  } else {
+    maxkb = (tkb * nch * rounds + (u64)h->n_sm * upc - 1) / ((u64)h->n_sm * upc);
+    maxkb = std::max<u64>(maxkb, 1024 / tc::kKB);
+  }
+  return std::min<u64>(maxkb, tc::kPieceMax / tc::kKB);
+}
+// Partial rows (pieces x rounds) of that plan, without building it (O(rows)).
+static u64 tc_nslots(const pe_ctx* h, u32 nch, u64 g0, u64 g1) {
+  const u64 maxkb = tc_maxkb(h, nch, g0, g1);
+  u64 n = 0;
+  for (u64 g = g0; g < g1; ++g) n += ((h->h_poff[g + 1] - h->h_poff[g]) / tc::kKB + maxkb - 1) / maxkb;
+  return n * h->tc_rounds;
+}
+// Rows [g0, g1) only (pe_eval's row blocks): pieces of those buckets, slots numbered from 0.
+static int tc_plan(const pe_ctx* h, u32 nch, u64 g0, u64 g1, bool upload, cudaStream_t s, pe_ctx::TcPlan** out) {
+  const auto key = std::make_tuple(nch, g0, g1);
+  auto it = h->tc_plans.find(key);
   pe_ctx::TcPlan* P = nullptr;
   if (it == h->tc_plans.end()) {
-    P = &h->tc_plans[nch];
-    const u64 G = h->G, tkb = h->t_pad / tc::kKB;
+    P = &h->tc_plans[key];
+    const u64 G = g1 - g0;
     const u32 rounds = h->tc_rounds;
-    u64 maxkb;
-    const int pm_env = env_int("PE_TC_PIECE", 0), upc = env_int("PE_TC_UPC", (int)kUnitsPerCta);
-    if (pm_env > 0) {
-      maxkb = std::max<u64>(1, (u64)pm_env / tc::kKB);
-    } else if (upc <= 0) {   // round-1 rule: pieces of up to twice the per-SM share
-      maxkb = 2 * ((h->t_pad + h->n_sm - 1) / h->n_sm) / tc::kKB;
-      maxkb = std::max<u64>(maxkb, 1024 / tc::kKB);
-    } else {
-      maxkb = (tkb * nch * rounds + (u64)h->n_sm * upc - 1) / ((u64)h->n_sm * upc);
-      maxkb = std::max<u64>(maxkb, 1024 / tc::kKB);
-    }
-    maxkb = std::min<u64>(maxkb, tc::kPieceMax / tc::kKB);
+    const u64 maxkb = tc_maxkb(h, nch, g0, g1);
     std::vector<u32> slot(G + 1);
-    for (u64 g = 0; g < G; ++g) {
-      slot[g] = (u32)P->pieces.size();
+    for (u64 gg = 0; gg < G; ++gg) {
+      const u64 g = g0 + gg;
+      slot[gg] = (u32)P->pieces.size();
       const u64 nkb = (h->h_poff[g + 1] - h->h_poff[g]) / tc::kKB;   // poff multiples of 32R
       const u64 np_g = (nkb + maxkb - 1) / maxkb;
       u64 kb0 = 0;
@@ -791,7 +846,10 @@ static int tc_plan(const pe_ctx* h, u32 nch, bool upload, cudaStream_t s, pe_ctx
       sload[b] += (u64)P->pieces[u / upp].y + 4;
     }
     std::vector<std::pair<u64, u32>> took;
-    for (u32 pc = 0; pc < P->npieces; ++pc) {   // pieces are size-sorted: LPT order
+    const int sch = env_int("PE_TC_SCHED", -1);   // testing: 0 snake, 1 LPT
+    // with >= 16 units per CTA the snake order is already within a few % of the mean: skip LPT
+    const bool try_lpt = sch == 1 || (sch < 0 && nunits < 16ull * grid);
+    for (u32 pc = 0; try_lpt && pc < P->npieces; ++pc) {   // pieces are size-sorted: LPT order
       const u64 cost = (u64)P->pieces[pc].y + 4;
       took.clear();
       for (u32 k = 0; k < upp; ++k) {
@@ -811,8 +869,7 @@ static int tc_plan(const pe_ctx* h, u32 nch, bool upload, cudaStream_t s, pe_ctx
     u64 lpt_max = 0, snake_max = 0;
     for (auto& x : heap) lpt_max = std::max(lpt_max, x.first);
     for (u64 x : sload) snake_max = std::max(snake_max, x);
-    const int sch = env_int("PE_TC_SCHED", -1);   // testing: 0 snake, 1 LPT
-    if (sch == 0 || (sch < 0 && !(lpt_max * 100 < snake_max * 97))) lists.swap(snake);
+    if (!try_lpt || sch == 0 || (sch < 0 && !(lpt_max * 100 < snake_max * 97))) lists.swap(snake);
     P->sched.assign(nunits + grid + 1, 0);
     u32 o = 0;
     for (u32 b = 0; b < grid; ++b) {
@@ -831,7 +888,10 @@ static int tc_plan(const pe_ctx* h, u32 nch, bool upload, cudaStream_t s, pe_ctx
     CU(cudaMemcpyAsync(P->d_slot_start, P->slot_start.data(), P->slot_start.size() * sizeof(u32),
                        cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(P->d_sched, P->sched.data(), P->sched.size() * sizeof(u32), cudaMemcpyHostToDevice, s));
-    CU(cudaStreamSynchronize(s));   // once per (handle, chunk count): later calls may use another stream
+    // (pageable sources: each copy has left the host vector when it returns; the plan's host
+    // vectors also live on in the cache.)  Later launches on any stream wait on this event.
+    CU(cudaEventCreateWithFlags(&P->uploaded, cudaEventDisableTiming));
+    CU(cudaEventRecord(P->uploaded, s));
   }
   *out = P;
   return PE_OK;
@@ -839,12 +899,14 @@ static int tc_plan(const pe_ctx* h, u32 nch, bool upload, cudaStream_t s, pe_ctx
 
 // Tensor-core evaluation (tc.cuh): per pass, chunk seeds -> k_tc (persistent, one CTA per SM)
 // -> k_fixup over the pieces' partial rows.
-static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s) {
+// Rows [g0, g1) of the output (default: all): out row g is d_out + g * ld.
+static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s, u64 g0 = 0, u64 g1 = ~0ull) {
+  if (g1 > h->G) g1 = h->G;
+  if (g0 >= g1) return PE_OK;
+  const u64 q0 = h->h_poff[g0], q1 = h->h_poff[g1];   // the rows' padded terms
   // pass length from the one-chunk plan: it has the most pieces (plans with more chunks per pass
   // use larger pieces), so its slot count bounds every pass's partial rows
-  pe_ctx::TcPlan* P1 = nullptr;
-  if (tc_plan(h, 1, false, s, &P1)) return g_last_error;
-  const u64 nslots = P1->nslots;
+  const u64 nslots = tc_nslots(h, 1, g0, g1);
   u64 Tp = h->partial_cap_bytes / 8 / std::max<u64>(nslots, 1) / tc::kChunk * tc::kChunk;
   Tp = std::max<u64>(Tp, tc::kChunk);
   Tp = std::min<u64>(Tp, (T + tc::kChunk - 1) / tc::kChunk * tc::kChunk);
@@ -876,12 +938,13 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
     const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
-    const u64 nseed = (u64)h->t_pad * ((nch + tc::kSeedChunks - 1) / tc::kSeedChunks);
-    tc::k_tc_seed<<<grid_for(nseed, 256), 256, 0, s>>>(h->d_c, h->d_m, h->d_tcMS, h->t_pad, nch, j0 + k0, h->d_seed,
-                                                       h->mp);
+    const u64 nseed = (q1 - q0) * ((nch + tc::kSeedChunks - 1) / tc::kSeedChunks);
+    tc::k_tc_seed<<<grid_for(nseed, 256), 256, 0, s>>>(h->d_c, h->d_m, h->d_tcMS, h->t_pad, q0, q1, nch, j0 + k0,
+                                                       h->d_seed, h->mp);
     CU(cudaGetLastError());
     pe_ctx::TcPlan* P = nullptr;
-    if (tc_plan(h, nch, true, s, &P)) return g_last_error;
+    if (tc_plan(h, nch, g0, g1, true, s, &P)) return g_last_error;
+    CU(cudaStreamWaitEvent(s, P->uploaded, 0));
     tc::TcArgs a;
     a.LS = h->d_seed;
     a.C = h->d_tcC;
@@ -958,8 +1021,8 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s)
     }
     if (h->timing) CU(cudaEventRecord(rec.e1, s));
     const u32 nkb = (np + 255) / 256;
-    k_fixup<<<(unsigned)(h->G * nkb), 256, 0, s>>>(h->d_partial, a.ldp, P->d_slot_start, (u32)h->G, np, nkb,
-                                                   d_out + k0, ld, h->mp);
+    k_fixup<<<(unsigned)((g1 - g0) * nkb), 256, 0, s>>>(h->d_partial, a.ldp, P->d_slot_start, (u32)(g1 - g0), np,
+                                                        nkb, d_out + g0 * ld + k0, ld, h->mp);
     CU(cudaGetLastError());
     if (h->timing) {
       CU(cudaEventRecord(rec.e2, s));
@@ -978,9 +1041,7 @@ static bool use_tc(const pe_ctx* h, u64 T) {
   if (h->tc_mode == 2) return true;
   if (h->tc_mode != 1 || T < tc_min_T(h->t_pad, h->p)) return false;
   const u64 row = (std::min<u64>(T, tc::kChunk) + 7) / 8 * 8;
-  pe_ctx::TcPlan* P1 = nullptr;
-  if (tc_plan(h, 1, false, nullptr, &P1)) return false;   // host-only: no CUDA call
-  return (u64)P1->nslots * row * sizeof(u64) <= h->partial_cap_bytes;
+  return tc_nslots(h, 1, 0, h->G) * row * sizeof(u64) <= h->partial_cap_bytes;
 }
 
 // automatic fast-method threshold: the measured crossover against k_tc (fast method)
@@ -1130,30 +1191,37 @@ extern "C" int pe_eval(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* out) {
       rc = set_err(PE_ENOMEM);
     else h->out_scratch_elems = need;
   }
-  // Long ranges on the tensor-core path: two column blocks of whole chunks, the first block's
-  // device->host copy (pitched: rows of the [G][T] result) overlapping the second's evaluation.
-  const u64 half = (T / 2 + tc::kChunk - 1) / tc::kChunk * tc::kChunk;
-  const bool split = rc == PE_OK && choose_kernel(h, T) == kKTc && T >= 2 * (u64)tc::kChunk && half < T &&
-                     choose_kernel(h, T - half) == kKTc;
-  if (split) {
+  // Tensor-core path: two ROW blocks [0, G1) and [G1, G) over all T points (tc_row_split) -- each
+  // launch keeps whole chunks -- with the first block's device->host copy (contiguous rows)
+  // overlapping the second's evaluation.
+  const u64 G1 = rc == PE_OK && choose_kernel(h, T) == kKTc ? h->split_g1 : 0;
+  bool done = false;
+  if (G1) {
     if (!h->copy_stream && cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
       rc = set_err(PE_ECUDA);
     if (rc == PE_OK && !h->copy_done && cudaEventCreateWithFlags(&h->copy_done, cudaEventDisableTiming) != cudaSuccess)
       rc = set_err(PE_ECUDA);
-    const u64 blk[2][2] = {{0, half}, {half, T - half}};
-    for (int b = 0; b < 2 && rc == PE_OK; ++b) {
-      rc = eval_device_impl(h, j0 + blk[b][0], blk[b][1], h->d_out_scratch + blk[b][0], T, h->stream);
+    const u64 blk[2][2] = {{0, G1}, {G1, h->G}};
+    int b = 0;
+    for (; b < 2 && rc == PE_OK; ++b) {
+      rc = eval_tc(h, j0, T, h->d_out_scratch, T, h->stream, blk[b][0], blk[b][1]);
       if (rc != PE_OK) break;
       if (cudaEventRecord(h->copy_done, h->stream) != cudaSuccess ||
           cudaStreamWaitEvent(h->copy_stream, h->copy_done, 0) != cudaSuccess ||
-          cudaMemcpy2DAsync(out + blk[b][0], T * sizeof(u64), h->d_out_scratch + blk[b][0], T * sizeof(u64),
-                            blk[b][1] * sizeof(u64), h->G, cudaMemcpyDeviceToHost, h->copy_stream) != cudaSuccess)
+          cudaMemcpyAsync(out + blk[b][0] * T, h->d_out_scratch + blk[b][0] * T, (blk[b][1] - blk[b][0]) * T * sizeof(u64),
+                          cudaMemcpyDeviceToHost, h->copy_stream) != cudaSuccess)
         rc = set_err(PE_ECUDA);
     }
     if (cudaStreamSynchronize(h->copy_stream) != cudaSuccess || cudaStreamSynchronize(h->stream) != cudaSuccess)
       if (rc == PE_OK) rc = set_err(PE_ECUDA);
-  } else {
-    if (rc == PE_OK) rc = eval_device_impl(h, j0, T, h->d_out_scratch, T, h->stream);
+    done = rc == PE_OK;
+    if (rc == PE_ENOMEM && b == 0 && h->tc_mode != 2) {   // automatic handle short of memory: whole path
+      cudaGetLastError();
+      rc = g_last_error = PE_OK;
+    }
+  }
+  if (!done && rc == PE_OK) {
+    rc = eval_device_impl(h, j0, T, h->d_out_scratch, T, h->stream);
     if (rc == PE_OK) {
       if (cudaMemcpyAsync(out, h->d_out_scratch, need * sizeof(u64), cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
           cudaStreamSynchronize(h->stream) != cudaSuccess)
@@ -1190,8 +1258,7 @@ extern "C" int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint
   if (!h) return set_err(PE_EINVAL);
   if (mode) *mode = h->tc_ok ? h->tc_mode : 0;
   if (pieces) {
-    pe_ctx::TcPlan* P1 = nullptr;
-    *pieces = h->tc_ok && tc_plan(h, 1, false, nullptr, &P1) == PE_OK ? P1->npieces : 0;
+    *pieces = h->tc_ok ? tc_nslots(h, 1, 0, h->G) / h->tc_rounds : 0;
   }
   if (min_T) *min_T = h->tc_ok ? (h->tc_mode == 2 ? 1 : tc_min_T(h->t_pad, h->p)) : 0;
   return PE_OK;

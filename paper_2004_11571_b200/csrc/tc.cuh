@@ -993,12 +993,13 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
 // Per evaluation pass: the chunk seeds LS[c][q] = c_q m_q^{js0 + c*kChunk}.  Thread = (term,
 // kSeedChunks consecutive chunks): one exponentiation, then products with m^{kChunk}.
 constexpr u32 kSeedChunks = 4;
+// Terms [q0, q1) only (a row block of pe_eval); LS keeps its [nch][t_pad] layout.
 static __global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, const u64* __restrict__ MS,
-                                 u64 t_pad, u32 nch, u64 js0, u64* __restrict__ LS, ModParams mp) {
+                                 u64 t_pad, u64 q0, u64 q1, u32 nch, u64 js0, u64* __restrict__ LS, ModParams mp) {
   const u32 ngrp = (nch + kSeedChunks - 1) / kSeedChunks;
-  const u64 total = t_pad * ngrp;
+  const u64 nq = q1 - q0, total = nq * ngrp;
   for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
-    const u64 grp = x / t_pad, q = x - grp * t_pad;
+    const u64 grp = x / nq, q = q0 + (x - grp * nq);
     const u32 ch0 = (u32)grp * kSeedChunks, ch1 = min(nch, ch0 + kSeedChunks);
     const u64 mC = MS[2 * q + 1];                        // Montgomery m^{kChunk}
     u64 s = seed_pow(c[q], m[q], js0 + (u64)ch0 * kChunk, mp);   // normal form, < p

@@ -1,0 +1,6 @@
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/r28_smoke.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/r28_tests.log 2>&1
+echo "rc=$?" >> gpurun_out/r28_tests.log
+PE_CREATE_PROF=1 timeout 300 python scripts/e2e_breakdown.py > gpurun_out/r28_e2e.txt 2>&1
+timeout 600 python bench.py --no-cpu > gpurun_out/r28_bench.json 2> gpurun_out/r28_bench.err
+echo done

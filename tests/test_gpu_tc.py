@@ -182,9 +182,9 @@ def test_mma_probe_rate():
 
 @pytest.mark.parametrize("T", [16385, 2 * 8192, 3 * 8192 + 5])
 def test_tc_host_eval_column_blocks(T):
-    """pe_eval on the tensor path splits long ranges into two column blocks of whole chunks and
-    overlaps the first block's pitched device->host copy with the second's evaluation: the
-    result equals pe_eval_device's (single pass) and the oracle's incremental evaluation."""
+    """pe_eval on the tensor path evaluates two row blocks (launches over a subset of the buckets)
+    and overlaps the first block's device->host copy with the second's evaluation: the result
+    equals pe_eval_device's (one launch over all rows) and the oracle's incremental evaluation."""
     import torch
     w = synth.random_small(540 + T % 97, P62, 6, 900, 4, T, 11)
     with pe.Context.from_workload(w, path=pe.PATH_TC) as ctx:
