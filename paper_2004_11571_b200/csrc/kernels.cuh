@@ -381,6 +381,37 @@ static __global__ void k_fixup(const u64* __restrict__ partial, u64 ldp, const u
   out[(u64)g * ld + k] = reduce128(hi, lo, mp);
 }
 
+// The same for rows with many slots (k_tc pieces of a large bucket; one term shard of config 5 is a
+// single 300-slot row): a 256-thread block covers (g, 32 points), warp w sums slots w, w + 8, ... with
+// coalesced 256-byte loads, and the 8 partial 128-bit sums meet in shared memory.
+static __global__ void __launch_bounds__(256) k_fixup_wide(const u64* __restrict__ partial, u64 ldp,
+                                                           const u32* __restrict__ slot_start, u32 G, u32 npts,
+                                                           u32 nkb, u64* __restrict__ out, u64 ld, ModParams mp) {
+  __shared__ u64 slo[8][32], shi[8][32];
+  const u32 g = blockIdx.x / nkb;
+  const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const u32 k = (blockIdx.x % nkb) * 32 + lane;
+  u64 lo = 0, hi = 0;
+  if (g < G && k < npts) {
+    for (u32 s = slot_start[g] + warp; s < slot_start[g + 1]; s += 8) {
+      const u64 v = partial[(u64)s * ldp + k];
+      lo += v;
+      hi += (lo < v);
+    }
+  }
+  slo[warp][lane] = lo;
+  shi[warp][lane] = hi;
+  __syncthreads();
+  if (warp == 0 && g < G && k < npts) {
+    for (int w = 1; w < 8; ++w) {
+      const u64 v = slo[w][lane];
+      lo += v;
+      hi += shi[w][lane] + (lo < v);
+    }
+    out[(u64)g * ld + k] = reduce128(hi, lo, mp);
+  }
+}
+
 // Multi-GPU assembly (pe_rows_addmod): dst[r][k] = (dst[r][k] + src[r][k]) mod p for canonical
 // residues (< p < 2^63, so the u64 sum cannot wrap) -- the root's sum of a bucket split between
 // two term ranges, i.e. the coefficient reduction of PAPER.md:489-503 across ranks.

@@ -133,7 +133,7 @@ struct pe_ctx {
   u32* h_status = nullptr;       // mapped host word: k_tc sets it when a pipeline wait times out
   // k_tc piece plans, one per chunk count of a pass (tc_plan): pieces, partial slots, unit schedule
   struct TcPlan {
-    u32 npieces = 0, nslots = 0, grid = 0;
+    u32 npieces = 0, nslots = 0, grid = 0, max_slots = 0;   // max_slots: most partial rows of one bucket
     std::vector<uint4> pieces;       // x = first padded term, y = K-blocks, z = slot (size-sorted)
     std::vector<u32> slot_start;     // [G+1] partial slots of bucket g (x rounds)
     std::vector<u32> sched;          // [nunits] units per CTA, then [grid + 1] offsets
@@ -822,6 +822,7 @@ static int tc_plan(const pe_ctx* h, u32 nch, u64 g0, u64 g1, bool upload, cudaSt
     P->npieces = (u32)P->pieces.size();
     P->nslots = P->npieces * rounds;
     for (auto& x : slot) x *= rounds;
+    for (u64 gg = 0; gg < G; ++gg) P->max_slots = std::max(P->max_slots, slot[gg + 1] - slot[gg]);
     P->slot_start = std::move(slot);
     // schedule
     const u32 upp = nch * rounds, nunits = P->npieces * upp;
@@ -1021,8 +1022,16 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s,
     }
     if (h->timing) CU(cudaEventRecord(rec.e1, s));
     const u32 nkb = (np + 255) / 256;
-    k_fixup<<<(unsigned)((g1 - g0) * nkb), 256, 0, s>>>(h->d_partial, a.ldp, P->d_slot_start, (u32)(g1 - g0), np,
-                                                        nkb, d_out + g0 * ld + k0, ld, h->mp);
+    // few rows of many pieces (a term shard holding one huge bucket): the thread-per-point kernel
+    // would leave most SMs idle, so split each row's slots over 8 warps instead
+    if (P->max_slots >= 16 && (g1 - g0) * nkb < 8ull * h->n_sm) {
+      const u32 nkw = (np + 31) / 32;
+      k_fixup_wide<<<(unsigned)((g1 - g0) * nkw), 256, 0, s>>>(h->d_partial, a.ldp, P->d_slot_start, (u32)(g1 - g0),
+                                                               np, nkw, d_out + g0 * ld + k0, ld, h->mp);
+    } else {
+      k_fixup<<<(unsigned)((g1 - g0) * nkb), 256, 0, s>>>(h->d_partial, a.ldp, P->d_slot_start, (u32)(g1 - g0), np,
+                                                          nkb, d_out + g0 * ld + k0, ld, h->mp);
+    }
     CU(cudaGetLastError());
     if (h->timing) {
       CU(cudaEventRecord(rec.e2, s));
