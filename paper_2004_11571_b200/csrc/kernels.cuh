@@ -125,7 +125,12 @@ static __global__ void k_keys(const E* __restrict__ exps, u64 a, u64 b, u32 n, u
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     my = max(my, __shfl_xor_sync(0xffffffffu, my, o));
   }
-  if ((threadIdx.x & 31) == 0) { atomicMax(kmax, mx); atomicMax(kmax + 1, my); }
+  __shared__ u32 bx, by;            // one atomic per block, not per warp (they all hit one address)
+  if (threadIdx.x == 0) { bx = 0; by = 0; }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) { atomicMax(&bx, mx); atomicMax(&by, my); }
+  __syncthreads();
+  if (threadIdx.x == 0) { atomicMax(kmax, bx); atomicMax(kmax + 1, by); }
 }
 // Keys (dx << 32 | dy) -> (dx << bd | dy) with dy < 2^bd: the same order in bx + bd bits, so the
 // radix sort runs ceil((bx + bd) / 8) passes instead of 8 (config 5: 2).

@@ -131,13 +131,30 @@ def bucket_keys(exps) -> np.ndarray:
     return (e[:, 0].astype(np.uint64) << np.uint64(32)) | e[:, 1].astype(np.uint64)
 
 
-def term_partition(exps, world: int):
+# Per-bucket cost of a shard in term-equivalents beyond its terms: tile padding (~half a 256-term
+# tile), its pieces' epilogues and its fix-up row (scripts/partition_probe.py: shards of many small
+# buckets ran ~8 % slower than equal-term shards of one large bucket).
+BUCKET_COST_TERMS = 384
+
+
+def term_partition(exps, world: int, bucket_cost: int = BUCKET_COST_TERMS):
     """Stable descending sort of the terms by (dx, dy) and the rank boundaries.
-    Returns (order, bounds): rank r owns terms order[bounds[r]:bounds[r+1]] (~t/world each)."""
+    Returns (order, bounds): rank r owns terms order[bounds[r]:bounds[r+1]], the cut points chosen
+    so that every rank carries about the same cost = terms + bucket_cost per bucket it touches."""
     key = bucket_keys(exps)
     order = np.argsort(~key, kind="stable")                  # descending (dx, dy)
     t = key.size
-    bounds = [(r * t) // world for r in range(world + 1)]
+    if t == 0 or world == 1:
+        return order, [(r * t) // world for r in range(world + 1)]
+    ks = key[order]
+    w = np.ones(t, dtype=np.float64)
+    w[np.r_[True, ks[1:] != ks[:-1]]] += bucket_cost        # charge each bucket at its first term
+    c = np.cumsum(w)
+    targets = c[-1] * np.arange(1, world) / world
+    cuts = np.searchsorted(c, targets, side="left") + 1
+    bounds = [0] + [int(min(max(x, 0), t)) for x in cuts] + [t]
+    for r in range(1, world + 1):                            # keep them ordered
+        bounds[r] = max(bounds[r], bounds[r - 1])
     return order, bounds
 
 
