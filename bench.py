@@ -529,9 +529,11 @@ def main():
         inc_cols = max(1, args.cpu_cols or 64)
         i_tp, i_dt = incremental_sample(w, inc_cols)
         cpu = {"value": n_tp / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+               "extrapolated_full_config_s": w.t * w.T / (n_tp / dt),
                "sample": f"{w.name}: all {w.t} terms x {ncols} random columns of T={w.T} "
                          f"(direct definition, OpenMP over columns), {dt:.1f} s",
                "incremental": {"value": i_tp / i_dt, "unit": UNIT, "cores": cores,
+                               "extrapolated_full_config_s": w.t * w.T / (i_tp / i_dt),
                                "sample": f"Alg. 1 checker (oracle incr_eval, OpenMP over rows): all {w.t} terms x "
                                          f"the first {inc_cols} columns, {i_dt:.1f} s"}}
 
