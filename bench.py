@@ -298,6 +298,9 @@ def main():
     info["G"] = ctx.G
     if term_shard:
         sh = TermShardedEval(bucket_keys(w.exps)[order], bounds, w.T, w.p, dev)
+        # one launch per rank, then the gather: splitting a rank's rows into two launches to hide
+        # the gather under the second (TermShardedEval.run_blocks) costs more than the 0.13 ms it
+        # hides at 8 ranks (scripts/partition_probe.py: 6.36x vs 6.56x predicted)
         info["G"] = sh.G
         local_tp = w_c.size * w.T
         info["uses_tc"] = ctx.uses_tc(w.T)

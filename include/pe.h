@@ -149,6 +149,20 @@ int pe_eval(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* out);
 int pe_eval_device(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* d_out, uint64_t ld,
                    void* stream);
 
+/*
+ * pe_eval_device_rows -- rows [g0, g1) of the result only, into d_out[g*ld + k] for g0 <= g < g1
+ * (the other rows untouched).  Asynchronous on `stream` like pe_eval_device.  A strict sub-range
+ * needs the tensor-core path for this T (pe_eval_kernel == 1), else PE_ENOTSUP; g0 = 0, g1 = G is
+ * plain pe_eval_device.  Used to overlap a row block's transfer with the next block's evaluation.
+ * Errors: PE_EINVAL (h NULL, g0 > g1 or g1 > G, d_out NULL, ld < T), PE_ERANGE, PE_ENOTSUP, PE_ECUDA.
+ */
+int pe_eval_device_rows(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t g0, uint64_t g1, uint64_t* d_out,
+                        uint64_t ld, void* stream);
+/* The handle's row split G1 for such overlap (pe_eval uses rows [0, G1) then [G1, G); chosen so the
+ * second block's evaluation covers the first block's transfer); 0 = no split
+ * (no tensor-core path, or G < 2). */
+uint64_t pe_row_split(const pe_ctx* h);
+
 void pe_destroy(pe_ctx* h); /* NULL-safe; synchronises the handle's device work */
 
 uint64_t pe_num_buckets(const pe_ctx* h);                   /* G (0 if h NULL) */

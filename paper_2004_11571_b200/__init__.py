@@ -30,7 +30,8 @@ EXPORTS = ["pe_create", "pe_create_ex", "pe_eval", "pe_eval_device", "pe_destroy
            "pe_bucket_exps", "pe_info", "pe_monomials", "pe_last_error", "pe_strerror",
            "pe_interp_bound_ok", "pe_set_timing", "pe_kernel_stats",
            "pe_create_batch", "pe_num_polys", "pe_poly_rows", "pe_bm_device", "pe_bm", "pe_tc_info",
-           "pe_rows_addmod", "pe_unshard_columns", "pe_eval_kernel", "pe_create_compact"]
+           "pe_rows_addmod", "pe_unshard_columns", "pe_eval_kernel", "pe_create_compact",
+           "pe_eval_device_rows", "pe_row_split"]
 #: every symbol include/pe_test.h declares (libpe_test.so)
 TEST_EXPORTS = ["pe_test_core", "pe_bench_core", "pe_bench_mma"]
 
@@ -88,6 +89,10 @@ def lib():
         L.pe_kernel_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         L.pe_kernel_stats.restype = ctypes.c_int
+        L.pe_eval_device_rows.argtypes = [vp, u64, u64, u64, u64, vp, u64, vp]
+        L.pe_eval_device_rows.restype = ctypes.c_int
+        L.pe_row_split.argtypes = [vp]
+        L.pe_row_split.restype = u64
         L.pe_create_compact.argtypes = [u64, u64, u32, vp, vp, vp, ctypes.POINTER(Config)]
         L.pe_create_compact.restype = vp
         L.pe_create_batch.argtypes = [u64, u32, vp, u32, vp, vp, vp, ctypes.POINTER(Config)]
@@ -273,6 +278,16 @@ class Context:
         _check(lib().pe_kernel_stats(self._h, ctypes.byref(n), ctypes.byref(s), ctypes.byref(f), ctypes.byref(tp)),
                "pe_kernel_stats")
         return {"step_launches": n.value, "step_ms": s.value, "fixup_ms": f.value, "term_points": tp.value}
+
+    def row_split(self) -> int:
+        """pe_row_split: the row G1 splitting evaluations into two overlappable blocks (0: none)."""
+        return int(lib().pe_row_split(self._h))
+
+    def eval_device_rows(self, j0: int, T: int, g0: int, g1: int, d_out: int, ld: int | None = None,
+                         stream: int = 0):
+        """pe_eval_device_rows: rows [g0, g1) into the [G, ld] device matrix at d_out."""
+        _check(lib().pe_eval_device_rows(self._h, j0, T, g0, g1, ctypes.c_void_p(d_out), T if ld is None else ld,
+                                         ctypes.c_void_p(stream)), "pe_eval_device_rows")
 
     def eval_device(self, j0: int, T: int, d_out: int, ld: int | None = None, stream: int = 0):
         """pe_eval_device into a device pointer (e.g. ``torch_tensor.data_ptr()``)."""

@@ -1181,6 +1181,27 @@ extern "C" int pe_eval_device(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* d_ou
   return rc;
 }
 
+extern "C" int pe_eval_device_rows(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t g0, uint64_t g1, uint64_t* d_out,
+                                   uint64_t ld, void* stream) {
+  g_last_error = PE_OK;
+  if (!h) return set_err(PE_EINVAL);
+  if (g0 == 0 && g1 == h->G) return pe_eval_device(h, j0, T, d_out, ld, stream);
+  if (g0 > g1 || g1 > h->G) return set_err(PE_EINVAL);
+  if (T && j0 + (T - 1) < j0) return set_err(PE_ERANGE);
+  if (T == 0 || g0 == g1) return PE_OK;
+  if (!d_out || ld < T) return set_err(PE_EINVAL);
+  if (choose_kernel(h, T) != kKTc) return set_err(PE_ENOTSUP);   // row ranges: tensor-core path only
+  if (tc_failed(h)) return set_err(PE_ECUDA);
+  int cur = 0;
+  CU(cudaGetDevice(&cur));
+  if (cur != h->device) CU(cudaSetDevice(h->device));
+  const int rc = eval_tc(h, j0, T, d_out, ld, (cudaStream_t)stream, g0, g1);
+  if (cur != h->device) cudaSetDevice(cur);
+  return rc;
+}
+
+extern "C" uint64_t pe_row_split(const pe_ctx* h) { return h && h->tc_ok ? h->split_g1 : 0; }
+
 extern "C" int pe_eval(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* out) {
   g_last_error = PE_OK;
   if (!h) return set_err(PE_EINVAL);

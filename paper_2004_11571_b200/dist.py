@@ -247,6 +247,74 @@ class TermShardedEval:
         self._combine()
         return self.out
 
+    # ---- overlapped form: a rank's rows in two blocks, block 0's transfer under block 1's evaluation
+    def set_splits(self, splits):
+        """Every rank's row split s_r (rows [0, s_r) then [s_r, G_r); 0 = one block), e.g. each
+        rank's pe_row_split gathered with all_gather_object once, outside the timed loop."""
+        assert len(splits) == self.world
+        self.splits = [int(x) for x in splits]
+
+    def _blocks(self, r):
+        g = self.G_r[r]
+        sp = getattr(self, "splits", None)
+        sp = sp[r] if sp else 0
+        if not g:
+            return []
+        return [(0, sp), (sp, g)] if 0 < sp < g else [(0, g)]
+
+    def _slices_in(self, r, a, b):
+        """The parts of rank r's transfer slices (``_slices``) inside its rows [a, b)."""
+        out = []
+        for sl in self._slices(r):
+            lo, hi = max(sl.start, a), min(sl.stop, b)
+            if lo < hi:
+                out.append(slice(lo, hi))
+        return out
+
+    def _dst(self, r, sl):
+        if self.overlap[r] and sl.start == 0:                    # the shared boundary row
+            return self.shared[r:r + 1]
+        o = self.row_off[r]
+        return self.out[o + sl.start:o + sl.stop]
+
+    def run_blocks(self, eval_rows, gather: bool = True):
+        """``run`` with each rank's rows evaluated in (up to) two blocks, ``eval_rows(a, b, local)``
+        filling rows [a, b) of this rank's [G_r, T] output: block 0's rows go out (NCCL P2P, on
+        NCCL's stream) while block 1 is evaluated on the compute stream, so most of the gather hides
+        under the second block.  Matching order per (root, rank) pair: block 0 then block 1."""
+        if self.world == 1 or not gather:
+            if self.G_r[self.rank]:
+                eval_rows(0, self.G_r[self.rank], self.local)
+            return self.out if self.world == 1 else None
+        works = []
+        for bi in range(2):
+            mine = self._blocks(self.rank)
+            if bi < len(mine):
+                eval_rows(mine[bi][0], mine[bi][1], self.local)
+            ops = []
+            if not self.is_root:
+                if bi < len(mine):
+                    for sl in self._slices_in(self.rank, *mine[bi]):
+                        ops.append(dist.P2POp(dist.isend, self.local[sl], self.root, self.group))
+            else:
+                for r in range(self.world):
+                    br = self._blocks(r)
+                    if bi >= len(br):
+                        continue
+                    for sl in self._slices_in(r, *br[bi]):
+                        if r == self.rank:
+                            self._dst(r, sl).copy_(self.local[sl])    # root's own rows (device copy)
+                        else:
+                            ops.append(dist.P2POp(dist.irecv, self._dst(r, sl), r, self.group))
+            if ops:
+                works += dist.batch_isend_irecv(ops)
+        for w in works:
+            w.wait()
+        if not self.is_root:
+            return None
+        self._combine()
+        return self.out
+
     def assemble(self, locals_):
         """Single process, no process group: ``locals_[r]`` is rank r's [G_r, T] output; the
         root's placement and boundary sums run exactly as in ``run``."""

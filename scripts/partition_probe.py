@@ -80,6 +80,43 @@ def main():
                           "kernels": [k for _, k, _ in per], "rows": [g for _, _, g in per], "max_rank_ms": mx,
                           "gather_ms_model": gather, "predicted_ms": mx + gather,
                           "predicted_speedup": base / (mx + gather)}), flush=True)
+        # overlapped form (TermShardedEval.run_blocks): each rank evaluates rows [0, s_r) then
+        # [s_r, G_r) (pe_row_split); block 0's rows cross NVLink while block 1 is evaluated
+        blk = []
+        for r in range(P):
+            mine = np.sort(order[bounds[r]:bounds[r + 1]])
+            with pe.Context(w.p, w.coeffs[mine], w.exps[mine], w.alpha, n=w.n) as ctx:
+                sp = ctx.row_split()
+                o = torch.empty((ctx.G, T), dtype=torch.int64, device="cuda")
+                s_ = torch.cuda.current_stream()
+                for _ in range(2):
+                    ctx.eval_device_rows(w.j0, T, 0, sp or ctx.G, o.data_ptr(), T, s_.cuda_stream)
+                    if sp:
+                        ctx.eval_device_rows(w.j0, T, sp, ctx.G, o.data_ptr(), T, s_.cuda_stream)
+                t0s, t1s = [], []
+                for _ in range(reps):
+                    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                    e[0].record(s_)
+                    ctx.eval_device_rows(w.j0, T, 0, sp or ctx.G, o.data_ptr(), T, s_.cuda_stream)
+                    e[1].record(s_)
+                    if sp:
+                        ctx.eval_device_rows(w.j0, T, sp, ctx.G, o.data_ptr(), T, s_.cuda_stream)
+                    e[2].record(s_)
+                    torch.cuda.synchronize()
+                    t0s.append(e[0].elapsed_time(e[1]))
+                    t1s.append(e[1].elapsed_time(e[2]))
+                blk.append((statistics.median(t0s), statistics.median(t1s), sp or ctx.G, ctx.G))
+                del o
+            torch.cuda.empty_cache()
+        in0 = sum(b[2] for b in blk[1:]) * T * 8 / (NVLINK_GBS * 1e9) * 1e3
+        in1 = sum(b[3] - b[2] for b in blk[1:]) * T * 8 / (NVLINK_GBS * 1e9) * 1e3
+        emax = max(b[0] + b[1] for b in blk)
+        e1min = min(b[1] for b in blk)
+        pred = emax + max(0.0, in0 - e1min) + in1
+        print(json.dumps({"P": P, "decomposition": "term ranges, 2 row blocks (overlapped gather)",
+                          "rank_block_ms": [[b[0], b[1]] for b in blk], "splits": [b[2] for b in blk],
+                          "max_rank_ms": emax, "gather_block0_ms_model": in0, "gather_block1_ms_model": in1,
+                          "predicted_ms": pred, "predicted_speedup": base / pred}), flush=True)
 
 
 if __name__ == "__main__":

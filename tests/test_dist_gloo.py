@@ -168,3 +168,62 @@ def test_term_partition_bookkeeping():
             assert rows == list(range(rows[0], rows[-1] + 1))
             covered += rows if not (a > 0 and not new_row[a]) else rows[1:]
         assert covered == list(range(int(row_of[-1]) + 1))
+
+
+# ---------------------------------------------------------------- overlapped row blocks
+def _blocks_worker(rank, world, port, args, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import synth
+        from paper_2004_11571_b200.dist import TermShardedEval, bucket_keys, term_partition
+        seed, t, T, p = args
+        w = synth.random_small(seed, p, 6, t, 3, T, 5)
+        w.exps[: int(0.5 * t), :2] = (2, 2)                     # one bucket across ranks
+        order, bounds = term_partition(w.exps, world)
+        sh = TermShardedEval(bucket_keys(w.exps)[order], bounds, T, w.p, torch.device("cpu"),
+                             addmod=_addmod_host(w.p))
+        mine = order[bounds[rank]:bounds[rank + 1]]
+        full = oracle.eval_direct(w.p, w.n, w.coeffs[mine], w.exps[mine], w.alpha, w.j0, T) if mine.size else None
+        splits = [None] * world
+        my_split = (rank * 7 + 1) % max(1, sh.G_r[rank]) if sh.G_r[rank] else 0   # arbitrary splits, some 0
+        dist.all_gather_object(splits, my_split)
+        sh.set_splits(splits)
+        calls = []
+
+        def eval_rows(a, b, local):            # rows [a, b) of this rank's output
+            calls.append((a, b))
+            local[a:b].copy_(torch.from_numpy(full[a:b].view(np.int64)))
+
+        res = sh.run_blocks(eval_rows)
+        assert sorted(calls) == sorted(sh._blocks(rank))
+        if rank == 0:
+            q.put(res.numpy().view(np.uint64).copy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,t,T,p", [(2, 300, 7, (1 << 62) - 57), (3, 400, 5, (1 << 63) - 25),
+                                         (4, 500, 3, (1 << 62) - 57)])
+def test_term_sharded_row_blocks_match_single(world, t, T, p):
+    """The overlapped gather (each rank's rows in two blocks, block 0 sent while block 1 is being
+    evaluated; TermShardedEval.run_blocks) reproduces the single-process oracle, whatever the
+    ranks' splits -- including none, and splits that cut a shared boundary row's rank."""
+    import oracle
+    import synth
+    seed = 91
+    w = synth.random_small(seed, p, 6, t, 3, T, 5)
+    w.exps[: int(0.5 * t), :2] = (2, 2)
+    ref = oracle.eval_direct(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, T)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_blocks_worker, args=(r, world, port, (seed, t, T, p), q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = q.get(timeout=180)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert np.array_equal(got, ref)

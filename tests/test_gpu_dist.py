@@ -96,3 +96,31 @@ def test_unshard_columns_ragged():
     pe.unshard_columns(out.data_ptr(), T + 2, blocks.data_ptr(), P, G, Tr, T)
     want = torch.cat([blocks[r] for r in range(P)], dim=1)[:, :T]
     assert torch.equal(out[:, :T], want) and bool((out[:, T:] == -1).all())
+
+
+def test_eval_device_rows_blocks_equal_full():
+    """pe_eval_device_rows: rows [0, s) then [s, G) (the handle's own split, and an arbitrary one)
+    fill exactly what one pe_eval_device does -- the building block of the overlapped gather
+    (TermShardedEval.run_blocks); a strict row range off the tensor-core path is PE_ENOTSUP."""
+    w = synth.gen_config(3, t=200_000, T=9000)
+    s_ = torch.cuda.current_stream().cuda_stream
+    with pe.Context.from_workload(w) as ctx:
+        G = ctx.G
+        full = torch.empty((G, w.T), dtype=torch.int64, device="cuda")
+        ctx.eval_device(w.j0, w.T, full.data_ptr(), w.T, s_)
+        for split in (ctx.row_split(), G // 3, 1, G - 1):
+            assert 0 < split < G
+            part = torch.full_like(full, -1)
+            ctx.eval_device_rows(w.j0, w.T, 0, split, part.data_ptr(), w.T, s_)
+            assert bool((part[split:] == -1).all())                     # other rows untouched
+            ctx.eval_device_rows(w.j0, w.T, split, G, part.data_ptr(), w.T, s_)
+            torch.cuda.synchronize()
+            assert torch.equal(part, full), split
+    with pe.Context.from_workload(w, path=pe.PATH_INT) as ctx:
+        assert ctx.row_split() == 0
+        buf = torch.empty((ctx.G, w.T), dtype=torch.int64, device="cuda")
+        with pytest.raises(pe.PEError) as ei:
+            ctx.eval_device_rows(w.j0, w.T, 0, 5, buf.data_ptr(), w.T, s_)
+        assert ei.value.code == pe.PE_ENOTSUP
+    ref = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
+    assert np.array_equal(full.cpu().numpy().view(np.uint64), ref)
