@@ -161,6 +161,8 @@ struct Call {
   u32 Lc, Lo, Bk, nb, nbo, lg;          // operand length, output length, block, blocks, out blocks, log2 S
   u32 lgnb, lgnops, lgnouts, lgnbo, lgLo, lgBk;   // the same as shifts (all powers of two)
   u32 nbz[4];           // op o has nonzero coefficients only in its first nbz[o] blocks (others: skipped)
+  const u32* len0;      // optional [njobs]: op 0 of job j has only len0[j] nonzero coefficients (Newton's
+                        // D and N: a bucket of s terms has deg D = s, so its upper blocks are zero)
   u32 keep;             // bit o: op o's spectra are already in place from the previous call (not redone)
   int kind;                             // kMerge / kMul / kTwoMinus
   // outputs
@@ -194,6 +196,7 @@ __global__ void __launch_bounds__(kNttThreads, 3) k_fast_fwd(Call a) {
   const u32 nu = min(per, nunits - u0), npts = nu * S;
   auto skipped = [&](u32 u) {
     const u32 blk = u & (a.nb - 1), o = (u >> a.lgnb) & (a.nops - 1);
+    if (o == 0 && a.len0 && blk >= ((a.len0[u >> (a.lgnb + a.lgnops)] + a.Bk - 1) >> a.lgBk)) return true;
     return ((a.keep >> o) & 1u) || blk >= a.nbz[o];
   };
   if (nu == 1 && skipped(u0)) return;          // whole CTA (one 8192-point unit) not needed
@@ -251,7 +254,13 @@ __global__ void __launch_bounds__(kNttThreads, 3) k_fast_pwinv(Call a) {
       } else {
         oa = 0u; ob = 1u;
       }
-      const u32 na = a.nbz[oa], nbb = a.nbz[ob];        // blocks beyond nbz are zero: no product
+      u32 na = a.nbz[oa], nbb = a.nbz[ob];              // blocks beyond nbz are zero: no product
+      if (a.len0) {
+        const u32 n0 = (a.len0[job] + a.Bk - 1) >> a.lgBk;
+        if (oa == 0) na = min(na, n0);
+        if (ob == 0) nbb = min(nbb, n0);
+      }
+      if (na == 0 || nbb == 0 || c + 1 > na + nbb - 1) continue;
       const u32 blo = c + 1 > nbb ? c + 1 - nbb : 0, bhi = min(c, na - 1);
       for (u32 ba = blo; ba <= bhi; ++ba) {
         const u32 bb = c - ba;
@@ -551,6 +560,7 @@ struct Plan {
   u64 row_cap = 0;
   u32 *d_spec = nullptr, *d_res = nullptr;
   u64 spec_elems = 0, res_elems = 0;
+  u32* d_rootlen = nullptr;    // [G]: a bucket of s padded terms has deg D = s, deg N < s -> s + 1
 };
 
 static void free_ws(Plan* P, cudaStream_t s) {
@@ -568,7 +578,7 @@ void destroy(Plan* P, cudaStream_t s) {
     if (L.d_kids) cudaFreeAsync(L.d_kids, s);
     if (L.d_roots) cudaFreeAsync(L.d_roots, s);
   }
-  for (void* q : {(void*)P->d_twf, (void*)P->d_twi, (void*)P->d_scale})
+  for (void* q : {(void*)P->d_twf, (void*)P->d_twi, (void*)P->d_scale, (void*)P->d_rootlen})
     if (q) cudaFreeAsync(q, s);
   delete P;
 }
@@ -584,8 +594,10 @@ int create(const std::vector<u64>& poff, const ModParams& mp, cudaStream_t s, Pl
   Level L5;
   L5.nnodes = (u32)P->ngroups;
   L5.njobs = 0;
+  std::vector<u32> rootlen(P->G);
   for (u64 g = 0; g < P->G; ++g) {
     cnt[g] = (poff[g + 1] - poff[g]) / 32;
+    rootlen[g] = (u32)std::min<u64>(poff[g + 1] - poff[g] + 1, 1ull << 30);   // > kTMax: no skipping
     off[g] = poff[g] / 32;
     if (cnt[g] == 1) L5.roots.push_back(make_uint2((u32)g, (u32)off[g]));
   }
@@ -658,11 +670,13 @@ int create(const std::vector<u64>& poff, const ModParams& mp, cudaStream_t s, Pl
   if (rc == PE_OK) {
     if (cudaMallocAsync((void**)&P->d_twf, twf.size() * sizeof(uint2), s) != cudaSuccess ||
         cudaMallocAsync((void**)&P->d_twi, twi.size() * sizeof(uint2), s) != cudaSuccess ||
-        cudaMallocAsync((void**)&P->d_scale, sc.size() * sizeof(uint2), s) != cudaSuccess)
+        cudaMallocAsync((void**)&P->d_scale, sc.size() * sizeof(uint2), s) != cudaSuccess ||
+        cudaMallocAsync((void**)&P->d_rootlen, std::max<u64>(P->G, 1) * sizeof(u32), s) != cudaSuccess)
       rc = PE_ENOMEM;
     else if (cudaMemcpyAsync(P->d_twf, twf.data(), twf.size() * sizeof(uint2), cudaMemcpyHostToDevice, s) ||
              cudaMemcpyAsync(P->d_twi, twi.data(), twi.size() * sizeof(uint2), cudaMemcpyHostToDevice, s) ||
-             cudaMemcpyAsync(P->d_scale, sc.data(), sc.size() * sizeof(uint2), cudaMemcpyHostToDevice, s))
+             cudaMemcpyAsync(P->d_scale, sc.data(), sc.size() * sizeof(uint2), cudaMemcpyHostToDevice, s) ||
+             cudaMemcpyAsync(P->d_rootlen, rootlen.data(), P->G * sizeof(u32), cudaMemcpyHostToDevice, s))
       rc = PE_ECUDA;
   }
   if (rc == PE_OK && cudaStreamSynchronize(s) != cudaSuccess) rc = PE_ECUDA;   // host vectors die here
@@ -787,6 +801,7 @@ int eval(Plan* P, const u64* d_c, const u64* d_m, const ModParams& mp, u64 j0, u
     a.nops = 2; a.nouts = 1; a.njobs = (u32)P->G; a.Lc = 2 * k; a.Lo = 2 * k;
     a.kind = kTwoMinus; a.dst[0] = W; a.dstride = T2; a.mp = mp;
     a.nbz[0] = 0; a.nbz[1] = k;               // Y has k coefficients: its upper blocks are zero
+    a.len0 = P->d_rootlen;                    // D's upper blocks are zero for buckets shorter than 2k
     if (int rc = run_call(P, a, s)) return rc;
     // Y <- Y W: op 1 is Y again, same length: its spectra from the call above are reused
     Call b{};
@@ -801,6 +816,7 @@ int eval(Plan* P, const u64* d_c, const u64* d_m, const ModParams& mp, u64 j0, u
   f.base[0] = RN; f.base[1] = Y; f.idx = nullptr; f.nidx = 1; f.ish = 0; f.rstride = T2;
   f.nops = 2; f.nouts = 1; f.njobs = (u32)P->G; f.Lc = T2; f.Lo = T2;
   f.kind = kMul; f.dst[0] = W; f.dstride = T2; f.mp = mp;
+  f.len0 = P->d_rootlen;                      // N: deg < s
   if (int rc = run_call(P, f, s)) return rc;
   k_fast_store<<<grid_for(P->G * T, 256), 256, 0, s>>>(W, P->G, T2, T, d_out, ld);
   FCU(cudaGetLastError());
