@@ -12,7 +12,9 @@ gather of the G x T_r blocks to rank 0.  T is sharded across 
 value  = t*T / device time per step (max over ranks), inputs resident in HBM.
 e2e    = the same metric through the C ABI from pinned HOST inputs to a HOST result:
          pe_create (H2D of coeffs/exps/alpha + device planning + K1) + pe_eval(_device)
-         + gather + D2H of the G x T result, every step.
+         + gather + D2H of the G x T result, every step, one polynomial at a time; the same with
+         uint8 exponents (pe_create_compact) under e2e.compact_exponents, whose "pipelined" entry is
+         a stream of polynomials with two in flight (the next one's create on a host thread).
 roofline = the dominant kernel.  Tensor-core path (default for config 5): k_tc's int8 tensor
          ops per launch (128 per term-point: 64 exact byte-pair MACs) / its CUDA-event launch
          time vs the int8 dense peak (2 x measured bf16), plus the tcgen05 i8 issue rate of the
@@ -318,6 +320,151 @@ def main():
         def step():
             return sh.run(eval_local, w.j0)
 
+    # ---- end-to-end: host inputs -> host result through the C ABI, every step
+    def run_e2e():
+        e2e = None
+        if not args.no_e2e:
+            pin = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64) if a.dtype == np.uint64
+                                             else np.ascontiguousarray(a).view(np.int32)).pin_memory()
+            h_c, h_e, h_a = pin(w_c), pin(w_e), pin(w.alpha)          # this rank's terms (all for N = 1)
+            G_all = sh.G if term_shard else ctx.G
+            h_out = torch.empty((G_all, w.T), dtype=torch.int64).pin_memory() if sh.is_root else None
+            L = pe.lib()
+            import ctypes
+
+            def create_h(compact=False):
+                if compact:
+                    h = L.pe_create_compact(w.p, w.t, w.n, ctypes.c_void_p(h_c.data_ptr()),
+                                            ctypes.c_void_p(h_e8.data_ptr()), ctypes.c_void_p(h_a.data_ptr()), None)
+                else:
+                    h = L.pe_create(w.p, w_c.size, w.n, ctypes.c_void_p(h_c.data_ptr()),
+                                    ctypes.c_void_p(h_e.data_ptr()), ctypes.c_void_p(h_a.data_ptr()))
+                if not h:
+                    raise pe.PEError(L.pe_last_error(), "pe_create")
+                return h
+
+            def eval_h(h):
+                try:
+                    if world == 1:
+                        rc = L.pe_eval(h, w.j0, w.T, ctypes.c_void_p(h_out.data_ptr()))
+                        if rc:
+                            raise pe.PEError(rc, "pe_eval")
+                    elif term_shard:
+                        def ev_rows(out):
+                            rc = L.pe_eval_device(h, w.j0, w.T, ctypes.c_void_p(out.data_ptr()), w.T,
+                                                  ctypes.c_void_p(stream.cuda_stream))
+                            if rc:
+                                raise pe.PEError(rc, "pe_eval_device")
+                        res = sh.run(ev_rows)
+                        if sh.is_root:
+                            h_out.copy_(res)
+                        torch.cuda.synchronize()
+                    else:
+                        def ev(j_first, cnt, out):
+                            rc = L.pe_eval_device(h, j_first, cnt, ctypes.c_void_p(out.data_ptr()), out.shape[1],
+                                                  ctypes.c_void_p(stream.cuda_stream))
+                            if rc:
+                                raise pe.PEError(rc, "pe_eval_device")
+                        res = sh.run(ev, w.j0)
+                        if sh.is_root:
+                            h_out.copy_(res)
+                        torch.cuda.synchronize()
+                finally:
+                    L.pe_destroy(h)
+
+            nrep = max(3, min(args.steps, 5))
+
+            def serial(compact=False):
+                # latency: one polynomial at a time, create -> eval -> result on the host
+                for _ in range(2):
+                    eval_h(create_h(compact))
+                ts = []
+                for _ in range(nrep):
+                    barrier()
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    eval_h(create_h(compact))
+                    torch.cuda.synchronize()
+                    ts.append(max_over_ranks(time.perf_counter() - t0))
+                return statistics.median(ts)
+
+            def pipelined(compact=False, k=None):
+                # throughput: a stream of polynomials, two in flight -- polynomial i+1's pe_create
+                # (its PCIe upload, sort and setup) runs on a host thread while polynomial i is
+                # evaluated and its result copied back; the libpe calls release the GIL (ctypes)
+                from concurrent.futures import ThreadPoolExecutor
+                k = k or max(6, min(args.steps, 10))
+
+                trace = os.environ.get("BENCH_E2E_TRACE") == "1"
+
+                def timed_create():
+                    a = time.perf_counter()
+                    h = create_h(compact)
+                    return h, a, time.perf_counter()
+
+                def run(n):
+                    marks = []
+                    fut = ex.submit(timed_create)
+                    for i in range(n):
+                        h, ca, cb = fut.result()
+                        if i + 1 < n:
+                            fut = ex.submit(timed_create)
+                        ea = time.perf_counter()
+                        eval_h(h)
+                        marks.append(time.perf_counter())
+                        if trace:
+                            log(f"e2e trace: create {1e3 * (cb - ca):.2f} wait {1e3 * (ea - max(cb, marks[-2] if i else ea)):.2f} "
+                                f"eval+destroy {1e3 * (marks[-1] - ea):.2f} ms")
+                    return marks
+
+                with ThreadPoolExecutor(1) as ex:
+                    run(3)                     # warm-up: the memory pool grows to two handles in flight
+                    barrier()
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    marks = run(k)
+                    torch.cuda.synchronize()
+                    dt = max_over_ranks(time.perf_counter() - t0) / k
+                steps = [1e3 * (b - a) for a, b in zip([t0] + marks[:-1], marks)]
+                return dt, k, steps
+
+            h_e8 = None
+            if world == 1 and int(w.exps.max()) < 256:
+                h_e8 = torch.from_numpy(np.ascontiguousarray(w.exps.astype(np.uint8))).pin_memory()
+            e2e_s = serial()
+            # the same through pe_create_compact (uint8 exponents: 120 MB instead of 480 MB over PCIe;
+            # every config's degrees are < 256), single GPU only
+            e2e_c = None
+            if h_e8 is not None:
+                ec = serial(True)
+                ecp, kp, ec_steps = pipelined(True)
+                e2e_c = {"value": w.t * w.T / ec, "unit": UNIT, "ms_per_step": 1e3 * ec,
+                         "h2d_bytes_per_step": w.coeffs.nbytes + h_e8.numel() + w.alpha.nbytes,
+                         "d2h_bytes_per_step": ctx.G * w.T * 8,
+                         "includes": "pe_create_compact (uint8 exponents) + pe_eval, host wall clock",
+                         "pipelined": {"value": w.t * w.T / ecp, "ms_per_step": 1e3 * ecp,
+                                       "step_ms": [round(x, 2) for x in ec_steps],
+                                       "how": f"{kp} polynomials back to back, two in flight: pe_create_compact "
+                                              "of the next on a host thread while the current one is evaluated "
+                                              "and copied back"}}
+            # the host result of the last e2e polynomial must equal the device-timed path's output
+            ref = step()
+            torch.cuda.synchronize()
+            e2e_ok = bool(torch.equal(ref.cpu(), h_out)) if sh.is_root else None
+            if sh.is_root and not e2e_ok:
+                raise SystemExit("bench.py: e2e host result differs from the device path's output")
+            h2d = (w.coeffs.nbytes + w.exps.nbytes + w.alpha.nbytes * world if term_shard
+                   else (w.coeffs.nbytes + w.exps.nbytes + w.alpha.nbytes) * world)
+            e2e = {"value": w.t * w.T / e2e_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_s,
+                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": G_all * w.T * 8,
+                   "includes": "one polynomial at a time: pe_create (H2D + sort + plan + K1) + eval + gather "
+                               "+ D2H, host wall clock, max over ranks",
+                   "matches_device_result": e2e_ok,
+                   "compact_exponents": e2e_c}
+
+        return e2e
+
+
     # ---- device-timed region (clock samples from the warm-up on: nvidia-smi starts slowly)
     with ClockSampler(local_rank) as clk:
         t_load0 = time.time()
@@ -426,101 +573,7 @@ def main():
                 "algorithmic_bytes_per_launch": 16 * w.t + 8 * ctx.G * sh.cnt}
         gpu_launches = 2 * ks["step_launches"]       # k_step + k_fixup per pass (rank 0)
 
-    # ---- end-to-end: host inputs -> host result through the C ABI, every step
-    e2e = None
-    if not args.no_e2e:
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64) if a.dtype == np.uint64
-                                         else np.ascontiguousarray(a).view(np.int32)).pin_memory()
-        h_c, h_e, h_a = pin(w_c), pin(w_e), pin(w.alpha)          # this rank's terms (all for N = 1)
-        G_all = sh.G if term_shard else ctx.G
-        h_out = torch.empty((G_all, w.T), dtype=torch.int64).pin_memory() if sh.is_root else None
-        L = pe.lib()
-        import ctypes
-
-        def e2e_step():
-            h = L.pe_create(w.p, w_c.size, w.n, ctypes.c_void_p(h_c.data_ptr()), ctypes.c_void_p(h_e.data_ptr()),
-                            ctypes.c_void_p(h_a.data_ptr()))
-            if not h:
-                raise pe.PEError(L.pe_last_error(), "pe_create")
-            try:
-                if world == 1:
-                    rc = L.pe_eval(h, w.j0, w.T, ctypes.c_void_p(h_out.data_ptr()))
-                    if rc:
-                        raise pe.PEError(rc, "pe_eval")
-                elif term_shard:
-                    def ev_rows(out):
-                        rc = L.pe_eval_device(h, w.j0, w.T, ctypes.c_void_p(out.data_ptr()), w.T,
-                                              ctypes.c_void_p(stream.cuda_stream))
-                        if rc:
-                            raise pe.PEError(rc, "pe_eval_device")
-                    res = sh.run(ev_rows)
-                    if sh.is_root:
-                        h_out.copy_(res)
-                    torch.cuda.synchronize()
-                else:
-                    def ev(j_first, cnt, out):
-                        rc = L.pe_eval_device(h, j_first, cnt, ctypes.c_void_p(out.data_ptr()), out.shape[1],
-                                              ctypes.c_void_p(stream.cuda_stream))
-                        if rc:
-                            raise pe.PEError(rc, "pe_eval_device")
-                    res = sh.run(ev, w.j0)
-                    if sh.is_root:
-                        h_out.copy_(res)
-                    torch.cuda.synchronize()
-            finally:
-                L.pe_destroy(h)
-
-        for _ in range(2):
-            e2e_step()
-        barrier()
-        torch.cuda.synchronize()
-        ts = []
-        for _ in range(max(3, min(args.steps, 5))):
-            barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            e2e_step()
-            torch.cuda.synchronize()
-            ts.append(max_over_ranks(time.perf_counter() - t0))
-        e2e_s = statistics.median(ts)
-        # the same cycle through pe_create_compact (uint8 exponents: 120 MB instead of 480 MB over
-        # PCIe; every config's degrees are < 256), single GPU only
-        e2e_c = None
-        if world == 1 and int(w.exps.max()) < 256:
-            h_e8 = torch.from_numpy(np.ascontiguousarray(w.exps.astype(np.uint8))).pin_memory()
-
-            def e2e_step_compact():
-                h = L.pe_create_compact(w.p, w.t, w.n, ctypes.c_void_p(h_c.data_ptr()),
-                                        ctypes.c_void_p(h_e8.data_ptr()), ctypes.c_void_p(h_a.data_ptr()), None)
-                if not h:
-                    raise pe.PEError(L.pe_last_error(), "pe_create_compact")
-                try:
-                    rc = L.pe_eval(h, w.j0, w.T, ctypes.c_void_p(h_out.data_ptr()))
-                    if rc:
-                        raise pe.PEError(rc, "pe_eval")
-                finally:
-                    L.pe_destroy(h)
-
-            for _ in range(2):
-                e2e_step_compact()
-            tc_ = []
-            for _ in range(max(3, min(args.steps, 5))):
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                e2e_step_compact()
-                torch.cuda.synchronize()
-                tc_.append(time.perf_counter() - t0)
-            ec = statistics.median(tc_)
-            e2e_c = {"value": w.t * w.T / ec, "unit": UNIT, "ms_per_step": 1e3 * ec,
-                     "h2d_bytes_per_step": w.coeffs.nbytes + h_e8.numel() + w.alpha.nbytes,
-                     "d2h_bytes_per_step": ctx.G * w.T * 8,
-                     "includes": "pe_create_compact (uint8 exponents) + pe_eval, host wall clock"}
-        h2d = (w.coeffs.nbytes + w.exps.nbytes + w.alpha.nbytes * world if term_shard
-               else (w.coeffs.nbytes + w.exps.nbytes + w.alpha.nbytes) * world)
-        e2e = {"value": w.t * w.T / e2e_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_s,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": G_all * w.T * 8,
-               "includes": "pe_create (H2D + sort + plan + K1) + eval + gather + D2H, host wall clock, max over ranks",
-               "compact_exponents": e2e_c}
+    e2e = run_e2e()
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None

@@ -163,7 +163,10 @@ int pe_eval_device_rows(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t g0, uint64_
  * (no tensor-core path, or G < 2). */
 uint64_t pe_row_split(const pe_ctx* h);
 
-void pe_destroy(pe_ctx* h); /* NULL-safe; synchronises the handle's device work */
+/* NULL-safe.  Waits for the handle's own streams and for the latest work each pe_eval_device(_rows)
+ * call enqueued on a caller stream, then frees the handle (stream-ordered); it does not synchronise
+ * the whole device, so other handles' work (e.g. another thread's pe_create) keeps running. */
+void pe_destroy(pe_ctx* h);
 
 uint64_t pe_num_buckets(const pe_ctx* h);                   /* G (0 if h NULL) */
 int pe_bucket_exps(const pe_ctx* h, uint32_t* dxdy);        /* HOST uint32[2G]: row g -> (dx,dy) */

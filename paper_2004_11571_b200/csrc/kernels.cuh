@@ -3,7 +3,7 @@
 //   k_keys        a2: bucket key (dx<<32 | dy) per term
 //   k_max_exp     max evaluated exponent (power-table size d)
 //   k_power_table a3: beta_k^e tables, Montgomery form
-//   k_setup       a3: m_i, Shoup w_i, reduced c_i in the padded tile layout
+//   k_setup       a3: m_i, Shoup w_i in the padded tile layout (k_setup_c: reduced c_i)
 //   k_step        a4+a5+a6: seed a_i = c_i m_i^{j_s}, then per point acc += a_i, a_i <- a_i m_i
 //                 with the per-(x,y) segmented reduction
 //   k_fixup       a6: cross-CTA carries of one bucket -> canonical out
@@ -215,10 +215,10 @@ static __global__ void k_monomials(const E* __restrict__ exps, u64 a, u64 b, u32
 // cnt[g] slots are the sorted terms bstart[g] .. bstart[g]+cnt[g]-1, the rest are padding (c = 0,
 // m = 1: contributes 0 at every point).  Coefficients reduced mod p (reading R5), m_i from
 // k_monomials, Shoup constant w_i = floor(m_i 2^64 / p).
-static __global__ void k_setup(const u64* __restrict__ coeffs, const u64* __restrict__ m_in,
+static __global__ void k_setup(const u64* __restrict__ m_in,
                         const u32* __restrict__ sorted_idx, const u64* __restrict__ poff,
                         const u64* __restrict__ bstart, u32 G, u64 t_pad,
-                        u64* __restrict__ c_out, u64* __restrict__ m_out, u64* __restrict__ w_out,
+                        u64* __restrict__ m_out, u64* __restrict__ w_out,
                         u32* __restrict__ perm_out, ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
     u32 lo = 0, hi = G;   // bucket g: poff[g] <= q < poff[g+1]
@@ -229,17 +229,26 @@ static __global__ void k_setup(const u64* __restrict__ coeffs, const u64* __rest
     const u32 g = lo;
     const u64 r = q - poff[g];
     const u64 cnt = bstart[g + 1] - bstart[g];
-    u64 c = 0, m = 1 % mp.p;
+    u64 m = 1 % mp.p;
     u32 src = 0xffffffffu;
     if (r < cnt) {
       src = sorted_idx[bstart[g] + r];
-      c = coeffs[src] % mp.p;
       m = m_in[src];
     }
-    c_out[q] = c;
     m_out[q] = m;
     w_out[q] = shoup_w_fast(m, mp);
     perm_out[q] = src;
+  }
+}
+
+// The coefficients in the same layout, reduced mod p (padding: c = 0).  Separate from k_setup so
+// that pe_create uploads them last, while the sort and the tensor-path setup (which need only the
+// exponents) run.
+static __global__ void k_setup_c(const u64* __restrict__ coeffs, const u32* __restrict__ perm, u64 t_pad,
+                                 u64* __restrict__ c_out, u64 p) {
+  for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
+    const u32 src = perm[q];
+    c_out[q] = src != 0xffffffffu ? coeffs[src] % p : 0;
   }
 }
 

@@ -12,7 +12,9 @@
 #include <cub/iterator/counting_input_iterator.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <map>
+#include <mutex>
 #include <tuple>
 #include <cstdio>
 #include <cstdlib>
@@ -131,6 +133,10 @@ struct pe_ctx {
   size_t seed_elems = 0;
   u32* d_tc_scratch = nullptr;   // k_tc per-CTA drained diagonal sums (n_sm x 2 x kDiag x kChunk u32)
   u32* h_status = nullptr;       // mapped host word: k_tc sets it when a pipeline wait times out
+  u32* d_status = nullptr;       // its device address
+  // caller streams pe_eval_device(_rows) enqueued work on, with an event after the latest such
+  // work: pe_destroy waits for these instead of synchronising the whole device
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> used;
   // k_tc piece plans, one per chunk count of a pass (tc_plan): pieces, partial slots, unit schedule
   struct TcPlan {
     u32 npieces = 0, nslots = 0, grid = 0, max_slots = 0;   // max_slots: most partial rows of one bucket
@@ -164,6 +170,42 @@ static void drop_recs(pe_ctx* h) {
   h->recs.clear();
 }
 
+// k_tc status words: mapped, portable pinned host memory handed out from 4-KB slabs that live for
+// the process -- cudaHostAlloc / cudaFreeHost per handle would serialise with (and cudaFreeHost
+// synchronise against) work other threads have in flight on the device
+static std::mutex g_status_mu;
+static std::vector<std::pair<u32*, u32*>> g_status_free;   // (host, device) words
+static int status_get(u32** host, u32** dev) {
+  std::lock_guard<std::mutex> lk(g_status_mu);
+  if (g_status_free.empty()) {
+    const int kWords = 1024;
+    u32* base = nullptr;
+    u32* dbase = nullptr;
+    if (cudaHostAlloc((void**)&base, kWords * sizeof(u32), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+      return PE_ENOMEM;
+    if (cudaHostGetDevicePointer((void**)&dbase, base, 0) != cudaSuccess) return PE_ECUDA;   // slab kept
+    for (int i = kWords - 1; i >= 0; --i) g_status_free.emplace_back(base + i, dbase + i);
+  }
+  *host = g_status_free.back().first;
+  *dev = g_status_free.back().second;
+  g_status_free.pop_back();
+  **host = 0;
+  return PE_OK;
+}
+static void status_put(u32* host, u32* dev) {
+  std::lock_guard<std::mutex> lk(g_status_mu);
+  g_status_free.emplace_back(host, dev);
+}
+
+static int note_use(pe_ctx* h, cudaStream_t s) {
+  for (auto& u : h->used)
+    if (u.first == s) return cudaEventRecord(u.second, s) == cudaSuccess ? PE_OK : PE_ECUDA;
+  cudaEvent_t e;
+  if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return PE_ECUDA;
+  h->used.emplace_back(s, e);
+  return cudaEventRecord(e, s) == cudaSuccess ? PE_OK : PE_ECUDA;
+}
+
 static void free_all(pe_ctx* h) {
   if (!h) return;
   drop_recs(h);
@@ -182,7 +224,7 @@ static void free_all(pe_ctx* h) {
   if (s) cudaStreamSynchronize(s);
   if (h->copy_stream) cudaStreamSynchronize(h->copy_stream), cudaStreamDestroy(h->copy_stream);
   if (h->copy_done) cudaEventDestroy(h->copy_done);
-  if (h->h_status) cudaFreeHost(h->h_status);
+  if (h->h_status) status_put(h->h_status, h->d_status), h->h_status = h->d_status = nullptr;
   if (h->fast) fast::destroy(h->fast, s), h->fast = nullptr;
   if (h->stream) cudaStreamDestroy(h->stream);
 }
@@ -290,12 +332,17 @@ static u64 tc_row_split(const pe_ctx* h) {
 struct CreateProf {
   bool on = false;
   std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  std::vector<double> host_ms;   // host clock when each mark was issued
+  static double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
   void mark(const char* what, cudaStream_t s) {
     if (!on) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, s);
     ev.push_back({what, e});
+    host_ms.push_back(now_ms());
   }
   ~CreateProf() {
     if (!on || ev.empty()) return;
@@ -303,7 +350,7 @@ struct CreateProf {
     for (size_t i = 1; i < ev.size(); ++i) {
       float ms = 0;
       cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
-      fprintf(stderr, "pe_create %-28s %8.3f ms\n", ev[i].first, ms);
+      fprintf(stderr, "pe_create %-28s device %8.3f ms  host %8.3f ms\n", ev[i].first, ms, host_ms[i] - host_ms[i - 1]);
     }
     for (auto& x : ev) cudaEventDestroy(x.second);
   }
@@ -350,19 +397,31 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
   }
 
   // ---- upload in chunks on a copy stream; keys (a2) and monomials (a3) of each chunk run on the
-  // handle's stream as soon as it lands, while the next chunks are still crossing PCIe
+  // handle's stream as soon as it lands, while the next chunks are still crossing PCIe.  The
+  // exponents go first: the sort, the plan and the tensor-path setup need only them, and run while
+  // the coefficients (needed by k_setup_c alone) follow.
   u64 *d_key, *d_key2, *d_m_in; u32 *d_idx, *d_idx2, *d_kmax;
   if (dalloc(&d_key, t) || dalloc(&d_key2, t) || dalloc(&d_idx, t) || dalloc(&d_idx2, t) || dalloc(&d_m_in, t) ||
       dalloc(&d_kmax, 2))
     return g_last_error;
   tmp.v.insert(tmp.v.end(), {d_key, d_key2, d_idx, d_idx2, d_m_in, d_kmax});
   CU(cudaMemsetAsync(d_kmax, 0, 2 * sizeof(u32), s));
+  // the coefficients are on the device; on every exit the handle stream waits for them before the
+  // temporaries (freed on that stream after this guard) can be reused
+  struct EvGuard {
+    cudaEvent_t& e;
+    cudaStream_t s;
+    ~EvGuard() { if (e) cudaStreamWaitEvent(s, e, 0), cudaEventDestroy(e); }
+  };
+  cudaEvent_t c_landed = nullptr;
+  EvGuard c_guard{c_landed, s};
   {
     cudaStream_t cs = nullptr;
     CU(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     const u64 nchunk = t >= (1u << 20) ? 8 : 1;
     std::vector<cudaEvent_t> ev(nchunk, nullptr);
     int rc = PE_OK;
+    if (cudaEventCreateWithFlags(&c_landed, cudaEventDisableTiming) != cudaSuccess) rc = PE_ECUDA;
     cudaEvent_t ready = nullptr;   // the copy stream starts after the handle stream's allocations
     if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventRecord(ready, s) != cudaSuccess || cudaStreamWaitEvent(cs, ready, 0) != cudaSuccess)
@@ -370,7 +429,6 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
     for (u64 k = 0; k < nchunk && rc == PE_OK; ++k) {
       const u64 a = t * k / nchunk, b = t * (k + 1) / nchunk;
       if (cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming) != cudaSuccess ||
-          cudaMemcpyAsync(d_coeffs + a, coeffs + a, (b - a) * sizeof(u64), cudaMemcpyHostToDevice, cs) != cudaSuccess ||
           cudaMemcpyAsync(d_exps + a * n, exps + a * n, (b - a) * n * sizeof(E), cudaMemcpyHostToDevice, cs) !=
               cudaSuccess ||
           cudaEventRecord(ev[k], cs) != cudaSuccess || cudaStreamWaitEvent(s, ev[k], 0) != cudaSuccess) {
@@ -381,6 +439,10 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
       k_monomials<<<grid_for(b - a, 256), 256, 0, s>>>(d_exps, a, b, n, d_table, d_alpha, d_m_in, h->mp);
       if (cudaGetLastError() != cudaSuccess) rc = PE_ECUDA;
     }
+    if (rc == PE_OK &&
+        (cudaMemcpyAsync(d_coeffs, coeffs, t * sizeof(u64), cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+         cudaEventRecord(c_landed, cs) != cudaSuccess))
+      rc = PE_ECUDA;
     for (auto e : ev) if (e) cudaEventDestroy(e);   // destruction is deferred until the events complete
     if (ready) cudaEventDestroy(ready);
     cudaStreamDestroy(cs);                           // likewise: returns at once, the copies still run
@@ -499,8 +561,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
       dalloc(&h->d_perm, h->t_pad) || dalloc(&h->d_wt_info, n_wt) || dalloc(&h->d_slot_start, G + 1))
     return g_last_error;
   prof.mark("host plan (+gaps)", s);
-  k_setup<<<grid_for(h->t_pad, 256), 256, 0, s>>>(d_coeffs, d_m_in, d_idxS, d_poff, d_bstart, (u32)G, h->t_pad,
-                                                   h->d_c, h->d_m, h->d_w, h->d_perm, h->mp);
+  k_setup<<<grid_for(h->t_pad, 256), 256, 0, s>>>(d_m_in, d_idxS, d_poff, d_bstart, (u32)G, h->t_pad,
+                                                   h->d_m, h->d_w, h->d_perm, h->mp);
   CU(cudaGetLastError());
 
   // ---- tensor-core path (tc.cuh): per-term strides + the piece plan
@@ -559,8 +621,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
     }
     CU(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
     h->tc_rounds = h->p < (1ull << 31) ? 1 : tc::kRounds;   // 4-byte digits: one round
-    if (cudaHostAlloc((void**)&h->h_status, sizeof(u32), cudaHostAllocMapped) != cudaSuccess) return set_err(PE_ENOMEM);
-    *h->h_status = 0;
+    if (int rc = status_get(&h->h_status, &h->d_status)) return set_err(rc);
     h->tc_ok = true;
   }
   // ---- k_step's warp-tile plan (host), computed while the setup kernels above run
@@ -605,6 +666,10 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
     if (rc != PE_OK) return set_err(rc);
   }
   prof.mark("tc setup + rplanes", s);
+  CU(cudaStreamWaitEvent(s, c_landed, 0));
+  k_setup_c<<<grid_for(h->t_pad, 256), 256, 0, s>>>(d_coeffs, h->d_perm, h->t_pad, h->d_c, h->mp.p);
+  CU(cudaGetLastError());
+  prof.mark("coefficients", s);
   CU(cudaStreamSynchronize(s));  // host vectors above must outlive the copies; tmp frees after
   return PE_OK;
 }
@@ -739,8 +804,12 @@ extern "C" void pe_destroy(pe_ctx* h) {
   int cur = 0;
   cudaGetDevice(&cur);
   cudaSetDevice(h->device);
+  // the handle's own streams, and the latest work it enqueued on each caller stream; not the
+  // whole device, so that destroying a handle does not wait for other handles' (threads') work
   if (h->stream) cudaStreamSynchronize(h->stream);
-  cudaDeviceSynchronize();
+  if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+  for (auto& u : h->used) cudaEventSynchronize(u.second), cudaEventDestroy(u.second);
+  h->used.clear();
   free_all(h);
   cudaSetDevice(cur);
   delete h;
@@ -925,17 +994,33 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s,
     h->seed_elems = (size_t)h->t_pad * nch_max * tc::kLSRec;
   }
   if (!h->d_tc_scratch) CU(cudaMallocAsync((void**)&h->d_tc_scratch, (size_t)h->n_sm * 2 * tc::kDiag * tc::kChunk * sizeof(u32), s));
-  u32* d_status = nullptr;
-  CU(cudaHostGetDevicePointer((void**)&d_status, h->h_status, 0));
+  u32* d_status = h->d_status;
   // kernel mode: 0 = lazy chains, 8 digits; 1 = p >= 2^62, exact chains, 8 digits; 2 = p < 2^31,
   // exact chains (values < 2^32), 4 digits, one round
   // 3 = 2^31 <= p < 2^54: lazy chains (values < 2^56), 7 digits, two rounds of 12 + 6 MMAs
   const int mode = h->p < (1ull << 31) ? 2 : h->p < (1ull << 54) ? 3 : (h->p >= (1ull << 62) ? 1 : 0);
-  CU(cudaFuncSetAttribute(tc::k_tc<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
-  CU(cudaFuncSetAttribute(tc::k_tc<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
-  CU(cudaFuncSetAttribute(tc::k_tc<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
-  CU(cudaFuncSetAttribute(tc::k_tc<false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
-  CU(cudaFuncSetAttribute(tc::k_tc<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes));
+  // k_tc's units are scheduled statically over its persistent CTAs, so every CTA must own its SM:
+  // it asks for the whole of the SM's shared memory (default; PE_TC_EXCLUSIVE=0: only what it
+  // uses), which keeps a concurrent kernel of another stream (e.g. a pe_create running beside this
+  // evaluation) from co-residing with one of its CTAs and making that CTA the launch's straggler
+  const void* tc_fns[5] = {(const void*)tc::k_tc<false, 0>, (const void*)tc::k_tc<false, 1>,
+                           (const void*)tc::k_tc<false, 2>, (const void*)tc::k_tc<false, 3>,
+                           (const void*)tc::k_tc<true, 0>};
+  static thread_local int smem_dev = -1, smem_dyn = 0;
+  if (smem_dev != h->device) {
+    int optin = 0;
+    CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+    size_t st = 0;
+    for (const void* f : tc_fns) {
+      cudaFuncAttributes fa;
+      CU(cudaFuncGetAttributes(&fa, f));
+      st = std::max(st, fa.sharedSizeBytes);
+    }
+    smem_dyn = std::max<int>((int)tc::kSmemBytes, optin - (int)st);
+    smem_dev = h->device;
+  }
+  const int tc_smem = env_int("PE_TC_EXCLUSIVE", 1) ? smem_dyn : (int)tc::kSmemBytes;
+  for (const void* f : tc_fns) CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem));
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
     const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
@@ -991,11 +1076,11 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s,
       CU(cudaMemset(d_prof, 0, nprof * sizeof(unsigned long long)));
       a.prof = d_prof;
     }
-    if (d_prof && mode == 0) tc::k_tc<true, 0><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
-    else if (mode == 1) tc::k_tc<false, 1><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
-    else if (mode == 2) tc::k_tc<false, 2><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
-    else if (mode == 3) tc::k_tc<false, 3><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
-    else tc::k_tc<false, 0><<<grid, tc::kThreads, tc::kSmemBytes, s>>>(a);
+    if (d_prof && mode == 0) tc::k_tc<true, 0><<<grid, tc::kThreads, tc_smem, s>>>(a);
+    else if (mode == 1) tc::k_tc<false, 1><<<grid, tc::kThreads, tc_smem, s>>>(a);
+    else if (mode == 2) tc::k_tc<false, 2><<<grid, tc::kThreads, tc_smem, s>>>(a);
+    else if (mode == 3) tc::k_tc<false, 3><<<grid, tc::kThreads, tc_smem, s>>>(a);
+    else tc::k_tc<false, 0><<<grid, tc::kThreads, tc_smem, s>>>(a);
     CU(cudaGetLastError());
     if (d_prof) {
       std::vector<unsigned long long> hp(nprof);
@@ -1176,7 +1261,8 @@ extern "C" int pe_eval_device(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t* d_ou
   int cur = 0;
   CU(cudaGetDevice(&cur));
   if (cur != h->device) CU(cudaSetDevice(h->device));   // kernels and stream-ordered allocations go to the handle's device
-  const int rc = eval_device_impl(h, j0, T, d_out, ld, (cudaStream_t)stream);
+  int rc = eval_device_impl(h, j0, T, d_out, ld, (cudaStream_t)stream);
+  if (note_use(h, (cudaStream_t)stream) != PE_OK && rc == PE_OK) rc = set_err(PE_ECUDA);
   if (cur != h->device) cudaSetDevice(cur);
   return rc;
 }
@@ -1195,7 +1281,8 @@ extern "C" int pe_eval_device_rows(pe_ctx* h, uint64_t j0, uint64_t T, uint64_t 
   int cur = 0;
   CU(cudaGetDevice(&cur));
   if (cur != h->device) CU(cudaSetDevice(h->device));
-  const int rc = eval_tc(h, j0, T, d_out, ld, (cudaStream_t)stream, g0, g1);
+  int rc = eval_tc(h, j0, T, d_out, ld, (cudaStream_t)stream, g0, g1);
+  if (note_use(h, (cudaStream_t)stream) != PE_OK && rc == PE_OK) rc = set_err(PE_ECUDA);
   if (cur != h->device) cudaSetDevice(cur);
   return rc;
 }
@@ -1303,11 +1390,11 @@ extern "C" int pe_monomials(const pe_ctx* h, uint64_t* m) {
   if (!h || (h->t && !m)) return set_err(PE_EINVAL);
   if (h->t == 0) return PE_OK;
   u64* d;
-  CU(cudaMalloc((void**)&d, h->t * sizeof(u64)));
+  CU(cudaMallocAsync((void**)&d, h->t * sizeof(u64), h->stream));
   k_scatter_m<<<grid_for(h->t_pad, 256), 256, 0, h->stream>>>(h->d_m, h->d_perm, h->t_pad, d);
   cudaError_t e = cudaMemcpyAsync(m, d, h->t * sizeof(u64), cudaMemcpyDeviceToHost, h->stream);
+  cudaFreeAsync(d, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-  cudaFree(d);
   if (e != cudaSuccess) return set_err(PE_ECUDA);
   return PE_OK;
 }
