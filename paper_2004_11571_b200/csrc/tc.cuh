@@ -41,6 +41,14 @@
 //              writes their 8 byte planes in the no-swizzle K-major UMMA layout; one warp's first
 //              lane copies the K-block's baby-step planes into the stage with TMA, the other's
 //              prefetches the group's next K-block of per-term records.
+//
+// Swapped form (MODE 4 / 5, 8-digit p >= 2^54, the default for those primes): the point-dependent
+// factor c m^{j_s} is folded into the baby steps instead, R'[i][v] = c_i m_i^{j_s + v}, and the
+// giant steps G[u][i] = m_i^{uV} become the point-independent factor, built once per handle
+// (k_tc_gplanes, Montgomery residues, 1 KB per term) and streamed into the A half of the stages by
+// TMA.  The producers then generate only the V = 64 baby-step rows per term and unit (half the
+// giant-step rows of the plain form) into the B half; the MMAs, the TMEM layout and the epilogue
+// are the same (sum_i G R' = 2^64 X, one REDC).
 #pragma once
 #include "modcore.cuh"
 
@@ -63,6 +71,7 @@ constexpr u32 kPlaneA = kLBOA + 2048;
 constexpr u32 kPlaneB = kV * 16;          // one plane's rows in one K half (1 KB)
 constexpr u32 kLBOB = 8 * kPlaneB;        // K-half stride (8 KB)
 constexpr u32 kStageBytes = 8 * kPlaneA + 2 * kLBOB;     // 8 L planes + 8 R planes (49152 B)
+constexpr u32 kGBytes = 8 * kPlaneA;      // one K-block's giant-step planes in the A layout (32 KB)
 // Per-term records (array of structs, so one K-block's data is two contiguous bulk copies):
 //   LS record (per chunk, 1 u64): the chunk seed c m^{j_s}
 //   C  record (10 u64): the giant-step chain multiplier m^{8V} and its Shoup constant, and the
@@ -90,14 +99,24 @@ static_assert(kSmemBytes + 256 <= 232448, "shared memory");
 // one wide MMA (B = planes t..t+k-1, N = 64k <= 256) covers k of them
 // group 2: the single round of the 4-digit mode (p < 2^31: values < 2^32), d = 0..6
 // group 4: the 7-digit mode's second round, d = 8..12
+// groups 5 / 6: the CTA-pair kernel's (tc2.cuh) balanced rounds, 32 digit pairs each --
+// d = {0, 1, 6, 7, 8, 9, 14} and d = {2, 3, 4, 5, 10, 11, 12, 13} -- so the two rounds of a piece
+// take equal time and, running side by side, share its giant-step planes through L2
 __host__ __device__ constexpr int group_diag(int g, int di) {
-  return g == 0 ? di : g == 1 ? (di < 7 ? 8 + di : -1) : g == 2 ? (di < 7 ? di : -1) : (di < 5 ? 8 + di : -1);
+  return g == 0 ? di
+       : g == 1 ? (di < 7 ? 8 + di : -1)
+       : g == 2 ? (di < 7 ? di : -1)
+       : g == 5 ? (di < 2 ? di : di < 6 ? 4 + di : di == 6 ? 14 : -1)
+       : g == 6 ? (di < 4 ? 2 + di : 6 + di)
+       : (di < 5 ? 8 + di : -1);
 }
 
 struct TcArgs {
   const u64* LS;         // [nch][t_pad] chunk seeds c m^{j_s}
   const u64* C;          // [t_pad][10] C records (giant-step chain multiplier, m^{rr V} table)
-  const uint8_t* Rp;     // [t_pad / 32][kRBytes] baby-step byte planes (k_tc_rplanes)
+  const uint8_t* Rp;     // [t_pad / 32][kRBytes] baby-step byte planes (k_tc_rplanes), MODE 0-3
+  const uint8_t* Gp;     // [t_pad / 32][2][kGBytes] giant-step byte planes, u < 128 then 128 <= u < 256
+                         // (k_tc_gplanes), MODE 4-5; the single-CTA kernel reads the first half
   const uint4* piece;    // x = first padded term, y = K-blocks, z = partial slot (sorted by size desc)
   const u32* sched;      // units of CTA b: sched[sched_off[b] .. sched_off[b+1])  (host LPT schedule)
   const u32* sched_off;  // [gridDim.x + 1]
@@ -722,7 +741,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
     const u32 tq = (u32)(lane >> 3), rr = (u32)(lane & 7);
     const u32 term0 = (u32)sub * 16 + tq * 4;     // first of the lane's 4 terms
     const u32 stage0 = smem_u32(smem) + (u32)my_stage * kStageBytes;
-    const u32 planes0 = stage0 + plane_off<kLBOA>(rr, term0);
+    constexpr bool SW = MODE >= 4;                        // swapped form: generate R' into the B half
+    const u32 planes0 = SW ? stage0 + 8 * kPlaneA + plane_off<kLBOB>(rr, term0) : stage0 + plane_off<kLBOA>(rr, term0);
     const u32 seed_off = term0 * kLSRec * 8;
     const u32 mul_off = kDataLS + (term0 * kCRec + kC_mL) * 8;
     const u32 g_off = kDataLS + (term0 * kCRec + kC_g0 + rr) * 8;
@@ -764,6 +784,9 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       if (leader) {
         if (PROF && (a.dbg == 4 || a.dbg == 6 || a.dbg == 7)) {
           mbar_arrive(&full[stage]);
+        } else if (SW) {
+          mbar_expect_tx(&full[stage], kGBytes);
+          bulk_g2s(stage0, a.Gp + ((u64)cur.q0 / kKB + cur.kb) * 2 * kGBytes, kGBytes, &full[stage]);
         } else {
           mbar_expect_tx(&full[stage], kRBytes);
           bulk_g2s(stage0 + 8 * kPlaneA, a.Rp + ((u64)cur.q0 / kKB + cur.kb) * kRBytes, kRBytes, &full[stage]);
@@ -771,7 +794,17 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       }
       if (loader && ahead.valid)
         load_kblock(a, ahead, data0 + (slot0 + ((guse + 1) & 1)) * kDataSlot, &dfull[slot0 + ((guse + 1) & 1)]);
-      if (!(PROF && (a.dbg == 2 || a.dbg >= 6))) {
+      if (SW && !(PROF && (a.dbg == 2 || a.dbg >= 6))) {
+        // baby-step rows rr + 8k (k < 8) of R' = c m^{j_s + v}
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+          store_digits<kPlaneB>(planes0 + (u32)k * 128u, x);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            x[e] = MODE == 5 ? mul_shoup2(x[e], sm[e], sw[e], np) : mul_shoup4(x[e], sm[e], sw[e], np);
+        }
+        store_digits<kPlaneB>(planes0 + 7u * 128u, x);
+      } else if (!(PROF && (a.dbg == 2 || a.dbg >= 6))) {
 #pragma unroll 3
         for (int k = 0; k < 15; ++k) {
           // row rr + 8k: the next 8-row core-matrix group, +128 bytes
@@ -913,16 +946,21 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
 // Per padded term (pe_create): the C record -- the giant-step chain multiplier m^{8V} (stride 8
 // rows of L), its Shoup constant and the Montgomery table m^{rr V} (rr < 8) -- and, for the
 // per-pass chunk seeds, Montgomery m^V and m^{kChunk}.
+// Swapped form (SW): the chain runs over the baby steps, so the multiplier is m^8 and the table
+// m^{rr} (rr < 8).
+template <bool SW>
 static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ C, u64* __restrict__ MS,
                                   ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
-    const u64 mV = mont_pow(to_mont(m[q], mp), kV, mp);
-    u64 g = mp.r1;                                     // Montgomery m^{rr V}
+    const u64 mm = to_mont(m[q], mp);
+    const u64 mV = mont_pow(mm, kV, mp);
+    const u64 step = SW ? mm : mV;
+    u64 g = mp.r1;                                     // Montgomery m^{rr V} (SW: m^{rr})
     for (int rr = 0; rr < 8; ++rr) {
       C[q * kCRec + kC_g0 + rr] = g;
-      g = mont_mul(g, mV, mp);
+      g = mont_mul(g, step, mp);
     }
-    const u64 aL = from_mont(g, mp);                   // m^{8V}
+    const u64 aL = from_mont(g, mp);                   // m^{8V} (SW: m^8)
     C[q * kCRec + kC_mL] = aL;
     C[q * kCRec + kC_wL] = shoup_w_fast(aL, mp);
     MS[2 * q] = mV;
@@ -986,6 +1024,63 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
     uint4* dst = (uint4*)(Rp + blk * 2 * kRBytes);
     const uint4* src = (const uint4*)st;
     for (u32 i = threadIdx.x; i < 2 * kRBytes / 16; i += kRpThreads) dst[i] = src[i];
+    __syncthreads();
+  }
+}
+
+// Per handle, swapped form (MODE 4 / 5): the giant-step byte planes G_s[i][u] = byte s of the
+// Montgomery residue m_i^{uV} 2^64 mod p for u < 2U (the CTA-pair kernel's M = 256 rows; the
+// single-CTA kernel uses u < U), in the A layout of a stage: [K-block][half h: u = 128h ..][32 KB].
+// Block = one (K-block, half), 2 warps (one per K half); lane = (4 terms, rows r + 8j, j < 16): 4
+// chains of stride 8 with the fixed multiplier m^{8V} (Shoup); the block leaves with 16-byte stores.
+constexpr int kGpThreads = 64;
+template <bool LAZY>
+static __global__ void __launch_bounds__(kGpThreads) k_tc_gplanes(const u64* __restrict__ m, u64 t_pad,
+                                                                  uint8_t* __restrict__ Gp, ModParams mp) {
+  __shared__ __align__(16) uint8_t st[kGBytes];
+  const u64 nblk = 2 * ((t_pad + kKB - 1) / kKB);   // (K-block, half) pairs
+  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const u32 ql = (u32)(lane >> 3), r = (u32)(lane & 7);
+  const u32 base = plane_off<kLBOA>(r, (u32)h * 16 + ql * 4);
+  for (u64 blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const u32 half = (u32)(blk & 1);
+    const u64 q0 = (blk >> 1) * kKB + (u64)h * 16 + ql * 4;
+    u64 y[4], mS[4], wS[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const u64 mm = to_mont(q0 + e < t_pad ? m[q0 + e] : 0ull, mp);
+      u64 mV = mm;
+#pragma unroll 1
+      for (int i = 0; i < 6; ++i) mV = mont_mul(mV, mV, mp);   // m^V, V = 64
+      const u64 m2V = mont_mul(mV, mV, mp), m4V = mont_mul(m2V, m2V, mp);
+      const u64 m8V = mont_mul(m4V, m4V, mp);
+      mS[e] = from_mont(m8V, mp);                        // normal m^{8V}: the chain's fixed multiplier
+      wS[e] = m8V * mp.pinv;                             // its Shoup constant
+      u64 x = mp.r1;
+      if (r & 1) x = mV;
+      if (r & 2) x = mont_mul(x, m2V, mp);
+      if (r & 4) x = mont_mul(x, m4V, mp);
+      if (half) {                                        // x m^{128 V} = x (m^{8V})^16
+        u64 t = m8V;
+#pragma unroll 1
+        for (int i = 0; i < 4; ++i) t = mont_mul(t, t, mp);
+        x = mont_mul(x, t, mp);
+      }
+      y[e] = x;                                          // m^{(128 half + r) V} (Montgomery residue)
+    }
+#pragma unroll 1
+    for (u32 j = 0; j < (u32)kU / 8; ++j) {              // row r + 8j
+      store_digits<kPlaneA>(smem_u32(st) + base + j * 128u, y);
+      if (j + 1 < (u32)kU / 8) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          y[e] = LAZY ? mul_shoup4(y[e], mS[e], wS[e], mp.np) : mul_shoup2(y[e], mS[e], wS[e], mp.np);
+      }
+    }
+    __syncthreads();
+    uint4* dst = (uint4*)(Gp + blk * kGBytes);
+    const uint4* src = (const uint4*)st;
+    for (u32 i = threadIdx.x; i < kGBytes / 16; i += kGpThreads) dst[i] = src[i];
     __syncthreads();
   }
 }
