@@ -27,7 +27,6 @@
 #include "fast.h"
 #include "kernels.cuh"
 #include "tc.cuh"
-#include "tc2.cuh"
 
 using namespace pe;
 
@@ -309,10 +308,7 @@ static unsigned grid_for(u64 n, unsigned block) {
 
 // ---------------------------------------------------------------- create
 static int tc_plan(const pe_ctx* h, u32 nch, u64 g0, u64 g1, bool upload, cudaStream_t s, pe_ctx::TcPlan** out);
-// nch | kPairBit: a plan of the CTA-pair kernel (tc2.cuh): nch 16384-point pair chunks dealt to
-// n_sm / 2 clusters instead of 8192-point chunks to n_sm CTAs
-static const u32 kPairBit = 1u << 31;
-static u32 tc_workers(const pe_ctx* h, u32 nch) { return (nch & kPairBit) ? (u32)h->n_sm / 2 : (u32)h->n_sm; }
+
 
 // pe_eval's row split for the tensor path: rows [0, G1) then [G1, G), the first block's device->host
 // copy overlapping the second's evaluation.  G1 minimises E1 + max(E2, D1) + D2 under a simple model
@@ -580,7 +576,7 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
     const u64 nrblk = (tp + 2 * tc::kKB - 1) / (2 * tc::kKB);
     // 8-digit primes (p >= 2^54) use the swapped form unless PE_TC_SWAP=0 (tc.cuh)
     h->tc_swap = h->p >= (1ull << 54) && env_int("PE_TC_SWAP", 1) != 0;
-    const u64 plane_bytes = h->tc_swap ? (tp + tc::kKB - 1) / tc::kKB * 2 * tc::kGBytes : nrblk * 2 * tc::kRBytes;
+    const u64 plane_bytes = h->tc_swap ? (tp + tc::kKB - 1) / tc::kKB * tc::kGBytes : nrblk * 2 * tc::kRBytes;
     const u64 tc_bytes = (u64)tc::kCRec * 8 * tp + 16 * tp + plane_bytes;
     const u64 cap = (u64)std::max(0, env_int("PE_TC_MEM_MB", 0)) << 20;
     int rc = PE_OK;
@@ -616,8 +612,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
         else tc::k_tc_setup<false><<<grid_for(tp, 256), 256, 0, s2>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
         const u64 nrp = (tp + 2 * tc::kKB - 1) / (2 * tc::kKB);   // blocks of 2 K-blocks
         const unsigned rpg = (unsigned)std::max<u64>(1, std::min<u64>(nrp, 148ull * 16));
-        const u64 ngp = 2 * ((tp + tc::kKB - 1) / tc::kKB);        // one (K-block, half) per block
-        const unsigned gpg = (unsigned)std::max<u64>(1, std::min<u64>(ngp, 148ull * 32));
+        const u64 ngp = 2 * ((tp + tc::kKB - 1) / tc::kKB);        // warp tasks (K-block, K half)
+        const unsigned gpg = (unsigned)std::max<u64>(1, std::min<u64>((ngp + 7) / 8, 148ull * 8));
         if (h->tc_swap && h->p < (1ull << 62))
           tc::k_tc_gplanes<true><<<gpg, tc::kGpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
         else if (h->tc_swap)
@@ -670,15 +666,12 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
   if (h->tc_ok) {
     h->split_g1 = tc_row_split(h);
     const u64 ranges[3][2] = {{0, h->G}, {0, h->split_g1}, {h->split_g1, h->G}};
-    const u32 shapes[3] = {1, 2, 1 | kPairBit};   // chunks per pass; the pair kernel's 16384-point pass
-    for (u32 nch : shapes) {
-      if ((nch & kPairBit) && !h->tc_swap) continue;
+    for (u32 nch = 1; nch <= 2; ++nch)
       for (auto& r : ranges) {
         if (r[0] >= r[1]) continue;
         pe_ctx::TcPlan* P = nullptr;
         if (tc_plan(h, nch, r[0], r[1], true, s, &P)) return g_last_error;
       }
-    }
   }
   if (h->fast_mode == 2) {
     const int rc = fast::create(h->h_poff, h->mp, s, &h->fast);
@@ -858,9 +851,8 @@ static int ensure_partial(pe_ctx* h, size_t need, cudaStream_t s) {
 // rest -- the round-1 snake order's property).  env PE_TC_PIECE (terms) / PE_TC_UPC override.
 static const u32 kUnitsPerCta = 6;
 // Largest piece (K-blocks) of a plan for rows [g0, g1) and nch chunks.
-static u64 tc_maxkb(const pe_ctx* h, u32 nch_in, u64 g0, u64 g1) {
-  const u32 nch = nch_in & ~kPairBit;
-  const u64 n_w = tc_workers(h, nch_in);
+static u64 tc_maxkb(const pe_ctx* h, u32 nch, u64 g0, u64 g1) {
+  const u64 n_w = (u64)h->n_sm;
   const u64 tkb = (h->h_poff[g1] - h->h_poff[g0]) / tc::kKB;
   const u32 rounds = h->tc_rounds;
   u64 maxkb;
@@ -884,16 +876,15 @@ static u64 tc_nslots(const pe_ctx* h, u32 nch, u64 g0, u64 g1) {
   return n * h->tc_rounds;
 }
 // Rows [g0, g1) only (pe_eval's row blocks): pieces of those buckets, slots numbered from 0.
-static int tc_plan(const pe_ctx* h, u32 nch_in, u64 g0, u64 g1, bool upload, cudaStream_t s, pe_ctx::TcPlan** out) {
-  const auto key = std::make_tuple(nch_in, g0, g1);
-  const u32 nch = nch_in & ~kPairBit;
+static int tc_plan(const pe_ctx* h, u32 nch, u64 g0, u64 g1, bool upload, cudaStream_t s, pe_ctx::TcPlan** out) {
+  const auto key = std::make_tuple(nch, g0, g1);
   auto it = h->tc_plans.find(key);
   pe_ctx::TcPlan* P = nullptr;
   if (it == h->tc_plans.end()) {
     P = &h->tc_plans[key];
     const u64 G = g1 - g0;
     const u32 rounds = h->tc_rounds;
-    const u64 maxkb = tc_maxkb(h, nch_in, g0, g1);
+    const u64 maxkb = tc_maxkb(h, nch, g0, g1);
     std::vector<u32> slot(G + 1);
     for (u64 gg = 0; gg < G; ++gg) {
       const u64 g = g0 + gg;
@@ -917,7 +908,7 @@ static int tc_plan(const pe_ctx* h, u32 nch_in, u64 g0, u64 g1, bool upload, cud
     P->slot_start = std::move(slot);
     // schedule
     const u32 upp = nch * rounds, nunits = P->npieces * upp;
-    const u32 grid = (u32)std::min<u64>(nunits, (u64)tc_workers(h, nch_in));   // CTAs, or clusters
+    const u32 grid = (u32)std::min<u64>(nunits, (u64)h->n_sm);
     P->grid = grid;
     std::vector<std::pair<u64, u32>> heap;   // (load, cta), min-heap
     for (u32 b = 0; b < grid; ++b) heap.push_back({0, b});
@@ -1046,42 +1037,15 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s,
   }
   const int tc_smem = env_int("PE_TC_EXCLUSIVE", 1) ? smem_dyn : (int)tc::kSmemBytes;
   for (const void* f : tc_fns) CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem));
-  int tc2_smem = (int)tc2::kSmemBytes2;
-  if (h->tc_swap) {
-    const void* f2[2] = {(const void*)tc2::k_tc2<4>, (const void*)tc2::k_tc2<5>};
-    if (env_int("PE_TC_EXCLUSIVE", 1)) {
-      int optin = 0;
-      CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-      size_t st = 0;
-      for (const void* f : f2) {
-        cudaFuncAttributes fa;
-        CU(cudaFuncGetAttributes(&fa, f));
-        st = std::max(st, fa.sharedSizeBytes);
-      }
-      tc2_smem = std::max<int>(tc2_smem, optin - (int)st);
-    }
-    for (const void* f : f2) CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2_smem));
-  }
-  // the CTA-pair kernel (tc2.cuh) for the swapped form when a pass has an even number of chunks
-  // (PE_TC_PAIR=0: never)
-  const bool pair_ok = h->tc_swap && env_int("PE_TC_PAIR", 1) != 0;
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
     const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
-    const bool pair = pair_ok && nch % 2 == 0;
-    const u32 nch_k = pair ? nch / 2 : nch;   // the kernel's chunks: 16384-point pair chunks or 8192-point
-    if (pair) {
-      const u64 nseed = (q1 - q0) * nch_k;
-      tc2::k_tc_seed2<<<grid_for(nseed, 256), 256, 0, s>>>(h->d_c, h->d_m, h->t_pad, q0, q1, nch_k, j0 + k0,
-                                                           h->d_seed, h->mp);
-    } else {
-      const u64 nseed = (q1 - q0) * ((nch + tc::kSeedChunks - 1) / tc::kSeedChunks);
-      tc::k_tc_seed<<<grid_for(nseed, 256), 256, 0, s>>>(h->d_c, h->d_m, h->d_tcMS, h->t_pad, q0, q1, nch, j0 + k0,
-                                                         h->d_seed, h->mp);
-    }
+    const u64 nseed = (q1 - q0) * ((nch + tc::kSeedChunks - 1) / tc::kSeedChunks);
+    tc::k_tc_seed<<<grid_for(nseed, 256), 256, 0, s>>>(h->d_c, h->d_m, h->d_tcMS, h->t_pad, q0, q1, nch, j0 + k0,
+                                                       h->d_seed, h->mp);
     CU(cudaGetLastError());
     pe_ctx::TcPlan* P = nullptr;
-    if (tc_plan(h, pair ? nch_k | kPairBit : nch, g0, g1, true, s, &P)) return g_last_error;
+    if (tc_plan(h, nch, g0, g1, true, s, &P)) return g_last_error;
     CU(cudaStreamWaitEvent(s, P->uploaded, 0));
     tc::TcArgs a;
     a.LS = h->d_seed;
@@ -1094,8 +1058,8 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s,
     a.t_pad = h->t_pad;
     a.npieces = P->npieces;
     a.rounds = h->tc_rounds;
-    a.nunits = P->npieces * nch_k * a.rounds;
-    a.nch = nch_k;
+    a.nunits = P->npieces * nch * a.rounds;
+    a.nch = nch;
     a.npts = np;
     for (int d = 0; d < 15; ++d) a.Wd[d] = h_powmod(2, 8 * (u64)d, h->p);
     a.C128 = h_powmod(2, 128, h->p);
@@ -1129,9 +1093,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s,
       CU(cudaMemset(d_prof, 0, nprof * sizeof(unsigned long long)));
       a.prof = d_prof;
     }
-    if (pair && mode == 4) tc2::k_tc2<4><<<2 * grid, tc2::kThreads2, tc2_smem, s>>>(a);
-    else if (pair) tc2::k_tc2<5><<<2 * grid, tc2::kThreads2, tc2_smem, s>>>(a);
-    else if (d_prof && mode == 0) tc::k_tc<true, 0><<<grid, tc::kThreads, tc_smem, s>>>(a);
+    if (d_prof && mode == 0) tc::k_tc<true, 0><<<grid, tc::kThreads, tc_smem, s>>>(a);
     else if (d_prof && mode == 4) tc::k_tc<true, 4><<<grid, tc::kThreads, tc_smem, s>>>(a);
     else if (mode == 4) tc::k_tc<false, 4><<<grid, tc::kThreads, tc_smem, s>>>(a);
     else if (mode == 5) tc::k_tc<false, 5><<<grid, tc::kThreads, tc_smem, s>>>(a);

@@ -99,24 +99,15 @@ static_assert(kSmemBytes + 256 <= 232448, "shared memory");
 // one wide MMA (B = planes t..t+k-1, N = 64k <= 256) covers k of them
 // group 2: the single round of the 4-digit mode (p < 2^31: values < 2^32), d = 0..6
 // group 4: the 7-digit mode's second round, d = 8..12
-// groups 5 / 6: the CTA-pair kernel's (tc2.cuh) balanced rounds, 32 digit pairs each --
-// d = {0, 1, 6, 7, 8, 9, 14} and d = {2, 3, 4, 5, 10, 11, 12, 13} -- so the two rounds of a piece
-// take equal time and, running side by side, share its giant-step planes through L2
 __host__ __device__ constexpr int group_diag(int g, int di) {
-  return g == 0 ? di
-       : g == 1 ? (di < 7 ? 8 + di : -1)
-       : g == 2 ? (di < 7 ? di : -1)
-       : g == 5 ? (di < 2 ? di : di < 6 ? 4 + di : di == 6 ? 14 : -1)
-       : g == 6 ? (di < 4 ? 2 + di : 6 + di)
-       : (di < 5 ? 8 + di : -1);
+  return g == 0 ? di : g == 1 ? (di < 7 ? 8 + di : -1) : g == 2 ? (di < 7 ? di : -1) : (di < 5 ? 8 + di : -1);
 }
 
 struct TcArgs {
   const u64* LS;         // [nch][t_pad] chunk seeds c m^{j_s}
   const u64* C;          // [t_pad][10] C records (giant-step chain multiplier, m^{rr V} table)
   const uint8_t* Rp;     // [t_pad / 32][kRBytes] baby-step byte planes (k_tc_rplanes), MODE 0-3
-  const uint8_t* Gp;     // [t_pad / 32][2][kGBytes] giant-step byte planes, u < 128 then 128 <= u < 256
-                         // (k_tc_gplanes), MODE 4-5; the single-CTA kernel reads the first half
+  const uint8_t* Gp;     // [t_pad / 32][kGBytes] giant-step byte planes (k_tc_gplanes), MODE 4-5
   const uint4* piece;    // x = first padded term, y = K-blocks, z = partial slot (sorted by size desc)
   const u32* sched;      // units of CTA b: sched[sched_off[b] .. sched_off[b+1])  (host LPT schedule)
   const u32* sched_off;  // [gridDim.x + 1]
@@ -786,7 +777,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
           mbar_arrive(&full[stage]);
         } else if (SW) {
           mbar_expect_tx(&full[stage], kGBytes);
-          bulk_g2s(stage0, a.Gp + ((u64)cur.q0 / kKB + cur.kb) * 2 * kGBytes, kGBytes, &full[stage]);
+          bulk_g2s(stage0, a.Gp + ((u64)cur.q0 / kKB + cur.kb) * kGBytes, kGBytes, &full[stage]);
         } else {
           mbar_expect_tx(&full[stage], kRBytes);
           bulk_g2s(stage0 + 8 * kPlaneA, a.Rp + ((u64)cur.q0 / kKB + cur.kb) * kRBytes, kRBytes, &full[stage]);
@@ -1029,59 +1020,64 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
 }
 
 // Per handle, swapped form (MODE 4 / 5): the giant-step byte planes G_s[i][u] = byte s of the
-// Montgomery residue m_i^{uV} 2^64 mod p for u < 2U (the CTA-pair kernel's M = 256 rows; the
-// single-CTA kernel uses u < U), in the A layout of a stage: [K-block][half h: u = 128h ..][32 KB].
-// Block = one (K-block, half), 2 warps (one per K half); lane = (4 terms, rows r + 8j, j < 16): 4
-// chains of stride 8 with the fixed multiplier m^{8V} (Shoup); the block leaves with 16-byte stores.
-constexpr int kGpThreads = 64;
+// Montgomery residue m_i^{uV} 2^64 mod p (u < U) in the A layout of each K-block's stage (32 KB).
+// Warp task = (K-block, K half): lane = (ql: 4 terms, r: rows r + 8j, j < 16), 4 chains of stride 8
+// with the fixed multiplier m^{8V} (Shoup).  A warp's store of one plane word covers 8 rows x 16
+// bytes = one 128-byte line, so the planes go straight to global memory.  The per-term powers
+// m^V, m^{2V}, m^{4V}, m^{8V} are computed once per term (lane r < 4 of the term's group) and
+// shuffled to the group's 8 lanes.
+constexpr int kGpThreads = 256;
 template <bool LAZY>
 static __global__ void __launch_bounds__(kGpThreads) k_tc_gplanes(const u64* __restrict__ m, u64 t_pad,
                                                                   uint8_t* __restrict__ Gp, ModParams mp) {
-  __shared__ __align__(16) uint8_t st[kGBytes];
-  const u64 nblk = 2 * ((t_pad + kKB - 1) / kKB);   // (K-block, half) pairs
-  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const u64 ntask = 2 * ((t_pad + kKB - 1) / kKB);
+  const int lane = threadIdx.x & 31;
   const u32 ql = (u32)(lane >> 3), r = (u32)(lane & 7);
-  const u32 base = plane_off<kLBOA>(r, (u32)h * 16 + ql * 4);
-  for (u64 blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-    const u32 half = (u32)(blk & 1);
-    const u64 q0 = (blk >> 1) * kKB + (u64)h * 16 + ql * 4;
+  const u64 nwarp = (u64)gridDim.x * (kGpThreads / 32);
+  for (u64 task = (u64)blockIdx.x * (kGpThreads / 32) + (threadIdx.x >> 5); task < ntask; task += nwarp) {
+    const u64 blk = task >> 1;
+    const u32 h = (u32)(task & 1);
+    const u64 q0 = blk * kKB + (u64)h * 16 + ql * 4;
+    // lane (ql, r): powers of term q0 + (r & 3)
+    const u64 q = q0 + (r & 3);
+    const u64 mm = to_mont(q < t_pad ? m[q] : 0ull, mp);
+    u64 mV = mm;
+#pragma unroll 1
+    for (int i = 0; i < 6; ++i) mV = mont_mul(mV, mV, mp);   // m^V, V = 64
+    const u64 m2V = mont_mul(mV, mV, mp), m4V = mont_mul(m2V, m2V, mp);
+    const u64 m8V = mont_mul(m4V, m4V, mp);
     u64 y[4], mS[4], wS[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const u64 mm = to_mont(q0 + e < t_pad ? m[q0 + e] : 0ull, mp);
-      u64 mV = mm;
-#pragma unroll 1
-      for (int i = 0; i < 6; ++i) mV = mont_mul(mV, mV, mp);   // m^V, V = 64
-      const u64 m2V = mont_mul(mV, mV, mp), m4V = mont_mul(m2V, m2V, mp);
-      const u64 m8V = mont_mul(m4V, m4V, mp);
-      mS[e] = from_mont(m8V, mp);                        // normal m^{8V}: the chain's fixed multiplier
-      wS[e] = m8V * mp.pinv;                             // its Shoup constant
+      const int src = (int)(ql * 8) + e;
+      const u64 v1 = __shfl_sync(0xffffffffu, mV, src), v2 = __shfl_sync(0xffffffffu, m2V, src);
+      const u64 v4 = __shfl_sync(0xffffffffu, m4V, src), v8 = __shfl_sync(0xffffffffu, m8V, src);
+      mS[e] = from_mont(v8, mp);                         // normal m^{8V}: the chain's fixed multiplier
+      wS[e] = v8 * mp.pinv;                              // its Shoup constant
       u64 x = mp.r1;
-      if (r & 1) x = mV;
-      if (r & 2) x = mont_mul(x, m2V, mp);
-      if (r & 4) x = mont_mul(x, m4V, mp);
-      if (half) {                                        // x m^{128 V} = x (m^{8V})^16
-        u64 t = m8V;
-#pragma unroll 1
-        for (int i = 0; i < 4; ++i) t = mont_mul(t, t, mp);
-        x = mont_mul(x, t, mp);
-      }
-      y[e] = x;                                          // m^{(128 half + r) V} (Montgomery residue)
+      if (r & 1) x = v1;
+      if (r & 2) x = mont_mul(x, v2, mp);
+      if (r & 4) x = mont_mul(x, v4, mp);
+      y[e] = x;                                          // m^{rV} (Montgomery residue)
     }
+    uint8_t* dst = Gp + blk * kGBytes + plane_off<kLBOA>(r, h * 16 + ql * 4);
 #pragma unroll 1
     for (u32 j = 0; j < (u32)kU / 8; ++j) {              // row r + 8j
-      store_digits<kPlaneA>(smem_u32(st) + base + j * 128u, y);
+      const u32 l0 = lo32(y[0]), l1 = lo32(y[1]), l2 = lo32(y[2]), l3 = lo32(y[3]);
+      const u32 h0 = hi32(y[0]), h1 = hi32(y[1]), h2 = hi32(y[2]), h3 = hi32(y[3]);
+      u32 wd[8];
+      u32 a = prmt(l0, l1, 0x5140), b = prmt(l2, l3, 0x5140), c = prmt(l0, l1, 0x7362), d = prmt(l2, l3, 0x7362);
+      wd[0] = prmt(a, b, 0x5410); wd[1] = prmt(a, b, 0x7632); wd[2] = prmt(c, d, 0x5410); wd[3] = prmt(c, d, 0x7632);
+      a = prmt(h0, h1, 0x5140); b = prmt(h2, h3, 0x5140); c = prmt(h0, h1, 0x7362); d = prmt(h2, h3, 0x7362);
+      wd[4] = prmt(a, b, 0x5410); wd[5] = prmt(a, b, 0x7632); wd[6] = prmt(c, d, 0x5410); wd[7] = prmt(c, d, 0x7632);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) *(u32*)(dst + (u32)t * kPlaneA + j * 128u) = wd[t];
       if (j + 1 < (u32)kU / 8) {
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           y[e] = LAZY ? mul_shoup4(y[e], mS[e], wS[e], mp.np) : mul_shoup2(y[e], mS[e], wS[e], mp.np);
       }
     }
-    __syncthreads();
-    uint4* dst = (uint4*)(Gp + blk * kGBytes);
-    const uint4* src = (const uint4*)st;
-    for (u32 i = threadIdx.x; i < kGBytes / 16; i += kGpThreads) dst[i] = src[i];
-    __syncthreads();
   }
 }
 

@@ -254,3 +254,20 @@ def test_tc_7digit_mode_equals_scalar_step():
     assert np.array_equal(a, b)
     ks = np.array([0, 1, 8191, 8192, 8999], np.uint64)
     assert np.array_equal(a[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
+
+
+@pytest.mark.parametrize("p", [P62, (1 << 54) + 159, (1 << 62) + 135, (1 << 63) - 25])
+@pytest.mark.parametrize("swap", ["0", "1"])
+def test_tc_plain_and_swapped_forms(monkeypatch, p, swap):
+    """For 8-digit primes (p >= 2^54) the default is the swapped form (giant-step planes built per
+    handle, baby steps c m^{j_s + v} generated per unit, tc.cuh MODE 4 / 5); PE_TC_SWAP=0 keeps the
+    plain form (baby-step planes per handle, giant steps generated, MODE 0 / 1).  Both equal the
+    direct oracle on sampled columns and the incremental checker in full, across a ragged third
+    chunk, lazy (p < 2^62) and exact (p >= 2^62) chains."""
+    monkeypatch.setenv("PE_TC_SWAP", swap)
+    w = synth.random_small(590 + p % 97, p, 7, 3000, 5, 2 * 8192 + 777, 11)
+    _, out = tc_eval(w)
+    ref = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
+    assert np.array_equal(out, ref)
+    ks = np.array([0, 8191, 8192, w.T - 1], np.uint64)
+    assert np.array_equal(out[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
