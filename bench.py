@@ -209,9 +209,10 @@ def workload_config(w):
     """The workload only (identical in both arms); implementation details go to impl_config."""
     return {"workload": w.name, "t": w.t, "n": w.n, "T": w.T, "j0": w.j0, "p": w.p,
             "term_points_per_step": w.t * w.T,
-            "l2": ("inputs larger than L2 (126 MB): the tensor-core step streams 5.2 GB of baby-step "
-                   "planes + 0.8 GB of per-term records per launch (config 5); the scalar step reads "
-                   "c, m, w (3 x 8 B x t_padded)")}
+            "l2": ("inputs larger than L2 (126 MB): the tensor-core step streams the handle's 10 GB of "
+                   "giant-step planes (1 KB per term; 0.5 KB of baby-step planes in the plain form) + "
+                   "0.8 GB of per-term records per launch (config 5); the scalar step reads c, m, w "
+                   "(3 x 8 B x t_padded)")}
 
 
 def impl_config(info):
