@@ -610,8 +610,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
       if (rc == PE_OK) {
         if (h->tc_swap) tc::k_tc_setup<true><<<grid_for(tp, 256), 256, 0, s2>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
         else tc::k_tc_setup<false><<<grid_for(tp, 256), 256, 0, s2>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
-        const u64 nrp = (tp + 2 * tc::kKB - 1) / (2 * tc::kKB);   // blocks of 2 K-blocks
-        const unsigned rpg = (unsigned)std::max<u64>(1, std::min<u64>(nrp, 148ull * 16));
+        const u64 nrp = 4 * ((tp + 2 * tc::kKB - 1) / (2 * tc::kKB));   // warp tasks (K-block, K half)
+        const unsigned rpg = (unsigned)std::max<u64>(1, std::min<u64>((nrp + 7) / 8, 148ull * 8));
         const u64 ngp = 2 * ((tp + tc::kKB - 1) / tc::kKB);        // warp tasks (K-block, K half)
         const unsigned gpg = (unsigned)std::max<u64>(1, std::min<u64>((ngp + 7) / 8, 148ull * 8));
         if (h->tc_swap && h->p < (1ull << 62))

@@ -961,39 +961,46 @@ static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __r
 
 // Per handle (pe_create): the baby-step byte planes R_t[i][v] = byte t of the Montgomery residue
 // m_i^v 2^64 mod p (v < V) in the stage layout of each K-block (any representative < 2^64 gives
-// exact byte products; the epilogue's REDC removes the 2^64).  Block = 2 K-blocks staged in
-// shared memory; thread = (4 terms, rows r + 8j): one warp's stores cover 8 consecutive rows x
-// 16 bytes, and the block leaves with 16-byte coalesced stores.
-constexpr int kRpThreads = 128;
+// exact byte products; the epilogue's REDC removes the 2^64).  Warp task = (K-block, K half):
+// lane = (ql: 4 terms, r: rows r + 8j, j < 8); a warp's store of one plane word covers 8 rows x 16
+// bytes = one 128-byte line, so the planes go straight to global memory.  m, m^2, m^4, m^8 of a
+// term are computed once (lane r < 4 of the term's group) and shuffled to the group's 8 lanes.
 // The stride-8 chain of a lane (rows r, r + 8, ...) multiplies by the fixed m^8 with Shoup products
 // (its constant is m8_mont * (-p^-1) mod 2^64, modcore.cuh shoup_w_fast): any representative below
 // 2^digits is exact for the MMAs, so LAZY chains (values < 4p) serve 2^31 <= p < 2^62 (8 digits, or 7
 // when p < 2^54: 4p < 2^56) and exact-quotient ones (< 2p) the 4-digit (p < 2^31) and p >= 2^62 modes.
+constexpr int kRpThreads = 256;
 template <bool LAZY>
 static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __restrict__ m, u64 t_pad,
                                                                   uint8_t* __restrict__ Rp, ModParams mp) {
-  __shared__ __align__(16) uint8_t st[2 * kRBytes];
-  const u64 nblk = (t_pad + 2 * kKB - 1) / (2 * kKB);   // Rp is allocated for a whole last block
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const u64 nkb = 2 * ((t_pad + 2 * kKB - 1) / (2 * kKB));   // Rp is allocated for whole pairs of K-blocks
+  const u64 ntask = 2 * nkb;
+  const int lane = threadIdx.x & 31;
   const u32 ql = (u32)(lane >> 3), r = (u32)(lane & 7);
-  const u32 kbl = (u32)warp >> 1, h = (u32)warp & 1;
-  const u32 base = kbl * kRBytes + h * kLBOB + r * 16u + ql * 4u;
-  for (u64 blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-    const u64 q0 = blk * 2 * kKB + kbl * kKB + h * 16 + ql * 4;
+  const u64 nwarp = (u64)gridDim.x * (kRpThreads / 32);
+  for (u64 task = (u64)blockIdx.x * (kRpThreads / 32) + (threadIdx.x >> 5); task < ntask; task += nwarp) {
+    const u64 blk = task >> 1;
+    const u32 h = (u32)(task & 1);
+    const u64 q0 = blk * kKB + (u64)h * 16 + ql * 4;
+    const u64 q = q0 + (r & 3);
+    const u64 mm = to_mont(q < t_pad ? m[q] : 0ull, mp);
+    const u64 m2 = mont_mul(mm, mm, mp), m4 = mont_mul(m2, m2, mp);
+    const u64 m8m = mont_mul(m4, m4, mp);                // Montgomery m^8 = m^8 2^64 mod p
     u64 y[4], m8[4], w8[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const u64 mm = to_mont(q0 + e < t_pad ? m[q0 + e] : 0ull, mp);
-      const u64 m2 = mont_mul(mm, mm, mp), m4 = mont_mul(m2, m2, mp);
-      const u64 m8m = mont_mul(m4, m4, mp);              // Montgomery m^8 = m^8 2^64 mod p
-      m8[e] = from_mont(m8m, mp);                        // normal m^8: the chain's fixed multiplier
-      w8[e] = m8m * mp.pinv;                             // its Shoup constant floor(m^8 2^64 / p)
+      const int src = (int)(ql * 8) + e;
+      const u64 v1 = __shfl_sync(0xffffffffu, mm, src), v2 = __shfl_sync(0xffffffffu, m2, src);
+      const u64 v4 = __shfl_sync(0xffffffffu, m4, src), v8 = __shfl_sync(0xffffffffu, m8m, src);
+      m8[e] = from_mont(v8, mp);                         // normal m^8: the chain's fixed multiplier
+      w8[e] = v8 * mp.pinv;                              // its Shoup constant floor(m^8 2^64 / p)
       u64 x = mp.r1;                                     // Montgomery 1 = m^0
-      if (r & 1) x = mm;
-      if (r & 2) x = mont_mul(x, m2, mp);
-      if (r & 4) x = mont_mul(x, m4, mp);
+      if (r & 1) x = v1;
+      if (r & 2) x = mont_mul(x, v2, mp);
+      if (r & 4) x = mont_mul(x, v4, mp);
       y[e] = x;                                          // m^r (Montgomery residue)
     }
+    uint8_t* dst = Rp + blk * kRBytes + h * kLBOB + r * 16u + ql * 4u;
 #pragma unroll 1
     for (u32 j = 0; j < (u32)kV / 8; ++j) {              // row r + 8j
       const u32 l0 = lo32(y[0]), l1 = lo32(y[1]), l2 = lo32(y[2]), l3 = lo32(y[3]);
@@ -1004,18 +1011,13 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
       a = prmt(h0, h1, 0x5140); b = prmt(h2, h3, 0x5140); c = prmt(h0, h1, 0x7362); d = prmt(h2, h3, 0x7362);
       wd[4] = prmt(a, b, 0x5410); wd[5] = prmt(a, b, 0x7632); wd[6] = prmt(c, d, 0x5410); wd[7] = prmt(c, d, 0x7632);
 #pragma unroll
-      for (int t = 0; t < 8; ++t) *(u32*)(st + base + (u32)t * kPlaneB + j * 128u) = wd[t];
+      for (int t = 0; t < 8; ++t) *(u32*)(dst + (u32)t * kPlaneB + j * 128u) = wd[t];
       if (j + 1 < (u32)kV / 8) {                         // row r + 8(j+1) = row r + 8j times m^8
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           y[e] = LAZY ? mul_shoup4(y[e], m8[e], w8[e], mp.np) : mul_shoup2(y[e], m8[e], w8[e], mp.np);
       }
     }
-    __syncthreads();
-    uint4* dst = (uint4*)(Rp + blk * 2 * kRBytes);
-    const uint4* src = (const uint4*)st;
-    for (u32 i = threadIdx.x; i < 2 * kRBytes / 16; i += kRpThreads) dst[i] = src[i];
-    __syncthreads();
   }
 }
 
