@@ -13,8 +13,7 @@ value  = t*T / device time per step (max over ranks), inputs resident in HBM.
 e2e    = the same metric through the C ABI from pinned HOST inputs to a HOST result:
          pe_create (H2D of coeffs/exps/alpha + device planning + K1) + pe_eval(_device)
          + gather + D2H of the G x T result, every step, one polynomial at a time; the same with
-         uint8 exponents (pe_create_compact) under e2e.compact_exponents, whose "pipelined" entry is
-         a stream of polynomials with two in flight (the next one's create on a host thread).
+         uint8 exponents (pe_create_compact) under e2e.compact_exponents.
 roofline = the dominant kernel.  Tensor-core path (default for config 5): k_tc's int8 tensor
          ops per launch (128 per term-point: 64 exact byte-pair MACs) / its CUDA-event launch
          time vs the int8 dense peak (2 x measured bf16), plus the tcgen05 i8 issue rate of the
@@ -389,46 +388,6 @@ def main():
                     ts.append(max_over_ranks(time.perf_counter() - t0))
                 return statistics.median(ts)
 
-            def pipelined(compact=False, k=None):
-                # throughput: a stream of polynomials, two in flight -- polynomial i+1's pe_create
-                # (its PCIe upload, sort and setup) runs on a host thread while polynomial i is
-                # evaluated and its result copied back; the libpe calls release the GIL (ctypes)
-                from concurrent.futures import ThreadPoolExecutor
-                k = k or max(6, min(args.steps, 10))
-
-                trace = os.environ.get("BENCH_E2E_TRACE") == "1"
-
-                def timed_create():
-                    a = time.perf_counter()
-                    h = create_h(compact)
-                    return h, a, time.perf_counter()
-
-                def run(n):
-                    marks = []
-                    fut = ex.submit(timed_create)
-                    for i in range(n):
-                        h, ca, cb = fut.result()
-                        if i + 1 < n:
-                            fut = ex.submit(timed_create)
-                        ea = time.perf_counter()
-                        eval_h(h)
-                        marks.append(time.perf_counter())
-                        if trace:
-                            log(f"e2e trace: create {1e3 * (cb - ca):.2f} wait {1e3 * (ea - max(cb, marks[-2] if i else ea)):.2f} "
-                                f"eval+destroy {1e3 * (marks[-1] - ea):.2f} ms")
-                    return marks
-
-                with ThreadPoolExecutor(1) as ex:
-                    run(3)                     # warm-up: the memory pool grows to two handles in flight
-                    barrier()
-                    torch.cuda.synchronize()
-                    t0 = time.perf_counter()
-                    marks = run(k)
-                    torch.cuda.synchronize()
-                    dt = max_over_ranks(time.perf_counter() - t0) / k
-                steps = [1e3 * (b - a) for a, b in zip([t0] + marks[:-1], marks)]
-                return dt, k, steps
-
             h_e8 = None
             if world == 1 and int(w.exps.max()) < 256:
                 h_e8 = torch.from_numpy(np.ascontiguousarray(w.exps.astype(np.uint8))).pin_memory()
@@ -438,16 +397,10 @@ def main():
             e2e_c = None
             if h_e8 is not None:
                 ec = serial(True)
-                ecp, kp, ec_steps = pipelined(True)
                 e2e_c = {"value": w.t * w.T / ec, "unit": UNIT, "ms_per_step": 1e3 * ec,
                          "h2d_bytes_per_step": w.coeffs.nbytes + h_e8.numel() + w.alpha.nbytes,
                          "d2h_bytes_per_step": ctx.G * w.T * 8,
-                         "includes": "pe_create_compact (uint8 exponents) + pe_eval, host wall clock",
-                         "pipelined": {"value": w.t * w.T / ecp, "ms_per_step": 1e3 * ecp,
-                                       "step_ms": [round(x, 2) for x in ec_steps],
-                                       "how": f"{kp} polynomials back to back, two in flight: pe_create_compact "
-                                              "of the next on a host thread while the current one is evaluated "
-                                              "and copied back"}}
+                         "includes": "pe_create_compact (uint8 exponents) + pe_eval, host wall clock"}
             # the host result of the last e2e polynomial must equal the device-timed path's output
             ref = step()
             torch.cuda.synchronize()
