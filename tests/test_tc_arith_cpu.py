@@ -102,3 +102,33 @@ def test_shoup_constant_identity():
         for m in [0, 1, p - 1] + [rnd.randrange(p) for _ in range(200)]:
             rem = (m << 64) % p
             assert (rem * ninv) % (1 << 64) == (m << 64) // p
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_swapped_form_reduction(seed):
+    """The swapped form (tc.cuh MODE 4 / 5): A = giant steps G[u] = m^{64u} as Montgomery residues
+    m^{64u} 2^64 mod p (point-independent, built per handle), B = baby steps R'[v] = c m^{j_s + v}
+    (lazy representatives < 4p from the Shoup chains).  The same diagonals, round split and
+    REDC give sum_i c_i m_i^{j_s + 64u + v} mod p: the byte identity does not care which side
+    carries the point-dependent factor."""
+    rng = random.Random(200 + seed)
+    p = P62
+    R64 = (1 << 64) % p
+    n = 48
+    c = [rng.randrange(p) for _ in range(n)]
+    m = [rng.randrange(1, p) for _ in range(n)]
+    js, u, v = rng.randrange(1, 1 << 40), rng.randrange(128), rng.randrange(64)
+    Gs = [(pow(mi, 64 * u, p) * R64) % p for mi in m]
+    Bs = [(ci * pow(mi, js + v, p)) % p + rng.randrange(4) * p for ci, mi in zip(c, m)]
+    Bs = [x if x < (1 << 64) else x - p for x in Bs]
+    want = sum(ci * pow(mi, js + 64 * u + v, p) for ci, mi in zip(c, m)) % p
+    D = diagonals(Gs, Bs)
+    total = 0
+    for rnd in (range(0, 8), range(8, 15)):
+        X = sum(D[d] << (8 * d) for d in rnd)
+        x = [(X >> (32 * k)) & 0xFFFFFFFF for k in range(5)]
+        acc = x[0] | (x[1] << 32)
+        for k in (2, 3, 4):
+            acc += x[k] * pow(2, 32 * k, p)
+        total += redc((acc >> 64) % p, acc & ((1 << 64) - 1), p)
+    assert total % p == want
