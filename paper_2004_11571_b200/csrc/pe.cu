@@ -596,9 +596,18 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
   if (h->tc_mode != 0 && (h->path == kInt4 || h->path == kInt2 || h->path == kFp64 || h->path == kInt32)) {
     const u64 tp = h->t_pad;
     prof.mark("k_setup (+copies)", s);
-    // the C records (k_tc_setup) and the baby-step planes (k_tc_rplanes) both depend only on m:
-    // the former runs on a side stream beside the latter
-    {
+    // swapped form: one kernel writes the giant-step planes, the C records and the seed powers.
+    // Plain form: the C records (k_tc_setup) and the baby-step planes (k_tc_rplanes) both depend
+    // only on m; the former runs on a side stream beside the latter.
+    if (h->tc_swap) {
+      const u64 ngp = 2 * ((tp + tc::kKB - 1) / tc::kKB);        // warp tasks (K-block, K half)
+      const unsigned gpg = (unsigned)std::max<u64>(1, std::min<u64>((ngp + 7) / 8, 148ull * 8));
+      if (h->p < (1ull << 62))
+        tc::k_tc_gplanes<true><<<gpg, tc::kGpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->d_tcC, h->d_tcMS, h->mp);
+      else
+        tc::k_tc_gplanes<false><<<gpg, tc::kGpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->d_tcC, h->d_tcMS, h->mp);
+      CU(cudaGetLastError());
+    } else {
       cudaStream_t s2 = nullptr;
       cudaEvent_t e_m = nullptr, e_done = nullptr;
       CU(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
@@ -608,17 +617,10 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
           cudaEventRecord(e_m, s) != cudaSuccess || cudaStreamWaitEvent(s2, e_m, 0) != cudaSuccess)
         rc = PE_ECUDA;
       if (rc == PE_OK) {
-        if (h->tc_swap) tc::k_tc_setup<true><<<grid_for(tp, 256), 256, 0, s2>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
-        else tc::k_tc_setup<false><<<grid_for(tp, 256), 256, 0, s2>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
+        tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s2>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
         const u64 nrp = 4 * ((tp + 2 * tc::kKB - 1) / (2 * tc::kKB));   // warp tasks (K-block, K half)
         const unsigned rpg = (unsigned)std::max<u64>(1, std::min<u64>((nrp + 7) / 8, 148ull * 8));
-        const u64 ngp = 2 * ((tp + tc::kKB - 1) / tc::kKB);        // warp tasks (K-block, K half)
-        const unsigned gpg = (unsigned)std::max<u64>(1, std::min<u64>((ngp + 7) / 8, 148ull * 8));
-        if (h->tc_swap && h->p < (1ull << 62))
-          tc::k_tc_gplanes<true><<<gpg, tc::kGpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
-        else if (h->tc_swap)
-          tc::k_tc_gplanes<false><<<gpg, tc::kGpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
-        else if (h->p >= (1ull << 31) && h->p < (1ull << 62))
+        if (h->p >= (1ull << 31) && h->p < (1ull << 62))
           tc::k_tc_rplanes<true><<<rpg, tc::kRpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
         else
           tc::k_tc_rplanes<false><<<rpg, tc::kRpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);

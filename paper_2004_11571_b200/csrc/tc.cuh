@@ -937,21 +937,18 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
 // Per padded term (pe_create): the C record -- the giant-step chain multiplier m^{8V} (stride 8
 // rows of L), its Shoup constant and the Montgomery table m^{rr V} (rr < 8) -- and, for the
 // per-pass chunk seeds, Montgomery m^V and m^{kChunk}.
-// Swapped form (SW): the chain runs over the baby steps, so the multiplier is m^8 and the table
-// m^{rr} (rr < 8).
-template <bool SW>
+// (The swapped form's records -- chain multiplier m^8, table m^{rr} -- are written by k_tc_gplanes.)
 static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ C, u64* __restrict__ MS,
                                   ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
     const u64 mm = to_mont(m[q], mp);
     const u64 mV = mont_pow(mm, kV, mp);
-    const u64 step = SW ? mm : mV;
-    u64 g = mp.r1;                                     // Montgomery m^{rr V} (SW: m^{rr})
+    u64 g = mp.r1;                                     // Montgomery m^{rr V}
     for (int rr = 0; rr < 8; ++rr) {
       C[q * kCRec + kC_g0 + rr] = g;
-      g = mont_mul(g, step, mp);
+      g = mont_mul(g, mV, mp);
     }
-    const u64 aL = from_mont(g, mp);                   // m^{8V} (SW: m^8)
+    const u64 aL = from_mont(g, mp);                   // m^{8V}
     C[q * kCRec + kC_mL] = aL;
     C[q * kCRec + kC_wL] = shoup_w_fast(aL, mp);
     MS[2 * q] = mV;
@@ -1027,11 +1024,13 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
 // with the fixed multiplier m^{8V} (Shoup).  A warp's store of one plane word covers 8 rows x 16
 // bytes = one 128-byte line, so the planes go straight to global memory.  The per-term powers
 // m^V, m^{2V}, m^{4V}, m^{8V} are computed once per term (lane r < 4 of the term's group) and
-// shuffled to the group's 8 lanes.
+// shuffled to the group's 8 lanes; the same lane also writes the term's C record (the swapped
+// chain's m^8, its Shoup constant, Montgomery m^{rr} for rr < 8) and seed powers (m^V, m^{kChunk}).
 constexpr int kGpThreads = 256;
 template <bool LAZY>
 static __global__ void __launch_bounds__(kGpThreads) k_tc_gplanes(const u64* __restrict__ m, u64 t_pad,
-                                                                  uint8_t* __restrict__ Gp, ModParams mp) {
+                                                                  uint8_t* __restrict__ Gp, u64* __restrict__ C,
+                                                                  u64* __restrict__ MS, ModParams mp) {
   const u64 ntask = 2 * ((t_pad + kKB - 1) / kKB);
   const int lane = threadIdx.x & 31;
   const u32 ql = (u32)(lane >> 3), r = (u32)(lane & 7);
@@ -1048,6 +1047,22 @@ static __global__ void __launch_bounds__(kGpThreads) k_tc_gplanes(const u64* __r
     for (int i = 0; i < 6; ++i) mV = mont_mul(mV, mV, mp);   // m^V, V = 64
     const u64 m2V = mont_mul(mV, mV, mp), m4V = mont_mul(m2V, m2V, mp);
     const u64 m8V = mont_mul(m4V, m4V, mp);
+    if (r < 4 && q < t_pad) {                            // the term's C record and seed powers
+      u64 g = mp.r1;
+#pragma unroll 1
+      for (int rr = 0; rr < 8; ++rr) {
+        C[q * kCRec + kC_g0 + rr] = g;                   // Montgomery m^{rr}
+        g = mont_mul(g, mm, mp);
+      }
+      const u64 a8 = from_mont(g, mp);                   // m^8
+      C[q * kCRec + kC_mL] = a8;
+      C[q * kCRec + kC_wL] = g * mp.pinv;                // shoup_w_fast(m^8)
+      u64 mC = m8V;                                      // m^{kChunk} = (m^{8V})^16
+#pragma unroll 1
+      for (int i = 0; i < 4; ++i) mC = mont_mul(mC, mC, mp);
+      MS[2 * q] = mV;
+      MS[2 * q + 1] = mC;
+    }
     u64 y[4], mS[4], wS[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
