@@ -84,7 +84,14 @@ typedef struct pe_config {
   int32_t R;     /* terms per lane: 1,2,4,8,16 (FP64: <= 8); auto picks by bucket sizes    */
   int32_t warps; /* warps per CTA, 1..16 (auto 8)                                          */
   int32_t chunk; /* points per CTA (multiple of 32; auto by grid coverage)                 */
+  int32_t tc_form; /* tensor-core path, 8-digit primes (p >= 2^54): PE_TC_FORM_PLAIN (default; baby-step
+                      planes m^v per handle, 0.5 KB per term, giant steps generated per evaluation) or
+                      PE_TC_FORM_SWAPPED (giant-step planes m^{64u} per handle, 1 KB per term, baby steps
+                      c m^{j+v} generated: half the generation, twice the plane bytes -- for handles
+                      evaluated many times).  Same results.  Below 2^54 always plain.
+                      env PE_TC_SWAP=0/1 overrides an automatic (0) choice. */
 } pe_config;
+enum { PE_TC_FORM_AUTO = 0, PE_TC_FORM_PLAIN = 1, PE_TC_FORM_SWAPPED = 2 };
 
 /*
  * pe_create -- build an evaluation handle on the CUDA device current at the call.
@@ -180,6 +187,9 @@ int pe_info(const pe_ctx* h, int32_t* path, int32_t* R, int32_t* warps, uint64_t
  * pieces (<= 8192 terms of one bucket each; env PE_TC_PIECE caps them lower, for tests).  Any
  * pointer may be NULL.  Errors: PE_EINVAL (h NULL). */
 int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint64_t* min_T);
+/* The handle's tensor-core form: PE_TC_FORM_PLAIN or PE_TC_FORM_SWAPPED, 0 if it has no tensor-core
+ * path (pe_config.tc_form).  PE_EINVAL if h is NULL. */
+int pe_tc_form(const pe_ctx* h);
 
 /* Which hot kernel an evaluation of T points on this handle runs: 0 = the scalar k_step, 1 = the
  * tensor-core k_tc, 2 = the fast product-tree method (the automatic choice: thresholds,

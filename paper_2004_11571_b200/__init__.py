@@ -22,6 +22,7 @@ TEST_LIB_PATH = os.path.join(_PKG, "libpe_test.so")   # include/pe_test.h: probe
 
 PE_OK, PE_EINVAL, PE_ENOTPRIME, PE_ERANGE, PE_ENOMEM, PE_ECUDA, PE_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
 PATH_AUTO, PATH_INT, PATH_FP64, PATH_INT32, PATH_TC, PATH_FAST = 0, 1, 2, 4, 5, 6
+TC_FORM_AUTO, TC_FORM_PLAIN, TC_FORM_SWAPPED = 0, 1, 2
 (CORE_SHOUP4, CORE_SHOUP2, CORE_MONT, CORE_FP64, CORE_FP64ADD, CORE_POW, CORE_SHOUP4RAW, CORE_HYB, CORE_HYBRAW,
  CORE_SHOUPW) = range(10)
 
@@ -31,7 +32,7 @@ EXPORTS = ["pe_create", "pe_create_ex", "pe_eval", "pe_eval_device", "pe_destroy
            "pe_interp_bound_ok", "pe_set_timing", "pe_kernel_stats",
            "pe_create_batch", "pe_num_polys", "pe_poly_rows", "pe_bm_device", "pe_bm", "pe_tc_info",
            "pe_rows_addmod", "pe_unshard_columns", "pe_eval_kernel", "pe_create_compact",
-           "pe_eval_device_rows", "pe_row_split"]
+           "pe_eval_device_rows", "pe_row_split", "pe_tc_form"]
 #: every symbol include/pe_test.h declares (libpe_test.so)
 TEST_EXPORTS = ["pe_test_core", "pe_bench_core", "pe_bench_mma"]
 
@@ -44,7 +45,7 @@ class PEError(RuntimeError):
 
 class Config(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int32), ("R", ctypes.c_int32), ("warps", ctypes.c_int32),
-                ("chunk", ctypes.c_int32)]
+                ("chunk", ctypes.c_int32), ("tc_form", ctypes.c_int32)]
 
 
 _lib = None
@@ -109,6 +110,8 @@ def lib():
         L.pe_tc_info.restype = ctypes.c_int
         L.pe_eval_kernel.argtypes = [vp, u64]
         L.pe_eval_kernel.restype = ctypes.c_int
+        L.pe_tc_form.argtypes = [vp]
+        L.pe_tc_form.restype = ctypes.c_int
         L.pe_rows_addmod.argtypes = [u64, vp, u64, vp, u64, u64, u64, vp]
         L.pe_rows_addmod.restype = ctypes.c_int
         L.pe_unshard_columns.argtypes = [vp, u64, vp, u64, u64, u64, u64, vp]
@@ -154,8 +157,9 @@ class Context:
     """An evaluation handle (``pe_create_ex``).  Arrays are host numpy arrays."""
 
     def __init__(self, p: int, coeffs, exps, alpha, n: int | None = None, path: int = PATH_AUTO,
-                 R: int = 0, warps: int = 0, chunk: int = 0, compact: bool = False):
-        """compact=True: exponents passed as uint8 (pe_create_compact; every degree must be < 256)."""
+                 R: int = 0, warps: int = 0, chunk: int = 0, compact: bool = False, tc_form: int = 0):
+        """compact=True: exponents passed as uint8 (pe_create_compact; every degree must be < 256).
+        tc_form: TC_FORM_PLAIN / TC_FORM_SWAPPED (tensor-core form for p >= 2^54), 0 = automatic."""
         coeffs = np.ascontiguousarray(coeffs, dtype=np.uint64).ravel()
         if compact:
             e = np.asarray(exps)
@@ -168,7 +172,7 @@ class Context:
         exps = exps.reshape(-1, n) if exps.size else np.zeros((0, n), exps.dtype)
         alpha = np.ascontiguousarray(alpha, dtype=np.uint64).ravel()
         self.p, self.n, self.t = int(p), int(n), int(coeffs.size)
-        cfg = Config(path, R, warps, chunk)
+        cfg = Config(path, R, warps, chunk, tc_form)
         L = lib()
         create = L.pe_create_compact if compact else L.pe_create_ex
         h = create(self.p, self.t, self.n, _ptr(coeffs), _ptr(exps), _ptr(alpha), ctypes.byref(cfg))
@@ -188,7 +192,7 @@ class Context:
         alpha = np.ascontiguousarray(alpha, dtype=np.uint64).ravel()
         self = cls.__new__(cls)
         self.p, self.n, self.t = int(p), int(n), int(coeffs.size)
-        cfg = Config(path, R, warps, chunk)
+        cfg = Config(path, R, warps, chunk, 0)
         L = lib()
         h = L.pe_create_batch(self.p, len(polys), _ptr(tper), self.n, _ptr(coeffs), _ptr(exps), _ptr(alpha),
                               ctypes.byref(cfg))
@@ -252,6 +256,13 @@ class Context:
         if k < 0:
             raise PEError(k, "pe_eval_kernel")
         return {0: "k_step", 1: "k_tc", 2: "fast"}[k]
+
+    def tc_form(self) -> int:
+        """TC_FORM_PLAIN / TC_FORM_SWAPPED, or 0 without a tensor-core path (pe_tc_form)."""
+        k = lib().pe_tc_form(self._h)
+        if k < 0:
+            raise PEError(k, "pe_tc_form")
+        return k
 
     def uses_tc(self, T: int) -> bool:
         """True if an evaluation of T points runs the tensor-core kernel (PE_PATH_TC / auto)."""

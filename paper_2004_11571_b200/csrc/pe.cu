@@ -125,6 +125,7 @@ struct pe_ctx {
   int tc_mode = 0;
   bool tc_ok = false;
   bool tc_swap = false;   // swapped form (tc.cuh MODE 4 / 5): giant-step planes per handle, baby steps generated
+  int tc_form_req = 0;    // pe_config.tc_form
   u32 tc_rounds = 2;
   int n_sm = 148;
   u64* d_tcC = nullptr;   // [t_pad][2] tensor-core path C records (tc.cuh)
@@ -574,8 +575,11 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
     // §6, ~624 B per padded term).  If it does not fit (the device, or the env cap PE_TC_MEM_MB),
     // an automatic handle degrades to the scalar k_step; a forced one (PE_PATH_TC) fails.
     const u64 nrblk = (tp + 2 * tc::kKB - 1) / (2 * tc::kKB);
-    // 8-digit primes (p >= 2^54) use the swapped form unless PE_TC_SWAP=0 (tc.cuh)
-    h->tc_swap = h->p >= (1ull << 54) && env_int("PE_TC_SWAP", 1) != 0;
+    // 8-digit primes (p >= 2^54) may use the swapped form (tc.cuh): pe_config.tc_form, or with
+    // PE_TC_FORM_AUTO the env override PE_TC_SWAP=1 (default plain)
+    const int form = h->tc_form_req != PE_TC_FORM_AUTO ? h->tc_form_req
+                   : (env_int("PE_TC_SWAP", 0) ? PE_TC_FORM_SWAPPED : PE_TC_FORM_PLAIN);
+    h->tc_swap = h->p >= (1ull << 54) && form == PE_TC_FORM_SWAPPED;
     const u64 plane_bytes = h->tc_swap ? (tp + tc::kKB - 1) / tc::kKB * tc::kGBytes : nrblk * 2 * tc::kRBytes;
     const u64 tc_bytes = (u64)tc::kCRec * 8 * tp + 16 * tp + plane_bytes;
     const u64 cap = (u64)std::max(0, env_int("PE_TC_MEM_MB", 0)) << 20;
@@ -758,7 +762,9 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
   int R = cfg && cfg->R ? cfg->R : env_int("PE_R", 0);
   int W = cfg && cfg->warps ? cfg->warps : env_int("PE_WARPS", 8);
   int chunk = cfg && cfg->chunk ? cfg->chunk : env_int("PE_CHUNK", 0);
-  if (W < 1 || W > kMaxWarps || chunk < 0 || chunk % kSuper) {
+  const int tc_form = cfg ? cfg->tc_form : PE_TC_FORM_AUTO;
+  if (W < 1 || W > kMaxWarps || chunk < 0 || chunk % kSuper || tc_form < PE_TC_FORM_AUTO ||
+      tc_form > PE_TC_FORM_SWAPPED) {
     set_err(PE_EINVAL);
     return nullptr;
   }
@@ -770,6 +776,7 @@ static pe_ctx* create_common(uint64_t p, uint32_t npoly, const uint64_t* t_per_p
   h->tc_mode = tc_mode;
   h->fast_mode = fast_mode;
   h->R = R; h->W = W; h->chunk_req = chunk;
+  h->tc_form_req = tc_form;
   h->partial_cap_bytes = (size_t)env_int("PE_PARTIAL_MB", 1024) << 20;
   h->poly_off = poly_off;
   h->poly_rows.assign(npoly + 1, 0);
@@ -1401,6 +1408,11 @@ extern "C" int pe_tc_info(const pe_ctx* h, int32_t* mode, uint64_t* pieces, uint
   }
   if (min_T) *min_T = h->tc_ok ? (h->tc_mode == 2 ? 1 : tc_min_T(h->t_pad, h->p)) : 0;
   return PE_OK;
+}
+
+extern "C" int pe_tc_form(const pe_ctx* h) {
+  if (!h) return set_err(PE_EINVAL);
+  return h->tc_ok ? (h->tc_swap ? PE_TC_FORM_SWAPPED : PE_TC_FORM_PLAIN) : 0;
 }
 
 extern "C" int pe_eval_kernel(const pe_ctx* h, uint64_t T) {

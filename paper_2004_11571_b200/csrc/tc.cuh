@@ -42,7 +42,7 @@
 //              lane copies the K-block's baby-step planes into the stage with TMA, the other's
 //              prefetches the group's next K-block of per-term records.
 //
-// Swapped form (MODE 4 / 5, 8-digit p >= 2^54, the default for those primes): the point-dependent
+// Swapped form (MODE 4 / 5, 8-digit p >= 2^54, pe_config.tc_form = PE_TC_FORM_SWAPPED): the point-dependent
 // factor c m^{j_s} is folded into the baby steps instead, R'[i][v] = c_i m_i^{j_s + v}, and the
 // giant steps G[u][i] = m_i^{uV} become the point-independent factor, built once per handle
 // (k_tc_gplanes, Montgomery residues, 1 KB per term) and streamed into the A half of the stages by

@@ -257,17 +257,36 @@ def test_tc_7digit_mode_equals_scalar_step():
 
 
 @pytest.mark.parametrize("p", [P62, (1 << 54) + 159, (1 << 62) + 135, (1 << 63) - 25])
-@pytest.mark.parametrize("swap", ["0", "1"])
-def test_tc_plain_and_swapped_forms(monkeypatch, p, swap):
-    """For 8-digit primes (p >= 2^54) the default is the swapped form (giant-step planes built per
-    handle, baby steps c m^{j_s + v} generated per unit, tc.cuh MODE 4 / 5); PE_TC_SWAP=0 keeps the
-    plain form (baby-step planes per handle, giant steps generated, MODE 0 / 1).  Both equal the
-    direct oracle on sampled columns and the incremental checker in full, across a ragged third
-    chunk, lazy (p < 2^62) and exact (p >= 2^62) chains."""
-    monkeypatch.setenv("PE_TC_SWAP", swap)
+@pytest.mark.parametrize("form", [pe.TC_FORM_PLAIN, pe.TC_FORM_SWAPPED])
+def test_tc_plain_and_swapped_forms(p, form):
+    """For 8-digit primes (p >= 2^54) pe_config.tc_form picks the plain form (default: baby-step
+    planes built per handle, giant steps generated per unit, tc.cuh MODE 0 / 1) or the swapped one
+    (giant-step planes per handle, baby steps c m^{j_s + v} generated, MODE 4 / 5).  Both equal the
+    incremental checker in full and the direct oracle on sampled columns, across a ragged third
+    chunk, with lazy (p < 2^62) and exact (p >= 2^62) chains."""
     w = synth.random_small(590 + p % 97, p, 7, 3000, 5, 2 * 8192 + 777, 11)
-    _, out = tc_eval(w)
+    with pe.Context.from_workload(w, path=pe.PATH_TC, tc_form=form) as ctx:
+        assert ctx.tc_form() == form
+        out = ctx.eval(w.j0, w.T)
     ref = oracle.eval_incremental(w.p, w.n, w.coeffs, w.exps, w.alpha, w.j0, w.T)
     assert np.array_equal(out, ref)
     ks = np.array([0, 8191, 8192, w.T - 1], np.uint64)
     assert np.array_equal(out[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
+
+
+def test_tc_form_defaults_and_limits():
+    """Automatic = plain; the swapped form only exists for 8-digit primes (below 2^54 a request for
+    it builds the plain form, whose 7- and 4-digit modes read baby-step planes); out-of-range
+    tc_form values are PE_EINVAL."""
+    w = synth.random_small(599, P62, 5, 300, 3, 100, 1)
+    with pe.Context.from_workload(w, path=pe.PATH_TC) as ctx:
+        assert ctx.tc_form() == pe.TC_FORM_PLAIN
+    w2 = synth.random_small(598, (1 << 50) - 27, 5, 300, 3, 100, 1)
+    with pe.Context.from_workload(w2, path=pe.PATH_TC, tc_form=pe.TC_FORM_SWAPPED) as ctx:
+        assert ctx.tc_form() == pe.TC_FORM_PLAIN
+        assert np.array_equal(ctx.eval(w2.j0, w2.T), oracle.eval_workload(w2))
+    with pe.Context.from_workload(w, path=pe.PATH_INT) as ctx:
+        assert ctx.tc_form() == 0
+    with pytest.raises(pe.PEError) as e:
+        pe.Context.from_workload(w, tc_form=3)
+    assert e.value.code == -1
