@@ -19,6 +19,12 @@ args = ap.parse_args()
 w = synth.gen_config(args.cfg)
 pre = set(filter(None, args.prelude.split(",")))
 keep = []
+if "dist" in pre:
+    import torch.distributed as dist  # noqa: F401
+    from paper_2004_11571_b200.dist import ShardedEval as _SE  # noqa: F401
+if "fork" in pre:
+    import subprocess
+    subprocess.run(["nvidia-smi", "-L"], stdout=subprocess.DEVNULL)
 if "dev" in pre:
     torch.cuda.set_device(0)
     _st = torch.cuda.current_stream(torch.device("cuda", 0))
@@ -33,6 +39,9 @@ if "ctx" in pre:
     if "sh" in pre:
         from paper_2004_11571_b200.dist import ShardedEval
         keep.append(ShardedEval(c.G, w.T, torch.device("cuda", 0)))
+if "fork2" in pre:
+    import subprocess
+    subprocess.run(["nvidia-smi", "-L"], stdout=subprocess.DEVNULL)
 L = pe.lib()
 pin = lambda a: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).pin_memory()
 if "order" in pre:     # bench.py's allocation order: coeffs, exps, alpha, result, uint8 exps
