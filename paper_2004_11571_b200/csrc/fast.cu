@@ -186,7 +186,7 @@ __device__ __forceinline__ const u64* op_ptr(const Call& a, u32 job, u32 o) {
 
 // Forward transforms: unit = (job, op, block) of prime blockIdx.y; a CTA holds kTile / S units.
 constexpr u32 kNttThreads = 256;
-__global__ void __launch_bounds__(kNttThreads, 3) k_fast_fwd(Call a) {
+__global__ void __launch_bounds__(kNttThreads, 4) k_fast_fwd(Call a) {
   extern __shared__ u32 X[];
   const int j = blockIdx.y;
   const PrimeC P = a.C.pr[j];
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kNttThreads, 3) k_fast_fwd(Call a) {
 
 // Pointwise products + inverse: unit = (job, out, out block c) of prime blockIdx.y.
 // out 0 of kMerge: N1 E2 + N2 E1 (ops 0,3 and 2,1); out 1: E1 E2 (ops 1,3); kMul: op0 op1.
-__global__ void __launch_bounds__(kNttThreads, 3) k_fast_pwinv(Call a) {
+__global__ void __launch_bounds__(kNttThreads, 4) k_fast_pwinv(Call a) {
   extern __shared__ u32 X[];
   const int j = blockIdx.y;
   const PrimeC P = a.C.pr[j];
