@@ -274,10 +274,11 @@ def test_tc_plain_and_swapped_forms(p, form):
     assert np.array_equal(out[:, ks.astype(np.int64)], oracle.eval_workload(w, ks=ks))
 
 
-def test_tc_form_defaults_and_limits():
+def test_tc_form_defaults_and_limits(monkeypatch):
     """Automatic = plain; the swapped form only exists for 8-digit primes (below 2^54 a request for
     it builds the plain form, whose 7- and 4-digit modes read baby-step planes); out-of-range
     tc_form values are PE_EINVAL."""
+    monkeypatch.delenv("PE_TC_SWAP", raising=False)
     w = synth.random_small(599, P62, 5, 300, 3, 100, 1)
     with pe.Context.from_workload(w, path=pe.PATH_TC) as ctx:
         assert ctx.tc_form() == pe.TC_FORM_PLAIN
