@@ -208,19 +208,34 @@ __host__ __device__ constexpr u32 idesc_n(int n) {
 // s + t - d_lo ...  The plane whose range covers every slot of the round (s = 0 for d = 0..7,
 // s = 7 for d = 8..14) goes first, so at K-block 0 it initialises all accumulators (acc = 0) and
 // every later MMA accumulates.  A plane issued as two MMAs keeps A in the collector.
-template <int G>
+// Order (wide_ord: planes 0, 7, 6, .., 1 for round 0 and 7, 1, 2, .., 6 for round 1): after the
+// initialising plane, the planes with the fewest partners come first and a plane's narrow MMA
+// precedes its wide one, so every K-block ends on wide MMAs and the tensor core's queue still holds
+// ~250 clk of work while the issuing warp crosses the K-block boundary (stage wait, commit, loop).
+// Measured: the stage handshake alone (scripts/mma_swz.cu k_hs) 0.72 -> 0.80 of the MMA floor;
+// whole k_tc on config 5 (ncu sm__cycles_elapsed) 13.47 M -> 13.20 M clk, bench +1.3 % burst and
+// +1 % sustained at the power cap (profiles/r02_ktc_issue_order.txt).  Moving the next stage's
+// wait in front of the last two MMAs as well took the MMA path alone to 0.86 of its floor, but
+// the whole kernel to 13.89 M clk (the producers then lose more to the tensor core's shared-
+// memory reads), so it is not used.  MMAs LO <= i < HI of the order are issued.
+__host__ __device__ constexpr int wide_ord(int g, int k) { return g == 0 ? (k == 0 ? 0 : 8 - k) : (k == 0 ? 7 : k == 7 ? 0 : k); }
+template <int G, int LO = 0, int HI = 16>
 __device__ __forceinline__ void issue_round_wide(u32 tb, uint64_t da, uint64_t db, bool first_kb) {
   constexpr int d_lo = G == 0 ? 0 : 8, d_hi = G == 0 ? 7 : 14;
+  int idx = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const int sd = G == 0 ? k : 7 - k;
+    const int sd = wide_ord(G, k);
     const int t_lo = d_lo - sd > 0 ? d_lo - sd : 0;
     const int t_hi = d_hi - sd < 7 ? d_hi - sd : 7;
     if (t_lo > t_hi) continue;
     const int nmma = (t_hi - t_lo) / 4 + 1;
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      if (c >= nmma) continue;
+    for (int cc = 0; cc < 2; ++cc) {
+      if (cc >= nmma) continue;
+      const int me = idx++;
+      if (me < LO || me >= HI) continue;
+      const int c = (nmma == 2 && k > 0) ? 1 - cc : cc;   // narrow part first (c = 1 is the tail run)
       const int ta = t_lo + 4 * c;
       const int tb2 = ta + 3 < t_hi ? ta + 3 : t_hi;
       const int n = 64 * (tb2 - ta + 1);
@@ -229,7 +244,7 @@ __device__ __forceinline__ void issue_round_wide(u32 tb, uint64_t da, uint64_t d
       const uint64_t ad = da + (uint64_t)((u32)sd * (kPlaneA >> 4));
       const uint64_t bd = db + (uint64_t)((u32)ta * (kPlaneB >> 4));
       if (nmma == 1) mma_u8n<0>(dt, ad, bd, idesc_n(n), acc);
-      else if (c == 0) mma_u8n<1>(dt, ad, bd, idesc_n(n), acc);
+      else if (cc == 0) mma_u8n<1>(dt, ad, bd, idesc_n(n), acc);
       else mma_u8n<2>(dt, ad, bd, idesc_n(n), acc);
     }
   }
