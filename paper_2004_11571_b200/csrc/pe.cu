@@ -127,6 +127,7 @@ struct pe_ctx {
   bool tc_swap = false;   // swapped form (tc.cuh MODE 4 / 5): giant-step planes per handle, baby steps generated
   int tc_form_req = 0;    // pe_config.tc_form
   u32 tc_rounds = 2;
+  u32 tc_v = 64, tc_chunk = 8192;   // baby steps and points per chunk of the handle's k_tc geometry (tc.cuh mode_v)
   int n_sm = 148;
   u64* d_tcC = nullptr;   // [t_pad][2] tensor-core path C records (tc.cuh)
   u64* d_tcMS = nullptr;  // [t_pad][2] Montgomery m^V, m^{kChunk} (k_tc_seed)
@@ -281,7 +282,8 @@ static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStrea
   return launch_step_path<kFp64>(R, grid, block, s, a);
 }
 
-// automatic tensor-core path from this many points (a chunk is tc::kChunk = 8192 points): k_tc
+// automatic tensor-core path from this many points (a chunk is 8192 points, 4096 in the V = 32
+// geometry of p >= 2^54): k_tc
 // costs a flat ~0.11 ms + 0.42 ns per padded term for any T <= 8192, k_step grows with t * T.
 // Measured crossovers (scripts/tc_threshold.py, profiles/r01_tc_threshold.jsonl): T ~ 860 for
 // 10^5 terms, ~480 for 10^6 (k_step INT), 512 vs FP64 Alg. 2 -- i.e. T* ~ 8.6e7 / t_pad, >= 512.
@@ -580,7 +582,10 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
     const int form = h->tc_form_req != PE_TC_FORM_AUTO ? h->tc_form_req
                    : (env_int("PE_TC_SWAP", 0) ? PE_TC_FORM_SWAPPED : PE_TC_FORM_PLAIN);
     h->tc_swap = h->p >= (1ull << 54) && form == PE_TC_FORM_SWAPPED;
-    const u64 plane_bytes = h->tc_swap ? (tp + tc::kKB - 1) / tc::kKB * tc::kGBytes : nrblk * 2 * tc::kRBytes;
+    // plain 8-digit modes (p >= 2^54): the single-round V = 32 geometry (256 B of planes per term)
+    h->tc_v = (!h->tc_swap && h->p >= (1ull << 54)) ? 32u : 64u;
+    h->tc_chunk = tc::chunk_pts((int)h->tc_v);
+    const u64 plane_bytes = h->tc_swap ? (tp + tc::kKB - 1) / tc::kKB * tc::kGBytes : nrblk * 2 * tc::r_bytes((int)h->tc_v);
     const u64 tc_bytes = (u64)tc::kCRec * 8 * tp + 16 * tp + plane_bytes;
     const u64 cap = (u64)std::max(0, env_int("PE_TC_MEM_MB", 0)) << 20;
     int rc = PE_OK;
@@ -621,13 +626,15 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
           cudaEventRecord(e_m, s) != cudaSuccess || cudaStreamWaitEvent(s2, e_m, 0) != cudaSuccess)
         rc = PE_ECUDA;
       if (rc == PE_OK) {
-        tc::k_tc_setup<<<grid_for(tp, 256), 256, 0, s2>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
+        if (h->tc_v == 32) tc::k_tc_setup<32><<<grid_for(tp, 256), 256, 0, s2>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
+        else tc::k_tc_setup<64><<<grid_for(tp, 256), 256, 0, s2>>>(h->d_m, tp, h->d_tcC, h->d_tcMS, h->mp);
         const u64 nrp = 4 * ((tp + 2 * tc::kKB - 1) / (2 * tc::kKB));   // warp tasks (K-block, K half)
         const unsigned rpg = (unsigned)std::max<u64>(1, std::min<u64>((nrp + 7) / 8, 148ull * 8));
-        if (h->p >= (1ull << 31) && h->p < (1ull << 62))
-          tc::k_tc_rplanes<true><<<rpg, tc::kRpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
-        else
-          tc::k_tc_rplanes<false><<<rpg, tc::kRpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
+        const bool lazy = h->p >= (1ull << 31) && h->p < (1ull << 62);
+        if (h->tc_v == 32 && lazy) tc::k_tc_rplanes<true, 32><<<rpg, tc::kRpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
+        else if (h->tc_v == 32) tc::k_tc_rplanes<false, 32><<<rpg, tc::kRpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
+        else if (lazy) tc::k_tc_rplanes<true, 64><<<rpg, tc::kRpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
+        else tc::k_tc_rplanes<false, 64><<<rpg, tc::kRpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->mp);
         if (cudaGetLastError() != cudaSuccess || cudaEventRecord(e_done, s2) != cudaSuccess ||
             cudaStreamWaitEvent(s, e_done, 0) != cudaSuccess)
           rc = PE_ECUDA;
@@ -638,7 +645,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
       if (rc != PE_OK) return set_err(rc);
     }
     CU(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
-    h->tc_rounds = h->p < (1ull << 31) ? 1 : tc::kRounds;   // 4-byte digits: one round
+    // 4-byte digits (7 diagonals) and the V = 32 geometry (15 x 32 columns): one round
+    h->tc_rounds = (h->p < (1ull << 31) || h->tc_v == 32) ? 1 : tc::kRounds;
     if (int rc = status_get(&h->h_status, &h->d_status)) return set_err(rc);
     h->tc_ok = true;
   }
@@ -667,13 +675,14 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
   CU(cudaMemcpyAsync(h->d_wt_info, wt_info.data(), n_wt * sizeof(uint2), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(h->d_slot_start, slot_start.data(), (G + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
 
-  // k_tc plans of the common evaluation shapes (1 or 2 chunks per pass; all rows, and pe_eval's two
+  // k_tc plans of the common evaluation shapes (8192- or 16384-point passes; all rows, and pe_eval's two
   // row blocks), built on the host while the setup kernels run and uploaded behind them
   if (h->tc_ok) {
     h->split_g1 = tc_row_split(h);
     const u64 ranges[3][2] = {{0, h->G}, {0, h->split_g1}, {h->split_g1, h->G}};
-    for (u32 nch = 1; nch <= 2; ++nch)
+    for (u32 k = 1; k <= 2; ++k)   // passes of 8192 and 16384 points
       for (auto& r : ranges) {
+        const u32 nch = k * (8192u / h->tc_chunk);
         if (r[0] >= r[1]) continue;
         pe_ctx::TcPlan* P = nullptr;
         if (tc_plan(h, nch, r[0], r[1], true, s, &P)) return g_last_error;
@@ -999,15 +1008,16 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s,
   // pass length from the one-chunk plan: it has the most pieces (plans with more chunks per pass
   // use larger pieces), so its slot count bounds every pass's partial rows
   const u64 nslots = tc_nslots(h, 1, g0, g1);
-  u64 Tp = h->partial_cap_bytes / 8 / std::max<u64>(nslots, 1) / tc::kChunk * tc::kChunk;
-  Tp = std::max<u64>(Tp, tc::kChunk);
-  Tp = std::min<u64>(Tp, (T + tc::kChunk - 1) / tc::kChunk * tc::kChunk);
-  Tp = std::min<u64>(Tp, (u64)tc::kChunk * 4096);
+  const u64 CH = h->tc_chunk;   // points per chunk of the handle's geometry
+  u64 Tp = h->partial_cap_bytes / 8 / std::max<u64>(nslots, 1) / CH * CH;
+  Tp = std::max<u64>(Tp, CH);
+  Tp = std::min<u64>(Tp, (T + CH - 1) / CH * CH);
+  Tp = std::min<u64>(Tp, CH * 4096);
   // every allocation of the evaluation comes before its first launch, so an automatic handle can
   // still fall back to k_step on PE_ENOMEM (eval_device_impl)
   // partial rows padded to a multiple of 8 points (the epilogue's 64-byte vector accesses)
   if (ensure_partial(h, (size_t)nslots * ((std::min<u64>(Tp, T) + 7) / 8 * 8), s)) return g_last_error;
-  const u32 nch_max = (u32)(Tp / tc::kChunk);
+  const u32 nch_max = (u32)(Tp / CH);
   if ((size_t)h->t_pad * nch_max * tc::kLSRec > h->seed_elems) {
     if (h->d_seed) cudaFreeAsync(h->d_seed, s);
     h->d_seed = nullptr;
@@ -1048,10 +1058,10 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s,
   for (const void* f : tc_fns) CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem));
   for (u64 k0 = 0; k0 < T; k0 += Tp) {
     const u32 np = (u32)std::min<u64>(Tp, T - k0);
-    const u32 nch = (np + tc::kChunk - 1) / tc::kChunk;
+    const u32 nch = (u32)((np + CH - 1) / CH);
     const u64 nseed = (q1 - q0) * ((nch + tc::kSeedChunks - 1) / tc::kSeedChunks);
-    tc::k_tc_seed<<<grid_for(nseed, 256), 256, 0, s>>>(h->d_c, h->d_m, h->d_tcMS, h->t_pad, q0, q1, nch, j0 + k0,
-                                                       h->d_seed, h->mp);
+    tc::k_tc_seed<<<grid_for(nseed, 256), 256, 0, s>>>(h->d_c, h->d_m, h->d_tcMS, h->t_pad, q0, q1, nch, (u32)CH,
+                                                       j0 + k0, h->d_seed, h->mp);
     CU(cudaGetLastError());
     pe_ctx::TcPlan* P = nullptr;
     if (tc_plan(h, nch, g0, g1, true, s, &P)) return g_last_error;
@@ -1163,7 +1173,7 @@ static bool use_tc(const pe_ctx* h, u64 T) {
   if (!h->tc_ok) return false;
   if (h->tc_mode == 2) return true;
   if (h->tc_mode != 1 || T < tc_min_T(h->t_pad, h->p)) return false;
-  const u64 row = (std::min<u64>(T, tc::kChunk) + 7) / 8 * 8;
+  const u64 row = (std::min<u64>(T, h->tc_chunk) + 7) / 8 * 8;
   return tc_nslots(h, 1, 0, h->G) * row * sizeof(u64) <= h->partial_cap_bytes;
 }
 

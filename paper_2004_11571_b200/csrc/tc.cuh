@@ -82,6 +82,17 @@ constexpr u32 kGBytes = 8 * kPlaneA;      // one K-block's giant-step planes in 
 constexpr int kLSRec = 1, kCRec = 10;
 enum { kC_mL = 0, kC_wL = 1, kC_g0 = 2 };
 constexpr u32 kRBytes = 2 * kLBOB;                    // one K-block's R planes (16384 B)
+// Geometry of a mode: V baby steps per chunk, a chunk = kU * V points.  The 8-digit plain modes
+// (0, 1) use V = 32: all 15 diagonals then fit TMEM at once (15 x 32 = 480 columns), so a unit is
+// (piece, chunk) in ONE round -- 8 MMAs of N = 256 per K-block (L plane s against the 8 baby-step
+// planes, slots s .. s + 7) -- with half the baby-step plane bytes per term (256 B) and one fold +
+// REDC per point instead of one per round.  The 4-digit (7 diagonals in one round), 7-digit and
+// swapped modes keep V = 64.
+__host__ __device__ constexpr int mode_v(int MODE) { return MODE <= 1 ? 32 : 64; }
+__host__ __device__ constexpr u32 plane_b(int V) { return (u32)V * 16; }      // one R plane, one K half
+__host__ __device__ constexpr u32 lbo_b(int V) { return 8 * plane_b(V); }     // R planes' K-half stride
+__host__ __device__ constexpr u32 r_bytes(int V) { return 2 * lbo_b(V); }     // one K-block's R planes
+__host__ __device__ constexpr u32 chunk_pts(int V) { return (u32)kU * (u32)V; }
 constexpr u32 kDataLS = kKB * kLSRec * 8;             // 256 B
 constexpr u32 kDataSlot = kDataLS + kKB * kCRec * 8;  // 2816 B
 constexpr int kDataSlots = 2 * kStages;               // 2 per producer group: current + next K-block
@@ -99,9 +110,12 @@ static_assert(kSmemBytes + 256 <= 232448, "shared memory");
 // one wide MMA (B = planes t..t+k-1, N = 64k <= 256) covers k of them
 // group 2: the single round of the 4-digit mode (p < 2^31: values < 2^32), d = 0..6
 // group 4: the 7-digit mode's second round, d = 8..12
+// group 5: the single round of the V = 32 geometry, d = 0..14 in slots 0..14
 __host__ __device__ constexpr int group_diag(int g, int di) {
-  return g == 0 ? di : g == 1 ? (di < 7 ? 8 + di : -1) : g == 2 ? (di < 7 ? di : -1) : (di < 5 ? 8 + di : -1);
+  return g == 0 ? (di < 8 ? di : -1) : g == 1 ? (di < 7 ? 8 + di : -1) : g == 2 ? (di < 7 ? di : -1)
+       : g == 5 ? (di < 15 ? di : -1) : (di < 5 ? 8 + di : -1);
 }
+__host__ __device__ constexpr int nslots(int g) { return g == 5 ? 15 : kDiag; }
 
 struct TcArgs {
   const u64* LS;         // [nch][t_pad] chunk seeds c m^{j_s}
@@ -248,6 +262,23 @@ __device__ __forceinline__ void issue_round_wide(u32 tb, uint64_t da, uint64_t d
       else mma_u8n<2>(dt, ad, bd, idesc_n(n), acc);
     }
   }
+}
+
+// Single-round geometry (V = 32): L plane s against all 8 baby-step planes is ONE MMA of N = 256
+// into slots s .. s + 7 (TMEM columns 32 s ..); 8 MMAs per K-block, all 256 wide.  At K-block 0
+// plane 0 initialises slots 0..7 and plane 7 goes second, split so that its t = 1..7 part
+// initialises slots 8..14 (its t = 0 part accumulates into slot 7); planes 1..6 then accumulate.
+__device__ __forceinline__ void issue_all32(u32 tb, uint64_t da, uint64_t db, bool first_kb) {
+  constexpr u32 V = 32, PB = plane_b(32) >> 4, PA = kPlaneA >> 4;
+  mma_u8n<0>(tb, da, db, idesc_n(256), first_kb ? 0u : 1u);
+  if (first_kb) {
+    mma_u8n<1>(tb + 7 * V, da + 7 * PA, db, idesc_n(32), 1u);
+    mma_u8n<2>(tb + 8 * V, da + 7 * PA, db + PB, idesc_n(224), 0u);
+  } else {
+    mma_u8n<0>(tb + 7 * V, da + 7 * PA, db, idesc_n(256), 1u);
+  }
+#pragma unroll
+  for (int sd = 1; sd < 7; ++sd) mma_u8n<0>(tb + (u32)sd * V, da + (uint64_t)(sd * PA), db, idesc_n(256), 1u);
 }
 
 // The 4-digit mode (p < 2^31): 16 digit pairs, diagonals 0..6 in one round, as 5 MMAs.  No L plane
@@ -493,11 +524,11 @@ __device__ __forceinline__ void fold_add(u32 (&X)[5], u32 Dv) {
 // buffer (raw[slot][v/4][u][v%4], u32: the diagonal sums themselves) and release TMEM (acce) as soon as the
 // last block is in registers -- only tcgen05.ld and fire-and-forget stores, so the MMA warp can
 // start the next round almost at once.  Four accumulators (32 registers) per tcgen05.wait.
-template <int G, int H>
+template <int G, int H, int V = kV>
 __device__ __forceinline__ void drain_ld(u32 tl, u32 v0, u32 (&D)[4][8]) {
 #pragma unroll
   for (int j = 0; j < 4; ++j)
-    if (group_diag(G, 4 * H + j) >= 0) tmem_ld8(tl + (u32)(4 * H + j) * kV + v0, D[j]);
+    if (group_diag(G, 4 * H + j) >= 0) tmem_ld8(tl + (u32)(4 * H + j) * V + v0, D[j]);
 }
 template <int G, int H>
 __device__ __forceinline__ void drain_fence(u32 (&D)[4][8]) {
@@ -505,13 +536,13 @@ __device__ __forceinline__ void drain_fence(u32 (&D)[4][8]) {
   for (int j = 0; j < 4; ++j)
     if (group_diag(G, 4 * H + j) >= 0) tmem_reg_fence(D[j]);
 }
-template <int G, int H>
+template <int G, int H, int V = kV>
 __device__ __forceinline__ void drain_st(u32 v0, u32* __restrict__ raw_u, const u32 (&D)[4][8]) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     if (group_diag(G, 4 * H + j) >= 0) {
       // raw[d][v / 4][u][v % 4]: a warp's 16-byte stores cover 512 contiguous bytes
-      uint4* p4 = (uint4*)(raw_u + (u32)(4 * H + j) * (kU * kV) + (v0 >> 2) * (kU * 4));
+      uint4* p4 = (uint4*)(raw_u + (u32)(4 * H + j) * (kU * (u32)V) + (v0 >> 2) * (kU * 4));
       p4[0] = make_uint4(D[j][0], D[j][1], D[j][2], D[j][3]);
       p4[kU] = make_uint4(D[j][4], D[j][5], D[j][6], D[j][7]);
     }
@@ -545,6 +576,38 @@ __device__ __forceinline__ void epi_drain(u32 tl, u32* __restrict__ raw_u, uint6
   }
 }
 
+// The single-round geometry (G = 5, V = 32): 15 diagonals x 32 columns as 16 blocks of 4 diagonals
+// x 8 columns (block b: v0 = 8 (b / 4), diagonals 4 (b % 4) ..), each block's tcgen05.ld in flight
+// while the previous block is stored.
+template <int H>
+__device__ __forceinline__ void drain5_ld(u32 tl, int b, u32 (&D)[4][8]) { drain_ld<5, H, 32>(tl, (u32)(b / 4) * 8, D); }
+__device__ __forceinline__ void epi_drain5(u32 tl, u32* __restrict__ raw_u, uint64_t* acce, bool st = true) {
+  u32 A[4][8], B[4][8];
+  drain5_ld<0>(tl, 0, A);
+  tmem_wait_ld();
+  drain_fence<5, 0>(A);
+#pragma unroll
+  for (int b = 0; b < 16; b += 2) {   // A holds block b (H = 0 or 2), B gets block b + 1 (H = 1 or 3)
+    const u32 v0 = (u32)(b / 4) * 8;
+    const bool lo = (b % 4) == 0;
+    if (lo) drain5_ld<1>(tl, b + 1, B); else drain5_ld<3>(tl, b + 1, B);
+    if (st) { if (lo) drain_st<5, 0, 32>(v0, raw_u, A); else drain_st<5, 2, 32>(v0, raw_u, A); }
+    tmem_wait_ld();
+    if (lo) drain_fence<5, 1>(B); else drain_fence<5, 3>(B);
+    if (b + 2 < 16) {
+      if (lo) drain5_ld<2>(tl, b + 2, A); else drain5_ld<0>(tl, b + 2, A);
+    } else {   // TMEM drained: the MMA may start the next unit
+      tc_fence_before();
+      mbar_arrive(acce);
+    }
+    if (st) { if (lo) drain_st<5, 1, 32>(v0, raw_u, B); else drain_st<5, 3, 32>(v0, raw_u, B); }
+    if (b + 2 < 16) {
+      tmem_wait_ld();
+      if (lo) drain_fence<5, 2>(A); else drain_fence<5, 0>(A);
+    }
+  }
+}
+
 // X (160-bit, 5 x u32) = sum_{d<15} D_d 2^{8d}, exactly (< 2^145): composed in 128-bit C
 // arithmetic (the compiler owns the carries) + a top word.
 template <int D8>
@@ -556,11 +619,11 @@ __device__ __forceinline__ void fold_in(u128_t& lo, u32& x4, u32 Dv) {
 }
 
 // X_G += sum over round G's accumulator slots DI.. of D[slot] << 8 d(slot)  (compile-time shifts)
-template <int G, int DI>
-__device__ __forceinline__ void fold_group(u128_t& acc, u32& x4, const u32 (&D)[kDiag][4], int j) {
-  if constexpr (DI < kDiag) {
+template <int G, int DI, int NS>
+__device__ __forceinline__ void fold_group(u128_t& acc, u32& x4, const u32 (&D)[NS][4], int j) {
+  if constexpr (DI < NS) {
     if constexpr (group_diag(G, DI) >= 0) fold_in<8 * group_diag(G, DI)>(acc, x4, D[DI][j]);
-    fold_group<G, DI + 1>(acc, x4, D, j);
+    fold_group<G, DI + 1, NS>(acc, x4, D, j);
   }
 }
 
@@ -575,18 +638,19 @@ __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" :: "l"(p) : "memory");
 }
 
-template <int G>
+template <int G, int V = kV>
 __device__ __forceinline__ void fold_row(const u32* __restrict__ rr_, u64* __restrict__ prow, u64 kbase, u32 npts,
                                          u64 C64, u64 C96, u64 C128, const ModParams& mp, u32 vbeg, u32 vend,
                                          bool disc) {
   const bool line_head = (threadIdx.x & 7) == 0;   // 8 consecutive rows x 16 B = one 128-B line
 #pragma unroll 1
   for (u32 v0 = vbeg; v0 < vend; v0 += 4) {
-    u32 D[kDiag][4];
+    constexpr int NS = nslots(G);
+    u32 D[NS][4];
 #pragma unroll
-    for (int di = 0; di < kDiag; ++di) {
+    for (int di = 0; di < NS; ++di) {
       if (group_diag(G, di) >= 0) {
-        const uint4 q = *(const uint4*)(rr_ + (u32)di * (kU * kV) + (v0 >> 2) * (kU * 4));
+        const uint4 q = *(const uint4*)(rr_ + (u32)di * (kU * (u32)V) + (v0 >> 2) * (kU * 4));
         D[di][0] = q.x; D[di][1] = q.y; D[di][2] = q.z; D[di][3] = q.w;
       }
     }
@@ -595,7 +659,7 @@ __device__ __forceinline__ void fold_row(const u32* __restrict__ rr_, u64* __res
     for (int j = 0; j < 4; ++j) {
       u128_t acc = 0;
       u32 x4 = 0;
-      fold_group<G, 0>(acc, x4, D, j);
+      fold_group<G, 0, NS>(acc, x4, D, j);
       // X mod p = (x0 + x1 2^32) + x2 (2^64 mod p) + x3 (2^96 mod p) + x4 (2^128 mod p)  (< 2^98)
       u64 lo = (u64)acc, hi = 0;
       const u64 x2 = (u64)(acc >> 64) & 0xffffffffull, x3 = (u64)(acc >> 96);
@@ -619,8 +683,8 @@ __device__ __forceinline__ void fold_row(const u32* __restrict__ rr_, u64* __res
       __syncwarp();
       if (line_head) {
 #pragma unroll
-        for (int di = 0; di < kDiag; ++di)
-          if (group_diag(G, di) >= 0) discard_l2(rr_ + (u32)di * (kU * kV) + (v0 >> 2) * (kU * 4));
+        for (int di = 0; di < NS; ++di)
+          if (group_diag(G, di) >= 0) discard_l2(rr_ + (u32)di * (kU * (u32)V) + (v0 >> 2) * (kU * 4));
       }
     }
     if (kbase + v0 + 4 <= npts) {
@@ -794,8 +858,9 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
           mbar_expect_tx(&full[stage], kGBytes);
           bulk_g2s(stage0, a.Gp + ((u64)cur.q0 / kKB + cur.kb) * kGBytes, kGBytes, &full[stage]);
         } else {
-          mbar_expect_tx(&full[stage], kRBytes);
-          bulk_g2s(stage0 + 8 * kPlaneA, a.Rp + ((u64)cur.q0 / kKB + cur.kb) * kRBytes, kRBytes, &full[stage]);
+          constexpr u32 RB = r_bytes(mode_v(MODE));
+          mbar_expect_tx(&full[stage], RB);
+          bulk_g2s(stage0 + 8 * kPlaneA, a.Rp + ((u64)cur.q0 / kKB + cur.kb) * RB, RB, &full[stage]);
         }
       }
       if (loader && ahead.valid)
@@ -847,7 +912,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
     const u64 C64 = a.Wd[8], C96 = a.Wd[12], C128 = a.C128;
     const u32 tbu = uni(tb);
     const uint64_t dA0 = smem_desc(uni(smem_u32(smem)), kLBOA);
-    const uint64_t dB0 = smem_desc(uni(smem_u32(smem)) + 8 * kPlaneA, kLBOB);
+    constexpr int VV = mode_v(MODE);   // baby steps per chunk (32: single-round geometry)
+    const uint64_t dB0 = smem_desc(uni(smem_u32(smem)) + 8 * kPlaneA, lbo_b(VV));
     u32 it = 0;
     for (u32 nunit = 0, unit = unit_id(a, 0); unit < a.nunits; unit = unit_id(a, ++nunit)) {
       uint4 pc; u32 chunk, g;
@@ -856,6 +922,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       g = uni(g);
       u64* prow = a.partial + ((u64)pc.z * a.rounds + g) * a.ldp;
       if (MODE == 2) g = 2;   // the 4-digit mode's single round
+      if (VV == 32) g = 5;    // the V = 32 geometry's single round
       u32* raw = raw_cta + (u64)(nunit & 1) * kDiag * (kU * kV);
       if (warp == kMmaWarp) {
         // (this raw buffer was last read two units ago by warps 2 / 3's fold of warp 0's rows;
@@ -877,7 +944,9 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
           // tcgen05.commit tracks the MMAs its own thread issued
           __syncwarp();
           if (elect_one()) {
-            if (PROF && a.dbg == 7) {   // one N = 64 MMA per digit pair (the previous issue form)
+            if (VV == 32) {
+              if (!(PROF && a.dbg == 1)) issue_all32(tbu, da, db, kb == 0);
+            } else if (PROF && a.dbg == 7) {   // one N = 64 MMA per digit pair (the previous issue form)
               if (g == 0) issue_round<0, true>(tbu, da, db, kb == 0);
               else issue_round<1, true>(tbu, da, db, kb == 0);
             } else if (!(PROF && a.dbg == 1)) {
@@ -901,7 +970,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       tc_fence_after();
       u32* raw_u = raw + (u64)u * 4;
       const bool st = !(PROF && a.dbg == 3);
-      if (MODE == 2) epi_drain<2>(tl, raw_u, &acce, st);
+      if (VV == 32) epi_drain5(tl, raw_u, &acce, st);
+      else if (MODE == 2) epi_drain<2>(tl, raw_u, &acce, st);
       else if (MODE == 3 && g == 1) epi_drain<4>(tl, raw_u, &acce, st);
       else if (g == 0) epi_drain<0>(tl, raw_u, &acce, st);
       else epi_drain<1>(tl, raw_u, &acce, st);
@@ -912,16 +982,17 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       // shares those SMSPs with producer warps)
       long long c2 = clk();
       for (int pass = 0; pass < (warp == kMmaWarp ? 0 : (warp == 1 ? 1 : 2)); ++pass) {
-        u32 ur = u, vbeg = 0, vend = (u32)kV;
+        u32 ur = u, vbeg = 0, vend = (u32)VV;
         if (pass == 1) {                 // warp 0's rows, once all 4 warps drained the unit
           mbar_wait<32>(&acce, nunit & 1, ab);
           ur = (u32)lane;
-          vbeg = warp == 2 ? 0u : (u32)kV / 2;
-          vend = vbeg + (u32)kV / 2;
+          vbeg = warp == 2 ? 0u : (u32)VV / 2;
+          vend = vbeg + (u32)VV / 2;
         }
         const u32* rr_ = raw + (u64)ur * 4;
-        const u64 kbase = (u64)chunk * kChunk + (u64)ur * kV;   // multiple of 8; ldp multiple of 8
-        if (MODE == 2) fold_row<2>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
+        const u64 kbase = (u64)chunk * chunk_pts(VV) + (u64)ur * VV;   // multiple of 8; ldp multiple of 8
+        if (VV == 32) fold_row<5, 32>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
+        else if (MODE == 2) fold_row<2>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
         else if (MODE == 3 && g == 1) fold_row<4>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
         else if (g == 0) fold_row<0>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
         else fold_row<1>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
@@ -953,11 +1024,12 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
 // rows of L), its Shoup constant and the Montgomery table m^{rr V} (rr < 8) -- and, for the
 // per-pass chunk seeds, Montgomery m^V and m^{kChunk}.
 // (The swapped form's records -- chain multiplier m^8, table m^{rr} -- are written by k_tc_gplanes.)
+template <int V>
 static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __restrict__ C, u64* __restrict__ MS,
                                   ModParams mp) {
   for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < t_pad; q += (u64)gridDim.x * blockDim.x) {
     const u64 mm = to_mont(m[q], mp);
-    const u64 mV = mont_pow(mm, kV, mp);
+    const u64 mV = mont_pow(mm, V, mp);
     u64 g = mp.r1;                                     // Montgomery m^{rr V}
     for (int rr = 0; rr < 8; ++rr) {
       C[q * kCRec + kC_g0 + rr] = g;
@@ -982,7 +1054,7 @@ static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __r
 // 2^digits is exact for the MMAs, so LAZY chains (values < 4p) serve 2^31 <= p < 2^62 (8 digits, or 7
 // when p < 2^54: 4p < 2^56) and exact-quotient ones (< 2p) the 4-digit (p < 2^31) and p >= 2^62 modes.
 constexpr int kRpThreads = 256;
-template <bool LAZY>
+template <bool LAZY, int V>
 static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __restrict__ m, u64 t_pad,
                                                                   uint8_t* __restrict__ Rp, ModParams mp) {
   const u64 nkb = 2 * ((t_pad + 2 * kKB - 1) / (2 * kKB));   // Rp is allocated for whole pairs of K-blocks
@@ -1012,9 +1084,9 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
       if (r & 4) x = mont_mul(x, v4, mp);
       y[e] = x;                                          // m^r (Montgomery residue)
     }
-    uint8_t* dst = Rp + blk * kRBytes + h * kLBOB + r * 16u + ql * 4u;
+    uint8_t* dst = Rp + blk * r_bytes(V) + h * lbo_b(V) + r * 16u + ql * 4u;
 #pragma unroll 1
-    for (u32 j = 0; j < (u32)kV / 8; ++j) {              // row r + 8j
+    for (u32 j = 0; j < (u32)V / 8; ++j) {               // row r + 8j
       const u32 l0 = lo32(y[0]), l1 = lo32(y[1]), l2 = lo32(y[2]), l3 = lo32(y[3]);
       const u32 h0 = hi32(y[0]), h1 = hi32(y[1]), h2 = hi32(y[2]), h3 = hi32(y[3]);
       u32 wd[8];
@@ -1023,8 +1095,8 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
       a = prmt(h0, h1, 0x5140); b = prmt(h2, h3, 0x5140); c = prmt(h0, h1, 0x7362); d = prmt(h2, h3, 0x7362);
       wd[4] = prmt(a, b, 0x5410); wd[5] = prmt(a, b, 0x7632); wd[6] = prmt(c, d, 0x5410); wd[7] = prmt(c, d, 0x7632);
 #pragma unroll
-      for (int t = 0; t < 8; ++t) *(u32*)(dst + (u32)t * kPlaneB + j * 128u) = wd[t];
-      if (j + 1 < (u32)kV / 8) {                         // row r + 8(j+1) = row r + 8j times m^8
+      for (int t = 0; t < 8; ++t) *(u32*)(dst + (u32)t * plane_b(V) + j * 128u) = wd[t];
+      if (j + 1 < (u32)V / 8) {                         // row r + 8(j+1) = row r + 8j times m^8
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           y[e] = LAZY ? mul_shoup4(y[e], m8[e], w8[e], mp.np) : mul_shoup2(y[e], m8[e], w8[e], mp.np);
@@ -1118,14 +1190,15 @@ static __global__ void __launch_bounds__(kGpThreads) k_tc_gplanes(const u64* __r
 constexpr u32 kSeedChunks = 4;
 // Terms [q0, q1) only (a row block of pe_eval); LS keeps its [nch][t_pad] layout.
 static __global__ void k_tc_seed(const u64* __restrict__ c, const u64* __restrict__ m, const u64* __restrict__ MS,
-                                 u64 t_pad, u64 q0, u64 q1, u32 nch, u64 js0, u64* __restrict__ LS, ModParams mp) {
+                                 u64 t_pad, u64 q0, u64 q1, u32 nch, u32 chunk, u64 js0, u64* __restrict__ LS,
+                                 ModParams mp) {
   const u32 ngrp = (nch + kSeedChunks - 1) / kSeedChunks;
   const u64 nq = q1 - q0, total = nq * ngrp;
   for (u64 x = blockIdx.x * (u64)blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
     const u64 grp = x / nq, q = q0 + (x - grp * nq);
     const u32 ch0 = (u32)grp * kSeedChunks, ch1 = min(nch, ch0 + kSeedChunks);
     const u64 mC = MS[2 * q + 1];                        // Montgomery m^{kChunk}
-    u64 s = seed_pow(c[q], m[q], js0 + (u64)ch0 * kChunk, mp);   // normal form, < p
+    u64 s = seed_pow(c[q], m[q], js0 + (u64)ch0 * chunk, mp);   // normal form, < p
     for (u32 ch = ch0; ch < ch1; ++ch) {
       LS[(u64)ch * t_pad + q] = s;
       s = mont_mul(s, mC, mp);                           // normal x Montgomery -> normal
