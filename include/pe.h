@@ -60,14 +60,16 @@ enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_INT32 = 4, P
  * env PE_FAST=0 off, 2 always.  Bit-identical results. */
 /* PE_PATH_TC forces the tensor-core form of the step (any p < 2^63; for 2^62 <= p the giant-step
  * chains use the exact-quotient Shoup product so every value keeps 8 bytes): each bucket's
- * block of T_c = 128 x 64 points is the product L * R of giant-step values c_i m_i^{j_s+64u} and
- * baby-step values m_i^v (the Vandermonde structure M_i(beta^t) = m_i^t, PAPER.md:420-427,
- * 465-478), computed exactly as 64 byte-by-byte int8 tcgen05 MMAs; the baby-step
- * planes are built once per handle (about 530 B per padded term of device memory).
+ * block of T_c = 128 x V points is the product L * R of giant-step values c_i m_i^{j_s+Vu} and
+ * baby-step values m_i^v, v < V (the Vandermonde structure M_i(beta^t) = m_i^t, PAPER.md:420-427,
+ * 465-478), computed exactly as 64 byte-by-byte int8 tcgen05 MMAs; V = 32 for
+ * p >= 2^54 (4096-point chunks, all 15 byte diagonals in one round), V = 64 below; the baby-step
+ * planes are built once per handle (about 260 B per padded term of device memory at V = 32,
+ * 530 B at V = 64).
  * PE_PATH_AUTO selects it for any p < 2^63 once T reaches the handle's measured threshold
  * (pe_tc_info): for 2^31 <= p, T >= 512 with >= 5*10^5 padded terms, else T >= 8.6e7 / t_pad clamped
  * to [512, 8192]; for p < 2^31 (against the 32-bit scalar core) T >= 9.5e7 / t_pad clamped to
- * [768, 8192].  It also needs one 8192-point chunk of partial rows (8 B x pieces x rounds per point)
+ * [768, 8192].  It also needs one chunk of partial rows (8 B x pieces x rounds per point)
  * to fit the partial-buffer cap (env PE_PARTIAL_MB, default 1024), and its handle memory to fit the
  * device (and env PE_TC_MEM_MB if set): otherwise an automatic handle degrades to the scalar
  * k_step (same results).  env PE_TC=0 off, 1 auto, 2 always; PE_PATH_INT never uses it.  Results
