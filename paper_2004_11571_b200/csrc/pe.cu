@@ -582,8 +582,8 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
     const int form = h->tc_form_req != PE_TC_FORM_AUTO ? h->tc_form_req
                    : (env_int("PE_TC_SWAP", 0) ? PE_TC_FORM_SWAPPED : PE_TC_FORM_PLAIN);
     h->tc_swap = h->p >= (1ull << 54) && form == PE_TC_FORM_SWAPPED;
-    // plain 8-digit modes (p >= 2^54): the single-round V = 32 geometry (256 B of planes per term)
-    h->tc_v = (!h->tc_swap && h->p >= (1ull << 54)) ? 32u : 64u;
+    // 8-digit modes (p >= 2^54), plain or swapped: the single-round V = 32 geometry (tc.cuh mode_v)
+    h->tc_v = h->p >= (1ull << 54) ? 32u : 64u;
     h->tc_chunk = tc::chunk_pts((int)h->tc_v);
     const u64 plane_bytes = h->tc_swap ? (tp + tc::kKB - 1) / tc::kKB * tc::kGBytes : nrblk * 2 * tc::r_bytes((int)h->tc_v);
     const u64 tc_bytes = (u64)tc::kCRec * 8 * tp + 16 * tp + plane_bytes;
@@ -612,9 +612,9 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
       const u64 ngp = 2 * ((tp + tc::kKB - 1) / tc::kKB);        // warp tasks (K-block, K half)
       const unsigned gpg = (unsigned)std::max<u64>(1, std::min<u64>((ngp + 7) / 8, 148ull * 8));
       if (h->p < (1ull << 62))
-        tc::k_tc_gplanes<true><<<gpg, tc::kGpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->d_tcC, h->d_tcMS, h->mp);
+        tc::k_tc_gplanes<true, 32><<<gpg, tc::kGpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->d_tcC, h->d_tcMS, h->mp);
       else
-        tc::k_tc_gplanes<false><<<gpg, tc::kGpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->d_tcC, h->d_tcMS, h->mp);
+        tc::k_tc_gplanes<false, 32><<<gpg, tc::kGpThreads, 0, s>>>(h->d_m, tp, h->d_tcR, h->d_tcC, h->d_tcMS, h->mp);
       CU(cudaGetLastError());
     } else {
       cudaStream_t s2 = nullptr;

@@ -88,7 +88,7 @@ constexpr u32 kRBytes = 2 * kLBOB;                    // one K-block's R planes 
 // planes, slots s .. s + 7) -- with half the baby-step plane bytes per term (256 B) and one fold +
 // REDC per point instead of one per round.  The 4-digit (7 diagonals in one round), 7-digit and
 // swapped modes keep V = 64.
-__host__ __device__ constexpr int mode_v(int MODE) { return MODE <= 1 ? 32 : 64; }
+__host__ __device__ constexpr int mode_v(int MODE) { return (MODE == 2 || MODE == 3) ? 64 : 32; }
 __host__ __device__ constexpr u32 plane_b(int V) { return (u32)V * 16; }      // one R plane, one K half
 __host__ __device__ constexpr u32 lbo_b(int V) { return 8 * plane_b(V); }     // R planes' K-half stride
 __host__ __device__ constexpr u32 r_bytes(int V) { return 2 * lbo_b(V); }     // one K-block's R planes
@@ -812,7 +812,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
     const u32 term0 = (u32)sub * 16 + tq * 4;     // first of the lane's 4 terms
     const u32 stage0 = smem_u32(smem) + (u32)my_stage * kStageBytes;
     constexpr bool SW = MODE >= 4;                        // swapped form: generate R' into the B half
-    const u32 planes0 = SW ? stage0 + 8 * kPlaneA + plane_off<kLBOB>(rr, term0) : stage0 + plane_off<kLBOA>(rr, term0);
+    const u32 planes0 = SW ? stage0 + 8 * kPlaneA + plane_off<lbo_b(mode_v(MODE))>(rr, term0) : stage0 + plane_off<kLBOA>(rr, term0);
     const u32 seed_off = term0 * kLSRec * 8;
     const u32 mul_off = kDataLS + (term0 * kCRec + kC_mL) * 8;
     const u32 g_off = kDataLS + (term0 * kCRec + kC_g0 + rr) * 8;
@@ -866,15 +866,17 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       if (loader && ahead.valid)
         load_kblock(a, ahead, data0 + (slot0 + ((guse + 1) & 1)) * kDataSlot, &dfull[slot0 + ((guse + 1) & 1)]);
       if (SW && !(PROF && (a.dbg == 2 || a.dbg >= 6))) {
-        // baby-step rows rr + 8k (k < 8) of R' = c m^{j_s + v}
+        // baby-step rows rr + 8k (k < V / 8) of R' = c m^{j_s + v}
+        constexpr int VV8 = mode_v(MODE) / 8;
+        constexpr u32 PB = plane_b(mode_v(MODE));
 #pragma unroll
-        for (int k = 0; k < 7; ++k) {
-          store_digits<kPlaneB>(planes0 + (u32)k * 128u, x);
+        for (int k = 0; k < VV8 - 1; ++k) {
+          store_digits<PB>(planes0 + (u32)k * 128u, x);
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             x[e] = MODE == 5 ? mul_shoup2(x[e], sm[e], sw[e], np) : mul_shoup4(x[e], sm[e], sw[e], np);
         }
-        store_digits<kPlaneB>(planes0 + 7u * 128u, x);
+        store_digits<PB>(planes0 + (u32)(VV8 - 1) * 128u, x);
       } else if (!(PROF && (a.dbg == 2 || a.dbg >= 6))) {
 #pragma unroll 3
         for (int k = 0; k < 15; ++k) {
@@ -1114,7 +1116,7 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
 // shuffled to the group's 8 lanes; the same lane also writes the term's C record (the swapped
 // chain's m^8, its Shoup constant, Montgomery m^{rr} for rr < 8) and seed powers (m^V, m^{kChunk}).
 constexpr int kGpThreads = 256;
-template <bool LAZY>
+template <bool LAZY, int V>
 static __global__ void __launch_bounds__(kGpThreads) k_tc_gplanes(const u64* __restrict__ m, u64 t_pad,
                                                                   uint8_t* __restrict__ Gp, u64* __restrict__ C,
                                                                   u64* __restrict__ MS, ModParams mp) {
@@ -1131,7 +1133,7 @@ static __global__ void __launch_bounds__(kGpThreads) k_tc_gplanes(const u64* __r
     const u64 mm = to_mont(q < t_pad ? m[q] : 0ull, mp);
     u64 mV = mm;
 #pragma unroll 1
-    for (int i = 0; i < 6; ++i) mV = mont_mul(mV, mV, mp);   // m^V, V = 64
+    for (int i = 0; (1 << i) < V; ++i) mV = mont_mul(mV, mV, mp);   // m^V (V a power of 2)
     const u64 m2V = mont_mul(mV, mV, mp), m4V = mont_mul(m2V, m2V, mp);
     const u64 m8V = mont_mul(m4V, m4V, mp);
     if (r < 4 && q < t_pad) {                            // the term's C record and seed powers
