@@ -577,28 +577,38 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
     // §6, ~624 B per padded term).  If it does not fit (the device, or the env cap PE_TC_MEM_MB),
     // an automatic handle degrades to the scalar k_step; a forced one (PE_PATH_TC) fails.
     const u64 nrblk = (tp + 2 * tc::kKB - 1) / (2 * tc::kKB);
-    // 8-digit primes (p >= 2^54) may use the swapped form (tc.cuh): pe_config.tc_form, or with
-    // PE_TC_FORM_AUTO the env override PE_TC_SWAP=1 (default plain)
-    const int form = h->tc_form_req != PE_TC_FORM_AUTO ? h->tc_form_req
-                   : (env_int("PE_TC_SWAP", 0) ? PE_TC_FORM_SWAPPED : PE_TC_FORM_PLAIN);
+    // 8-digit primes (p >= 2^54): the swapped form (tc.cuh; giant-step planes per handle, 1 KB per
+    // term) unless pe_config.tc_form asks for the plain one; with PE_TC_FORM_AUTO the env override
+    // PE_TC_SWAP=0/1 decides, and an automatic swapped handle whose planes do not fit (the device,
+    // or PE_TC_MEM_MB) falls back to the plain form (256 B per term) before the scalar k_step.
+    const bool auto_form = h->tc_form_req == PE_TC_FORM_AUTO;
+    const int form = !auto_form ? h->tc_form_req
+                   : (env_int("PE_TC_SWAP", 1) ? PE_TC_FORM_SWAPPED : PE_TC_FORM_PLAIN);
     h->tc_swap = h->p >= (1ull << 54) && form == PE_TC_FORM_SWAPPED;
     // 8-digit modes (p >= 2^54), plain or swapped: the single-round V = 32 geometry (tc.cuh mode_v)
     h->tc_v = h->p >= (1ull << 54) ? 32u : 64u;
     h->tc_chunk = tc::chunk_pts((int)h->tc_v);
-    const u64 plane_bytes = h->tc_swap ? (tp + tc::kKB - 1) / tc::kKB * tc::kGBytes : nrblk * 2 * tc::r_bytes((int)h->tc_v);
-    const u64 tc_bytes = (u64)tc::kCRec * 8 * tp + 16 * tp + plane_bytes;
     const u64 cap = (u64)std::max(0, env_int("PE_TC_MEM_MB", 0)) << 20;
     int rc = PE_OK;
-    if (cap && tc_bytes > cap) rc = PE_ENOMEM;
-    if (rc == PE_OK && (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp) || dalloc(&h->d_tcMS, (size_t)2 * tp) ||
-                        dalloc(&h->d_tcR, (size_t)plane_bytes)))
-      rc = g_last_error;
-    if (rc != PE_OK) {
-      if (h->tc_mode == 2 || rc != PE_ENOMEM) return set_err(rc);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      const u64 plane_bytes = h->tc_swap ? (tp + tc::kKB - 1) / tc::kKB * tc::kGBytes : nrblk * 2 * tc::r_bytes((int)h->tc_v);
+      const u64 tc_bytes = (u64)tc::kCRec * 8 * tp + 16 * tp + plane_bytes;
+      rc = PE_OK;
+      if (cap && tc_bytes > cap) rc = PE_ENOMEM;
+      if (rc == PE_OK && (dalloc(&h->d_tcC, (size_t)tc::kCRec * tp) || dalloc(&h->d_tcMS, (size_t)2 * tp) ||
+                          dalloc(&h->d_tcR, (size_t)plane_bytes)))
+        rc = g_last_error;
+      if (rc == PE_OK) break;
+      if (rc != PE_ENOMEM) return set_err(rc);
       for (void** q : {(void**)&h->d_tcC, (void**)&h->d_tcMS, (void**)&h->d_tcR})
         if (*q) { cudaFreeAsync(*q, s); *q = nullptr; }
       cudaGetLastError();               // allocation failures are not sticky; clear the record
       g_last_error = PE_OK;
+      if (!(auto_form && h->tc_swap)) break;
+      h->tc_swap = false;               // automatic form: retry with the plain form's smaller planes
+    }
+    if (rc != PE_OK) {
+      if (h->tc_mode == 2) return set_err(rc);
       h->tc_mode = 0;                   // the rest of the tensor-path setup is skipped below
     }
   }

@@ -76,24 +76,28 @@ def config5_ref():
     return w, full
 
 
-@pytest.mark.parametrize("path,compact", [(pe.PATH_AUTO, False), (pe.PATH_INT, False), (pe.PATH_AUTO, True)])
-def test_config5_full(path, compact, config5_ref):
-    """Full size in the bench launch configuration (PATH_AUTO = the tensor-core k_tc; PATH_INT = the
-    scalar k_step; compact = the uint8-exponent entry pe_create_compact), compared over the WHOLE
-    G x T output with the incremental checker, plus 24
-    columns against the direct definition -- chosen to hit every TMEM lane quarter (u = 0..127 in
-    groups of 32) of both 8192-point chunks, the chunk edges and v = 0 / 63."""
+@pytest.mark.parametrize("path,compact,form", [(pe.PATH_AUTO, False, pe.TC_FORM_AUTO), (pe.PATH_INT, False, pe.TC_FORM_AUTO),
+                                              (pe.PATH_AUTO, True, pe.TC_FORM_AUTO), (pe.PATH_TC, False, pe.TC_FORM_PLAIN)])
+def test_config5_full(path, compact, form, config5_ref):
+    """Full size in the bench launch configuration (PATH_AUTO = the tensor-core k_tc in its default
+    swapped form; PATH_TC + TC_FORM_PLAIN = its plain form; PATH_INT = the scalar k_step; compact =
+    the uint8-exponent entry pe_create_compact), compared over the WHOLE G x T output with the
+    incremental checker, plus columns against the direct definition -- chosen to hit every TMEM lane
+    quarter (u = 0..127 in groups of 32) of the four 4096-point chunks (128 x 32 points, the V = 32
+    geometry of p >= 2^54), the chunk edges and v = 0 / 31."""
     w, full = config5_ref
-    with pe.Context.from_workload(w, path=path, compact=compact) as ctx:
-        assert ctx.uses_tc(w.T) == (path == pe.PATH_AUTO)
+    with pe.Context.from_workload(w, path=path, compact=compact, tc_form=form) as ctx:
+        assert ctx.uses_tc(w.T) == (path != pe.PATH_INT)
+        if path != pe.PATH_INT:
+            assert ctx.tc_form() == (pe.TC_FORM_PLAIN if form == pe.TC_FORM_PLAIN else pe.TC_FORM_SWAPPED)
         out = ctx.eval(w.j0, w.T)
         rows = ctx.buckets()
     assert rows.tolist() == oracle.buckets(w.exps, w.n).tolist()
     bad = np.argwhere(out != full)
     assert bad.size == 0, f"{len(bad)} mismatches vs the incremental checker, first {bad[:5].tolist()}"
-    ks = np.array(sorted({0, 1, 63, 64, 777, 8191, 8192, 12345, 16382, 16383}
-                         | {c * 8192 + u * 64 + v for c in (0, 1) for u in (5, 40, 77, 120) for v in (0, 33) if (u + v) % 2}
-                         | {c * 8192 + u * 64 + 63 for c in (0, 1) for u in (31, 32, 95, 96)}), np.uint64)
+    ks = np.array(sorted({0, 1, 31, 32, 777, 4095, 4096, 8191, 8192, 12345, 16382, 16383}
+                         | {c * 4096 + u * 32 + v for c in range(4) for u in (5, 40, 77, 120) for v in (0, 17) if (u + v + c) % 2}
+                         | {c * 4096 + u * 32 + 31 for c in (0, 3) for u in (31, 32, 95, 96)}), np.uint64)
     ref = oracle.eval_workload(w, ks=ks)
     assert np.array_equal(out[:, ks.astype(np.int64)], ref)
 

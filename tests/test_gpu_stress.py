@@ -34,12 +34,14 @@ def _repeat_equal(ctx, w, runs):
     return ref.cpu().numpy().view(np.uint64)
 
 
-def test_config5_repeated_launches_bitwise():
+@pytest.mark.parametrize("form", [pe.TC_FORM_AUTO, pe.TC_FORM_PLAIN])
+def test_config5_repeated_launches_bitwise(form):
     """50 back-to-back evaluations of BASELINE config 5 (t = 10^7, T = 16384: ~49 units per CTA,
-    the bench launch configuration) are bitwise identical; the first is checked on sampled columns
-    (the full G x T comparison is test_gpu_parity.py::test_config5_full)."""
+    the bench launch configuration; default swapped form and the plain form) are bitwise
+    identical; the first is checked on sampled columns (the full G x T comparison is
+    test_gpu_parity.py::test_config5_full)."""
     w = synth.gen_config(5)
-    with pe.Context.from_workload(w) as ctx:
+    with pe.Context.from_workload(w, tc_form=form) as ctx:
         assert ctx.uses_tc(w.T)
         first = _repeat_equal(ctx, w, 50)
     ks = np.array([0, 2591, 8192 + 40 * 64 + 7, 16383], np.uint64)

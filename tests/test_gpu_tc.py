@@ -275,13 +275,19 @@ def test_tc_plain_and_swapped_forms(p, form):
 
 
 def test_tc_form_defaults_and_limits(monkeypatch):
-    """Automatic = plain; the swapped form only exists for 8-digit primes (below 2^54 a request for
-    it builds the plain form, whose 7- and 4-digit modes read baby-step planes); out-of-range
-    tc_form values are PE_EINVAL."""
+    """Automatic = swapped for 8-digit primes (PE_TC_SWAP=0 makes it plain); the swapped form only
+    exists for 8-digit primes (below 2^54 a request for it builds the plain form, whose 7- and
+    4-digit modes read baby-step planes); out-of-range tc_form values are PE_EINVAL."""
     monkeypatch.delenv("PE_TC_SWAP", raising=False)
     w = synth.random_small(599, P62, 5, 300, 3, 100, 1)
     with pe.Context.from_workload(w, path=pe.PATH_TC) as ctx:
+        assert ctx.tc_form() == pe.TC_FORM_SWAPPED
+    monkeypatch.setenv("PE_TC_SWAP", "0")
+    with pe.Context.from_workload(w, path=pe.PATH_TC) as ctx:
         assert ctx.tc_form() == pe.TC_FORM_PLAIN
+    with pe.Context.from_workload(w, path=pe.PATH_TC, tc_form=pe.TC_FORM_SWAPPED) as ctx:
+        assert ctx.tc_form() == pe.TC_FORM_SWAPPED   # an explicit request beats the env override
+    monkeypatch.delenv("PE_TC_SWAP", raising=False)
     w2 = synth.random_small(598, (1 << 50) - 27, 5, 300, 3, 100, 1)
     with pe.Context.from_workload(w2, path=pe.PATH_TC, tc_form=pe.TC_FORM_SWAPPED) as ctx:
         assert ctx.tc_form() == pe.TC_FORM_PLAIN
@@ -291,3 +297,23 @@ def test_tc_form_defaults_and_limits(monkeypatch):
     with pytest.raises(pe.PEError) as e:
         pe.Context.from_workload(w, tc_form=3)
     assert e.value.code == -1
+
+
+def test_auto_form_falls_back_to_plain_when_memory_is_short(monkeypatch):
+    """An automatic handle whose swapped-form planes (1 KB per term) exceed PE_TC_MEM_MB but whose
+    plain-form planes (256 B per term) fit gets the plain form -- same bits, checked against the
+    oracle; a cap below both leaves it on k_step."""
+    monkeypatch.delenv("PE_TC_SWAP", raising=False)
+    w = synth.gen_config(3)   # 10^6 terms: swapped ~1.1 GB, plain ~0.36 GB of tensor-path memory
+    ks = np.array([0, 1, 777, w.T - 1], np.uint64)
+    ref = oracle.eval_workload(w, ks=ks)
+    monkeypatch.setenv("PE_TC_MEM_MB", "600")
+    with pe.Context.from_workload(w) as ctx:
+        assert ctx.tc_form() == pe.TC_FORM_PLAIN and ctx.uses_tc(w.T)
+        out = ctx.eval(w.j0, w.T)
+    assert np.array_equal(out[:, ks.astype(np.int64)], ref)
+    monkeypatch.setenv("PE_TC_MEM_MB", "100")
+    with pe.Context.from_workload(w) as ctx:
+        assert ctx.tc_form() == 0 and not ctx.uses_tc(w.T)
+        out = ctx.eval(w.j0, w.T)
+    assert np.array_equal(out[:, ks.astype(np.int64)], ref)
