@@ -132,3 +132,69 @@ def test_swapped_form_reduction(seed):
             acc += x[k] * pow(2, 32 * k, p)
         total += redc((acc >> 64) % p, acc & ((1 << 64) - 1), p)
     assert total % p == want
+
+
+def issue_all32_emulated(Lbytes, Rbytes, nkb):
+    """Emulates tc.cuh issue_all32 over nkb K-blocks on byte planes: per K-block, L plane s times
+    the 8 baby-step planes t is ONE MMA into slots s .. s + 7 (slot d = s + t); at K-block 0 plane 0
+    overwrites slots 0..7, plane 7 goes second split into t = 0 (accumulates slot 7) and t = 1..7
+    (overwrites slots 8..14), planes 1..6 accumulate.  Slots start as garbage, as TMEM does.
+    Lbytes[s][i], Rbytes[t][i]: byte s / t of term i; a K-block is 32 consecutive terms."""
+    rng = random.Random(7)
+    slot = [rng.getrandbits(32) for _ in range(15)]          # uninitialised TMEM
+
+    def mma(s, t_lo, t_hi, kb, acc):
+        for t in range(t_lo, t_hi + 1):
+            part = sum(Lbytes[s][i] * Rbytes[t][i] for i in range(32 * kb, 32 * kb + 32))
+            slot[s + t] = ((slot[s + t] if acc else 0) + part) % (1 << 32)
+
+    for kb in range(nkb):
+        first = kb == 0
+        mma(0, 0, 7, kb, not first)
+        if first:
+            mma(7, 0, 0, kb, True)
+            mma(7, 1, 7, kb, False)
+        else:
+            mma(7, 0, 7, kb, True)
+        for s in range(1, 7):
+            mma(s, 0, 7, kb, True)
+    return slot
+
+
+@pytest.mark.parametrize("seed,swapped", [(0, False), (1, False), (2, True), (3, True)])
+def test_single_round_v32_schedule_and_reduction(seed, swapped):
+    """The V = 32 geometry of the 8-digit modes (tc.cuh issue_all32 / epi_drain5 / fold_row<5, 32>):
+    the emulated kb-0 initialisation scheme reproduces every diagonal D_d of the byte-diagonal
+    identity exactly (mod 2^32, as the s32 TMEM accumulator), and ONE fold of all 15 diagonals
+    (X < 2^145) plus one REDC gives sum_i c_i m_i^{j_s + 32u + v} mod p -- plain form (lazy giant
+    steps c m^{j_s + 32u} x Montgomery baby steps m^v 2^64) and swapped form (Montgomery giant steps
+    m^{32u} 2^64 x lazy baby steps c m^{j_s + v}) alike.  Python integers, no kernel code."""
+    rng = random.Random(300 + seed)
+    p = P62
+    R64 = (1 << 64) % p
+    nkb = 3
+    n = 32 * nkb
+    c = [rng.randrange(p) for _ in range(n)]
+    m = [rng.randrange(1, p) for _ in range(n)]
+    js, u, v = rng.randrange(1, 1 << 40), rng.randrange(128), rng.randrange(32)
+    if swapped:
+        A = [(pow(mi, 32 * u, p) * R64) % p for mi in m]
+        B = [(ci * pow(mi, js + v, p)) % p + rng.randrange(4) * p for ci, mi in zip(c, m)]
+        B = [x if x < (1 << 64) else x - p for x in B]
+    else:
+        A = [(ci * pow(mi, js + 32 * u, p)) % p + rng.randrange(4) * p for ci, mi in zip(c, m)]
+        A = [x if x < (1 << 64) else x - p for x in A]
+        B = [(pow(mi, v, p) * R64) % p for mi in m]
+    want = sum(ci * pow(mi, js + 32 * u + v, p) for ci, mi in zip(c, m)) % p
+    Ab = [[(x >> (8 * s)) & 0xFF for x in A] for s in range(8)]
+    Bb = [[(x >> (8 * t)) & 0xFF for x in B] for t in range(8)]
+    slots = issue_all32_emulated(Ab, Bb, nkb)
+    assert slots == diagonals(A, B)                          # every D_d < 2^32 here: exact
+    X = sum(slots[d] << (8 * d) for d in range(15))
+    assert X < (1 << 145)
+    x = [(X >> (32 * k)) & 0xFFFFFFFF for k in range(5)]
+    acc = x[0] | (x[1] << 32)
+    for k in (2, 3, 4):
+        acc += x[k] * pow(2, 32 * k, p)
+    assert (acc >> 64) < p                                   # REDC's precondition without the fallback
+    assert redc(acc >> 64, acc & ((1 << 64) - 1), p) == want
