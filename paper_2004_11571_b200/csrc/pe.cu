@@ -12,6 +12,7 @@
 #include <cub/iterator/counting_input_iterator.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <map>
 #include <mutex>
@@ -289,8 +290,18 @@ static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStrea
 // 10^5 terms, ~480 for 10^6 (k_step INT), 512 vs FP64 Alg. 2 -- i.e. T* ~ 8.6e7 / t_pad, >= 512.
 // p < 2^31 competes with the 4-IMAD-slot 32-bit Shoup k_step instead: crossovers T ~ 770 (10^6
 // terms) and ~930 (10^5) against k_tc's 4-digit mode (scripts/tc_threshold_p31.py).
+// p >= 2^54 (the V = 32 geometry, 4096-point chunks; scripts/tc_threshold_v32.py,
+// profiles/r02_tc_threshold_v32.jsonl): crossovers T ~ 540 / 380 / 280 / 235 at 1.3e4 / 1.0e5 /
+// 3.1e5 / 1.0e6 padded terms, fitted by T* = max(3400 t_pad^-0.19, 7.3e6 / t_pad) (the second term:
+// tiny handles, where k_step's cost is ~flat while k_tc keeps its ~0.045 ms floor), in [192, 8192].
+static u64 tc_min_T_v32(u64 t_pad) {
+  const double tp = (double)std::max<u64>(t_pad, 1);
+  const double t = std::max(3400.0 * std::pow(tp, -0.19), 7.3e6 / tp);
+  return std::min<u64>(8192, std::max<u64>(192, (u64)std::ceil(t)));
+}
 static u64 tc_min_T(u64 t_pad, u64 p) {
   const u64 tp = std::max<u64>(t_pad, 1);
+  if (p >= (1ull << 54)) return tc_min_T_v32(t_pad);
   if (p < (1ull << 31)) return std::min<u64>(8192, std::max<u64>(768, 95000000ull / tp));
   if (t_pad >= 500000) return 512;
   return std::min<u64>(8192, std::max<u64>(512, 86000000ull / tp));

@@ -3,6 +3,8 @@ the C ABI.  The path factors each bucket's 128 x 64-point chunk into giant-step 
 values (the Vandermonde structure m_i^{j} = m_i^{j_s + 64u} m_i^{v}, u < 128, v < 64,
 PAPER.md:420-427) and sums their 64 byte-pair products on int8 tensor cores; results must be bit-identical to the oracle
 (canonical residues are unique, R14)."""
+import math
+
 import numpy as np
 import pytest
 
@@ -118,20 +120,36 @@ def test_tc_equals_scalar_step_and_fermat():
     assert np.array_equal(a, c)
 
 
+def v32_min_T(tp):
+    """pe.cu tc_min_T_v32: the automatic threshold of the V = 32 geometry (p >= 2^54), fitted to the
+    measured crossovers (profiles/r02_tc_threshold_v32.jsonl)."""
+    return min(8192, max(192, math.ceil(max(3400.0 * tp ** -0.19, 7.3e6 / tp))))
+
+
 def test_tc_auto_selection():
-    """PE_PATH_AUTO: tensor path for any p < 2^63 and T >= the handle's threshold (8.6e7 / t_pad
-    clamped to [512, 8192]; 512 from 5*10^5 padded terms); never for PE_PATH_INT or PE_PATH_FP64."""
+    """PE_PATH_AUTO: tensor path for any p < 2^63 and T >= the handle's threshold (p >= 2^54:
+    max(3400 t_pad^-0.19, 7.3e6 / t_pad) in [192, 8192]; 2^31 <= p < 2^54: 8.6e7 / t_pad clamped to
+    [512, 8192], 512 from 5*10^5 padded terms); never for PE_PATH_INT or PE_PATH_FP64."""
     w = synth.random_small(524, P62, 5, 100, 3, 10, 1)
     with pe.Context.from_workload(w) as ctx:
-        assert ctx.info()["tc_min_T"] == 8192
-        assert ctx.uses_tc(8192) and not ctx.uses_tc(8191)
+        tp = ctx.info()["t_padded"]
+        m = ctx.info()["tc_min_T"]
+        assert abs(m - v32_min_T(tp)) <= 1 and m > 4000                  # tiny handle: k_step almost always
+        assert ctx.uses_tc(m) and not ctx.uses_tc(m - 1)
     w2 = synth.gen_config(2, T=10)
     with pe.Context.from_workload(w2) as ctx:
         tp = ctx.info()["t_padded"]
-        assert ctx.info()["tc_min_T"] == max(512, 86_000_000 // tp) and ctx.uses_tc(1000)   # config 2
+        assert abs(ctx.info()["tc_min_T"] - v32_min_T(tp)) <= 1 and ctx.uses_tc(1000)   # config 2
     w3 = synth.gen_config(3, t=600_000, T=10)
     with pe.Context.from_workload(w3) as ctx:
-        assert ctx.info()["tc_min_T"] == 512 and ctx.uses_tc(512) and not ctx.uses_tc(511)
+        m = ctx.info()["tc_min_T"]
+        assert 192 <= m <= 300 and ctx.uses_tc(m) and not ctx.uses_tc(m - 1)
+    w7 = synth.gen_config(3, t=600_000, T=10)                          # 7-digit mode keeps the V = 64 rule
+    w7.p = (1 << 50) - 27
+    w7.coeffs %= np.uint64(w7.p)
+    w7.alpha %= np.uint64(w7.p)
+    with pe.Context.from_workload(w7) as ctx:
+        assert ctx.info()["tc_min_T"] == 512
     w31 = synth.random_small(527, (1 << 31) - 1, 6, 600_000 // 8, 9, 10, 1)   # p < 2^31: vs 32-bit k_step
     with pe.Context.from_workload(w31) as ctx:
         tp = ctx.info()["t_padded"]
