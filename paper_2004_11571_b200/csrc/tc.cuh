@@ -18,22 +18,28 @@
 // for <= 8192 terms per accumulation (a "piece"; the s32 TMEM accumulator wraps mod 2^32 without
 // saturation, so its bits read as u32 are exact).  X mod p = sum_d D_d (2^{8d} mod p) mod p.
 //
-// Shapes: U = M = 128 (TMEM lanes), V = 64, K-block = 32 terms (one kind::i8 MMA K step).  The
-// 15 diagonals do not fit TMEM at once (15 x 64 columns > 512), so a piece is evaluated in 2
-// rounds, d = 0..7 and d = 8..14 (slot = d - d_lo); a unit is (piece, chunk, round) and reduces
-// its own part X_g into its own partial row (X mod p = sum of the parts).  Because the round's
-// partners t of one L plane s are consecutive, and the baby-step planes sit plane after plane in
-// each K half, each (s, run of t) is ONE MMA with N = 64k <= 256 (22 MMAs per K-block for both
-// rounds).  The baby-step planes R = m^v do not depend on the points: they are built once per
-// handle and streamed into the stages by TMA, so per evaluation only the giant steps are
-// generated (1 modular product per 32 term-points).
+// Shapes: U = M = 128 (TMEM lanes), K-block = 32 terms (one kind::i8 MMA K step), V by mode
+// (mode_v):
+//   V = 32 (8-digit modes, p >= 2^54 -- config 5): all 15 diagonals fit TMEM at once (15 x 32 =
+//     480 of 512 columns), so a unit is (piece, chunk of 128 x 32 points) in ONE round: per
+//     K-block, L plane s against the 8 consecutive R planes is ONE MMA of N = 256 into slots
+//     s .. s + 7 (issue_all32), one fold + REDC per point (epi_drain5, fold_row<5, 32>).
+//   V = 64 (4- and 7-digit modes, p < 2^54): 15 (resp. 13) diagonals do not fit at once, so a
+//     piece runs in 2 rounds (d = 0..7 and 8..14, slot = d - d_lo; the 4-digit mode's 7 fit in
+//     one) and a unit is (piece, chunk, round) reducing its own part X_g into its own partial row
+//     (X mod p = sum of the parts).  A round's partners t of one L plane s are consecutive and
+//     the baby-step planes sit plane after plane in each K half, so each (s, run of t) is ONE MMA
+//     with N = 64k <= 256 (22 MMAs per K-block for both rounds).
+// The baby-step planes R = m^v do not depend on the points: they are built once per handle and
+// streamed into the stages by TMA, so per evaluation only the giant steps are generated (1
+// modular product per 32 term-points).
 //
 // Warp roles (one CTA per SM, 12 warps = 3 per SMSP, persistent; units are piece-major and dealt
-// to the CTAs in snake order):
+// to the CTAs in snake order or by the host's LPT schedule):
 //   warps 0-3  epilogue: tcgen05.ld the unit's diagonals (TMEM lane = u) into the unit's raw
 //              buffer (per-CTA, L2-resident), release TMEM; then an exact 160-bit fold of the
-//              round's diagonals and one reduction mod p per point (warps 1-3; warps 2 / 3 also
-//              cover warp 0's rows) -> partial[slot][chunk*kChunk + u*kV + v].  Warp 0 issues
+//              unit's diagonals and one reduction mod p per point (warps 1-3; warps 2 / 3 also
+//              cover warp 0's rows) -> partial[slot][chunk * 128 V + u V + v].  Warp 0 issues
 //              every unit's MMAs (tcgen05.mma.cta_group::1.kind::i8, elect.sync leader) and
 //              allocates TMEM.
 //   warps 4-11 producers, 2 per smem stage: each generates 16 terms x 128 giant-step rows of one
@@ -42,13 +48,14 @@
 //              lane copies the K-block's baby-step planes into the stage with TMA, the other's
 //              prefetches the group's next K-block of per-term records.
 //
-// Swapped form (MODE 4 / 5, 8-digit p >= 2^54, pe_config.tc_form = PE_TC_FORM_SWAPPED): the point-dependent
-// factor c m^{j_s} is folded into the baby steps instead, R'[i][v] = c_i m_i^{j_s + v}, and the
-// giant steps G[u][i] = m_i^{uV} become the point-independent factor, built once per handle
-// (k_tc_gplanes, Montgomery residues, 1 KB per term) and streamed into the A half of the stages by
-// TMA.  The producers then generate only the V = 64 baby-step rows per term and unit (half the
-// giant-step rows of the plain form) into the B half; the MMAs, the TMEM layout and the epilogue
-// are the same (sum_i G R' = 2^64 X, one REDC).
+// Swapped form (MODE 4 / 5, 8-digit p >= 2^54; the automatic form, pe_config.tc_form): the
+// point-dependent factor c m^{j_s} is folded into the baby steps instead, R'[i][v] =
+// c_i m_i^{j_s + v}, and the giant steps G[u][i] = m_i^{uV} become the point-independent factor,
+// built once per handle (k_tc_gplanes, Montgomery residues, 1 KB per term) and streamed into the
+// A half of the stages by TMA.  The producers then generate only the V = 32 baby-step rows per
+// term and unit (a quarter of the plain form's 128 giant-step rows) into the B half; the MMAs,
+// the TMEM layout and the epilogue are the same (sum_i G R' = 2^64 X, one REDC).  On config 5 the
+// tensor core then binds: 91 % tensor-pipe utilisation (profiles/r02_ktc_summary.json).
 #pragma once
 #include "modcore.cuh"
 
@@ -56,7 +63,7 @@ namespace pe {
 namespace tc {
 
 constexpr int kU = 128;                   // giant steps per chunk  (MMA M / TMEM lanes)
-constexpr int kV = 64;                    // baby steps per chunk   (MMA N)
+constexpr int kV = 64;                    // baby steps per chunk of the V = 64 modes (mode_v)
 constexpr u32 kChunk = kU * kV;           // points per chunk
 constexpr int kKB = 32;                   // terms per K-block (one i8 MMA K step)
 constexpr int kStages = 4;
