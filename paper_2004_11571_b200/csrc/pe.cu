@@ -596,8 +596,9 @@ static int create_impl(pe_ctx* h, const u64* coeffs, const E* exps, const u64* a
     const int form = !auto_form ? h->tc_form_req
                    : (env_int("PE_TC_SWAP", 1) ? PE_TC_FORM_SWAPPED : PE_TC_FORM_PLAIN);
     h->tc_swap = h->p >= (1ull << 54) && form == PE_TC_FORM_SWAPPED;
-    // 8-digit modes (p >= 2^54), plain or swapped: the single-round V = 32 geometry (tc.cuh mode_v)
-    h->tc_v = h->p >= (1ull << 54) ? 32u : 64u;
+    // 7- and 8-digit modes (p >= 2^31), plain or swapped: the single-round V = 32 geometry (tc.cuh
+    // mode_v); the 4-digit mode (p < 2^31) keeps V = 64 (its 7 diagonals already fit one round)
+    h->tc_v = h->p >= (1ull << 31) ? 32u : 64u;
     h->tc_chunk = tc::chunk_pts((int)h->tc_v);
     const u64 cap = (u64)std::max(0, env_int("PE_TC_MEM_MB", 0)) << 20;
     int rc = PE_OK;

@@ -95,7 +95,7 @@ constexpr u32 kRBytes = 2 * kLBOB;                    // one K-block's R planes 
 // planes, slots s .. s + 7) -- with half the baby-step plane bytes per term (256 B) and one fold +
 // REDC per point instead of one per round.  The 4-digit (7 diagonals in one round), 7-digit and
 // swapped modes keep V = 64.
-__host__ __device__ constexpr int mode_v(int MODE) { return (MODE == 2 || MODE == 3) ? 64 : 32; }
+__host__ __device__ constexpr int mode_v(int MODE) { return MODE == 2 ? 64 : 32; }
 __host__ __device__ constexpr u32 plane_b(int V) { return (u32)V * 16; }      // one R plane, one K half
 __host__ __device__ constexpr u32 lbo_b(int V) { return 8 * plane_b(V); }     // R planes' K-half stride
 __host__ __device__ constexpr u32 r_bytes(int V) { return 2 * lbo_b(V); }     // one K-block's R planes
@@ -117,12 +117,13 @@ static_assert(kSmemBytes + 256 <= 232448, "shared memory");
 // one wide MMA (B = planes t..t+k-1, N = 64k <= 256) covers k of them
 // group 2: the single round of the 4-digit mode (p < 2^31: values < 2^32), d = 0..6
 // group 4: the 7-digit mode's second round, d = 8..12
-// group 5: the single round of the V = 32 geometry, d = 0..14 in slots 0..14
+// group 5: the single round of the V = 32 geometry, d = 0..14 in slots 0..14 (8 digits);
+// group 6: the same for 7 digits (2^31 <= p < 2^54), d = 0..12 in slots 0..12
 __host__ __device__ constexpr int group_diag(int g, int di) {
   return g == 0 ? (di < 8 ? di : -1) : g == 1 ? (di < 7 ? 8 + di : -1) : g == 2 ? (di < 7 ? di : -1)
-       : g == 5 ? (di < 15 ? di : -1) : (di < 5 ? 8 + di : -1);
+       : g == 5 ? (di < 15 ? di : -1) : g == 6 ? (di < 13 ? di : -1) : (di < 5 ? 8 + di : -1);
 }
-__host__ __device__ constexpr int nslots(int g) { return g == 5 ? 15 : kDiag; }
+__host__ __device__ constexpr int nslots(int g) { return g == 5 ? 15 : g == 6 ? 13 : kDiag; }
 
 struct TcArgs {
   const u64* LS;         // [nch][t_pad] chunk seeds c m^{j_s}
@@ -286,6 +287,23 @@ __device__ __forceinline__ void issue_all32(u32 tb, uint64_t da, uint64_t db, bo
   }
 #pragma unroll
   for (int sd = 1; sd < 7; ++sd) mma_u8n<0>(tb + (u32)sd * V, da + (uint64_t)(sd * PA), db, idesc_n(256), 1u);
+}
+
+// The 7-digit modes (2^31 <= p < 2^54: lazy values < 4p < 2^56) on the V = 32 geometry: L plane s
+// (s < 7) against the 7 baby-step planes t < 7 is one MMA of N = 224 into slots s .. s + 6 (13
+// slots, 416 columns); at K-block 0 plane 0 initialises slots 0..6 and plane 6, split, initialises
+// slots 7..12 (its t = 0 part accumulates into slot 6).
+__device__ __forceinline__ void issue_all32_7(u32 tb, uint64_t da, uint64_t db, bool first_kb) {
+  constexpr u32 V = 32, PB = plane_b(32) >> 4, PA = kPlaneA >> 4;
+  mma_u8n<0>(tb, da, db, idesc_n(224), first_kb ? 0u : 1u);
+  if (first_kb) {
+    mma_u8n<1>(tb + 6 * V, da + 6 * PA, db, idesc_n(32), 1u);
+    mma_u8n<2>(tb + 7 * V, da + 6 * PA, db + PB, idesc_n(192), 0u);
+  } else {
+    mma_u8n<0>(tb + 6 * V, da + 6 * PA, db, idesc_n(224), 1u);
+  }
+#pragma unroll
+  for (int sd = 1; sd < 6; ++sd) mma_u8n<0>(tb + (u32)sd * V, da + (uint64_t)(sd * PA), db, idesc_n(224), 1u);
 }
 
 // The 4-digit mode (p < 2^31): 16 digit pairs, diagonals 0..6 in one round, as 5 MMAs.  No L plane
@@ -586,31 +604,32 @@ __device__ __forceinline__ void epi_drain(u32 tl, u32* __restrict__ raw_u, uint6
 // The single-round geometry (G = 5, V = 32): 15 diagonals x 32 columns as 16 blocks of 4 diagonals
 // x 8 columns (block b: v0 = 8 (b / 4), diagonals 4 (b % 4) ..), each block's tcgen05.ld in flight
 // while the previous block is stored.
-template <int H>
-__device__ __forceinline__ void drain5_ld(u32 tl, int b, u32 (&D)[4][8]) { drain_ld<5, H, 32>(tl, (u32)(b / 4) * 8, D); }
+template <int G, int H>
+__device__ __forceinline__ void drain5_ld(u32 tl, int b, u32 (&D)[4][8]) { drain_ld<G, H, 32>(tl, (u32)(b / 4) * 8, D); }
+template <int G>
 __device__ __forceinline__ void epi_drain5(u32 tl, u32* __restrict__ raw_u, uint64_t* acce, bool st = true) {
   u32 A[4][8], B[4][8];
-  drain5_ld<0>(tl, 0, A);
+  drain5_ld<G, 0>(tl, 0, A);
   tmem_wait_ld();
-  drain_fence<5, 0>(A);
+  drain_fence<G, 0>(A);
 #pragma unroll
   for (int b = 0; b < 16; b += 2) {   // A holds block b (H = 0 or 2), B gets block b + 1 (H = 1 or 3)
     const u32 v0 = (u32)(b / 4) * 8;
     const bool lo = (b % 4) == 0;
-    if (lo) drain5_ld<1>(tl, b + 1, B); else drain5_ld<3>(tl, b + 1, B);
-    if (st) { if (lo) drain_st<5, 0, 32>(v0, raw_u, A); else drain_st<5, 2, 32>(v0, raw_u, A); }
+    if (lo) drain5_ld<G, 1>(tl, b + 1, B); else drain5_ld<G, 3>(tl, b + 1, B);
+    if (st) { if (lo) drain_st<G, 0, 32>(v0, raw_u, A); else drain_st<G, 2, 32>(v0, raw_u, A); }
     tmem_wait_ld();
-    if (lo) drain_fence<5, 1>(B); else drain_fence<5, 3>(B);
+    if (lo) drain_fence<G, 1>(B); else drain_fence<G, 3>(B);
     if (b + 2 < 16) {
-      if (lo) drain5_ld<2>(tl, b + 2, A); else drain5_ld<0>(tl, b + 2, A);
+      if (lo) drain5_ld<G, 2>(tl, b + 2, A); else drain5_ld<G, 0>(tl, b + 2, A);
     } else {   // TMEM drained: the MMA may start the next unit
       tc_fence_before();
       mbar_arrive(acce);
     }
-    if (st) { if (lo) drain_st<5, 1, 32>(v0, raw_u, B); else drain_st<5, 3, 32>(v0, raw_u, B); }
+    if (st) { if (lo) drain_st<G, 1, 32>(v0, raw_u, B); else drain_st<G, 3, 32>(v0, raw_u, B); }
     if (b + 2 < 16) {
       tmem_wait_ld();
-      if (lo) drain_fence<5, 2>(A); else drain_fence<5, 0>(A);
+      if (lo) drain_fence<G, 2>(A); else drain_fence<G, 0>(A);
     }
   }
 }
@@ -931,7 +950,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       g = uni(g);
       u64* prow = a.partial + ((u64)pc.z * a.rounds + g) * a.ldp;
       if (MODE == 2) g = 2;   // the 4-digit mode's single round
-      if (VV == 32) g = 5;    // the V = 32 geometry's single round
+      if (VV == 32) g = MODE == 3 ? 6 : 5;   // the V = 32 geometry's single round (7 / 8 digits)
       u32* raw = raw_cta + (u64)(nunit & 1) * kDiag * (kU * kV);
       if (warp == kMmaWarp) {
         // (this raw buffer was last read two units ago by warps 2 / 3's fold of warp 0's rows;
@@ -954,7 +973,9 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
           __syncwarp();
           if (elect_one()) {
             if (VV == 32) {
-              if (!(PROF && a.dbg == 1)) issue_all32(tbu, da, db, kb == 0);
+              if (PROF && a.dbg == 1) {
+              } else if (MODE == 3) issue_all32_7(tbu, da, db, kb == 0);
+              else issue_all32(tbu, da, db, kb == 0);
             } else if (PROF && a.dbg == 7) {   // one N = 64 MMA per digit pair (the previous issue form)
               if (g == 0) issue_round<0, true>(tbu, da, db, kb == 0);
               else issue_round<1, true>(tbu, da, db, kb == 0);
@@ -979,7 +1000,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       tc_fence_after();
       u32* raw_u = raw + (u64)u * 4;
       const bool st = !(PROF && a.dbg == 3);
-      if (VV == 32) epi_drain5(tl, raw_u, &acce, st);
+      if (VV == 32 && MODE == 3) epi_drain5<6>(tl, raw_u, &acce, st);
+      else if (VV == 32) epi_drain5<5>(tl, raw_u, &acce, st);
       else if (MODE == 2) epi_drain<2>(tl, raw_u, &acce, st);
       else if (MODE == 3 && g == 1) epi_drain<4>(tl, raw_u, &acce, st);
       else if (g == 0) epi_drain<0>(tl, raw_u, &acce, st);
@@ -1000,7 +1022,8 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
         }
         const u32* rr_ = raw + (u64)ur * 4;
         const u64 kbase = (u64)chunk * chunk_pts(VV) + (u64)ur * VV;   // multiple of 8; ldp multiple of 8
-        if (VV == 32) fold_row<5, 32>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
+        if (VV == 32 && MODE == 3) fold_row<6, 32>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
+        else if (VV == 32) fold_row<5, 32>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
         else if (MODE == 2) fold_row<2>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
         else if (MODE == 3 && g == 1) fold_row<4>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
         else if (g == 0) fold_row<0>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);

@@ -198,3 +198,57 @@ def test_single_round_v32_schedule_and_reduction(seed, swapped):
         acc += x[k] * pow(2, 32 * k, p)
     assert (acc >> 64) < p                                   # REDC's precondition without the fallback
     assert redc(acc >> 64, acc & ((1 << 64) - 1), p) == want
+
+
+def issue_all32_7_emulated(Lbytes, Rbytes, nkb):
+    """tc.cuh issue_all32_7 (7 digits): per K-block L plane s < 7 times the baby-step planes t < 7
+    is one MMA into slots s .. s + 6; at K-block 0 plane 0 overwrites slots 0..6 and plane 6 goes
+    second, split into t = 0 (accumulates slot 6) and t = 1..6 (overwrites slots 7..12)."""
+    rng = random.Random(8)
+    slot = [rng.getrandbits(32) for _ in range(13)]
+
+    def mma(s, t_lo, t_hi, kb, acc):
+        for t in range(t_lo, t_hi + 1):
+            part = sum(Lbytes[s][i] * Rbytes[t][i] for i in range(32 * kb, 32 * kb + 32))
+            slot[s + t] = ((slot[s + t] if acc else 0) + part) % (1 << 32)
+
+    for kb in range(nkb):
+        first = kb == 0
+        mma(0, 0, 6, kb, not first)
+        if first:
+            mma(6, 0, 0, kb, True)
+            mma(6, 1, 6, kb, False)
+        else:
+            mma(6, 0, 6, kb, True)
+        for s in range(1, 6):
+            mma(s, 0, 6, kb, True)
+    return slot
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_single_round_v32_seven_digits(seed):
+    """The 7-digit mode (2^31 <= p < 2^54) on the V = 32 geometry: lazy giant steps < 4p < 2^56 and
+    Montgomery baby steps < p have 7 bytes; the emulated issue_all32_7 schedule reproduces the 13
+    byte diagonals, and one 13-diagonal fold + REDC gives sum_i c_i m_i^{j_s + 32u + v} mod p."""
+    rng = random.Random(400 + seed)
+    p = (1 << 50) - 27
+    R64 = (1 << 64) % p
+    nkb = 3
+    n = 32 * nkb
+    c = [rng.randrange(p) for _ in range(n)]
+    m = [rng.randrange(1, p) for _ in range(n)]
+    js, u, v = rng.randrange(1, 1 << 40), rng.randrange(128), rng.randrange(32)
+    A = [(ci * pow(mi, js + 32 * u, p)) % p + rng.randrange(4) * p for ci, mi in zip(c, m)]
+    B = [(pow(mi, v, p) * R64) % p for mi in m]
+    assert max(A) < (1 << 56) and max(B) < (1 << 56)
+    want = sum(ci * pow(mi, js + 32 * u + v, p) for ci, mi in zip(c, m)) % p
+    Ab = [[(x >> (8 * s)) & 0xFF for x in A] for s in range(7)]
+    Bb = [[(x >> (8 * t)) & 0xFF for x in B] for t in range(7)]
+    slots = issue_all32_7_emulated(Ab, Bb, nkb)
+    assert slots == diagonals(A, B)[:13] and diagonals(A, B)[13:] == [0, 0]
+    X = sum(slots[d] << (8 * d) for d in range(13))
+    x = [(X >> (32 * k)) & 0xFFFFFFFF for k in range(5)]
+    acc = x[0] | (x[1] << 32)
+    for k in (2, 3, 4):
+        acc += x[k] * pow(2, 32 * k, p)
+    assert redc(acc >> 64, acc & ((1 << 64) - 1), p) == want
