@@ -1051,7 +1051,7 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s,
   u32* d_status = h->d_status;
   // kernel mode: 0 = lazy chains, 8 digits; 1 = p >= 2^62, exact chains, 8 digits; 2 = p < 2^31,
   // exact chains (values < 2^32), 4 digits, one round
-  // 3 = 2^31 <= p < 2^54: lazy chains (values < 2^56), 7 digits, two rounds of 12 + 6 MMAs
+  // 3 = 2^31 <= p < 2^54: lazy chains (values < 2^56), 7 digits, one round of 7 MMAs (V = 32)
   // 4 / 5: the swapped forms of 0 / 1 (giant-step planes per handle, baby steps generated)
   int mode = h->p < (1ull << 31) ? 2 : h->p < (1ull << 54) ? 3 : (h->p >= (1ull << 62) ? 1 : 0);
   if (h->tc_swap) mode += 4;

@@ -20,16 +20,17 @@
 //
 // Shapes: U = M = 128 (TMEM lanes), K-block = 32 terms (one kind::i8 MMA K step), V by mode
 // (mode_v):
-//   V = 32 (8-digit modes, p >= 2^54 -- config 5): all 15 diagonals fit TMEM at once (15 x 32 =
-//     480 of 512 columns), so a unit is (piece, chunk of 128 x 32 points) in ONE round: per
-//     K-block, L plane s against the 8 consecutive R planes is ONE MMA of N = 256 into slots
-//     s .. s + 7 (issue_all32), one fold + REDC per point (epi_drain5, fold_row<5, 32>).
-//   V = 64 (4- and 7-digit modes, p < 2^54): 15 (resp. 13) diagonals do not fit at once, so a
-//     piece runs in 2 rounds (d = 0..7 and 8..14, slot = d - d_lo; the 4-digit mode's 7 fit in
-//     one) and a unit is (piece, chunk, round) reducing its own part X_g into its own partial row
-//     (X mod p = sum of the parts).  A round's partners t of one L plane s are consecutive and
-//     the baby-step planes sit plane after plane in each K half, so each (s, run of t) is ONE MMA
-//     with N = 64k <= 256 (22 MMAs per K-block for both rounds).
+//   V = 32 (8-digit modes, p >= 2^54 -- config 5 -- and 7-digit modes, 2^31 <= p < 2^54): all 15
+//     (13) diagonals fit TMEM at once (15 x 32 = 480 of 512 columns), so a unit is (piece, chunk
+//     of 128 x 32 points) in ONE round: per K-block, L plane s against the 8 (7) consecutive R
+//     planes is ONE MMA of N = 256 (224) into slots s .. s + 7 (issue_all32 / issue_all32_7), one
+//     fold + REDC per point (epi_drain5<5 / 6>, fold_row<5 / 6, 32>).
+//   V = 64 (the 4-digit mode, p < 2^31: 7 diagonals, one round of 5 MMAs; and the two-round forms
+//     kept for reference -- issue_round_wide, issue_round7_*): with 8 digits 15 x 64 columns do
+//     not fit, so a piece ran in 2 rounds (d = 0..7 and 8..14, slot = d - d_lo) and a unit was
+//     (piece, chunk, round) reducing its own part X_g into its own partial row (X mod p = sum of
+//     the parts); a round's partners t of one L plane s are consecutive, so each (s, run of t) is
+//     ONE MMA with N = 64k <= 256.
 // The baby-step planes R = m^v do not depend on the points: they are built once per handle and
 // streamed into the stages by TMA, so per evaluation only the giant steps are generated (1
 // modular product per 32 term-points).
@@ -89,12 +90,13 @@ constexpr u32 kGBytes = 8 * kPlaneA;      // one K-block's giant-step planes in 
 constexpr int kLSRec = 1, kCRec = 10;
 enum { kC_mL = 0, kC_wL = 1, kC_g0 = 2 };
 constexpr u32 kRBytes = 2 * kLBOB;                    // one K-block's R planes (16384 B)
-// Geometry of a mode: V baby steps per chunk, a chunk = kU * V points.  The 8-digit plain modes
-// (0, 1) use V = 32: all 15 diagonals then fit TMEM at once (15 x 32 = 480 columns), so a unit is
-// (piece, chunk) in ONE round -- 8 MMAs of N = 256 per K-block (L plane s against the 8 baby-step
-// planes, slots s .. s + 7) -- with half the baby-step plane bytes per term (256 B) and one fold +
-// REDC per point instead of one per round.  The 4-digit (7 diagonals in one round), 7-digit and
-// swapped modes keep V = 64.
+// Geometry of a mode: V baby steps per chunk, a chunk = kU * V points.  Every mode but the 4-digit
+// one uses V = 32: all 15 (7 digits: 13) diagonals then fit TMEM at once (15 x 32 = 480 columns), so
+// a unit is (piece, chunk) in ONE round -- 8 MMAs of N = 256 per K-block (L plane s against the 8
+// baby-step planes, slots s .. s + 7) -- with half the baby-step plane bytes per term (256 B) and
+// one fold + REDC per point instead of one per round; the plain and swapped 8-digit forms alike.
+// The 4-digit mode (p < 2^31: 7 diagonals, one round at V = 64) keeps V = 64, where V = 32 would
+// double its generation per point.
 __host__ __device__ constexpr int mode_v(int MODE) { return MODE == 2 ? 64 : 32; }
 __host__ __device__ constexpr u32 plane_b(int V) { return (u32)V * 16; }      // one R plane, one K half
 __host__ __device__ constexpr u32 lbo_b(int V) { return 8 * plane_b(V); }     // R planes' K-half stride
@@ -787,7 +789,7 @@ __device__ __forceinline__ void load_kblock(const TcArgs& a, const KIter& k, u32
 // MODE 0: p < 2^62, lazy Shoup chains (values < 4p < 2^64), 8 byte digits, 2 rounds.
 // MODE 1: 2^62 <= p < 2^63, exact-quotient chains (values < 2p < 2^64), 8 digits, 2 rounds.
 // MODE 2: p < 2^31, exact-quotient chains (values < 2p < 2^32), 4 digits, 1 round of 5 MMAs.
-// MODE 3: 2^31 <= p < 2^54, lazy chains (values < 4p < 2^56), 7 digits, 2 rounds of 12 + 6 MMAs.
+// MODE 3: 2^31 <= p < 2^54, lazy chains (values < 4p < 2^56), 7 digits, one round of 7 MMAs (V = 32).
 template <bool PROF, int MODE>
 static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 warps: <= 168 regs/thread
   unsigned long long g_entry = 0;
