@@ -381,11 +381,13 @@ k_step(StepArgs args) {
 }
 
 // out[g*ld + k] = sum over the bucket's partial slots, mod p.  One thread per (g, k).
+// skip1: rows with a single slot were written to `out` by k_tc directly (TcArgs::direct)
 static __global__ void k_fixup(const u64* __restrict__ partial, u64 ldp, const u32* __restrict__ slot_start,
-                        u32 G, u32 npts, u32 nkb, u64* __restrict__ out, u64 ld, ModParams mp) {
+                        u32 G, u32 npts, u32 nkb, u64* __restrict__ out, u64 ld, ModParams mp, int skip1) {
   const u32 g = blockIdx.x / nkb;
   const u32 k = (blockIdx.x % nkb) * blockDim.x + threadIdx.x;
   if (g >= G || k >= npts) return;
+  if (skip1 && slot_start[g + 1] - slot_start[g] == 1) return;
   u64 lo = 0, hi = 0;
   for (u32 s = slot_start[g]; s < slot_start[g + 1]; ++s) {
     const u64 v = partial[(u64)s * ldp + k];
@@ -400,9 +402,11 @@ static __global__ void k_fixup(const u64* __restrict__ partial, u64 ldp, const u
 // coalesced 256-byte loads, and the 8 partial 128-bit sums meet in shared memory.
 static __global__ void __launch_bounds__(256) k_fixup_wide(const u64* __restrict__ partial, u64 ldp,
                                                            const u32* __restrict__ slot_start, u32 G, u32 npts,
-                                                           u32 nkb, u64* __restrict__ out, u64 ld, ModParams mp) {
+                                                           u32 nkb, u64* __restrict__ out, u64 ld, ModParams mp,
+                                                           int skip1) {
   __shared__ u64 slo[8][32], shi[8][32];
   const u32 g = blockIdx.x / nkb;
+  if (g < G && skip1 && slot_start[g + 1] - slot_start[g] == 1) return;   // whole block: uniform exit
   const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const u32 k = (blockIdx.x % nkb) * 32 + lane;
   u64 lo = 0, hi = 0;

@@ -934,7 +934,11 @@ static int tc_plan(const pe_ctx* h, u32 nch, u64 g0, u64 g1, bool upload, cudaSt
       u64 kb0 = 0;
       for (u64 k = 0; k < np_g; ++k) {
         const u64 len = nkb / np_g + (k < nkb % np_g ? 1 : 0);
-        P->pieces.push_back(make_uint4((u32)(h->h_poff[g] + kb0 * tc::kKB), (u32)len, (u32)P->pieces.size(), 0));
+        // w = 1 + the bucket's row (relative to g0) for a bucket's sole piece in a one-round geometry:
+        // its partial row is already the canonical result, so k_tc may write it to the output row
+        // directly (TcArgs::direct) and the fix-up skips that row
+        const u32 sole = (np_g == 1 && rounds == 1) ? (u32)(gg + 1) : 0u;
+        P->pieces.push_back(make_uint4((u32)(h->h_poff[g] + kb0 * tc::kKB), (u32)len, (u32)P->pieces.size(), sole));
         kb0 += len;
       }
     }
@@ -1096,6 +1100,10 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s,
     a.piece = P->d_piece;
     a.partial = h->d_partial;
     a.ldp = (np + 7) / 8 * 8;
+    // sole-piece rows straight into the output when its rows keep the epilogue's 16-B stores aligned
+    a.out = d_out + g0 * ld + k0;
+    a.ldo = ld;
+    a.direct = (env_int("PE_TC_DIRECT", 1) && ld % 2 == 0 && ((uintptr_t)a.out & 15) == 0) ? 1 : 0;
     a.t_pad = h->t_pad;
     a.npieces = P->npieces;
     a.rounds = h->tc_rounds;
@@ -1173,10 +1181,10 @@ static int eval_tc(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaStream_t s,
     if (P->max_slots >= 16 && (g1 - g0) * nkb < 8ull * h->n_sm) {
       const u32 nkw = (np + 31) / 32;
       k_fixup_wide<<<(unsigned)((g1 - g0) * nkw), 256, 0, s>>>(h->d_partial, a.ldp, P->d_slot_start, (u32)(g1 - g0),
-                                                               np, nkw, d_out + g0 * ld + k0, ld, h->mp);
+                                                               np, nkw, d_out + g0 * ld + k0, ld, h->mp, a.direct);
     } else {
       k_fixup<<<(unsigned)((g1 - g0) * nkb), 256, 0, s>>>(h->d_partial, a.ldp, P->d_slot_start, (u32)(g1 - g0), np,
-                                                          nkb, d_out + g0 * ld + k0, ld, h->mp);
+                                                          nkb, d_out + g0 * ld + k0, ld, h->mp, a.direct);
     }
     CU(cudaGetLastError());
     if (h->timing) {
@@ -1298,7 +1306,7 @@ static int eval_device_impl(pe_ctx* h, u64 j0, u64 T, u64* d_out, u64 ld, cudaSt
     if (h->timing) CU(cudaEventRecord(rec.e1, s));
     const u32 nkb = (np + 255) / 256;
     k_fixup<<<(unsigned)(h->G * nkb), 256, 0, s>>>(h->d_partial, np, h->d_slot_start, (u32)h->G, np, nkb,
-                                                   d_out + k0, ld, h->mp);
+                                                   d_out + k0, ld, h->mp, 0);
     CU(cudaGetLastError());
     if (h->timing) {
       CU(cudaEventRecord(rec.e2, s));

@@ -136,6 +136,9 @@ struct TcArgs {
   const u32* sched;      // units of CTA b: sched[sched_off[b] .. sched_off[b+1])  (host LPT schedule)
   const u32* sched_off;  // [gridDim.x + 1]
   u64* partial;          // [n_slots][ldp]
+  u64* out;              // output row of the launch's first bucket, at the pass's first point
+  u64 ldo;               // its leading dimension
+  int direct;            // 1: a bucket's sole piece (piece.w = 1 + row) writes its row of out directly
   u64 ldp, t_pad;
   u32 npieces, nunits, npts, nch;
   u32 rounds;            // diagonal rounds per (piece, chunk): 2 (8-byte digits) or 1 (4-byte, p < 2^31)
@@ -951,6 +954,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       const u32 nkb = uni(pc.y);
       g = uni(g);
       u64* prow = a.partial + ((u64)pc.z * a.rounds + g) * a.ldp;
+      if (a.direct && pc.w) prow = a.out + (u64)(pc.w - 1) * a.ldo;   // sole piece: the final row
       if (MODE == 2) g = 2;   // the 4-digit mode's single round
       if (VV == 32) g = MODE == 3 ? 6 : 5;   // the V = 32 geometry's single round (7 / 8 digits)
       u32* raw = raw_cta + (u64)(nunit & 1) * kDiag * (kU * kV);
