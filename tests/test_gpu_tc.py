@@ -335,3 +335,29 @@ def test_auto_form_falls_back_to_plain_when_memory_is_short(monkeypatch):
         assert ctx.tc_form() == 0 and not ctx.uses_tc(w.T)
         out = ctx.eval(w.j0, w.T)
     assert np.array_equal(out[:, ks.astype(np.int64)], ref)
+
+
+@pytest.mark.parametrize("pad,direct,cap_mb", [(13, "1", 0), (14, "1", 0), (0, "0", 0), (6, "1", 8)])
+def test_tc_direct_rows_ld_and_padding(monkeypatch, pad, direct, cap_mb):
+    """k_tc writes a bucket's sole piece straight into its output row when the rows keep 16-B
+    alignment (even ld, aligned base) -- an odd ld (pad 13) or PE_TC_DIRECT=0 sends every row
+    through the fix-up instead.  Either way the result equals the oracle, padding columns stay
+    untouched, and a ragged multi-pass range (partial-buffer cap) splits passes at chunk
+    boundaries of the output row."""
+    import torch
+    monkeypatch.setenv("PE_TC_DIRECT", direct)
+    if cap_mb:
+        monkeypatch.setenv("PE_PARTIAL_MB", str(cap_mb))   # one 4096-point chunk per pass: 2 passes
+    w = synth.gen_config(2, t=60_000, T=5000)      # buckets of one piece and of several
+    ks = np.array([0, 1, 2047, 4095, 4096, 4999], np.uint64)
+    ref = oracle.eval_workload(w, ks=ks)
+    with pe.Context.from_workload(w, path=pe.PATH_TC) as ctx:
+        G, T = ctx.G, w.T
+        assert ctx.info()["tc_pieces"] >= G
+        buf = torch.full((G, T + pad), -1, dtype=torch.int64, device="cuda")
+        ctx.eval_device(w.j0, T, buf.data_ptr(), T + pad)
+        torch.cuda.synchronize()
+    got = buf.cpu().numpy().view(np.uint64)
+    assert np.array_equal(got[:, ks.astype(np.int64)], ref)
+    if pad:
+        assert np.all(got[:, T:] == np.uint64(2**64 - 1))
