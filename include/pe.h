@@ -73,7 +73,8 @@ enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_INT32 = 4, P
  * [768, 8192].  It also needs one chunk of partial rows (8 B x pieces x rounds per point)
  * to fit the partial-buffer cap (env PE_PARTIAL_MB, default 1024), and its handle memory to fit the
  * device (and env PE_TC_MEM_MB if set): otherwise an automatic handle degrades to the scalar
- * k_step (same results).  env PE_TC=0 off, 1 auto, 2 always; PE_PATH_INT never uses it.  Results
+ * k_step (same results).  env PE_TC=0 off, 1 auto, 2 always; PE_PATH_INT never uses it; PE_TC_DIRECT=0
+ * makes every output row go through the fix-up (default: a bucket's sole piece writes its row directly).  Results
  * are bit-identical either way. */
 /* PE_PATH_INT32 is reported by pe_info only: every p < 2^31 (any requested path except FP64)
  * uses 32-bit Shoup products. */
