@@ -294,14 +294,18 @@ static cudaError_t launch_step(int path, int R, dim3 grid, dim3 block, cudaStrea
 // profiles/r02_tc_threshold_v32.jsonl): crossovers T ~ 540 / 380 / 280 / 235 at 1.3e4 / 1.0e5 /
 // 3.1e5 / 1.0e6 padded terms, fitted by T* = max(3400 t_pad^-0.19, 7.3e6 / t_pad) (the second term:
 // tiny handles, where k_step's cost is ~flat while k_tc keeps its ~0.045 ms floor), in [192, 8192].
-static u64 tc_min_T_v32(u64 t_pad) {
+// The 7-digit mode (2^31 <= p < 2^54, V = 32 since session 2) against the FP64 Alg. 2 k_step
+// (scripts/tc_threshold_v32.py --p50, profiles/r02_tc_threshold_v32_p50.jsonl): crossovers T ~ 510 /
+// 420 / 330 / 270 at the same term counts, fitted by max(2200 t_pad^-0.144, 7.3e6 / t_pad).
+static u64 tc_min_T_v32(u64 t_pad, double a, double b) {
   const double tp = (double)std::max<u64>(t_pad, 1);
-  const double t = std::max(3400.0 * std::pow(tp, -0.19), 7.3e6 / tp);
+  const double t = std::max(a * std::pow(tp, -b), 7.3e6 / tp);
   return std::min<u64>(8192, std::max<u64>(192, (u64)std::ceil(t)));
 }
 static u64 tc_min_T(u64 t_pad, u64 p) {
   const u64 tp = std::max<u64>(t_pad, 1);
-  if (p >= (1ull << 54)) return tc_min_T_v32(t_pad);
+  if (p >= (1ull << 54)) return tc_min_T_v32(t_pad, 3400.0, 0.19);
+  if (p >= (1ull << 31)) return tc_min_T_v32(t_pad, 2200.0, 0.144);
   if (p < (1ull << 31)) return std::min<u64>(8192, std::max<u64>(768, 95000000ull / tp));
   if (t_pad >= 500000) return 512;
   return std::min<u64>(8192, std::max<u64>(512, 86000000ull / tp));

@@ -3,6 +3,7 @@
 events around pe_eval_device, mean of 5 after a warm-up) -- sets tc_min_T for p >= 2^54.
 
     python scripts/tc_threshold_v32.py > profiles/r02_tc_threshold_v32.jsonl
+    python scripts/tc_threshold_v32.py --p50 > profiles/r02_tc_threshold_v32_p50.jsonl   (7 digits vs FP64 Alg. 2)
 """
 import json
 import os
@@ -10,6 +11,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2004_11571_b200 as pe  # noqa: E402
@@ -29,9 +31,16 @@ def dev_ms(ctx, w, T, reps=5):
     return e0.elapsed_time(e1) / reps
 
 
+P50 = (1 << 50) - 27
+seven = "--p50" in sys.argv     # the 7-digit mode (2^31 <= p < 2^54) against the FP64 Alg. 2 k_step
 for cfg, t in ((2, 10_000), (2, 100_000), (3, 300_000), (3, 1_000_000)):
     w = synth.gen_config(cfg, t=t)
-    with pe.Context.from_workload(w, path=pe.PATH_INT) as ci, pe.Context.from_workload(w, path=pe.PATH_TC) as ct:
+    if seven:
+        w.p = P50
+        w.coeffs %= np.uint64(P50)
+        w.alpha = (w.alpha % np.uint64(P50 - 1)) + np.uint64(1)
+    scalar = pe.PATH_FP64 if seven else pe.PATH_INT
+    with pe.Context.from_workload(w, path=scalar) as ci, pe.Context.from_workload(w, path=pe.PATH_TC) as ct:
         for T in (32, 64, 128, 192, 256, 384, 512, 768, 1024):
             a, b = dev_ms(ci, w, T), dev_ms(ct, w, T)
             print(json.dumps({"cfg": cfg, "t": t, "t_pad": ct.info()["t_padded"], "min_T_now": ct.info()["tc_min_T"],

@@ -128,8 +128,8 @@ def v32_min_T(tp):
 
 def test_tc_auto_selection():
     """PE_PATH_AUTO: tensor path for any p < 2^63 and T >= the handle's threshold (p >= 2^54:
-    max(3400 t_pad^-0.19, 7.3e6 / t_pad) in [192, 8192]; 2^31 <= p < 2^54: 8.6e7 / t_pad clamped to
-    [512, 8192], 512 from 5*10^5 padded terms); never for PE_PATH_INT or PE_PATH_FP64."""
+    max(3400 t_pad^-0.19, 7.3e6 / t_pad) in [192, 8192]; 2^31 <= p < 2^54: max(2200 t_pad^-0.144,
+    7.3e6 / t_pad) in [192, 8192]); never for PE_PATH_INT or PE_PATH_FP64."""
     w = synth.random_small(524, P62, 5, 100, 3, 10, 1)
     with pe.Context.from_workload(w) as ctx:
         tp = ctx.info()["t_padded"]
@@ -144,12 +144,15 @@ def test_tc_auto_selection():
     with pe.Context.from_workload(w3) as ctx:
         m = ctx.info()["tc_min_T"]
         assert 192 <= m <= 300 and ctx.uses_tc(m) and not ctx.uses_tc(m - 1)
-    w7 = synth.gen_config(3, t=600_000, T=10)                          # 7-digit mode keeps the V = 64 rule
+    w7 = synth.gen_config(3, t=600_000, T=10)                          # 7-digit mode: its own fit
     w7.p = (1 << 50) - 27
     w7.coeffs %= np.uint64(w7.p)
-    w7.alpha %= np.uint64(w7.p)
+    w7.alpha = (w7.alpha % np.uint64(w7.p - 1)) + np.uint64(1)
     with pe.Context.from_workload(w7) as ctx:
-        assert ctx.info()["tc_min_T"] == 512
+        tp = ctx.info()["t_padded"]
+        m = ctx.info()["tc_min_T"]
+        assert abs(m - min(8192, max(192, math.ceil(max(2200.0 * tp ** -0.144, 7.3e6 / tp))))) <= 1
+        assert ctx.uses_tc(m) and not ctx.uses_tc(m - 1)
     w31 = synth.random_small(527, (1 << 31) - 1, 6, 600_000 // 8, 9, 10, 1)   # p < 2^31: vs 32-bit k_step
     with pe.Context.from_workload(w31) as ctx:
         tp = ctx.info()["t_padded"]
