@@ -915,8 +915,13 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
           if (MODE == 2) store_digits4<kPlaneA>(planes0 + (u32)k * 128u, x);
           else store_digits<kPlaneA>(planes0 + (u32)k * 128u, x);
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            x[e] = (MODE == 1 || MODE == 2) ? mul_shoup2(x[e], sm[e], sw[e], np) : mul_shoup4(x[e], sm[e], sw[e], np);
+          for (int e = 0; e < 4; ++e) {
+            // p < 2^31: 32-bit Shoup (3 IMADs instead of the 64-bit form's ~10); its constant
+            // floor(m 2^32 / p) is the high word of the record's floor(m 2^64 / p), and values stay
+            // < 2p < 2^32 (4 digits)
+            if (MODE == 2) x[e] = mul_shoup32((u32)x[e], (u32)sm[e], (u32)(sw[e] >> 32), (u32)mp.p);
+            else x[e] = MODE == 1 ? mul_shoup2(x[e], sm[e], sw[e], np) : mul_shoup4(x[e], sm[e], sw[e], np);
+          }
         }
         if (MODE == 2) store_digits4<kPlaneA>(planes0 + 15u * 128u, x);   // last row: no product after it
         else store_digits<kPlaneA>(planes0 + 15u * 128u, x);
