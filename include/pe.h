@@ -69,8 +69,8 @@ enum { PE_PATH_AUTO = 0, PE_PATH_INT = 1, PE_PATH_FP64 = 2, PE_PATH_INT32 = 4, P
  * PE_PATH_AUTO selects it for any p < 2^63 once T reaches the handle's measured threshold
  * (pe_tc_info): for p >= 2^54 (V = 32), T >= max(3400 t_pad^-0.19, 7.3e6 / t_pad) clamped to
  * [192, 8192]; for 2^31 <= p < 2^54, T >= max(2200 t_pad^-0.144, 7.3e6 / t_pad) clamped to
- * [192, 8192]; for p < 2^31 (against the 32-bit scalar core) T >= 9.5e7 / t_pad clamped to
- * [768, 8192].  It also needs one chunk of partial rows (8 B x pieces x rounds per point)
+ * [192, 8192]; for p < 2^31 (against the 32-bit scalar core) T >= max(1350 t_pad^-0.045,
+ * 1.1e7 / t_pad) clamped to [512, 8192].  It also needs one chunk of partial rows (8 B x pieces x rounds per point)
  * to fit the partial-buffer cap (env PE_PARTIAL_MB, default 1024), and its handle memory to fit the
  * device (and env PE_TC_MEM_MB if set): otherwise an automatic handle degrades to the scalar
  * k_step (same results).  env PE_TC=0 off, 1 auto, 2 always; PE_PATH_INT never uses it; PE_TC_DIRECT=0

@@ -306,7 +306,13 @@ static u64 tc_min_T(u64 t_pad, u64 p) {
   const u64 tp = std::max<u64>(t_pad, 1);
   if (p >= (1ull << 54)) return tc_min_T_v32(t_pad, 3400.0, 0.19);
   if (p >= (1ull << 31)) return tc_min_T_v32(t_pad, 2200.0, 0.144);
-  if (p < (1ull << 31)) return std::min<u64>(8192, std::max<u64>(768, 95000000ull / tp));
+  // p < 2^31: the 4-digit mode with 32-bit Shoup producers against the 32-bit Shoup k_step
+  // (scripts/tc_threshold_v32.py --p31, profiles/r02_tc_threshold_p31_shoup32.jsonl): crossovers
+  // T ~ 850 / 780 / 750 / 730 at 1.3e4 / 1.0e5 / 3.1e5 / 1.0e6 padded terms
+  if (p < (1ull << 31)) {
+    const double t = std::max(1350.0 * std::pow((double)tp, -0.045), 1.1e7 / (double)tp);
+    return std::min<u64>(8192, std::max<u64>(512, (u64)std::ceil(t)));
+  }
   if (t_pad >= 500000) return 512;
   return std::min<u64>(8192, std::max<u64>(512, 86000000ull / tp));
 }

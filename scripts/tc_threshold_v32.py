@@ -4,6 +4,7 @@ events around pe_eval_device, mean of 5 after a warm-up) -- sets tc_min_T for p 
 
     python scripts/tc_threshold_v32.py > profiles/r02_tc_threshold_v32.jsonl
     python scripts/tc_threshold_v32.py --p50 > profiles/r02_tc_threshold_v32_p50.jsonl   (7 digits vs FP64 Alg. 2)
+    python scripts/tc_threshold_v32.py --p31 > profiles/r02_tc_threshold_p31_shoup32.jsonl (4 digits vs 32-bit k_step)
 """
 import json
 import os
@@ -33,15 +34,20 @@ def dev_ms(ctx, w, T, reps=5):
 
 P50 = (1 << 50) - 27
 seven = "--p50" in sys.argv     # the 7-digit mode (2^31 <= p < 2^54) against the FP64 Alg. 2 k_step
+four = "--p31" in sys.argv      # the 4-digit mode (p = 2^31 - 1) against the 32-bit Shoup k_step
+P31 = (1 << 31) - 1
 for cfg, t in ((2, 10_000), (2, 100_000), (3, 300_000), (3, 1_000_000)):
     w = synth.gen_config(cfg, t=t)
     if seven:
         w.p = P50
         w.coeffs %= np.uint64(P50)
         w.alpha = (w.alpha % np.uint64(P50 - 1)) + np.uint64(1)
+    if four:
+        w.p = P31
+        w.alpha = (w.alpha % np.uint64(P31 - 1)) + np.uint64(1)
     scalar = pe.PATH_FP64 if seven else pe.PATH_INT
     with pe.Context.from_workload(w, path=scalar) as ci, pe.Context.from_workload(w, path=pe.PATH_TC) as ct:
-        for T in (32, 64, 128, 192, 256, 384, 512, 768, 1024):
+        for T in ((128, 256, 384, 512, 768, 1024, 1536, 2048) if four else (32, 64, 128, 192, 256, 384, 512, 768, 1024)):
             a, b = dev_ms(ci, w, T), dev_ms(ct, w, T)
             print(json.dumps({"cfg": cfg, "t": t, "t_pad": ct.info()["t_padded"], "min_T_now": ct.info()["tc_min_T"],
                               "T": T, "k_step_ms": a, "k_tc_ms": b, "tc_faster": b < a}), flush=True)

@@ -129,7 +129,8 @@ def v32_min_T(tp):
 def test_tc_auto_selection():
     """PE_PATH_AUTO: tensor path for any p < 2^63 and T >= the handle's threshold (p >= 2^54:
     max(3400 t_pad^-0.19, 7.3e6 / t_pad) in [192, 8192]; 2^31 <= p < 2^54: max(2200 t_pad^-0.144,
-    7.3e6 / t_pad) in [192, 8192]); never for PE_PATH_INT or PE_PATH_FP64."""
+    7.3e6 / t_pad) in [192, 8192]; p < 2^31: max(1350 t_pad^-0.045, 1.1e7 / t_pad) in [512, 8192]);
+    never for PE_PATH_INT or PE_PATH_FP64."""
     w = synth.random_small(524, P62, 5, 100, 3, 10, 1)
     with pe.Context.from_workload(w) as ctx:
         tp = ctx.info()["t_padded"]
@@ -156,7 +157,7 @@ def test_tc_auto_selection():
     w31 = synth.random_small(527, (1 << 31) - 1, 6, 600_000 // 8, 9, 10, 1)   # p < 2^31: vs 32-bit k_step
     with pe.Context.from_workload(w31) as ctx:
         tp = ctx.info()["t_padded"]
-        assert ctx.info()["tc_min_T"] == min(8192, max(768, 95_000_000 // tp))
+        assert abs(ctx.info()["tc_min_T"] - min(8192, max(512, math.ceil(max(1350.0 * tp ** -0.045, 1.1e7 / tp))))) <= 1
     with pe.Context.from_workload(w, path=pe.PATH_INT) as ctx:
         assert not ctx.uses_tc(10**6)
     w50 = synth.random_small(525, (1 << 50) - 27, 5, 100, 3, 10, 1)
