@@ -341,7 +341,9 @@ static int tc_plan(const pe_ctx* h, u32 nch, u64 g0, u64 g1, bool upload, cudaSt
 // the second block, whose copy, the exposed tail, is ~1/4 of the result).  0 = no split.
 static u64 tc_row_split(const pe_ctx* h) {
   if (h->G < 2) return 0;
-  const double ce = 1.0 / 2e13, cd = 8.0 / 5e10, tp = (double)h->t_pad;
+  // ce: k_tc seconds per padded term-point (config 5 runs at ~2.4e13; env PE_SPLIT_RATE_T in units of
+  // 1e12 for experiments -- 20 / 24 / 30 measure the same e2e within noise), cd: D2H seconds per byte-point
+  const double ce = 1.0 / (env_int("PE_SPLIT_RATE_T", 24) * 1e12), cd = 8.0 / 5e10, tp = (double)h->t_pad;
   double best = tp * ce + (double)h->G * cd;   // no split
   u64 G1 = 0;
   for (u64 g = 1; g < h->G; ++g) {
