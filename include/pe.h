@@ -88,14 +88,16 @@ typedef struct pe_config {
   int32_t R;     /* terms per lane: 1,2,4,8,16 (FP64: <= 8); auto picks by bucket sizes    */
   int32_t warps; /* warps per CTA, 1..16 (auto 8)                                          */
   int32_t chunk; /* points per CTA (multiple of 32; auto by grid coverage)                 */
-  int32_t tc_form; /* tensor-core path, 8-digit primes (p >= 2^54): PE_TC_FORM_SWAPPED (the automatic
-                      choice: giant-step planes m^{32u} per handle, 1 KB per term, the 32 baby steps
+  int32_t tc_form; /* tensor-core path, 7- and 8-digit primes (p >= 2^31): PE_TC_FORM_SWAPPED
+                      (giant-step planes m^{32u} per handle, 1 KB per term, the 32 baby steps
                       c m^{j+v} per term and chunk generated -- a quarter of the plain form's
-                      generation; config 5 evaluates 13-15 % faster) or PE_TC_FORM_PLAIN (baby-step
-                      planes m^v per handle, 256 B per term, the 128 giant steps generated; 3x less
-                      DRAM per evaluation).  Same results.  Below 2^54 always plain.  An automatic
-                      handle whose swapped planes do not fit the device (or env PE_TC_MEM_MB) takes
-                      the plain form; env PE_TC_SWAP=0/1 overrides the automatic (0) choice. */
+                      generation; config 5 evaluates 13-15 % faster; the automatic choice for
+                      p >= 2^54) or PE_TC_FORM_PLAIN (baby-step planes m^v per handle, 256 B per term,
+                      the 128 giant steps generated; 3x less DRAM per evaluation; the automatic
+                      choice for 2^31 <= p < 2^54, where the swapped form measured no gain).  Same
+                      results.  Below 2^31 always plain.  An automatic handle whose swapped planes
+                      do not fit the device (or env PE_TC_MEM_MB) takes the plain form; env
+                      PE_TC_SWAP=0/1 overrides the automatic (0) choice. */
 } pe_config;
 enum { PE_TC_FORM_AUTO = 0, PE_TC_FORM_PLAIN = 1, PE_TC_FORM_SWAPPED = 2 };
 

@@ -793,8 +793,10 @@ __device__ __forceinline__ void load_kblock(const TcArgs& a, const KIter& k, u32
 // MODE 1: 2^62 <= p < 2^63, exact-quotient chains (values < 2p < 2^64), 8 digits, 2 rounds.
 // MODE 2: p < 2^31, exact-quotient chains (values < 2p < 2^32), 4 digits, 1 round of 5 MMAs.
 // MODE 3: 2^31 <= p < 2^54, lazy chains (values < 4p < 2^56), 7 digits, one round of 7 MMAs (V = 32).
+// MODE 4 / 5 / 6: the swapped forms of modes 0 / 1 / 3 (giant-step planes per handle, baby steps generated).
 template <bool PROF, int MODE>
 static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 warps: <= 168 regs/thread
+  constexpr bool SEVEN = MODE == 3 || MODE == 6;   // 7-digit modes (plain / swapped)
   unsigned long long g_entry = 0;
   if (PROF) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
   extern __shared__ uint8_t dsm[];
@@ -961,7 +963,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       u64* prow = a.partial + ((u64)pc.z * a.rounds + g) * a.ldp;
       if (a.direct && pc.w) prow = a.out + (u64)(pc.w - 1) * a.ldo;   // sole piece: the final row
       if (MODE == 2) g = 2;   // the 4-digit mode's single round
-      if (VV == 32) g = MODE == 3 ? 6 : 5;   // the V = 32 geometry's single round (7 / 8 digits)
+      if (VV == 32) g = SEVEN ? 6 : 5;   // the V = 32 geometry's single round (7 / 8 digits)
       u32* raw = raw_cta + (u64)(nunit & 1) * kDiag * (kU * kV);
       if (warp == kMmaWarp) {
         // (this raw buffer was last read two units ago by warps 2 / 3's fold of warp 0's rows;
@@ -985,7 +987,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
           if (elect_one()) {
             if (VV == 32) {
               if (PROF && a.dbg == 1) {
-              } else if (MODE == 3) issue_all32_7(tbu, da, db, kb == 0);
+              } else if (SEVEN) issue_all32_7(tbu, da, db, kb == 0);
               else issue_all32(tbu, da, db, kb == 0);
             } else if (PROF && a.dbg == 7) {   // one N = 64 MMA per digit pair (the previous issue form)
               if (g == 0) issue_round<0, true>(tbu, da, db, kb == 0);
@@ -1011,7 +1013,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
       tc_fence_after();
       u32* raw_u = raw + (u64)u * 4;
       const bool st = !(PROF && a.dbg == 3);
-      if (VV == 32 && MODE == 3) epi_drain5<6>(tl, raw_u, &acce, st);
+      if (VV == 32 && SEVEN) epi_drain5<6>(tl, raw_u, &acce, st);
       else if (VV == 32) epi_drain5<5>(tl, raw_u, &acce, st);
       else if (MODE == 2) epi_drain<2>(tl, raw_u, &acce, st);
       else if (MODE == 3 && g == 1) epi_drain<4>(tl, raw_u, &acce, st);
@@ -1033,7 +1035,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_tc(TcArgs a) {   // 12 w
         }
         const u32* rr_ = raw + (u64)ur * 4;
         const u64 kbase = (u64)chunk * chunk_pts(VV) + (u64)ur * VV;   // multiple of 8; ldp multiple of 8
-        if (VV == 32 && MODE == 3) fold_row<6, 32>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
+        if (VV == 32 && SEVEN) fold_row<6, 32>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
         else if (VV == 32) fold_row<5, 32>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
         else if (MODE == 2) fold_row<2>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);
         else if (MODE == 3 && g == 1) fold_row<4>(rr_, prow, kbase, a.npts, C64, C96, C128, mp, vbeg, vend, a.discard);

@@ -1,5 +1,5 @@
 """Randomised differential parity: every hot kernel (k_step through PE_PATH_INT / FP64, k_tc through
-PE_PATH_TC in both tensor-core forms for p >= 2^54, the fast product-tree method through PE_PATH_FAST, and the automatic choice) against
+PE_PATH_TC in both tensor-core forms for p >= 2^31, the fast product-tree method through PE_PATH_FAST, and the automatic choice) against
 the direct CPU oracle on seeded random shapes -- primes across every arithmetic mode (p < 2^31,
 the 7-digit range, p < 2^50, lazy-4 and exact-quotient 62/63-bit), n from 2 to 10, 1 to 3000 terms
 with repeated (x, y) buckets, T from 1 to 2500 with ragged tails, j0 from 0 to near 2^64."""
@@ -38,8 +38,9 @@ def test_random_shapes_all_kernels(seed):
     if w.p < (1 << 50):
         paths.append(pe.PATH_FP64)
     variants = [(path, False, pe.TC_FORM_AUTO) for path in paths] + [(pe.PATH_AUTO, True, pe.TC_FORM_AUTO)]   # + uint8 exponents
-    if w.p >= (1 << 54):   # both tensor-core forms of the 8-digit modes (the automatic one is swapped)
+    if w.p >= (1 << 31):   # both tensor-core forms of the 7- and 8-digit modes
         variants.append((pe.PATH_TC, False, pe.TC_FORM_PLAIN))
+        variants.append((pe.PATH_TC, False, pe.TC_FORM_SWAPPED))
     for path, compact, form in variants:
         with pe.Context.from_workload(w, path=path, compact=compact, tc_form=form) as ctx:
             out = ctx.eval(w.j0, w.T)

@@ -297,9 +297,9 @@ def test_tc_plain_and_swapped_forms(p, form):
 
 
 def test_tc_form_defaults_and_limits(monkeypatch):
-    """Automatic = swapped for 8-digit primes (PE_TC_SWAP=0 makes it plain); the swapped form only
-    exists for 8-digit primes (below 2^54 a request for it builds the plain form, whose 7- and
-    4-digit modes read baby-step planes); out-of-range tc_form values are PE_EINVAL."""
+    """Automatic = swapped for 8-digit primes, plain for 7-digit ones (PE_TC_SWAP=0/1 overrides);
+    7-digit primes may request the swapped form; the 4-digit mode (p < 2^31) has only the plain
+    form (a request for the swapped one builds it); out-of-range tc_form values are PE_EINVAL."""
     monkeypatch.delenv("PE_TC_SWAP", raising=False)
     w = synth.random_small(599, P62, 5, 300, 3, 100, 1)
     with pe.Context.from_workload(w, path=pe.PATH_TC) as ctx:
@@ -310,10 +310,15 @@ def test_tc_form_defaults_and_limits(monkeypatch):
     with pe.Context.from_workload(w, path=pe.PATH_TC, tc_form=pe.TC_FORM_SWAPPED) as ctx:
         assert ctx.tc_form() == pe.TC_FORM_SWAPPED   # an explicit request beats the env override
     monkeypatch.delenv("PE_TC_SWAP", raising=False)
-    w2 = synth.random_small(598, (1 << 50) - 27, 5, 300, 3, 100, 1)
-    with pe.Context.from_workload(w2, path=pe.PATH_TC, tc_form=pe.TC_FORM_SWAPPED) as ctx:
+    w2 = synth.random_small(598, (1 << 50) - 27, 5, 300, 3, 100, 1)     # 7 digits: both forms exist
+    for form in (pe.TC_FORM_AUTO, pe.TC_FORM_SWAPPED):
+        with pe.Context.from_workload(w2, path=pe.PATH_TC, tc_form=form) as ctx:
+            assert ctx.tc_form() == (pe.TC_FORM_SWAPPED if form == pe.TC_FORM_SWAPPED else pe.TC_FORM_PLAIN)
+            assert np.array_equal(ctx.eval(w2.j0, w2.T), oracle.eval_workload(w2))
+    w3 = synth.random_small(597, (1 << 31) - 1, 5, 300, 3, 100, 1)      # 4 digits: plain only
+    with pe.Context.from_workload(w3, path=pe.PATH_TC, tc_form=pe.TC_FORM_SWAPPED) as ctx:
         assert ctx.tc_form() == pe.TC_FORM_PLAIN
-        assert np.array_equal(ctx.eval(w2.j0, w2.T), oracle.eval_workload(w2))
+        assert np.array_equal(ctx.eval(w3.j0, w3.T), oracle.eval_workload(w3))
     with pe.Context.from_workload(w, path=pe.PATH_INT) as ctx:
         assert ctx.tc_form() == 0
     with pytest.raises(pe.PEError) as e:
