@@ -1172,24 +1172,31 @@ static __global__ void __launch_bounds__(kGpThreads) k_tc_gplanes(const u64* __r
     const u32 h = (u32)(task & 1);
     const u64 q0 = blk * kKB + (u64)h * 16 + ql * 4;
     // lane (ql, r): powers of term q0 + (r & 3)
+    static_assert(V == 32, "the shared 8-step prologue below assumes log2(V) + 3 == 8");
     const u64 q = q0 + (r & 3);
     const u64 mm = to_mont(q < t_pad ? m[q] : 0ull, mp);
-    u64 mV = mm;
-#pragma unroll 1
-    for (int i = 0; (1 << i) < V; ++i) mV = mont_mul(mV, mV, mp);   // m^V (V a power of 2)
-    const u64 m2V = mont_mul(mV, mV, mp), m4V = mont_mul(m2V, m2V, mp);
-    const u64 m8V = mont_mul(m4V, m4V, mp);
-    if (r < 4 && q < t_pad) {                            // the term's C record and seed powers
-      u64 g = mp.r1;
-#pragma unroll 1
-      for (int rr = 0; rr < 8; ++rr) {
-        C[q * kCRec + kC_g0 + rr] = g;                   // Montgomery m^{rr}
-        g = mont_mul(g, mm, mp);
-      }
-      const u64 a8 = from_mont(g, mp);                   // m^8
-      C[q * kCRec + kC_mL] = a8;
-      C[q * kCRec + kC_wL] = g * mp.pinv;                // shoup_w_fast(m^8)
-      u64 mC = m8V;                                      // m^{kChunk} = (m^{8V})^16
+    // One 8-step chain, branch-free across the two lanes of a term: lanes r < 4 square
+    // (m -> m^V -> m^{2V} -> m^{4V} -> m^{8V}), lanes r >= 4 walk the C record's Montgomery
+    // m^{rr}, rr < 8 (ending at m^8).
+    const bool sq = r < 4;
+    const bool rec = !sq && q < t_pad;
+    u64 x = sq ? mm : mp.r1, mV = 0, m2V = 0, m4V = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (rec) C[q * kCRec + kC_g0 + k] = x;             // Montgomery m^{k}
+      x = mont_mul(x, sq ? x : mm, mp);
+      if (k == 4) mV = x;
+      if (k == 5) m2V = x;
+      if (k == 6) m4V = x;
+    }
+    // x = m^{8V} (r < 4) or m^8 (r >= 4), Montgomery: normal form and Shoup constant for both
+    const u64 nx = from_mont(x, mp), wx = x * mp.pinv;
+    if (rec) {
+      C[q * kCRec + kC_mL] = nx;                         // m^8
+      C[q * kCRec + kC_wL] = wx;                         // shoup_w_fast(m^8)
+    }
+    if (sq && q < t_pad) {                               // seed powers
+      u64 mC = x;                                        // m^{kChunk} = (m^{8V})^16
 #pragma unroll 1
       for (int i = 0; i < 4; ++i) mC = mont_mul(mC, mC, mp);
       MS[2 * q] = mV;
@@ -1198,11 +1205,11 @@ static __global__ void __launch_bounds__(kGpThreads) k_tc_gplanes(const u64* __r
     u64 y[4], mS[4], wS[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int src = (int)(ql * 8) + e;
+      const int src = (int)(ql * 8) + e;                 // lane r = e < 4: term q0 + e's powers
       const u64 v1 = __shfl_sync(0xffffffffu, mV, src), v2 = __shfl_sync(0xffffffffu, m2V, src);
-      const u64 v4 = __shfl_sync(0xffffffffu, m4V, src), v8 = __shfl_sync(0xffffffffu, m8V, src);
-      mS[e] = from_mont(v8, mp);                         // normal m^{8V}: the chain's fixed multiplier
-      wS[e] = v8 * mp.pinv;                              // its Shoup constant
+      const u64 v4 = __shfl_sync(0xffffffffu, m4V, src);
+      mS[e] = __shfl_sync(0xffffffffu, nx, src);         // normal m^{8V}: the chain's fixed multiplier
+      wS[e] = __shfl_sync(0xffffffffu, wx, src);         // its Shoup constant
       u64 x = mp.r1;
       if (r & 1) x = v1;
       if (r & 2) x = mont_mul(x, v2, mp);
