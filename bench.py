@@ -231,8 +231,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-cols", type=int, default=0, help="oracle sample columns (0 = 4 x cores)")
-    ap.add_argument("--sustain-s", type=float, default=0.0,
-                    help="also run the device step back to back for this many seconds (power-capped figure)")
+    ap.add_argument("--sustain-s", type=float, default=3.0,
+                    help="also run the device step back to back for this many seconds (power-capped "
+                         "figure, reported as 'sustained'; 0 skips it)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
