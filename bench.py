@@ -95,8 +95,27 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.p = None
+        self.nv = []                     # NVML samples (t, sm_mhz, reason bits): every ~10 ms
+        self._stop = None
+
+    def _nvml_loop(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            while not self._stop.is_set():
+                self.nv.append((time.time(), nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                self._stop.wait(0.01)
+            nv.nvmlShutdown()
+        except Exception:                # evidence only: never fail the bench over it
+            pass
 
     def __enter__(self):
+        import threading
+        self._stop = threading.Event()
+        self._th = threading.Thread(target=self._nvml_loop, daemon=True)
+        self._th.start()
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
@@ -106,6 +125,8 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
+        self._stop.set()
+        self._th.join(timeout=5)
         self.lines = []
         if self.p:
             self.p.terminate()
@@ -144,9 +165,18 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(name)
         load = [s for s in sm if s > 0.5 * mx] if mx else sm
-        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm),
-                "power_w_median": statistics.median(pw) if pw else None, "power_w_max": max(pw) if pw else None}
+        out = {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx or None,
+               "reasons": sorted(reasons), "samples": len(sm),
+               "power_w_median": statistics.median(pw) if pw else None, "power_w_max": max(pw) if pw else None}
+        # NVML every ~10 ms over the same window: the short burst gets more than nvidia-smi's 100-ms lines
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        nv = [x for x in self.nv if t0 is None or t0 <= x[0] <= t1]
+        if nv:
+            out["nvml_10ms"] = {"samples": len(nv), "sm_mhz": statistics.median(x[1] for x in nv),
+                                "sm_mhz_min": min(x[1] for x in nv),
+                                "reasons": sorted(k for k, b in bits.items() if any(x[2] & b for x in nv))}
+        return out
 
 
 # ---------------------------------------------------------------- CPU oracle leg
