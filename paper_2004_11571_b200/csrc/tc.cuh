@@ -1092,8 +1092,9 @@ static __global__ void k_tc_setup(const u64* __restrict__ m, u64 t_pad, u64* __r
 // m_i^v 2^64 mod p (v < V) in the stage layout of each K-block (any representative < 2^64 gives
 // exact byte products; the epilogue's REDC removes the 2^64).  Warp task = (K-block, K half):
 // lane = (ql: 4 terms, r: rows r + 8j, j < 8); a warp's store of one plane word covers 8 rows x 16
-// bytes = one 128-byte line, so the planes go straight to global memory.  m, m^2, m^4, m^8 of a
-// term are computed once (lane r < 4 of the term's group) and shuffled to the group's 8 lanes.
+// bytes = one 128-byte line, so the planes go straight to global memory.  m, m^2, m^3, m^4 and the
+// normal m^8 with its Shoup constant are computed once per term (lane r < 4 of the term's group) and
+// shuffled to the group's 8 lanes, so each lane's row start m^r costs at most one product.
 // The stride-8 chain of a lane (rows r, r + 8, ...) multiplies by the fixed m^8 with Shoup products
 // (its constant is m8_mont * (-p^-1) mod 2^64, modcore.cuh shoup_w_fast): any representative below
 // 2^digits is exact for the MMAs, so LAZY chains (values < 4p) serve 2^31 <= p < 2^62 (8 digits, or 7
@@ -1115,19 +1116,20 @@ static __global__ void __launch_bounds__(kRpThreads) k_tc_rplanes(const u64* __r
     const u64 mm = to_mont(q < t_pad ? m[q] : 0ull, mp);
     const u64 m2 = mont_mul(mm, mm, mp), m4 = mont_mul(m2, m2, mp);
     const u64 m8m = mont_mul(m4, m4, mp);                // Montgomery m^8 = m^8 2^64 mod p
+    const u64 m3 = mont_mul(m2, mm, mp);
+    const u64 n8 = from_mont(m8m, mp), s8 = m8m * mp.pinv;   // normal m^8 and its Shoup constant
     u64 y[4], m8[4], w8[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int src = (int)(ql * 8) + e;
       const u64 v1 = __shfl_sync(0xffffffffu, mm, src), v2 = __shfl_sync(0xffffffffu, m2, src);
-      const u64 v4 = __shfl_sync(0xffffffffu, m4, src), v8 = __shfl_sync(0xffffffffu, m8m, src);
-      m8[e] = from_mont(v8, mp);                         // normal m^8: the chain's fixed multiplier
-      w8[e] = v8 * mp.pinv;                              // its Shoup constant floor(m^8 2^64 / p)
-      u64 x = mp.r1;                                     // Montgomery 1 = m^0
-      if (r & 1) x = v1;
-      if (r & 2) x = mont_mul(x, v2, mp);
+      const u64 v3 = __shfl_sync(0xffffffffu, m3, src), v4 = __shfl_sync(0xffffffffu, m4, src);
+      m8[e] = __shfl_sync(0xffffffffu, n8, src);         // normal m^8: the chain's fixed multiplier
+      w8[e] = __shfl_sync(0xffffffffu, s8, src);         // its Shoup constant floor(m^8 2^64 / p)
+      const u32 r2 = r & 3;                              // one product at most: m^{r&3} [x m^4]
+      u64 x = r2 == 0 ? mp.r1 : r2 == 1 ? v1 : r2 == 2 ? v2 : v3;
       if (r & 4) x = mont_mul(x, v4, mp);
-      y[e] = x;                                          // m^r (Montgomery residue)
+      y[e] = x;                                          // m^r (Montgomery residue, canonical)
     }
     uint8_t* dst = Rp + blk * r_bytes(V) + h * lbo_b(V) + r * 16u + ql * 4u;
 #pragma unroll 1
@@ -1195,6 +1197,7 @@ static __global__ void __launch_bounds__(kGpThreads) k_tc_gplanes(const u64* __r
       C[q * kCRec + kC_mL] = nx;                         // m^8
       C[q * kCRec + kC_wL] = wx;                         // shoup_w_fast(m^8)
     }
+    const u64 m3V = mont_mul(m2V, mV, mp);               // lanes r < 4 (unused elsewhere)
     if (sq && q < t_pad) {                               // seed powers
       u64 mC = x;                                        // m^{kChunk} = (m^{8V})^16
 #pragma unroll 1
@@ -1207,14 +1210,13 @@ static __global__ void __launch_bounds__(kGpThreads) k_tc_gplanes(const u64* __r
     for (int e = 0; e < 4; ++e) {
       const int src = (int)(ql * 8) + e;                 // lane r = e < 4: term q0 + e's powers
       const u64 v1 = __shfl_sync(0xffffffffu, mV, src), v2 = __shfl_sync(0xffffffffu, m2V, src);
-      const u64 v4 = __shfl_sync(0xffffffffu, m4V, src);
+      const u64 v3 = __shfl_sync(0xffffffffu, m3V, src), v4 = __shfl_sync(0xffffffffu, m4V, src);
       mS[e] = __shfl_sync(0xffffffffu, nx, src);         // normal m^{8V}: the chain's fixed multiplier
       wS[e] = __shfl_sync(0xffffffffu, wx, src);         // its Shoup constant
-      u64 x = mp.r1;
-      if (r & 1) x = v1;
-      if (r & 2) x = mont_mul(x, v2, mp);
+      const u32 r2 = r & 3;                              // one product at most: m^{(r&3)V} [x m^{4V}]
+      u64 x = r2 == 0 ? mp.r1 : r2 == 1 ? v1 : r2 == 2 ? v2 : v3;
       if (r & 4) x = mont_mul(x, v4, mp);
-      y[e] = x;                                          // m^{rV} (Montgomery residue)
+      y[e] = x;                                          // m^{rV} (Montgomery residue, canonical)
     }
     uint8_t* dst = Gp + blk * kGBytes + plane_off<kLBOA>(r, h * 16 + ql * 4);
 #pragma unroll 1
